@@ -1,0 +1,35 @@
+# Builds the in-tree shared libraries (they travel to the GPU box with the
+# snapshot; nothing is pip-installed):
+#   paper_2209_02478_b200/libmimose_cuda.so  - sm_100a kernels + allocator + executor (C ABI)
+#   paper_2209_02478_b200/libmimose_host.so  - host planner (C ABI over include/mimose)
+NVCC    ?= nvcc
+CXX     ?= g++
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+PKG     := paper_2209_02478_b200
+CSRC    := $(PKG)/csrc
+BUILD   := build
+NVFLAGS := $(ARCH) -O3 -std=c++20 -lineinfo -Xcompiler -fPIC -Iinclude -I$(CSRC) \
+           --expt-relaxed-constexpr -Xcompiler -Wall
+CXXFLAGS:= -O2 -std=c++20 -fPIC -Wall -Wextra -Iinclude
+
+CU_SRCS := $(wildcard $(CSRC)/*.cu)
+CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) $(wildcard include/*.h) \
+           $(wildcard include/mimose/*.hpp)
+
+all: $(PKG)/libmimose_cuda.so $(PKG)/libmimose_host.so
+
+$(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(BUILD)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(PKG)/libmimose_cuda.so: $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS)
+
+$(PKG)/libmimose_host.so: $(CSRC)/host/planner_capi.cpp $(HDRS)
+	$(CXX) $(CXXFLAGS) -shared -o $@ $<
+
+clean:
+	rm -rf $(BUILD) $(PKG)/*.so
+
+.PHONY: all clean

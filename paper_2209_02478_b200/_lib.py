@@ -1,0 +1,116 @@
+"""ctypes binding of the in-tree C ABI libraries.
+
+``libmimose_cuda.so`` (include/mimose_cuda.h) is the device side: budget
+arena, sm_100a kernels, layer executor, trainer. ``libmimose_host.so``
+(include/mimose_planner.h) is the host planner over include/mimose/*.hpp.
+
+There is no fallback: if a library is missing, loading raises. Run
+``make`` (or ``__graft_entry__.build()``) first.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+CUDA_LIB_PATH = os.path.join(_HERE, "libmimose_cuda.so")
+HOST_LIB_PATH = os.path.join(_HERE, "libmimose_host.so")
+
+_cuda = None
+_host = None
+
+
+class MimoseError(RuntimeError):
+    pass
+
+
+NUM_TAGS = 8
+TAGS = ["param", "grad", "optim", "act", "boundary", "transient", "input", "other"]
+
+
+class MemStats(C.Structure):
+    _fields_ = [
+        ("budget", C.c_int64),
+        ("reserved", C.c_int64),
+        ("peak_reserved", C.c_int64),
+        ("requested", C.c_int64),
+        ("peak_requested", C.c_int64),
+        ("largest_free", C.c_int64),
+        ("n_live", C.c_int64),
+        ("n_allocs", C.c_int64),
+        ("n_failures", C.c_int64),
+        ("tag_requested", C.c_int64 * NUM_TAGS),
+        ("tag_peak", C.c_int64 * NUM_TAGS),
+    ]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("tag_")}
+        d["tag_requested"] = {TAGS[i]: self.tag_requested[i] for i in range(NUM_TAGS)}
+        d["tag_peak"] = {TAGS[i]: self.tag_peak[i] for i in range(NUM_TAGS)}
+        return d
+
+
+class GemmArgs(C.Structure):
+    _fields_ = [
+        ("M", C.c_int), ("N", C.c_int), ("K", C.c_int), ("nb1", C.c_int), ("nb2", C.c_int),
+        ("a", C.c_void_p), ("a_rows", C.c_int64), ("a_cols", C.c_int64), ("lda", C.c_int64),
+        ("a_bs1", C.c_int64), ("a_bs2", C.c_int64), ("a_mn", C.c_int),
+        ("b", C.c_void_p), ("b_rows", C.c_int64), ("b_cols", C.c_int64), ("ldb", C.c_int64),
+        ("b_bs1", C.c_int64), ("b_bs2", C.c_int64), ("b_mn", C.c_int),
+        ("epi", C.c_int),
+        ("out", C.c_void_p), ("out2", C.c_void_p), ("aux", C.c_void_p), ("bias", C.c_void_p),
+        ("ldo", C.c_int64), ("obs1", C.c_int64), ("obs2", C.c_int64),
+        ("alpha", C.c_float), ("beta", C.c_float),
+        ("force_bn", C.c_int),
+    ]
+
+
+# (name, restype, argtypes) for every symbol include/mimose_cuda.h declares.
+CUDA_SYMBOLS = [
+    ("mimose_abi_version", C.c_int, []),
+    ("mimose_last_error", C.c_char_p, []),
+    ("mimose_launch_count", C.c_uint64, []),
+    ("mimose_ctx_create", C.c_int, [C.c_int, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("mimose_ctx_destroy", C.c_int, [C.c_void_p]),
+    ("mimose_alloc", C.c_int, [C.c_void_p, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]),
+    ("mimose_free", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mimose_mem_stats_get", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
+    ("mimose_mem_reset_peak", C.c_int, [C.c_void_p]),
+    ("mimose_book_create", C.c_int, [C.c_int64, C.POINTER(C.c_void_p)]),
+    ("mimose_book_destroy", C.c_int, [C.c_void_p]),
+    ("mimose_book_alloc", C.c_int64, [C.c_void_p, C.c_int64, C.c_int]),
+    ("mimose_book_free", C.c_int, [C.c_void_p, C.c_int64]),
+    ("mimose_book_stats", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
+    ("mimose_gemm", C.c_int, [C.POINTER(GemmArgs), C.c_void_p]),
+]
+
+
+def _bind(lib, symbols):
+    for name, res, args in symbols:
+        fn = getattr(lib, name)  # AttributeError == missing export: fail loudly
+        fn.restype = res
+        fn.argtypes = args
+
+
+def cuda_lib():
+    """Load libmimose_cuda.so (raises if it was not built)."""
+    global _cuda
+    if _cuda is None:
+        if not os.path.exists(CUDA_LIB_PATH):
+            raise MimoseError(f"{CUDA_LIB_PATH} missing: run `make` (no CPU fallback exists)")
+        lib = C.CDLL(CUDA_LIB_PATH)
+        _bind(lib, CUDA_SYMBOLS)
+        try:
+            from . import _cuda_syms  # noqa: F401  (extended symbol table)
+            _bind(lib, _cuda_syms.SYMBOLS)
+        except ImportError:
+            pass
+        _cuda = lib
+    return _cuda
+
+
+def check(rc, lib=None):
+    if rc != 0:
+        lib = lib or cuda_lib()
+        raise MimoseError(lib.mimose_last_error().decode())
+    return rc

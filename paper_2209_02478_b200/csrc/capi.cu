@@ -1,0 +1,149 @@
+// C ABI implementation: context, allocator, operator entry points.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "allocator.hpp"
+#include "capi_common.hpp"
+#include "mimose_cuda.h"
+#include "ops.hpp"
+
+using mimose_rt::ArenaBook;
+using mimose_rt::DeviceArena;
+using mimose_rt::MemStats;
+
+namespace mimose_capi {
+thread_local std::string g_last_error;
+int fail(const std::string& msg) {
+  g_last_error = msg;
+  return 1;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace mimose_capi
+
+using mimose_capi::cuda_fail;
+using mimose_capi::fail;
+
+struct mimose_book {
+  ArenaBook book;
+};
+
+namespace {
+void copy_stats(const MemStats& s, mimose_mem_stats* o) {
+  o->budget = s.budget;
+  o->reserved = s.reserved;
+  o->peak_reserved = s.peak_reserved;
+  o->requested = s.requested;
+  o->peak_requested = s.peak_requested;
+  o->largest_free = s.largest_free;
+  o->n_live = s.n_live;
+  o->n_allocs = s.n_allocs;
+  o->n_failures = s.n_failures;
+  for (int t = 0; t < MIMOSE_NUM_TAGS; ++t) {
+    o->tag_requested[t] = s.tag_requested[t];
+    o->tag_peak[t] = s.tag_peak[t];
+  }
+}
+}  // namespace
+
+extern "C" {
+
+int mimose_abi_version(void) { return MIMOSE_ABI_VERSION; }
+const char* mimose_last_error(void) { return mimose_capi::g_last_error.c_str(); }
+uint64_t mimose_launch_count(void) { return mimose_ops::launch_count(); }
+
+int mimose_ctx_create(int device, int64_t budget_bytes, mimose_ctx** out) {
+  if (out == nullptr) return fail("mimose_ctx_create: null out");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  auto* ctx = new (std::nothrow) mimose_ctx();
+  if (ctx == nullptr) return fail("out of host memory");
+  ctx->device = device;
+  std::string err = ctx->arena.init(budget_bytes);
+  if (!err.empty()) {
+    delete ctx;
+    return fail("mimose_ctx_create: " + err);
+  }
+  *out = ctx;
+  return 0;
+}
+
+int mimose_ctx_destroy(mimose_ctx* ctx) {
+  delete ctx;
+  return 0;
+}
+
+int mimose_alloc(mimose_ctx* ctx, int64_t bytes, int tag, void** out) {
+  if (ctx == nullptr || out == nullptr) return fail("mimose_alloc: null argument");
+  void* p = ctx->arena.alloc(bytes, tag);
+  if (p == nullptr) {
+    return fail("mimose_alloc: budget exceeded (request " + std::to_string(bytes) +
+                " B, live " + std::to_string(ctx->arena.stats().reserved) + " B of " +
+                std::to_string(ctx->arena.stats().budget) + " B)");
+  }
+  *out = p;
+  return 0;
+}
+
+int mimose_free(mimose_ctx* ctx, void* ptr) {
+  if (ctx == nullptr) return fail("mimose_free: null ctx");
+  if (!ctx->arena.free(ptr)) return fail("mimose_free: pointer not owned by the arena");
+  return 0;
+}
+
+int mimose_mem_stats_get(mimose_ctx* ctx, mimose_mem_stats* out) {
+  if (ctx == nullptr || out == nullptr) return fail("mimose_mem_stats_get: null argument");
+  copy_stats(ctx->arena.stats(), out);
+  return 0;
+}
+
+int mimose_mem_reset_peak(mimose_ctx* ctx) {
+  if (ctx == nullptr) return fail("mimose_mem_reset_peak: null ctx");
+  ctx->arena.reset_peak();
+  return 0;
+}
+
+int mimose_book_create(int64_t capacity, mimose_book** out) {
+  if (out == nullptr || capacity <= 0) return fail("mimose_book_create: bad argument");
+  *out = new mimose_book();
+  (*out)->book.reset(capacity);
+  return 0;
+}
+int mimose_book_destroy(mimose_book* b) {
+  delete b;
+  return 0;
+}
+int64_t mimose_book_alloc(mimose_book* b, int64_t bytes, int tag) {
+  return b->book.allocate(bytes, tag);
+}
+int mimose_book_free(mimose_book* b, int64_t offset) {
+  return b->book.release(offset) ? 0 : fail("mimose_book_free: unknown offset");
+}
+int mimose_book_stats(mimose_book* b, mimose_mem_stats* out) {
+  copy_stats(b->book.stats(), out);
+  return 0;
+}
+
+int mimose_gemm(const mimose_gemm_args* a, void* stream) {
+  if (a == nullptr) return fail("mimose_gemm: null args");
+  mimose_ops::GemmCall c;
+  c.M = a->M; c.N = a->N; c.K = a->K; c.nb1 = a->nb1; c.nb2 = a->nb2;
+  c.A = {a->a, a->a_rows, a->a_cols, a->lda, a->a_bs1, a->a_bs2};
+  c.a_mn = a->a_mn != 0;
+  c.B = {a->b, a->b_rows, a->b_cols, a->ldb, a->b_bs1, a->b_bs2};
+  c.b_mn = a->b_mn != 0;
+  c.epi = a->epi;
+  c.out = a->out; c.out2 = a->out2; c.aux = a->aux; c.bias = a->bias;
+  c.ldo = a->ldo; c.obs1 = a->obs1; c.obs2 = a->obs2;
+  c.alpha = a->alpha; c.beta = a->beta;
+  c.force_bn = a->force_bn;
+  cudaError_t e = mimose_ops::gemm(c, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_gemm");
+  return 0;
+}
+
+}  // extern "C"

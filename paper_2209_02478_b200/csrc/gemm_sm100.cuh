@@ -1,0 +1,305 @@
+// Persistent warp-specialised bf16 GEMM for sm_100a:
+//   TMA (128B-swizzled tiles) -> smem ring (mbarrier full/empty) ->
+//   tcgen05.mma (one elected thread, fp32 accumulators in TMEM, double
+//   buffered) -> tcgen05.ld epilogue (bias / GELU / dGELU / fp32 store).
+//
+//   D[z][m][n] = sum_k A[z][m][k] * B[z][n][k]
+//
+// Either operand may be K-major (k contiguous) or MN-major (m/n contiguous),
+// which is what lets the same kernel run forward (X W^T), data-gradient
+// (dY W) and weight-gradient (dY^T X) contractions plus every batched
+// attention contraction (QK^T, PV, dO V^T, P^T dO, dS K, dS^T Q) without a
+// transpose pass. Batched operands are addressed through 4-D tensor maps
+// (cols, rows, batch1, batch2), so per-head views into the fused QKV buffer
+// need no copies.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "ptx_sm100.cuh"
+
+namespace mimose_dev {
+
+enum EpiKind : int {
+  kEpiBf16 = 0,      // out(bf16) = alpha*acc + bias
+  kEpiBiasGelu = 1,  // out(bf16) = u = acc + bias ; out2(bf16) = gelu(u)
+  kEpiDGelu = 2,     // out(bf16) = acc * gelu'(aux)
+  kEpiF32 = 3,       // out(f32)  = alpha*acc + beta*out
+};
+
+struct GemmParams {
+  int M, N, K;
+  int nb1, nb2;             // batch = nb1 * nb2; z -> (z % nb1, z / nb1)
+  int a_mn, b_mn;           // operand majors (0 = K-major, 1 = MN-major)
+  void* out;                // bf16 or f32 depending on epilogue
+  void* out2;               // bf16 (GELU output)
+  const __nv_bfloat16* aux; // bf16, same addressing as out (dGELU input)
+  const float* bias;        // [N] or nullptr
+  long long ldo, obs1, obs2;  // output strides in elements
+  float alpha, beta;
+  int vec;                  // 1 if 16-byte vector stores/loads are aligned
+};
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+  return cdf + x * pdf;
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
+                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int S = Cfg::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + S * Cfg::kABytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;   // [2]
+  uint64_t* tempty = tfull + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+
+  const int tiles_m = (p.M + kBM - 1) / kBM;
+  const int tiles_n = (p.N + BN - 1) / BN;
+  const int tiles_per_batch = tiles_m * tiles_n;
+  const int num_tiles = tiles_per_batch * p.nb1 * p.nb2;
+  const int num_kb = (p.K + kBK - 1) / kBK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int z = tile / tiles_per_batch;
+        const int t_in = tile % tiles_per_batch;
+        const int m0 = (t_in % tiles_m) * kBM;
+        const int n0 = (t_in / tiles_m) * BN;
+        const int b1 = z % p.nb1, b2 = z / p.nb1;
+        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+          uint8_t* a_dst = sA + s * Cfg::kABytes;
+          uint8_t* b_dst = sB + s * Cfg::kBBytes;
+          const int k0 = kb * kBK;
+          if (!p.a_mn) {
+            tma_load_4d(&tmA, &full[s], a_dst, k0, m0, b1, b2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < kBM / 64; ++j)
+              tma_load_4d(&tmA, &full[s], a_dst + j * 8192, m0 + 64 * j, k0, b1, b2);
+          }
+          if (!p.b_mn) {
+            tma_load_4d(&tmB, &full[s], b_dst, k0, n0, b1, b2);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_4d(&tmB, &full[s], b_dst + j * 8192, n0 + 64 * j, k0, b1, b2);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = idesc_bf16_f32(kBM, BN, p.a_mn != 0, p.b_mn != 0);
+    // K-major: advance 16 elements = 32 B inside the 128 B swizzle row.
+    // MN-major: advance 16 K-rows = 2048 B; LBO = 64 rows * 128 B between MN blocks.
+    const uint32_t a_step = p.a_mn ? 2048u : 32u;
+    const uint32_t b_step = p.b_mn ? 2048u : 32u;
+    const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
+    const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
+    int it = 0, local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int acc = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * BN;
+      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int s = it % S;
+        const uint32_t ph = (it / S) & 1;
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t a_addr = smem_u32(sA + s * Cfg::kABytes);
+          const uint32_t b_addr = smem_u32(sB + s * Cfg::kBBytes);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t da = smem_desc_sw128(a_addr + kk * a_step, a_lbo, 1024);
+            const uint64_t db = smem_desc_sw128(b_addr + kk * b_step, b_lbo, 1024);
+            umma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[s]);
+          if (kb == num_kb - 1) umma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    int local = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+      const int z = tile / tiles_per_batch;
+      const int t_in = tile % tiles_per_batch;
+      const int m0 = (t_in % tiles_m) * kBM;
+      const int n0 = (t_in / tiles_m) * BN;
+      const int b1 = z % p.nb1, b2 = z / p.nb1;
+      const int acc = local & 1;
+      const uint32_t aph = (local >> 1) & 1;
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+
+      const int row = m0 + quarter * 32 + static_cast<int>(lane);
+      const bool row_ok = row < p.M;
+      const long long obase = (long long)b2 * p.obs2 + (long long)b1 * p.obs1 +
+                              (long long)row * p.ldo;
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 16) {
+        float v[16];
+        __syncwarp();
+        tmem_ld16(t_row + c, v);
+        const int col0 = n0 + c;
+        if (row_ok && col0 < p.N) {
+        const bool full16 = p.vec && col0 + 16 <= p.N;
+        if constexpr (EPI == kEpiF32) {
+          float* o = reinterpret_cast<float*>(p.out) + obase + col0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
+          if (full16) {
+            float4* o4 = reinterpret_cast<float4*>(o);
+            if (p.beta != 0.f) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                float4 old = o4[q];
+                v[4 * q + 0] += p.beta * old.x;
+                v[4 * q + 1] += p.beta * old.y;
+                v[4 * q + 2] += p.beta * old.z;
+                v[4 * q + 3] += p.beta * old.w;
+              }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          } else {
+            for (int i = 0; i < 16 && col0 + i < p.N; ++i)
+              o[i] = v[i] + (p.beta != 0.f ? p.beta * o[i] : 0.f);
+          }
+        } else {
+          if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
+            if (p.bias != nullptr) {
+              if (full16) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += __ldg(p.bias + col0 + i);
+              } else {
+                for (int i = 0; i < 16 && col0 + i < p.N; ++i) v[i] += __ldg(p.bias + col0 + i);
+              }
+            }
+          }
+          if constexpr (EPI == kEpiDGelu) {
+            const __nv_bfloat16* ax = p.aux + obase + col0;
+            if (full16) {
+              const uint4* a4 = reinterpret_cast<const uint4*>(ax);
+              uint4 raw[2] = {a4[0], a4[1]};
+              const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(raw);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[i] *= dgelu_f(__bfloat162float(av[i]));
+            } else {
+              for (int i = 0; i < 16 && col0 + i < p.N; ++i)
+                v[i] *= dgelu_f(__bfloat162float(ax[i]));
+            }
+          }
+          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + obase + col0;
+          alignas(16) __nv_bfloat16 hv[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(v[i]);
+          if (full16) {
+            uint4* o4 = reinterpret_cast<uint4*>(o);
+            o4[0] = reinterpret_cast<const uint4*>(hv)[0];
+            o4[1] = reinterpret_cast<const uint4*>(hv)[1];
+          } else {
+            for (int i = 0; i < 16 && col0 + i < p.N; ++i) o[i] = hv[i];
+          }
+          if constexpr (EPI == kEpiBiasGelu) {
+            // GELU of the bf16-rounded pre-activation, so recompute and the
+            // saved u agree bit for bit with what backward differentiates.
+#pragma unroll
+            for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(gelu_f(__bfloat162float(hv[i])));
+            __nv_bfloat16* o2 = reinterpret_cast<__nv_bfloat16*>(p.out2) + obase + col0;
+            if (full16) {
+              uint4* o4 = reinterpret_cast<uint4*>(o2);
+              o4[0] = reinterpret_cast<const uint4*>(hv)[0];
+              o4[1] = reinterpret_cast<const uint4*>(hv)[1];
+            } else {
+              for (int i = 0; i < 16 && col0 + i < p.N; ++i) o2[i] = hv[i];
+            }
+          }
+        }
+        }  // row_ok && col0 < N
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+}  // namespace mimose_dev

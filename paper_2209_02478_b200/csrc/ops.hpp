@@ -1,0 +1,47 @@
+// Internal (C++) interface of the device operators. The public boundary is the
+// C ABI in include/mimose_cuda.h; this header is shared by the operator
+// translation units and the training executor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mimose_ops {
+
+// bf16 matrix view: logical [nb2][nb1][rows][cols], `cols` contiguous.
+// Strides are in elements.
+struct MatView {
+  const void* ptr = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0, bs1 = 0, bs2 = 0;
+};
+
+enum Epi : int { kEpiBf16 = 0, kEpiBiasGelu = 1, kEpiDGelu = 2, kEpiF32 = 3 };
+
+// D[z][m][n] = sum_k A[z][m][k] B[z][n][k]
+//   A: a_mn == false -> view rows=M cols=K ; true -> view rows=K cols=M
+//   B: b_mn == false -> view rows=N cols=K ; true -> view rows=K cols=N
+struct GemmCall {
+  int M = 0, N = 0, K = 0, nb1 = 1, nb2 = 1;
+  MatView A;
+  bool a_mn = false;
+  MatView B;
+  bool b_mn = false;
+  int epi = kEpiBf16;
+  void* out = nullptr;
+  void* out2 = nullptr;
+  const void* aux = nullptr;
+  const float* bias = nullptr;
+  int64_t ldo = 0, obs1 = 0, obs2 = 0;
+  float alpha = 1.f, beta = 0.f;
+  int force_bn = 0;  // 0 = heuristic; 64/128/256 for tests
+};
+
+cudaError_t gemm(const GemmCall& c, cudaStream_t stream);
+
+// Number of kernels launched by this module since process start (telemetry
+// for the bench's gpu_launches count).
+uint64_t launch_count();
+void count_launch();
+
+}  // namespace mimose_ops

@@ -1,0 +1,70 @@
+"""Thin torch-facing wrappers over the C-ABI device operators (tests/bench).
+
+torch is only plumbing here (device buffers, streams); all arithmetic runs in
+the sm_100a kernels of libmimose_cuda.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from ._lib import GemmArgs, check, cuda_lib
+
+EPI_BF16, EPI_BIAS_GELU, EPI_DGELU, EPI_F32 = 0, 1, 2, 3
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _view(t: torch.Tensor, nb1: int, nb2: int):
+    """Describe a bf16 tensor as (ptr, rows, cols, ld, bs1, bs2).
+
+    Accepts 2-D [rows, cols] (nb1 = nb2 = 1), 3-D [nb1, rows, cols] and
+    4-D [nb2, nb1, rows, cols] strided views with a contiguous last dim.
+    """
+    assert t.dtype == torch.bfloat16 and t.stride(-1) == 1
+    if t.dim() == 2:
+        return t.data_ptr(), t.shape[0], t.shape[1], t.stride(0), 0, 0
+    if t.dim() == 3:
+        assert t.shape[0] == nb1 and nb2 == 1
+        return t.data_ptr(), t.shape[1], t.shape[2], t.stride(1), t.stride(0), 0
+    assert t.dim() == 4 and t.shape[0] == nb2 and t.shape[1] == nb1
+    return t.data_ptr(), t.shape[2], t.shape[3], t.stride(2), t.stride(1), t.stride(0)
+
+
+def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None, bias=None,
+         alpha=1.0, beta=0.0, force_bn=0, stream=None):
+    """out[z] = alpha * op(a)[z] @ op(b)[z]^T with the kernel's epilogue.
+
+    a: [.., M, K] (a_mn False) or [.., K, M] (a_mn True); b: [.., N, K] or [.., K, N].
+    out: [.., M, N] (bf16, or fp32 for EPI_F32).
+    """
+    nb2 = out.shape[0] if out.dim() == 4 else 1
+    nb1 = out.shape[-3] if out.dim() >= 3 else 1
+    M, N = out.shape[-2], out.shape[-1]
+    pa = _view(a, nb1, nb2)
+    pb = _view(b, nb1, nb2)
+    K = pa[1] if a_mn else pa[2]
+    assert (pb[1] if b_mn else pb[2]) == K
+    args = GemmArgs()
+    args.M, args.N, args.K, args.nb1, args.nb2 = M, N, K, nb1, nb2
+    args.a, args.a_rows, args.a_cols, args.lda, args.a_bs1, args.a_bs2 = pa
+    args.a_mn = int(a_mn)
+    args.b, args.b_rows, args.b_cols, args.ldb, args.b_bs1, args.b_bs2 = pb
+    args.b_mn = int(b_mn)
+    args.epi = epi
+    args.out = out.data_ptr()
+    args.out2 = out2.data_ptr() if out2 is not None else None
+    args.aux = aux.data_ptr() if aux is not None else None
+    args.bias = bias.data_ptr() if bias is not None else None
+    args.ldo = out.stride(-2)
+    args.obs1 = out.stride(-3) if out.dim() >= 3 else 0
+    args.obs2 = out.stride(0) if out.dim() == 4 else 0
+    args.alpha, args.beta = alpha, beta
+    args.force_bn = force_bn
+    lib = cuda_lib()
+    check(lib.mimose_gemm(C.byref(args), _stream(stream)))
+    return out

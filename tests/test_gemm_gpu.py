@@ -1,0 +1,138 @@
+"""tcgen05 GEMM vs a plain PyTorch fp32 reference of the same contraction.
+
+Tolerance: inputs are bf16 (exact in fp32), accumulation is fp32 in TMEM, so
+the only error is the final bf16 rounding of the output (rel 2^-8) plus fp32
+summation-order noise: |out - ref| <= 1e-2 * |ref| + 1e-2 * rms(ref).
+fp32 outputs: |out - ref| <= 1e-4 * rms(ref) * sqrt(K/64) + 1e-5 * |ref|.
+"""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ops():
+    from paper_2209_02478_b200 import ops
+    return ops
+
+
+def _check_bf16(out, ref):
+    ref = ref.float()
+    rms = ref.pow(2).mean().sqrt().item() + 1e-6
+    err = (out.float() - ref).abs()
+    bound = 1e-2 * ref.abs() + 1e-2 * rms
+    assert torch.all(err <= bound), f"max err {err.max().item()} (rms {rms})"
+
+
+def _check_f32(out, ref, K):
+    rms = ref.pow(2).mean().sqrt().item() + 1e-6
+    err = (out - ref).abs()
+    bound = 1e-4 * rms * math.sqrt(max(K, 64) / 64) + 1e-5 * ref.abs()
+    assert torch.all(err <= bound), f"max err {err.max().item()} (rms {rms})"
+
+
+def _rand(*shape, dev="cuda"):
+    return torch.randn(*shape, device=dev).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("shape", [(256, 256, 128), (200, 72, 80), (1000, 770, 768), (128, 2304, 64)])
+def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape):
+    ops = _ops()
+    torch.manual_seed(0)
+    M, N, K = shape
+    A = _rand(M, K)
+    B = _rand(N, K)
+    a_arg = A.t().contiguous() if a_mn else A
+    b_arg = B.t().contiguous() if b_mn else B
+    if (a_arg.stride(0) * 2) % 16 or (b_arg.stride(0) * 2) % 16:
+        pytest.skip("TMA needs 16-byte row pitch")
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn)
+    torch.cuda.synchronize()
+    _check_bf16(out, A.float() @ B.float().t())
+
+
+@pytest.mark.parametrize("bn", [128, 256])
+def test_gemm_f32_beta(cuda_device, bn):
+    ops = _ops()
+    torch.manual_seed(1)
+    M, N, K = 768, 3072, 4096
+    # weight-gradient form: dW[N,K] = dY^T X with both operands MN-major
+    dY = _rand(K, M)  # [T, N_out]
+    X = _rand(K, N)   # [T, K_in]
+    out = torch.randn(M, N, device="cuda")
+    ref = out * 0.5 + dY.float().t() @ X.float()
+    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, beta=0.5, force_bn=bn)
+    torch.cuda.synchronize()
+    _check_f32(out, ref, K)
+
+
+def test_gemm_bias_gelu_and_dgelu(cuda_device):
+    ops = _ops()
+    torch.manual_seed(2)
+    M, N, K = 517, 3072, 768
+    X = _rand(M, K)
+    W = _rand(N, K) * 0.05
+    bias = torch.randn(N, device="cuda")
+    u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    g = torch.empty_like(u)
+    ops.gemm(X, W, u, epi=ops.EPI_BIAS_GELU, out2=g, bias=bias)
+    torch.cuda.synchronize()
+    u_ref = X.float() @ W.float().t() + bias
+    _check_bf16(u, u_ref)
+    g_ref = torch.nn.functional.gelu(u.float())
+    assert torch.allclose(g.float(), g_ref, rtol=1e-2, atol=1e-2)
+
+    # dGELU epilogue: out = (dY W) * gelu'(u)
+    dY = _rand(M, K)
+    du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    W2 = _rand(K, N) * 0.05  # FFN2 weight [H, 4H]: dgrad B operand is MN-major view [K=H, N=4H]
+    ops.gemm(dY, W2, du, b_mn=True, epi=ops.EPI_DGELU, aux=u)
+    torch.cuda.synchronize()
+    uf = u.float().requires_grad_(True)
+    torch.nn.functional.gelu(uf).backward(torch.ones_like(uf))
+    ref = (dY.float() @ W2.float()) * uf.grad
+    _check_bf16(du, ref)
+
+
+@pytest.mark.parametrize("S", [64, 128, 200, 512])
+def test_gemm_attention_views(cuda_device, S):
+    """Per-head batched views into a fused [B*S, 3H] QKV buffer (no copies)."""
+    ops = _ops()
+    torch.manual_seed(3)
+    B, nh, d = 3, 12, 64
+    H = nh * d
+    qkv = _rand(B * S, 3 * H)
+    q = qkv.view(B, S, 3, nh, d)[:, :, 0].permute(0, 2, 1, 3)  # [B, nh, S, d] strided
+    k = qkv.view(B, S, 3, nh, d)[:, :, 1].permute(0, 2, 1, 3)
+    v = qkv.view(B, S, 3, nh, d)[:, :, 2].permute(0, 2, 1, 3)
+    ld = (S + 7) // 8 * 8
+    scores_buf = torch.empty(B, nh, S, ld, device="cuda", dtype=torch.bfloat16)
+    scores = scores_buf[..., :S]
+    scale = 1.0 / math.sqrt(d)
+    ops.gemm(q, k, scores, alpha=scale)
+    torch.cuda.synchronize()
+    ref = (q.float() @ k.float().transpose(-1, -2)) * scale
+    _check_bf16(scores, ref)
+
+    # ctx = P V with V MN-major (d contiguous), written head-interleaved into [B*S, H]
+    P = torch.softmax(ref, -1).to(torch.bfloat16)
+    Pbuf = torch.zeros(B, nh, S, ld, device="cuda", dtype=torch.bfloat16)
+    Pbuf[..., :S] = P
+    ctx = torch.empty(B * S, H, device="cuda", dtype=torch.bfloat16)
+    ctx_v = ctx.view(B, S, nh, d).permute(0, 2, 1, 3)
+    ops.gemm(Pbuf[..., :S], v, ctx_v, b_mn=True)
+    torch.cuda.synchronize()
+    _check_bf16(ctx_v, P.float() @ v.float())
+
+    # dV = P^T dO (both MN-major), dK = dS^T Q
+    dO = _rand(B, nh, S, d)
+    dV = torch.empty(B, nh, S, d, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(Pbuf[..., :S], dO, dV, a_mn=True, b_mn=True)
+    torch.cuda.synchronize()
+    _check_bf16(dV, P.float().transpose(-1, -2) @ dO.float())
