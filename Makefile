@@ -14,6 +14,11 @@ CXXFLAGS:= -O2 -std=c++20 -fPIC -Wall -Wextra -Iinclude
 
 CU_SRCS := $(wildcard $(CSRC)/*.cu)
 CU_OBJS := $(patsubst $(CSRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))
+# host-only translation units (C++20, built by g++: nvcc's front end is not
+# used for the planner headers)
+CPP_SRCS := $(wildcard $(CSRC)/*.cpp)
+CPP_OBJS := $(patsubst $(CSRC)/%.cpp,$(BUILD)/%.cpp.o,$(CPP_SRCS))
+CUDA_INC := $(dir $(shell which $(NVCC)))../include
 HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) $(wildcard include/*.h) \
            $(wildcard include/mimose/*.hpp)
 
@@ -23,8 +28,12 @@ $(BUILD)/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(BUILD)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(PKG)/libmimose_cuda.so: $(CU_OBJS)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS)
+$(BUILD)/%.cpp.o: $(CSRC)/%.cpp $(HDRS)
+	@mkdir -p $(BUILD)
+	$(CXX) $(CXXFLAGS) -I$(CSRC) -I$(CUDA_INC) -c $< -o $@
+
+$(PKG)/libmimose_cuda.so: $(CU_OBJS) $(CPP_OBJS)
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) $(CPP_OBJS)
 
 $(PKG)/libmimose_host.so: $(CSRC)/host/planner_capi.cpp $(HDRS)
 	$(CXX) $(CXXFLAGS) -shared -o $@ $<

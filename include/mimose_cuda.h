@@ -94,6 +94,117 @@ typedef struct {
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);
 
+/* ------------------------------------------------------------------ trainer
+ * The training executor: BERT-style encoder blocks (post-LN, GELU FFN,
+ * materialised attention) + multiple-choice head, trained with AdamW under
+ * the context's byte budget. Replaces the reference's replayed iteration
+ * (harness.hpp:139 run_experiment, Mimose branch harness.hpp:215-296) with a
+ * real one; planning calls the host planner (include/mimose) in-process. */
+typedef struct {
+  int layers, hidden, heads, ffn, vocab, max_pos, type_vocab;
+  int num_choices;        /* multiple-choice group size C (batch % C == 0) */
+  float hidden_dropout, attn_dropout, ln_eps, init_std;
+  uint64_t seed;
+} mimose_model_cfg;
+
+enum {
+  MIMOSE_PLANNER_MIMOSE = 0, /* two-phase input-aware planner (the product) */
+  MIMOSE_PLANNER_NONE = 1,   /* no checkpointing (throughput reference) */
+  MIMOSE_PLANNER_ALL = 2,    /* checkpoint every block */
+  MIMOSE_PLANNER_STATIC = 3  /* plan once for seq_max, reuse (baselines.hpp:20) */
+};
+
+typedef struct {
+  int planner;
+  int batch;                   /* sequences per step B (x = B * S) */
+  int seq_min, seq_max;        /* S range -> model input range [B*seq_min, B*seq_max] */
+  int64_t reserve_bytes;       /* < 0: automatic (extras at seq_max + margin) */
+  double bucket_tolerance;     /* scheduler.hpp:26 */
+  double cache_tolerance;      /* scheduler.hpp:27 */
+  int max_sheltered_iters;     /* collector.hpp:92 */
+  int collect_new_sizes_always;/* collector.hpp:93 */
+  int estimator_order;         /* harness.hpp:53 */
+  float lr, beta1, beta2, adam_eps, weight_decay, max_grad_norm;
+} mimose_train_cfg;
+
+enum {
+  MIMOSE_PHASE_PLANNED = 0,   /* responsive: cache hit or freshly generated plan */
+  MIMOSE_PHASE_COLLECT = 1,   /* sheltered: measuring pass, all blocks dropped */
+  MIMOSE_PHASE_SHELTERED = 2, /* sheltered: seen size, all blocks dropped */
+  MIMOSE_PHASE_PLAIN = 3,     /* planner none / all / static / forced */
+  MIMOSE_PHASE_FALLBACK = 4   /* post-window collection (too few sizes to fit) */
+};
+
+typedef struct {
+  int64_t iter;
+  int64_t x;
+  int batch, seq;
+  int phase;
+  int cache_hit;
+  int plan_size;
+  int insufficient;
+  int fit_order;               /* order of the fit performed this step, -1 none */
+  float loss;                  /* filled by the host-input step (after D2H) */
+  int64_t peak_requested;      /* arena peak during this step */
+  int64_t peak_reserved;
+  int64_t predicted_kept;      /* constant + predicted kept bytes (scheduler view) */
+  int64_t budget;
+  double plan_us;              /* lookup_or_plan wall time */
+  double fit_us;               /* fit wall time */
+  uint64_t dropped_mask_lo;    /* bit i = block i dropped (blocks 0..63) */
+} mimose_step_report;
+
+typedef void (*mimose_grad_hook)(void* user, float* grads, int64_t n, void* stream);
+
+int mimose_trainer_create(mimose_ctx* ctx, const mimose_model_cfg* m, const mimose_train_cfg* t,
+                          mimose_trainer** out);
+int mimose_trainer_destroy(mimose_trainer* tr);
+/* Full step from HOST inputs (pinned for async copies): H2D, forward,
+ * backward, grad hook, AdamW, loss D2H (synchronises the stream).
+ * tokens/types: [batch*seq] int32, labels: [batch/num_choices] int32. */
+int mimose_trainer_step(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                        const int32_t* labels, int batch, int seq, void* stream,
+                        mimose_step_report* rep);
+/* Same, without the optimizer (gradients left in the flat grad buffer). */
+int mimose_trainer_forward_backward(mimose_trainer* tr, const int32_t* tokens,
+                                    const int32_t* types, const int32_t* labels, int batch,
+                                    int seq, void* stream, mimose_step_report* rep);
+/* Step from DEVICE-resident inputs (no host sync; loss stays on device).
+ * perm/seg/uid: token tables from mimose_build_token_tables. */
+int mimose_trainer_step_device(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                               const int32_t* labels, const int32_t* perm, const int32_t* seg,
+                               const int32_t* uid, int n_unique, int batch, int seq,
+                               int do_optimizer, void* stream, mimose_step_report* rep);
+int mimose_trainer_optimizer_step(mimose_trainer* tr, float grad_scale, void* stream);
+/* Force a plan (block ids) for subsequent steps (active=0 restores the planner). */
+int mimose_trainer_force_plan(mimose_trainer* tr, const int* ids, int n, int active);
+int mimose_trainer_set_grad_hook(mimose_trainer* tr, mimose_grad_hook fn, void* user);
+
+/* Device buffers: fp32 master params, bf16 params, fp32 grads (flat). */
+int mimose_trainer_buffers(mimose_trainer* tr, float** p32, void** p16, float** g32,
+                           int64_t* n, float** d_loss, float** d_logits);
+int mimose_trainer_param_count(mimose_trainer* tr);
+int mimose_trainer_param_info(mimose_trainer* tr, int i, const char** name, int64_t* offset,
+                              int64_t* numel);
+/* Re-derive the bf16 copy after params_f32 was written externally. */
+int mimose_trainer_sync_params(mimose_trainer* tr, void* stream);
+
+/* Planner state as the reference's own text formats (caller frees with
+ * mimose_free_string): collected samples (collector.hpp:198 CSV), fitted
+ * estimator (estimator.hpp:182 dump), model document (model_spec.hpp:268). */
+int mimose_trainer_samples_csv(mimose_trainer* tr, char** out);
+int mimose_trainer_estimator_text(mimose_trainer* tr, char** out);
+int mimose_trainer_model_text(mimose_trainer* tr, char** out);
+int mimose_trainer_info(mimose_trainer* tr, int64_t* constant_bytes, int64_t* reserve_bytes,
+                        int64_t* budget, int* trained, int64_t* cache_hits,
+                        int64_t* cache_misses);
+void mimose_free_string(char* s);
+
+/* Host helper: stable counting sort of token ids for the deterministic
+ * word-embedding gradient. perm: [T], seg: [T+1], uid: [T]. */
+int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32_t* perm,
+                              int32_t* seg, int32_t* uid, int* n_unique);
+
 #ifdef __cplusplus
 }
 #endif

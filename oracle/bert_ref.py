@@ -1,0 +1,184 @@
+"""CPU numerics oracle for the B200 training step (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may use
+this module, and only as the checker / the timed CPU baseline - never as the
+product path.
+
+What it restates: the transformer-block training step the north star puts on
+the GPU (post-LN BERT encoder block with materialised
+attention, GELU FFN, multiple-choice head, AdamW-free fwd+bwd), in plain
+PyTorch-CPU fp32/fp64 with autograd. The reference has no tensor code (its
+layer is the byte polynomial of reference proj/include/mimose/model_spec.hpp:
+76-78, its iteration the replay of simulator.hpp:104-160), so numerical
+parity here is anchored on the paper's framework - HuggingFace
+BertForMultipleChoice as of transformers v4.18 on PyTorch 1.11
+ - whose block structure this follows:
+  embeddings = dropout(LN(word + position + token_type))
+  block:  h1 = LN(h + dropout(Wo . attn(h)))  attn probs dropped out
+          h2 = LN(h1 + dropout(W2 . gelu(W1 . h1)))       (exact erf GELU)
+  head:   logits = dropout(tanh(Wp . h[:, 0])) . wc + bc ; CE over choices
+"parity unpinned" against the reference itself (no reference vectors exist
+for tensors); loss/grad agreement with the GPU is checked at stated
+tolerances in tests/test_trainer_gpu.py.
+
+Dropout masks are reproduced bit-exactly with a numpy restatement of the
+Philox4x32-10 counter scheme the kernels use, so parity holds with dropout on.
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict
+
+import numpy as np
+import torch
+
+SITE_ATTN_PROBS, SITE_ATTN_OUT, SITE_FFN_OUT, SITE_EMBED, SITE_POOL = 0, 1, 2, 3, 4
+
+# ----------------------------------------------------------------- Philox
+_M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_W0, _W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
+_MASK32 = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(seed: int, stream: int, groups: np.ndarray) -> np.ndarray:
+    """Philox4x32-10 with key=seed, counter=(group_lo, group_hi, stream_lo, stream_hi).
+
+    Returns uint32 [len(groups), 4]. Restates mimose_dev::Philox (csrc/common.cuh).
+    """
+    g = groups.astype(np.uint64)
+    c0 = (g & _MASK32).astype(np.uint32)
+    c1 = (g >> np.uint64(32)).astype(np.uint32)
+    c2 = np.full_like(c0, np.uint32(stream & 0xFFFFFFFF))
+    c3 = np.full_like(c0, np.uint32((stream >> 32) & 0xFFFFFFFF))
+    k0 = np.uint32(seed & 0xFFFFFFFF)
+    k1 = np.uint32((seed >> 32) & 0xFFFFFFFF)
+    with np.errstate(over="ignore"):
+        for _ in range(10):
+            p0 = c0.astype(np.uint64) * _M0
+            p1 = c2.astype(np.uint64) * _M1
+            hi0, lo0 = (p0 >> np.uint64(32)).astype(np.uint32), (p0 & _MASK32).astype(np.uint32)
+            hi1, lo1 = (p1 >> np.uint64(32)).astype(np.uint32), (p1 & _MASK32).astype(np.uint32)
+            c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+            k0 = np.uint32((int(k0) + int(_W0)) & 0xFFFFFFFF)
+            k1 = np.uint32((int(k1) + int(_W1)) & 0xFFFFFFFF)
+    return np.stack([c0, c1, c2, c3], axis=-1)
+
+
+def dropout_threshold(p: float) -> int:
+    if p <= 0.0:
+        return 0
+    t = p * 4294967296.0
+    thr = 0xFFFFFFFF if t >= 4294967295.0 else int(t)
+    return max(thr, 1)
+
+
+def keep_mask(p: float, seed: int, stream: int, idx: np.ndarray) -> np.ndarray:
+    """Boolean keep mask for element indices `idx` (any shape)."""
+    thr = dropout_threshold(p)
+    if thr == 0:
+        return np.ones(idx.shape, dtype=bool)
+    flat = idx.reshape(-1).astype(np.uint64)
+    groups = flat >> np.uint64(2)
+    ug, inv = np.unique(groups, return_inverse=True)
+    r = philox4x32_10(seed, stream, ug)
+    words = r[inv, (flat & np.uint64(3)).astype(np.int64)]
+    return (words >= np.uint32(thr)).reshape(idx.shape)
+
+
+def stream_id(step: int, layer: int, site: int) -> int:
+    return (step << 20) | ((layer & 0xFFFF) << 4) | site
+
+
+# ----------------------------------------------------------------- model
+def param_shapes(cfg) -> Dict[str, tuple]:
+    H, F, V, P, Ty = cfg.hidden, cfg.ffn, cfg.vocab, cfg.max_pos, cfg.type_vocab
+    shp = {
+        "embeddings.word": (V, H), "embeddings.position": (P, H),
+        "embeddings.token_type": (Ty, H),
+        "embeddings.ln.weight": (H,), "embeddings.ln.bias": (H,),
+        "pooler.weight": (H, H), "pooler.bias": (H,),
+        "classifier.weight": (H,), "classifier.bias": (1,),
+    }
+    for l in range(cfg.layers):
+        p = f"layer.{l}."
+        shp.update({
+            p + "attn.qkv.weight": (3 * H, H), p + "attn.qkv.bias": (3 * H,),
+            p + "attn.out.weight": (H, H), p + "attn.out.bias": (H,),
+            p + "attn.ln.weight": (H,), p + "attn.ln.bias": (H,),
+            p + "ffn.in.weight": (F, H), p + "ffn.in.bias": (F,),
+            p + "ffn.out.weight": (H, F), p + "ffn.out.bias": (H,),
+            p + "ffn.ln.weight": (H,), p + "ffn.ln.bias": (H,),
+        })
+    return shp
+
+
+def _drop(x: torch.Tensor, p: float, seed: int, stream: int, idx: np.ndarray) -> torch.Tensor:
+    if p <= 0.0:
+        return x
+    m = torch.from_numpy(keep_mask(p, seed, stream, idx)).to(x.dtype)
+    return x * m * (1.0 / (1.0 - p))
+
+
+def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.ndarray,
+                   labels: np.ndarray, cfg, step: int = 0, dtype=torch.float32):
+    """Forward + backward on CPU. Returns (loss, logits, {name: grad ndarray})."""
+    shapes = param_shapes(cfg)
+    P = {k: torch.tensor(np.asarray(v, dtype=np.float64).reshape(shapes[k]), dtype=dtype,
+                         requires_grad=True) for k, v in params.items() if k in shapes}
+    B, S = tokens.shape
+    H, nh, L = cfg.hidden, cfg.heads, cfg.layers
+    d = H // nh
+    T = B * S
+    ld = (S + 7) // 8 * 8
+    seed = cfg.seed
+    ph, pa = cfg.hidden_dropout, cfg.attn_dropout
+    tok = torch.from_numpy(tokens.astype(np.int64)).reshape(-1)
+    typ = torch.from_numpy(types.astype(np.int64)).reshape(-1)
+    pos = torch.arange(S).repeat(B)
+    hid_idx = (np.arange(T, dtype=np.uint64)[:, None] * np.uint64(H)
+               + np.arange(H, dtype=np.uint64)[None, :])
+
+    def ln(x, w, b):
+        return torch.nn.functional.layer_norm(x, (H,), P[w], P[b], eps=cfg.ln_eps)
+
+    e = P["embeddings.word"][tok] + P["embeddings.position"][pos] + P["embeddings.token_type"][typ]
+    h = _drop(ln(e, "embeddings.ln.weight", "embeddings.ln.bias"), ph, seed,
+              stream_id(step, L, SITE_EMBED), hid_idx)
+    rows = np.arange(B * nh * S, dtype=np.uint64).reshape(B, nh, S, 1)
+    att_idx = rows * np.uint64(ld) + np.arange(S, dtype=np.uint64)[None, None, None, :]
+    for l in range(L):
+        p = f"layer.{l}."
+        qkv = h @ P[p + "attn.qkv.weight"].T + P[p + "attn.qkv.bias"]
+        q, k, v = (qkv[:, i * H:(i + 1) * H].reshape(B, S, nh, d).permute(0, 2, 1, 3)
+                   for i in range(3))
+        sc = (q @ k.transpose(-1, -2)) / math.sqrt(d)
+        pr = torch.softmax(sc, dim=-1)
+        pr = _drop(pr, pa, seed, stream_id(step, l, SITE_ATTN_PROBS), att_idx)
+        ctx = (pr @ v).permute(0, 2, 1, 3).reshape(T, H)
+        a = ctx @ P[p + "attn.out.weight"].T + P[p + "attn.out.bias"]
+        h1 = ln(h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx),
+                p + "attn.ln.weight", p + "attn.ln.bias")
+        u = h1 @ P[p + "ffn.in.weight"].T + P[p + "ffn.in.bias"]
+        g = torch.nn.functional.gelu(u)
+        f = g @ P[p + "ffn.out.weight"].T + P[p + "ffn.out.bias"]
+        h = ln(h1 + _drop(f, ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx),
+               p + "ffn.ln.weight", p + "ffn.ln.bias")
+    cls = h.reshape(B, S, H)[:, 0, :]
+    pooled = torch.tanh(cls @ P["pooler.weight"].T + P["pooler.bias"])
+    pool_idx = (np.arange(B, dtype=np.uint64)[:, None] * np.uint64(H)
+                + np.arange(H, dtype=np.uint64)[None, :])
+    pooled = _drop(pooled, ph, seed, stream_id(step, L, SITE_POOL), pool_idx)
+    logits = pooled @ P["classifier.weight"] + P["classifier.bias"]
+    C = cfg.num_choices
+    lg = logits.reshape(B // C, C)
+    loss = torch.nn.functional.cross_entropy(lg, torch.from_numpy(labels.astype(np.int64)))
+    loss.backward()
+    grads = {k: t.grad.detach().numpy().reshape(-1).copy() for k, t in P.items()}
+    return float(loss.detach()), logits.detach().numpy(), grads
+
+
+def numpy_bf16_round(x: np.ndarray) -> np.ndarray:
+    """Round fp32 values to bf16 (round-to-nearest-even), returned as fp32."""
+    a = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = ((a + np.uint64(0x7FFF) + ((a >> np.uint64(16)) & np.uint64(1))) >> np.uint64(16)) << np.uint64(16)
+    return (r & np.uint64(0xFFFFFFFF)).astype(np.uint32).view(np.float32)

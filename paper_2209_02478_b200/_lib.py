@@ -65,6 +65,49 @@ class GemmArgs(C.Structure):
     ]
 
 
+class ModelCfg(C.Structure):
+    _fields_ = [
+        ("layers", C.c_int), ("hidden", C.c_int), ("heads", C.c_int), ("ffn", C.c_int),
+        ("vocab", C.c_int), ("max_pos", C.c_int), ("type_vocab", C.c_int),
+        ("num_choices", C.c_int),
+        ("hidden_dropout", C.c_float), ("attn_dropout", C.c_float), ("ln_eps", C.c_float),
+        ("init_std", C.c_float),
+        ("seed", C.c_uint64),
+    ]
+
+
+class TrainCfg(C.Structure):
+    _fields_ = [
+        ("planner", C.c_int), ("batch", C.c_int), ("seq_min", C.c_int), ("seq_max", C.c_int),
+        ("reserve_bytes", C.c_int64),
+        ("bucket_tolerance", C.c_double), ("cache_tolerance", C.c_double),
+        ("max_sheltered_iters", C.c_int), ("collect_new_sizes_always", C.c_int),
+        ("estimator_order", C.c_int),
+        ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
+        ("weight_decay", C.c_float), ("max_grad_norm", C.c_float),
+    ]
+
+
+class StepReport(C.Structure):
+    _fields_ = [
+        ("iter", C.c_int64), ("x", C.c_int64), ("batch", C.c_int), ("seq", C.c_int),
+        ("phase", C.c_int), ("cache_hit", C.c_int), ("plan_size", C.c_int),
+        ("insufficient", C.c_int), ("fit_order", C.c_int), ("loss", C.c_float),
+        ("peak_requested", C.c_int64), ("peak_reserved", C.c_int64),
+        ("predicted_kept", C.c_int64), ("budget", C.c_int64),
+        ("plan_us", C.c_double), ("fit_us", C.c_double),
+        ("dropped_mask_lo", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+GRAD_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+_P = C.c_void_p
+_I32P = C.POINTER(C.c_int32)
+
 # (name, restype, argtypes) for every symbol include/mimose_cuda.h declares.
 CUDA_SYMBOLS = [
     ("mimose_abi_version", C.c_int, []),
@@ -82,6 +125,35 @@ CUDA_SYMBOLS = [
     ("mimose_book_free", C.c_int, [C.c_void_p, C.c_int64]),
     ("mimose_book_stats", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
     ("mimose_gemm", C.c_int, [C.POINTER(GemmArgs), C.c_void_p]),
+    ("mimose_trainer_create", C.c_int,
+     [_P, C.POINTER(ModelCfg), C.POINTER(TrainCfg), C.POINTER(C.c_void_p)]),
+    ("mimose_trainer_destroy", C.c_int, [_P]),
+    ("mimose_trainer_step", C.c_int,
+     [_P, _P, _P, _P, C.c_int, C.c_int, _P, C.POINTER(StepReport)]),
+    ("mimose_trainer_forward_backward", C.c_int,
+     [_P, _P, _P, _P, C.c_int, C.c_int, _P, C.POINTER(StepReport)]),
+    ("mimose_trainer_step_device", C.c_int,
+     [_P, _P, _P, _P, _P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P,
+      C.POINTER(StepReport)]),
+    ("mimose_trainer_optimizer_step", C.c_int, [_P, C.c_float, _P]),
+    ("mimose_trainer_force_plan", C.c_int, [_P, C.POINTER(C.c_int), C.c_int, C.c_int]),
+    ("mimose_trainer_set_grad_hook", C.c_int, [_P, GRAD_HOOK, _P]),
+    ("mimose_trainer_buffers", C.c_int,
+     [_P, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P), C.POINTER(C.c_int64),
+      C.POINTER(_P), C.POINTER(_P)]),
+    ("mimose_trainer_param_count", C.c_int, [_P]),
+    ("mimose_trainer_param_info", C.c_int,
+     [_P, C.c_int, C.POINTER(C.c_char_p), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("mimose_trainer_sync_params", C.c_int, [_P, _P]),
+    ("mimose_trainer_samples_csv", C.c_int, [_P, C.POINTER(_P)]),
+    ("mimose_trainer_estimator_text", C.c_int, [_P, C.POINTER(_P)]),
+    ("mimose_trainer_model_text", C.c_int, [_P, C.POINTER(_P)]),
+    ("mimose_trainer_info", C.c_int,
+     [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+      C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    ("mimose_free_string", None, [_P]),
+    ("mimose_build_token_tables", C.c_int,
+     [_P, C.c_int64, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]),
 ]
 
 
@@ -100,11 +172,6 @@ def cuda_lib():
             raise MimoseError(f"{CUDA_LIB_PATH} missing: run `make` (no CPU fallback exists)")
         lib = C.CDLL(CUDA_LIB_PATH)
         _bind(lib, CUDA_SYMBOLS)
-        try:
-            from . import _cuda_syms  # noqa: F401  (extended symbol table)
-            _bind(lib, _cuda_syms.SYMBOLS)
-        except ImportError:
-            pass
         _cuda = lib
     return _cuda
 
@@ -114,3 +181,11 @@ def check(rc, lib=None):
         lib = lib or cuda_lib()
         raise MimoseError(lib.mimose_last_error().decode())
     return rc
+
+
+def take_string(lib, ptr):
+    """Copy a library-allocated C string and free it."""
+    try:
+        return C.cast(ptr, C.c_char_p).value.decode()
+    finally:
+        lib.mimose_free_string(ptr)

@@ -1,0 +1,89 @@
+// Device helpers shared by the memory-bound kernels: counter-based dropout
+// RNG, bf16 <-> fp32 vector packing, warp reductions.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dropout_cfg.hpp"
+
+namespace mimose_dev {
+
+// ------------------------------------------------------------------ Philox
+// Philox4x32-10 (Salmon et al., SC'11). Dropout masks are a pure function of
+// (seed, stream, element index): recompute of a dropped layer and the
+// sheltered measuring pass regenerate bit-identical masks without saving
+// them (replaces the paper's RNG save/restore).
+struct Philox {
+  uint32_t r[4];
+  __device__ __forceinline__ Philox(uint64_t seed, uint64_t stream, uint64_t group) {
+    uint32_t c0 = (uint32_t)group, c1 = (uint32_t)(group >> 32);
+    uint32_t c2 = (uint32_t)stream, c3 = (uint32_t)(stream >> 32);
+    uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+      const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+      c0 = hi1 ^ c1 ^ k0;
+      c1 = lo1;
+      c2 = hi0 ^ c3 ^ k1;
+      c3 = lo0;
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    r[0] = c0; r[1] = c1; r[2] = c2; r[3] = c3;
+  }
+};
+
+// keep-mask bits for 8 consecutive elements starting at `idx` (idx % 8 == 0):
+// element idx + e uses word (e & 3) of Philox group (idx >> 2) + (e >> 2).
+__device__ __forceinline__ uint32_t dropout_mask8(const DropoutCfg& d, uint64_t idx) {
+  if (d.threshold == 0) return 0xFFu;
+  const Philox a(d.seed, d.stream, idx >> 2);
+  const Philox b(d.seed, d.stream, (idx >> 2) + 1);
+  uint32_t m = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    m |= (a.r[e] >= d.threshold ? 1u : 0u) << e;
+    m |= (b.r[e] >= d.threshold ? 1u : 0u) << (e + 4);
+  }
+  return m;
+}
+
+// ------------------------------------------------------------------ vectors
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 raw = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 raw;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = raw;
+}
+
+// Round-trip through bf16 (value a kernel would observe after store + load).
+__device__ __forceinline__ float bf16r(float x) { return __bfloat162float(__float2bfloat16_rn(x)); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+}  // namespace mimose_dev

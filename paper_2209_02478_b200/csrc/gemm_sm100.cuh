@@ -25,7 +25,7 @@
 namespace mimose_dev {
 
 enum EpiKind : int {
-  kEpiBf16 = 0,      // out(bf16) = alpha*acc + bias
+  kEpiBf16 = 0,      // out(bf16) = alpha*acc + bias (+ aux)
   kEpiBiasGelu = 1,  // out(bf16) = u = acc + bias ; out2(bf16) = gelu(u)
   kEpiDGelu = 2,     // out(bf16) = acc * gelu'(aux)
   kEpiF32 = 3,       // out(f32)  = alpha*acc + beta*out
@@ -245,6 +245,21 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                 for (int i = 0; i < 16; ++i) v[i] += __ldg(p.bias + col0 + i);
               } else {
                 for (int i = 0; i < 16 && col0 + i < p.N; ++i) v[i] += __ldg(p.bias + col0 + i);
+              }
+            }
+          }
+          if constexpr (EPI == kEpiBf16) {
+            // optional residual: out = alpha*acc + bias + aux (gradient sums)
+            if (p.aux != nullptr) {
+              const __nv_bfloat16* ax = p.aux + obase + col0;
+              if (full16) {
+                const uint4* a4 = reinterpret_cast<const uint4*>(ax);
+                uint4 raw[2] = {a4[0], a4[1]};
+                const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(raw);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += __bfloat162float(av[i]);
+              } else {
+                for (int i = 0; i < 16 && col0 + i < p.N; ++i) v[i] += __bfloat162float(ax[i]);
               }
             }
           }

@@ -1,0 +1,767 @@
+// Memory-bound sm_100a kernels of the transformer step: residual + dropout +
+// LayerNorm (fwd / bwd), embedding gather + LayerNorm, scaled softmax +
+// dropout (fwd / bwd), deterministic column reductions, embedding gradients,
+// multiple-choice head + cross-entropy, fused AdamW with global-norm clip.
+//
+// Rules every kernel here follows:
+//   * 16-byte vector loads/stores, one warp per row, warp-shuffle reductions;
+//   * no atomics: every reduction is two-stage in a fixed order, so a
+//     recomputed (checkpointed) layer and a saved one produce bit-identical
+//     gradients;
+//   * dropout masks come from Philox(seed, stream, element) - never stored.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "ops.hpp"
+#include "ops_mem.hpp"
+
+namespace mimose_dev {
+
+using bf16 = __nv_bfloat16;
+
+// =====================================================================
+// LayerNorm forward (one warp per row; VPL 8-element chunks per lane)
+// =====================================================================
+template <int VPL>
+__device__ __forceinline__ void ln_row_finish(float (&z)[VPL][8], int row, int lane,
+                                              const mimose_ops::LnFwdArgs& a) {
+  constexpr int H = VPL * 256;
+  // z arrives already rounded to bf16 (what is saved is what is normalised)
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < VPL; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += z[c][e];
+  const float mean = warp_sum(s) * (1.f / H);
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < VPL; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float d = z[c][e] - mean;
+      q += d * d;
+    }
+  const float var = warp_sum(q) * (1.f / H);
+  const float rstd = rsqrtf(var + a.eps);
+  if (a.stats != nullptr && lane == 0)
+    reinterpret_cast<float2*>(a.stats)[row] = make_float2(mean, rstd);
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    const uint64_t idx = (uint64_t)row * H + col;
+    float y[8], g[8], b[8];
+    const float4* g4 = reinterpret_cast<const float4*>(a.gamma + col);
+    const float4* b4 = reinterpret_cast<const float4*>(a.beta + col);
+    *reinterpret_cast<float4*>(g) = g4[0];
+    *reinterpret_cast<float4*>(g + 4) = g4[1];
+    *reinterpret_cast<float4*>(b) = b4[0];
+    *reinterpret_cast<float4*>(b + 4) = b4[1];
+    const uint32_t m = dropout_mask8(a.out_drop, idx);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = (z[c][e] - mean) * rstd * g[e] + b[e];
+      y[e] = ((m >> e) & 1u) ? v * a.out_drop.scale : 0.f;
+    }
+    store8(static_cast<bf16*>(a.y) + idx, y);
+  }
+}
+
+// z = res + dropout(branch); y = LN(z)
+template <int VPL>
+__global__ void __launch_bounds__(256) add_ln_fwd_kernel(const mimose_ops::LnFwdArgs a) {
+  constexpr int H = VPL * 256;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= a.rows) return;
+  float z[VPL][8];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    const uint64_t idx = (uint64_t)row * H + col;
+    float br[8];
+    load8(static_cast<const bf16*>(a.br) + idx, br);
+    const uint32_t m = dropout_mask8(a.br_drop, idx);
+    float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (a.res != nullptr) load8(static_cast<const bf16*>(a.res) + idx, r);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      z[c][e] = bf16r(r[e] + (((m >> e) & 1u) ? br[e] * a.br_drop.scale : 0.f));
+    if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + idx, z[c]);
+  }
+  ln_row_finish<VPL>(z, row, lane, a);
+}
+
+// z = word[tok] + pos[s] + type[tt]; y = dropout(LN(z))
+template <int VPL>
+__global__ void __launch_bounds__(256) embed_ln_fwd_kernel(const mimose_ops::LnFwdArgs a,
+                                                          const int32_t* tok, const int32_t* tt,
+                                                          const bf16* word, const bf16* pos,
+                                                          const bf16* type, int S) {
+  constexpr int H = VPL * 256;
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= a.rows) return;
+  const int64_t w = tok[row];
+  const int64_t t = tt[row];
+  const int64_t s = row % S;
+  float z[VPL][8];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    const int col = 8 * (lane + 32 * c);
+    float x0[8], x1[8], x2[8];
+    load8(word + w * H + col, x0);
+    load8(pos + s * H + col, x1);
+    load8(type + t * H + col, x2);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) z[c][e] = bf16r(x0[e] + x1[e] + x2[e]);
+    if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + (uint64_t)row * H + col, z[c]);
+  }
+  ln_row_finish<VPL>(z, row, lane, a);
+}
+
+// =====================================================================
+// LayerNorm backward (+ dropout backward of the branch / of the input)
+//   dy_eff = (dy + dy2) [* in-dropout mask]
+//   dz     = rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy_eff * gamma
+//   dbr    = dz * branch-dropout mask * scale
+// per-block partials: [3][H] = {sum dy_eff*xhat, sum dy_eff, sum dbr}
+// =====================================================================
+template <int VPL>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const mimose_ops::LnBwdArgs a) {
+  constexpr int H = VPL * 256;
+  extern __shared__ float red[];  // [8 warps][3][H]
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  float acc_g[VPL][8], acc_b[VPL][8], acc_d[VPL][8];
+#pragma unroll
+  for (int c = 0; c < VPL; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc_g[c][e] = acc_b[c][e] = acc_d[c][e] = 0.f;
+
+  for (int row = blockIdx.x * 8 + warp; row < a.rows; row += gridDim.x * 8) {
+    const float2 st = reinterpret_cast<const float2*>(a.stats)[row];
+    float xh[VPL][8], dy[VPL][8], gg[VPL][8];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      const uint64_t idx = (uint64_t)row * H + col;
+      float zz[8], g[8];
+      load8(static_cast<const bf16*>(a.z) + idx, zz);
+      load8(static_cast<const bf16*>(a.dy) + idx, dy[c]);
+      if (a.dy2 != nullptr) {
+        float d2[8];
+        load8(static_cast<const bf16*>(a.dy2) + idx, d2);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dy[c][e] += d2[e];
+      }
+      const uint32_t m = dropout_mask8(a.in_drop, idx);
+      const float4* g4 = reinterpret_cast<const float4*>(a.gamma + col);
+      *reinterpret_cast<float4*>(g) = g4[0];
+      *reinterpret_cast<float4*>(g + 4) = g4[1];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (a.in_drop.threshold != 0) dy[c][e] = ((m >> e) & 1u) ? dy[c][e] * a.in_drop.scale : 0.f;
+        xh[c][e] = (zz[e] - st.x) * st.y;
+        gg[c][e] = dy[c][e] * g[e];
+        s1 += gg[c][e];
+        s2 += gg[c][e] * xh[c][e];
+      }
+    }
+    const float mg = warp_sum(s1) * (1.f / H);
+    const float mgx = warp_sum(s2) * (1.f / H);
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      const uint64_t idx = (uint64_t)row * H + col;
+      float dz[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dz[e] = st.y * (gg[c][e] - mg - xh[c][e] * mgx);
+      store8(static_cast<bf16*>(a.dz) + idx, dz);
+      const uint32_t m = dropout_mask8(a.br_drop, idx);
+      float db[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        db[e] = bf16r(((m >> e) & 1u) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
+      if (a.dbr != nullptr) store8(static_cast<bf16*>(a.dbr) + idx, db);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        acc_g[c][e] += dy[c][e] * xh[c][e];
+        acc_b[c][e] += dy[c][e];
+        acc_d[c][e] += db[e];
+      }
+    }
+  }
+  // fixed-order block reduction -> partial[blockIdx.x][3][H]
+#pragma unroll
+  for (int c = 0; c < VPL; ++c) {
+    const int col = 8 * (lane + 32 * c);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      red[(warp * 3 + 0) * H + col + e] = acc_g[c][e];
+      red[(warp * 3 + 1) * H + col + e] = acc_b[c][e];
+      red[(warp * 3 + 2) * H + col + e] = acc_d[c][e];
+    }
+  }
+  __syncthreads();
+  float* out = a.partial + (size_t)blockIdx.x * 3 * H;
+  for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) {
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w * 3 * H + i];
+    out[i] = s;
+  }
+}
+
+// sum over blocks of partial[nblk][W] -> out segments (fixed order)
+__global__ void reduce_partials_kernel(const float* __restrict__ partial, int nblk, int W,
+                                       int seg, float* o0, float* o1, float* o2) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= W) return;
+  float s = 0.f;
+  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * W + i];
+  const int k = i / seg, j = i % seg;
+  float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
+  if (o != nullptr) o[j] = s;
+}
+
+// =====================================================================
+// column sums of a bf16 matrix [rows][N] (ld) with optional 2-way grouping
+// partial[blockIdx.y][G][N]
+// =====================================================================
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restrict__ x, int rows,
+                                                             int N, int64_t ld,
+                                                             const int32_t* __restrict__ grp,
+                                                             int G, float* __restrict__ partial) {
+  __shared__ float red[8][2][256];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int col = (blockIdx.x * 32 + tx) * 8;
+  float acc[2][8] = {};
+  if (col < N) {
+    for (int r = blockIdx.y * 8 + ty; r < rows; r += gridDim.y * 8) {
+      float v[8];
+      load8(x + (int64_t)r * ld + col, v);
+      const int g = grp != nullptr ? grp[r] : 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        acc[0][e] += g == 0 ? v[e] : 0.f;
+        acc[1][e] += g == 1 ? v[e] : 0.f;
+      }
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < 2; ++g)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[ty][g][tx * 8 + e] = acc[g][e];
+  __syncthreads();
+  for (int i = threadIdx.x; i < G * 256; i += 256) {
+    const int g = i / 256, c = i % 256;
+    const int gc = blockIdx.x * 256 + c;
+    if (gc >= N) continue;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) s += red[w][g][c];
+    partial[((size_t)blockIdx.y * G + g) * N + gc] = s;
+  }
+}
+
+// =====================================================================
+// scaled softmax + dropout over rows of S (row pitch ld, ld % 8 == 0)
+// =====================================================================
+template <int MAXV>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict__ s_in,
+                                                          bf16* __restrict__ p_out,
+                                                          bf16* __restrict__ pd_out, int64_t rows,
+                                                          int S, int ld, DropoutCfg drop) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const bf16* in = s_in + row * ld;
+  float v[MAXV][8];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < MAXV; ++c) {
+    const int j0 = 8 * (lane + 32 * c);
+    if (j0 < S) {
+      load8(in + j0, v[c]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (j0 + e >= S) v[c][e] = -INFINITY;
+        mx = fmaxf(mx, v[c][e]);
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[c][e] = -INFINITY;
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < MAXV; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[c][e] = __expf(v[c][e] - mx);
+      sum += v[c][e];
+    }
+  const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+  for (int c = 0; c < MAXV; ++c) {
+    const int j0 = 8 * (lane + 32 * c);
+    if (j0 >= ld) continue;
+    float p[8], pd[8];
+    const uint32_t m = dropout_mask8(drop, (uint64_t)row * ld + j0);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      p[e] = bf16r(v[c][e] * inv);
+      pd[e] = ((m >> e) & 1u) ? p[e] * drop.scale : 0.f;
+    }
+    store8(p_out + row * ld + j0, p);
+    if (pd_out != nullptr) store8(pd_out + row * ld + j0, pd);
+  }
+}
+
+// dS = P * (dP - sum_j dP_j P_j) * scale,  dP = dPd * mask * (1/(1-p)); in place over dPd
+template <int MAXV>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(const bf16* __restrict__ P,
+                                                          bf16* __restrict__ dpd, int64_t rows,
+                                                          int S, int ld, DropoutCfg drop,
+                                                          float scale) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float p[MAXV][8], dp[MAXV][8];
+  float dot = 0.f;
+#pragma unroll
+  for (int c = 0; c < MAXV; ++c) {
+    const int j0 = 8 * (lane + 32 * c);
+    if (j0 < S) {
+      load8(P + row * ld + j0, p[c]);
+      load8(dpd + row * ld + j0, dp[c]);
+      const uint32_t m = dropout_mask8(drop, (uint64_t)row * ld + j0);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        dp[c][e] = ((m >> e) & 1u) ? dp[c][e] * drop.scale : 0.f;
+        if (j0 + e >= S) p[c][e] = 0.f;
+        dot += dp[c][e] * p[c][e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p[c][e] = dp[c][e] = 0.f;
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int c = 0; c < MAXV; ++c) {
+    const int j0 = 8 * (lane + 32 * c);
+    if (j0 >= ld) continue;
+    float ds[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) ds[e] = p[c][e] * (dp[c][e] - dot) * scale;
+    store8(dpd + row * ld + j0, ds);
+  }
+}
+
+// =====================================================================
+// embedding gradients
+// =====================================================================
+// one warp per distinct token id: rows of `de` listed (ascending position)
+// in perm[seg[u] .. seg[u+1]) are summed in order -> dword[id[u]]
+__global__ void __launch_bounds__(256) embed_word_grad_kernel(const bf16* __restrict__ de, int H,
+                                                              const int32_t* __restrict__ perm,
+                                                              const int32_t* __restrict__ seg,
+                                                              const int32_t* __restrict__ uid,
+                                                              int n_unique,
+                                                              float* __restrict__ dword) {
+  const int lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (u >= n_unique) return;
+  const int b = seg[u], e = seg[u + 1];
+  float* out = dword + (int64_t)uid[u] * H;
+  for (int c0 = lane * 8; c0 < H; c0 += 256) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int k = b; k < e; ++k) {
+      float v[8];
+      load8(de + (int64_t)perm[k] * H + c0, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+    float4* o4 = reinterpret_cast<float4*>(out + c0);
+    o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// dpos[s] = sum_b de[b*S + s]
+__global__ void embed_pos_grad_kernel(const bf16* __restrict__ de, int B, int S, int H,
+                                      float* __restrict__ dpos) {
+  const int s = blockIdx.x;
+  for (int c0 = threadIdx.x * 8; c0 < H; c0 += blockDim.x * 8) {
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < B; ++b) {
+      float v[8];
+      load8(de + ((int64_t)b * S + s) * H + c0, v);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] += v[i];
+    }
+    float4* o4 = reinterpret_cast<float4*>(dpos + (int64_t)s * H + c0);
+    o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+}
+
+// =====================================================================
+// multiple-choice head: pooled = tanh(pre); logits = dropout(pooled).wc + bc;
+// loss = mean_q CE(softmax over C choices); writes dpre (bf16), dwc, dbc
+// Single CTA (B <= a few hundred rows).
+// =====================================================================
+__global__ void __launch_bounds__(1024) mc_head_kernel(const bf16* __restrict__ pre, int B, int H,
+                                                       int C, const float* __restrict__ wc,
+                                                       const float* __restrict__ bc,
+                                                       const int32_t* __restrict__ labels,
+                                                       DropoutCfg drop, float* __restrict__ loss,
+                                                       float* __restrict__ logits_out,
+                                                       bf16* __restrict__ dpre,
+                                                       float* __restrict__ dwc,
+                                                       float* __restrict__ dbc) {
+  extern __shared__ float sh[];  // logits[B], dlogit[B]
+  float* lg = sh;
+  float* dl = sh + B;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  // logits: one warp per row
+  for (int b = warp; b < B; b += nw) {
+    float s = 0.f;
+    for (int c = lane; c < H; c += 32) {
+      const uint64_t idx = (uint64_t)b * H + c;
+      const Philox ph(drop.seed, drop.stream, idx >> 2);
+      const bool keep = drop.threshold == 0 || ph.r[idx & 3] >= drop.threshold;
+      const float t = tanhf(__bfloat162float(pre[idx]));
+      s += keep ? t * drop.scale * wc[c] : 0.f;
+    }
+    s = warp_sum(s);
+    if (lane == 0) lg[b] = s + bc[0];
+  }
+  __syncthreads();
+  const int Q = B / C;
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int q = 0; q < Q; ++q) {
+      float mx = -INFINITY;
+      for (int c = 0; c < C; ++c) mx = fmaxf(mx, lg[q * C + c]);
+      float se = 0.f;
+      for (int c = 0; c < C; ++c) se += expf(lg[q * C + c] - mx);
+      const float lse = mx + logf(se);
+      tot += lse - lg[q * C + labels[q]];
+      for (int c = 0; c < C; ++c) {
+        const float pr = expf(lg[q * C + c] - lse);
+        dl[q * C + c] = (pr - (c == labels[q] ? 1.f : 0.f)) / (float)Q;
+      }
+    }
+    loss[0] = tot / (float)Q;
+    float db = 0.f;
+    for (int b = 0; b < B; ++b) db += dl[b];
+    dbc[0] = db;
+  }
+  __syncthreads();
+  if (logits_out != nullptr)
+    for (int b = threadIdx.x; b < B; b += blockDim.x) logits_out[b] = lg[b];
+  // dwc[c] = sum_b dl[b] * td[b,c] ; dpre = dl[b]*wc[c]*mask*scale*(1 - t^2)
+  for (int c = threadIdx.x; c < H; c += blockDim.x) {
+    float acc = 0.f;
+    for (int b = 0; b < B; ++b) {
+      const uint64_t idx = (uint64_t)b * H + c;
+      const Philox ph(drop.seed, drop.stream, idx >> 2);
+      const bool keep = drop.threshold == 0 || ph.r[idx & 3] >= drop.threshold;
+      const float t = tanhf(__bfloat162float(pre[idx]));
+      acc += keep ? dl[b] * t * drop.scale : 0.f;
+      const float dt = keep ? dl[b] * wc[c] * drop.scale : 0.f;
+      dpre[idx] = __float2bfloat16_rn(dt * (1.f - t * t));
+    }
+    dwc[c] = acc;
+  }
+}
+
+// =====================================================================
+// optimizer: global grad-norm (two-stage) + fused AdamW
+// =====================================================================
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const float* __restrict__ g, int64_t n,
+                                                            float* __restrict__ partial) {
+  __shared__ float red[8];
+  float s = 0.f;
+  const int64_t n4 = n / 4;
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = g4[i];
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  if (blockIdx.x == 0)
+    for (int64_t i = n4 * 4 + threadIdx.x; i < n; i += blockDim.x) s += g[i] * g[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    partial[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_partials_kernel(const float* __restrict__ partial, int n, float* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += partial[i];
+    out[0] = (float)s;
+  }
+}
+
+__global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float* __restrict__ m,
+                                                    float* __restrict__ v,
+                                                    const float* __restrict__ g,
+                                                    bf16* __restrict__ p16, int64_t n,
+                                                    int64_t n_decay, const float* __restrict__ norm2,
+                                                    mimose_ops::AdamWArgs a) {
+  float clip = 1.f;
+  if (a.max_grad_norm > 0.f) {
+    const float nrm = sqrtf(norm2[0]);
+    clip = fminf(1.f, a.max_grad_norm / (nrm * a.grad_scale + 1e-6f));
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i] * clip * a.grad_scale;
+    float pi = p[i];
+    if (i < n_decay) pi -= a.lr * a.weight_decay * pi;
+    const float mi = a.beta1 * m[i] + (1.f - a.beta1) * gi;
+    const float vi = a.beta2 * v[i] + (1.f - a.beta2) * gi * gi;
+    m[i] = mi;
+    v[i] = vi;
+    const float mh = mi / a.bc1, vh = vi / a.bc2;
+    pi -= a.lr * mh / (sqrtf(vh) + a.eps);
+    p[i] = pi;
+    p16[i] = __float2bfloat16_rn(pi);
+  }
+}
+
+// deterministic N(mean, std) init: Box-Muller over Philox(seed, stream, i/2)
+__global__ void init_normal_kernel(float* __restrict__ p, int64_t n, float mean, float std,
+                                   uint64_t seed, uint64_t stream) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Philox ph(seed, stream, (uint64_t)i >> 1);
+    const int k = (int)(i & 1) * 2;
+    const float u1 = ((float)(ph.r[k] >> 8) + 1.f) * (1.f / 16777216.f);  // (0, 1]
+    const float u2 = (float)(ph.r[k + 1] >> 8) * (1.f / 16777216.f);
+    p[i] = mean + std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+  }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restrict__ out,
+                                   int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __float2bfloat16_rn(in[i]);
+}
+
+}  // namespace mimose_dev
+
+// =====================================================================
+// host launchers
+// =====================================================================
+namespace mimose_ops {
+
+using mimose_dev::bf16;
+
+namespace {
+int grid_for(int64_t work, int per_block) { return (int)((work + per_block - 1) / per_block); }
+int persistent_blocks() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+}  // namespace
+
+int ln_bwd_blocks(int rows) {
+  const int want = (rows + 7) / 8;
+  const int cap = 2 * persistent_blocks();
+  return want < cap ? want : cap;
+}
+
+cudaError_t add_ln_fwd(const LnFwdArgs& a, int H, cudaStream_t s) {
+  const int g = grid_for(a.rows, 8);
+  switch (H) {
+    case 256: mimose_dev::add_ln_fwd_kernel<1><<<g, 256, 0, s>>>(a); break;
+    case 512: mimose_dev::add_ln_fwd_kernel<2><<<g, 256, 0, s>>>(a); break;
+    case 768: mimose_dev::add_ln_fwd_kernel<3><<<g, 256, 0, s>>>(a); break;
+    case 1024: mimose_dev::add_ln_fwd_kernel<4><<<g, 256, 0, s>>>(a); break;
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t embed_ln_fwd(const LnFwdArgs& a, int H, const int32_t* tok, const int32_t* tt,
+                         const void* word, const void* pos, const void* type, int S,
+                         cudaStream_t s) {
+  const int g = grid_for(a.rows, 8);
+  auto w = static_cast<const bf16*>(word);
+  auto p = static_cast<const bf16*>(pos);
+  auto t = static_cast<const bf16*>(type);
+  switch (H) {
+    case 256: mimose_dev::embed_ln_fwd_kernel<1><<<g, 256, 0, s>>>(a, tok, tt, w, p, t, S); break;
+    case 512: mimose_dev::embed_ln_fwd_kernel<2><<<g, 256, 0, s>>>(a, tok, tt, w, p, t, S); break;
+    case 768: mimose_dev::embed_ln_fwd_kernel<3><<<g, 256, 0, s>>>(a, tok, tt, w, p, t, S); break;
+    case 1024: mimose_dev::embed_ln_fwd_kernel<4><<<g, 256, 0, s>>>(a, tok, tt, w, p, t, S); break;
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  return cudaGetLastError();
+}
+
+template <int VPL>
+static cudaError_t ln_bwd_t(const LnBwdArgs& a, int nblk, cudaStream_t s) {
+  constexpr int H = VPL * 256;
+  const int smem = 8 * 3 * H * (int)sizeof(float);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(mimose_dev::ln_bwd_kernel<VPL>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  mimose_dev::ln_bwd_kernel<VPL><<<nblk, 256, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float* dbias,
+                   cudaStream_t s) {
+  const int nblk = ln_bwd_blocks(a.rows);
+  cudaError_t e;
+  switch (H) {
+    case 256: e = ln_bwd_t<1>(a, nblk, s); break;
+    case 512: e = ln_bwd_t<2>(a, nblk, s); break;
+    case 768: e = ln_bwd_t<3>(a, nblk, s); break;
+    case 1024: e = ln_bwd_t<4>(a, nblk, s); break;
+    default: return cudaErrorInvalidValue;
+  }
+  count_launch();
+  if (e != cudaSuccess) return e;
+  mimose_dev::reduce_partials_kernel<<<grid_for(3 * H, 256), 256, 0, s>>>(a.partial, nblk, 3 * H,
+                                                                         H, dgamma, dbeta, dbias);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int colsum_row_blocks(int rows) {
+  const int want = (rows + 63) / 64;
+  return want < 64 ? (want < 1 ? 1 : want) : 64;
+}
+
+cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,
+                   float* partial, float* out, cudaStream_t s) {
+  if (N % 8 || ld % 8 || G < 1 || G > 2) return cudaErrorInvalidValue;
+  const int rb = colsum_row_blocks(rows);
+  dim3 grid((N + 255) / 256, rb);
+  mimose_dev::colsum_partial_kernel<<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N, ld,
+                                                         groups, G, partial);
+  count_launch();
+  mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, 256), 256, 0, s>>>(
+      partial, rb, G * N, G * N, out, nullptr, nullptr);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
+                        const mimose_dev::DropoutCfg& d, cudaStream_t s) {
+  const int g = (int)((rows + 7) / 8);
+  auto in = static_cast<const bf16*>(scores);
+  auto p = static_cast<bf16*>(P);
+  auto pd = static_cast<bf16*>(Pd);
+  if (ld <= 256) mimose_dev::softmax_fwd_kernel<1><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  else if (ld <= 512) mimose_dev::softmax_fwd_kernel<2><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  else if (ld <= 1024) mimose_dev::softmax_fwd_kernel<4><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  else if (ld <= 2048) mimose_dev::softmax_fwd_kernel<8><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  else return cudaErrorInvalidValue;
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
+                        const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
+  const int g = (int)((rows + 7) / 8);
+  auto p = static_cast<const bf16*>(P);
+  auto dp = static_cast<bf16*>(dPd);
+  if (ld <= 256) mimose_dev::softmax_bwd_kernel<1><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  else if (ld <= 512) mimose_dev::softmax_bwd_kernel<2><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  else if (ld <= 1024) mimose_dev::softmax_bwd_kernel<4><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  else if (ld <= 2048) mimose_dev::softmax_bwd_kernel<8><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  else return cudaErrorInvalidValue;
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
+                            const int32_t* uid, int n_unique, float* dword, cudaStream_t s) {
+  if (n_unique == 0) return cudaSuccess;
+  mimose_dev::embed_word_grad_kernel<<<grid_for(n_unique, 8), 256, 0, s>>>(
+      static_cast<const bf16*>(de), H, perm, seg, uid, n_unique, dword);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t embed_pos_grad(const void* de, int B, int S, int H, float* dpos, cudaStream_t s) {
+  mimose_dev::embed_pos_grad_kernel<<<S, 128, 0, s>>>(static_cast<const bf16*>(de), B, S, H, dpos);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t mc_head(const void* pre, int B, int H, int C, const float* wc, const float* bc,
+                    const int32_t* labels, const mimose_dev::DropoutCfg& d, float* loss,
+                    float* logits, void* dpre, float* dwc, float* dbc, cudaStream_t s) {
+  if (B % C) return cudaErrorInvalidValue;
+  mimose_dev::mc_head_kernel<<<1, 1024, 2 * B * sizeof(float), s>>>(
+      static_cast<const bf16*>(pre), B, H, C, wc, bc, labels, d, loss, logits,
+      static_cast<bf16*>(dpre), dwc, dbc);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int sumsq_blocks() { return 2 * persistent_blocks(); }
+
+cudaError_t grad_norm2(const float* g, int64_t n, float* partial, float* out, cudaStream_t s) {
+  const int nb = sumsq_blocks();
+  mimose_dev::sumsq_partial_kernel<<<nb, 256, 0, s>>>(g, n, partial);
+  count_launch();
+  mimose_dev::sum_partials_kernel<<<1, 32, 0, s>>>(partial, nb, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t adamw(float* p, float* m, float* v, const float* g, void* p16, int64_t n,
+                  int64_t n_decay, const float* norm2, const AdamWArgs& a, cudaStream_t s) {
+  mimose_dev::adamw_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
+      p, m, v, g, static_cast<bf16*>(p16), n, n_decay, norm2, a);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t init_normal(float* p, int64_t n, float mean, float std, uint64_t seed,
+                        uint64_t stream, cudaStream_t s) {
+  mimose_dev::init_normal_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(p, n, mean, std, seed,
+                                                                         stream);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s) {
+  mimose_dev::f32_to_bf16_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
+      in, static_cast<bf16*>(out), n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace mimose_ops

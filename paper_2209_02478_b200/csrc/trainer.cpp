@@ -1,0 +1,1096 @@
+// Layer executor + Mimose training loop; see trainer.hpp.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+
+#include "ops.hpp"
+#include "ops_mem.hpp"
+#include "trainer.hpp"
+
+namespace mimose_rt {
+
+using bf16raw = uint16_t;  // bf16 storage viewed from host code (pointer arithmetic only)
+using mimose_ops::GemmCall;
+using mimose_ops::MatView;
+
+namespace {
+
+constexpr int64_t kAlignElems = 64;  // 256 B (fp32) / 128 B (bf16) per tensor
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int round8(int v) { return (v + 7) / 8 * 8; }
+
+MatView mat(const void* p, int64_t rows, int64_t cols, int64_t ld) {
+  MatView v;
+  v.ptr = p;
+  v.rows = rows;
+  v.cols = cols;
+  v.ld = ld;
+  return v;
+}
+
+// per-head [B][nh][S][64] view into a row-major [T][row_ld] buffer
+MatView head_view(const void* base, int64_t part_off, int S, int64_t row_ld) {
+  MatView v;
+  v.ptr = static_cast<const bf16raw*>(base) + part_off;
+  v.rows = S;
+  v.cols = 64;
+  v.ld = row_ld;
+  v.bs1 = 64;
+  v.bs2 = (int64_t)S * row_ld;
+  return v;
+}
+
+// [B][nh][S][S] score view with row pitch ld
+MatView sq_view(const void* base, int S, int ld, int nh) {
+  MatView v;
+  v.ptr = base;
+  v.rows = S;
+  v.cols = S;
+  v.ld = ld;
+  v.bs1 = (int64_t)S * ld;
+  v.bs2 = (int64_t)nh * S * ld;
+  return v;
+}
+
+void run_gemm(const GemmCall& c, cudaStream_t s) { ck(mimose_ops::gemm(c, s), "gemm"); }
+
+// Y[T,N] = X[T,K] W[N,K]^T (+bias) ; epilogue variants
+GemmCall linear_call(const void* X, const void* W, int64_t T, int N, int K, void* Y, int epi,
+                     const float* bias) {
+  GemmCall c;
+  c.M = (int)T;
+  c.N = N;
+  c.K = K;
+  c.A = mat(X, T, K, K);
+  c.B = mat(W, N, K, K);
+  c.epi = epi;
+  c.out = Y;
+  c.bias = bias;
+  c.ldo = N;
+  return c;
+}
+
+// dX[T,K] = dY[T,N] W[N,K] (+ aux)
+GemmCall dgrad_call(const void* dY, const void* W, int64_t T, int N, int K, void* dX, int epi,
+                    const void* aux) {
+  GemmCall c;
+  c.M = (int)T;
+  c.N = K;
+  c.K = N;
+  c.A = mat(dY, T, N, N);
+  c.B = mat(W, N, K, K);  // rows = reduction dim -> MN-major
+  c.b_mn = true;
+  c.epi = epi;
+  c.out = dX;
+  c.aux = aux;
+  c.ldo = K;
+  return c;
+}
+
+// dW[N,K] (fp32) = dY[T,N]^T X[T,K]
+GemmCall wgrad_call(const void* dY, const void* X, int64_t T, int N, int K, float* dW) {
+  GemmCall c;
+  c.M = N;
+  c.N = K;
+  c.K = (int)T;
+  c.A = mat(dY, T, N, N);
+  c.a_mn = true;
+  c.B = mat(X, T, K, K);
+  c.b_mn = true;
+  c.epi = mimose_ops::kEpiF32;
+  c.out = dW;
+  c.ldo = K;
+  return c;
+}
+
+uint64_t stream_id(uint64_t step, int layer, int site) {
+  return (step << 20) | (static_cast<uint64_t>(layer & 0xFFFF) << 4) | static_cast<uint64_t>(site);
+}
+
+enum Site { kSiteAttnProbs = 0, kSiteAttnOut = 1, kSiteFfnOut = 2, kSiteEmbed = 3, kSitePool = 4 };
+
+}  // namespace
+
+// ------------------------------------------------------------------ tables
+int build_token_tables(const int32_t* tokens, int64_t T, int V, int32_t* perm, int32_t* seg,
+                       int32_t* uid) {
+  std::vector<int32_t> count(static_cast<size_t>(V) + 1, 0);
+  for (int64_t i = 0; i < T; ++i) {
+    const int32_t t = tokens[i];
+    if (t < 0 || t >= V) throw std::runtime_error("token id out of range");
+    count[t + 1] += 1;
+  }
+  for (int v = 0; v < V; ++v) count[v + 1] += count[v];
+  std::vector<int32_t> next(count.begin(), count.end() - 1);
+  for (int64_t i = 0; i < T; ++i) perm[next[tokens[i]]++] = static_cast<int32_t>(i);
+  int nu = 0;
+  for (int v = 0; v < V; ++v) {
+    if (count[v + 1] > count[v]) {
+      seg[nu] = count[v];
+      uid[nu] = v;
+      ++nu;
+    }
+  }
+  seg[nu] = static_cast<int32_t>(T);
+  return nu;
+}
+
+// ------------------------------------------------------------------ setup
+void* Trainer::take(int64_t bytes, int tag) {
+  void* p = ctx_->arena.alloc(bytes, tag);
+  if (p == nullptr) {
+    const auto& st = ctx_->arena.stats();
+    throw std::runtime_error("budget exceeded: request " + std::to_string(bytes) + " B with " +
+                             std::to_string(st.reserved) + " B live of " +
+                             std::to_string(st.budget) + " B (largest free " +
+                             std::to_string(st.largest_free) + " B)");
+  }
+  return p;
+}
+
+void Trainer::drop(void*& p) {
+  if (p != nullptr) {
+    if (!ctx_->arena.free(p)) throw std::runtime_error("arena free of unknown pointer");
+    p = nullptr;
+  }
+}
+
+Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_cfg& t)
+    : ctx_(ctx), m_(m), t_(t) {
+  H_ = m.hidden;
+  nh_ = m.heads;
+  F_ = m.ffn;
+  L_ = m.layers;
+  if (H_ % 256 || H_ > 1024 || H_ / nh_ != 64 || F_ % 64 || L_ < 1 || L_ > 64)
+    throw std::runtime_error("unsupported model shape (need hidden % 256 == 0, <= 1024, head dim 64)");
+  if (m.type_vocab < 1 || m.type_vocab > 2) throw std::runtime_error("type_vocab must be 1 or 2");
+  if (t.batch % m.num_choices) throw std::runtime_error("batch must be a multiple of num_choices");
+  if (t.seq_min < 1 || t.seq_max < t.seq_min || t.seq_max > m.max_pos || round8(t.seq_max) > 2048)
+    throw std::runtime_error("bad sequence range");
+
+  build_params();
+  cudaStream_t s = nullptr;
+  init_params(s);
+
+  // persistent scratch for the deterministic two-stage reductions
+  const int64_t Tmax = (int64_t)t.batch * t.seq_max;
+  const int lnb = mimose_ops::ln_bwd_blocks((int)Tmax);
+  ln_partial_ = static_cast<float*>(take((int64_t)lnb * 3 * H_ * 4, kTagOther));
+  const int64_t widest = std::max<int64_t>(std::max<int64_t>(3 * H_, F_), 2 * H_);
+  col_partial_ =
+      static_cast<float*>(take((int64_t)mimose_ops::colsum_row_blocks((int)Tmax) * widest * 4 + 1024, kTagOther));
+  norm_partial_ = static_cast<float*>(take((int64_t)mimose_ops::sumsq_blocks() * 4, kTagOther));
+  norm2_ = static_cast<float*>(take(4, kTagOther));
+  d_loss_ = static_cast<float*>(take(4, kTagOther));
+  d_logits_ = static_cast<float*>(take((int64_t)t.batch * 4, kTagOther));
+  ck(cudaMallocHost(&h_loss_, sizeof(float)), "cudaMallocHost");
+  stage_elems_ = 5 * Tmax + t.batch + 8;
+  ck(cudaMallocHost(&h_stage_, stage_elems_ * sizeof(int32_t)), "cudaMallocHost");
+  ev_.resize(2 * L_);
+  for (auto& e : ev_) ck(cudaEventCreate(&e), "cudaEventCreate");
+  ck(cudaStreamSynchronize(s), "init sync");
+
+  constant_bytes_ = ctx_->arena.stats().requested;
+  build_spec();
+}
+
+Trainer::~Trainer() {
+  for (auto& e : ev_) cudaEventDestroy(e);
+  if (h_loss_) cudaFreeHost(h_loss_);
+  if (h_stage_) cudaFreeHost(h_stage_);
+  // arena memory is released with the context
+}
+
+ParamRef Trainer::add_param(const std::string& name, int64_t n, bool decay,
+                            std::vector<ParamRef*>& fix) {
+  (void)fix;
+  (void)decay;
+  ParamRef r;
+  r.n = n;
+  r.off = nparam_;
+  nparam_ += (n + kAlignElems - 1) / kAlignElems * kAlignElems;
+  param_names_.push_back(name);
+  param_refs_.push_back(r);
+  return r;
+}
+
+void Trainer::build_params() {
+  std::vector<ParamRef*> fix;
+  const int64_t H = H_, F = F_;
+  lp_.resize(L_);
+  // decayed tensors first (matrices + embeddings), then biases / LayerNorm
+  word_ = add_param("embeddings.word", (int64_t)m_.vocab * H, true, fix);
+  pos_ = add_param("embeddings.position", (int64_t)m_.max_pos * H, true, fix);
+  type_ = add_param("embeddings.token_type", (int64_t)m_.type_vocab * H, true, fix);
+  for (int l = 0; l < L_; ++l) {
+    const std::string p = "layer." + std::to_string(l) + ".";
+    lp_[l].wqkv = add_param(p + "attn.qkv.weight", 3 * H * H, true, fix);
+    lp_[l].wo = add_param(p + "attn.out.weight", H * H, true, fix);
+    lp_[l].w1 = add_param(p + "ffn.in.weight", F * H, true, fix);
+    lp_[l].w2 = add_param(p + "ffn.out.weight", H * F, true, fix);
+  }
+  wp_ = add_param("pooler.weight", H * H, true, fix);
+  wc_ = add_param("classifier.weight", H, true, fix);
+  n_decay_ = nparam_;
+  eln_g_ = add_param("embeddings.ln.weight", H, false, fix);
+  eln_b_ = add_param("embeddings.ln.bias", H, false, fix);
+  for (int l = 0; l < L_; ++l) {
+    const std::string p = "layer." + std::to_string(l) + ".";
+    lp_[l].bqkv = add_param(p + "attn.qkv.bias", 3 * H, false, fix);
+    lp_[l].bo = add_param(p + "attn.out.bias", H, false, fix);
+    lp_[l].ln1_g = add_param(p + "attn.ln.weight", H, false, fix);
+    lp_[l].ln1_b = add_param(p + "attn.ln.bias", H, false, fix);
+    lp_[l].b1 = add_param(p + "ffn.in.bias", F, false, fix);
+    lp_[l].b2 = add_param(p + "ffn.out.bias", H, false, fix);
+    lp_[l].ln2_g = add_param(p + "ffn.ln.weight", H, false, fix);
+    lp_[l].ln2_b = add_param(p + "ffn.ln.bias", H, false, fix);
+  }
+  bp_ = add_param("pooler.bias", H, false, fix);
+  bc_ = add_param("classifier.bias", 1, false, fix);
+
+  p32_ = static_cast<float*>(take(nparam_ * 4, kTagParam));
+  p16_ = take(nparam_ * 2, kTagParam);
+  g32_ = static_cast<float*>(take(nparam_ * 4, kTagGrad));
+  am_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
+  av_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
+}
+
+void Trainer::init_params(cudaStream_t s) {
+  ck(cudaMemsetAsync(p32_, 0, nparam_ * 4, s), "memset");
+  ck(cudaMemsetAsync(g32_, 0, nparam_ * 4, s), "memset");
+  ck(cudaMemsetAsync(am_, 0, nparam_ * 4, s), "memset");
+  ck(cudaMemsetAsync(av_, 0, nparam_ * 4, s), "memset");
+  uint64_t k = 0;
+  auto normal = [&](const ParamRef& r) {
+    ck(mimose_ops::init_normal(p32_ + r.off, r.n, 0.f, m_.init_std, m_.seed, 0xA000 + (k++), s),
+       "init_normal");
+  };
+  auto ones = [&](const ParamRef& r) {
+    std::vector<float> v(static_cast<size_t>(r.n), 1.f);
+    ck(cudaMemcpy(p32_ + r.off, v.data(), r.n * 4, cudaMemcpyHostToDevice), "memcpy");
+  };
+  normal(word_);
+  normal(pos_);
+  normal(type_);
+  for (auto& l : lp_) {
+    normal(l.wqkv);
+    normal(l.wo);
+    normal(l.w1);
+    normal(l.w2);
+    ones(l.ln1_g);
+    ones(l.ln2_g);
+  }
+  normal(wp_);
+  normal(wc_);
+  ones(eln_g_);
+  ck(mimose_ops::f32_to_bf16(p32_, p16_, nparam_, s), "f32_to_bf16");
+}
+
+int64_t Trainer::extras_bytes(int S) const {
+  // bytes outside the planner-managed blocks that can be live at once:
+  // inputs + token tables, embedding saves (z0, stats, h0), head tensors,
+  // the output boundaries of every block (the scheduler's excess does not
+  // count a dropped block's retained output), and one block's backward
+  // workspace (mirrors the allocation order of layer_bwd).
+  const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
+  const int64_t ld = round8(S);
+  const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
+  const int64_t act = 2 * T * H;
+  const int64_t inputs = 4 * (5 * T + B + 8);
+  const int64_t embed = 2 * act + 8 * T;
+  const int64_t head = 2 * (2 * B * H) + act;
+  const int64_t bounds = (int64_t)L_ * act;
+  // backward live set, worst stage: dy, dz2, df/du, dh1 ... dctx, dPd, dqkv, dz1
+  const int64_t s1 = act * 3 + 2 * T * F;                   // dy, dz2, df, du
+  const int64_t s2 = act * 4 + quad + 2 * T * 3 * H;        // dz1, da, dctx, dx, dPd, dqkv
+  const int64_t work = std::max(s1, s2);
+  return inputs + embed + head + bounds + work;
+}
+
+void Trainer::build_spec() {
+  const int64_t H = H_, F = F_;
+  const double B = t_.batch;
+  spec_ = mimose::ModelSpec{};
+  spec_.constant_footprint = constant_bytes_;
+  spec_.input_min = (int64_t)t_.batch * t_.seq_min;
+  spec_.input_max = (int64_t)t_.batch * t_.seq_max;
+  const double p_quad = (m_.attn_dropout > 0.f ? 2.0 : 1.0) * nh_ * 2.0 / B;
+  for (int l = 0; l < L_; ++l) {
+    mimose::LayerSpec ls;
+    ls.id = l;
+    ls.position = l;
+    ls.stage_id = l;
+    ls.category = mimose::LayerCategory::QuadraticStructure;
+    // prior a(x): saved tensors per token + materialised probabilities
+    ls.activation_coeffs = {0.0, static_cast<double>(16 * H + 4 * F + 16), p_quad};
+    ls.boundary_coeffs = {0.0, static_cast<double>(2 * H)};
+    ls.forward_time_coeffs = {0.01, 1e-6};
+    spec_.layers.push_back(ls);
+  }
+  mimose::validate_model(spec_);
+
+  sched_ = mimose::SchedulerConfig{};
+  sched_.budget_bytes = ctx_->arena.stats().budget;
+  const int64_t margin = sched_.budget_bytes / 50;  // 2% fragmentation margin
+  sched_.reserve_bytes = t_.reserve_bytes >= 0 ? t_.reserve_bytes : extras_bytes(t_.seq_max) + margin;
+  if (sched_.reserve_bytes >= sched_.budget_bytes) sched_.reserve_bytes = sched_.budget_bytes - 1;
+  sched_.bucket_tolerance = t_.bucket_tolerance;
+  sched_.cache_tolerance = t_.cache_tolerance;
+  sched_.excess_includes_constant = true;
+  ccfg_.max_sheltered_iters = t_.max_sheltered_iters;
+  ccfg_.collect_new_sizes_always = t_.collect_new_sizes_always != 0;
+}
+
+void Trainer::param_info(int i, const char** name, int64_t* off, int64_t* n) const {
+  if (i < 0 || i >= param_count()) throw std::runtime_error("param index out of range");
+  *name = param_names_[i].c_str();
+  *off = param_refs_[i].off;
+  *n = param_refs_[i].n;
+}
+
+void Trainer::set_forced_plan(const int* ids, int n, int active) {
+  forced_active_ = active != 0;
+  forced_.assign(ids, ids + (ids ? n : 0));
+}
+
+// ------------------------------------------------------------ layer forward
+void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
+                        cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_, F = F_;
+  const int S = g.S, ld = g.ld, nh = nh_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  const bool keep = save != nullptr;
+  const int act_tag = keep ? kTagAct : kTagTransient;
+  const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
+
+  // QKV projection
+  void* qkv = take(T * 3 * H * 2, act_tag);
+  run_gemm(linear_call(h, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
+                   p32_ + P.bqkv.off),
+       s);
+  // scores = q k^T / sqrt(64), batched over (head, sequence)
+  void* sc = take(quad, kTagTransient);
+  {
+    GemmCall c;
+    c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
+    c.A = head_view(qkv, 0, S, 3 * H);
+    c.B = head_view(qkv, H, S, 3 * H);
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = sc; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
+    c.alpha = 0.125f;
+    run_gemm(c, s);
+  }
+  void* Pm = take(quad, act_tag);
+  void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
+  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+  ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s), "softmax_fwd");
+  drop(sc);
+  // ctx = Pd V, written head-interleaved into [T, H]
+  void* ctx = take(T * H * 2, act_tag);
+  {
+    GemmCall c;
+    c.M = S; c.N = 64; c.K = S; c.nb1 = nh; c.nb2 = g.B;
+    c.A = sq_view(Pd ? Pd : Pm, S, ld, nh);
+    c.B = head_view(qkv, 2 * H, S, 3 * H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = ctx; c.ldo = H; c.obs1 = 64; c.obs2 = (int64_t)S * H;
+    run_gemm(c, s);
+  }
+  if (!keep) {
+    drop(qkv);
+    drop(Pm);
+    drop(Pd);
+  }
+  // attention output projection + residual + LN1
+  void* a = take(T * H * 2, kTagTransient);
+  run_gemm(linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, a, mimose_ops::kEpiBf16, p32_ + P.bo.off), s);
+  if (!keep) drop(ctx);
+  void* z1 = keep ? take(T * H * 2, act_tag) : nullptr;
+  void* st1 = keep ? take(T * 8, act_tag) : nullptr;
+  void* h1 = take(T * H * 2, act_tag);
+  {
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.res = h; la.br = a;
+    la.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
+    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
+    la.z = z1; la.stats = st1; la.y = h1;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+  }
+  drop(a);
+  // FFN
+  void* u = take(T * F * 2, act_tag);
+  void* gg = take(T * F * 2, act_tag);
+  {
+    GemmCall c = linear_call(h1, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
+                             p32_ + P.b1.off);
+    c.out2 = gg;
+    run_gemm(c, s);
+  }
+  if (!keep) drop(u);
+  void* f = take(T * H * 2, kTagTransient);
+  run_gemm(linear_call(gg, W + P.w2.off, T, (int)H, (int)F, f, mimose_ops::kEpiBf16, p32_ + P.b2.off), s);
+  if (!keep) drop(gg);
+  void* z2 = keep ? take(T * H * 2, act_tag) : nullptr;
+  void* st2 = keep ? take(T * 8, act_tag) : nullptr;
+  {
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.res = h1; la.br = f;
+    la.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
+    la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
+    la.z = z2; la.stats = st2; la.y = y;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+  }
+  drop(f);
+  if (!keep) {
+    drop(h1);
+    return;
+  }
+  save->qkv = qkv; save->P = Pm; save->Pd = Pd; save->ctx = ctx;
+  save->z1 = z1; save->st1 = st1; save->h1 = h1;
+  save->u = u; save->g = gg; save->z2 = z2; save->st2 = st2;
+}
+
+void Trainer::free_save(LayerSave& sv) {
+  drop(sv.qkv); drop(sv.P); drop(sv.Pd); drop(sv.ctx); drop(sv.z1); drop(sv.st1); drop(sv.h1);
+  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2);
+}
+
+// ----------------------------------------------------------- layer backward
+// Consumes dy (freed) and the saved set (freed); returns dx (grad of h).
+void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
+                         cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_, F = F_;
+  const int S = g.S, ld = g.ld, nh = nh_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  float* G = g32_;
+  const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
+  const bool hid_drop = m_.hidden_dropout > 0.f;
+
+  // LN2 backward (+ FFN-output dropout backward, db2)
+  void* dz2 = take(T * H * 2, kTagTransient);
+  void* df = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+  {
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dy; a.z = sv.z2; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
+    a.dz = dz2; a.dbr = df;
+    a.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.b2.off, s), "ln_bwd");
+  }
+  drop(dy);
+  drop(sv.z2); drop(sv.st2);
+  void* dfp = df ? df : dz2;
+  // FFN2: dW2 = df^T g ; du = (df W2) * gelu'(u)
+  run_gemm(wgrad_call(dfp, sv.g, T, (int)H, (int)F, G + P.w2.off), s);
+  drop(sv.g);
+  void* du = take(T * F * 2, kTagTransient);
+  run_gemm(dgrad_call(dfp, W + P.w2.off, T, (int)H, (int)F, du, mimose_ops::kEpiDGelu, sv.u), s);
+  drop(df);
+  drop(sv.u);
+  ck(mimose_ops::colsum(du, (int)T, (int)F, F, nullptr, 1, col_partial_, G + P.b1.off, s), "colsum");
+  // FFN1: dW1 = du^T h1 ; dh1 = du W1 + dz2 (residual)
+  run_gemm(wgrad_call(du, sv.h1, T, (int)F, (int)H, G + P.w1.off), s);
+  drop(sv.h1);
+  void* dh1 = take(T * H * 2, kTagTransient);
+  run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dh1, mimose_ops::kEpiBf16, dz2), s);
+  drop(du);
+  drop(dz2);
+  // LN1 backward (+ attention-output dropout backward, dbo)
+  void* dz1 = take(T * H * 2, kTagTransient);
+  void* da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+  {
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dh1; a.z = sv.z1; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
+    a.dz = dz1; a.dbr = da;
+    a.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, G + P.bo.off, s), "ln_bwd");
+  }
+  drop(dh1);
+  drop(sv.z1); drop(sv.st1);
+  void* dap = da ? da : dz1;
+  // output projection: dWo = da^T ctx ; dctx = da Wo
+  run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
+  drop(sv.ctx);
+  void* dctx = take(T * H * 2, kTagTransient);
+  run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
+  drop(da);
+  // attention: dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
+  void* dP = take(quad, kTagTransient);
+  {
+    GemmCall c;
+    c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
+    c.A = head_view(dctx, 0, S, H);
+    c.B = head_view(sv.qkv, 2 * H, S, 3 * H);
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = dP; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
+    run_gemm(c, s);
+  }
+  void* dqkv = take(T * 3 * H * 2, kTagTransient);
+  {
+    GemmCall c;
+    c.M = S; c.N = 64; c.K = S; c.nb1 = nh; c.nb2 = g.B;
+    c.A = sq_view(sv.Pd ? sv.Pd : sv.P, S, ld, nh);
+    c.a_mn = true;
+    c.B = head_view(dctx, 0, S, H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = static_cast<bf16raw*>(dqkv) + 2 * H;
+    c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
+    run_gemm(c, s);
+  }
+  drop(dctx);
+  drop(sv.Pd);
+  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+  ck(mimose_ops::softmax_bwd(sv.P, dP, (int64_t)g.B * nh * S, S, ld, pdrop, 0.125f, s), "softmax_bwd");
+  drop(sv.P);
+  {
+    GemmCall c;  // dQ = dS K
+    c.M = S; c.N = 64; c.K = S; c.nb1 = nh; c.nb2 = g.B;
+    c.A = sq_view(dP, S, ld, nh);
+    c.B = head_view(sv.qkv, H, S, 3 * H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = dqkv; c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
+    run_gemm(c, s);
+    // dK = dS^T Q
+    c.A = sq_view(dP, S, ld, nh);
+    c.a_mn = true;
+    c.B = head_view(sv.qkv, 0, S, 3 * H);
+    c.out = static_cast<bf16raw*>(dqkv) + H;
+    run_gemm(c, s);
+  }
+  drop(dP);
+  drop(sv.qkv);
+  // QKV projection: dbqkv, dWqkv = dqkv^T h ; dx = dqkv Wqkv + dz1 (residual)
+  ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
+     "colsum");
+  run_gemm(wgrad_call(dqkv, h, T, 3 * (int)H, (int)H, G + P.wqkv.off), s);
+  void* dx = take(T * H * 2, kTagTransient);
+  run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx, mimose_ops::kEpiBf16, dz1), s);
+  drop(dqkv);
+  drop(dz1);
+  return dx;
+}
+
+// ------------------------------------------------------------ phase machine
+void Trainer::refit(mimose_step_report* rep) {
+  const int order = std::min(t_.estimator_order, cstate_.distinct_sizes() - 1);
+  const auto t0 = std::chrono::steady_clock::now();
+  est_ = mimose::fit(cstate_.samples, order);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (rep) {
+    rep->fit_us += std::chrono::duration<double, std::micro>(t1 - t0).count();
+    rep->fit_order = order;
+  }
+  // the plan cache is kept across refits, as the reference harness does
+  // measured profile -> model document (activation coefficients = the fit
+  // padded to order 2 when possible, forward time = per-layer linear fit)
+  for (auto& ls : spec_.layers) {
+    const auto& c = est_.per_layer_coeffs.at(ls.id);
+    std::array<double, 3> a{0, 0, 0};
+    for (size_t k = 0; k < c.size() && k < 3; ++k) a[k] = c[k];
+    double sx = 0, sy = 0, sxx = 0, sxy = 0;
+    int n = 0;
+    for (const auto& smp : cstate_.samples) {
+      if (smp.layer_id != ls.id) continue;
+      const double x = static_cast<double>(smp.input_size), yv = smp.measured_forward_ms;
+      sx += x; sy += yv; sxx += x * x; sxy += x * yv; ++n;
+    }
+    double t1c = 0.0, t0c = n ? sy / n : 0.01;
+    if (n >= 2 && (n * sxx - sx * sx) > 0) {
+      t1c = (n * sxy - sx * sy) / (n * sxx - sx * sx);
+      t0c = (sy - t1c * sx) / n;
+    }
+    // keep the document valid (validate_model invariants) if the fit is odd
+    mimose::ModelSpec trial = spec_;
+    for (auto& tl : trial.layers)
+      if (tl.id == ls.id) {
+        tl.activation_coeffs = a;
+        tl.forward_time_coeffs = {t0c, t1c};
+      }
+    try {
+      mimose::validate_model(trial);
+      spec_ = trial;
+    } catch (const mimose::Error&) {
+    }
+  }
+}
+
+Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_step_report* rep) {
+  plan = mimose::CheckpointPlan{};
+  plan.source_input_size = x;
+  if (forced_active_) {
+    plan.dropped_layers = forced_;
+    plan.normalize();
+    return Mode::Plain;
+  }
+  switch (t_.planner) {
+    case MIMOSE_PLANNER_NONE:
+      return Mode::Plain;
+    case MIMOSE_PLANNER_ALL:
+      for (int l = 0; l < L_; ++l) plan.dropped_layers.push_back(l);
+      return Mode::Plain;
+    case MIMOSE_PLANNER_STATIC: {
+      // provisioned once for the largest input from the analytic profile
+      static_cast<void>(0);
+      mimose::EstimatorModel ex = mimose::exact_estimator(spec_);
+      plan = mimose::static_max_plan(ex, spec_, spec_.input_max, sched_);
+      return Mode::Plain;
+    }
+    default:
+      break;
+  }
+  const bool unseen = cstate_.seen_sizes.count(x) == 0;
+  if (!trained_) {
+    if (mimose::should_collect(cstate_, x, iter_, ccfg_)) return Mode::Collect;
+    if (iter_ < ccfg_.max_sheltered_iters) return Mode::AllLayers;
+    if (unseen && cstate_.distinct_sizes() < t_.estimator_order + 1) {
+      rep->phase = MIMOSE_PHASE_FALLBACK;
+      return Mode::Collect;
+    }
+    refit(rep);
+    trained_ = true;
+  }
+  if (ccfg_.collect_new_sizes_always && unseen) return Mode::Collect;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, x, sched_);
+  const auto t1 = std::chrono::steady_clock::now();
+  rep->plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
+  if (!hit) {
+    cache_.entries[x].generated_at_iter = iter_;
+    p.generated_at_iter = iter_;
+  }
+  rep->cache_hit = hit ? 1 : 0;
+  rep->predicted_kept = mimose::detail::estimated_kept_bytes(est_, spec_, p, x);
+  plan = p;
+  return Mode::Planned;
+}
+
+// ------------------------------------------------------------------- step
+void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
+                               mimose_step_report* rep) {
+  if (B != t_.batch) throw std::runtime_error("batch differs from the configured batch");
+  if (S < t_.seq_min || S > t_.seq_max) throw std::runtime_error("sequence length outside range");
+  StepGeo g;
+  g.B = B;
+  g.S = S;
+  g.ld = round8(S);
+  g.T = (int64_t)B * S;
+  g.step = static_cast<uint64_t>(iter_);
+  const int64_t x = g.T;
+  const int64_t T = g.T, H = H_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  float* G = g32_;
+
+  mimose_step_report local{};
+  mimose_step_report* r = rep ? rep : &local;
+  std::memset(r, 0, sizeof(*r));
+  r->iter = iter_;
+  r->x = x;
+  r->batch = B;
+  r->seq = S;
+  r->fit_order = -1;
+  r->budget = ctx_->arena.stats().budget;
+  r->phase = MIMOSE_PHASE_PLAIN;
+
+  mimose::CheckpointPlan plan;
+  const Mode mode = decide(x, plan, r);
+  if (mode == Mode::Collect && r->phase != MIMOSE_PHASE_FALLBACK) r->phase = MIMOSE_PHASE_COLLECT;
+  if (mode == Mode::AllLayers) r->phase = MIMOSE_PHASE_SHELTERED;
+  if (mode == Mode::Planned) r->phase = MIMOSE_PHASE_PLANNED;
+  std::vector<char> dropped(L_, 0);
+  if (mode == Mode::Collect || mode == Mode::AllLayers) {
+    std::fill(dropped.begin(), dropped.end(), 1);
+  } else {
+    for (int id : plan.dropped_layers)
+      if (id >= 0 && id < L_) dropped[id] = 1;
+  }
+  for (int l = 0; l < L_; ++l)
+    if (dropped[l]) {
+      r->plan_size += 1;
+      if (l < 64) r->dropped_mask_lo |= (uint64_t)1 << l;
+    }
+  r->insufficient = plan.insufficient_budget ? 1 : 0;
+  if (mode != Mode::Planned)
+    r->predicted_kept = constant_bytes_;  // informational only
+
+  ctx_->arena.reset_peak();
+
+  // ---- embeddings
+  void* z0 = take(T * H * 2, kTagAct);
+  void* st0 = take(T * 8, kTagAct);
+  void* h0 = take(T * H * 2, kTagAct);
+  {
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T;
+    la.gamma = p32_ + eln_g_.off; la.beta = p32_ + eln_b_.off; la.eps = m_.ln_eps;
+    la.z = z0; la.stats = st0; la.y = h0;
+    la.out_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+    ck(mimose_ops::embed_ln_fwd(la, (int)H, in.tokens, in.types, W + word_.off, W + pos_.off,
+                                W + type_.off, S, s),
+       "embed_ln_fwd");
+  }
+
+  // ---- encoder blocks
+  std::vector<void*> out(L_, nullptr);
+  std::vector<LayerSave> saves(L_);
+  std::vector<int64_t> measured(L_, 0);
+  const bool collect = mode == Mode::Collect;
+  for (int l = 0; l < L_; ++l) {
+    const void* hin = l == 0 ? h0 : out[l - 1];
+    if (collect) {
+      // measuring pass: full save set; the arena's requested-bytes delta is
+      // the block's activation footprint a_l(x) (output included), then
+      // everything but the output (the checkpoint boundary) is released.
+      const int64_t before = ctx_->arena.stats().requested;
+      ck(cudaEventRecord(ev_[2 * l], s), "event");
+      out[l] = take(T * H * 2, kTagBoundary);
+      layer_fwd(l, hin, out[l], &saves[l], g, s);
+      ck(cudaEventRecord(ev_[2 * l + 1], s), "event");
+      measured[l] = ctx_->arena.stats().requested - before;
+      free_save(saves[l]);
+    } else if (dropped[l]) {
+      out[l] = take(T * H * 2, kTagBoundary);
+      layer_fwd(l, hin, out[l], nullptr, g, s);
+    } else {
+      out[l] = take(T * H * 2, kTagAct);
+      layer_fwd(l, hin, out[l], &saves[l], g, s);
+    }
+  }
+
+  // ---- multiple-choice head: pooled = tanh(cls Wp^T + bp) -> logits -> CE
+  void* pre = take((int64_t)B * H * 2, kTagTransient);
+  {
+    GemmCall c;
+    c.M = B; c.N = (int)H; c.K = (int)H;
+    c.A = mat(out[L_ - 1], B, H, (int64_t)S * H);  // row 0 of every sequence
+    c.B = mat(W + wp_.off, H, H, H);
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = pre; c.ldo = H; c.bias = p32_ + bp_.off;
+    run_gemm(c, s);
+  }
+  void* dpre = take((int64_t)B * H * 2, kTagTransient);
+  ck(mimose_ops::mc_head(pre, B, (int)H, m_.num_choices, p32_ + wc_.off, p32_ + bc_.off,
+                         in.labels,
+                         mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSitePool)),
+                         d_loss_, d_logits_, dpre, G + wc_.off, G + bc_.off, s),
+     "mc_head");
+  drop(pre);
+  void* dy = take(T * H * 2, kTagTransient);
+  ck(cudaMemsetAsync(dy, 0, T * H * 2, s), "memset");
+  {
+    // dWp = dpre^T cls ; dbp = sum dpre ; dcls = dpre Wp -> rows s=0 of dy
+    GemmCall c;
+    c.M = (int)H; c.N = (int)H; c.K = B;
+    c.A = mat(dpre, B, H, H);
+    c.a_mn = true;
+    c.B = mat(out[L_ - 1], B, H, (int64_t)S * H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiF32;
+    c.out = G + wp_.off; c.ldo = H;
+    run_gemm(c, s);
+    ck(mimose_ops::colsum(dpre, B, (int)H, H, nullptr, 1, col_partial_, G + bp_.off, s), "colsum");
+    GemmCall d = dgrad_call(dpre, W + wp_.off, B, (int)H, (int)H, dy, mimose_ops::kEpiBf16, nullptr);
+    d.ldo = (int64_t)S * H;
+    run_gemm(d, s);
+  }
+  drop(dpre);
+
+  // ---- backward through the blocks (recompute dropped ones first)
+  for (int l = L_ - 1; l >= 0; --l) {
+    const void* hin = l == 0 ? h0 : out[l - 1];
+    if (dropped[l]) layer_fwd(l, hin, out[l], &saves[l], g, s);  // recompute, same streams
+    void* dx = layer_bwd(l, hin, saves[l], dy, g, s);
+    drop(out[l]);
+    dy = dx;
+  }
+
+  // ---- embedding backward
+  ck(cudaMemsetAsync(G + word_.off, 0, word_.n * 4, s), "memset");
+  ck(cudaMemsetAsync(G + pos_.off, 0, pos_.n * 4, s), "memset");
+  void* de = take(T * H * 2, kTagTransient);
+  {
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dy; a.z = z0; a.stats = st0; a.gamma = p32_ + eln_g_.off;
+    a.in_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+    a.dz = de;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + eln_g_.off, G + eln_b_.off, nullptr, s), "ln_bwd");
+  }
+  drop(dy);
+  drop(z0); drop(st0); drop(h0);
+  ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s),
+     "embed_word_grad");
+  ck(mimose_ops::embed_pos_grad(de, B, S, (int)H, G + pos_.off, s), "embed_pos_grad");
+  ck(mimose_ops::colsum(de, (int)T, (int)H, H, m_.type_vocab == 2 ? in.types : nullptr,
+                        m_.type_vocab, col_partial_, G + type_.off, s),
+     "colsum");
+  drop(de);
+
+  const auto& st = ctx_->arena.stats();
+  r->peak_requested = st.peak_requested;
+  r->peak_reserved = st.peak_reserved;
+
+  // ---- commit collector measurements (reference collector.hpp:129-184)
+  if (collect) {
+    ck(cudaEventSynchronize(ev_[2 * L_ - 1]), "event sync");
+    const bool fresh = cstate_.seen_sizes.count(x) == 0;
+    for (int l = 0; l < L_ && fresh; ++l) {
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, ev_[2 * l], ev_[2 * l + 1]), "event elapsed");
+      mimose::CollectedSample smp;
+      smp.layer_id = l;
+      smp.input_size = x;
+      smp.measured_activation_bytes = measured[l];
+      smp.measured_forward_ms = ms;
+      smp.valid = true;  // blocks are flat: no nested checkpoint scopes to filter
+      cstate_.samples.push_back(smp);
+    }
+    cstate_.seen_sizes.insert(x);
+    cstate_.collected_iterations += 1;
+    if (trained_ && ccfg_.collect_new_sizes_always) refit(r);
+  }
+  history_.push_back(*r);
+  iter_ += 1;
+}
+
+void Trainer::optimizer_step(float grad_scale, cudaStream_t s) {
+  adam_t_ += 1;
+  mimose_ops::AdamWArgs a;
+  a.lr = t_.lr;
+  a.beta1 = t_.beta1;
+  a.beta2 = t_.beta2;
+  a.eps = t_.adam_eps;
+  a.weight_decay = t_.weight_decay;
+  a.max_grad_norm = t_.max_grad_norm;
+  a.grad_scale = grad_scale;
+  a.bc1 = 1.f - std::pow(t_.beta1, (float)adam_t_);
+  a.bc2 = 1.f - std::pow(t_.beta2, (float)adam_t_);
+  if (a.max_grad_norm > 0.f) ck(mimose_ops::grad_norm2(g32_, nparam_, norm_partial_, norm2_, s), "grad_norm2");
+  ck(mimose_ops::adamw(p32_, am_, av_, g32_, p16_, nparam_, n_decay_, norm2_, a, s), "adamw");
+}
+
+void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
+                        int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep) {
+  const int64_t T = (int64_t)B * S;
+  const int Q = B / m_.num_choices;
+  if (5 * T + Q + 1 > stage_elems_) throw std::runtime_error("staging buffer too small");
+  int32_t* tk = h_stage_;
+  int32_t* ty = tk + T;
+  int32_t* lb = ty + T;
+  int32_t* pm = lb + Q;
+  int32_t* sg = pm + T;
+  int32_t* ui = sg + T + 1;
+  std::memcpy(tk, tokens, T * 4);
+  if (types) std::memcpy(ty, types, T * 4);
+  else std::memset(ty, 0, T * 4);
+  std::memcpy(lb, labels, Q * 4);
+  for (int64_t i = 0; i < T; ++i)
+    if (ty[i] < 0 || ty[i] >= m_.type_vocab) throw std::runtime_error("token type out of range");
+  for (int q = 0; q < Q; ++q)
+    if (lb[q] < 0 || lb[q] >= m_.num_choices) throw std::runtime_error("label out of range");
+  const int nu = build_token_tables(tk, T, m_.vocab, pm, sg, ui);
+  const int64_t n_in = 2 * T + Q + T + (nu + 1) + nu;
+  int32_t* d = static_cast<int32_t*>(take(n_in * 4 + 64, kTagInput));
+  // contiguous upload (uid packed right after seg)
+  std::memmove(sg + nu + 1, ui, nu * 4);
+  ck(cudaMemcpyAsync(d, h_stage_, n_in * 4, cudaMemcpyHostToDevice, s), "H2D inputs");
+  StepInputs in;
+  in.tokens = d;
+  in.types = d + T;
+  in.labels = d + 2 * T;
+  in.perm = d + 2 * T + Q;
+  in.seg = in.perm + T;
+  in.uid = in.seg + nu + 1;
+  in.n_unique = nu;
+  forward_backward(in, B, S, s, rep);
+  void* dv = d;
+  drop(dv);
+  if (do_optimizer) {
+    if (hook_) hook_(hook_user_, g32_, nparam_, s);
+    optimizer_step(1.f, s);
+  }
+  ck(cudaMemcpyAsync(h_loss_, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H loss");
+  ck(cudaStreamSynchronize(s), "step sync");
+  if (rep) rep->loss = *h_loss_;
+  if (!history_.empty()) history_.back().loss = *h_loss_;
+}
+
+}  // namespace mimose_rt
+
+// =================================================================== C ABI
+using mimose_capi::fail;
+using mimose_rt::Trainer;
+
+struct mimose_trainer {
+  Trainer* impl = nullptr;
+};
+
+namespace {
+template <typename Fn>
+int guarded(const char* what, Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(std::string(what) + ": " + e.what());
+  }
+}
+char* dup_string(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+int mimose_trainer_create(mimose_ctx* ctx, const mimose_model_cfg* m, const mimose_train_cfg* t,
+                          mimose_trainer** out) {
+  if (!ctx || !m || !t || !out) return fail("mimose_trainer_create: null argument");
+  return guarded("mimose_trainer_create", [&] {
+    auto* tr = new mimose_trainer();
+    try {
+      tr->impl = new Trainer(ctx, *m, *t);
+    } catch (...) {
+      delete tr;
+      throw;
+    }
+    *out = tr;
+  });
+}
+
+int mimose_trainer_destroy(mimose_trainer* tr) {
+  if (tr) {
+    delete tr->impl;
+    delete tr;
+  }
+  return 0;
+}
+
+int mimose_trainer_step(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                        const int32_t* labels, int batch, int seq, void* stream,
+                        mimose_step_report* rep) {
+  return guarded("mimose_trainer_step", [&] {
+    tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep);
+  });
+}
+
+int mimose_trainer_forward_backward(mimose_trainer* tr, const int32_t* tokens,
+                                    const int32_t* types, const int32_t* labels, int batch,
+                                    int seq, void* stream, mimose_step_report* rep) {
+  return guarded("mimose_trainer_forward_backward", [&] {
+    tr->impl->step_host(tokens, types, labels, batch, seq, 0, static_cast<cudaStream_t>(stream), rep);
+  });
+}
+
+int mimose_trainer_step_device(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                               const int32_t* labels, const int32_t* perm, const int32_t* seg,
+                               const int32_t* uid, int n_unique, int batch, int seq,
+                               int do_optimizer, void* stream, mimose_step_report* rep) {
+  return guarded("mimose_trainer_step_device", [&] {
+    mimose_rt::StepInputs in;
+    in.tokens = tokens; in.types = types; in.labels = labels;
+    in.perm = perm; in.seg = seg; in.uid = uid; in.n_unique = n_unique;
+    auto s = static_cast<cudaStream_t>(stream);
+    tr->impl->forward_backward(in, batch, seq, s, rep);
+    if (do_optimizer) tr->impl->optimizer_step(1.f, s);
+  });
+}
+
+int mimose_trainer_optimizer_step(mimose_trainer* tr, float grad_scale, void* stream) {
+  return guarded("mimose_trainer_optimizer_step", [&] {
+    tr->impl->optimizer_step(grad_scale, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mimose_trainer_force_plan(mimose_trainer* tr, const int* ids, int n, int active) {
+  return guarded("mimose_trainer_force_plan", [&] { tr->impl->set_forced_plan(ids, n, active); });
+}
+
+int mimose_trainer_set_grad_hook(mimose_trainer* tr, mimose_grad_hook fn, void* user) {
+  tr->impl->set_grad_hook(fn, user);
+  return 0;
+}
+
+int mimose_trainer_buffers(mimose_trainer* tr, float** p32, void** p16, float** g32, int64_t* n,
+                           float** d_loss, float** d_logits) {
+  if (p32) *p32 = tr->impl->params_f32();
+  if (p16) *p16 = tr->impl->params_bf16();
+  if (g32) *g32 = tr->impl->grads();
+  if (n) *n = tr->impl->num_params();
+  if (d_loss) *d_loss = tr->impl->d_loss();
+  if (d_logits) *d_logits = tr->impl->d_logits();
+  return 0;
+}
+
+int mimose_trainer_param_count(mimose_trainer* tr) { return tr->impl->param_count(); }
+
+int mimose_trainer_param_info(mimose_trainer* tr, int i, const char** name, int64_t* offset,
+                              int64_t* numel) {
+  return guarded("mimose_trainer_param_info", [&] { tr->impl->param_info(i, name, offset, numel); });
+}
+
+int mimose_trainer_sync_params(mimose_trainer* tr, void* stream) {
+  return guarded("mimose_trainer_sync_params", [&] {
+    mimose_rt::ck(mimose_ops::f32_to_bf16(tr->impl->params_f32(), tr->impl->params_bf16(),
+                                          tr->impl->num_params(), static_cast<cudaStream_t>(stream)),
+                  "f32_to_bf16");
+  });
+}
+
+int mimose_trainer_samples_csv(mimose_trainer* tr, char** out) {
+  return guarded("mimose_trainer_samples_csv", [&] {
+    std::ostringstream os;
+    mimose::write_samples_csv(tr->impl->collector().samples, os);
+    *out = dup_string(os.str());
+  });
+}
+
+int mimose_trainer_estimator_text(mimose_trainer* tr, char** out) {
+  return guarded("mimose_trainer_estimator_text", [&] {
+    *out = dup_string(mimose::estimator_to_string(tr->impl->estimator()));
+  });
+}
+
+int mimose_trainer_model_text(mimose_trainer* tr, char** out) {
+  return guarded("mimose_trainer_model_text", [&] {
+    *out = dup_string(mimose::model_to_string(tr->impl->spec()));
+  });
+}
+
+int mimose_trainer_info(mimose_trainer* tr, int64_t* constant_bytes, int64_t* reserve_bytes,
+                        int64_t* budget, int* trained, int64_t* cache_hits,
+                        int64_t* cache_misses) {
+  if (constant_bytes) *constant_bytes = tr->impl->constant_bytes();
+  if (reserve_bytes) *reserve_bytes = tr->impl->reserve_bytes();
+  if (budget) *budget = tr->impl->sched().budget_bytes;
+  if (trained) *trained = tr->impl->trained() ? 1 : 0;
+  if (cache_hits) *cache_hits = tr->impl->cache().hits;
+  if (cache_misses) *cache_misses = tr->impl->cache().misses;
+  return 0;
+}
+
+void mimose_free_string(char* s) { std::free(s); }
+
+int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32_t* perm,
+                              int32_t* seg, int32_t* uid, int* n_unique) {
+  return guarded("mimose_build_token_tables", [&] {
+    *n_unique = mimose_rt::build_token_tables(tokens, T, vocab, perm, seg, uid);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,176 @@
+// Layer executor + Mimose training loop on one B200 (SURVEY §2.4 P1, C1, and
+// §8(a) a14/a16-a18).
+//
+// The trainer runs the reference's two-phase machine
+// (reference harness.hpp:215-296) for real: sheltered iterations measure
+// every encoder block's activation bytes as the budget arena's
+// requested-bytes delta around the block's forward (and its time with
+// cudaEvents); the host fits the reference estimator (include/mimose/
+// estimator.hpp `fit`), and responsive iterations apply
+// `lookup_or_plan` plans: a dropped block forwards in no-save mode keeping
+// only its output, and is re-forwarded (same kernels, same Philox streams)
+// right before its backward.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "capi_common.hpp"
+#include "mimose/mimose.hpp"
+#include "mimose_cuda.h"
+
+namespace mimose_rt {
+
+struct ParamRef {
+  int64_t off = 0;  // element offset into the flat parameter buffers
+  int64_t n = 0;
+};
+
+struct LayerParams {
+  ParamRef wqkv, bqkv, wo, bo, ln1_g, ln1_b, w1, b1, w2, b2, ln2_g, ln2_b;
+};
+
+struct LayerSave {
+  void *qkv = nullptr, *P = nullptr, *Pd = nullptr, *ctx = nullptr, *z1 = nullptr,
+       *h1 = nullptr, *u = nullptr, *g = nullptr, *z2 = nullptr, *st1 = nullptr,
+       *st2 = nullptr;
+};
+
+struct StepGeo {
+  int B = 0, S = 0, ld = 0;
+  int64_t T = 0;
+  uint64_t step = 0;
+};
+
+struct StepInputs {  // device pointers
+  const int32_t* tokens = nullptr;
+  const int32_t* types = nullptr;
+  const int32_t* labels = nullptr;
+  const int32_t* perm = nullptr;
+  const int32_t* seg = nullptr;
+  const int32_t* uid = nullptr;
+  int n_unique = 0;
+};
+
+class Trainer {
+ public:
+  Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_cfg& t);
+  ~Trainer();
+
+  // One forward + backward (no optimizer). Host-side phase machine decides
+  // the plan. Loss stays on device (d_loss()).
+  void forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
+                        mimose_step_report* rep);
+  void optimizer_step(float grad_scale, cudaStream_t s);
+
+  // host inputs -> staged H2D -> forward_backward (+ hook + optimizer) -> loss D2H
+  void step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
+                 int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep);
+
+  void set_forced_plan(const int* ids, int n, int active);
+  void set_grad_hook(mimose_grad_hook fn, void* user) {
+    hook_ = fn;
+    hook_user_ = user;
+  }
+
+  // introspection
+  float* params_f32() const { return p32_; }
+  void* params_bf16() const { return p16_; }
+  float* grads() const { return g32_; }
+  int64_t num_params() const { return nparam_; }
+  float* d_loss() const { return d_loss_; }
+  float* d_logits() const { return d_logits_; }
+  const mimose::ModelSpec& spec() const { return spec_; }
+  const mimose::CollectorState& collector() const { return cstate_; }
+  const mimose::EstimatorModel& estimator() const { return est_; }
+  bool trained() const { return trained_; }
+  const mimose::PlanCache& cache() const { return cache_; }
+  const mimose::SchedulerConfig& sched() const { return sched_; }
+  const std::vector<mimose_step_report>& history() const { return history_; }
+  int64_t constant_bytes() const { return constant_bytes_; }
+  int64_t reserve_bytes() const { return sched_.effective_reserve(); }
+  int param_count() const { return static_cast<int>(param_names_.size()); }
+  void param_info(int i, const char** name, int64_t* off, int64_t* n) const;
+  int64_t extras_bytes(int S) const;
+
+ private:
+  // arena helpers (throw on budget breach)
+  void* take(int64_t bytes, int tag);
+  void drop(void*& p);
+  ParamRef add_param(const std::string& name, int64_t n, bool decay, std::vector<ParamRef*>& fix);
+
+  void build_params();
+  void init_params(cudaStream_t s);
+  void build_spec();
+
+  // layer executor
+  void layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
+                 cudaStream_t s);
+  void* layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
+                  cudaStream_t s);
+  void free_save(LayerSave& sv);
+
+  // phase machine (reference harness.hpp:215-296)
+  enum class Mode { Plain, Collect, AllLayers, Planned };
+  Mode decide(int64_t x, mimose::CheckpointPlan& plan, mimose_step_report* rep);
+  void refit(mimose_step_report* rep);
+
+  mimose_ctx* ctx_;
+  mimose_model_cfg m_;
+  mimose_train_cfg t_;
+  int H_, nh_, F_, L_;
+
+  float* p32_ = nullptr;
+  void* p16_ = nullptr;
+  float* g32_ = nullptr;
+  float* am_ = nullptr;
+  float* av_ = nullptr;
+  int64_t nparam_ = 0, n_decay_ = 0;
+  std::vector<std::string> param_names_;
+  std::vector<ParamRef> param_refs_;
+  ParamRef word_, pos_, type_, eln_g_, eln_b_, wp_, bp_, wc_, bc_;
+  std::vector<LayerParams> lp_;
+
+  float* ln_partial_ = nullptr;
+  float* col_partial_ = nullptr;
+  float* norm_partial_ = nullptr;
+  float* norm2_ = nullptr;
+  float* d_loss_ = nullptr;
+  float* d_logits_ = nullptr;
+  float* h_loss_ = nullptr;  // pinned
+
+  // pinned staging for host inputs
+  int32_t* h_stage_ = nullptr;
+  int64_t stage_elems_ = 0;
+
+  std::vector<cudaEvent_t> ev_;  // 2 per layer (collector timing)
+
+  mimose::ModelSpec spec_;
+  mimose::SchedulerConfig sched_;
+  mimose::CollectorConfig ccfg_;
+  mimose::CollectorState cstate_;
+  mimose::EstimatorModel est_;
+  mimose::PlanCache cache_;
+  bool trained_ = false;
+  int64_t iter_ = 0;
+  int adam_t_ = 0;
+  int64_t constant_bytes_ = 0;
+  std::vector<mimose_step_report> history_;
+
+  bool forced_active_ = false;
+  std::vector<int> forced_;
+
+  mimose_grad_hook hook_ = nullptr;
+  void* hook_user_ = nullptr;
+};
+
+// Counting sort of token ids (stable): perm lists positions grouped by id
+// (ascending position inside a group), seg[u]..seg[u+1] delimits group u,
+// uid[u] is its id. Returns the number of distinct ids.
+int build_token_tables(const int32_t* tokens, int64_t T, int V, int32_t* perm, int32_t* seg,
+                       int32_t* uid);
+
+}  // namespace mimose_rt

@@ -1,0 +1,349 @@
+"""Python facade over the C-ABI trainer (libmimose_cuda.so).
+
+This mirrors the reference's experiment surface (reference
+proj/include/mimose/harness.hpp:48-118 ``ExperimentConfig`` / ``IterationRow``)
+for a real GPU training run: every step returns an IterationRow-shaped dict
+with the measured peak bytes instead of simulated ones. All compute happens in
+the sm_100a kernels behind the C ABI; torch is used only to hand over device
+pointers / streams and to view device buffers.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Callable, Dict, Optional
+
+import numpy as np
+
+from . import _lib
+from ._lib import MimoseError, check, cuda_lib
+
+PLANNERS = {"mimose": 0, "none": 1, "all": 2, "static-max": 3}
+PHASES = {0: "planned", 1: "collect", 2: "sheltered", 3: "plain", 4: "fallback-collect"}
+
+
+@dataclasses.dataclass
+class ModelConfig:
+    layers: int = 12
+    hidden: int = 768
+    heads: int = 12
+    ffn: int = 3072
+    vocab: int = 30522
+    max_pos: int = 512
+    type_vocab: int = 2
+    num_choices: int = 4
+    hidden_dropout: float = 0.1
+    attn_dropout: float = 0.1
+    ln_eps: float = 1e-12
+    init_std: float = 0.02
+    seed: int = 1234
+
+    def to_c(self):
+        c = _lib.ModelCfg()
+        for f in dataclasses.fields(self):
+            setattr(c, f.name, getattr(self, f.name))
+        return c
+
+
+@dataclasses.dataclass
+class TrainConfig:
+    planner: str = "mimose"
+    batch: int = 64
+    seq_min: int = 64
+    seq_max: int = 512
+    reserve_bytes: int = -1
+    bucket_tolerance: float = 0.10
+    cache_tolerance: float = 0.0
+    max_sheltered_iters: int = 10
+    collect_new_sizes_always: bool = False
+    estimator_order: int = 2
+    lr: float = 5e-5
+    beta1: float = 0.9
+    beta2: float = 0.999
+    adam_eps: float = 1e-8
+    weight_decay: float = 0.01
+    max_grad_norm: float = 1.0
+
+    def to_c(self):
+        c = _lib.TrainCfg()
+        for f in dataclasses.fields(self):
+            v = getattr(self, f.name)
+            if f.name == "planner":
+                v = PLANNERS[v]
+            setattr(c, f.name, int(v) if isinstance(v, bool) else v)
+        return c
+
+
+# Named configurations of BASELINE.json (multiple-choice head variants).
+PRESETS = {
+    # configs[0]: small BERT-like encoder, 4 layers, hidden 256, S 32-256
+    "small4-h256": (ModelConfig(layers=4, hidden=256, heads=4, ffn=1024),
+                    TrainConfig(batch=8, seq_min=32, seq_max=256)),
+    # configs[1]: BERT-base multiple choice (SWAG-shaped 16 x 4 choices), S 64-512
+    "bert-base-mc": (ModelConfig(), TrainConfig(batch=64, seq_min=64, seq_max=512)),
+}
+
+
+class _DevArray:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {
+            "shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3,
+            "strides": None,
+        }
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return getattr(stream, "cuda_stream", stream)
+
+
+class Context:
+    """One device + its budget arena (every byte the trainer uses lives here)."""
+
+    def __init__(self, budget_bytes: int, device: int = 0):
+        self.lib = cuda_lib()
+        h = C.c_void_p()
+        check(self.lib.mimose_ctx_create(device, int(budget_bytes), C.byref(h)))
+        self.handle = h
+        self.device = device
+
+    def mem_stats(self) -> dict:
+        st = _lib.MemStats()
+        check(self.lib.mimose_mem_stats_get(self.handle, C.byref(st)))
+        return st.as_dict()
+
+    def close(self):
+        if self.handle:
+            self.lib.mimose_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Trainer:
+    def __init__(self, model: ModelConfig, train: TrainConfig, budget_bytes: int,
+                 device: int = 0):
+        self.model = model
+        self.train = train
+        self.ctx = Context(budget_bytes, device)
+        self.lib = self.ctx.lib
+        h = C.c_void_p()
+        check(self.lib.mimose_trainer_create(self.ctx.handle, C.byref(model.to_c()),
+                                             C.byref(train.to_c()), C.byref(h)))
+        self.handle = h
+        self._hook = None
+        self.rows = []
+
+    # ------------------------------------------------------------ steps
+    def step(self, tokens, types, labels, *, optimizer: bool = True, stream=None) -> dict:
+        """Host inputs (numpy / CPU torch, int32): H2D + fwd + bwd (+ AdamW) + loss D2H."""
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        B, S = tokens.shape
+        types = np.ascontiguousarray(
+            types if types is not None else np.zeros_like(tokens), dtype=np.int32)
+        labels = np.ascontiguousarray(labels, dtype=np.int32)
+        rep = _lib.StepReport()
+        fn = self.lib.mimose_trainer_step if optimizer else self.lib.mimose_trainer_forward_backward
+        check(fn(self.handle, tokens.ctypes.data, types.ctypes.data, labels.ctypes.data, B, S,
+                 _stream_handle(stream), C.byref(rep)))
+        d = self._row(rep)
+        self.rows.append(d)
+        return d
+
+    def step_pinned(self, tokens, types, labels, *, optimizer: bool = True, stream=None) -> dict:
+        """Host inputs already in pinned torch tensors (async H2D inside the step)."""
+        B, S = tokens.shape
+        rep = _lib.StepReport()
+        fn = self.lib.mimose_trainer_step if optimizer else self.lib.mimose_trainer_forward_backward
+        check(fn(self.handle, tokens.data_ptr(), types.data_ptr(), labels.data_ptr(), B, S,
+                 _stream_handle(stream), C.byref(rep)))
+        d = self._row(rep)
+        self.rows.append(d)
+        return d
+
+    def step_device(self, batch: "DeviceBatch", *, optimizer: bool = True, stream=None) -> dict:
+        """Device-resident inputs; no host synchronisation (loss stays on device)."""
+        rep = _lib.StepReport()
+        check(self.lib.mimose_trainer_step_device(
+            self.handle, batch.tokens.data_ptr(), batch.types.data_ptr(), batch.labels.data_ptr(),
+            batch.perm.data_ptr(), batch.seg.data_ptr(), batch.uid.data_ptr(), batch.n_unique,
+            batch.B, batch.S, int(optimizer), _stream_handle(stream), C.byref(rep)))
+        d = self._row(rep)
+        self.rows.append(d)
+        return d
+
+    def optimizer_step(self, grad_scale: float = 1.0, stream=None):
+        check(self.lib.mimose_trainer_optimizer_step(self.handle, grad_scale,
+                                                     _stream_handle(stream)))
+
+    @staticmethod
+    def _row(rep) -> dict:
+        d = rep.as_dict()
+        d["phase_name"] = PHASES.get(d["phase"], str(d["phase"]))
+        d["dropped"] = [i for i in range(64) if (d["dropped_mask_lo"] >> i) & 1]
+        return d
+
+    # ------------------------------------------------------------ control
+    def force_plan(self, ids, active: bool = True):
+        ids = list(ids)
+        arr = (C.c_int * max(1, len(ids)))(*ids)
+        check(self.lib.mimose_trainer_force_plan(self.handle, arr, len(ids), int(active)))
+
+    def set_grad_hook(self, fn: Optional[Callable]):
+        """fn(grads_tensor, stream_handle) runs after backward, before AdamW."""
+        if fn is None:
+            self._hook = None
+            check(self.lib.mimose_trainer_set_grad_hook(self.handle, _lib.GRAD_HOOK(), None))
+            return
+        grads = self.grads()
+
+        def _cb(user, ptr, n, stream):
+            fn(grads, stream)
+
+        self._hook = _lib.GRAD_HOOK(_cb)
+        check(self.lib.mimose_trainer_set_grad_hook(self.handle, self._hook, None))
+
+    # ------------------------------------------------------------ buffers
+    def _buffers(self):
+        p32, p16, g32, dl, dlg = (C.c_void_p() for _ in range(5))
+        n = C.c_int64()
+        check(self.lib.mimose_trainer_buffers(self.handle, C.byref(p32), C.byref(p16),
+                                              C.byref(g32), C.byref(n), C.byref(dl),
+                                              C.byref(dlg)))
+        return p32.value, p16.value, g32.value, n.value, dl.value, dlg.value
+
+    def params(self):
+        import torch
+        p32, _, _, n, _, _ = self._buffers()
+        return torch.as_tensor(_DevArray(p32, n, "<f4"), device="cuda")
+
+    def params_bf16(self):
+        import torch
+        _, p16, _, n, _, _ = self._buffers()
+        return torch.as_tensor(_DevArray(p16, n, "<i2"), device="cuda").view(torch.bfloat16)
+
+    def grads(self):
+        import torch
+        _, _, g32, n, _, _ = self._buffers()
+        return torch.as_tensor(_DevArray(g32, n, "<f4"), device="cuda")
+
+    def loss_device(self):
+        import torch
+        _, _, _, _, dl, _ = self._buffers()
+        return torch.as_tensor(_DevArray(dl, 1, "<f4"), device="cuda")
+
+    def logits_device(self):
+        import torch
+        _, _, _, _, _, dlg = self._buffers()
+        return torch.as_tensor(_DevArray(dlg, self.train.batch, "<f4"), device="cuda")
+
+    def param_table(self) -> Dict[str, tuple]:
+        out = {}
+        for i in range(self.lib.mimose_trainer_param_count(self.handle)):
+            name = C.c_char_p()
+            off = C.c_int64()
+            n = C.c_int64()
+            check(self.lib.mimose_trainer_param_info(self.handle, i, C.byref(name), C.byref(off),
+                                                     C.byref(n)))
+            out[name.value.decode()] = (off.value, n.value)
+        return out
+
+    def sync_params(self, stream=None):
+        check(self.lib.mimose_trainer_sync_params(self.handle, _stream_handle(stream)))
+
+    # ------------------------------------------------------------ planner state
+    def _text(self, fn) -> str:
+        p = C.c_void_p()
+        check(fn(self.handle, C.byref(p)))
+        return _lib.take_string(self.lib, p)
+
+    def samples_csv(self) -> str:
+        return self._text(self.lib.mimose_trainer_samples_csv)
+
+    def estimator_text(self) -> str:
+        return self._text(self.lib.mimose_trainer_estimator_text)
+
+    def model_text(self) -> str:
+        return self._text(self.lib.mimose_trainer_model_text)
+
+    def info(self) -> dict:
+        c, r, b = C.c_int64(), C.c_int64(), C.c_int64()
+        t = C.c_int()
+        h, m = C.c_int64(), C.c_int64()
+        check(self.lib.mimose_trainer_info(self.handle, C.byref(c), C.byref(r), C.byref(b),
+                                           C.byref(t), C.byref(h), C.byref(m)))
+        return {"constant_bytes": c.value, "reserve_bytes": r.value, "budget": b.value,
+                "trained": bool(t.value), "cache_hits": h.value, "cache_misses": m.value}
+
+    def mem_stats(self) -> dict:
+        return self.ctx.mem_stats()
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.mimose_trainer_destroy(self.handle)
+            self.handle = None
+        self.ctx.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def token_tables(tokens: np.ndarray, vocab: int):
+    """Host counting sort for the deterministic word-embedding gradient."""
+    lib = cuda_lib()
+    tokens = np.ascontiguousarray(tokens, dtype=np.int32).ravel()
+    T = tokens.size
+    perm = np.empty(T, np.int32)
+    seg = np.empty(T + 1, np.int32)
+    uid = np.empty(max(T, 1), np.int32)
+    nu = C.c_int()
+    check(lib.mimose_build_token_tables(tokens.ctypes.data, T, vocab, perm.ctypes.data,
+                                        seg.ctypes.data, uid.ctypes.data, C.byref(nu)))
+    return perm, seg[: nu.value + 1].copy(), uid[: nu.value].copy(), nu.value
+
+
+@dataclasses.dataclass
+class DeviceBatch:
+    """One step's inputs resident on the device (torch int32 tensors)."""
+    tokens: "object"
+    types: "object"
+    labels: "object"
+    perm: "object"
+    seg: "object"
+    uid: "object"
+    n_unique: int
+    B: int
+    S: int
+
+    @staticmethod
+    def from_host(tokens, types, labels, vocab, device="cuda"):
+        import torch
+        tokens = np.ascontiguousarray(tokens, dtype=np.int32)
+        B, S = tokens.shape
+        perm, seg, uid, nu = token_tables(tokens, vocab)
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.int32)).to(device)
+        return DeviceBatch(t(tokens), t(types), t(labels), t(perm), t(seg),
+                           t(uid if nu else np.zeros(1, np.int32)), nu, B, S)
+
+
+def synthetic_batch(rng: np.random.Generator, B: int, S: int, vocab: int, num_choices: int,
+                    type_vocab: int = 2):
+    """SWAG-shaped synthetic multiple-choice batch (uniform token ids)."""
+    tokens = rng.integers(0, vocab, size=(B, S), dtype=np.int32)
+    types = np.zeros((B, S), np.int32)
+    if type_vocab > 1:
+        split = rng.integers(1, S, size=B)
+        types[np.arange(S)[None, :] >= split[:, None]] = 1
+    labels = rng.integers(0, num_choices, size=B // num_choices, dtype=np.int32)
+    return tokens, types, labels
