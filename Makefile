@@ -32,11 +32,13 @@ $(BUILD)/%.cpp.o: $(CSRC)/%.cpp $(HDRS)
 	@mkdir -p $(BUILD)
 	$(CXX) $(CXXFLAGS) -I$(CSRC) -I$(CUDA_INC) -c $< -o $@
 
-$(PKG)/libmimose_cuda.so: $(CU_OBJS) $(CPP_OBJS)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) $(CPP_OBJS)
+$(PKG)/libmimose_cuda.so: $(CU_OBJS) $(CPP_OBJS) $(CSRC)/exports.map
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -Xlinker --version-script=$(CSRC)/exports.map \
+	  -Xlinker --exclude-libs,ALL -o $@ $(CU_OBJS) $(CPP_OBJS)
 
 $(PKG)/libmimose_host.so: $(CSRC)/host/planner_capi.cpp $(HDRS)
-	$(CXX) $(CXXFLAGS) -shared -o $@ $<
+	$(CXX) $(CXXFLAGS) -shared -Wl,--version-script=$(CSRC)/exports.map -Wl,--exclude-libs,ALL \
+	  -o $@ $<
 
 clean:
 	rm -rf $(BUILD) $(PKG)/*.so

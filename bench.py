@@ -1,0 +1,458 @@
+#!/usr/bin/env python
+"""Benchmark: samples/s of Mimose input-aware checkpointing training on B200
+under a fixed per-GPU memory budget with dynamic sequence lengths.
+
+Workload (BASELINE.json configs[1]): BERT-base multiple-choice fine-tune,
+SWAG-shaped synthetic data (16 questions x 4 choices = 64 sequences per rank
+per step), sequence length S drawn per step from uniform:64:512 with the
+reference's own sampler (include/mimose/workload.hpp sample_workload, seed
+base+rank), random-init weights (N(0, 0.02)), AdamW, dropout 0.1, bf16
+compute. Budget = 40 % of the measured no-checkpoint peak at S_max
+(everything - weights, grads, AdamW state, activations, workspace - lives in
+the budget arena).
+
+Arms
+  default            this repo's B200 path (python bench.py --gpus N ...)
+  --impl reference   the CPU path: the oracle's PyTorch-CPU fp32 restatement
+                     of the same training step (the reference itself is a
+                     byte/ms simulator with no tensor code), all host cores,
+                     bounded sub-batch per step, rank 0 only.
+
+One JSON line on rank 0. Timing: W untimed warm-up steps after the planner's
+sheltered calibration window, then exactly K steps bracketed by barrier +
+synchronize, CUDA events on the launching stream, max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "samples/sec under fixed GPU mem budget, dynamic seqlen, 1/2/4/8 B200; mem-pred err"
+GiB = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--budget-frac", type=float, default=0.4)
+    ap.add_argument("--preset", default="bert-base-mc")
+    ap.add_argument("--dist", default="uniform:64:512")
+    ap.add_argument("--seed", type=int, default=2024)
+    ap.add_argument("--no-baseline", action="store_true", help="skip no-ckpt throughput arm")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--profile-only", action="store_true",
+                    help="short run for ncu (no comparison arms, no cpu baseline)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 7:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def sizes_for(dist, batch, iters, seed):
+    from paper_2209_02478_b200 import planner
+    xs = planner.host_lib().workload(dist, 1, iters, seed)
+    return [int(x) for x in xs]
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def dist_init(n):
+    if n <= 1 and "WORLD_SIZE" not in os.environ:
+        return 0, 1, 0
+    import torch.distributed as dist
+    import torch
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", n))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def allmax(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(v, world):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ----------------------------------------------------------------- CPU arm
+def cpu_step_sample(model_cfg, S, sub_batch, rng, threads):
+    """One bounded CPU training step (oracle fp32 fwd+bwd + AdamW) of
+    `sub_batch` sequences of length S; returns seconds."""
+    import numpy as np
+    import torch
+    from oracle import bert_ref
+    from paper_2209_02478_b200.trainer import synthetic_batch
+    torch.set_num_threads(threads)
+    shapes = bert_ref.param_shapes(model_cfg)
+    g = np.random.default_rng(0)
+    params = {k: (g.standard_normal(int(np.prod(s))).astype(np.float32) * 0.02
+                  if (k.endswith("weight") and "ln" not in k) or k.startswith("embeddings.")
+                  and "ln" not in k else
+                  (np.ones(int(np.prod(s)), np.float32) if "ln.weight" in k
+                   else np.zeros(int(np.prod(s)), np.float32)))
+              for k, s in shapes.items()}
+    tok, typ, lab = synthetic_batch(rng, sub_batch, S, model_cfg.vocab, model_cfg.num_choices)
+    t0 = time.perf_counter()
+    _, _, grads = bert_ref.loss_and_grads(params, tok, typ, lab, model_cfg, step=0)
+    # AdamW update of every parameter (what the GPU step also does)
+    for k, gr in grads.items():
+        p = torch.from_numpy(params[k])
+        gt = torch.from_numpy(gr)
+        m = torch.zeros_like(p)
+        v = torch.zeros_like(p)
+        m.mul_(0.9).add_(gt, alpha=0.1)
+        v.mul_(0.999).addcmul_(gt, gt, value=0.001)
+        p.mul_(1 - 5e-5 * 0.01).addcdiv_(m, v.sqrt().add_(1e-8), value=-5e-5)
+    return time.perf_counter() - t0
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    import numpy as np
+    from paper_2209_02478_b200.trainer import PRESETS
+    model_cfg, train_cfg = PRESETS[args.preset]
+    threads = os.cpu_count() or 1
+    sub = 4  # sequences per sampled CPU step (one multiple-choice question)
+    xs = sizes_for(args.dist, train_cfg.batch, args.warmup + args.steps, args.seed)
+    rng = np.random.default_rng(args.seed)
+    for S in xs[:args.warmup]:
+        cpu_step_sample(model_cfg, S, sub, rng, threads)
+    tot = 0.0
+    for S in xs[args.warmup:]:
+        tot += cpu_step_sample(model_cfg, S, sub, rng, threads)
+    value = sub * args.steps / tot
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "samples/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+        "config": {"workload": f"{args.preset} (BASELINE configs[1]) CPU port", "global_batch": sub,
+                   "seq_len": args.dist, "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
+                         "sample": f"{sub} sequences per step (1 question x 4 choices) at the "
+                                   f"step's drawn S; oracle/bert_ref.py fp32 fwd+bwd + AdamW"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, rank, world, local):
+    import numpy as np
+    import torch
+    from paper_2209_02478_b200 import _lib
+    from paper_2209_02478_b200.trainer import (PRESETS, DeviceBatch, Trainer, synthetic_batch)
+    import dataclasses
+
+    lib = _lib.cuda_lib()
+    model_cfg, train_cfg = PRESETS[args.preset]
+    B = train_cfg.batch
+    S_max = train_cfg.seq_max
+    stream = torch.cuda.current_stream()
+    pk, pk_kind = peaks()
+
+    # 1. no-checkpoint peak at S_max (defines the budget denominator)
+    free, total = torch.cuda.mem_get_info()
+    probe_budget = int(min(free * 0.85, 150 * GiB))
+    probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"), probe_budget, local)
+    rng = np.random.default_rng(args.seed + 1000 * rank)
+    probe.step(*synthetic_batch(rng, B, S_max, model_cfg.vocab, model_cfg.num_choices),
+               optimizer=False, stream=stream)
+    peak_none = int(allmax(probe.rows[-1]["peak_reserved"], world))
+    probe.close()
+    budget = int(args.budget_frac * peak_none)
+
+    n_total = args.warmup + args.steps
+    seqs = sizes_for(args.dist, B, 10_000, args.seed + rank)  # rank r: seed base + r
+
+    def batches(seq_list, seed):
+        g = np.random.default_rng(seed)
+        return [synthetic_batch(g, B, s, model_cfg.vocab, model_cfg.num_choices)
+                for s in seq_list]
+
+    def allreduce_hook(tr):
+        if world == 1:
+            return None
+        import torch.distributed as dist
+        grads = tr.grads()
+
+        def hook():
+            dist.all_reduce(grads)
+        return hook
+
+    def timed_run(tr, host_batches, dev_batches):
+        """W warm-up + K timed device-input steps; returns (ms list, rows)."""
+        hook = allreduce_hook(tr)
+        scale = 1.0 / world
+
+        def one(db):
+            tr.step_device(db, optimizer=False, stream=stream)
+            if hook:
+                hook()
+            tr.optimizer_step(scale, stream=stream)
+
+        for db in dev_batches[:args.warmup]:
+            one(db)
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        l0 = lib.mimose_launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for db in dev_batches[args.warmup:]:
+            one(db)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = ev0.elapsed_time(ev1)
+        launches = lib.mimose_launch_count() - l0
+        return ms, launches
+
+    # 2. Mimose trainer under the budget; sheltered calibration window first
+    tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="mimose"), budget, local)
+    calib = tr.train.max_sheltered_iters + 2
+    cal_batches = batches(seqs[:calib], args.seed + 7 * rank + 1)
+    t_cal0 = time.perf_counter()
+    for b in cal_batches:
+        tr.step(*b, stream=stream)
+    calib_s = time.perf_counter() - t_cal0
+    run_seqs = seqs[calib:calib + n_total]
+    hb = batches(run_seqs, args.seed + 7 * rank + 2)
+    db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in hb]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms, launches = timed_run(tr, hb, db)
+    ms_max = allmax(ms, world)
+    rows = tr.rows[-args.steps:]
+    samples = B * args.steps * world
+    value = samples / (ms_max / 1000.0)
+
+    # memory discipline + prediction error + planning overhead over the timed steps
+    max_peak = max(r["peak_reserved"] for r in rows)
+    over = [r for r in rows if r["peak_reserved"] > budget]
+    pred = [r["pred_err_max"] for r in rows if r["pred_layers"] > 0]
+    plan_us = sum(r["plan_us"] + r["fit_us"] for r in rows)
+    dropped_avg = sum(r["plan_size"] for r in rows) / len(rows)
+
+    # 3. roofline: GEMM family timed per launch (CUDA events) on 2 extra steps
+    extra = batches(seqs[calib + n_total:calib + n_total + 2], args.seed + 99)
+    extra_db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in extra]
+    import ctypes as C
+    lib.mimose_gemm_profile_enable(1)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for d in extra_db:
+        tr.step_device(d, optimizer=True, stream=stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    fl, gms, gl = C.c_double(), C.c_double(), C.c_int64()
+    _lib.check(lib.mimose_gemm_profile_read(C.byref(fl), C.byref(gms), C.byref(gl)))
+    lib.mimose_gemm_profile_enable(0)
+    step_ms_prof = e0.elapsed_time(e1)
+    achieved_tflops = fl.value / (gms.value / 1000.0) / 1e12 if gms.value > 0 else 0.0
+    peak_tf = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)))
+
+    # 4. e2e: public API with HOST (pinned) inputs, H2D + loss D2H inside the region
+    e2e_batches = batches(seqs[calib + n_total + 2:calib + 2 * n_total + 2], args.seed + 5)
+    pinned = [tuple(torch.from_numpy(a).pin_memory() for a in b) for b in e2e_batches]
+    h2d = 0
+    for b in pinned[:args.warmup]:
+        tr.step_pinned(*b, stream=stream) if world == 1 else None
+    # N>1: forward_backward + allreduce + optimizer through the same public calls
+    def e2e_one(b):
+        if world == 1:
+            tr.step_pinned(*b, stream=stream)
+        else:
+            tr.step_pinned(*b, optimizer=False, stream=stream)
+            import torch.distributed as dist
+            dist.all_reduce(tr.grads())
+            tr.optimizer_step(1.0 / world, stream=stream)
+    if world > 1:
+        for b in pinned[:args.warmup]:
+            e2e_one(b)
+    torch.cuda.synchronize()
+    barrier(world)
+    t0 = time.perf_counter()
+    for b in pinned[args.warmup:]:
+        e2e_one(b)
+        h2d += sum(x.numel() * 4 for x in b)
+    torch.cuda.synchronize()
+    e2e_s = allmax(time.perf_counter() - t0, world)
+    e2e_value = samples / e2e_s
+    h2d_per_step = h2d // args.steps  # tokens + types + labels (token tables are built on host)
+
+    # 5. no-checkpoint, unlimited-memory throughput on the same size stream
+    nock = None
+    if not args.no_baseline and not args.profile_only:
+        base = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"),
+                       int(peak_none * 1.15) + GiB, local)
+        ms_none, _ = timed_run(base, hb, db)
+        ms_none = allmax(ms_none, world)
+        nock = samples / (ms_none / 1000.0)
+        base.close()
+
+    # 6. CPU baseline (rank 0, N=1 only): bounded sample of the same workload
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu and not args.profile_only:
+        threads = os.cpu_count() or 1
+        g = np.random.default_rng(1)
+        S_s = run_seqs[:3]
+        tot = sum(cpu_step_sample(model_cfg, S, 4, g, threads) for S in S_s)
+        cpu = {"value": 4 * len(S_s) / tot, "unit": "samples/s", "cores": threads, "kind": "port",
+               "sample": f"3 steps x 4 sequences (one question) at S={S_s}; oracle/bert_ref.py "
+                         f"PyTorch-CPU fp32 fwd+bwd + AdamW, {threads} threads"}
+
+    info = tr.info()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (uniform token ids, N(0,0.02) random-init weights)",
+            "config": {
+                "workload": "bert-base-mc: BERT-base (L12 H768 A12 F3072 V30522) multiple-choice "
+                            "fine-tune, SWAG-shaped 16x4 choices (BASELINE configs[1])",
+                "global_batch": B * world, "seq_len": args.dist, "parallelism": f"dp{world}",
+                "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
+                "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
+                "l2": "not flushed: per-step working set (GBs of activations) >> 126 MB L2",
+                "calibration": f"{calib} planner-calibration steps (sheltered collection window "
+                               f"+ fit) run before warm-up, {calib_s:.2f} s",
+            },
+            "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / peak_tf,
+                         "traffic": None,
+                         "kernel": "gemm_bf16_tn_kernel (tcgen05) family",
+                         "gemm_ms_share_of_step": gms.value / step_ms_prof if step_ms_prof else None,
+                         "gemm_launches": gl.value, "peak_kind": pk_kind + " sustained"},
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_per_step,
+                    "d2h_bytes_per_step": 4},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "mimose": {
+                "no_ckpt_samples_per_s": nock,
+                "frac_of_no_ckpt": (value / nock) if nock else None,
+                "max_peak_bytes": max_peak, "budget_bytes": budget,
+                "steps_over_budget": len(over), "arena_failures": tr.mem_stats()["n_failures"],
+                "mem_pred_err_max": max(pred) if pred else None,
+                "mem_pred_err_mean": (sum(pred) / len(pred)) if pred else None,
+                "planning_overhead_frac": (plan_us / 1000.0) / ms if ms else None,
+                "avg_dropped_blocks": dropped_avg,
+                "constant_bytes": info["constant_bytes"], "reserve_bytes": info["reserve_bytes"],
+                "cache_hits": info["cache_hits"], "cache_misses": info["cache_misses"],
+            },
+        }
+        print(json.dumps(line), flush=True)
+    tr.close()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", 0))
+        world = int(os.environ.get("WORLD_SIZE", args.gpus))
+        run_reference_arm(args, rank, world)
+        return
+    rank, world, local = dist_init(args.gpus)
+    run_gpu_arm(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,6 +94,13 @@ typedef struct {
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);
 
+/* GEMM profiling (roofline evidence): while enabled, every GEMM launch is
+ * bracketed by CUDA events on its stream; read() synchronises and returns
+ * the summed algorithmic flops (2*M*N*K*batch), summed kernel ms and the
+ * number of launches since enable. */
+int mimose_gemm_profile_enable(int enable);
+int mimose_gemm_profile_read(double* flops, double* ms, int64_t* launches);
+
 /* ------------------------------------------------------------------ trainer
  * The training executor: BERT-style encoder blocks (post-LN, GELU FFN,
  * materialised attention) + multiple-choice head, trained with AdamW under
@@ -152,6 +159,9 @@ typedef struct {
   double plan_us;              /* lookup_or_plan wall time */
   double fit_us;               /* fit wall time */
   uint64_t dropped_mask_lo;    /* bit i = block i dropped (blocks 0..63) */
+  double pred_err_mean;        /* |predict(l,x) - measured a_l(x)| / measured, kept blocks */
+  double pred_err_max;
+  int pred_layers;             /* kept blocks the error was measured on */
 } mimose_step_report;
 
 typedef void (*mimose_grad_hook)(void* user, float* grads, int64_t n, void* stream);

@@ -97,6 +97,7 @@ class StepReport(C.Structure):
         ("predicted_kept", C.c_int64), ("budget", C.c_int64),
         ("plan_us", C.c_double), ("fit_us", C.c_double),
         ("dropped_mask_lo", C.c_uint64),
+        ("pred_err_mean", C.c_double), ("pred_err_max", C.c_double), ("pred_layers", C.c_int),
     ]
 
     def as_dict(self):
@@ -125,6 +126,9 @@ CUDA_SYMBOLS = [
     ("mimose_book_free", C.c_int, [C.c_void_p, C.c_int64]),
     ("mimose_book_stats", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
     ("mimose_gemm", C.c_int, [C.POINTER(GemmArgs), C.c_void_p]),
+    ("mimose_gemm_profile_enable", C.c_int, [C.c_int]),
+    ("mimose_gemm_profile_read", C.c_int,
+     [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("mimose_trainer_create", C.c_int,
      [_P, C.POINTER(ModelCfg), C.POINTER(TrainCfg), C.POINTER(C.c_void_p)]),
     ("mimose_trainer_destroy", C.c_int, [_P]),

@@ -146,4 +146,15 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   return 0;
 }
 
+int mimose_gemm_profile_enable(int enable) {
+  mimose_ops::gemm_profile_enable(enable != 0);
+  return 0;
+}
+
+int mimose_gemm_profile_read(double* flops, double* ms, int64_t* launches) {
+  cudaError_t e = mimose_ops::gemm_profile_read(flops, ms, launches);
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_gemm_profile_read");
+  return 0;
+}
+
 }  // extern "C"

@@ -6,6 +6,8 @@
 #include <atomic>
 #include <cstdio>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "gemm_sm100.cuh"
 #include "ops.hpp"
@@ -20,6 +22,14 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 std::atomic<uint64_t> g_launches{0};
+
+// optional per-launch event bracketing (roofline evidence)
+struct GemmProfile {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+  std::vector<double> flops;
+  size_t used = 0;
+} g_prof;
 
 EncodeFn encode_fn() {
   static EncodeFn fn = [] {
@@ -138,12 +148,49 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
 
   const int64_t tiles = (int64_t)((c.M + 127) / 128) * ((c.N + bn - 1) / bn) * c.nb1 * c.nb2;
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
-  switch (bn) {
-    case 64: return launch_bn<64>(c.epi, ta, tb, p, grid, stream);
-    case 128: return launch_bn<128>(c.epi, ta, tb, p, grid, stream);
-    case 256: return launch_bn<256>(c.epi, ta, tb, p, grid, stream);
+  std::pair<cudaEvent_t, cudaEvent_t>* pe = nullptr;
+  if (g_prof.on) {
+    if (g_prof.used == g_prof.ev.size()) {
+      std::pair<cudaEvent_t, cudaEvent_t> e;
+      cudaEventCreate(&e.first);
+      cudaEventCreate(&e.second);
+      g_prof.ev.push_back(e);
+    }
+    pe = &g_prof.ev[g_prof.used++];
+    g_prof.flops.push_back(2.0 * c.M * (double)c.N * c.K * c.nb1 * c.nb2);
+    cudaEventRecord(pe->first, stream);
   }
-  return cudaErrorInvalidValue;
+  cudaError_t err = cudaErrorInvalidValue;
+  switch (bn) {
+    case 64: err = launch_bn<64>(c.epi, ta, tb, p, grid, stream); break;
+    case 128: err = launch_bn<128>(c.epi, ta, tb, p, grid, stream); break;
+    case 256: err = launch_bn<256>(c.epi, ta, tb, p, grid, stream); break;
+  }
+  if (pe != nullptr) cudaEventRecord(pe->second, stream);
+  return err;
+}
+
+void gemm_profile_enable(bool on) {
+  g_prof.on = on;
+  g_prof.used = 0;
+  g_prof.flops.clear();
+}
+
+cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches) {
+  double f = 0.0, t = 0.0;
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    cudaError_t e = cudaEventSynchronize(g_prof.ev[i].second);
+    if (e != cudaSuccess) return e;
+    float m = 0.f;
+    e = cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second);
+    if (e != cudaSuccess) return e;
+    t += m;
+    f += g_prof.flops[i];
+  }
+  *flops = f;
+  *ms = t;
+  *launches = (int64_t)g_prof.used;
+  return cudaSuccess;
 }
 
 }  // namespace mimose_ops

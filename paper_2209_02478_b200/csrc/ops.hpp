@@ -38,6 +38,8 @@ struct GemmCall {
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);
+void gemm_profile_enable(bool on);
+cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches);
 
 // Number of kernels launched by this module since process start (telemetry
 // for the bench's gpu_launches count).

@@ -766,9 +766,27 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
       out[l] = take(T * H * 2, kTagBoundary);
       layer_fwd(l, hin, out[l], nullptr, g, s);
     } else {
+      const int64_t before = ctx_->arena.stats().requested;
       out[l] = take(T * H * 2, kTagAct);
       layer_fwd(l, hin, out[l], &saves[l], g, s);
+      measured[l] = ctx_->arena.stats().requested - before;
     }
+  }
+  // memory-prediction error on the kept blocks (allocator-measured a_l(x))
+  if (trained_) {
+    double sum = 0.0, mx = 0.0;
+    int n = 0;
+    for (int l = 0; l < L_; ++l) {
+      if (dropped[l] || measured[l] <= 0) continue;
+      const double pred = static_cast<double>(mimose::predict(est_, l, x));
+      const double err = std::abs(pred - static_cast<double>(measured[l])) / static_cast<double>(measured[l]);
+      sum += err;
+      mx = std::max(mx, err);
+      ++n;
+    }
+    r->pred_layers = n;
+    r->pred_err_mean = n ? sum / n : 0.0;
+    r->pred_err_max = mx;
   }
 
   // ---- multiple-choice head: pooled = tanh(cls Wp^T + bp) -> logits -> CE
