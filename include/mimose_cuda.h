@@ -89,7 +89,11 @@ typedef struct {
   void* out; void* out2; const void* aux; const float* bias;
   int64_t ldo, obs1, obs2;
   float alpha, beta;
-  int force_bn;
+  int force_bn;      /* 0 = heuristic tile width; 64 / 128 / 256 forces it */
+  int direct_store;  /* 1 = per-thread stores instead of smem + TMA store (tests) */
+  int split_k;       /* fp32 outputs: 0 auto (needs workspace), 1 off, >1 forced */
+  void* workspace;   /* fp32 split-K partials, >= split_k * M * N * 4 bytes */
+  int64_t workspace_bytes;
 } mimose_gemm_args;
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);
@@ -100,6 +104,8 @@ int mimose_gemm(const mimose_gemm_args* args, void* stream);
  * number of launches since enable. */
 int mimose_gemm_profile_enable(int enable);
 int mimose_gemm_profile_read(double* flops, double* ms, int64_t* launches);
+/* Per-launch CSV (M,N,K,batch,bn,a_mn,b_mn,epi,grid,ms,tflops); free with mimose_free_string. */
+int mimose_gemm_profile_csv(char** out);
 
 /* ------------------------------------------------------------------ trainer
  * The training executor: BERT-style encoder blocks (post-LN, GELU FFN,

@@ -61,7 +61,8 @@ class GemmArgs(C.Structure):
         ("out", C.c_void_p), ("out2", C.c_void_p), ("aux", C.c_void_p), ("bias", C.c_void_p),
         ("ldo", C.c_int64), ("obs1", C.c_int64), ("obs2", C.c_int64),
         ("alpha", C.c_float), ("beta", C.c_float),
-        ("force_bn", C.c_int),
+        ("force_bn", C.c_int), ("direct_store", C.c_int),
+        ("split_k", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
     ]
 
 
@@ -127,6 +128,7 @@ CUDA_SYMBOLS = [
     ("mimose_book_stats", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
     ("mimose_gemm", C.c_int, [C.POINTER(GemmArgs), C.c_void_p]),
     ("mimose_gemm_profile_enable", C.c_int, [C.c_int]),
+    ("mimose_gemm_profile_csv", C.c_int, [C.POINTER(C.c_void_p)]),
     ("mimose_gemm_profile_read", C.c_int,
      [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("mimose_trainer_create", C.c_int,

@@ -1,6 +1,7 @@
 // C ABI implementation: context, allocator, operator entry points.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -141,6 +142,10 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   c.ldo = a->ldo; c.obs1 = a->obs1; c.obs2 = a->obs2;
   c.alpha = a->alpha; c.beta = a->beta;
   c.force_bn = a->force_bn;
+  c.direct_store = a->direct_store != 0;
+  c.split_k = a->split_k;
+  c.workspace = a->workspace;
+  c.workspace_bytes = a->workspace_bytes;
   cudaError_t e = mimose_ops::gemm(c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "mimose_gemm");
   return 0;
@@ -148,6 +153,14 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
 
 int mimose_gemm_profile_enable(int enable) {
   mimose_ops::gemm_profile_enable(enable != 0);
+  return 0;
+}
+
+int mimose_gemm_profile_csv(char** out) {
+  const std::string s = mimose_ops::gemm_profile_csv();
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  *out = p;
   return 0;
 }
 

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cstdio>
 #include <mutex>
+#include <string>
 #include <utility>
 #include <vector>
 
@@ -28,6 +29,7 @@ struct GemmProfile {
   bool on = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
   std::vector<double> flops;
+  std::vector<std::string> desc;
   size_t used = 0;
 } g_prof;
 
@@ -54,32 +56,37 @@ int sm_count() {
   return n;
 }
 
-// 4-D map (cols, rows, nb1, nb2) over a bf16 view with a {64, box_rows} box,
-// 128-byte swizzle, zero fill out of bounds.
-bool make_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box_rows) {
+// 4-D map (cols, rows, nb1, nb2) with a {box_cols, box_rows} box, 128-byte
+// swizzle, zero fill out of bounds. esz 2 = bf16, 4 = fp32.
+bool make_map_t(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                int64_t bs1, int64_t bs2, int nb1, int nb2, uint32_t box_cols, uint32_t box_rows,
+                int esz, bool sw64 = false) {
   EncodeFn fn = encode_fn();
   if (fn == nullptr) return false;
-  const uint64_t esz = 2;
-  cuuint64_t dims[4] = {(cuuint64_t)v.cols, (cuuint64_t)v.rows, (cuuint64_t)nb1,
-                        (cuuint64_t)nb2};
-  uint64_t plane = (uint64_t)v.ld * (uint64_t)v.rows * esz;
+  cuuint64_t dims[4] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)nb1, (cuuint64_t)nb2};
+  uint64_t plane = (uint64_t)ld * (uint64_t)rows * esz;
   plane = (plane + 15) & ~uint64_t(15);
-  cuuint64_t strides[3] = {(cuuint64_t)(v.ld * esz),
-                           (cuuint64_t)(nb1 > 1 ? v.bs1 * esz : plane),
-                           (cuuint64_t)(nb2 > 1 ? v.bs2 * esz : plane)};
-  cuuint32_t box[4] = {64, box_rows, 1, 1};
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * esz), (cuuint64_t)(nb1 > 1 ? bs1 * esz : plane),
+                           (cuuint64_t)(nb2 > 1 ? bs2 * esz : plane)};
+  cuuint32_t box[4] = {box_cols, box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(v.ptr), dims,
-                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(map, esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                  4, const_cast<void*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  sw64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
+bool make_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box_rows) {
+  return make_map_t(map, v.ptr, v.rows, v.cols, v.ld, v.bs1, v.bs2, nb1, nb2, 64, box_rows, 2);
+}
+
 template <int BN, int EPI>
-cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb,
-                     const mimose_dev::GemmParams& p, int grid, cudaStream_t stream) {
-  using Cfg = mimose_dev::GemmCfg<BN>;
+cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
+                     const CUtensorMap& td2, const mimose_dev::GemmParams& p, int grid,
+                     cudaStream_t stream) {
+  using Cfg = mimose_dev::GemmCfg<BN, EPI>;
   auto kern = mimose_dev::gemm_bf16_tn_kernel<BN, EPI>;
   static bool configured = false;
   if (!configured) {
@@ -88,19 +95,20 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb,
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<grid, mimose_dev::kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, p);
+  kern<<<grid, mimose_dev::kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 template <int BN>
 cudaError_t launch_bn(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+                      const CUtensorMap& td, const CUtensorMap& td2,
                       const mimose_dev::GemmParams& p, int grid, cudaStream_t s) {
   switch (epi) {
-    case kEpiBf16: return launch_t<BN, mimose_dev::kEpiBf16>(ta, tb, p, grid, s);
-    case kEpiBiasGelu: return launch_t<BN, mimose_dev::kEpiBiasGelu>(ta, tb, p, grid, s);
-    case kEpiDGelu: return launch_t<BN, mimose_dev::kEpiDGelu>(ta, tb, p, grid, s);
-    case kEpiF32: return launch_t<BN, mimose_dev::kEpiF32>(ta, tb, p, grid, s);
+    case kEpiBf16: return launch_t<BN, mimose_dev::kEpiBf16>(ta, tb, td, td2, p, grid, s);
+    case kEpiBiasGelu: return launch_t<BN, mimose_dev::kEpiBiasGelu>(ta, tb, td, td2, p, grid, s);
+    case kEpiDGelu: return launch_t<BN, mimose_dev::kEpiDGelu>(ta, tb, td, td2, p, grid, s);
+    case kEpiF32: return launch_t<BN, mimose_dev::kEpiF32>(ta, tb, td, td2, p, grid, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -115,7 +123,72 @@ int pick_bn(const GemmCall& c) {
   return 128;
 }
 
+// out[m][n] (ld) = sum_s ws[s][m][n] (+ beta * out), fixed summation order
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                     float* __restrict__ out, long long ldo, float beta) {
+  const long long total = (long long)M * N;
+  const bool v4 = (N % 4 == 0) && (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (v4) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4;
+         i += (long long)gridDim.x * blockDim.x) {
+      const long long e = i * 4;
+      const long long m = e / N, n = e % N;
+      float4 acc = reinterpret_cast<const float4*>(ws)[i];
+      for (int s = 1; s < splits; ++s) {
+        const float4 t = reinterpret_cast<const float4*>(ws + (long long)s * total)[i];
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      float4* o = reinterpret_cast<float4*>(out + m * ldo + n);
+      if (beta != 0.f) {
+        const float4 old = *o;
+        acc.x += beta * old.x; acc.y += beta * old.y; acc.z += beta * old.z; acc.w += beta * old.w;
+      }
+      *o = acc;
+    }
+  } else {
+    for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+      const long long m = e / N, n = e % N;
+      float acc = ws[e];
+      for (int s = 1; s < splits; ++s) acc += ws[(long long)s * total + e];
+      float* o = out + m * ldo + n;
+      *o = acc + (beta != 0.f ? beta * *o : 0.f);
+    }
+  }
+}
+
+// wave efficiency of `tiles` CTAs on the SMs
+double wave_eff(int64_t tiles) {
+  const int64_t sm = sm_count();
+  const int64_t waves = (tiles + sm - 1) / sm;
+  return (double)tiles / (double)(waves * sm);
+}
+
 }  // namespace
+
+int pick_split_k(int M, int N, int K, int bn) {
+  const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + bn - 1) / bn);
+  const int kb = (K + 63) / 64;
+  int best = 1;
+  double best_eff = wave_eff(tiles);
+  for (int s = 2; s <= 8; ++s) {
+    if (kb / s < 8) break;  // keep >= 8 k-blocks per split
+    const double e = wave_eff(tiles * s);
+    if (e > best_eff + 0.05) {
+      best = s;
+      best_eff = e;
+    }
+  }
+  return best;
+}
+
+int64_t splitk_workspace_bytes(int M, int N, int K) {
+  GemmCall c;
+  c.M = M; c.N = N; c.K = K; c.epi = kEpiF32;
+  const int bn = pick_bn(c);
+  int s = pick_split_k(M, N, K, bn);
+  return s > 1 ? (int64_t)s * M * N * 4 : 0;
+}
 
 uint64_t launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -126,6 +199,14 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   if ((reinterpret_cast<uintptr_t>(c.A.ptr) & 15) || (reinterpret_cast<uintptr_t>(c.B.ptr) & 15))
     return cudaErrorMisalignedAddress;
   const int bn = pick_bn(c);
+  int splits = 1;
+  if (c.epi == kEpiF32 && c.nb1 == 1 && c.nb2 == 1 && c.workspace != nullptr && c.split_k != 1 &&
+      c.N % 4 == 0 && (reinterpret_cast<uintptr_t>(c.workspace) & 15) == 0) {
+    splits = c.split_k > 1 ? c.split_k : pick_split_k(c.M, c.N, c.K, bn);
+    const int kb = (c.K + 63) / 64;
+    if (splits > kb) splits = kb;
+    while (splits > 1 && (int64_t)splits * c.M * c.N * 4 > c.workspace_bytes) --splits;
+  }
   CUtensorMap ta, tb;
   if (!make_map(&ta, c.A, c.nb1, c.nb2, c.a_mn ? 64u : 128u)) return cudaErrorInvalidValue;
   if (!make_map(&tb, c.B, c.nb1, c.nb2, c.b_mn ? 64u : (uint32_t)bn))
@@ -145,8 +226,44 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     p.vec = (c.ldo % vel == 0) && (c.obs1 % vel == 0) && (c.obs2 % vel == 0) && al(c.out) &&
             (c.out2 == nullptr || al(c.out2)) && (c.aux == nullptr || al(c.aux));
   }
+  {
+    // every split must own >= 1 k-block (an empty split would never signal
+    // its accumulator): recompute the split count from the per-split depth
+    const int kb = (c.K + 63) / 64;
+    const int kbps = (kb + splits - 1) / splits;
+    splits = (kb + kbps - 1) / kbps;
+    p.kb_per_split = kbps;
+  }
+  p.splits = splits;
+  // output through TMA when the view is addressable (16 B pitch / batch strides)
+  CUtensorMap td{}, td2{};
+  if (splits > 1) {
+    // partials: workspace viewed as [splits][M][N] fp32, split index = batch 1
+    // fp32 chunk: 32 columns (128 B) -- every tile width here has >= 128 B halves
+    if (!make_map_t(&td, c.workspace, c.M, c.N, c.N, (int64_t)c.M * c.N, 0, splits, 1, 32, 32, 4))
+      return cudaErrorInvalidValue;
+    p.tma_store = 1;
+    p.beta = 0.f;
+  } else {
+    const int esz = c.epi == kEpiF32 ? 4 : 2;
+    const int cb = (bn / 2) * esz >= 128 ? 128 : 64;  // GemmCfg::kChunkBytes
+    const uint32_t cw = cb / esz;
+    const bool sw64 = cb == 64;
+    auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    bool ok = !c.direct_store && !(c.epi == kEpiF32 && c.beta != 0.f) && al(c.out) &&
+              (c.ldo * esz) % 16 == 0 && (c.nb1 == 1 || (c.obs1 * esz) % 16 == 0) &&
+              (c.nb2 == 1 || (c.obs2 * esz) % 16 == 0) &&
+              (c.epi != kEpiBiasGelu || (c.out2 != nullptr && al(c.out2)));
+    ok = ok && make_map_t(&td, c.out, c.M, c.N, c.ldo, c.obs1, c.obs2, c.nb1, c.nb2, cw, 32, esz,
+                          sw64);
+    if (ok && c.epi == kEpiBiasGelu)
+      ok = make_map_t(&td2, c.out2, c.M, c.N, c.ldo, c.obs1, c.obs2, c.nb1, c.nb2, cw, 32, esz,
+                      sw64);
+    p.tma_store = ok ? 1 : 0;
+  }
 
-  const int64_t tiles = (int64_t)((c.M + 127) / 128) * ((c.N + bn - 1) / bn) * c.nb1 * c.nb2;
+  const int64_t tiles =
+      (int64_t)((c.M + 127) / 128) * ((c.N + bn - 1) / bn) * c.nb1 * c.nb2 * splits;
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
   std::pair<cudaEvent_t, cudaEvent_t>* pe = nullptr;
   if (g_prof.on) {
@@ -158,13 +275,25 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     }
     pe = &g_prof.ev[g_prof.used++];
     g_prof.flops.push_back(2.0 * c.M * (double)c.N * c.K * c.nb1 * c.nb2);
+    g_prof.desc.push_back(std::to_string(c.M) + "," + std::to_string(c.N) + "," +
+                          std::to_string(c.K) + "," + std::to_string(c.nb1 * c.nb2) + "," +
+                          std::to_string(bn) + "," + std::to_string((int)c.a_mn) + "," +
+                          std::to_string((int)c.b_mn) + "," + std::to_string(c.epi) + "," +
+                          std::to_string(grid));
     cudaEventRecord(pe->first, stream);
   }
   cudaError_t err = cudaErrorInvalidValue;
   switch (bn) {
-    case 64: err = launch_bn<64>(c.epi, ta, tb, p, grid, stream); break;
-    case 128: err = launch_bn<128>(c.epi, ta, tb, p, grid, stream); break;
-    case 256: err = launch_bn<256>(c.epi, ta, tb, p, grid, stream); break;
+    case 64: err = launch_bn<64>(c.epi, ta, tb, td, td2, p, grid, stream); break;
+    case 128: err = launch_bn<128>(c.epi, ta, tb, td, td2, p, grid, stream); break;
+    case 256: err = launch_bn<256>(c.epi, ta, tb, td, td2, p, grid, stream); break;
+  }
+  if (err == cudaSuccess && splits > 1) {
+    splitk_reduce_kernel<<<2 * sm_count(), 256, 0, stream>>>(
+        static_cast<const float*>(c.workspace), splits, c.M, c.N, static_cast<float*>(c.out),
+        c.ldo, c.beta);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    err = cudaGetLastError();
   }
   if (pe != nullptr) cudaEventRecord(pe->second, stream);
   return err;
@@ -174,6 +303,19 @@ void gemm_profile_enable(bool on) {
   g_prof.on = on;
   g_prof.used = 0;
   g_prof.flops.clear();
+  g_prof.desc.clear();
+}
+
+std::string gemm_profile_csv() {
+  std::string out = "M,N,K,batch,bn,a_mn,b_mn,epi,grid,ms,tflops\n";
+  for (size_t i = 0; i < g_prof.used; ++i) {
+    cudaEventSynchronize(g_prof.ev[i].second);
+    float m = 0.f;
+    cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second);
+    out += g_prof.desc[i] + "," + std::to_string(m) + "," +
+           std::to_string(m > 0 ? g_prof.flops[i] / (m * 1e-3) / 1e12 : 0.0) + "\n";
+  }
+  return out;
 }
 
 cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches) {

@@ -1,7 +1,8 @@
 // Persistent warp-specialised bf16 GEMM for sm_100a:
 //   TMA (128B-swizzled tiles) -> smem ring (mbarrier full/empty) ->
 //   tcgen05.mma (one elected thread, fp32 accumulators in TMEM, double
-//   buffered) -> tcgen05.ld epilogue (bias / GELU / dGELU / fp32 store).
+//   buffered) -> tcgen05.ld epilogue (bias / GELU / dGELU / residual / fp32)
+//   -> swizzled smem staging -> TMA bulk tensor store.
 //
 //   D[z][m][n] = sum_k A[z][m][k] * B[z][n][k]
 //
@@ -11,7 +12,10 @@
 // attention contraction (QK^T, PV, dO V^T, P^T dO, dS K, dS^T Q) without a
 // transpose pass. Batched operands are addressed through 4-D tensor maps
 // (cols, rows, batch1, batch2), so per-head views into the fused QKV buffer
-// need no copies.
+// need no copies. The output is written through a 4-D tensor map as well
+// (full 128-byte lines, clipped at the M/N edges by the TMA unit); views the
+// TMA cannot address (unaligned pitch, fp32 read-modify-write) fall back to
+// per-thread vector stores.
 #pragma once
 
 #include <cuda.h>
@@ -37,25 +41,42 @@ struct GemmParams {
   int a_mn, b_mn;           // operand majors (0 = K-major, 1 = MN-major)
   void* out;                // bf16 or f32 depending on epilogue
   void* out2;               // bf16 (GELU output)
-  const __nv_bfloat16* aux; // bf16, same addressing as out (dGELU input)
+  const __nv_bfloat16* aux; // bf16, same addressing as out (dGELU input / residual)
   const float* bias;        // [N] or nullptr
   long long ldo, obs1, obs2;  // output strides in elements
   float alpha, beta;
-  int vec;                  // 1 if 16-byte vector stores/loads are aligned
+  int vec;                  // 1 if 16-byte vector stores/loads are aligned (fallback path)
+  int tma_store;            // 1: stage through smem + TMA store
+  int splits;               // split-K factor (>1: fp32 partials, batch must be 1)
+  int kb_per_split;         // k-blocks per split
 };
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 192;  // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int kEpiWarps = 8;        // two warps per TMEM lane quarter (column halves)
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
+constexpr int kSmemBudget = 227 * 1024;
 
-template <int BN>
+template <int BN, int EPI>
 struct GemmCfg {
-  static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kNOut = EPI == kEpiBiasGelu ? 2 : 1;
+  static constexpr int kEsz = EPI == kEpiF32 ? 4 : 2;
+  // staged row chunk: 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B) when a warp's
+  // half-tile is narrower than 128 B
+  static constexpr int kChunkBytes = (BN / 2) * kEsz >= 128 ? 128 : 64;
+  static constexpr int kChunkCols = kChunkBytes / kEsz;
+  // per epilogue warp: 2 buffers of 32 rows x 128 B (double buffer, or the
+  // u / gelu(u) pair of the GELU epilogue)
+  static constexpr int kStagingBytes = kEpiWarps * 2 * 4096;
+  static constexpr int kStagesRaw =
+      (kSmemBudget - 1024 - 256 - kStagingBytes) / kStageBytes;
+  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmemBytes = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
+  static_assert(kStages >= 2, "not enough shared memory for a pipeline");
 };
 
 __device__ __forceinline__ float gelu_f(float x) {
@@ -67,18 +88,80 @@ __device__ __forceinline__ float dgelu_f(float x) {
   return cdf + x * pdf;
 }
 
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// Epilogue math on NV consecutive accumulator columns of one row (values in
+// v, first column col0). Results in v (and g for the GELU output).
+template <int EPI, int NV>
+__device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], const GemmParams& p,
+                                              long long obase, int col0, bool row_ok) {
+  if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu || EPI == kEpiF32) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] *= p.alpha;
+  }
+  if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
+    if (p.bias != nullptr) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+        if (col0 + i < p.N) v[i] += __ldg(p.bias + col0 + i);
+    }
+  }
+  if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
+    if (p.aux != nullptr && row_ok) {
+      const __nv_bfloat16* ax = p.aux + obase + col0;
+      if (p.vec && col0 + NV <= p.N) {
+#pragma unroll
+        for (int q = 0; q < NV / 8; ++q) {
+          const uint4 raw = *reinterpret_cast<const uint4*>(ax + 8 * q);
+          const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float a = __bfloat162float(av[i]);
+            if constexpr (EPI == kEpiBf16) v[8 * q + i] += a;
+            else v[8 * q + i] *= dgelu_f(a);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          if (col0 + i < p.N) {
+            const float a = __bfloat162float(ax[i]);
+            if constexpr (EPI == kEpiBf16) v[i] += a;
+            else v[i] *= dgelu_f(a);
+          }
+        }
+      }
+    }
+  }
+  if constexpr (EPI == kEpiBiasGelu) {
+    // GELU of the bf16-rounded pre-activation, so recompute and the saved u
+    // agree bit for bit with what backward differentiates.
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
+      g[i] = gelu_f(v[i]);
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
-                        const __grid_constant__ CUtensorMap tmB, const GemmParams p) {
-  using Cfg = GemmCfg<BN>;
+                        const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmD,
+                        const __grid_constant__ CUtensorMap tmD2, const GemmParams p) {
+  using Cfg = GemmCfg<BN, EPI>;
   constexpr int S = Cfg::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::kStageBytes);
+  uint8_t* sD = smem + S * Cfg::kStageBytes;  // epilogue staging (1024-aligned)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
@@ -90,19 +173,23 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int tiles_m = (p.M + kBM - 1) / kBM;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int tiles_per_batch = tiles_m * tiles_n;
-  const int num_tiles = tiles_per_batch * p.nb1 * p.nb2;
+  const int num_tiles = tiles_per_batch * p.nb1 * p.nb2 * p.splits;
   const int num_kb = (p.K + kBK - 1) / kBK;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (p.tma_store) {
+      tma_prefetch(&tmD);
+      if (EPI == kEpiBiasGelu) tma_prefetch(&tmD2);
+    }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -117,12 +204,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int it = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int z = tile / tiles_per_batch;
+        const int zz = tile / tiles_per_batch;
         const int t_in = tile % tiles_per_batch;
         const int m0 = (t_in % tiles_m) * kBM;
         const int n0 = (t_in / tiles_m) * BN;
+        const int split = zz % p.splits, z = zz / p.splits;
         const int b1 = z % p.nb1, b2 = z / p.nb1;
-        for (int kb = 0; kb < num_kb; ++kb, ++it) {
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
@@ -160,10 +250,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
+      const int split = (tile / tiles_per_batch) % p.splits;
+      const int kb_n = min(num_kb, (split + 1) * p.kb_per_split) - split * p.kb_per_split;
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < num_kb; ++kb, ++it) {
+      for (int kb = 0; kb < kb_n; ++kb, ++it) {
         const int s = it % S;
         const uint32_t ph = (it / S) & 1;
         mbar_wait(&full[s], ph);
@@ -178,21 +270,30 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             umma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
           umma_commit(&empty[s]);
-          if (kb == num_kb - 1) umma_commit(&tfull[acc]);
+          if (kb == kb_n - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
       }
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
-    int local = 0;
+    const int ew = warp - 2;            // epilogue warp 0..7
+    const int quarter = warp & 3;       // TMEM lane quarter this warp may access
+    const int half = ew >> 2;           // which half of the tile's columns
+    constexpr int CB = Cfg::kChunkBytes;
+    constexpr int CW = Cfg::kChunkCols;
+    constexpr int NCH = CB / 16;        // 16-byte chunks per staged row
+    uint8_t* wbuf = sD + ew * (2 * 4096);
+    int local = 0, chunk_seq = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
-      const int z = tile / tiles_per_batch;
+      const int zz = tile / tiles_per_batch;
       const int t_in = tile % tiles_per_batch;
       const int m0 = (t_in % tiles_m) * kBM;
       const int n0 = (t_in / tiles_m) * BN;
-      const int b1 = z % p.nb1, b2 = z / p.nb1;
+      const int split = zz % p.splits, z = zz / p.splits;
+      // split-K partials are addressed as batch index b1 = split of the workspace
+      const int b1 = p.splits > 1 ? split : z % p.nb1;
+      const int b2 = p.splits > 1 ? 0 : z / p.nb1;
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       mbar_wait(&tfull[acc], aph);
@@ -203,111 +304,128 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const long long obase = (long long)b2 * p.obs2 + (long long)b1 * p.obs1 +
                               (long long)row * p.ldo;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+      const int c_begin = half * (BN / 2), c_end = c_begin + BN / 2;
 
+      if (p.tma_store) {
+        // ---- staged path: TMEM -> regs -> swizzled smem -> TMA store
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        __syncwarp();
-        tmem_ld16(t_row + c, v);
-        const int col0 = n0 + c;
-        if (row_ok && col0 < p.N) {
-        const bool full16 = p.vec && col0 + 16 <= p.N;
-        if constexpr (EPI == kEpiF32) {
-          float* o = reinterpret_cast<float*>(p.out) + obase + col0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
-          if (full16) {
-            float4* o4 = reinterpret_cast<float4*>(o);
-            if (p.beta != 0.f) {
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                float4 old = o4[q];
-                v[4 * q + 0] += p.beta * old.x;
-                v[4 * q + 1] += p.beta * old.y;
-                v[4 * q + 2] += p.beta * old.z;
-                v[4 * q + 3] += p.beta * old.w;
-              }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-          } else {
-            for (int i = 0; i < 16 && col0 + i < p.N; ++i)
-              o[i] = v[i] + (p.beta != 0.f ? p.beta * o[i] : 0.f);
+        for (int c = c_begin; c < c_end; c += CW, ++chunk_seq) {
+          if (n0 + c >= p.N) break;
+          uint8_t* sb = wbuf + (Cfg::kNOut == 1 ? (chunk_seq & 1) * 4096 : 0);
+          if (lane == 0) {
+            if constexpr (Cfg::kNOut == 1) bulk_wait_read<1>();  // this buffer's last store read it
+            else bulk_wait_read<0>();
           }
-        } else {
-          if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
+          __syncwarp();
+          float v[CW], g[CW];
+          {
+            uint32_t r[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
-            if (p.bias != nullptr) {
-              if (full16) {
+            for (int h = 0; h < CW / 32; ++h) {
+              tmem_ld32_nowait(t_row + c + 32 * h, r);
+              tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += __ldg(p.bias + col0 + i);
-              } else {
-                for (int i = 0; i < 16 && col0 + i < p.N; ++i) v[i] += __ldg(p.bias + col0 + i);
-              }
+              for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(r[i]);
             }
           }
-          if constexpr (EPI == kEpiBf16) {
-            // optional residual: out = alpha*acc + bias + aux (gradient sums)
-            if (p.aux != nullptr) {
-              const __nv_bfloat16* ax = p.aux + obase + col0;
-              if (full16) {
-                const uint4* a4 = reinterpret_cast<const uint4*>(ax);
-                uint4 raw[2] = {a4[0], a4[1]};
-                const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(raw);
+          epilogue_math<EPI, CW>(v, g, p, obase, n0 + c, row_ok);
+          const uint32_t rbase = smem_u32(sb) + lane * CB;
+          const uint32_t sw = CB == 128 ? (lane & 7) : ((lane >> 1) & 3);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] += __bfloat162float(av[i]);
-              } else {
-                for (int i = 0; i < 16 && col0 + i < p.N; ++i) v[i] += __bfloat162float(ax[i]);
-              }
-            }
-          }
-          if constexpr (EPI == kEpiDGelu) {
-            const __nv_bfloat16* ax = p.aux + obase + col0;
-            if (full16) {
-              const uint4* a4 = reinterpret_cast<const uint4*>(ax);
-              uint4 raw[2] = {a4[0], a4[1]};
-              const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(raw);
-#pragma unroll
-              for (int i = 0; i < 16; ++i) v[i] *= dgelu_f(__bfloat162float(av[i]));
+          for (int j = 0; j < NCH; ++j) {
+            const uint32_t addr = rbase + ((j ^ sw) << 4);
+            if constexpr (EPI == kEpiF32) {
+              st_shared_v4(addr, __float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                           __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
             } else {
-              for (int i = 0; i < 16 && col0 + i < p.N; ++i)
-                v[i] *= dgelu_f(__bfloat162float(ax[i]));
+              st_shared_v4(addr, pack_bf16x2(v[8 * j], v[8 * j + 1]),
+                           pack_bf16x2(v[8 * j + 2], v[8 * j + 3]),
+                           pack_bf16x2(v[8 * j + 4], v[8 * j + 5]),
+                           pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
+            }
+            if constexpr (EPI == kEpiBiasGelu) {
+              st_shared_v4(addr + 4096, pack_bf16x2(g[8 * j], g[8 * j + 1]),
+                           pack_bf16x2(g[8 * j + 2], g[8 * j + 3]),
+                           pack_bf16x2(g[8 * j + 4], g[8 * j + 5]),
+                           pack_bf16x2(g[8 * j + 6], g[8 * j + 7]));
             }
           }
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + obase + col0;
-          alignas(16) __nv_bfloat16 hv[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(v[i]);
-          if (full16) {
-            uint4* o4 = reinterpret_cast<uint4*>(o);
-            o4[0] = reinterpret_cast<const uint4*>(hv)[0];
-            o4[1] = reinterpret_cast<const uint4*>(hv)[1];
-          } else {
-            for (int i = 0; i < 16 && col0 + i < p.N; ++i) o[i] = hv[i];
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmD, sb, n0 + c, m0 + quarter * 32, b1, b2);
+            if constexpr (EPI == kEpiBiasGelu)
+              tma_store_4d(&tmD2, sb + 4096, n0 + c, m0 + quarter * 32, b1, b2);
+            bulk_commit();
           }
-          if constexpr (EPI == kEpiBiasGelu) {
-            // GELU of the bf16-rounded pre-activation, so recompute and the
-            // saved u agree bit for bit with what backward differentiates.
+        }
+      } else {
+        // ---- fallback: per-thread vector stores (pitch not TMA-addressable)
+#pragma unroll 1
+        for (int c = c_begin; c < c_end; c += 16) {
+          float v[16], g[16];
+          __syncwarp();
+          tmem_ld16(t_row + c, v);
+          const int col0 = n0 + c;
+          if (row_ok && col0 < p.N) {
+            const bool full16 = p.vec && col0 + 16 <= p.N;
+            if constexpr (EPI == kEpiF32) {
+              float* o = reinterpret_cast<float*>(p.out) + obase + col0;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(gelu_f(__bfloat162float(hv[i])));
-            __nv_bfloat16* o2 = reinterpret_cast<__nv_bfloat16*>(p.out2) + obase + col0;
-            if (full16) {
-              uint4* o4 = reinterpret_cast<uint4*>(o2);
-              o4[0] = reinterpret_cast<const uint4*>(hv)[0];
-              o4[1] = reinterpret_cast<const uint4*>(hv)[1];
+              for (int i = 0; i < 16; ++i) v[i] *= p.alpha;
+              if (full16) {
+                float4* o4 = reinterpret_cast<float4*>(o);
+                if (p.beta != 0.f) {
+#pragma unroll
+                  for (int q = 0; q < 4; ++q) {
+                    float4 old = o4[q];
+                    v[4 * q + 0] += p.beta * old.x;
+                    v[4 * q + 1] += p.beta * old.y;
+                    v[4 * q + 2] += p.beta * old.z;
+                    v[4 * q + 3] += p.beta * old.w;
+                  }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+              } else {
+                for (int i = 0; i < 16 && col0 + i < p.N; ++i)
+                  o[i] = v[i] + (p.beta != 0.f ? p.beta * o[i] : 0.f);
+              }
             } else {
-              for (int i = 0; i < 16 && col0 + i < p.N; ++i) o2[i] = hv[i];
+              epilogue_math<EPI, 16>(v, g, p, obase, col0, row_ok);
+              __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + obase + col0;
+              alignas(16) __nv_bfloat16 hv[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(v[i]);
+              if (full16) {
+                uint4* o4 = reinterpret_cast<uint4*>(o);
+                o4[0] = reinterpret_cast<const uint4*>(hv)[0];
+                o4[1] = reinterpret_cast<const uint4*>(hv)[1];
+              } else {
+                for (int i = 0; i < 16 && col0 + i < p.N; ++i) o[i] = hv[i];
+              }
+              if constexpr (EPI == kEpiBiasGelu) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) hv[i] = __float2bfloat16_rn(g[i]);
+                __nv_bfloat16* o2 = reinterpret_cast<__nv_bfloat16*>(p.out2) + obase + col0;
+                if (full16) {
+                  uint4* o4 = reinterpret_cast<uint4*>(o2);
+                  o4[0] = reinterpret_cast<const uint4*>(hv)[0];
+                  o4[1] = reinterpret_cast<const uint4*>(hv)[1];
+                } else {
+                  for (int i = 0; i < 16 && col0 + i < p.N; ++i) o2[i] = hv[i];
+                }
+              }
             }
           }
         }
-        }  // row_ok && col0 < N
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
+    if (p.tma_store && lane == 0) bulk_wait<0>();
   }
 
   __syncthreads();

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 namespace mimose_ops {
 
@@ -35,11 +36,22 @@ struct GemmCall {
   int64_t ldo = 0, obs1 = 0, obs2 = 0;
   float alpha = 1.f, beta = 0.f;
   int force_bn = 0;  // 0 = heuristic; 64/128/256 for tests
+  bool direct_store = false;  // tests: force the per-thread store epilogue
+  // deterministic split-K for fp32 (weight-gradient) outputs: partials go to
+  // `workspace` ([splits][M][N] fp32) and are summed in a fixed order.
+  // split_k: 0 = automatic when a workspace is given, 1 = off, >1 forced.
+  int split_k = 0;
+  void* workspace = nullptr;
+  int64_t workspace_bytes = 0;
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);
+// split-K choice for an fp32 (weight-gradient) GEMM and the workspace it needs
+int pick_split_k(int M, int N, int K, int bn);
+int64_t splitk_workspace_bytes(int M, int N, int K);
 void gemm_profile_enable(bool on);
 cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches);
+std::string gemm_profile_csv();
 
 // Number of kernels launched by this module since process start (telemetry
 // for the bench's gpu_launches count).

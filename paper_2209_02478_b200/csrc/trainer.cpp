@@ -96,7 +96,9 @@ GemmCall dgrad_call(const void* dY, const void* W, int64_t T, int N, int K, void
   return c;
 }
 
-// dW[N,K] (fp32) = dY[T,N]^T X[T,K]
+// dW[N,K] (fp32) = dY[T,N]^T X[T,K]; split-K over T into `ws` when it helps
+void* g_wgrad_ws = nullptr;
+int64_t g_wgrad_ws_bytes = 0;
 GemmCall wgrad_call(const void* dY, const void* X, int64_t T, int N, int K, float* dW) {
   GemmCall c;
   c.M = N;
@@ -109,6 +111,8 @@ GemmCall wgrad_call(const void* dY, const void* X, int64_t T, int N, int K, floa
   c.epi = mimose_ops::kEpiF32;
   c.out = dW;
   c.ldo = K;
+  c.workspace = g_wgrad_ws;
+  c.workspace_bytes = g_wgrad_ws_bytes;
   return c;
 }
 
@@ -189,6 +193,16 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   col_partial_ =
       static_cast<float*>(take((int64_t)mimose_ops::colsum_row_blocks((int)Tmax) * widest * 4 + 1024, kTagOther));
   norm_partial_ = static_cast<float*>(take((int64_t)mimose_ops::sumsq_blocks() * 4, kTagOther));
+  {
+    // split-K workspace for the weight-gradient GEMMs (largest need over the shapes)
+    const int h = H_, f = F_;
+    int64_t ws = 0;
+    const int shapes[4][2] = {{h, f}, {f, h}, {3 * h, h}, {h, h}};
+    for (const auto& sh : shapes)
+      ws = std::max(ws, mimose_ops::splitk_workspace_bytes(sh[0], sh[1], (int)Tmax));
+    wgrad_ws_bytes_ = ws;
+    wgrad_ws_ = ws > 0 ? take(ws, kTagOther) : nullptr;
+  }
   norm2_ = static_cast<float*>(take(4, kTagOther));
   d_loss_ = static_cast<float*>(take(4, kTagOther));
   d_logits_ = static_cast<float*>(take((int64_t)t.batch * 4, kTagOther));
@@ -728,6 +742,8 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     r->predicted_kept = constant_bytes_;  // informational only
 
   ctx_->arena.reset_peak();
+  g_wgrad_ws = wgrad_ws_;
+  g_wgrad_ws_bytes = wgrad_ws_bytes_;
 
   // ---- embeddings
   void* z0 = take(T * H * 2, kTagAct);

@@ -138,6 +138,8 @@ class Trainer {
   float* col_partial_ = nullptr;
   float* norm_partial_ = nullptr;
   float* norm2_ = nullptr;
+  void* wgrad_ws_ = nullptr;  // split-K partials of the weight-gradient GEMMs
+  int64_t wgrad_ws_bytes_ = 0;
   float* d_loss_ = nullptr;
   float* d_logits_ = nullptr;
   float* h_loss_ = nullptr;  // pinned

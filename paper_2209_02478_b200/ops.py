@@ -36,7 +36,8 @@ def _view(t: torch.Tensor, nb1: int, nb2: int):
 
 
 def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None, bias=None,
-         alpha=1.0, beta=0.0, force_bn=0, stream=None):
+         alpha=1.0, beta=0.0, force_bn=0, direct_store=False, split_k=1,
+         workspace=None, stream=None):
     """out[z] = alpha * op(a)[z] @ op(b)[z]^T with the kernel's epilogue.
 
     a: [.., M, K] (a_mn False) or [.., K, M] (a_mn True); b: [.., N, K] or [.., K, N].
@@ -65,6 +66,11 @@ def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None
     args.obs2 = out.stride(0) if out.dim() == 4 else 0
     args.alpha, args.beta = alpha, beta
     args.force_bn = force_bn
+    args.direct_store = int(direct_store)
+    args.split_k = split_k
+    if workspace is not None:
+        args.workspace = workspace.data_ptr()
+        args.workspace_bytes = workspace.numel() * workspace.element_size()
     lib = cuda_lib()
     check(lib.mimose_gemm(C.byref(args), _stream(stream)))
     return out

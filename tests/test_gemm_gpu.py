@@ -37,11 +37,12 @@ def _rand(*shape, dev="cuda"):
     return torch.randn(*shape, device=dev).to(torch.bfloat16)
 
 
+@pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("bn", [64, 128, 256])
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 256, 128), (200, 72, 80), (1000, 770, 768), (128, 2304, 64)])
-def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape):
+def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct):
     ops = _ops()
     torch.manual_seed(0)
     M, N, K = shape
@@ -52,13 +53,14 @@ def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape):
     if (a_arg.stride(0) * 2) % 16 or (b_arg.stride(0) * 2) % 16:
         pytest.skip("TMA needs 16-byte row pitch")
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn)
+    ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn, direct_store=direct)
     torch.cuda.synchronize()
     _check_bf16(out, A.float() @ B.float().t())
 
 
+@pytest.mark.parametrize("beta", [0.0, 0.5])
 @pytest.mark.parametrize("bn", [128, 256])
-def test_gemm_f32_beta(cuda_device, bn):
+def test_gemm_f32_beta(cuda_device, bn, beta):
     ops = _ops()
     torch.manual_seed(1)
     M, N, K = 768, 3072, 4096
@@ -66,16 +68,17 @@ def test_gemm_f32_beta(cuda_device, bn):
     dY = _rand(K, M)  # [T, N_out]
     X = _rand(K, N)   # [T, K_in]
     out = torch.randn(M, N, device="cuda")
-    ref = out * 0.5 + dY.float().t() @ X.float()
-    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, beta=0.5, force_bn=bn)
+    ref = out * beta + dY.float().t() @ X.float()
+    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, beta=beta, force_bn=bn)
     torch.cuda.synchronize()
     _check_f32(out, ref, K)
 
 
-def test_gemm_bias_gelu_and_dgelu(cuda_device):
+@pytest.mark.parametrize("M", [517, 1024])
+def test_gemm_bias_gelu_and_dgelu(cuda_device, M):
     ops = _ops()
     torch.manual_seed(2)
-    M, N, K = 517, 3072, 768
+    N, K = 3072, 768
     X = _rand(M, K)
     W = _rand(N, K) * 0.05
     bias = torch.randn(N, device="cuda")
@@ -136,3 +139,36 @@ def test_gemm_attention_views(cuda_device, S):
     ops.gemm(Pbuf[..., :S], dO, dV, a_mn=True, b_mn=True)
     torch.cuda.synchronize()
     _check_bf16(dV, P.float().transpose(-1, -2) @ dO.float())
+
+
+def test_gemm_residual_aux_add(cuda_device):
+    """bf16 epilogue with a residual: out = A B^T + aux (gradient sums)."""
+    ops = _ops()
+    torch.manual_seed(4)
+    M, N, K = 700, 768, 3072
+    A = _rand(M, K)
+    B = _rand(N, K) * 0.05
+    aux = _rand(M, N)
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    ops.gemm(A, B, out, aux=aux)
+    torch.cuda.synchronize()
+    _check_bf16(out, A.float() @ B.float().t() + aux.float())
+
+
+@pytest.mark.parametrize("split", [0, 2, 4, 7])
+@pytest.mark.parametrize("shape", [(768, 768, 18432), (2304, 768, 4096), (104, 200, 1000)])
+def test_gemm_wgrad_split_k(cuda_device, split, shape):
+    """Deterministic split-K (fp32 partials + fixed-order reduce) for weight grads."""
+    ops = _ops()
+    torch.manual_seed(5)
+    M, N, K = shape
+    dY = _rand(K, M)
+    X = _rand(K, N)
+    ws = torch.empty(8 * M * N, device="cuda")
+    out = torch.empty(M, N, device="cuda")
+    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, split_k=split, workspace=ws)
+    out2 = torch.empty_like(out)
+    ops.gemm(dY, X, out2, a_mn=True, b_mn=True, epi=ops.EPI_F32, split_k=split, workspace=ws)
+    torch.cuda.synchronize()
+    _check_f32(out, dY.float().t() @ X.float(), K)
+    assert torch.equal(out, out2)  # run-to-run bitwise
