@@ -68,9 +68,9 @@ struct GemmCfg {
   // half-tile is narrower than 128 B
   static constexpr int kChunkBytes = (BN / 2) * kEsz >= 128 ? 128 : 64;
   static constexpr int kChunkCols = kChunkBytes / kEsz;
-  // per epilogue warp: 2 buffers of 32 rows x 128 B (double buffer, or the
-  // u / gelu(u) pair of the GELU epilogue)
-  static constexpr int kStagingBytes = kEpiWarps * 2 * 4096;
+  // per epilogue warp: kNOut buffers of 32 rows x 128 B (single-buffered:
+  // the TMA store drains 4 KB from smem long before the next chunk is ready)
+  static constexpr int kStagingBytes = kEpiWarps * kNOut * 4096;
   static constexpr int kStagesRaw =
       (kSmemBudget - 1024 - 256 - kStagingBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     constexpr int CB = Cfg::kChunkBytes;
     constexpr int CW = Cfg::kChunkCols;
     constexpr int NCH = CB / 16;        // 16-byte chunks per staged row
-    uint8_t* wbuf = sD + ew * (2 * 4096);
+    uint8_t* wbuf = sD + ew * (Cfg::kNOut * 4096);
     int local = 0, chunk_seq = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int zz = tile / tiles_per_batch;
@@ -311,11 +311,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
         for (int c = c_begin; c < c_end; c += CW, ++chunk_seq) {
           if (n0 + c >= p.N) break;
-          uint8_t* sb = wbuf + (Cfg::kNOut == 1 ? (chunk_seq & 1) * 4096 : 0);
-          if (lane == 0) {
-            if constexpr (Cfg::kNOut == 1) bulk_wait_read<1>();  // this buffer's last store read it
-            else bulk_wait_read<0>();
-          }
+          uint8_t* sb = wbuf;
+          if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
           __syncwarp();
           float v[CW], g[CW];
           {

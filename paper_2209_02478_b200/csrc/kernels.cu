@@ -270,46 +270,67 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restr
 
 // =====================================================================
 // scaled softmax + dropout over rows of S (row pitch ld, ld % 8 == 0)
+//
+// A group of L lanes owns one row (32 / L rows per warp); every lane issues
+// all of its MAXC 16-byte loads before reducing, so each thread keeps up to
+// MAXC loads in flight (rows here are only S <= 2048 elements long, one
+// warp per row would leave most of the HBM pipe idle).
 // =====================================================================
-template <int MAXV>
+template <int L>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int L>
+__device__ __forceinline__ float group_max(float v) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int L, int MAXC>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict__ s_in,
                                                           bf16* __restrict__ p_out,
                                                           bf16* __restrict__ pd_out, int64_t rows,
                                                           int S, int ld, DropoutCfg drop) {
+  constexpr int R = 32 / L;
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  const bf16* in = s_in + row * ld;
-  float v[MAXV][8];
+  const int sub = lane % L;
+  const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
+  const bool live = row < rows;
+  const bf16* in = s_in + (live ? row : 0) * ld;
+  float v[MAXC][8];
   float mx = -INFINITY;
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int j0 = 8 * (lane + 32 * c);
-    if (j0 < S) {
-      load8(in + j0, v[c]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (j0 + e >= S) v[c][e] = -INFINITY;
-        mx = fmaxf(mx, v[c][e]);
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) v[c][e] = -INFINITY;
-    }
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
+    if (live && j0 < S) load8(in + j0, v[c]);
   }
-  mx = warp_max(mx);
-  float sum = 0.f;
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c)
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      v[c][e] = __expf(v[c][e] - mx);
+      if (!live || j0 + e >= S) v[c][e] = -INFINITY;
+      mx = fmaxf(mx, v[c][e]);
+    }
+  }
+  mx = group_max<L>(mx);
+  float sum = 0.f;
+  const float mxl = mx * 1.4426950408889634f;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      v[c][e] = exp2f(v[c][e] * 1.4426950408889634f - mxl);
       sum += v[c][e];
     }
-  const float inv = 1.f / warp_sum(sum);
+  const float inv = 1.f / group_sum<L>(sum);
+  if (!live) return;
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int j0 = 8 * (lane + 32 * c);
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
     if (j0 >= ld) continue;
     float p[8], pd[8];
     const uint32_t m = dropout_mask8(drop, (uint64_t)row * ld + j0);
@@ -324,43 +345,49 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
 }
 
 // dS = P * (dP - sum_j dP_j P_j) * scale,  dP = dPd * mask * (1/(1-p)); in place over dPd
-template <int MAXV>
+template <int L, int MAXC>
 __global__ void __launch_bounds__(256) softmax_bwd_kernel(const bf16* __restrict__ P,
                                                           bf16* __restrict__ dpd, int64_t rows,
                                                           int S, int ld, DropoutCfg drop,
                                                           float scale) {
+  constexpr int R = 32 / L;
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  float p[MAXV][8], dp[MAXV][8];
-  float dot = 0.f;
+  const int sub = lane % L;
+  const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
+  const bool live = row < rows;
+  const int64_t base = (live ? row : 0) * ld;
+  float p[MAXC][8], dp[MAXC][8];
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int j0 = 8 * (lane + 32 * c);
-    if (j0 < S) {
-      load8(P + row * ld + j0, p[c]);
-      load8(dpd + row * ld + j0, dp[c]);
-      const uint32_t m = dropout_mask8(drop, (uint64_t)row * ld + j0);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        dp[c][e] = ((m >> e) & 1u) ? dp[c][e] * drop.scale : 0.f;
-        if (j0 + e >= S) p[c][e] = 0.f;
-        dot += dp[c][e] * p[c][e];
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) p[c][e] = dp[c][e] = 0.f;
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
+    if (live && j0 < S) {
+      load8(P + base + j0, p[c]);
+      load8(dpd + base + j0, dp[c]);
     }
   }
-  dot = warp_sum(dot);
+  float dot = 0.f;
 #pragma unroll
-  for (int c = 0; c < MAXV; ++c) {
-    const int j0 = 8 * (lane + 32 * c);
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
+    const uint32_t m = (live && j0 < S) ? dropout_mask8(drop, (uint64_t)row * ld + j0) : 0u;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const bool in = live && j0 + e < S;
+      dp[c][e] = (in && ((m >> e) & 1u)) ? dp[c][e] * drop.scale : 0.f;
+      p[c][e] = in ? p[c][e] : 0.f;
+      dot += dp[c][e] * p[c][e];
+    }
+  }
+  dot = group_sum<L>(dot);
+  if (!live) return;
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
     if (j0 >= ld) continue;
     float ds[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) ds[e] = p[c][e] * (dp[c][e] - dot) * scale;
-    store8(dpd + row * ld + j0, ds);
+    store8(dpd + base + j0, ds);
   }
 }
 
@@ -528,19 +555,40 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     const float nrm = sqrtf(norm2[0]);
     clip = fminf(1.f, a.max_grad_norm / (nrm * a.grad_scale + 1e-6f));
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+  const float gs = clip * a.grad_scale;
+  // n and n_decay are multiples of 4 (64-element aligned parameter tensors)
+  const int64_t n4 = n / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const float gi = g[i] * clip * a.grad_scale;
-    float pi = p[i];
-    if (i < n_decay) pi -= a.lr * a.weight_decay * pi;
-    const float mi = a.beta1 * m[i] + (1.f - a.beta1) * gi;
-    const float vi = a.beta2 * v[i] + (1.f - a.beta2) * gi * gi;
-    m[i] = mi;
-    v[i] = vi;
-    const float mh = mi / a.bc1, vh = vi / a.bc2;
-    pi -= a.lr * mh / (sqrtf(vh) + a.eps);
-    p[i] = pi;
-    p16[i] = __float2bfloat16_rn(pi);
+    float4 pv = reinterpret_cast<const float4*>(p)[i];
+    float4 mv = reinterpret_cast<const float4*>(m)[i];
+    float4 vv = reinterpret_cast<const float4*>(v)[i];
+    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    const bool decay = 4 * i < n_decay;
+    float* pp = &pv.x;
+    float* mp = &mv.x;
+    float* vp = &vv.x;
+    const float* gp = &gv.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float gi = gp[k] * gs;
+      float pi = pp[k];
+      if (decay) pi -= a.lr * a.weight_decay * pi;
+      const float mi = a.beta1 * mp[k] + (1.f - a.beta1) * gi;
+      const float vi = a.beta2 * vp[k] + (1.f - a.beta2) * gi * gi;
+      mp[k] = mi;
+      vp[k] = vi;
+      pi -= a.lr * (mi / a.bc1) / (sqrtf(vi / a.bc2) + a.eps);
+      pp[k] = pi;
+    }
+    reinterpret_cast<float4*>(p)[i] = pv;
+    reinterpret_cast<float4*>(m)[i] = mv;
+    reinterpret_cast<float4*>(v)[i] = vv;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(pv.x, pv.y), hi = __floats2bfloat162_rn(pv.z, pv.w);
+    uint2 packed;
+    packed.x = *reinterpret_cast<uint32_t*>(&lo);
+    packed.y = *reinterpret_cast<uint32_t*>(&hi);
+    reinterpret_cast<uint2*>(p16)[i] = packed;
   }
 }
 
@@ -675,16 +723,31 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
   return cudaGetLastError();
 }
 
+template <int L, int MAXC>
+static void softmax_fwd_t(const bf16* in, bf16* p, bf16* pd, int64_t rows, int S, int ld,
+                          const mimose_dev::DropoutCfg& d, cudaStream_t s) {
+  const int64_t rows_per_block = 8 * (32 / L);
+  const int g = (int)((rows + rows_per_block - 1) / rows_per_block);
+  mimose_dev::softmax_fwd_kernel<L, MAXC><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+}
+template <int L, int MAXC>
+static void softmax_bwd_t(const bf16* p, bf16* dp, int64_t rows, int S, int ld,
+                          const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
+  const int64_t rows_per_block = 8 * (32 / L);
+  const int g = (int)((rows + rows_per_block - 1) / rows_per_block);
+  mimose_dev::softmax_bwd_kernel<L, MAXC><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+}
+
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, cudaStream_t s) {
-  const int g = (int)((rows + 7) / 8);
   auto in = static_cast<const bf16*>(scores);
   auto p = static_cast<bf16*>(P);
   auto pd = static_cast<bf16*>(Pd);
-  if (ld <= 256) mimose_dev::softmax_fwd_kernel<1><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
-  else if (ld <= 512) mimose_dev::softmax_fwd_kernel<2><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
-  else if (ld <= 1024) mimose_dev::softmax_fwd_kernel<4><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
-  else if (ld <= 2048) mimose_dev::softmax_fwd_kernel<8><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  if (ld <= 128) softmax_fwd_t<8, 2>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 256) softmax_fwd_t<8, 4>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 512) softmax_fwd_t<8, 8>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 1024) softmax_fwd_t<16, 8>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 2048) softmax_fwd_t<32, 8>(in, p, pd, rows, S, ld, d, s);
   else return cudaErrorInvalidValue;
   count_launch();
   return cudaGetLastError();
@@ -692,13 +755,13 @@ cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int
 
 cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
-  const int g = (int)((rows + 7) / 8);
   auto p = static_cast<const bf16*>(P);
   auto dp = static_cast<bf16*>(dPd);
-  if (ld <= 256) mimose_dev::softmax_bwd_kernel<1><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
-  else if (ld <= 512) mimose_dev::softmax_bwd_kernel<2><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
-  else if (ld <= 1024) mimose_dev::softmax_bwd_kernel<4><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
-  else if (ld <= 2048) mimose_dev::softmax_bwd_kernel<8><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  if (ld <= 128) softmax_bwd_t<8, 2>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 256) softmax_bwd_t<8, 4>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 512) softmax_bwd_t<8, 8>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 1024) softmax_bwd_t<16, 8>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 2048) softmax_bwd_t<32, 8>(p, dp, rows, S, ld, d, scale, s);
   else return cudaErrorInvalidValue;
   count_launch();
   return cudaGetLastError();
