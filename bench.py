@@ -345,34 +345,42 @@ def run_gpu_arm(args, rank, world, local):
     achieved_tflops = fl.value / (gms.value / 1000.0) / 1e12 if gms.value > 0 else 0.0
     peak_tf = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)))
 
-    # 4. e2e: public API with HOST (pinned) inputs, H2D + loss D2H inside the region
-    e2e_batches = batches(seqs[calib + n_total + 2:calib + 2 * n_total + 2], args.seed + 5)
+    # 4. e2e: public API with HOST (pinned) inputs, H2D + loss D2H inside the region.
+    #    N=1: mimose_trainer_step_async + mimose_trainer_loss with a one-step lag
+    #    (the host issues step i+1 while step i runs; every step's loss is read
+    #    back inside the timed region). N>1: forward_backward + all-reduce + AdamW.
+    e2e_batches = batches(run_seqs, args.seed + 5)  # same sizes as the device-resident run
     pinned = [tuple(torch.from_numpy(a).pin_memory() for a in b) for b in e2e_batches]
-    h2d = 0
-    for b in pinned[:args.warmup]:
-        tr.step_pinned(*b, stream=stream) if world == 1 else None
-    # N>1: forward_backward + allreduce + optimizer through the same public calls
-    def e2e_one(b):
+    losses = []
+
+    def e2e_run(group):
         if world == 1:
-            tr.step_pinned(*b, stream=stream)
+            prev = None
+            for b in group:
+                row = tr.step_async(*b, stream=stream)
+                if prev is not None:
+                    losses.append(tr.loss(prev))
+                prev = row["iter"]
+            if prev is not None:
+                losses.append(tr.loss(prev))
         else:
-            tr.step_pinned(*b, optimizer=False, stream=stream)
             import torch.distributed as dist
-            dist.all_reduce(tr.grads())
-            tr.optimizer_step(1.0 / world, stream=stream)
-    if world > 1:
-        for b in pinned[:args.warmup]:
-            e2e_one(b)
+            for b in group:
+                row = tr.step_pinned(*b, optimizer=False, stream=stream)
+                dist.all_reduce(tr.grads())
+                tr.optimizer_step(1.0 / world, stream=stream)
+                losses.append(row["loss"])
+
+    e2e_run(pinned[:args.warmup])
     torch.cuda.synchronize()
     barrier(world)
     t0 = time.perf_counter()
-    for b in pinned[args.warmup:]:
-        e2e_one(b)
-        h2d += sum(x.numel() * 4 for x in b)
+    e2e_run(pinned[args.warmup:])
     torch.cuda.synchronize()
     e2e_s = allmax(time.perf_counter() - t0, world)
     e2e_value = samples / e2e_s
-    h2d_per_step = h2d // args.steps  # tokens + types + labels (token tables are built on host)
+    h2d_per_step = sum(x.numel() * 4 for b in pinned[args.warmup:] for x in b) // args.steps
+    host_ms = [r["host_ms"] for r in tr.rows[-args.steps:]]
 
     # 5. no-checkpoint, unlimited-memory throughput on the same size stream
     nock = None
@@ -420,7 +428,12 @@ def run_gpu_arm(args, rank, world, local):
                          "gemm_launches": gl.value, "peak_kind": pk_kind + " sustained"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_per_step,
-                    "d2h_bytes_per_step": 4},
+                    "d2h_bytes_per_step": 4,
+                    "api": "mimose_trainer_step_async + mimose_trainer_loss (1-step lag)"
+                    if world == 1 else "mimose_trainer_forward_backward + NCCL all-reduce + "
+                                       "mimose_trainer_optimizer_step",
+                    "host_ms_per_step": sum(host_ms) / len(host_ms),
+                    "losses_finite": all(l == l for l in losses)},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
             "mimose": {

@@ -168,6 +168,7 @@ typedef struct {
   double pred_err_mean;        /* |predict(l,x) - measured a_l(x)| / measured, kept blocks */
   double pred_err_max;
   int pred_layers;             /* kept blocks the error was measured on */
+  double host_ms;              /* host wall time spent issuing this step's work */
 } mimose_step_report;
 
 typedef void (*mimose_grad_hook)(void* user, float* grads, int64_t n, void* stream);
@@ -181,7 +182,14 @@ int mimose_trainer_destroy(mimose_trainer* tr);
 int mimose_trainer_step(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
                         const int32_t* labels, int batch, int seq, void* stream,
                         mimose_step_report* rep);
-/* Same, without the optimizer (gradients left in the flat grad buffer). */
+/* Pipelined variant: same work, but the loss read-back is left in flight
+ * (pinned ring of 4); fetch it with mimose_trainer_loss. Lets the host issue
+ * step i+1 while step i runs. */
+int mimose_trainer_step_async(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                              const int32_t* labels, int batch, int seq, void* stream,
+                              mimose_step_report* rep);
+int mimose_trainer_loss(mimose_trainer* tr, int64_t iter, float* loss);
+/* Same as mimose_trainer_step, without the optimizer (gradients left in the flat grad buffer). */
 int mimose_trainer_forward_backward(mimose_trainer* tr, const int32_t* tokens,
                                     const int32_t* types, const int32_t* labels, int batch,
                                     int seq, void* stream, mimose_step_report* rep);

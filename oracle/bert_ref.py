@@ -65,24 +65,31 @@ def philox4x32_10(seed: int, stream: int, groups: np.ndarray) -> np.ndarray:
 
 
 def dropout_threshold(p: float) -> int:
+    """16-bit keep threshold round(p * 65536), clamped to [1, 65535] (0 = off)."""
     if p <= 0.0:
         return 0
-    t = p * 4294967296.0
-    thr = 0xFFFFFFFF if t >= 4294967295.0 else int(t)
+    t = p * 65536.0 + 0.5
+    thr = 65535 if t >= 65535.0 else int(t)
     return max(thr, 1)
 
 
 def keep_mask(p: float, seed: int, stream: int, idx: np.ndarray) -> np.ndarray:
-    """Boolean keep mask for element indices `idx` (any shape)."""
+    """Boolean keep mask for element indices `idx` (any shape).
+
+    Element i uses the 16-bit half (i & 1) of word ((i & 7) >> 1) of
+    Philox4x32-10(seed, stream, i >> 3) - one Philox call per 8 elements
+    (restates mimose_dev::dropout_mask8, csrc/common.cuh)."""
     thr = dropout_threshold(p)
     if thr == 0:
         return np.ones(idx.shape, dtype=bool)
     flat = idx.reshape(-1).astype(np.uint64)
-    groups = flat >> np.uint64(2)
+    groups = flat >> np.uint64(3)
     ug, inv = np.unique(groups, return_inverse=True)
     r = philox4x32_10(seed, stream, ug)
-    words = r[inv, (flat & np.uint64(3)).astype(np.int64)]
-    return (words >= np.uint32(thr)).reshape(idx.shape)
+    e = (flat & np.uint64(7)).astype(np.int64)
+    words = r[inv, e >> 1].astype(np.uint64)
+    half = ((words >> (np.uint64(16) * (e & 1).astype(np.uint64))) & np.uint64(0xFFFF))
+    return (half >= np.uint64(thr)).reshape(idx.shape)
 
 
 def stream_id(step: int, layer: int, site: int) -> int:

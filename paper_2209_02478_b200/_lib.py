@@ -99,6 +99,7 @@ class StepReport(C.Structure):
         ("plan_us", C.c_double), ("fit_us", C.c_double),
         ("dropped_mask_lo", C.c_uint64),
         ("pred_err_mean", C.c_double), ("pred_err_max", C.c_double), ("pred_layers", C.c_int),
+        ("host_ms", C.c_double),
     ]
 
     def as_dict(self):
@@ -136,6 +137,9 @@ CUDA_SYMBOLS = [
     ("mimose_trainer_destroy", C.c_int, [_P]),
     ("mimose_trainer_step", C.c_int,
      [_P, _P, _P, _P, C.c_int, C.c_int, _P, C.POINTER(StepReport)]),
+    ("mimose_trainer_step_async", C.c_int,
+     [_P, _P, _P, _P, C.c_int, C.c_int, _P, C.POINTER(StepReport)]),
+    ("mimose_trainer_loss", C.c_int, [_P, C.c_int64, C.POINTER(C.c_float)]),
     ("mimose_trainer_forward_backward", C.c_int,
      [_P, _P, _P, _P, C.c_int, C.c_int, _P, C.POINTER(StepReport)]),
     ("mimose_trainer_step_device", C.c_int,

@@ -38,18 +38,27 @@ struct Philox {
 };
 
 // keep-mask bits for 8 consecutive elements starting at `idx` (idx % 8 == 0):
-// element idx + e uses word (e & 3) of Philox group (idx >> 2) + (e >> 2).
+// one Philox call per 8 elements; element idx + e compares the 16-bit half
+// (e & 1) of word (e >> 1) of Philox(seed, stream, idx >> 3) with the
+// threshold round(p * 65536).
 __device__ __forceinline__ uint32_t dropout_mask8(const DropoutCfg& d, uint64_t idx) {
   if (d.threshold == 0) return 0xFFu;
-  const Philox a(d.seed, d.stream, idx >> 2);
-  const Philox b(d.seed, d.stream, (idx >> 2) + 1);
+  const Philox a(d.seed, d.stream, idx >> 3);
   uint32_t m = 0;
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    m |= (a.r[e] >= d.threshold ? 1u : 0u) << e;
-    m |= (b.r[e] >= d.threshold ? 1u : 0u) << (e + 4);
+  for (int e = 0; e < 8; ++e) {
+    const uint32_t r16 = (a.r[e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+    m |= (r16 >= d.threshold ? 1u : 0u) << e;
   }
   return m;
+}
+
+// keep decision for a single element (head kernel)
+__device__ __forceinline__ bool dropout_keep1(const DropoutCfg& d, uint64_t idx) {
+  if (d.threshold == 0) return true;
+  const Philox a(d.seed, d.stream, idx >> 3);
+  const int e = static_cast<int>(idx & 7);
+  return ((a.r[e >> 1] >> (16 * (e & 1))) & 0xFFFFu) >= d.threshold;
 }
 
 // ------------------------------------------------------------------ vectors

@@ -8,7 +8,7 @@ namespace mimose_dev {
 struct DropoutCfg {
   uint64_t seed = 0;
   uint64_t stream = 0;
-  uint32_t threshold = 0;  // keep iff rand >= threshold; 0 disables dropout
+  uint32_t threshold = 0;  // keep iff 16-bit rand >= threshold; 0 disables dropout
   float scale = 1.f;       // 1 / (1 - p)
 };
 

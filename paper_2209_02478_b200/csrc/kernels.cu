@@ -216,16 +216,27 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const mimose_ops::LnBwdArgs
   }
 }
 
-// sum over blocks of partial[nblk][W] -> out segments (fixed order)
-__global__ void reduce_partials_kernel(const float* __restrict__ partial, int nblk, int W,
-                                       int seg, float* o0, float* o1, float* o2) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= W) return;
+// sum over blocks of partial[nblk][W] -> out segments. 8 row-phases per
+// column, each summed in order, then combined in a fixed order: deterministic.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial,
+                                                              int nblk, int W, int seg, float* o0,
+                                                              float* o1, float* o2) {
+  __shared__ float red[8][33];
+  const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
+  const int i = blockIdx.x * 32 + x;
   float s = 0.f;
-  for (int b = 0; b < nblk; ++b) s += partial[(size_t)b * W + i];
-  const int k = i / seg, j = i % seg;
-  float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
-  if (o != nullptr) o[j] = s;
+  if (i < W)
+    for (int b = y; b < nblk; b += 8) s += partial[(size_t)b * W + i];
+  red[y][x] = s;
+  __syncthreads();
+  if (y == 0 && i < W) {
+    float t = red[0][x];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][x];
+    const int k = i / seg, j = i % seg;
+    float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
+    if (o != nullptr) o[j] = t;
+  }
 }
 
 // =====================================================================
@@ -289,41 +300,54 @@ __device__ __forceinline__ float group_max(float v) {
   return v;
 }
 
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
+
+// All loads of a lane are issued before any arithmetic; exp is evaluated once.
 template <int L, int MAXC>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict__ s_in,
                                                           bf16* __restrict__ p_out,
                                                           bf16* __restrict__ pd_out, int64_t rows,
                                                           int S, int ld, DropoutCfg drop) {
   constexpr int R = 32 / L;
+  constexpr float kLog2e = 1.4426950408889634f;
   const int lane = threadIdx.x & 31;
   const int sub = lane % L;
   const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
   const bool live = row < rows;
   const bf16* in = s_in + (live ? row : 0) * ld;
+  uint4 raw[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) {
+    const int j0 = 8 * (sub + L * c);
+    raw[c] = (live && j0 < S) ? *reinterpret_cast<const uint4*>(in + j0) : make_uint4(0, 0, 0, 0);
+  }
   float v[MAXC][8];
   float mx = -INFINITY;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    if (live && j0 < S) load8(in + j0, v[c]);
-  }
-#pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    const int j0 = 8 * (sub + L * c);
+    unpack8(raw[c], v[c]);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      if (!live || j0 + e >= S) v[c][e] = -INFINITY;
+      v[c][e] = (live && j0 + e < S) ? v[c][e] * kLog2e : -INFINITY;
       mx = fmaxf(mx, v[c][e]);
     }
   }
   mx = group_max<L>(mx);
   float sum = 0.f;
-  const float mxl = mx * 1.4426950408889634f;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      v[c][e] = exp2f(v[c][e] * 1.4426950408889634f - mxl);
+      v[c][e] = exp2f(v[c][e] - mx);
       sum += v[c][e];
     }
   const float inv = 1.f / group_sum<L>(sum);
@@ -346,7 +370,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
 
 // dS = P * (dP - sum_j dP_j P_j) * scale,  dP = dPd * mask * (1/(1-p)); in place over dPd
 template <int L, int MAXC>
-__global__ void __launch_bounds__(256) softmax_bwd_kernel(const bf16* __restrict__ P,
+__global__ void __launch_bounds__(256, (MAXC > 4) ? 1 : 2) softmax_bwd_kernel(const bf16* __restrict__ P,
                                                           bf16* __restrict__ dpd, int64_t rows,
                                                           int S, int ld, DropoutCfg drop,
                                                           float scale) {
@@ -356,27 +380,29 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const bf16* __restrict
   const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
   const bool live = row < rows;
   const int64_t base = (live ? row : 0) * ld;
-  float p[MAXC][8], dp[MAXC][8];
+  uint4 praw[MAXC], draw[MAXC];
+  uint32_t mbits = 0;  // keep bits, 8 per chunk... packed 4 chunks per word below
+  uint32_t mk[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    if (live && j0 < S) {
-      load8(P + base + j0, p[c]);
-      load8(dpd + base + j0, dp[c]);
-    }
+    const bool in = live && j0 < S;
+    praw[c] = in ? *reinterpret_cast<const uint4*>(P + base + j0) : make_uint4(0, 0, 0, 0);
+    draw[c] = in ? *reinterpret_cast<const uint4*>(dpd + base + j0) : make_uint4(0, 0, 0, 0);
   }
+  (void)mbits;
   float dot = 0.f;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    const uint32_t m = (live && j0 < S) ? dropout_mask8(drop, (uint64_t)row * ld + j0) : 0u;
+    mk[c] = (live && j0 < S) ? dropout_mask8(drop, (uint64_t)row * ld + j0) : 0u;
+    if (!(live && j0 < S)) continue;
+    float p[8], dp[8];
+    unpack8(praw[c], p);
+    unpack8(draw[c], dp);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const bool in = live && j0 + e < S;
-      dp[c][e] = (in && ((m >> e) & 1u)) ? dp[c][e] * drop.scale : 0.f;
-      p[c][e] = in ? p[c][e] : 0.f;
-      dot += dp[c][e] * p[c][e];
-    }
+    for (int e = 0; e < 8; ++e)
+      if (j0 + e < S && ((mk[c] >> e) & 1u)) dot += dp[e] * drop.scale * p[e];
   }
   dot = group_sum<L>(dot);
   if (!live) return;
@@ -384,9 +410,16 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(const bf16* __restrict
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
     if (j0 >= ld) continue;
-    float ds[8];
+    float p[8], dp[8], ds[8];
+    unpack8(praw[c], p);
+    unpack8(draw[c], dp);
+    const uint32_t m = mk[c];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) ds[e] = p[c][e] * (dp[c][e] - dot) * scale;
+    for (int e = 0; e < 8; ++e) {
+      const bool in = j0 + e < S;
+      const float g = (in && ((m >> e) & 1u)) ? dp[e] * drop.scale : 0.f;
+      ds[e] = in ? p[e] * (g - dot) * scale : 0.f;
+    }
     store8(dpd + base + j0, ds);
   }
 }
@@ -462,8 +495,7 @@ __global__ void __launch_bounds__(1024) mc_head_kernel(const bf16* __restrict__ 
     float s = 0.f;
     for (int c = lane; c < H; c += 32) {
       const uint64_t idx = (uint64_t)b * H + c;
-      const Philox ph(drop.seed, drop.stream, idx >> 2);
-      const bool keep = drop.threshold == 0 || ph.r[idx & 3] >= drop.threshold;
+      const bool keep = dropout_keep1(drop, idx);
       const float t = tanhf(__bfloat162float(pre[idx]));
       s += keep ? t * drop.scale * wc[c] : 0.f;
     }
@@ -499,8 +531,7 @@ __global__ void __launch_bounds__(1024) mc_head_kernel(const bf16* __restrict__ 
     float acc = 0.f;
     for (int b = 0; b < B; ++b) {
       const uint64_t idx = (uint64_t)b * H + c;
-      const Philox ph(drop.seed, drop.stream, idx >> 2);
-      const bool keep = drop.threshold == 0 || ph.r[idx & 3] >= drop.threshold;
+      const bool keep = dropout_keep1(drop, idx);
       const float t = tanhf(__bfloat162float(pre[idx]));
       acc += keep ? dl[b] * t * drop.scale : 0.f;
       const float dt = keep ? dl[b] * wc[c] * drop.scale : 0.f;
@@ -698,8 +729,8 @@ cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float
   }
   count_launch();
   if (e != cudaSuccess) return e;
-  mimose_dev::reduce_partials_kernel<<<grid_for(3 * H, 256), 256, 0, s>>>(a.partial, nblk, 3 * H,
-                                                                         H, dgamma, dbeta, dbias);
+  mimose_dev::reduce_partials_kernel<<<grid_for(3 * H, 32), 256, 0, s>>>(a.partial, nblk, 3 * H,
+                                                                        H, dgamma, dbeta, dbias);
   count_launch();
   return cudaGetLastError();
 }
@@ -717,7 +748,7 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
   mimose_dev::colsum_partial_kernel<<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N, ld,
                                                          groups, G, partial);
   count_launch();
-  mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, 256), 256, 0, s>>>(
+  mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, 32), 256, 0, s>>>(
       partial, rb, G * N, G * N, out, nullptr, nullptr);
   count_launch();
   return cudaGetLastError();
@@ -743,10 +774,11 @@ cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int
   auto in = static_cast<const bf16*>(scores);
   auto p = static_cast<bf16*>(P);
   auto pd = static_cast<bf16*>(Pd);
-  if (ld <= 128) softmax_fwd_t<8, 2>(in, p, pd, rows, S, ld, d, s);
+  if (ld <= 64) softmax_fwd_t<8, 1>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 128) softmax_fwd_t<8, 2>(in, p, pd, rows, S, ld, d, s);
   else if (ld <= 256) softmax_fwd_t<8, 4>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 512) softmax_fwd_t<8, 8>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 1024) softmax_fwd_t<16, 8>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 512) softmax_fwd_t<16, 4>(in, p, pd, rows, S, ld, d, s);
+  else if (ld <= 1024) softmax_fwd_t<32, 4>(in, p, pd, rows, S, ld, d, s);
   else if (ld <= 2048) softmax_fwd_t<32, 8>(in, p, pd, rows, S, ld, d, s);
   else return cudaErrorInvalidValue;
   count_launch();
@@ -757,10 +789,13 @@ cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
   auto p = static_cast<const bf16*>(P);
   auto dp = static_cast<bf16*>(dPd);
-  if (ld <= 128) softmax_bwd_t<8, 2>(p, dp, rows, S, ld, d, scale, s);
+  // two operands per chunk: at most 4 chunks per lane keeps the kernel in
+  // registers (no spills) at 2 CTAs / SM
+  if (ld <= 64) softmax_bwd_t<8, 1>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 128) softmax_bwd_t<8, 2>(p, dp, rows, S, ld, d, scale, s);
   else if (ld <= 256) softmax_bwd_t<8, 4>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 512) softmax_bwd_t<8, 8>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 1024) softmax_bwd_t<16, 8>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 512) softmax_bwd_t<16, 4>(p, dp, rows, S, ld, d, scale, s);
+  else if (ld <= 1024) softmax_bwd_t<32, 4>(p, dp, rows, S, ld, d, scale, s);
   else if (ld <= 2048) softmax_bwd_t<32, 8>(p, dp, rows, S, ld, d, scale, s);
   else return cudaErrorInvalidValue;
   count_launch();

@@ -83,9 +83,9 @@ inline DropoutCfg make_dropout(float p, uint64_t seed, uint64_t stream) {
   if (p <= 0.f) return d;
   d.seed = seed;
   d.stream = stream;
-  const double t = static_cast<double>(p) * 4294967296.0;
-  d.threshold = t >= 4294967295.0 ? 0xFFFFFFFFu : static_cast<uint32_t>(t);
-  if (d.threshold == 0) d.threshold = 1;
+  const double t = static_cast<double>(p) * 65536.0 + 0.5;
+  uint32_t thr = t >= 65535.0 ? 65535u : static_cast<uint32_t>(t);
+  d.threshold = thr == 0 ? 1u : thr;
   d.scale = 1.f / (1.f - p);
   return d;
 }

@@ -206,9 +206,16 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   norm2_ = static_cast<float*>(take(4, kTagOther));
   d_loss_ = static_cast<float*>(take(4, kTagOther));
   d_logits_ = static_cast<float*>(take((int64_t)t.batch * 4, kTagOther));
-  ck(cudaMallocHost(&h_loss_, sizeof(float)), "cudaMallocHost");
+  ck(cudaMallocHost(&h_loss_, kLossRing * sizeof(float)), "cudaMallocHost");
+  for (int j = 0; j < kLossRing; ++j) {
+    ck(cudaEventCreateWithFlags(&loss_ev_[j], cudaEventDisableTiming), "event");
+    loss_iter_[j] = -1;
+  }
   stage_elems_ = 5 * Tmax + t.batch + 8;
-  ck(cudaMallocHost(&h_stage_, stage_elems_ * sizeof(int32_t)), "cudaMallocHost");
+  for (int k = 0; k < 2; ++k) {
+    ck(cudaMallocHost(&h_stage_[k], stage_elems_ * sizeof(int32_t)), "cudaMallocHost");
+    ck(cudaEventCreateWithFlags(&stage_ev_[k], cudaEventDisableTiming), "event");
+  }
   ev_.resize(2 * L_);
   for (auto& e : ev_) ck(cudaEventCreate(&e), "cudaEventCreate");
   ck(cudaStreamSynchronize(s), "init sync");
@@ -220,7 +227,12 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
 Trainer::~Trainer() {
   for (auto& e : ev_) cudaEventDestroy(e);
   if (h_loss_) cudaFreeHost(h_loss_);
-  if (h_stage_) cudaFreeHost(h_stage_);
+  for (int k = 0; k < 2; ++k) {
+    if (h_stage_[k]) cudaFreeHost(h_stage_[k]);
+    if (stage_ev_[k]) cudaEventDestroy(stage_ev_[k]);
+  }
+  for (int j = 0; j < kLossRing; ++j)
+    if (loss_ev_[j]) cudaEventDestroy(loss_ev_[j]);
   // arena memory is released with the context
 }
 
@@ -709,6 +721,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   auto* W = static_cast<bf16raw*>(p16_);
   float* G = g32_;
 
+  const auto host_t0 = std::chrono::steady_clock::now();
   mimose_step_report local{};
   mimose_step_report* r = rep ? rep : &local;
   std::memset(r, 0, sizeof(*r));
@@ -874,6 +887,8 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
      "colsum");
   drop(de);
 
+  r->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0)
+                   .count();
   const auto& st = ctx_->arena.stats();
   r->peak_requested = st.peak_requested;
   r->peak_reserved = st.peak_reserved;
@@ -918,11 +933,15 @@ void Trainer::optimizer_step(float grad_scale, cudaStream_t s) {
 }
 
 void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
-                        int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep) {
+                        int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep,
+                        bool sync) {
   const int64_t T = (int64_t)B * S;
   const int Q = B / m_.num_choices;
   if (5 * T + Q + 1 > stage_elems_) throw std::runtime_error("staging buffer too small");
-  int32_t* tk = h_stage_;
+  // double-buffered pinned staging: wait for the H2D that last read this slot
+  const int k = static_cast<int>(iter_ & 1);
+  if (stage_used_[k]) ck(cudaEventSynchronize(stage_ev_[k]), "staging wait");
+  int32_t* tk = h_stage_[k];
   int32_t* ty = tk + T;
   int32_t* lb = ty + T;
   int32_t* pm = lb + Q;
@@ -941,7 +960,9 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
   int32_t* d = static_cast<int32_t*>(take(n_in * 4 + 64, kTagInput));
   // contiguous upload (uid packed right after seg)
   std::memmove(sg + nu + 1, ui, nu * 4);
-  ck(cudaMemcpyAsync(d, h_stage_, n_in * 4, cudaMemcpyHostToDevice, s), "H2D inputs");
+  ck(cudaMemcpyAsync(d, h_stage_[k], n_in * 4, cudaMemcpyHostToDevice, s), "H2D inputs");
+  ck(cudaEventRecord(stage_ev_[k], s), "event");
+  stage_used_[k] = true;
   StepInputs in;
   in.tokens = d;
   in.types = d + T;
@@ -950,6 +971,7 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
   in.seg = in.perm + T;
   in.uid = in.seg + nu + 1;
   in.n_unique = nu;
+  const int64_t this_iter = iter_;
   forward_backward(in, B, S, s, rep);
   void* dv = d;
   drop(dv);
@@ -957,10 +979,27 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
     if (hook_) hook_(hook_user_, g32_, nparam_, s);
     optimizer_step(1.f, s);
   }
-  ck(cudaMemcpyAsync(h_loss_, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H loss");
-  ck(cudaStreamSynchronize(s), "step sync");
-  if (rep) rep->loss = *h_loss_;
-  if (!history_.empty()) history_.back().loss = *h_loss_;
+  // loss read-back into a pinned ring slot (read later by loss(iter) or now)
+  const int j = static_cast<int>(this_iter % kLossRing);
+  if (loss_iter_[j] >= 0) ck(cudaEventSynchronize(loss_ev_[j]), "loss slot wait");
+  ck(cudaMemcpyAsync(h_loss_ + j, d_loss_, sizeof(float), cudaMemcpyDeviceToHost, s), "D2H loss");
+  ck(cudaEventRecord(loss_ev_[j], s), "event");
+  loss_iter_[j] = this_iter;
+  if (sync) {
+    const float v = loss(this_iter);
+    if (rep) rep->loss = v;
+  }
+}
+
+float Trainer::loss(int64_t iter) {
+  const int j = static_cast<int>(iter % kLossRing);
+  if (iter < 0 || loss_iter_[j] != iter)
+    throw std::runtime_error("loss of iteration " + std::to_string(iter) + " is not available");
+  ck(cudaEventSynchronize(loss_ev_[j]), "loss wait");
+  const float v = h_loss_[j];
+  for (auto& h : history_)
+    if (h.iter == iter) h.loss = v;
+  return v;
 }
 
 }  // namespace mimose_rt
@@ -1021,6 +1060,19 @@ int mimose_trainer_step(mimose_trainer* tr, const int32_t* tokens, const int32_t
   return guarded("mimose_trainer_step", [&] {
     tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep);
   });
+}
+
+int mimose_trainer_step_async(mimose_trainer* tr, const int32_t* tokens, const int32_t* types,
+                              const int32_t* labels, int batch, int seq, void* stream,
+                              mimose_step_report* rep) {
+  return guarded("mimose_trainer_step_async", [&] {
+    tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep,
+                        /*sync=*/false);
+  });
+}
+
+int mimose_trainer_loss(mimose_trainer* tr, int64_t iter, float* loss) {
+  return guarded("mimose_trainer_loss", [&] { *loss = tr->impl->loss(iter); });
 }
 
 int mimose_trainer_forward_backward(mimose_trainer* tr, const int32_t* tokens,

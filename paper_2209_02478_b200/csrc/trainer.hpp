@@ -68,7 +68,10 @@ class Trainer {
 
   // host inputs -> staged H2D -> forward_backward (+ hook + optimizer) -> loss D2H
   void step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
-                 int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep);
+                 int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep,
+                 bool sync = true);
+  // loss of a host-input step (blocks until that step's read-back landed)
+  float loss(int64_t iter);
 
   void set_forced_plan(const int* ids, int n, int active);
   void set_grad_hook(mimose_grad_hook fn, void* user) {
@@ -142,10 +145,15 @@ class Trainer {
   int64_t wgrad_ws_bytes_ = 0;
   float* d_loss_ = nullptr;
   float* d_logits_ = nullptr;
-  float* h_loss_ = nullptr;  // pinned
+  static constexpr int kLossRing = 4;
+  float* h_loss_ = nullptr;  // pinned ring of read-back losses
+  cudaEvent_t loss_ev_[kLossRing] = {};
+  int64_t loss_iter_[kLossRing] = {};
 
-  // pinned staging for host inputs
-  int32_t* h_stage_ = nullptr;
+  // double-buffered pinned staging for host inputs
+  int32_t* h_stage_[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev_[2] = {};
+  bool stage_used_[2] = {false, false};
   int64_t stage_elems_ = 0;
 
   std::vector<cudaEvent_t> ev_;  // 2 per layer (collector timing)

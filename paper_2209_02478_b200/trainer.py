@@ -169,6 +169,22 @@ class Trainer:
         self.rows.append(d)
         return d
 
+    def step_async(self, tokens, types, labels, *, stream=None) -> dict:
+        """Pinned host inputs; returns without waiting for the loss (see loss())."""
+        B, S = tokens.shape
+        rep = _lib.StepReport()
+        check(self.lib.mimose_trainer_step_async(self.handle, tokens.data_ptr(), types.data_ptr(),
+                                                 labels.data_ptr(), B, S, _stream_handle(stream),
+                                                 C.byref(rep)))
+        d = self._row(rep)
+        self.rows.append(d)
+        return d
+
+    def loss(self, iteration: int) -> float:
+        out = C.c_float()
+        check(self.lib.mimose_trainer_loss(self.handle, iteration, C.byref(out)))
+        return float(out.value)
+
     def step_device(self, batch: "DeviceBatch", *, optimizer: bool = True, stream=None) -> dict:
         """Device-resident inputs; no host synchronisation (loss stays on device)."""
         rep = _lib.StepReport()
