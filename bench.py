@@ -52,6 +52,11 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-baseline", action="store_true", help="skip no-ckpt throughput arm")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    ap.add_argument("--size-stream", default="shared", choices=["shared", "per-rank"],
+                    help="DP length policy: 'shared' = every rank draws S from the same seeded "
+                         "stream (length-synchronised sampling, no stragglers; data differs per "
+                         "rank); 'per-rank' = seed base+rank (independent lengths, max-over-"
+                         "ranks straggler cost)")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu (no comparison arms, no cpu baseline)")
     return ap.parse_args()
@@ -130,10 +135,16 @@ def dist_init(n):
     import torch
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", n))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", local))
+    # NCCL over NVLink on real multi-GPU runs; MIMOSE_DIST_BACKEND=gloo lets the
+    # N>1 code path be exercised with several ranks sharing one GPU (tests).
+    backend = os.environ.get("MIMOSE_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend, rank=rank, world_size=world)
     return rank, world, local
 
 
@@ -244,7 +255,8 @@ def run_gpu_arm(args, rank, world, local):
 
     # 1. no-checkpoint peak at S_max (defines the budget denominator)
     free, total = torch.cuda.mem_get_info()
-    probe_budget = int(min(free * 0.85, 150 * GiB))
+    ranks_here = max(1, world // max(1, torch.cuda.device_count()))
+    probe_budget = int(min(free * 0.85 / ranks_here, 150 * GiB))
     probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"), probe_budget, local)
     rng = np.random.default_rng(args.seed + 1000 * rank)
     probe.step(*synthetic_batch(rng, B, S_max, model_cfg.vocab, model_cfg.num_choices),
@@ -254,7 +266,9 @@ def run_gpu_arm(args, rank, world, local):
     budget = int(args.budget_frac * peak_none)
 
     n_total = args.warmup + args.steps
-    seqs = sizes_for(args.dist, B, 10_000, args.seed + rank)  # rank r: seed base + r
+    # sizes: reference sampler; 'per-rank' seeds base + rank, 'shared' seeds base
+    seqs = sizes_for(args.dist, B, 10_000,
+                     args.seed + (rank if args.size_stream == "per-rank" else 0))
 
     def batches(seq_list, seed):
         g = np.random.default_rng(seed)
@@ -414,6 +428,7 @@ def run_gpu_arm(args, rank, world, local):
                 "workload": "bert-base-mc: BERT-base (L12 H768 A12 F3072 V30522) multiple-choice "
                             "fine-tune, SWAG-shaped 16x4 choices (BASELINE configs[1])",
                 "global_batch": B * world, "seq_len": args.dist, "parallelism": f"dp{world}",
+                "dp_size_stream": args.size_stream,
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
                 "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
                 "l2": "not flushed: per-step working set (GBs of activations) >> 126 MB L2",

@@ -71,11 +71,13 @@ struct GemmCfg {
   // per epilogue warp: kNOut buffers of 32 rows x 128 B (single-buffered:
   // the TMA store drains 4 KB from smem long before the next chunk is ready)
   static constexpr int kStagingBytes = kEpiWarps * kNOut * 4096;
+  static constexpr int kBiasBytes = 2 * BN * 4;  // tile bias slice, per accumulator stage
   static constexpr int kStagesRaw =
-      (kSmemBudget - 1024 - 256 - kStagingBytes) / kStageBytes;
+      (kSmemBudget - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr int kSmemBytes = kStages * kStageBytes + kStagingBytes + 1024 + 256;
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 256;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
 };
 
@@ -113,28 +115,38 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // Epilogue math on NV consecutive accumulator columns of one row (values in
-// v, first column col0). Results in v (and g for the GELU output).
+// v, first column col0). `bias_t` points at this chunk's slice of the tile's
+// bias staged in shared memory (or is null); `aux_pre` holds the chunk's aux
+// row prefetched before the TMEM load (or is null: load here). Results in v
+// (and g for the GELU output).
 template <int EPI, int NV>
 __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], const GemmParams& p,
-                                              long long obase, int col0, bool row_ok) {
+                                              long long obase, int col0, bool row_ok,
+                                              const float* bias_t, const uint4* aux_pre) {
   if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu || EPI == kEpiF32) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) v[i] *= p.alpha;
   }
   if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
-    if (p.bias != nullptr) {
+    if (bias_t != nullptr) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i)
-        if (col0 + i < p.N) v[i] += __ldg(p.bias + col0 + i);
+      for (int q = 0; q < NV / 4; ++q) {
+        const float4 b = *reinterpret_cast<const float4*>(bias_t + 4 * q);  // smem broadcast
+        v[4 * q] += b.x;
+        v[4 * q + 1] += b.y;
+        v[4 * q + 2] += b.z;
+        v[4 * q + 3] += b.w;
+      }
     }
   }
   if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
     if (p.aux != nullptr && row_ok) {
       const __nv_bfloat16* ax = p.aux + obase + col0;
-      if (p.vec && col0 + NV <= p.N) {
+      if (aux_pre != nullptr || (p.vec && col0 + NV <= p.N)) {
 #pragma unroll
         for (int q = 0; q < NV / 8; ++q) {
-          const uint4 raw = *reinterpret_cast<const uint4*>(ax + 8 * q);
+          const uint4 raw = aux_pre != nullptr ? aux_pre[q]
+                                               : *reinterpret_cast<const uint4*>(ax + 8 * q);
           const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(&raw);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -180,7 +192,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
   uint8_t* sD = smem + S * Cfg::kStageBytes;  // epilogue staging (1024-aligned)
-  uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes);
+  float* sBias = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [2][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes + Cfg::kBiasBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
@@ -317,6 +330,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int b2 = p.splits > 1 ? 0 : z / p.nb1;
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
+      // stage this tile's bias slice once (all 8 epilogue warps, then a named
+      // barrier); double-buffered by accumulator stage
+      float* tb = nullptr;
+      if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
+        if (p.bias != nullptr) {
+          tb = sBias + acc * BN;
+          for (int i = ew * 32 + static_cast<int>(lane); i < BN; i += kEpiWarps * 32)
+            tb[i] = n0 + i < p.N ? __ldg(p.bias + n0 + i) : 0.f;
+          asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        }
+      }
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
 
@@ -336,6 +360,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) bulk_wait_read<0>();  // previous chunk's store has read the buffer
           __syncwarp();
           float v[CW], g[CW];
+          // issue the aux-row loads before waiting on TMEM so the two latencies overlap
+          uint4 aux_pre[CW / 8];
+          bool have_pre = false;
+          if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
+            if (p.aux != nullptr && row_ok && p.vec && n0 + c + CW <= p.N) {
+              const __nv_bfloat16* ax = p.aux + obase + n0 + c;
+#pragma unroll
+              for (int q = 0; q < CW / 8; ++q) aux_pre[q] = *reinterpret_cast<const uint4*>(ax + 8 * q);
+              have_pre = true;
+            }
+          }
           {
             uint32_t r[32];
 #pragma unroll
@@ -346,7 +381,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
               for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(r[i]);
             }
           }
-          epilogue_math<EPI, CW>(v, g, p, obase, n0 + c, row_ok);
+          epilogue_math<EPI, CW>(v, g, p, obase, n0 + c, row_ok, tb ? tb + c : nullptr,
+                                 have_pre ? aux_pre : nullptr);
           const uint32_t rbase = smem_u32(sb) + lane * CB;
           const uint32_t sw = CB == 128 ? (lane & 7) : ((lane >> 1) & 3);
 #pragma unroll
@@ -411,7 +447,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   o[i] = v[i] + (p.beta != 0.f ? p.beta * o[i] : 0.f);
               }
             } else {
-              epilogue_math<EPI, 16>(v, g, p, obase, col0, row_ok);
+              epilogue_math<EPI, 16>(v, g, p, obase, col0, row_ok, tb ? tb + c : nullptr,
+                                     nullptr);
               __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out) + obase + col0;
               alignas(16) __nv_bfloat16 hv[16];
 #pragma unroll

@@ -769,18 +769,47 @@ static void softmax_bwd_t(const bf16* p, bf16* dp, int64_t rows, int S, int ld,
   mimose_dev::softmax_bwd_kernel<L, MAXC><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
 }
 
+// Dispatch: L lanes per row (8 for rows up to 512, 16 up to 1024, 32 up to
+// 2048) and exactly MAXC = ceil(chunks / L) chunks per lane, so no lane runs
+// fully predicated-off chunk slots.
+#define MIMOSE_SOFTMAX_CASES(FN)                                                   \
+  switch (maxc) {                                                                  \
+    case 1: FN(1); break;                                                          \
+    case 2: FN(2); break;                                                          \
+    case 3: FN(3); break;                                                          \
+    case 4: FN(4); break;                                                          \
+    case 5: FN(5); break;                                                          \
+    case 6: FN(6); break;                                                          \
+    case 7: FN(7); break;                                                          \
+    default: FN(8); break;                                                         \
+  }
+
+static bool softmax_geometry(int ld, int* L, int* maxc) {
+  const int chunks = ld / 8;
+  if (ld <= 512) *L = 8;
+  else if (ld <= 1024) *L = 16;
+  else if (ld <= 2048) *L = 32;
+  else return false;
+  *maxc = (chunks + *L - 1) / *L;
+  return *maxc >= 1 && *maxc <= 8;
+}
+
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, cudaStream_t s) {
   auto in = static_cast<const bf16*>(scores);
   auto p = static_cast<bf16*>(P);
   auto pd = static_cast<bf16*>(Pd);
-  if (ld <= 64) softmax_fwd_t<8, 1>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 128) softmax_fwd_t<8, 2>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 256) softmax_fwd_t<8, 4>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 512) softmax_fwd_t<16, 4>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 1024) softmax_fwd_t<32, 4>(in, p, pd, rows, S, ld, d, s);
-  else if (ld <= 2048) softmax_fwd_t<32, 8>(in, p, pd, rows, S, ld, d, s);
-  else return cudaErrorInvalidValue;
+  int L = 0, maxc = 0;
+  if (!softmax_geometry(ld, &L, &maxc)) return cudaErrorInvalidValue;
+#define FWD8(M) softmax_fwd_t<8, M>(in, p, pd, rows, S, ld, d, s)
+#define FWD16(M) softmax_fwd_t<16, M>(in, p, pd, rows, S, ld, d, s)
+#define FWD32(M) softmax_fwd_t<32, M>(in, p, pd, rows, S, ld, d, s)
+  if (L == 8) { MIMOSE_SOFTMAX_CASES(FWD8) }
+  else if (L == 16) { MIMOSE_SOFTMAX_CASES(FWD16) }
+  else { MIMOSE_SOFTMAX_CASES(FWD32) }
+#undef FWD8
+#undef FWD16
+#undef FWD32
   count_launch();
   return cudaGetLastError();
 }
@@ -789,15 +818,17 @@ cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
   auto p = static_cast<const bf16*>(P);
   auto dp = static_cast<bf16*>(dPd);
-  // two operands per chunk: at most 4 chunks per lane keeps the kernel in
-  // registers (no spills) at 2 CTAs / SM
-  if (ld <= 64) softmax_bwd_t<8, 1>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 128) softmax_bwd_t<8, 2>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 256) softmax_bwd_t<8, 4>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 512) softmax_bwd_t<16, 4>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 1024) softmax_bwd_t<32, 4>(p, dp, rows, S, ld, d, scale, s);
-  else if (ld <= 2048) softmax_bwd_t<32, 8>(p, dp, rows, S, ld, d, scale, s);
-  else return cudaErrorInvalidValue;
+  int L = 0, maxc = 0;
+  if (!softmax_geometry(ld, &L, &maxc)) return cudaErrorInvalidValue;
+#define BWD8(M) softmax_bwd_t<8, M>(p, dp, rows, S, ld, d, scale, s)
+#define BWD16(M) softmax_bwd_t<16, M>(p, dp, rows, S, ld, d, scale, s)
+#define BWD32(M) softmax_bwd_t<32, M>(p, dp, rows, S, ld, d, scale, s)
+  if (L == 8) { MIMOSE_SOFTMAX_CASES(BWD8) }
+  else if (L == 16) { MIMOSE_SOFTMAX_CASES(BWD16) }
+  else { MIMOSE_SOFTMAX_CASES(BWD32) }
+#undef BWD8
+#undef BWD16
+#undef BWD32
   count_launch();
   return cudaGetLastError();
 }
