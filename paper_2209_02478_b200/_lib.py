@@ -13,7 +13,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-CUDA_LIB_PATH = os.path.join(_HERE, "libmimose_cuda.so")
+# MIMOSE_CUDA_LIB: alternate in-tree build (A/B kernel timing in tools/ only)
+CUDA_LIB_PATH = os.environ.get("MIMOSE_CUDA_LIB", os.path.join(_HERE, "libmimose_cuda.so"))
 HOST_LIB_PATH = os.path.join(_HERE, "libmimose_host.so")
 
 _cuda = None

@@ -85,10 +85,20 @@ struct GemmCfg {
 // the e^{-z^2} it needs (reused by the GELU derivative). The GELU output is
 // rounded to bf16 (rel. 2^-9), so this is exact for every purpose here while
 // costing ~1/3 of erff.
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
 __device__ __forceinline__ float erf_as(float z, float& ez2) {
   const float a = fabsf(z);
-  const float t = __frcp_rn(fmaf(0.3275911f, a, 1.0f));
-  ez2 = exp2f(-1.4426950408889634f * z * z);
+  const float t = rcp_approx(fmaf(0.3275911f, a, 1.0f));
+  ez2 = ex2_approx(-1.4426950408889634f * z * z);
   float poly = fmaf(1.061405429f, t, -1.453152027f);
   poly = fmaf(poly, t, 1.421413741f);
   poly = fmaf(poly, t, -0.284496736f);
@@ -97,6 +107,15 @@ __device__ __forceinline__ float erf_as(float z, float& ez2) {
   return copysignf(r, z);
 }
 
+#ifdef MIMOSE_GELU_ERFF  // libm erff variant (A/B timing only)
+__device__ __forceinline__ float gelu_f(float x) {
+  return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f));
+}
+__device__ __forceinline__ float dgelu_f(float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  return cdf + x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
+#else
 // exact-erf GELU: x * Phi(x) = 0.5 x (1 + erf(x / sqrt 2))
 __device__ __forceinline__ float gelu_f(float x) {
   float e;
@@ -108,6 +127,7 @@ __device__ __forceinline__ float dgelu_f(float x) {
   const float cdf = 0.5f * (1.0f + erf_as(x * 0.70710678118654752f, e));
   return fmaf(x * 0.39894228040143268f, e, cdf);
 }
+#endif
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
