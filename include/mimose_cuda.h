@@ -124,7 +124,8 @@ enum {
   MIMOSE_PLANNER_MIMOSE = 0, /* two-phase input-aware planner (the product) */
   MIMOSE_PLANNER_NONE = 1,   /* no checkpointing (throughput reference) */
   MIMOSE_PLANNER_ALL = 2,    /* checkpoint every block */
-  MIMOSE_PLANNER_STATIC = 3  /* plan once for seq_max, reuse (baselines.hpp:20) */
+  MIMOSE_PLANNER_STATIC = 3, /* plan once for seq_max, reuse (baselines.hpp:20) */
+  MIMOSE_PLANNER_DTR = 4     /* reactive eviction on the real arena (baselines.hpp:62) */
 };
 
 typedef struct {
@@ -219,6 +220,11 @@ int mimose_trainer_sync_params(mimose_trainer* tr, void* stream);
 int mimose_trainer_samples_csv(mimose_trainer* tr, char** out);
 int mimose_trainer_estimator_text(mimose_trainer* tr, char** out);
 int mimose_trainer_model_text(mimose_trainer* tr, char** out);
+/* The run so far through the reference's report writers (harness.hpp:339-379):
+ * IterationRow CSV + key/value summary, with MEASURED peaks (arena) and
+ * device milliseconds per iteration; recompute_ms from the fitted per-block
+ * forward-time model; plain_* from that model (3 x sum f). */
+int mimose_trainer_report(mimose_trainer* tr, char** summary, char** csv);
 int mimose_trainer_info(mimose_trainer* tr, int64_t* constant_bytes, int64_t* reserve_bytes,
                         int64_t* budget, int* trained, int64_t* cache_hits,
                         int64_t* cache_misses);

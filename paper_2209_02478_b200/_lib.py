@@ -159,6 +159,7 @@ CUDA_SYMBOLS = [
     ("mimose_trainer_samples_csv", C.c_int, [_P, C.POINTER(_P)]),
     ("mimose_trainer_estimator_text", C.c_int, [_P, C.POINTER(_P)]),
     ("mimose_trainer_model_text", C.c_int, [_P, C.POINTER(_P)]),
+    ("mimose_trainer_report", C.c_int, [_P, C.POINTER(_P), C.POINTER(_P)]),
     ("mimose_trainer_info", C.c_int,
      [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
       C.POINTER(C.c_int), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

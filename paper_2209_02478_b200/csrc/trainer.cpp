@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstring>
 #include <sstream>
+#include <set>
 #include <stdexcept>
 
 #include "ops.hpp"
@@ -224,7 +225,84 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   build_spec();
 }
 
+mimose::SimReport Trainer::report() {
+  mimose::SimReport rep;
+  rep.planner = t_.planner == MIMOSE_PLANNER_NONE     ? mimose::PlannerChoice::None
+                : t_.planner == MIMOSE_PLANNER_STATIC ? mimose::PlannerChoice::StaticMax
+                : t_.planner == MIMOSE_PLANNER_DTR    ? mimose::PlannerChoice::Dtr
+                                                      : mimose::PlannerChoice::Mimose;
+  rep.budget_bytes = sched_.budget_bytes;
+  rep.reserve_bytes = sched_.effective_reserve();
+  rep.iterations = static_cast<int64_t>(history_.size());
+  std::set<int64_t> distinct;
+  for (size_t i = 0; i < history_.size(); ++i) {
+    const mimose_step_report& h = history_[i];
+    mimose::IterationRow row;
+    row.iter = h.iter;
+    row.x = h.x;
+    row.planner = rep.planner;
+    row.cache_hit = h.cache_hit != 0;
+    row.peak_bytes = h.peak_reserved;  // measured (arena), not simulated
+    float ms = 0.f;
+    if (i < step_ev_.size()) {
+      ck(cudaEventSynchronize(step_ev_[i].second), "event");
+      ck(cudaEventElapsedTime(&ms, step_ev_[i].first, step_ev_[i].second), "event");
+    }
+    row.iteration_ms = ms;
+    // recompute cost from the measured per-block forward-time model
+    double rc = 0.0;
+    for (const auto& l : spec_.layers)
+      if (l.id < 64 && ((h.dropped_mask_lo >> l.id) & 1u)) rc += l.forward_ms(h.x);
+    row.recompute_ms = rc;
+    row.sheltered = h.phase == MIMOSE_PHASE_COLLECT || h.phase == MIMOSE_PHASE_SHELTERED ||
+                    h.phase == MIMOSE_PHASE_FALLBACK;
+    row.plan_size = h.plan_size;
+    row.insufficient = h.insufficient != 0;
+    distinct.insert(h.x);
+    const double plain = mimose::detail::plain_iteration_ms(spec_, h.x);
+    if (row.sheltered) {
+      rep.sheltered_iterations += 1;
+      rep.collector_overhead_ms += row.iteration_ms - plain;
+    }
+    if (h.phase == MIMOSE_PHASE_FALLBACK) rep.fallback_sheltered_iterations += 1;
+    if (row.peak_bytes > rep.budget_bytes) rep.oom_risk_iterations += 1;
+    if (row.insufficient) rep.insufficient_budget_iterations += 1;
+    if (h.fit_order >= 0) {
+      rep.fit_order = h.fit_order;
+      if (rep.fit_at_iter < 0) rep.fit_at_iter = h.iter;
+    }
+    rep.planner_wall_ms += h.plan_us / 1000.0;
+    rep.fit_wall_ms += h.fit_us / 1000.0;
+    rep.total_time_ms += row.iteration_ms;
+    rep.recompute_total_ms += row.recompute_ms;
+    rep.plain_total_ms += plain;
+    rep.mean_peak_bytes += static_cast<double>(row.peak_bytes);
+    rep.rows.push_back(row);
+  }
+  rep.collector_iterations = cstate_.collected_iterations;
+  rep.cache_hits = cache_.hits;
+  rep.cache_misses = cache_.misses;
+  rep.planner_invocations = cache_.misses;
+  rep.distinct_sizes = static_cast<int64_t>(distinct.size());
+  if (rep.iterations > 0) {
+    const double n = static_cast<double>(rep.iterations);
+    rep.mean_peak_bytes /= n;
+    rep.plain_iteration_ms = rep.plain_total_ms / n;
+    if (rep.plain_iteration_ms > 0.0) {
+      rep.overhead_iterations =
+          (rep.collector_overhead_ms + rep.planner_wall_ms + rep.fit_wall_ms) /
+          rep.plain_iteration_ms;
+      rep.slowdown_vs_plain = rep.total_time_ms / rep.plain_total_ms;
+    }
+  }
+  return rep;
+}
+
 Trainer::~Trainer() {
+  for (auto& e : step_ev_) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
   for (auto& e : ev_) cudaEventDestroy(e);
   if (h_loss_) cudaFreeHost(h_loss_);
   for (int k = 0; k < 2; ++k) {
@@ -340,6 +418,20 @@ int64_t Trainer::extras_bytes(int S) const {
   const int64_t s2 = act * 4 + quad + 2 * T * 3 * H;        // dz1, da, dctx, dx, dPd, dqkv
   const int64_t work = std::max(s1, s2);
   return inputs + embed + head + bounds + work;
+}
+
+// Bytes that appear only transiently after the forward (head + one block's
+// backward workspace) plus a 2 % fragmentation margin: what the reactive
+// evictor must leave free.
+int64_t Trainer::dtr_headroom(int S) const {
+  const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
+  const int64_t ld = round8(S);
+  const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
+  const int64_t act = 2 * T * H;
+  const int64_t head = 2 * (2 * B * H) + act;
+  const int64_t s1 = act * 3 + 2 * T * F;
+  const int64_t s2 = act * 4 + quad + 2 * T * 3 * H;
+  return head + std::max(s1, s2) + ctx_->arena.stats().budget / 50;
 }
 
 void Trainer::build_spec() {
@@ -665,6 +757,7 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
   }
   switch (t_.planner) {
     case MIMOSE_PLANNER_NONE:
+    case MIMOSE_PLANNER_DTR:
       return Mode::Plain;
     case MIMOSE_PLANNER_ALL:
       for (int l = 0; l < L_; ++l) plan.dropped_layers.push_back(l);
@@ -755,6 +848,13 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     r->predicted_kept = constant_bytes_;  // informational only
 
   ctx_->arena.reset_peak();
+  {
+    std::pair<cudaEvent_t, cudaEvent_t> ev;
+    ck(cudaEventCreate(&ev.first), "event");
+    ck(cudaEventCreate(&ev.second), "event");
+    ck(cudaEventRecord(ev.first, s), "event");
+    step_ev_.push_back(ev);
+  }
   g_wgrad_ws = wgrad_ws_;
   g_wgrad_ws_bytes = wgrad_ws_bytes_;
 
@@ -778,8 +878,46 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   std::vector<LayerSave> saves(L_);
   std::vector<int64_t> measured(L_, 0);
   const bool collect = mode == Mode::Collect;
+  // ---- DTR-style reactive eviction (reference baselines.hpp:62-159) on the
+  // real arena: before a block needs a_l(x) more bytes than fit under the
+  // budget minus the backward headroom, evict the resident saved set that
+  // maximises staleness * bytes / forward_ms down to its boundary output.
+  const bool dtr = t_.planner == MIMOSE_PLANNER_DTR && !forced_active_;
+  int64_t tick = 0;
+  std::vector<int64_t> last_use(L_, 0);
+  const int64_t dtr_room = ctx_->arena.stats().budget - dtr_headroom(S);
+  auto need_of = [&](int l) {
+    const auto& ls = spec_.layers[static_cast<size_t>(l)];
+    return static_cast<int64_t>(ls.activation_at(static_cast<double>(x)));
+  };
+  auto evict_until = [&](int64_t need, int upto) {
+    while (ctx_->arena.stats().reserved + need > dtr_room) {
+      int victim = -1;
+      double best = -1.0;
+      for (int j = 0; j < upto; ++j) {
+        if (dropped[j] || saves[j].qkv == nullptr) continue;
+        const double ms = std::max(1e-3, spec_.layers[static_cast<size_t>(j)].forward_ms(x));
+        const double score = static_cast<double>(tick - last_use[j]) *
+                             static_cast<double>(std::max<int64_t>(measured[j], 1)) / ms;
+        if (score > best) {
+          best = score;
+          victim = j;
+        }
+      }
+      if (victim < 0) return;  // nothing left to evict: the arena decides
+      free_save(saves[victim]);
+      dropped[victim] = 1;
+      r->plan_size += 1;
+      if (victim < 64) r->dropped_mask_lo |= (uint64_t)1 << victim;
+    }
+  };
   for (int l = 0; l < L_; ++l) {
     const void* hin = l == 0 ? h0 : out[l - 1];
+    if (dtr) {
+      ++tick;
+      evict_until(need_of(l), l);
+      last_use[l] = tick;
+    }
     if (collect) {
       // measuring pass: full save set; the arena's requested-bytes delta is
       // the block's activation footprint a_l(x) (output included), then
@@ -859,6 +997,11 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   // ---- backward through the blocks (recompute dropped ones first)
   for (int l = L_ - 1; l >= 0; --l) {
     const void* hin = l == 0 ? h0 : out[l - 1];
+    if (dtr) {
+      ++tick;
+      if (dropped[l]) evict_until(need_of(l) - 2 * T * H, l);
+      last_use[l] = tick;
+    }
     if (dropped[l]) layer_fwd(l, hin, out[l], &saves[l], g, s);  // recompute, same streams
     void* dx = layer_bwd(l, hin, saves[l], dy, g, s);
     drop(out[l]);
@@ -912,6 +1055,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     cstate_.collected_iterations += 1;
     if (trained_ && ccfg_.collect_new_sizes_always) refit(r);
   }
+  ck(cudaEventRecord(step_ev_.back().second, s), "event");
   history_.push_back(*r);
   iter_ += 1;
 }
@@ -1155,6 +1299,17 @@ int mimose_trainer_estimator_text(mimose_trainer* tr, char** out) {
 int mimose_trainer_model_text(mimose_trainer* tr, char** out) {
   return guarded("mimose_trainer_model_text", [&] {
     *out = dup_string(mimose::model_to_string(tr->impl->spec()));
+  });
+}
+
+int mimose_trainer_report(mimose_trainer* tr, char** summary, char** csv) {
+  return guarded("mimose_trainer_report", [&] {
+    const mimose::SimReport rep = tr->impl->report();
+    std::ostringstream s, c;
+    mimose::write_report_summary(rep, s);
+    mimose::write_report_csv(rep, c);
+    *summary = dup_string(s.str());
+    *csv = dup_string(c.str());
   });
 }
 

@@ -98,6 +98,10 @@ class Trainer {
   int param_count() const { return static_cast<int>(param_names_.size()); }
   void param_info(int i, const char** name, int64_t* off, int64_t* n) const;
   int64_t extras_bytes(int S) const;
+  int64_t dtr_headroom(int S) const;
+  // the run so far in the reference's report schema (harness.hpp:57-118):
+  // per-iteration rows with MEASURED peak bytes and device milliseconds
+  mimose::SimReport report();
 
  private:
   // arena helpers (throw on budget breach)
@@ -169,6 +173,8 @@ class Trainer {
   int adam_t_ = 0;
   int64_t constant_bytes_ = 0;
   std::vector<mimose_step_report> history_;
+  // per-step device time (events on the step's stream), for the report
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_ev_;
 
   bool forced_active_ = false;
   std::vector<int> forced_;

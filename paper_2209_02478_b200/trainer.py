@@ -18,7 +18,7 @@ import numpy as np
 from . import _lib
 from ._lib import MimoseError, check, cuda_lib
 
-PLANNERS = {"mimose": 0, "none": 1, "all": 2, "static-max": 3}
+PLANNERS = {"mimose": 0, "none": 1, "all": 2, "static-max": 3, "dtr": 4}
 PHASES = {0: "planned", 1: "collect", 2: "sheltered", 3: "plain", 4: "fallback-collect"}
 
 
@@ -289,6 +289,12 @@ class Trainer:
 
     def model_text(self) -> str:
         return self._text(self.lib.mimose_trainer_model_text)
+
+    def report(self):
+        """(summary, csv) in the reference's report formats (harness.hpp:339-379)."""
+        a, b = C.c_void_p(), C.c_void_p()
+        check(self.lib.mimose_trainer_report(self.handle, C.byref(a), C.byref(b)))
+        return _lib.take_string(self.lib, a), _lib.take_string(self.lib, b)
 
     def info(self) -> dict:
         c, r, b = C.c_int64(), C.c_int64(), C.c_int64()

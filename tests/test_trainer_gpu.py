@@ -154,4 +154,48 @@ def test_mimose_phases_budget_and_plan_parity(cuda_device):
         assert r["dropped_mask_lo"] == m
         assert r["insufficient"] == i
         assert r["cache_hit"] == h
+    # the run through the reference's own report writers (harness.hpp:339-379)
+    summary, csv = tr.report()
+    lines = csv.strip().splitlines()
+    assert lines[0] == ("iter,x,planner,cache_hit,peak_bytes,iteration_ms,recompute_ms,sheltered,"
+                        "plan_size,insufficient")
+    assert len(lines) == 1 + len(rows)
+    for line, r in zip(lines[1:], rows):
+        f = line.split(",")
+        assert int(f[1]) == r["x"] and f[2] == "mimose" and int(f[4]) == r["peak_reserved"]
+        assert float(f[5]) > 0.0
+    keys = [l.split(":")[0] for l in summary.strip().splitlines()]
+    assert keys[:3] == ["planner", "iterations", "workload_seed"] and "oom_risk_iterations" in keys
+    assert "oom_risk_iterations: 0" in summary
+    tr.close()
+
+
+def test_dtr_reactive_eviction_on_the_arena(cuda_device):
+    """DTR baseline (reference baselines.hpp:62-159) on the real allocator: evicts
+    under pressure, never fails an allocation, and - recompute being
+    deterministic - yields the same gradients as the unconstrained step."""
+    rng = np.random.default_rng(21)
+    S_max, B = 256, 32
+    shape = dict(TINY, layers=6, max_pos=256)
+
+    def make(planner, budget):
+        m = ModelConfig(hidden_dropout=0.1, attn_dropout=0.1, seed=78, **shape)
+        t = TrainConfig(planner=planner, batch=B, seq_min=32, seq_max=S_max)
+        return Trainer(m, t, budget)
+
+    batch = synthetic_batch(rng, B, S_max, TINY["vocab"], 4)
+    ref = make("none", 8 * GiB)
+    r0 = ref.step(*batch, optimizer=False)
+    torch.cuda.synchronize()
+    g0 = ref.grads().clone()
+    peak = r0["peak_reserved"]
+    ref.close()
+    tr = make("dtr", int(0.6 * peak))
+    r1 = tr.step(*batch, optimizer=False)
+    torch.cuda.synchronize()
+    assert r1["plan_size"] > 0                      # evictions happened
+    assert r1["peak_reserved"] <= int(0.6 * peak)
+    assert tr.mem_stats()["n_failures"] == 0
+    assert r1["loss"] == r0["loss"]
+    assert torch.equal(tr.grads(), g0)
     tr.close()
