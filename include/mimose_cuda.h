@@ -139,6 +139,7 @@ typedef struct {
   int collect_new_sizes_always;/* collector.hpp:93 */
   int estimator_order;         /* harness.hpp:53 */
   float lr, beta1, beta2, adam_eps, weight_decay, max_grad_norm;
+  int attn_fused;              /* 1: fused score+softmax kernels (S <= 512); 0: GEMM + softmax kernels */
 } mimose_train_cfg;
 
 enum {

@@ -87,6 +87,7 @@ class TrainCfg(C.Structure):
         ("estimator_order", C.c_int),
         ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
         ("weight_decay", C.c_float), ("max_grad_norm", C.c_float),
+        ("attn_fused", C.c_int),
     ]
 
 

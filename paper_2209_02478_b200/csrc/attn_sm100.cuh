@@ -1,0 +1,368 @@
+// Fused attention-score kernels for sm_100a (S <= 512): the batched
+// contraction runs on tcgen05 with the whole key row of a 128-query tile in
+// TMEM (256 or 512 fp32 columns), and the softmax lives in the epilogue, so
+// the S x S score matrix never round-trips through HBM.
+//
+//   forward : S = alpha * Q K^T  ->  P = softmax(S), Pd = dropout(P)   (P, Pd stored)
+//   backward: dPd = dO V^T       ->  dS = P * (dP - rowsum(dP * P)) * scale,
+//                                    dP = dPd * mask / (1 - p)           (dS stored)
+//
+// Row statistics: the 8 epilogue warps split each row into two column
+// halves (TMEM lane quarter x half); partial max / sum / dot are exchanged
+// through shared memory with a named barrier. Output chunks go through
+// 128B-swizzled staging buffers and TMA bulk stores, like the GEMM epilogue.
+// The materialised P / Pd / dS keep the reference's quadratic activation term
+// (reference proj/models/bert12.model c2) exactly as the unfused path does.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "common.cuh"
+#include "ptx_sm100.cuh"
+
+namespace mimose_dev {
+
+struct AttnParams {
+  int S, ld, nh, B;
+  float alpha;                // fwd: score scale (1/sqrt(d))
+  float ds_scale;             // bwd: scale folded into dS (1/sqrt(d))
+  DropoutCfg drop;
+  const __nv_bfloat16* P;     // bwd: saved probabilities [B][nh][S][ld]
+  int store_pd;               // fwd: also store the dropped-out probabilities
+};
+
+template <int NC>
+struct AttnCfg {
+  static constexpr int kABytes = 128 * 64 * 2;
+  static constexpr int kBBytes = NC * 64 * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStages = NC == 512 ? 1 : 2;
+  static constexpr int kAcc = NC == 512 ? 1 : 2;  // TMEM accumulators (512 columns total)
+  static constexpr int kStagingBytes = 8 * 2 * 4096;
+  static constexpr int kRedBytes = 2 * 2 * 2 * 128 * 4;  // [tile parity][max|sum][half][row]
+  static constexpr int kSmemBytes =
+      kStages * kStageBytes + kStagingBytes + kRedBytes + 1024 + 256;
+};
+
+__device__ __forceinline__ float ex2f(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2_(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+}
+
+template <int NC, bool BWD>
+__global__ void __launch_bounds__(320, 1)
+    attn_scores_kernel(const __grid_constant__ CUtensorMap tmA,
+                       const __grid_constant__ CUtensorMap tmB,
+                       const __grid_constant__ CUtensorMap tmO1,
+                       const __grid_constant__ CUtensorMap tmO2, const AttnParams p) {
+  using Cfg = AttnCfg<NC>;
+  constexpr int NS = Cfg::kStages;
+  constexpr int HALF = NC / 2;
+  constexpr float kLog2e = 1.4426950408889634f;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + NS * Cfg::kABytes;
+  uint8_t* sD = smem + NS * Cfg::kStageBytes;
+  float* red = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [2][2][2][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes + Cfg::kRedBytes);
+  uint64_t* empty = full + NS;
+  uint64_t* tfull = empty + NS;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const int tiles_m = (p.S + 127) / 128;
+  const int num_tiles = tiles_m * p.nh * p.B;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    tma_prefetch(&tmO1);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+        const int z = tile / tiles_m;
+        const int m0 = (tile % tiles_m) * 128;
+        const int b1 = z % p.nh, b2 = z / p.nh;
+        const int s = it % NS;
+        const uint32_t ph = (it / NS) & 1;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+        tma_load_4d(&tmA, &full[s], sA + s * Cfg::kABytes, 0, m0, b1, b2);
+#pragma unroll
+        for (int part = 0; part < NC / 256; ++part)
+          tma_load_4d(&tmB, &full[s], sB + s * Cfg::kBBytes + part * 256 * 128, 0, part * 256, b1,
+                      b2);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = idesc_bf16_f32(128, 256, false, false);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int s = it % NS;
+      const uint32_t ph = (it / NS) & 1;
+      const int acc = it % Cfg::kAcc;
+      const uint32_t aph = (it / Cfg::kAcc) & 1;
+      mbar_wait(&tempty[acc], aph ^ 1);
+      tc_fence_after();
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a_addr = smem_u32(sA + s * Cfg::kABytes);
+        const uint32_t b_addr = smem_u32(sB + s * Cfg::kBBytes);
+#pragma unroll
+        for (int part = 0; part < NC / 256; ++part) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t da = smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+            const uint64_t db = smem_desc_sw128(b_addr + part * 256 * 128 + kk * 32, 16, 1024);
+            umma_bf16(tmem_base + acc * NC + part * 256, da, db, idesc, kk != 0 ? 1u : 0u);
+          }
+        }
+        umma_commit(&empty[s]);
+        umma_commit(&tfull[acc]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 2;
+    const int quarter = warp & 3;
+    const int half = ew >> 2;
+    const int r_local = quarter * 32 + static_cast<int>(lane);
+    uint8_t* wbuf = sD + ew * (2 * 4096);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      // row-statistic exchange buffers, double-buffered by tile parity so a
+      // warp running ahead cannot overwrite what its partner has yet to read
+      float* red_a = red + (it & 1) * 512;  // [2][128] max / dot
+      float* red_b = red_a + 256;           // [2][128] sum
+      const int z = tile / tiles_m;
+      const int m0 = (tile % tiles_m) * 128;
+      const int b1 = z % p.nh, b2 = z / p.nh;
+      const int acc = it % Cfg::kAcc;
+      const uint32_t aph = (it / Cfg::kAcc) & 1;
+      const int i = m0 + r_local;  // query row
+      const bool row_ok = i < p.S;
+      const int64_t grow = ((int64_t)z * p.S + (row_ok ? i : 0));  // row of the [B*nh*S][ld] view
+      mbar_wait(&tfull[acc], aph);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NC + half * HALF;
+      const int c0 = half * HALF;  // first column of this warp's half
+
+      if constexpr (!BWD) {
+        // ---- pass 1: row max (log2 domain)
+        const float sc = p.alpha * kLog2e;
+        float mx = -INFINITY;
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 32) {
+          if (c0 + c >= p.S) break;
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c0 + c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]) * sc);
+        }
+        red_a[half * 128 + r_local] = mx;
+        epi_bar();
+        mx = fmaxf(red_a[r_local], red_a[128 + r_local]);
+        // ---- pass 2: row sum of exp
+        float sum = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 32) {
+          if (c0 + c >= p.S) break;
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 32; ++e)
+            if (c0 + c + e < p.S) sum += ex2f(__uint_as_float(r[e]) * sc - mx);
+        }
+        red_b[half * 128 + r_local] = sum;
+        epi_bar();
+        const float inv = 1.f / (red_b[r_local] + red_b[128 + r_local]);
+        // ---- pass 3: normalise, dropout, stage, TMA store (64-column chunks)
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 64) {
+          if (c0 + c >= p.S) break;
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          float v[64];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t r[32];
+            tmem_ld32_nowait(t_row + c + 32 * h, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) {
+              const int col = c0 + c + 32 * h + e;
+              v[32 * h + e] = col < p.S ? ex2f(__uint_as_float(r[e]) * sc - mx) * inv : 0.f;
+            }
+          }
+          const uint32_t rbase = smem_u32(wbuf) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float pv[8], dv[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pv[e] = bf16r(v[8 * j + e]);
+            const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * j)
+                                      : 0xFFu;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dv[e] = ((m >> e) & 1u) ? pv[e] * p.drop.scale : 0.f;
+            const uint32_t addr = rbase + ((j ^ (lane & 7)) << 4);
+            st_shared_v4(addr, pack_bf16x2_(pv[0], pv[1]), pack_bf16x2_(pv[2], pv[3]),
+                         pack_bf16x2_(pv[4], pv[5]), pack_bf16x2_(pv[6], pv[7]));
+            if (p.store_pd)
+              st_shared_v4(addr + 4096, pack_bf16x2_(dv[0], dv[1]), pack_bf16x2_(dv[2], dv[3]),
+                           pack_bf16x2_(dv[4], dv[5]), pack_bf16x2_(dv[6], dv[7]));
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
+            if (p.store_pd) tma_store_4d(&tmO2, wbuf + 4096, c0 + c, m0 + quarter * 32, b1, b2);
+            bulk_commit();
+          }
+        }
+      } else {
+        // ---- backward: pass 1 dot = sum_j dP_j P_j (dP = dPd * mask * scale)
+        const __nv_bfloat16* prow = p.P + grow * p.ld;
+        float dot = 0.f;
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 32) {
+          if (c0 + c >= p.S) break;
+          uint4 pr[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            pr[q] = (row_ok && c0 + c + 8 * q < p.S)
+                        ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
+                        : make_uint4(0, 0, 0, 0);
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * q)
+                                      : 0u;
+            float pf[8];
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pr[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]);
+              pf[2 * e] = f.x;
+              pf[2 * e + 1] = f.y;
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = c0 + c + 8 * q + e;
+              if (col < p.S && ((m >> e) & 1u))
+                dot += __uint_as_float(r[8 * q + e]) * p.drop.scale * pf[e];
+            }
+          }
+        }
+        red_a[half * 128 + r_local] = dot;
+        epi_bar();
+        dot = red_a[r_local] + red_a[128 + r_local];
+        // ---- pass 2: dS = P * (dP - dot) * scale -> stage -> TMA store
+#pragma unroll 1
+        for (int c = 0; c < HALF; c += 64) {
+          if (c0 + c >= p.S) break;
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          const uint32_t rbase = smem_u32(wbuf) + lane * 128;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint4 pr[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              pr[q] = (row_ok && c0 + c + 32 * h + 8 * q < p.S)
+                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 32 * h + 8 * q)
+                          : make_uint4(0, 0, 0, 0);
+            uint32_t r[32];
+            tmem_ld32_nowait(t_row + c + 32 * h, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int colq = c0 + c + 32 * h + 8 * q;
+              const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + colq) : 0u;
+              float pf[8], ds[8];
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pr[q]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                pf[2 * e] = f.x;
+                pf[2 * e + 1] = f.y;
+              }
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const bool in = colq + e < p.S;
+                const float g = (in && ((m >> e) & 1u)) ? __uint_as_float(r[8 * q + e]) * p.drop.scale
+                                                        : 0.f;
+                ds[e] = in ? pf[e] * (g - dot) * p.ds_scale : 0.f;
+              }
+              const int j = 4 * h + q;  // 16-byte chunk index inside the 128-byte row
+              st_shared_v4(rbase + ((j ^ (lane & 7)) << 4), pack_bf16x2_(ds[0], ds[1]),
+                           pack_bf16x2_(ds[2], ds[3]), pack_bf16x2_(ds[4], ds[5]),
+                           pack_bf16x2_(ds[6], ds[7]));
+            }
+          }
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
+            bulk_commit();
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace mimose_dev

@@ -14,6 +14,7 @@
 
 #include "gemm_sm100.cuh"
 #include "ops.hpp"
+#include "ops_attn.hpp"
 
 namespace mimose_ops {
 
@@ -225,6 +226,16 @@ double wave_eff(int64_t tiles) {
 }
 
 }  // namespace
+
+bool make_operand_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box_rows) {
+  return make_map(map, v, nb1, nb2, box_rows);
+}
+
+bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                     int64_t bs1, int64_t bs2, int nb1, int nb2) {
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16) return false;
+  return make_map_t(map, ptr, rows, cols, ld, bs1, bs2, nb1, nb2, 64, 32, 2);
+}
 
 int pick_split_k(int M, int N, int K, int bn) {
   const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + bn - 1) / bn);

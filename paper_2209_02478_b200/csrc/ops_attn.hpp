@@ -1,0 +1,31 @@
+// Fused attention-score operators (attn.cu) and the tensor-map helpers they
+// share with the GEMM (gemm.cu).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dropout_cfg.hpp"
+#include "ops.hpp"
+
+namespace mimose_ops {
+
+// bf16 operand map over a 4-D view with a {64, box_rows} SWIZZLE_128B box
+bool make_operand_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box_rows);
+// bf16 output map (rows x cols, pitch ld, batch strides) with a {64, 32} box
+bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
+                     int64_t bs1, int64_t bs2, int nb1, int nb2);
+
+bool attn_fused_supported(int S);
+// P = softmax(alpha * Q K^T), Pd = dropout(P) (Pd may be null when p = 0)
+cudaError_t attn_scores_fwd(const MatView& q, const MatView& k, void* P, void* Pd, int S, int ld,
+                            int nh, int B, float alpha, const mimose_dev::DropoutCfg& drop,
+                            cudaStream_t s);
+// dS = P * (dP - rowsum(dP * P)) * ds_scale with dP = dropout'(dO V^T)
+cudaError_t attn_scores_bwd(const MatView& dout, const MatView& v, const void* P, void* dS, int S,
+                            int ld, int nh, int B, float ds_scale,
+                            const mimose_dev::DropoutCfg& drop, cudaStream_t s);
+
+}  // namespace mimose_ops

@@ -10,6 +10,7 @@
 #include <stdexcept>
 
 #include "ops.hpp"
+#include "ops_attn.hpp"
 #include "ops_mem.hpp"
 #include "trainer.hpp"
 
@@ -496,9 +497,17 @@ void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const St
   run_gemm(linear_call(h, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
                    p32_ + P.bqkv.off),
        s);
-  // scores = q k^T / sqrt(64), batched over (head, sequence)
-  void* sc = take(quad, kTagTransient);
-  {
+  void* Pm = take(quad, act_tag);
+  void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
+  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+  if (t_.attn_fused && mimose_ops::attn_fused_supported(S)) {
+    // fused: scores stay in TMEM, softmax + dropout in the epilogue
+    ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
+                                   Pd, S, ld, nh, g.B, 0.125f, pdrop, s),
+       "attn_scores_fwd");
+  } else {
+    // scores = q k^T / sqrt(64), batched over (head, sequence); then softmax
+    void* sc = take(quad, kTagTransient);
     GemmCall c;
     c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
     c.A = head_view(qkv, 0, S, 3 * H);
@@ -507,12 +516,9 @@ void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const St
     c.out = sc; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
     c.alpha = 0.125f;
     run_gemm(c, s);
+    ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s), "softmax_fwd");
+    drop(sc);
   }
-  void* Pm = take(quad, act_tag);
-  void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
-  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s), "softmax_fwd");
-  drop(sc);
   // ctx = Pd V, written head-interleaved into [T, H]
   void* ctx = take(T * H * 2, act_tag);
   {
@@ -646,16 +652,6 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
   drop(da);
   // attention: dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
-  void* dP = take(quad, kTagTransient);
-  {
-    GemmCall c;
-    c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
-    c.A = head_view(dctx, 0, S, H);
-    c.B = head_view(sv.qkv, 2 * H, S, 3 * H);
-    c.epi = mimose_ops::kEpiBf16;
-    c.out = dP; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
-    run_gemm(c, s);
-  }
   void* dqkv = take(T * 3 * H * 2, kTagTransient);
   {
     GemmCall c;
@@ -669,10 +665,26 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
     c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
     run_gemm(c, s);
   }
-  drop(dctx);
   drop(sv.Pd);
+  void* dP = take(quad, kTagTransient);
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  ck(mimose_ops::softmax_bwd(sv.P, dP, (int64_t)g.B * nh * S, S, ld, pdrop, 0.125f, s), "softmax_bwd");
+  if (t_.attn_fused && mimose_ops::attn_fused_supported(S)) {
+    // fused: dPd stays in TMEM; softmax backward in the epilogue writes dS
+    ck(mimose_ops::attn_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
+                                   sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop, s),
+       "attn_scores_bwd");
+  } else {
+    GemmCall c;
+    c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
+    c.A = head_view(dctx, 0, S, H);
+    c.B = head_view(sv.qkv, 2 * H, S, 3 * H);
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = dP; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
+    run_gemm(c, s);
+    ck(mimose_ops::softmax_bwd(sv.P, dP, (int64_t)g.B * nh * S, S, ld, pdrop, 0.125f, s),
+       "softmax_bwd");
+  }
+  drop(dctx);
   drop(sv.P);
   {
     GemmCall c;  // dQ = dS K

@@ -63,6 +63,9 @@ class TrainConfig:
     adam_eps: float = 1e-8
     weight_decay: float = 0.01
     max_grad_norm: float = 1.0
+    # fused score+softmax kernels (attn_sm100.cuh). Measured slower than the
+    # GEMM + softmax-kernel pair for S < 512 (profiles/README.md), so opt-in.
+    attn_fused: bool = False
 
     def to_c(self):
         c = _lib.TrainCfg()

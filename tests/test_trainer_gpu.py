@@ -51,11 +51,14 @@ def _grads_by_name(tr):
     return {name: g[off:off + n].copy() for name, (off, n) in tr.param_table().items()}
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
-@pytest.mark.parametrize("S", [16, 45])
-def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S):
+@pytest.mark.parametrize("S", [16, 45, 96])
+def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
+    """Fused (scores in TMEM, softmax in the epilogue) and unfused attention
+    paths both match the fp32 CPU oracle."""
     from oracle import bert_ref
-    tr = _tiny_trainer(dropout=dropout)
+    tr = _tiny_trainer(dropout=dropout, attn_fused=fused)
     rng = np.random.default_rng(5)
     tok, typ, lab = synthetic_batch(rng, 8, S, TINY["vocab"], 4)
     params = _oracle_params(tr)
@@ -78,14 +81,15 @@ def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S):
     tr.close()
 
 
-def test_checkpointed_grads_bitwise_equal_plain(cuda_device):
+@pytest.mark.parametrize("fused", [False, True])
+def test_checkpointed_grads_bitwise_equal_plain(cuda_device, fused):
     """Recompute is deterministic: dropping any subset of blocks gives the
     exact same gradients (dropout on, so Philox regeneration is exercised)."""
     rng = np.random.default_rng(9)
     tok, typ, lab = synthetic_batch(rng, 8, 40, TINY["vocab"], 4)
     grads = []
     for forced in ([], [0], [1], [0, 1]):
-        tr = _tiny_trainer(dropout=0.1)
+        tr = _tiny_trainer(dropout=0.1, attn_fused=fused)
         tr.force_plan(forced)
         rep = tr.step(tok, typ, lab, optimizer=False)
         assert rep["dropped"] == forced

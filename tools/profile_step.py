@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--seq", type=int, default=288)
     ap.add_argument("--planner", default="mimose")
     ap.add_argument("--gemm-csv", default="")
+    ap.add_argument("--attn-fused", action="store_true")
+    ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -31,7 +33,8 @@ def main():
     peak = probe.rows[-1]["peak_reserved"]
     probe.close()
     budget = int(args.budget_frac * peak) if args.planner == "mimose" else int(1.2 * peak)
-    tr = Trainer(m, dataclasses.replace(t, planner=args.planner), budget)
+    tr = Trainer(m, dataclasses.replace(t, planner=args.planner, attn_fused=args.attn_fused),
+                 budget)
     for s in [64, 512, 200, 350, 128, 480, 300, 96, 420, 256, 160, 384]:
         tr.step(*synthetic_batch(rng, t.batch, s, m.vocab, m.num_choices))
     db = DeviceBatch.from_host(*synthetic_batch(rng, t.batch, args.seq, m.vocab, m.num_choices),
@@ -46,6 +49,15 @@ def main():
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     print({k: r[k] for k in ("seq", "phase_name", "plan_size", "peak_reserved")})
+    if args.time_steps:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.time_steps):
+            tr.step_device(db)
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"seq {args.seq} attn_fused={args.attn_fused}: "
+              f"{e0.elapsed_time(e1) / args.time_steps:.3f} ms/step (plan_size {r['plan_size']})")
     if args.gemm_csv:
         p = C.c_void_p()
         lib.mimose_gemm_profile_csv(C.byref(p))
