@@ -113,11 +113,23 @@ int mimose_gemm_profile_csv(char** out);
  * the context's byte budget. Replaces the reference's replayed iteration
  * (harness.hpp:139 run_experiment, Mimose branch harness.hpp:215-296) with a
  * real one; planning calls the host planner (include/mimose) in-process. */
+enum { MIMOSE_ARCH_BERT = 0, MIMOSE_ARCH_GPT2 = 1 };
+enum { MIMOSE_HEAD_MC = 0, MIMOSE_HEAD_QA = 1, MIMOSE_HEAD_LM = 2, MIMOSE_HEAD_MLM = 3 };
+
+/* Label layouts per head (int32): MC [batch/num_choices] choice ids; QA
+ * [2*batch] (start, end) positions; LM [batch*seq] next-token ids, -1 ignored;
+ * MLM [batch*seq] original ids at masked positions, -1 elsewhere. LM and MLM
+ * decoders are tied to the word embeddings. */
 typedef struct {
-  int layers, hidden, heads, ffn, vocab, max_pos, type_vocab;
+  int layers, hidden, heads, ffn, vocab, max_pos, type_vocab; /* type_vocab 0: none */
   int num_choices;        /* multiple-choice group size C (batch % C == 0) */
   float hidden_dropout, attn_dropout, ln_eps, init_std;
   uint64_t seed;
+  int arch;               /* MIMOSE_ARCH_BERT: post-LN block, embedding LayerNorm;
+                             MIMOSE_ARCH_GPT2: pre-LN block, final LayerNorm */
+  int head;               /* MIMOSE_HEAD_* */
+  int causal;             /* causal self-attention mask */
+  int gelu_tanh;          /* GELU tanh approximation (GPT-2 "gelu_new") instead of erf */
 } mimose_model_cfg;
 
 enum {

@@ -97,15 +97,32 @@ def stream_id(step: int, layer: int, site: int) -> int:
 
 
 # ----------------------------------------------------------------- model
+ARCH_BERT, ARCH_GPT2 = 0, 1
+HEAD_MC, HEAD_QA, HEAD_LM, HEAD_MLM = 0, 1, 2, 3
+
+
+def _c(cfg, name, default=0):
+    return getattr(cfg, name, default)
+
+
 def param_shapes(cfg) -> Dict[str, tuple]:
     H, F, V, P, Ty = cfg.hidden, cfg.ffn, cfg.vocab, cfg.max_pos, cfg.type_vocab
-    shp = {
-        "embeddings.word": (V, H), "embeddings.position": (P, H),
-        "embeddings.token_type": (Ty, H),
-        "embeddings.ln.weight": (H,), "embeddings.ln.bias": (H,),
-        "pooler.weight": (H, H), "pooler.bias": (H,),
-        "classifier.weight": (H,), "classifier.bias": (1,),
-    }
+    arch, head = _c(cfg, "arch"), _c(cfg, "head")
+    shp = {"embeddings.word": (V, H), "embeddings.position": (P, H)}
+    if Ty > 0:
+        shp["embeddings.token_type"] = (Ty, H)
+    if arch == ARCH_BERT:
+        shp.update({"embeddings.ln.weight": (H,), "embeddings.ln.bias": (H,)})
+    else:
+        shp.update({"final_ln.weight": (H,), "final_ln.bias": (H,)})
+    if head == HEAD_MC:
+        shp.update({"pooler.weight": (H, H), "pooler.bias": (H,),
+                    "classifier.weight": (H,), "classifier.bias": (1,)})
+    elif head == HEAD_QA:
+        shp.update({"qa.weight": (2, H), "qa.bias": (2,)})
+    elif head == HEAD_MLM:
+        shp.update({"mlm.transform.weight": (H, H), "mlm.transform.bias": (H,),
+                    "mlm.ln.weight": (H,), "mlm.ln.bias": (H,), "mlm.decoder.bias": (V,)})
     for l in range(cfg.layers):
         p = f"layer.{l}."
         shp.update({
@@ -128,19 +145,29 @@ def _drop(x: torch.Tensor, p: float, seed: int, stream: int, idx: np.ndarray) ->
 
 def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.ndarray,
                    labels: np.ndarray, cfg, step: int = 0, dtype=torch.float32):
-    """Forward + backward on CPU. Returns (loss, logits, {name: grad ndarray})."""
+    """Forward + backward on CPU. Returns (loss, logits, {name: grad ndarray}).
+
+    Architectures (cfg.arch): 0 post-LN BERT block, 1 pre-LN GPT-2 block
+    (attention causal when cfg.causal). Heads (cfg.head) and label layouts:
+      0 multiple choice  labels [B / C]
+      1 extractive QA    labels [2 B] = (start, end) per sequence
+      2 causal LM (tied) labels [B * S] next-token ids, -1 ignored
+      3 masked LM (tied) labels [B * S] original ids at masked positions, -1 elsewhere
+    """
     shapes = param_shapes(cfg)
     P = {k: torch.tensor(np.asarray(v, dtype=np.float64).reshape(shapes[k]), dtype=dtype,
                          requires_grad=True) for k, v in params.items() if k in shapes}
     B, S = tokens.shape
     H, nh, L = cfg.hidden, cfg.heads, cfg.layers
+    arch, head = _c(cfg, "arch"), _c(cfg, "head")
+    causal = bool(_c(cfg, "causal"))
+    gelu_kind = "tanh" if _c(cfg, "gelu_tanh") else "none"
     d = H // nh
     T = B * S
     ld = (S + 7) // 8 * 8
     seed = cfg.seed
     ph, pa = cfg.hidden_dropout, cfg.attn_dropout
     tok = torch.from_numpy(tokens.astype(np.int64)).reshape(-1)
-    typ = torch.from_numpy(types.astype(np.int64)).reshape(-1)
     pos = torch.arange(S).repeat(B)
     hid_idx = (np.arange(T, dtype=np.uint64)[:, None] * np.uint64(H)
                + np.arange(H, dtype=np.uint64)[None, :])
@@ -148,37 +175,77 @@ def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.
     def ln(x, w, b):
         return torch.nn.functional.layer_norm(x, (H,), P[w], P[b], eps=cfg.ln_eps)
 
-    e = P["embeddings.word"][tok] + P["embeddings.position"][pos] + P["embeddings.token_type"][typ]
-    h = _drop(ln(e, "embeddings.ln.weight", "embeddings.ln.bias"), ph, seed,
-              stream_id(step, L, SITE_EMBED), hid_idx)
+    e = P["embeddings.word"][tok] + P["embeddings.position"][pos]
+    if cfg.type_vocab > 0:
+        typ = torch.from_numpy(types.astype(np.int64)).reshape(-1)
+        e = e + P["embeddings.token_type"][typ]
+    if arch == ARCH_BERT:
+        e = ln(e, "embeddings.ln.weight", "embeddings.ln.bias")
+    h = _drop(e, ph, seed, stream_id(step, L, SITE_EMBED), hid_idx)
     rows = np.arange(B * nh * S, dtype=np.uint64).reshape(B, nh, S, 1)
     att_idx = rows * np.uint64(ld) + np.arange(S, dtype=np.uint64)[None, None, None, :]
-    for l in range(L):
-        p = f"layer.{l}."
-        qkv = h @ P[p + "attn.qkv.weight"].T + P[p + "attn.qkv.bias"]
+    cmask = torch.triu(torch.ones(S, S, dtype=torch.bool), diagonal=1) if causal else None
+
+    def attention(x, p, l):
+        qkv = x @ P[p + "attn.qkv.weight"].T + P[p + "attn.qkv.bias"]
         q, k, v = (qkv[:, i * H:(i + 1) * H].reshape(B, S, nh, d).permute(0, 2, 1, 3)
                    for i in range(3))
         sc = (q @ k.transpose(-1, -2)) / math.sqrt(d)
+        if cmask is not None:
+            sc = sc.masked_fill(cmask, float("-inf"))
         pr = torch.softmax(sc, dim=-1)
         pr = _drop(pr, pa, seed, stream_id(step, l, SITE_ATTN_PROBS), att_idx)
         ctx = (pr @ v).permute(0, 2, 1, 3).reshape(T, H)
-        a = ctx @ P[p + "attn.out.weight"].T + P[p + "attn.out.bias"]
-        h1 = ln(h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx),
-                p + "attn.ln.weight", p + "attn.ln.bias")
-        u = h1 @ P[p + "ffn.in.weight"].T + P[p + "ffn.in.bias"]
-        g = torch.nn.functional.gelu(u)
-        f = g @ P[p + "ffn.out.weight"].T + P[p + "ffn.out.bias"]
-        h = ln(h1 + _drop(f, ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx),
-               p + "ffn.ln.weight", p + "ffn.ln.bias")
-    cls = h.reshape(B, S, H)[:, 0, :]
-    pooled = torch.tanh(cls @ P["pooler.weight"].T + P["pooler.bias"])
-    pool_idx = (np.arange(B, dtype=np.uint64)[:, None] * np.uint64(H)
-                + np.arange(H, dtype=np.uint64)[None, :])
-    pooled = _drop(pooled, ph, seed, stream_id(step, L, SITE_POOL), pool_idx)
-    logits = pooled @ P["classifier.weight"] + P["classifier.bias"]
-    C = cfg.num_choices
-    lg = logits.reshape(B // C, C)
-    loss = torch.nn.functional.cross_entropy(lg, torch.from_numpy(labels.astype(np.int64)))
+        return ctx @ P[p + "attn.out.weight"].T + P[p + "attn.out.bias"]
+
+    def ffn(x, p):
+        u = x @ P[p + "ffn.in.weight"].T + P[p + "ffn.in.bias"]
+        return torch.nn.functional.gelu(u, approximate=gelu_kind) @ P[p + "ffn.out.weight"].T \
+            + P[p + "ffn.out.bias"]
+
+    for l in range(L):
+        p = f"layer.{l}."
+        if arch == ARCH_BERT:
+            a = attention(h, p, l)
+            h1 = ln(h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx),
+                    p + "attn.ln.weight", p + "attn.ln.bias")
+            h = ln(h1 + _drop(ffn(h1, p), ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx),
+                   p + "ffn.ln.weight", p + "ffn.ln.bias")
+        else:
+            a = attention(ln(h, p + "attn.ln.weight", p + "attn.ln.bias"), p, l)
+            h1 = h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx)
+            f = ffn(ln(h1, p + "ffn.ln.weight", p + "ffn.ln.bias"), p)
+            h = h1 + _drop(f, ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx)
+    if arch == ARCH_GPT2:
+        h = ln(h, "final_ln.weight", "final_ln.bias")
+
+    lab = torch.from_numpy(labels.astype(np.int64))
+    if head == HEAD_MC:
+        cls = h.reshape(B, S, H)[:, 0, :]
+        pooled = torch.tanh(cls @ P["pooler.weight"].T + P["pooler.bias"])
+        pool_idx = (np.arange(B, dtype=np.uint64)[:, None] * np.uint64(H)
+                    + np.arange(H, dtype=np.uint64)[None, :])
+        pooled = _drop(pooled, ph, seed, stream_id(step, L, SITE_POOL), pool_idx)
+        logits = pooled @ P["classifier.weight"] + P["classifier.bias"]
+        C = cfg.num_choices
+        loss = torch.nn.functional.cross_entropy(logits.reshape(B // C, C), lab)
+    elif head == HEAD_QA:
+        logits = (h @ P["qa.weight"].T + P["qa.bias"]).reshape(B, S, 2)
+        st, en = lab.reshape(B, 2)[:, 0], lab.reshape(B, 2)[:, 1]
+        loss = 0.5 * (torch.nn.functional.cross_entropy(logits[..., 0], st)
+                      + torch.nn.functional.cross_entropy(logits[..., 1], en))
+    elif head == HEAD_LM:
+        logits = h @ P["embeddings.word"].T
+        loss = torch.nn.functional.cross_entropy(logits, lab, ignore_index=-1)
+    else:
+        sel = lab >= 0
+        x = h[sel]
+        t = x @ P["mlm.transform.weight"].T + P["mlm.transform.bias"]
+        t = torch.nn.functional.gelu(t, approximate=gelu_kind)
+        t = torch.nn.functional.layer_norm(t, (H,), P["mlm.ln.weight"], P["mlm.ln.bias"],
+                                           eps=cfg.ln_eps)
+        logits = t @ P["embeddings.word"].T + P["mlm.decoder.bias"]
+        loss = torch.nn.functional.cross_entropy(logits, lab[sel])
     loss.backward()
     grads = {k: t.grad.detach().numpy().reshape(-1).copy() for k, t in P.items()}
     return float(loss.detach()), logits.detach().numpy(), grads

@@ -75,6 +75,7 @@ class ModelCfg(C.Structure):
         ("hidden_dropout", C.c_float), ("attn_dropout", C.c_float), ("ln_eps", C.c_float),
         ("init_std", C.c_float),
         ("seed", C.c_uint64),
+        ("arch", C.c_int), ("head", C.c_int), ("causal", C.c_int), ("gelu_tanh", C.c_int),
     ]
 
 

@@ -293,6 +293,10 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   p.bias = c.bias;
   p.ldo = c.ldo; p.obs1 = c.obs1; p.obs2 = c.obs2;
   p.alpha = c.alpha; p.beta = c.beta;
+  p.gelu_tanh = c.gelu_tanh;
+  p.drop = c.drop;
+  if (c.drop.threshold != 0 && (c.epi != kEpiBf16 || c.nb1 != 1 || c.nb2 != 1 || c.N % 8 != 0))
+    return cudaErrorInvalidValue;  // dropout index = row * ldo + col, 8-column groups
   {
     const int64_t vel = c.epi == kEpiF32 ? 4 : 8;  // elements per 16 bytes
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };

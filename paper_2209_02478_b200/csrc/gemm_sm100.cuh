@@ -24,6 +24,7 @@
 
 #include <cstdint>
 
+#include "common.cuh"
 #include "ptx_sm100.cuh"
 
 namespace mimose_dev {
@@ -49,6 +50,8 @@ struct GemmParams {
   int tma_store;            // 1: stage through smem + TMA store
   int splits;               // split-K factor (>1: fp32 partials, batch must be 1)
   int kb_per_split;         // k-blocks per split
+  int gelu_tanh;            // GELU flavour of kEpiBiasGelu / kEpiDGelu: 0 erf, 1 tanh
+  DropoutCfg drop;          // kEpiBf16: dropout on (alpha*acc + bias) before adding aux
 };
 
 constexpr int kBM = 128;
@@ -129,6 +132,24 @@ __device__ __forceinline__ float dgelu_f(float x) {
 }
 #endif
 
+// tanh-approximation GELU ("gelu_new", GPT-2): 0.5 x (1 + tanh(k0 (x + k1 x^3)))
+__device__ __forceinline__ float tanh_approx(float x) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float gelu_tanh_f(float x) {
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  return 0.5f * x * (1.0f + tanh_approx(u));
+}
+__device__ __forceinline__ float dgelu_tanh_f(float x) {
+  const float x2 = x * x;
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x2, x);
+  const float t = tanh_approx(u);
+  const float du = 0.7978845608028654f * fmaf(0.134145f, x2, 1.0f);
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * du;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -159,6 +180,18 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
       }
     }
   }
+  if constexpr (EPI == kEpiBf16) {
+    // branch dropout (pre-LN residual: out = aux + dropout(x W^T + b))
+    if (p.drop.threshold != 0) {
+#pragma unroll
+      for (int q = 0; q < NV / 8; ++q) {
+        const uint32_t m = dropout_mask8(p.drop, (uint64_t)obase + col0 + 8 * q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          v[8 * q + e] = ((m >> e) & 1u) ? v[8 * q + e] * p.drop.scale : 0.f;
+      }
+    }
+  }
   if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
     if (p.aux != nullptr && row_ok) {
       const __nv_bfloat16* ax = p.aux + obase + col0;
@@ -172,7 +205,7 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
           for (int i = 0; i < 8; ++i) {
             const float a = __bfloat162float(av[i]);
             if constexpr (EPI == kEpiBf16) v[8 * q + i] += a;
-            else v[8 * q + i] *= dgelu_f(a);
+            else v[8 * q + i] *= p.gelu_tanh ? dgelu_tanh_f(a) : dgelu_f(a);
           }
         }
       } else {
@@ -181,7 +214,7 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
           if (col0 + i < p.N) {
             const float a = __bfloat162float(ax[i]);
             if constexpr (EPI == kEpiBf16) v[i] += a;
-            else v[i] *= dgelu_f(a);
+            else v[i] *= p.gelu_tanh ? dgelu_tanh_f(a) : dgelu_f(a);
           }
         }
       }
@@ -193,7 +226,7 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       v[i] = __bfloat162float(__float2bfloat16_rn(v[i]));
-      g[i] = gelu_f(v[i]);
+      g[i] = p.gelu_tanh ? gelu_tanh_f(v[i]) : gelu_f(v[i]);
     }
   }
 }

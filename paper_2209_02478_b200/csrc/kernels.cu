@@ -29,6 +29,19 @@ template <int VPL>
 __device__ __forceinline__ void ln_row_finish(float (&z)[VPL][8], int row, int lane,
                                               const mimose_ops::LnFwdArgs& a) {
   constexpr int H = VPL * 256;
+  if (a.skip_ln) {  // plain (residual) sum: y = dropout_out(z)
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      const uint64_t idx = (uint64_t)row * H + col;
+      const uint32_t m = dropout_mask8(a.out_drop, idx);
+      float y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[e] = ((m >> e) & 1u) ? z[c][e] * a.out_drop.scale : 0.f;
+      store8(static_cast<bf16*>(a.y) + idx, y);
+    }
+    return;
+  }
   // z arrives already rounded to bf16 (what is saved is what is normalised)
   float s = 0.f;
 #pragma unroll
@@ -105,16 +118,16 @@ __global__ void __launch_bounds__(256) embed_ln_fwd_kernel(const mimose_ops::LnF
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (row >= a.rows) return;
   const int64_t w = tok[row];
-  const int64_t t = tt[row];
+  const int64_t t = tt != nullptr ? tt[row] : 0;
   const int64_t s = row % S;
   float z[VPL][8];
 #pragma unroll
   for (int c = 0; c < VPL; ++c) {
     const int col = 8 * (lane + 32 * c);
-    float x0[8], x1[8], x2[8];
+    float x0[8], x1[8], x2[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     load8(word + w * H + col, x0);
     load8(pos + s * H + col, x1);
-    load8(type + t * H + col, x2);
+    if (type != nullptr) load8(type + t * H + col, x2);
 #pragma unroll
     for (int e = 0; e < 8; ++e) z[c][e] = bf16r(x0[e] + x1[e] + x2[e]);
     if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + (uint64_t)row * H + col, z[c]);
@@ -180,6 +193,12 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const mimose_ops::LnBwdArgs
       float dz[8];
 #pragma unroll
       for (int e = 0; e < 8; ++e) dz[e] = st.y * (gg[c][e] - mg - xh[c][e] * mgx);
+      if (a.dres != nullptr) {
+        float rr[8];
+        load8(static_cast<const bf16*>(a.dres) + idx, rr);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dz[e] += rr[e];
+      }
       store8(static_cast<bf16*>(a.dz) + idx, dz);
       const uint32_t m = dropout_mask8(a.br_drop, idx);
       float db[8];
@@ -315,7 +334,8 @@ template <int L, int MAXC>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict__ s_in,
                                                           bf16* __restrict__ p_out,
                                                           bf16* __restrict__ pd_out, int64_t rows,
-                                                          int S, int ld, DropoutCfg drop) {
+                                                          int S, int ld, DropoutCfg drop,
+                                                          int causal) {
   constexpr int R = 32 / L;
   constexpr float kLog2e = 1.4426950408889634f;
   const int lane = threadIdx.x & 31;
@@ -323,11 +343,13 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
   const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
   const bool live = row < rows;
   const bf16* in = s_in + (live ? row : 0) * ld;
+  // causal: keys j > query i (= row within its sequence) are masked out
+  const int jmax = causal ? static_cast<int>(row % S) + 1 : S;
   uint4 raw[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    raw[c] = (live && j0 < S) ? *reinterpret_cast<const uint4*>(in + j0) : make_uint4(0, 0, 0, 0);
+    raw[c] = (live && j0 < jmax) ? *reinterpret_cast<const uint4*>(in + j0) : make_uint4(0, 0, 0, 0);
   }
   float v[MAXC][8];
   float mx = -INFINITY;
@@ -337,7 +359,7 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
     unpack8(raw[c], v[c]);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      v[c][e] = (live && j0 + e < S) ? v[c][e] * kLog2e : -INFINITY;
+      v[c][e] = (live && j0 + e < jmax) ? v[c][e] * kLog2e : -INFINITY;
       mx = fmaxf(mx, v[c][e]);
     }
   }
@@ -434,7 +456,8 @@ __global__ void __launch_bounds__(256) embed_word_grad_kernel(const bf16* __rest
                                                               const int32_t* __restrict__ seg,
                                                               const int32_t* __restrict__ uid,
                                                               int n_unique,
-                                                              float* __restrict__ dword) {
+                                                              float* __restrict__ dword,
+                                                              int accumulate) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (u >= n_unique) return;
@@ -449,6 +472,11 @@ __global__ void __launch_bounds__(256) embed_word_grad_kernel(const bf16* __rest
       for (int i = 0; i < 8; ++i) acc[i] += v[i];
     }
     float4* o4 = reinterpret_cast<float4*>(out + c0);
+    if (accumulate) {  // tied decoder: its weight gradient is already in place
+      const float4 p0 = o4[0], p1 = o4[1];
+      acc[0] = p0.x + acc[0]; acc[1] = p0.y + acc[1]; acc[2] = p0.z + acc[2]; acc[3] = p0.w + acc[3];
+      acc[4] = p1.x + acc[4]; acc[5] = p1.y + acc[5]; acc[6] = p1.z + acc[6]; acc[7] = p1.w + acc[7];
+    }
     o4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     o4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
@@ -643,6 +671,225 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ in, bf16* __restric
     out[i] = __float2bfloat16_rn(in[i]);
 }
 
+
+// =====================================================================
+// elementwise helpers, row gather / scatter, deterministic sums
+// =====================================================================
+__global__ void dropout_apply_kernel(const bf16* __restrict__ in, bf16* __restrict__ out,
+                                     int64_t n8, DropoutCfg d) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float v[8];
+    load8(in + 8 * i, v);
+    const uint32_t m = dropout_mask8(d, (uint64_t)(8 * i));
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = ((m >> e) & 1u) ? v[e] * d.scale : 0.f;
+    store8(out + 8 * i, v);
+  }
+}
+
+__device__ __forceinline__ float gelu_erf_grad(float x) {
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
+         x * 0.39894228040143268f * __expf(-0.5f * x * x);
+}
+__device__ __forceinline__ float gelu_tanh_grad(float x) {
+  const float x2 = x * x;
+  const float t = tanhf(0.7978845608028654f * fmaf(0.044715f * x, x2, x));
+  return 0.5f * (1.0f + t) + 0.5f * x * (1.0f - t * t) * 0.7978845608028654f * fmaf(0.134145f, x2, 1.0f);
+}
+
+__global__ void dgelu_apply_kernel(const bf16* __restrict__ dg, const bf16* __restrict__ u,
+                                   bf16* __restrict__ out, int64_t n8, int tanh_form) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float a[8], x[8];
+    load8(dg + 8 * i, a);
+    load8(u + 8 * i, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) a[e] *= tanh_form ? gelu_tanh_grad(x[e]) : gelu_erf_grad(x[e]);
+    store8(out + 8 * i, a);
+  }
+}
+
+// one warp per row
+__global__ void gather_rows_kernel(const bf16* __restrict__ src, const int32_t* __restrict__ idx,
+                                   int n, int H, bf16* __restrict__ dst, int scatter) {
+  const int r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= n) return;
+  const int64_t from = scatter ? r : idx[r];
+  const int64_t to = scatter ? idx[r] : r;
+  for (int c = lane * 8; c < H; c += 256)
+    *reinterpret_cast<uint4*>(dst + to * H + c) = *reinterpret_cast<const uint4*>(src + from * H + c);
+}
+
+// single CTA, fixed order: out = scale * sum x
+__global__ void __launch_bounds__(1024) sum_f32_kernel(const float* __restrict__ x, int n,
+                                                       float scale, float* __restrict__ out) {
+  __shared__ float red[1024];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < n; i += 1024) acc += x[i];
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0] * scale;
+}
+
+// =====================================================================
+// extractive-QA head (one CTA per sequence)
+// =====================================================================
+__global__ void __launch_bounds__(512) qa_head_kernel(const bf16* __restrict__ x, int S, int H,
+                                                      const float* __restrict__ w,
+                                                      const float* __restrict__ bias,
+                                                      const int32_t* __restrict__ labels,
+                                                      float inv_count,
+                                                      float* __restrict__ logits,
+                                                      float* __restrict__ dl,
+                                                      float* __restrict__ loss_parts) {
+  extern __shared__ float sh[];  // [2][S]
+  const int b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int t = warp; t < S; t += nw) {
+    const bf16* row = x + ((int64_t)b * S + t) * H;
+    float s0 = 0.f, s1 = 0.f;
+    for (int c = lane * 8; c < H; c += 256) {
+      float v[8];
+      load8(row + c, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        s0 += v[e] * w[c + e];
+        s1 += v[e] * w[H + c + e];
+      }
+    }
+    s0 = warp_sum(s0);
+    s1 = warp_sum(s1);
+    if (lane == 0) {
+      sh[t] = s0 + bias[0];
+      sh[S + t] = s1 + bias[1];
+    }
+  }
+  __syncthreads();
+  // two warps: k = 0 (start) and k = 1 (end) softmax / CE over the S positions
+  if (warp < 2) {
+    const int k = warp;
+    float* lg = sh + k * S;
+    float mx = -INFINITY;
+    for (int t = lane; t < S; t += 32) mx = fmaxf(mx, lg[t]);
+    mx = warp_max(mx);
+    float se = 0.f;
+    for (int t = lane; t < S; t += 32) se += expf(lg[t] - mx);
+    se = warp_sum(se);
+    const float lse = mx + logf(se);
+    const int lab = labels[2 * b + k];
+    for (int t = lane; t < S; t += 32) {
+      const int64_t r = (int64_t)b * S + t;
+      logits[2 * r + k] = lg[t];
+      dl[2 * r + k] = (expf(lg[t] - lse) - (t == lab ? 1.f : 0.f)) * inv_count;
+    }
+    if (lane == 0) loss_parts[2 * b + k] = (lse - lg[lab]) * inv_count;
+  }
+}
+
+// dx[t] = dl[t][0] * w0 + dl[t][1] * w1 ; partials of dW[k][h] = sum_t dl[t][k] x[t][h]
+// and db[k] = sum_t dl[t][k] over row block blockIdx.y
+__global__ void __launch_bounds__(256) qa_head_bwd_kernel(const bf16* __restrict__ x,
+                                                          const float* __restrict__ dl, int T,
+                                                          int H, const float* __restrict__ w,
+                                                          bf16* __restrict__ dx,
+                                                          float* __restrict__ partial) {
+  const int W = 2 * H + 2;
+  const int h = blockIdx.x * 256 + threadIdx.x;  // column (h < H) or bias slot
+  float a0 = 0.f, a1 = 0.f;
+  const int rows_per = (T + gridDim.y - 1) / gridDim.y;
+  const int r0 = blockIdx.y * rows_per, r1 = min(T, r0 + rows_per);
+  for (int t = r0; t < r1; ++t) {
+    const float d0 = dl[2 * t], d1 = dl[2 * t + 1];
+    if (h < H) {
+      const float xv = __bfloat162float(x[(int64_t)t * H + h]);
+      a0 += d0 * xv;
+      a1 += d1 * xv;
+      dx[(int64_t)t * H + h] = __float2bfloat16_rn(d0 * w[h] + d1 * w[H + h]);
+    } else if (h == H) {
+      a0 += d0;
+      a1 += d1;
+    }
+  }
+  float* out = partial + (size_t)blockIdx.y * W;
+  if (h < H) {
+    out[h] = a0;
+    out[H + h] = a1;
+  } else if (h == H) {
+    out[2 * H] = a0;
+    out[2 * H + 1] = a1;
+  }
+}
+
+// =====================================================================
+// row-wise softmax cross-entropy over a large vocabulary (one CTA per row)
+// =====================================================================
+__global__ void __launch_bounds__(512) ce_rows_kernel(bf16* __restrict__ logits, int V, int ld,
+                                                      const int32_t* __restrict__ labels,
+                                                      float grad_scale,
+                                                      float* __restrict__ loss_rows) {
+  __shared__ float red[32];
+  const int64_t r = blockIdx.x;
+  bf16* row = logits + r * ld;
+  const int lab = labels[r];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (lab < 0) {  // ignored position: zero gradient row
+    for (int c = tid * 8; c < ld; c += blockDim.x * 8)
+      *reinterpret_cast<uint4*>(row + c) = make_uint4(0, 0, 0, 0);
+    if (tid == 0) loss_rows[r] = 0.f;
+    return;
+  }
+  // pass 1: max
+  float mx = -INFINITY;
+  for (int c = tid * 8; c < V; c += blockDim.x * 8) {
+    float v[8];
+    load8(row + c, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (c + e < V) mx = fmaxf(mx, v[e]);
+  }
+  mx = warp_max(mx);
+  if (lane == 0) red[warp] = mx;
+  __syncthreads();
+  mx = -INFINITY;
+  for (int i = 0; i < nw; ++i) mx = fmaxf(mx, red[i]);
+  __syncthreads();
+  // pass 2: sum of exp
+  float se = 0.f;
+  for (int c = tid * 8; c < V; c += blockDim.x * 8) {
+    float v[8];
+    load8(row + c, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      if (c + e < V) se += __expf(v[e] - mx);
+  }
+  se = warp_sum(se);
+  if (lane == 0) red[warp] = se;
+  __syncthreads();
+  se = 0.f;
+  for (int i = 0; i < nw; ++i) se += red[i];
+  const float lse = mx + logf(se);
+  const float target = __bfloat162float(row[lab]);
+  __syncthreads();
+  // pass 3: gradient in place
+  for (int c = tid * 8; c < ld; c += blockDim.x * 8) {
+    float v[8];
+    load8(row + c, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = c + e;
+      v[e] = j < V ? (__expf(v[e] - lse) - (j == lab ? 1.f : 0.f)) * grad_scale : 0.f;
+    }
+    store8(row + c, v);
+  }
+  if (tid == 0) loss_rows[r] = lse - target;
+}
 }  // namespace mimose_dev
 
 // =====================================================================
@@ -756,10 +1003,10 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
 
 template <int L, int MAXC>
 static void softmax_fwd_t(const bf16* in, bf16* p, bf16* pd, int64_t rows, int S, int ld,
-                          const mimose_dev::DropoutCfg& d, cudaStream_t s) {
+                          const mimose_dev::DropoutCfg& d, cudaStream_t s, int causal) {
   const int64_t rows_per_block = 8 * (32 / L);
   const int g = (int)((rows + rows_per_block - 1) / rows_per_block);
-  mimose_dev::softmax_fwd_kernel<L, MAXC><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d);
+  mimose_dev::softmax_fwd_kernel<L, MAXC><<<g, 256, 0, s>>>(in, p, pd, rows, S, ld, d, causal);
 }
 template <int L, int MAXC>
 static void softmax_bwd_t(const bf16* p, bf16* dp, int64_t rows, int S, int ld,
@@ -795,15 +1042,16 @@ static bool softmax_geometry(int ld, int* L, int* maxc) {
 }
 
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
-                        const mimose_dev::DropoutCfg& d, cudaStream_t s) {
+                        const mimose_dev::DropoutCfg& d, cudaStream_t s, bool causal) {
+  const int cz = causal ? 1 : 0;
   auto in = static_cast<const bf16*>(scores);
   auto p = static_cast<bf16*>(P);
   auto pd = static_cast<bf16*>(Pd);
   int L = 0, maxc = 0;
   if (!softmax_geometry(ld, &L, &maxc)) return cudaErrorInvalidValue;
-#define FWD8(M) softmax_fwd_t<8, M>(in, p, pd, rows, S, ld, d, s)
-#define FWD16(M) softmax_fwd_t<16, M>(in, p, pd, rows, S, ld, d, s)
-#define FWD32(M) softmax_fwd_t<32, M>(in, p, pd, rows, S, ld, d, s)
+#define FWD8(M) softmax_fwd_t<8, M>(in, p, pd, rows, S, ld, d, s, cz)
+#define FWD16(M) softmax_fwd_t<16, M>(in, p, pd, rows, S, ld, d, s, cz)
+#define FWD32(M) softmax_fwd_t<32, M>(in, p, pd, rows, S, ld, d, s, cz)
   if (L == 8) { MIMOSE_SOFTMAX_CASES(FWD8) }
   else if (L == 16) { MIMOSE_SOFTMAX_CASES(FWD16) }
   else { MIMOSE_SOFTMAX_CASES(FWD32) }
@@ -834,10 +1082,11 @@ cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
 }
 
 cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
-                            const int32_t* uid, int n_unique, float* dword, cudaStream_t s) {
+                            const int32_t* uid, int n_unique, float* dword, cudaStream_t s,
+                            bool accumulate) {
   if (n_unique == 0) return cudaSuccess;
   mimose_dev::embed_word_grad_kernel<<<grid_for(n_unique, 8), 256, 0, s>>>(
-      static_cast<const bf16*>(de), H, perm, seg, uid, n_unique, dword);
+      static_cast<const bf16*>(de), H, perm, seg, uid, n_unique, dword, accumulate ? 1 : 0);
   count_launch();
   return cudaGetLastError();
 }
@@ -889,6 +1138,84 @@ cudaError_t init_normal(float* p, int64_t n, float mean, float std, uint64_t see
 cudaError_t f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s) {
   mimose_dev::f32_to_bf16_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
       in, static_cast<bf16*>(out), n);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t dropout_apply(const void* in, void* out, int64_t n, const DropoutCfg& d,
+                          cudaStream_t s) {
+  if (n % 8) return cudaErrorInvalidValue;
+  mimose_dev::dropout_apply_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
+      static_cast<const bf16*>(in), static_cast<bf16*>(out), n / 8, d);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t dgelu_apply(const void* dg, const void* u, void* out, int64_t n, bool tanh_form,
+                        cudaStream_t s) {
+  if (n % 8) return cudaErrorInvalidValue;
+  mimose_dev::dgelu_apply_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
+      static_cast<const bf16*>(dg), static_cast<const bf16*>(u), static_cast<bf16*>(out), n / 8,
+      tanh_form ? 1 : 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t gather_rows(const void* src, const int32_t* idx, int n, int H, void* dst,
+                        cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  mimose_dev::gather_rows_kernel<<<grid_for(n, 8), 256, 0, s>>>(
+      static_cast<const bf16*>(src), idx, n, H, static_cast<bf16*>(dst), 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t scatter_rows(const void* src, const int32_t* idx, int n, int H, void* dst,
+                         cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  mimose_dev::gather_rows_kernel<<<grid_for(n, 8), 256, 0, s>>>(
+      static_cast<const bf16*>(src), idx, n, H, static_cast<bf16*>(dst), 1);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t sum_f32(const float* x, int n, float scale, float* out, cudaStream_t s) {
+  mimose_dev::sum_f32_kernel<<<1, 1024, 0, s>>>(x, n, scale, out);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t qa_head(const void* x, int B, int S, int H, const float* w, const float* b,
+                    const int32_t* labels, float* logits, float* dlogits, float* loss_parts,
+                    cudaStream_t s) {
+  mimose_dev::qa_head_kernel<<<B, 512, 2 * S * sizeof(float), s>>>(
+      static_cast<const bf16*>(x), S, H, w, b, labels, 1.f / (2.f * B), logits, dlogits,
+      loss_parts);
+  count_launch();
+  return cudaGetLastError();
+}
+
+int qa_row_blocks(int T) { return T < 64 ? 1 : 64; }
+
+cudaError_t qa_head_bwd(const void* x, const float* dlogits, int T, int H, const float* w,
+                        void* dx, float* partial, float* dW, float* db, cudaStream_t s) {
+  const int rb = qa_row_blocks(T);
+  dim3 grid((H + 1 + 255) / 256, rb);
+  mimose_dev::qa_head_bwd_kernel<<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), dlogits, T, H,
+                                                      w, static_cast<bf16*>(dx), partial);
+  count_launch();
+  const int W = 2 * H + 2;
+  mimose_dev::reduce_partials_kernel<<<grid_for(W, 32), 256, 0, s>>>(partial, rb, W, 2 * H, dW,
+                                                                    db, nullptr);
+  count_launch();
+  return cudaGetLastError();
+}
+
+cudaError_t ce_rows(void* logits, int rows, int V, int ld, const int32_t* labels,
+                    float grad_scale, float* loss_rows, cudaStream_t s) {
+  if (ld % 8) return cudaErrorInvalidValue;
+  mimose_dev::ce_rows_kernel<<<rows, 512, 0, s>>>(static_cast<bf16*>(logits), V, ld, labels,
+                                                  grad_scale, loss_rows);
   count_launch();
   return cudaGetLastError();
 }

@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <string>
 
+#include "dropout_cfg.hpp"
+
 namespace mimose_ops {
 
 // bf16 matrix view: logical [nb2][nb1][rows][cols], `cols` contiguous.
@@ -43,6 +45,8 @@ struct GemmCall {
   int split_k = 0;
   void* workspace = nullptr;
   int64_t workspace_bytes = 0;
+  int gelu_tanh = 0;              // GELU flavour for kEpiBiasGelu / kEpiDGelu
+  mimose_dev::DropoutCfg drop;    // kEpiBf16: dropout on the product before adding aux
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);

@@ -24,6 +24,7 @@ struct LnFwdArgs {
   void* stats = nullptr;       // float2 {mean, rstd} per row (null: not saved)
   void* y = nullptr;           // bf16 output
   DropoutCfg out_drop;
+  bool skip_ln = false;        // y = dropout_out(z): plain (residual) sum, no LayerNorm
 };
 
 struct LnBwdArgs {
@@ -37,6 +38,8 @@ struct LnBwdArgs {
   void* dz = nullptr;          // bf16 grad of z (residual path)
   void* dbr = nullptr;         // bf16 grad of the dropped-out branch (nullable)
   DropoutCfg br_drop;
+  const void* dres = nullptr;  // bf16 residual gradient added to dz AFTER the LN backward
+                               // (pre-LN blocks: x + f(LN(x)))
   float* partial = nullptr;    // [ln_bwd_blocks(rows)][3][H] scratch
 };
 
@@ -62,11 +65,43 @@ cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float
 cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,
                    float* partial, float* out, cudaStream_t s);
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
-                        const DropoutCfg& d, cudaStream_t s);
+                        const DropoutCfg& d, cudaStream_t s, bool causal = false);
 cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const DropoutCfg& d, float scale, cudaStream_t s);
 cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
-                            const int32_t* uid, int n_unique, float* dword, cudaStream_t s);
+                            const int32_t* uid, int n_unique, float* dword, cudaStream_t s,
+                            bool accumulate = false);
+
+// out = in * keep-mask * scale over n (multiple of 8) bf16 elements; element
+// index = position in the buffer (the forward's dropout index)
+cudaError_t dropout_apply(const void* in, void* out, int64_t n, const DropoutCfg& d,
+                          cudaStream_t s);
+// out = dg * gelu'(u)
+cudaError_t dgelu_apply(const void* dg, const void* u, void* out, int64_t n, bool tanh_form,
+                        cudaStream_t s);
+// rows gather / scatter of bf16 [*, H]: dst[i] = src[idx[i]] ; dst[idx[i]] = src[i]
+cudaError_t gather_rows(const void* src, const int32_t* idx, int n, int H, void* dst,
+                        cudaStream_t s);
+cudaError_t scatter_rows(const void* src, const int32_t* idx, int n, int H, void* dst,
+                         cudaStream_t s);
+// out = scale * sum(x[0..n)) in a fixed order (single CTA)
+cudaError_t sum_f32(const float* x, int n, float scale, float* out, cudaStream_t s);
+
+// extractive-QA head: logits[t] = (x[t] . w0 + b0, x[t] . w1 + b1); CE over the
+// S positions of each sequence for start / end; dlogits [T][2] fp32 (scaled by
+// 1 / (2 B)) and per-sequence loss partials (already / (2 B))
+cudaError_t qa_head(const void* x, int B, int S, int H, const float* w, const float* b,
+                    const int32_t* labels, float* logits, float* dlogits, float* loss_parts,
+                    cudaStream_t s);
+// dx[t] = dl[t][0] w0 + dl[t][1] w1 (bf16); partial sums for dW [2][H] and db [2]
+cudaError_t qa_head_bwd(const void* x, const float* dlogits, int T, int H, const float* w,
+                        void* dx, float* partial, float* dW, float* db, cudaStream_t s);
+int qa_row_blocks(int T);
+// row-wise softmax cross-entropy over V classes of bf16 logits [rows][ld]:
+// loss_rows[r] = lse - logit[label] (0 for label < 0); logits are overwritten
+// by dlogits = (softmax - onehot) * grad_scale (zero rows for ignored labels)
+cudaError_t ce_rows(void* logits, int rows, int V, int ld, const int32_t* labels,
+                    float grad_scale, float* loss_rows, cudaStream_t s);
 cudaError_t embed_pos_grad(const void* de, int B, int S, int H, float* dpos, cudaStream_t s);
 cudaError_t mc_head(const void* pre, int B, int H, int C, const float* wc, const float* bc,
                     const int32_t* labels, const DropoutCfg& d, float* loss, float* logits,

@@ -178,8 +178,12 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   L_ = m.layers;
   if (H_ % 256 || H_ > 1024 || H_ / nh_ != 64 || F_ % 64 || L_ < 1 || L_ > 64)
     throw std::runtime_error("unsupported model shape (need hidden % 256 == 0, <= 1024, head dim 64)");
-  if (m.type_vocab < 1 || m.type_vocab > 2) throw std::runtime_error("type_vocab must be 1 or 2");
-  if (t.batch % m.num_choices) throw std::runtime_error("batch must be a multiple of num_choices");
+  if (m.arch != MIMOSE_ARCH_BERT && m.arch != MIMOSE_ARCH_GPT2) throw std::runtime_error("unknown arch");
+  if (m.head < MIMOSE_HEAD_MC || m.head > MIMOSE_HEAD_MLM) throw std::runtime_error("unknown head");
+  if (m.type_vocab < 0 || m.type_vocab > 2) throw std::runtime_error("type_vocab must be 0, 1 or 2");
+  if (m.head == MIMOSE_HEAD_MC && (m.num_choices < 1 || t.batch % m.num_choices))
+    throw std::runtime_error("batch must be a multiple of num_choices");
+  if (m.vocab < 2) throw std::runtime_error("bad vocab");
   if (t.seq_min < 1 || t.seq_max < t.seq_min || t.seq_max > m.max_pos || round8(t.seq_max) > 2048)
     throw std::runtime_error("bad sequence range");
 
@@ -191,7 +195,8 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   const int64_t Tmax = (int64_t)t.batch * t.seq_max;
   const int lnb = mimose_ops::ln_bwd_blocks((int)Tmax);
   ln_partial_ = static_cast<float*>(take((int64_t)lnb * 3 * H_ * 4, kTagOther));
-  const int64_t widest = std::max<int64_t>(std::max<int64_t>(3 * H_, F_), 2 * H_);
+  int64_t widest = std::max<int64_t>(std::max<int64_t>(3 * H_, F_), 2 * H_);
+  if (m.head == MIMOSE_HEAD_MLM) widest = std::max<int64_t>(widest, (m.vocab + 63) / 64 * 64);
   col_partial_ =
       static_cast<float*>(take((int64_t)mimose_ops::colsum_row_blocks((int)Tmax) * widest * 4 + 1024, kTagOther));
   norm_partial_ = static_cast<float*>(take((int64_t)mimose_ops::sumsq_blocks() * 4, kTagOther));
@@ -199,7 +204,8 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
     // split-K workspace for the weight-gradient GEMMs (largest need over the shapes)
     const int h = H_, f = F_;
     int64_t ws = 0;
-    const int shapes[4][2] = {{h, f}, {f, h}, {3 * h, h}, {h, h}};
+    const int v = (m.head == MIMOSE_HEAD_LM || m.head == MIMOSE_HEAD_MLM) ? m.vocab : h;
+    const int shapes[5][2] = {{h, f}, {f, h}, {3 * h, h}, {h, h}, {v, h}};
     for (const auto& sh : shapes)
       ws = std::max(ws, mimose_ops::splitk_workspace_bytes(sh[0], sh[1], (int)Tmax));
     wgrad_ws_bytes_ = ws;
@@ -207,13 +213,15 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   }
   norm2_ = static_cast<float*>(take(4, kTagOther));
   d_loss_ = static_cast<float*>(take(4, kTagOther));
-  d_logits_ = static_cast<float*>(take((int64_t)t.batch * 4, kTagOther));
+  // MC: one logit per sequence ; QA: start / end logit per token
+  d_logits_ = static_cast<float*>(
+      take((m.head == MIMOSE_HEAD_QA ? 2 * Tmax : (int64_t)t.batch) * 4, kTagOther));
   ck(cudaMallocHost(&h_loss_, kLossRing * sizeof(float)), "cudaMallocHost");
   for (int j = 0; j < kLossRing; ++j) {
     ck(cudaEventCreateWithFlags(&loss_ev_[j], cudaEventDisableTiming), "event");
     loss_iter_[j] = -1;
   }
-  stage_elems_ = 5 * Tmax + t.batch + 8;
+  stage_elems_ = 8 * Tmax + 2 * t.batch + 8;
   for (int k = 0; k < 2; ++k) {
     ck(cudaMallocHost(&h_stage_[k], stage_elems_ * sizeof(int32_t)), "cudaMallocHost");
     ck(cudaEventCreateWithFlags(&stage_ev_[k], cudaEventDisableTiming), "event");
@@ -328,14 +336,17 @@ ParamRef Trainer::add_param(const std::string& name, int64_t n, bool decay,
   return r;
 }
 
+// Parameter names follow oracle/bert_ref.py param_shapes (HF BERT / GPT-2
+// tensors with fused QKV). Tied LM / MLM decoders reuse embeddings.word.
 void Trainer::build_params() {
   std::vector<ParamRef*> fix;
   const int64_t H = H_, F = F_;
+  const bool bert = m_.arch == MIMOSE_ARCH_BERT;
   lp_.resize(L_);
   // decayed tensors first (matrices + embeddings), then biases / LayerNorm
   word_ = add_param("embeddings.word", (int64_t)m_.vocab * H, true, fix);
   pos_ = add_param("embeddings.position", (int64_t)m_.max_pos * H, true, fix);
-  type_ = add_param("embeddings.token_type", (int64_t)m_.type_vocab * H, true, fix);
+  if (m_.type_vocab > 0) type_ = add_param("embeddings.token_type", (int64_t)m_.type_vocab * H, true, fix);
   for (int l = 0; l < L_; ++l) {
     const std::string p = "layer." + std::to_string(l) + ".";
     lp_[l].wqkv = add_param(p + "attn.qkv.weight", 3 * H * H, true, fix);
@@ -343,11 +354,20 @@ void Trainer::build_params() {
     lp_[l].w1 = add_param(p + "ffn.in.weight", F * H, true, fix);
     lp_[l].w2 = add_param(p + "ffn.out.weight", H * F, true, fix);
   }
-  wp_ = add_param("pooler.weight", H * H, true, fix);
-  wc_ = add_param("classifier.weight", H, true, fix);
+  switch (m_.head) {
+    case MIMOSE_HEAD_MC:
+      wp_ = add_param("pooler.weight", H * H, true, fix);
+      wc_ = add_param("classifier.weight", H, true, fix);
+      break;
+    case MIMOSE_HEAD_QA: qaw_ = add_param("qa.weight", 2 * H, true, fix); break;
+    case MIMOSE_HEAD_MLM: mlmw_ = add_param("mlm.transform.weight", H * H, true, fix); break;
+    default: break;
+  }
   n_decay_ = nparam_;
-  eln_g_ = add_param("embeddings.ln.weight", H, false, fix);
-  eln_b_ = add_param("embeddings.ln.bias", H, false, fix);
+  if (bert) {
+    eln_g_ = add_param("embeddings.ln.weight", H, false, fix);
+    eln_b_ = add_param("embeddings.ln.bias", H, false, fix);
+  }
   for (int l = 0; l < L_; ++l) {
     const std::string p = "layer." + std::to_string(l) + ".";
     lp_[l].bqkv = add_param(p + "attn.qkv.bias", 3 * H, false, fix);
@@ -359,14 +379,35 @@ void Trainer::build_params() {
     lp_[l].ln2_g = add_param(p + "ffn.ln.weight", H, false, fix);
     lp_[l].ln2_b = add_param(p + "ffn.ln.bias", H, false, fix);
   }
-  bp_ = add_param("pooler.bias", H, false, fix);
-  bc_ = add_param("classifier.bias", 1, false, fix);
+  if (!bert) {
+    fln_g_ = add_param("final_ln.weight", H, false, fix);
+    fln_b_ = add_param("final_ln.bias", H, false, fix);
+  }
+  switch (m_.head) {
+    case MIMOSE_HEAD_MC:
+      bp_ = add_param("pooler.bias", H, false, fix);
+      bc_ = add_param("classifier.bias", 1, false, fix);
+      break;
+    case MIMOSE_HEAD_QA: qab_ = add_param("qa.bias", 2, false, fix); break;
+    case MIMOSE_HEAD_MLM:
+      mlmb_ = add_param("mlm.transform.bias", H, false, fix);
+      mlm_g_ = add_param("mlm.ln.weight", H, false, fix);
+      mlm_beta_ = add_param("mlm.ln.bias", H, false, fix);
+      decb_ = add_param("mlm.decoder.bias", m_.vocab, false, fix);
+      break;
+    default: break;
+  }
 
   p32_ = static_cast<float*>(take(nparam_ * 4, kTagParam));
   p16_ = take(nparam_ * 2, kTagParam);
   g32_ = static_cast<float*>(take(nparam_ * 4, kTagGrad));
   am_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
   av_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
+}
+
+bool Trainer::fused_attn(int S) const {
+  // the fused score kernels have no causal mask: causal models use the pair
+  return t_.attn_fused && !m_.causal && mimose_ops::attn_fused_supported(S);
 }
 
 void Trainer::init_params(cudaStream_t s) {
@@ -383,9 +424,14 @@ void Trainer::init_params(cudaStream_t s) {
     std::vector<float> v(static_cast<size_t>(r.n), 1.f);
     ck(cudaMemcpy(p32_ + r.off, v.data(), r.n * 4, cudaMemcpyHostToDevice), "memcpy");
   };
+  auto maybe = [&](const ParamRef& r, bool one) {
+    if (r.n == 0) return;
+    if (one) ones(r);
+    else normal(r);
+  };
   normal(word_);
   normal(pos_);
-  normal(type_);
+  maybe(type_, false);
   for (auto& l : lp_) {
     normal(l.wqkv);
     normal(l.wo);
@@ -394,10 +440,49 @@ void Trainer::init_params(cudaStream_t s) {
     ones(l.ln1_g);
     ones(l.ln2_g);
   }
-  normal(wp_);
-  normal(wc_);
-  ones(eln_g_);
+  maybe(wp_, false);
+  maybe(wc_, false);
+  maybe(qaw_, false);
+  maybe(mlmw_, false);
+  maybe(eln_g_, true);
+  maybe(fln_g_, true);
+  maybe(mlm_g_, true);
   ck(mimose_ops::f32_to_bf16(p32_, p16_, nparam_, s), "f32_to_bf16");
+}
+
+// Peak bytes the task head (and the GPT-2 final LayerNorm) holds at once,
+// mirroring head_fwd_bwd's allocation order. MLM is sized for every token
+// masked (the count is only known per step).
+int64_t Trainer::head_bytes(int S) const {
+  const int64_t B = t_.batch, T = B * S, H = H_;
+  const int64_t act = 2 * T * H;
+  const int64_t Vp = (m_.vocab + 63) / 64 * 64;
+  int64_t head = 0;
+  switch (m_.head) {
+    case MIMOSE_HEAD_MC: head = act + 2 * (2 * B * H); break;
+    case MIMOSE_HEAD_QA:
+      head = act + 8 * T + 8 * B + (int64_t)mimose_ops::qa_row_blocks((int)T) * (2 * H + 2) * 4;
+      break;
+    case MIMOSE_HEAD_LM: head = act + 2 * T * Vp + 4 * T; break;
+    default: head = 6 * act + 8 * T + 2 * T * Vp + 4 * T; break;
+  }
+  if (m_.arch == MIMOSE_ARCH_GPT2) head += 2 * act + 8 * T;  // xf, stats, d(final LN)
+  return head + 64 * 1024;
+}
+
+// Worst live set of one block's backward outside its saved tensors (mirrors
+// the allocation order of layer_bwd / attn_bwd).
+int64_t Trainer::block_work_bytes(int S) const {
+  const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
+  const int64_t ld = round8(S);
+  const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
+  const int64_t act = 2 * T * H;
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  // post-LN: dy, dz2, df, du | dz1, da, dctx, dx, dP, dqkv
+  // pre-LN:  dy, df, du, dh1, da, dx2 | dh1, da, dctx, dP, dqkv, dx, dx1
+  const int64_t s1 = act * (pre ? 5 : 3) + 2 * T * F;
+  const int64_t s2 = act * (pre ? 5 : 4) + quad + 2 * T * 3 * H;
+  return std::max(s1, s2);
 }
 
 int64_t Trainer::extras_bytes(int S) const {
@@ -405,34 +490,20 @@ int64_t Trainer::extras_bytes(int S) const {
   // inputs + token tables, embedding saves (z0, stats, h0), head tensors,
   // the output boundaries of every block (the scheduler's excess does not
   // count a dropped block's retained output), and one block's backward
-  // workspace (mirrors the allocation order of layer_bwd).
-  const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
-  const int64_t ld = round8(S);
-  const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
+  // workspace.
+  const int64_t B = t_.batch, T = B * S, H = H_;
   const int64_t act = 2 * T * H;
-  const int64_t inputs = 4 * (5 * T + B + 8);
-  const int64_t embed = 2 * act + 8 * T;
-  const int64_t head = 2 * (2 * B * H) + act;
+  const int64_t inputs = 4 * (7 * T + 2 * B + 8);
+  const int64_t embed = m_.arch == MIMOSE_ARCH_BERT ? 2 * act + 8 * T : act;
   const int64_t bounds = (int64_t)L_ * act;
-  // backward live set, worst stage: dy, dz2, df/du, dh1 ... dctx, dPd, dqkv, dz1
-  const int64_t s1 = act * 3 + 2 * T * F;                   // dy, dz2, df, du
-  const int64_t s2 = act * 4 + quad + 2 * T * 3 * H;        // dz1, da, dctx, dx, dPd, dqkv
-  const int64_t work = std::max(s1, s2);
-  return inputs + embed + head + bounds + work;
+  return inputs + embed + head_bytes(S) + bounds + block_work_bytes(S);
 }
 
 // Bytes that appear only transiently after the forward (head + one block's
 // backward workspace) plus a 2 % fragmentation margin: what the reactive
 // evictor must leave free.
 int64_t Trainer::dtr_headroom(int S) const {
-  const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
-  const int64_t ld = round8(S);
-  const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
-  const int64_t act = 2 * T * H;
-  const int64_t head = 2 * (2 * B * H) + act;
-  const int64_t s1 = act * 3 + 2 * T * F;
-  const int64_t s2 = act * 4 + quad + 2 * T * 3 * H;
-  return head + std::max(s1, s2) + ctx_->arena.stats().budget / 50;
+  return head_bytes(S) + block_work_bytes(S) + ctx_->arena.stats().budget / 50;
 }
 
 void Trainer::build_spec() {
@@ -481,26 +552,26 @@ void Trainer::set_forced_plan(const int* ids, int n, int active) {
   forced_.assign(ids, ids + (ids ? n : 0));
 }
 
-// ------------------------------------------------------------ layer forward
-void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
-                        cudaStream_t s) {
+// ------------------------------------------------------------ attention
+// qkv = x Wqkv^T + bqkv ; P = softmax(q k^T / 8 [causal]) ; Pd = dropout(P) ;
+// ctx = Pd v (head-interleaved [T, H]). Saved tensors go to *save when kept.
+void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
-  const int64_t T = g.T, H = H_, F = F_;
+  const int64_t T = g.T, H = H_;
   const int S = g.S, ld = g.ld, nh = nh_;
   auto* W = static_cast<bf16raw*>(p16_);
   const bool keep = save != nullptr;
   const int act_tag = keep ? kTagAct : kTagTransient;
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
 
-  // QKV projection
   void* qkv = take(T * 3 * H * 2, act_tag);
-  run_gemm(linear_call(h, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
-                   p32_ + P.bqkv.off),
-       s);
+  run_gemm(linear_call(x, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
+                       p32_ + P.bqkv.off),
+           s);
   void* Pm = take(quad, act_tag);
   void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  if (t_.attn_fused && mimose_ops::attn_fused_supported(S)) {
+  if (fused_attn(S)) {
     // fused: scores stay in TMEM, softmax + dropout in the epilogue
     ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, s),
@@ -516,7 +587,8 @@ void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const St
     c.out = sc; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
     c.alpha = 0.125f;
     run_gemm(c, s);
-    ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s), "softmax_fwd");
+    ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s, m_.causal != 0),
+       "softmax_fwd");
     drop(sc);
   }
   // ctx = Pd V, written head-interleaved into [T, H]
@@ -531,127 +603,23 @@ void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const St
     c.out = ctx; c.ldo = H; c.obs1 = 64; c.obs2 = (int64_t)S * H;
     run_gemm(c, s);
   }
-  if (!keep) {
+  if (keep) {
+    save->qkv = qkv; save->P = Pm; save->Pd = Pd;
+  } else {
     drop(qkv);
     drop(Pm);
     drop(Pd);
   }
-  // attention output projection + residual + LN1
-  void* a = take(T * H * 2, kTagTransient);
-  run_gemm(linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, a, mimose_ops::kEpiBf16, p32_ + P.bo.off), s);
-  if (!keep) drop(ctx);
-  void* z1 = keep ? take(T * H * 2, act_tag) : nullptr;
-  void* st1 = keep ? take(T * 8, act_tag) : nullptr;
-  void* h1 = take(T * H * 2, act_tag);
-  {
-    mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.res = h; la.br = a;
-    la.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
-    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
-    la.z = z1; la.stats = st1; la.y = h1;
-    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-  }
-  drop(a);
-  // FFN
-  void* u = take(T * F * 2, act_tag);
-  void* gg = take(T * F * 2, act_tag);
-  {
-    GemmCall c = linear_call(h1, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
-                             p32_ + P.b1.off);
-    c.out2 = gg;
-    run_gemm(c, s);
-  }
-  if (!keep) drop(u);
-  void* f = take(T * H * 2, kTagTransient);
-  run_gemm(linear_call(gg, W + P.w2.off, T, (int)H, (int)F, f, mimose_ops::kEpiBf16, p32_ + P.b2.off), s);
-  if (!keep) drop(gg);
-  void* z2 = keep ? take(T * H * 2, act_tag) : nullptr;
-  void* st2 = keep ? take(T * 8, act_tag) : nullptr;
-  {
-    mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.res = h1; la.br = f;
-    la.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
-    la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
-    la.z = z2; la.stats = st2; la.y = y;
-    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-  }
-  drop(f);
-  if (!keep) {
-    drop(h1);
-    return;
-  }
-  save->qkv = qkv; save->P = Pm; save->Pd = Pd; save->ctx = ctx;
-  save->z1 = z1; save->st1 = st1; save->h1 = h1;
-  save->u = u; save->g = gg; save->z2 = z2; save->st2 = st2;
+  return ctx;
 }
 
-void Trainer::free_save(LayerSave& sv) {
-  drop(sv.qkv); drop(sv.P); drop(sv.Pd); drop(sv.ctx); drop(sv.z1); drop(sv.st1); drop(sv.h1);
-  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2);
-}
-
-// ----------------------------------------------------------- layer backward
-// Consumes dy (freed) and the saved set (freed); returns dx (grad of h).
-void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
-                         cudaStream_t s) {
-  const LayerParams& P = lp_[l];
-  const int64_t T = g.T, H = H_, F = F_;
+// Attention backward from dctx (consumed) through the saved qkv / P / Pd
+// (freed); returns dqkv [T, 3H].
+void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cudaStream_t s) {
+  const int64_t T = g.T, H = H_;
   const int S = g.S, ld = g.ld, nh = nh_;
-  auto* W = static_cast<bf16raw*>(p16_);
-  float* G = g32_;
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
-  const bool hid_drop = m_.hidden_dropout > 0.f;
-
-  // LN2 backward (+ FFN-output dropout backward, db2)
-  void* dz2 = take(T * H * 2, kTagTransient);
-  void* df = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
-  {
-    mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dy; a.z = sv.z2; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
-    a.dz = dz2; a.dbr = df;
-    a.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
-    a.partial = ln_partial_;
-    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.b2.off, s), "ln_bwd");
-  }
-  drop(dy);
-  drop(sv.z2); drop(sv.st2);
-  void* dfp = df ? df : dz2;
-  // FFN2: dW2 = df^T g ; du = (df W2) * gelu'(u)
-  run_gemm(wgrad_call(dfp, sv.g, T, (int)H, (int)F, G + P.w2.off), s);
-  drop(sv.g);
-  void* du = take(T * F * 2, kTagTransient);
-  run_gemm(dgrad_call(dfp, W + P.w2.off, T, (int)H, (int)F, du, mimose_ops::kEpiDGelu, sv.u), s);
-  drop(df);
-  drop(sv.u);
-  ck(mimose_ops::colsum(du, (int)T, (int)F, F, nullptr, 1, col_partial_, G + P.b1.off, s), "colsum");
-  // FFN1: dW1 = du^T h1 ; dh1 = du W1 + dz2 (residual)
-  run_gemm(wgrad_call(du, sv.h1, T, (int)F, (int)H, G + P.w1.off), s);
-  drop(sv.h1);
-  void* dh1 = take(T * H * 2, kTagTransient);
-  run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dh1, mimose_ops::kEpiBf16, dz2), s);
-  drop(du);
-  drop(dz2);
-  // LN1 backward (+ attention-output dropout backward, dbo)
-  void* dz1 = take(T * H * 2, kTagTransient);
-  void* da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
-  {
-    mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dh1; a.z = sv.z1; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
-    a.dz = dz1; a.dbr = da;
-    a.br_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
-    a.partial = ln_partial_;
-    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, G + P.bo.off, s), "ln_bwd");
-  }
-  drop(dh1);
-  drop(sv.z1); drop(sv.st1);
-  void* dap = da ? da : dz1;
-  // output projection: dWo = da^T ctx ; dctx = da Wo
-  run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
-  drop(sv.ctx);
-  void* dctx = take(T * H * 2, kTagTransient);
-  run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
-  drop(da);
-  // attention: dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
+  // dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
   void* dqkv = take(T * 3 * H * 2, kTagTransient);
   {
     GemmCall c;
@@ -668,12 +636,13 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   drop(sv.Pd);
   void* dP = take(quad, kTagTransient);
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  if (t_.attn_fused && mimose_ops::attn_fused_supported(S)) {
+  if (fused_attn(S)) {
     // fused: dPd stays in TMEM; softmax backward in the epilogue writes dS
     ck(mimose_ops::attn_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
                                    sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop, s),
        "attn_scores_bwd");
   } else {
+    // causal: P is exactly 0 above the diagonal, so softmax' gives dS = 0 there
     GemmCall c;
     c.M = S; c.N = S; c.K = 64; c.nb1 = nh; c.nb2 = g.B;
     c.A = head_view(dctx, 0, S, H);
@@ -704,14 +673,241 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   }
   drop(dP);
   drop(sv.qkv);
-  // QKV projection: dbqkv, dWqkv = dqkv^T h ; dx = dqkv Wqkv + dz1 (residual)
+  return dqkv;
+}
+
+// ------------------------------------------------------------ layer forward
+// BERT (post-LN):  h1 = LN1(h + drop(attn(h))) ; y = LN2(h1 + drop(ffn(h1)))
+// GPT-2 (pre-LN):  h1 = h + drop(attn(LN1(h))) ; y = h1 + drop(ffn(LN2(h1)))
+// LayerSave slots: post-LN z1/st1 = LN1 input/stats, h1 = LN1 output, z2/st2 =
+// LN2 input/stats; pre-LN z1 = LN1 output x1, st1, h1, z2 = LN2 output x2, st2.
+void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
+                        cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_, F = F_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  const bool keep = save != nullptr;
+  const int act_tag = keep ? kTagAct : kTagTransient;
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  const auto attn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
+  const auto ffn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
+
+  void* z1 = nullptr;
+  void* st1 = nullptr;
+  const void* ain = h;
+  if (pre) {
+    z1 = take(T * H * 2, act_tag);  // x1 = LN1(h)
+    st1 = keep ? take(T * 8, act_tag) : nullptr;
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.br = h;
+    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
+    la.stats = st1; la.y = z1;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    ain = z1;
+  }
+  void* ctx = attn_fwd(l, ain, save, g, s);
+  if (pre && !keep) drop(z1);
+  // attention output projection, residual, LayerNorm
+  void* a = take(T * H * 2, kTagTransient);
+  run_gemm(linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, a, mimose_ops::kEpiBf16, p32_ + P.bo.off), s);
+  if (!keep) drop(ctx);
+  void* h1 = nullptr;
+  void* x2 = nullptr;  // FFN input
+  void* z2 = nullptr;
+  void* st2 = nullptr;
+  if (pre) {
+    h1 = take(T * H * 2, act_tag);
+    x2 = take(T * H * 2, act_tag);
+    st2 = keep ? take(T * 8, act_tag) : nullptr;
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
+    la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
+    la.z = h1; la.stats = st2; la.y = x2;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    z2 = x2;
+  } else {
+    z1 = keep ? take(T * H * 2, act_tag) : nullptr;
+    st1 = keep ? take(T * 8, act_tag) : nullptr;
+    h1 = take(T * H * 2, act_tag);
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
+    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
+    la.z = z1; la.stats = st1; la.y = h1;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    x2 = h1;
+  }
+  drop(a);
+  // FFN
+  void* u = take(T * F * 2, act_tag);
+  void* gg = take(T * F * 2, act_tag);
+  {
+    GemmCall c = linear_call(x2, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
+                             p32_ + P.b1.off);
+    c.out2 = gg;
+    c.gelu_tanh = m_.gelu_tanh;
+    run_gemm(c, s);
+  }
+  if (!keep) drop(u);
+  if (pre) {
+    if (!keep) drop(x2);
+    // y = h1 + dropout(g W2^T + b2): dropout + residual in the GEMM epilogue
+    GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, y, mimose_ops::kEpiBf16,
+                             p32_ + P.b2.off);
+    c.aux = h1;
+    c.drop = ffn_out_drop;
+    run_gemm(c, s);
+    if (!keep) {
+      drop(gg);
+      drop(h1);
+      return;
+    }
+  } else {
+    void* f = take(T * H * 2, kTagTransient);
+    run_gemm(linear_call(gg, W + P.w2.off, T, (int)H, (int)F, f, mimose_ops::kEpiBf16, p32_ + P.b2.off), s);
+    if (!keep) drop(gg);
+    z2 = keep ? take(T * H * 2, act_tag) : nullptr;
+    st2 = keep ? take(T * 8, act_tag) : nullptr;
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.res = h1; la.br = f; la.br_drop = ffn_out_drop;
+    la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
+    la.z = z2; la.stats = st2; la.y = y;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    drop(f);
+    if (!keep) {
+      drop(h1);
+      return;
+    }
+  }
+  save->ctx = ctx;
+  save->z1 = z1; save->st1 = st1; save->h1 = h1;
+  save->u = u; save->g = gg; save->z2 = z2; save->st2 = st2;
+}
+
+void Trainer::free_save(LayerSave& sv) {
+  drop(sv.qkv); drop(sv.P); drop(sv.Pd); drop(sv.ctx); drop(sv.z1); drop(sv.st1); drop(sv.h1);
+  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2);
+}
+
+// ----------------------------------------------------------- layer backward
+// Consumes dy (freed) and the saved set (freed); returns dx (grad of h).
+void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
+                         cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_, F = F_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  float* G = g32_;
+  const bool hid_drop = m_.hidden_dropout > 0.f;
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  const auto attn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
+  const auto ffn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
+
+  // FFN-output residual / dropout / LN2 backward -> df (grad of the FFN output)
+  void* dres = nullptr;  // gradient reaching h1 through the residual
+  void* df = nullptr;
+  if (pre) {
+    dres = dy;  // y = h1 + drop(f): d h1 (residual part) = dy
+    if (hid_drop) {
+      df = take(T * H * 2, kTagTransient);
+      ck(mimose_ops::dropout_apply(dy, df, T * H, ffn_out_drop, s), "dropout_apply");
+    }
+    ck(mimose_ops::colsum(df ? df : dy, (int)T, (int)H, H, nullptr, 1, col_partial_, G + P.b2.off, s),
+       "colsum");
+  } else {
+    dres = take(T * H * 2, kTagTransient);  // dz2
+    df = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dy; a.z = sv.z2; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
+    a.dz = dres; a.dbr = df; a.br_drop = ffn_out_drop;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.b2.off, s), "ln_bwd");
+    drop(dy);
+    drop(sv.z2); drop(sv.st2);
+  }
+  void* dfp = df ? df : (pre ? dy : dres);
+  // FFN2: dW2 = df^T g ; du = (df W2) * gelu'(u)
+  run_gemm(wgrad_call(dfp, sv.g, T, (int)H, (int)F, G + P.w2.off), s);
+  drop(sv.g);
+  void* du = take(T * F * 2, kTagTransient);
+  {
+    GemmCall c = dgrad_call(dfp, W + P.w2.off, T, (int)H, (int)F, du, mimose_ops::kEpiDGelu, sv.u);
+    c.gelu_tanh = m_.gelu_tanh;
+    run_gemm(c, s);
+  }
+  drop(df);
+  drop(sv.u);
+  ck(mimose_ops::colsum(du, (int)T, (int)F, F, nullptr, 1, col_partial_, G + P.b1.off, s), "colsum");
+  // FFN1: dW1 = du^T x2
+  void*& x2 = pre ? sv.z2 : sv.h1;
+  run_gemm(wgrad_call(du, x2, T, (int)F, (int)H, G + P.w1.off), s);
+  drop(x2);
+  void* dh1 = take(T * H * 2, kTagTransient);
+  void* da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+  if (pre) {
+    // dx2 = du W1 ; d h1 = LN2'(dx2) + dy ; da = drop'(d h1), dbo
+    void* dx2 = take(T * H * 2, kTagTransient);
+    run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dx2, mimose_ops::kEpiBf16, nullptr), s);
+    drop(du);
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dx2; a.z = sv.h1; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
+    a.dres = dres;
+    a.dz = dh1; a.dbr = da; a.br_drop = attn_out_drop;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.bo.off, s), "ln_bwd");
+    drop(dx2);
+    drop(dy);
+    drop(sv.h1); drop(sv.st2);
+  } else {
+    // d h1 = du W1 + dz2 (residual) ; LN1 backward (+ attention-output dropout, dbo)
+    run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dh1, mimose_ops::kEpiBf16, dres), s);
+    drop(du);
+    drop(dres);
+    void* dz1 = take(T * H * 2, kTagTransient);
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dh1; a.z = sv.z1; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
+    a.dz = dz1; a.dbr = da; a.br_drop = attn_out_drop;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, G + P.bo.off, s), "ln_bwd");
+    drop(dh1);
+    drop(sv.z1); drop(sv.st1);
+    dh1 = dz1;  // gradient reaching the block input through the residual
+  }
+  void* dap = da ? da : dh1;
+  // output projection: dWo = da^T ctx ; dctx = da Wo
+  run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
+  drop(sv.ctx);
+  void* dctx = take(T * H * 2, kTagTransient);
+  run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
+  drop(da);
+  void* dqkv = attn_bwd(l, sv, dctx, g, s);
+  // QKV projection: dbqkv, dWqkv = dqkv^T xin
   ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
      "colsum");
-  run_gemm(wgrad_call(dqkv, h, T, 3 * (int)H, (int)H, G + P.wqkv.off), s);
+  run_gemm(wgrad_call(dqkv, pre ? sv.z1 : h, T, 3 * (int)H, (int)H, G + P.wqkv.off), s);
   void* dx = take(T * H * 2, kTagTransient);
-  run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx, mimose_ops::kEpiBf16, dz1), s);
-  drop(dqkv);
-  drop(dz1);
+  if (pre) {
+    // dx1 = dqkv Wqkv ; dx = LN1'(dx1) + d h1
+    void* dx1 = take(T * H * 2, kTagTransient);
+    run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx1, mimose_ops::kEpiBf16, nullptr), s);
+    drop(dqkv);
+    drop(sv.z1);
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dx1; a.z = h; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
+    a.dres = dh1;
+    a.dz = dx;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, nullptr, s), "ln_bwd");
+    drop(dx1);
+    drop(sv.st1);
+  } else {
+    // dx = dqkv Wqkv + dz1 (residual)
+    run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx, mimose_ops::kEpiBf16, dh1), s);
+    drop(dqkv);
+  }
+  drop(dh1);
   return dx;
 }
 
@@ -810,6 +1006,178 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
   return Mode::Planned;
 }
 
+// ------------------------------------------------------------------- heads
+// Forward + loss + backward of the task head on `hidden` ([T, H] final hidden
+// states); returns d hidden (bf16 [T, H], caller frees). Loss -> d_loss_.
+void* Trainer::head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g,
+                            cudaStream_t s) {
+  const int64_t T = g.T, H = H_;
+  const int B = g.B, S = g.S;
+  auto* W = static_cast<bf16raw*>(p16_);
+  float* G = g32_;
+  void* dh = take(T * H * 2, kTagTransient);
+  if (m_.head == MIMOSE_HEAD_MC) {
+    // pooled = tanh(cls Wp^T + bp) -> dropout -> logits -> CE over choices
+    void* pre = take((int64_t)B * H * 2, kTagTransient);
+    {
+      GemmCall c;
+      c.M = B; c.N = (int)H; c.K = (int)H;
+      c.A = mat(hidden, B, H, (int64_t)S * H);  // row 0 of every sequence
+      c.B = mat(W + wp_.off, H, H, H);
+      c.epi = mimose_ops::kEpiBf16;
+      c.out = pre; c.ldo = H; c.bias = p32_ + bp_.off;
+      run_gemm(c, s);
+    }
+    void* dpre = take((int64_t)B * H * 2, kTagTransient);
+    ck(mimose_ops::mc_head(pre, B, (int)H, m_.num_choices, p32_ + wc_.off, p32_ + bc_.off,
+                           in.labels,
+                           mimose_ops::make_dropout(m_.hidden_dropout, m_.seed,
+                                                    stream_id(g.step, L_, kSitePool)),
+                           d_loss_, d_logits_, dpre, G + wc_.off, G + bc_.off, s),
+       "mc_head");
+    drop(pre);
+    ck(cudaMemsetAsync(dh, 0, T * H * 2, s), "memset");
+    GemmCall c;  // dWp = dpre^T cls
+    c.M = (int)H; c.N = (int)H; c.K = B;
+    c.A = mat(dpre, B, H, H);
+    c.a_mn = true;
+    c.B = mat(hidden, B, H, (int64_t)S * H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiF32;
+    c.out = G + wp_.off; c.ldo = H;
+    run_gemm(c, s);
+    ck(mimose_ops::colsum(dpre, B, (int)H, H, nullptr, 1, col_partial_, G + bp_.off, s), "colsum");
+    GemmCall d = dgrad_call(dpre, W + wp_.off, B, (int)H, (int)H, dh, mimose_ops::kEpiBf16, nullptr);
+    d.ldo = (int64_t)S * H;  // dcls -> rows s = 0
+    run_gemm(d, s);
+    drop(dpre);
+    return dh;
+  }
+  if (m_.head == MIMOSE_HEAD_QA) {
+    float* dl = static_cast<float*>(take(T * 2 * 4, kTagTransient));
+    float* parts = static_cast<float*>(take((int64_t)2 * B * 4, kTagTransient));
+    ck(mimose_ops::qa_head(hidden, B, S, (int)H, p32_ + qaw_.off, p32_ + qab_.off, in.labels,
+                           d_logits_, dl, parts, s),
+       "qa_head");
+    ck(mimose_ops::sum_f32(parts, 2 * B, 1.f, d_loss_, s), "sum_f32");
+    float* qpart = static_cast<float*>(
+        take((int64_t)mimose_ops::qa_row_blocks((int)T) * (2 * H + 2) * 4, kTagTransient));
+    ck(mimose_ops::qa_head_bwd(hidden, dl, (int)T, (int)H, p32_ + qaw_.off, dh, qpart,
+                               G + qaw_.off, G + qab_.off, s),
+       "qa_head_bwd");
+    void* q = qpart;
+    drop(q);
+    void* v = dl;
+    drop(v);
+    v = parts;
+    drop(v);
+    return dh;
+  }
+  // tied vocabulary decoders
+  const int V = m_.vocab;
+  const int Vp = (V + 63) / 64 * 64;
+  const bool mlm = m_.head == MIMOSE_HEAD_MLM;
+  const int rows = mlm ? in.n_mask : (int)T;
+  const float inv = 1.f / static_cast<float>(std::max(1, mlm ? in.n_mask : in.n_valid));
+  void* xm = nullptr;    // MLM: gathered masked rows
+  void* ut = nullptr;    // MLM transform pre-activation
+  void* gt = nullptr;    // MLM transform GELU output (LN input)
+  void* stt = nullptr;   // MLM LN stats
+  const void* dec_in = hidden;
+  if (mlm) {
+    if (rows == 0) throw std::runtime_error("MLM step without masked positions");
+    xm = take((int64_t)rows * H * 2, kTagTransient);
+    ck(mimose_ops::gather_rows(hidden, in.mask_pos, rows, (int)H, xm, s), "gather_rows");
+    ut = take((int64_t)rows * H * 2, kTagTransient);
+    gt = take((int64_t)rows * H * 2, kTagTransient);
+    GemmCall c = linear_call(xm, W + mlmw_.off, rows, (int)H, (int)H, ut, mimose_ops::kEpiBiasGelu,
+                             p32_ + mlmb_.off);
+    c.out2 = gt;
+    c.gelu_tanh = m_.gelu_tanh;
+    run_gemm(c, s);
+    void* t = take((int64_t)rows * H * 2, kTagTransient);
+    stt = take((int64_t)rows * 8, kTagTransient);
+    mimose_ops::LnFwdArgs la;
+    la.rows = rows; la.br = gt;
+    la.gamma = p32_ + mlm_g_.off; la.beta = p32_ + mlm_beta_.off; la.eps = m_.ln_eps;
+    la.stats = stt; la.y = t;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    dec_in = t;
+  }
+  void* logits = take((int64_t)rows * Vp * 2, kTagTransient);
+  {
+    GemmCall c = linear_call(dec_in, W + word_.off, rows, V, (int)H, logits, mimose_ops::kEpiBf16,
+                             mlm ? p32_ + decb_.off : nullptr);
+    c.ldo = Vp;
+    run_gemm(c, s);
+  }
+  float* lrows = static_cast<float*>(take((int64_t)rows * 4, kTagTransient));
+  ck(mimose_ops::ce_rows(logits, rows, V, Vp, mlm ? in.mask_lab : in.labels, inv, lrows, s),
+     "ce_rows");
+  ck(mimose_ops::sum_f32(lrows, rows, inv, d_loss_, s), "sum_f32");
+  void* lr = lrows;
+  drop(lr);
+  // logits now hold dlogits (bf16, already scaled by 1 / count)
+  if (mlm)
+    ck(mimose_ops::colsum(logits, rows, Vp, Vp, nullptr, 1, col_partial_, G + decb_.off, s),
+       "colsum");
+  {
+    // tied decoder weight gradient written in full (the embedding scatter adds to it)
+    GemmCall c;
+    c.M = V; c.N = (int)H; c.K = rows;
+    c.A = mat(logits, rows, V, Vp);
+    c.a_mn = true;
+    c.B = mat(dec_in, rows, H, H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiF32;
+    c.out = G + word_.off; c.ldo = H;
+    c.workspace = g_wgrad_ws;
+    c.workspace_bytes = g_wgrad_ws_bytes;
+    run_gemm(c, s);
+  }
+  void* ddec = mlm ? take((int64_t)rows * H * 2, kTagTransient) : dh;
+  {
+    GemmCall c;  // d dec_in = dlogits Wword
+    c.M = rows; c.N = (int)H; c.K = V;
+    c.A = mat(logits, rows, V, Vp);
+    c.B = mat(W + word_.off, V, H, H);
+    c.b_mn = true;
+    c.epi = mimose_ops::kEpiBf16;
+    c.out = ddec; c.ldo = H;
+    run_gemm(c, s);
+  }
+  drop(logits);
+  if (!mlm) return dh;
+  // MLM transform backward: LN, GELU, dense; scatter to the masked positions
+  void* dg = take((int64_t)rows * H * 2, kTagTransient);
+  {
+    mimose_ops::LnBwdArgs a;
+    a.rows = rows; a.dy = ddec; a.z = gt; a.stats = stt; a.gamma = p32_ + mlm_g_.off;
+    a.dz = dg;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + mlm_g_.off, G + mlm_beta_.off, nullptr, s), "ln_bwd");
+  }
+  void* dtv = const_cast<void*>(dec_in);
+  drop(dtv);
+  drop(ddec);
+  drop(stt);
+  drop(gt);
+  void* du = take((int64_t)rows * H * 2, kTagTransient);
+  ck(mimose_ops::dgelu_apply(dg, ut, du, (int64_t)rows * H, m_.gelu_tanh != 0, s), "dgelu_apply");
+  drop(dg);
+  drop(ut);
+  ck(mimose_ops::colsum(du, rows, (int)H, H, nullptr, 1, col_partial_, G + mlmb_.off, s), "colsum");
+  run_gemm(wgrad_call(du, xm, rows, (int)H, (int)H, G + mlmw_.off), s);
+  void* dxm = take((int64_t)rows * H * 2, kTagTransient);
+  run_gemm(dgrad_call(du, W + mlmw_.off, rows, (int)H, (int)H, dxm, mimose_ops::kEpiBf16, nullptr), s);
+  drop(du);
+  drop(xm);
+  ck(cudaMemsetAsync(dh, 0, T * H * 2, s), "memset");
+  ck(mimose_ops::scatter_rows(dxm, in.mask_pos, rows, (int)H, dh, s), "scatter_rows");
+  drop(dxm);
+  return dh;
+}
+
 // ------------------------------------------------------------------- step
 void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
                                mimose_step_report* rep) {
@@ -870,18 +1238,24 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   g_wgrad_ws = wgrad_ws_;
   g_wgrad_ws_bytes = wgrad_ws_bytes_;
 
-  // ---- embeddings
-  void* z0 = take(T * H * 2, kTagAct);
-  void* st0 = take(T * 8, kTagAct);
+  // ---- embeddings: BERT z0 = word + pos (+ type), h0 = dropout(LN(z0));
+  //                  GPT-2 h0 = dropout(word + pos) (no LayerNorm)
+  const bool bert = m_.arch == MIMOSE_ARCH_BERT;
+  void* z0 = bert ? take(T * H * 2, kTagAct) : nullptr;
+  void* st0 = bert ? take(T * 8, kTagAct) : nullptr;
   void* h0 = take(T * H * 2, kTagAct);
   {
     mimose_ops::LnFwdArgs la;
     la.rows = (int)T;
-    la.gamma = p32_ + eln_g_.off; la.beta = p32_ + eln_b_.off; la.eps = m_.ln_eps;
+    la.skip_ln = !bert;
+    la.gamma = bert ? p32_ + eln_g_.off : nullptr;
+    la.beta = bert ? p32_ + eln_b_.off : nullptr;
+    la.eps = m_.ln_eps;
     la.z = z0; la.stats = st0; la.y = h0;
     la.out_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
-    ck(mimose_ops::embed_ln_fwd(la, (int)H, in.tokens, in.types, W + word_.off, W + pos_.off,
-                                W + type_.off, S, s),
+    ck(mimose_ops::embed_ln_fwd(la, (int)H, in.tokens, m_.type_vocab > 0 ? in.types : nullptr,
+                                W + word_.off, W + pos_.off,
+                                m_.type_vocab > 0 ? W + type_.off : nullptr, S, s),
        "embed_ln_fwd");
   }
 
@@ -968,43 +1342,33 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     r->pred_err_max = mx;
   }
 
-  // ---- multiple-choice head: pooled = tanh(cls Wp^T + bp) -> logits -> CE
-  void* pre = take((int64_t)B * H * 2, kTagTransient);
-  {
-    GemmCall c;
-    c.M = B; c.N = (int)H; c.K = (int)H;
-    c.A = mat(out[L_ - 1], B, H, (int64_t)S * H);  // row 0 of every sequence
-    c.B = mat(W + wp_.off, H, H, H);
-    c.epi = mimose_ops::kEpiBf16;
-    c.out = pre; c.ldo = H; c.bias = p32_ + bp_.off;
-    run_gemm(c, s);
+  // ---- final LayerNorm (pre-LN / GPT-2) and the task head (forward + backward)
+  void* hidden = out[L_ - 1];
+  void* xf = nullptr;
+  void* stf = nullptr;
+  if (!bert) {
+    xf = take(T * H * 2, kTagAct);
+    stf = take(T * 8, kTagAct);
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.br = out[L_ - 1];
+    la.gamma = p32_ + fln_g_.off; la.beta = p32_ + fln_b_.off; la.eps = m_.ln_eps;
+    la.stats = stf; la.y = xf;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    hidden = xf;
   }
-  void* dpre = take((int64_t)B * H * 2, kTagTransient);
-  ck(mimose_ops::mc_head(pre, B, (int)H, m_.num_choices, p32_ + wc_.off, p32_ + bc_.off,
-                         in.labels,
-                         mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSitePool)),
-                         d_loss_, d_logits_, dpre, G + wc_.off, G + bc_.off, s),
-     "mc_head");
-  drop(pre);
-  void* dy = take(T * H * 2, kTagTransient);
-  ck(cudaMemsetAsync(dy, 0, T * H * 2, s), "memset");
-  {
-    // dWp = dpre^T cls ; dbp = sum dpre ; dcls = dpre Wp -> rows s=0 of dy
-    GemmCall c;
-    c.M = (int)H; c.N = (int)H; c.K = B;
-    c.A = mat(dpre, B, H, H);
-    c.a_mn = true;
-    c.B = mat(out[L_ - 1], B, H, (int64_t)S * H);
-    c.b_mn = true;
-    c.epi = mimose_ops::kEpiF32;
-    c.out = G + wp_.off; c.ldo = H;
-    run_gemm(c, s);
-    ck(mimose_ops::colsum(dpre, B, (int)H, H, nullptr, 1, col_partial_, G + bp_.off, s), "colsum");
-    GemmCall d = dgrad_call(dpre, W + wp_.off, B, (int)H, (int)H, dy, mimose_ops::kEpiBf16, nullptr);
-    d.ldo = (int64_t)S * H;
-    run_gemm(d, s);
+  void* dy = head_fwd_bwd(in, hidden, g, s);
+  if (!bert) {
+    void* dl = take(T * H * 2, kTagTransient);
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dy; a.z = out[L_ - 1]; a.stats = stf; a.gamma = p32_ + fln_g_.off;
+    a.dz = dl;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + fln_g_.off, G + fln_b_.off, nullptr, s), "ln_bwd");
+    drop(dy);
+    drop(xf);
+    drop(stf);
+    dy = dl;
   }
-  drop(dpre);
 
   // ---- backward through the blocks (recompute dropped ones first)
   for (int l = L_ - 1; l >= 0; --l) {
@@ -1021,25 +1385,32 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   }
 
   // ---- embedding backward
-  ck(cudaMemsetAsync(G + word_.off, 0, word_.n * 4, s), "memset");
+  const bool tied = m_.head == MIMOSE_HEAD_LM || m_.head == MIMOSE_HEAD_MLM;
+  if (!tied) ck(cudaMemsetAsync(G + word_.off, 0, word_.n * 4, s), "memset");
   ck(cudaMemsetAsync(G + pos_.off, 0, pos_.n * 4, s), "memset");
   void* de = take(T * H * 2, kTagTransient);
-  {
+  const auto edrop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+  if (bert) {
     mimose_ops::LnBwdArgs a;
     a.rows = (int)T; a.dy = dy; a.z = z0; a.stats = st0; a.gamma = p32_ + eln_g_.off;
-    a.in_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+    a.in_drop = edrop;
     a.dz = de;
     a.partial = ln_partial_;
     ck(mimose_ops::ln_bwd(a, (int)H, G + eln_g_.off, G + eln_b_.off, nullptr, s), "ln_bwd");
+  } else {
+    ck(mimose_ops::dropout_apply(dy, de, T * H, edrop, s), "dropout_apply");
   }
   drop(dy);
   drop(z0); drop(st0); drop(h0);
-  ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s),
+  // tied decoders (LM / MLM) already wrote their [V, H] weight gradient: add
+  ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s,
+                                 tied),
      "embed_word_grad");
   ck(mimose_ops::embed_pos_grad(de, B, S, (int)H, G + pos_.off, s), "embed_pos_grad");
-  ck(mimose_ops::colsum(de, (int)T, (int)H, H, m_.type_vocab == 2 ? in.types : nullptr,
-                        m_.type_vocab, col_partial_, G + type_.off, s),
-     "colsum");
+  if (m_.type_vocab > 0)
+    ck(mimose_ops::colsum(de, (int)T, (int)H, H, m_.type_vocab == 2 ? in.types : nullptr,
+                          m_.type_vocab, col_partial_, G + type_.off, s),
+       "colsum");
   drop(de);
 
   r->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0)
@@ -1088,12 +1459,80 @@ void Trainer::optimizer_step(float grad_scale, cudaStream_t s) {
   ck(mimose_ops::adamw(p32_, am_, av_, g32_, p16_, nparam_, n_decay_, norm2_, a, s), "adamw");
 }
 
+// Checks host labels against the head's layout; for MLM writes the masked
+// row indices / labels to pos/lab and returns their count, for LM returns the
+// number of labelled positions.
+static int check_labels(const mimose_model_cfg& m, const int32_t* lb, int n, int S,
+                        int32_t* pos, int32_t* lab) {
+  int cnt = 0;
+  for (int q = 0; q < n; ++q) {
+    const int32_t v = lb[q];
+    switch (m.head) {
+      case MIMOSE_HEAD_MC:
+        if (v < 0 || v >= m.num_choices) throw std::runtime_error("label out of range");
+        break;
+      case MIMOSE_HEAD_QA:
+        if (v < 0 || v >= S) throw std::runtime_error("span label out of range");
+        break;
+      default:
+        if (v < -1 || v >= m.vocab) throw std::runtime_error("token label out of range");
+        if (v >= 0) {
+          if (pos) {
+            pos[cnt] = q;
+            lab[cnt] = v;
+          }
+          ++cnt;
+        }
+    }
+  }
+  return cnt;
+}
+
+// Device-resident labels of the token heads: the loss normaliser (LM) and
+// the masked-row list (MLM) are host quantities, so the labels are read back
+// once (the stream is synchronised) and the MLM row list is uploaded.
+void Trainer::device_labels(StepInputs& in, int B, int S, cudaStream_t s) {
+  if (m_.head != MIMOSE_HEAD_LM && m_.head != MIMOSE_HEAD_MLM) return;
+  const int64_t T = (int64_t)B * S;
+  std::vector<int32_t> lb(static_cast<size_t>(T)), pos(static_cast<size_t>(2 * T));
+  ck(cudaMemcpyAsync(lb.data(), in.labels, T * 4, cudaMemcpyDeviceToHost, s), "D2H labels");
+  ck(cudaStreamSynchronize(s), "label sync");
+  const bool mlm = m_.head == MIMOSE_HEAD_MLM;
+  const int cnt = check_labels(m_, lb.data(), (int)T, S, mlm ? pos.data() : nullptr,
+                               mlm ? pos.data() + T : nullptr);
+  in.n_valid = cnt;
+  if (!mlm || cnt == 0) return;
+  std::memmove(pos.data() + cnt, pos.data() + T, cnt * 4);
+  auto* d = static_cast<int32_t*>(take((int64_t)2 * cnt * 4 + 64, kTagInput));
+  ck(cudaMemcpyAsync(d, pos.data(), (int64_t)2 * cnt * 4, cudaMemcpyHostToDevice, s), "H2D rows");
+  ck(cudaStreamSynchronize(s), "label sync");
+  in.mask_pos = d;
+  in.mask_lab = d + cnt;
+  in.n_mask = cnt;
+}
+
+void Trainer::release_device_labels(StepInputs& in) {
+  if (in.mask_pos == nullptr) return;
+  void* p = const_cast<int32_t*>(in.mask_pos);
+  drop(p);
+  in.mask_pos = in.mask_lab = nullptr;
+}
+
+int Trainer::label_count(int B, int S) const {
+  switch (m_.head) {
+    case MIMOSE_HEAD_MC: return B / m_.num_choices;
+    case MIMOSE_HEAD_QA: return 2 * B;
+    default: return B * S;
+  }
+}
+
 void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
                         int S, int do_optimizer, cudaStream_t s, mimose_step_report* rep,
                         bool sync) {
   const int64_t T = (int64_t)B * S;
-  const int Q = B / m_.num_choices;
-  if (5 * T + Q + 1 > stage_elems_) throw std::runtime_error("staging buffer too small");
+  const int Q = label_count(B, S);
+  const bool mlm = m_.head == MIMOSE_HEAD_MLM;
+  if (7 * T + Q + 1 > stage_elems_) throw std::runtime_error("staging buffer too small");
   // double-buffered pinned staging: wait for the H2D that last read this slot
   const int k = static_cast<int>(iter_ & 1);
   if (stage_used_[k]) ck(cudaEventSynchronize(stage_ev_[k]), "staging wait");
@@ -1104,18 +1543,19 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
   int32_t* sg = pm + T;
   int32_t* ui = sg + T + 1;
   std::memcpy(tk, tokens, T * 4);
-  if (types) std::memcpy(ty, types, T * 4);
+  if (types && m_.type_vocab > 0) std::memcpy(ty, types, T * 4);
   else std::memset(ty, 0, T * 4);
   std::memcpy(lb, labels, Q * 4);
   for (int64_t i = 0; i < T; ++i)
-    if (ty[i] < 0 || ty[i] >= m_.type_vocab) throw std::runtime_error("token type out of range");
-  for (int q = 0; q < Q; ++q)
-    if (lb[q] < 0 || lb[q] >= m_.num_choices) throw std::runtime_error("label out of range");
+    if (ty[i] < 0 || ty[i] >= std::max(1, m_.type_vocab)) throw std::runtime_error("token type out of range");
   const int nu = build_token_tables(tk, T, m_.vocab, pm, sg, ui);
-  const int64_t n_in = 2 * T + Q + T + (nu + 1) + nu;
-  int32_t* d = static_cast<int32_t*>(take(n_in * 4 + 64, kTagInput));
-  // contiguous upload (uid packed right after seg)
+  // contiguous upload (uid packed right after seg, MLM rows after uid)
   std::memmove(sg + nu + 1, ui, nu * 4);
+  int32_t* mp = sg + nu + 1 + nu;
+  const int cnt = check_labels(m_, lb, Q, S, mlm ? mp : nullptr, mlm ? mp + T : nullptr);
+  if (mlm) std::memmove(mp + cnt, mp + T, cnt * 4);
+  const int64_t n_in = 2 * T + Q + T + (nu + 1) + nu + (mlm ? 2 * cnt : 0);
+  int32_t* d = static_cast<int32_t*>(take(n_in * 4 + 64, kTagInput));
   ck(cudaMemcpyAsync(d, h_stage_[k], n_in * 4, cudaMemcpyHostToDevice, s), "H2D inputs");
   ck(cudaEventRecord(stage_ev_[k], s), "event");
   stage_used_[k] = true;
@@ -1127,6 +1567,12 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
   in.seg = in.perm + T;
   in.uid = in.seg + nu + 1;
   in.n_unique = nu;
+  in.n_valid = cnt;
+  if (mlm) {
+    in.mask_pos = in.uid + nu;
+    in.mask_lab = in.mask_pos + cnt;
+    in.n_mask = cnt;
+  }
   const int64_t this_iter = iter_;
   forward_backward(in, B, S, s, rep);
   void* dv = d;
@@ -1248,7 +1694,9 @@ int mimose_trainer_step_device(mimose_trainer* tr, const int32_t* tokens, const 
     in.tokens = tokens; in.types = types; in.labels = labels;
     in.perm = perm; in.seg = seg; in.uid = uid; in.n_unique = n_unique;
     auto s = static_cast<cudaStream_t>(stream);
+    tr->impl->device_labels(in, batch, seq, s);
     tr->impl->forward_backward(in, batch, seq, s, rep);
+    tr->impl->release_device_labels(in);
     if (do_optimizer) tr->impl->optimizer_step(1.f, s);
   });
 }

@@ -53,6 +53,10 @@ struct StepInputs {  // device pointers
   const int32_t* seg = nullptr;
   const int32_t* uid = nullptr;
   int n_unique = 0;
+  int n_valid = 0;                     // LM: labelled (>= 0) positions
+  const int32_t* mask_pos = nullptr;   // MLM: masked row indices [n_mask]
+  const int32_t* mask_lab = nullptr;   // MLM: their labels [n_mask]
+  int n_mask = 0;
 };
 
 class Trainer {
@@ -98,6 +102,8 @@ class Trainer {
   int param_count() const { return static_cast<int>(param_names_.size()); }
   void param_info(int i, const char** name, int64_t* off, int64_t* n) const;
   int64_t extras_bytes(int S) const;
+  int64_t head_bytes(int S) const;
+  int64_t block_work_bytes(int S) const;
   int64_t dtr_headroom(int S) const;
   // the run so far in the reference's report schema (harness.hpp:57-118):
   // per-iteration rows with MEASURED peak bytes and device milliseconds
@@ -118,6 +124,16 @@ class Trainer {
                  cudaStream_t s);
   void* layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
                   cudaStream_t s);
+  void* attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g, cudaStream_t s);
+  void* attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
+  bool fused_attn(int S) const;
+  void* head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g, cudaStream_t s);
+  int label_count(int B, int S) const;
+ public:
+  void device_labels(StepInputs& in, int B, int S, cudaStream_t s);
+  void release_device_labels(StepInputs& in);
+
+ private:
   void free_save(LayerSave& sv);
 
   // phase machine (reference harness.hpp:215-296)
@@ -139,6 +155,7 @@ class Trainer {
   std::vector<std::string> param_names_;
   std::vector<ParamRef> param_refs_;
   ParamRef word_, pos_, type_, eln_g_, eln_b_, wp_, bp_, wc_, bc_;
+  ParamRef fln_g_, fln_b_, qaw_, qab_, mlmw_, mlmb_, mlm_g_, mlm_beta_, decb_;
   std::vector<LayerParams> lp_;
 
   float* ln_partial_ = nullptr;

@@ -37,12 +37,19 @@ class ModelConfig:
     ln_eps: float = 1e-12
     init_std: float = 0.02
     seed: int = 1234
+    arch: int = 0        # 0 post-LN BERT block, 1 pre-LN GPT-2 block
+    head: int = 0        # 0 multiple choice, 1 extractive QA, 2 causal LM (tied), 3 masked LM (tied)
+    causal: int = 0
+    gelu_tanh: int = 0
 
     def to_c(self):
         c = _lib.ModelCfg()
         for f in dataclasses.fields(self):
             setattr(c, f.name, getattr(self, f.name))
         return c
+
+    def labels_count(self, B: int, S: int) -> int:
+        return {0: B // self.num_choices, 1: 2 * B, 2: B * S, 3: B * S}[self.head]
 
 
 @dataclasses.dataclass
@@ -77,13 +84,28 @@ class TrainConfig:
         return c
 
 
-# Named configurations of BASELINE.json (multiple-choice head variants).
+# Named configurations of BASELINE.json configs[0..4].
 PRESETS = {
     # configs[0]: small BERT-like encoder, 4 layers, hidden 256, S 32-256
     "small4-h256": (ModelConfig(layers=4, hidden=256, heads=4, ffn=1024),
                     TrainConfig(batch=8, seq_min=32, seq_max=256)),
     # configs[1]: BERT-base multiple choice (SWAG-shaped 16 x 4 choices), S 64-512
     "bert-base-mc": (ModelConfig(), TrainConfig(batch=64, seq_min=64, seq_max=512)),
+    # configs[2]: RoBERTa-base / -large extractive QA (SQuAD-shaped), S up to 512
+    "roberta-base-qa": (ModelConfig(vocab=50265, max_pos=514, type_vocab=1, ln_eps=1e-5, head=1),
+                        TrainConfig(batch=12, seq_min=153, seq_max=512)),
+    "roberta-large-qa": (ModelConfig(layers=24, hidden=1024, heads=16, ffn=4096, vocab=50265,
+                                     max_pos=514, type_vocab=1, ln_eps=1e-5, head=1),
+                         TrainConfig(batch=12, seq_min=153, seq_max=512)),
+    # configs[3]: GPT-2 medium causal LM, S 128-1024
+    "gpt2-medium-lm": (ModelConfig(layers=24, hidden=1024, heads=16, ffn=4096, vocab=50257,
+                                   max_pos=1024, type_vocab=0, ln_eps=1e-5, arch=1, head=2,
+                                   causal=1, gelu_tanh=1),
+                       TrainConfig(batch=8, seq_min=128, seq_max=1024)),
+    # configs[4]: BERT-large MLM pretraining-shaped, S 128-2048 (extended position table)
+    "bert-large-mlm": (ModelConfig(layers=24, hidden=1024, heads=16, ffn=4096, max_pos=2048,
+                                   head=3),
+                       TrainConfig(batch=8, seq_min=128, seq_max=2048)),
 }
 
 
@@ -260,9 +282,17 @@ class Trainer:
         return torch.as_tensor(_DevArray(dl, 1, "<f4"), device="cuda")
 
     def logits_device(self):
+        """Last step's head logits (fp32): MC [B] per choice, QA [B * S][2]
+        (start, end). The tied token decoders (LM / MLM) keep no logits."""
         import torch
         _, _, _, _, _, dlg = self._buffers()
-        return torch.as_tensor(_DevArray(dlg, self.train.batch, "<f4"), device="cuda")
+        if self.model.head == 0:
+            return torch.as_tensor(_DevArray(dlg, self.train.batch, "<f4"), device="cuda")
+        if self.model.head == 1:
+            S = self.rows[-1]["seq"]
+            n = 2 * self.train.batch * S
+            return torch.as_tensor(_DevArray(dlg, n, "<f4"), device="cuda").reshape(-1, 2)
+        raise ValueError("token heads (LM / MLM) do not retain logits")
 
     def param_table(self) -> Dict[str, tuple]:
         out = {}
@@ -371,4 +401,31 @@ def synthetic_batch(rng: np.random.Generator, B: int, S: int, vocab: int, num_ch
         split = rng.integers(1, S, size=B)
         types[np.arange(S)[None, :] >= split[:, None]] = 1
     labels = rng.integers(0, num_choices, size=B // num_choices, dtype=np.int32)
+    return tokens, types, labels
+
+
+def synthetic_task_batch(rng: np.random.Generator, cfg: ModelConfig, B: int, S: int,
+                         mask_prob: float = 0.15):
+    """Synthetic batch for cfg.head with the label layout the head expects.
+
+    MC: [B / C] choice ids; QA: [2 B] (start, end) spans; LM: [B * S] next-token
+    ids with the last position of each sequence ignored (-1); MLM: [B * S]
+    original ids at ~mask_prob of the positions (at least one), -1 elsewhere.
+    """
+    if cfg.head == 0:
+        return synthetic_batch(rng, B, S, cfg.vocab, cfg.num_choices, max(cfg.type_vocab, 1))
+    tokens = rng.integers(0, cfg.vocab, size=(B, S), dtype=np.int32)
+    types = np.zeros((B, S), np.int32)
+    if cfg.head == 1:
+        st = rng.integers(0, S, size=B)
+        en = np.minimum(S - 1, st + rng.integers(0, 8, size=B))
+        labels = np.stack([st, en], axis=1).reshape(-1).astype(np.int32)
+    elif cfg.head == 2:
+        labels = np.full((B, S), -1, np.int32)
+        labels[:, :-1] = tokens[:, 1:]
+        labels = labels.reshape(-1)
+    else:
+        sel = rng.random((B, S)) < mask_prob
+        sel.reshape(-1)[rng.integers(0, B * S)] = True
+        labels = np.where(sel, tokens, -1).astype(np.int32).reshape(-1)
     return tokens, types, labels

@@ -44,20 +44,49 @@ def test_dropout_mask_rate():
 class _Cfg:
     layers, hidden, heads, ffn, vocab, max_pos, type_vocab = 1, 128, 2, 64, 20, 16, 2
     num_choices, hidden_dropout, attn_dropout, ln_eps, seed = 2, 0.0, 0.0, 1e-5, 3
+    arch, head, causal, gelu_tanh = 0, 0, 0, 0
 
 
-def test_oracle_gradients_match_finite_differences():
+def _labels(cfg, rng, B, S):
+    if cfg.head == 0:
+        return rng.integers(0, cfg.num_choices, size=B // cfg.num_choices).astype(np.int32)
+    if cfg.head == 1:
+        return rng.integers(0, S, size=2 * B).astype(np.int32)
+    lab = rng.integers(0, cfg.vocab, size=B * S).astype(np.int32)
+    lab[rng.random(B * S) < (0.2 if cfg.head == 2 else 0.7)] = -1
+    return lab
+
+
+VARIANTS = {
+    "bert-mc": dict(),
+    "bert-qa": dict(head=1),
+    "bert-mlm": dict(head=3),
+    "gpt2-lm": dict(arch=1, head=2, causal=1, gelu_tanh=1, type_vocab=0),
+}
+CHECK = {
+    "bert-mc": ["layer.0.attn.qkv.weight", "layer.0.ffn.in.bias", "pooler.weight",
+                "embeddings.ln.weight", "classifier.bias"],
+    "bert-qa": ["layer.0.attn.out.weight", "qa.weight", "qa.bias", "embeddings.token_type"],
+    "bert-mlm": ["mlm.transform.weight", "mlm.ln.weight", "mlm.decoder.bias", "embeddings.word"],
+    "gpt2-lm": ["layer.0.attn.qkv.weight", "layer.0.ffn.out.weight", "final_ln.weight",
+                "embeddings.word", "embeddings.position"],
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_oracle_gradients_match_finite_differences(variant):
     cfg = _Cfg()
+    for k, v in VARIANTS[variant].items():
+        setattr(cfg, k, v)
     rng = np.random.default_rng(0)
     shapes = bert_ref.param_shapes(cfg)
     params = {k: rng.standard_normal(int(np.prod(s))) * (0.5 if "ln.weight" not in k else 0.1)
               + (1.0 if "ln.weight" in k else 0.0) for k, s in shapes.items()}
     tok = rng.integers(0, cfg.vocab, size=(4, 6)).astype(np.int32)
     typ = (rng.random((4, 6)) > 0.5).astype(np.int32)
-    lab = np.array([0, 1], np.int32)
+    lab = _labels(cfg, rng, 4, 6)
     loss, _, grads = bert_ref.loss_and_grads(params, tok, typ, lab, cfg, dtype=torch.float64)
-    for name in ["layer.0.attn.qkv.weight", "layer.0.ffn.in.bias", "pooler.weight",
-                 "embeddings.ln.weight", "classifier.bias"]:
+    for name in CHECK[variant]:
         for j in rng.choice(params[name].size, size=min(3, params[name].size), replace=False):
             p2 = {k: v.copy() for k, v in params.items()}
             h = 1e-6

@@ -17,7 +17,8 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
-from paper_2209_02478_b200.trainer import ModelConfig, TrainConfig, Trainer, synthetic_batch  # noqa: E402
+from paper_2209_02478_b200.trainer import (ModelConfig, TrainConfig, Trainer,  # noqa: E402
+                                           synthetic_batch, synthetic_task_batch)
 
 TINY = dict(layers=2, hidden=256, heads=4, ffn=1024, vocab=512, max_pos=128, type_vocab=2,
             num_choices=4)
@@ -38,7 +39,8 @@ def _oracle_params(tr):
     for name, (off, n) in tr.param_table().items():
         # GEMM operands / embedding tables are consumed in bf16; biases, LayerNorm
         # parameters and the classifier vector in fp32.
-        bf16_used = name.endswith(".weight") and ("ln" not in name) and name != "classifier.weight"
+        bf16_used = (name.endswith(".weight") and ("ln" not in name)
+                     and name not in ("classifier.weight", "qa.weight"))
         bf16_used = bf16_used or name.startswith("embeddings.") and "ln" not in name
         src = p16 if bf16_used else p32
         out[name] = src[off:off + n].copy()
@@ -79,6 +81,98 @@ def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
             cos = float(np.dot(g, ref) / (np.linalg.norm(g) * nr + 1e-30))
             assert cos >= 0.995, f"{name}: cosine {cos}"
     tr.close()
+
+
+# model families beyond BERT multiple choice (SURVEY §8 a17/a18 workloads):
+# extractive QA (RoBERTa / BERT), masked LM (BERT pre-training), causal LM
+# (GPT-2: pre-LN, causal attention, tanh GELU, final LN, tied decoder; odd V).
+VARIANTS = {
+    "bert-qa": dict(TINY, type_vocab=1, head=1),
+    "bert-mlm": dict(TINY, head=3),
+    "gpt2-lm": dict(TINY, type_vocab=0, arch=1, head=2, causal=1, gelu_tanh=1, vocab=509),
+    "gpt2-mlm-notype": dict(TINY, type_vocab=0, arch=1, head=3, vocab=500),
+}
+
+
+def _variant_trainer(shape, dropout=0.0, planner="none", batch=8, seq=(16, 96)):
+    m = ModelConfig(hidden_dropout=dropout, attn_dropout=dropout, seed=77, **shape)
+    t = TrainConfig(planner=planner, batch=batch, seq_min=seq[0], seq_max=seq[1])
+    return Trainer(m, t, 4 * GiB)
+
+
+def _check_grads(got, ref_grads):
+    # absolute floor 5e-4 (L2): gradients that are exactly zero in exact
+    # arithmetic (e.g. the last LN bias under QA, whose per-sequence softmax
+    # gradients sum to zero) keep bf16 rounding noise on the GPU
+    for name, ref in ref_grads.items():
+        g = got[name]
+        nr = np.linalg.norm(ref)
+        err = np.linalg.norm(g - ref)
+        assert err <= 8e-2 * nr + 5e-4, f"{name}: rel err {err / max(nr, 1e-12):.3e}"
+        if nr > 1e-6:
+            cos = float(np.dot(g, ref) / (np.linalg.norm(g) * nr + 1e-30))
+            assert cos >= 0.995, f"{name}: cosine {cos}"
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("dropout", [0.0, 0.1])
+@pytest.mark.parametrize("S", [24, 61])
+def test_variant_parity_vs_cpu_oracle(cuda_device, variant, dropout, S):
+    from oracle import bert_ref
+    tr = _variant_trainer(VARIANTS[variant], dropout=dropout)
+    rng = np.random.default_rng(21)
+    tok, typ, lab = synthetic_task_batch(rng, tr.model, 8, S)
+    params = _oracle_params(tr)
+    assert set(params) == set(bert_ref.param_shapes(tr.model))
+    rep = tr.step(tok, typ, lab, optimizer=False)
+    ref_loss, ref_logits, ref_grads = bert_ref.loss_and_grads(params, tok, typ, lab, tr.model,
+                                                              step=0)
+    assert math.isfinite(rep["loss"])
+    assert abs(rep["loss"] - ref_loss) <= 2e-2 * max(1.0, abs(ref_loss)), (rep["loss"], ref_loss)
+    if tr.model.head == 1:
+        logits = tr.logits_device().cpu().numpy()
+        assert np.allclose(logits, ref_logits.reshape(-1, 2), atol=5e-2, rtol=5e-2)
+    _check_grads(_grads_by_name(tr), ref_grads)
+    tr.close()
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_variant_checkpointed_grads_bitwise(cuda_device, variant):
+    rng = np.random.default_rng(23)
+    shape = VARIANTS[variant]
+    grads = []
+    for forced in ([], [1], [0, 1]):
+        tr = _variant_trainer(shape, dropout=0.1)
+        batch = synthetic_task_batch(np.random.default_rng(23), tr.model, 8, 40)
+        tr.force_plan(forced)
+        rep = tr.step(*batch, optimizer=False)
+        torch.cuda.synchronize()
+        grads.append((rep["loss"], tr.grads().clone()))
+        tr.close()
+    for loss, g in grads[1:]:
+        assert loss == grads[0][0]
+        assert torch.equal(g, grads[0][1])
+
+
+@pytest.mark.parametrize("variant", ["gpt2-lm", "bert-mlm"])
+def test_variant_device_inputs_match_host(cuda_device, variant):
+    """step_device (labels on the GPU) == step (host labels) for token heads."""
+    from paper_2209_02478_b200.trainer import DeviceBatch
+    shape = VARIANTS[variant]
+    out = []
+    for dev in (False, True):
+        tr = _variant_trainer(shape, dropout=0.1)
+        tok, typ, lab = synthetic_task_batch(np.random.default_rng(29), tr.model, 8, 33)
+        if dev:
+            tr.step_device(DeviceBatch.from_host(tok, typ, lab, tr.model.vocab), optimizer=False)
+            loss = float(tr.loss_device().item())
+        else:
+            loss = tr.step(tok, typ, lab, optimizer=False)["loss"]
+        torch.cuda.synchronize()
+        out.append((loss, tr.grads().clone()))
+        tr.close()
+    assert out[0][0] == out[1][0]
+    assert torch.equal(out[0][1], out[1][1])
 
 
 @pytest.mark.parametrize("fused", [False, True])
