@@ -9,7 +9,13 @@ reference's own sampler (include/mimose/workload.hpp sample_workload, seed
 base+rank), random-init weights (N(0, 0.02)), AdamW, dropout 0.1, bf16
 compute. Budget = 40 % of the measured no-checkpoint peak at S_max
 (everything - weights, grads, AdamW state, activations, workspace - lives in
-the budget arena).
+the budget arena). --preset picks the other BASELINE configs (parity /
+reporting runs): small4-h256, roberta-{base,large}-qa, gpt2-medium-lm,
+bert-large-mlm, each with its own default size distribution and budget.
+
+N > 1: one rank per GPU; the gradient exchange is the library's own NCCL
+communicator (mimose_dp_*) with bucketed all-reduce issued as the backward
+finishes each block (MIMOSE_DP=torch: one torch all-reduce after backward).
 
 Arms
   default            this repo's B200 path (python bench.py --gpus N ...)
@@ -46,9 +52,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--budget-frac", type=float, default=0.4)
+    ap.add_argument("--budget-frac", type=float, default=None,
+                    help="budget as a fraction of the no-ckpt peak (default: per preset)")
     ap.add_argument("--preset", default="bert-base-mc")
-    ap.add_argument("--dist", default="uniform:64:512")
+    ap.add_argument("--dist", default=None, help="size distribution (default: per preset)")
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-baseline", action="store_true", help="skip no-ckpt throughput arm")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
@@ -59,7 +66,14 @@ def parse():
                          "ranks straggler cost)")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu (no comparison arms, no cpu baseline)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    from paper_2209_02478_b200.trainer import PRESET_INFO
+    _, dist_default, frac_default = PRESET_INFO[args.preset]
+    if args.dist is None:
+        args.dist = dist_default
+    if args.budget_frac is None:
+        args.budget_frac = frac_default
+    return args
 
 
 # ----------------------------------------------------------------- helpers
@@ -181,7 +195,7 @@ def cpu_step_sample(model_cfg, S, sub_batch, rng, threads):
     import numpy as np
     import torch
     from oracle import bert_ref
-    from paper_2209_02478_b200.trainer import synthetic_batch
+    from paper_2209_02478_b200.trainer import synthetic_task_batch
     torch.set_num_threads(threads)
     shapes = bert_ref.param_shapes(model_cfg)
     g = np.random.default_rng(0)
@@ -191,7 +205,7 @@ def cpu_step_sample(model_cfg, S, sub_batch, rng, threads):
                   (np.ones(int(np.prod(s)), np.float32) if "ln.weight" in k
                    else np.zeros(int(np.prod(s)), np.float32)))
               for k, s in shapes.items()}
-    tok, typ, lab = synthetic_batch(rng, sub_batch, S, model_cfg.vocab, model_cfg.num_choices)
+    tok, typ, lab = synthetic_task_batch(rng, model_cfg, sub_batch, S)
     t0 = time.perf_counter()
     _, _, grads = bert_ref.loss_and_grads(params, tok, typ, lab, model_cfg, step=0)
     # AdamW update of every parameter (what the GPU step also does)
@@ -210,10 +224,10 @@ def run_reference_arm(args, rank, world):
     if rank != 0:
         return
     import numpy as np
-    from paper_2209_02478_b200.trainer import PRESETS
+    from paper_2209_02478_b200.trainer import PRESETS, PRESET_INFO
     model_cfg, train_cfg = PRESETS[args.preset]
     threads = os.cpu_count() or 1
-    sub = 4  # sequences per sampled CPU step (one multiple-choice question)
+    sub = model_cfg.num_choices if model_cfg.head == 0 else 1  # one question / sequence
     xs = sizes_for(args.dist, train_cfg.batch, args.warmup + args.steps, args.seed)
     rng = np.random.default_rng(args.seed)
     for S in xs[:args.warmup]:
@@ -227,11 +241,11 @@ def run_reference_arm(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": f"{args.preset} (BASELINE configs[1]) CPU port", "global_batch": sub,
+        "config": {"workload": f"{PRESET_INFO[args.preset][0]} - CPU port", "global_batch": sub,
                    "seq_len": args.dist, "parallelism": "cpu"},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
-                         "sample": f"{sub} sequences per step (1 question x 4 choices) at the "
-                                   f"step's drawn S; oracle/bert_ref.py fp32 fwd+bwd + AdamW"},
+                         "sample": f"{sub} sequence(s) per step at the step's drawn S; "
+                                   f"oracle/bert_ref.py fp32 fwd+bwd + AdamW"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -243,7 +257,8 @@ def run_gpu_arm(args, rank, world, local):
     import numpy as np
     import torch
     from paper_2209_02478_b200 import _lib
-    from paper_2209_02478_b200.trainer import (PRESETS, DeviceBatch, Trainer, synthetic_batch)
+    from paper_2209_02478_b200.trainer import (PRESETS, PRESET_INFO, DeviceBatch, Trainer,
+                                               synthetic_task_batch)
     import dataclasses
 
     lib = _lib.cuda_lib()
@@ -259,8 +274,7 @@ def run_gpu_arm(args, rank, world, local):
     probe_budget = int(min(free * 0.85 / ranks_here, 150 * GiB))
     probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"), probe_budget, local)
     rng = np.random.default_rng(args.seed + 1000 * rank)
-    probe.step(*synthetic_batch(rng, B, S_max, model_cfg.vocab, model_cfg.num_choices),
-               optimizer=False, stream=stream)
+    probe.step(*synthetic_task_batch(rng, model_cfg, B, S_max), optimizer=False, stream=stream)
     peak_none = int(allmax(probe.rows[-1]["peak_reserved"], world))
     probe.close()
     budget = int(args.budget_frac * peak_none)
@@ -272,11 +286,22 @@ def run_gpu_arm(args, rank, world, local):
 
     def batches(seq_list, seed):
         g = np.random.default_rng(seed)
-        return [synthetic_batch(g, B, s, model_cfg.vocab, model_cfg.num_choices)
-                for s in seq_list]
+        return [synthetic_task_batch(g, model_cfg, B, s) for s in seq_list]
+
+    # gradient exchange for N > 1: the library's own NCCL communicator with
+    # bucketed all-reduce overlapping the backward (MIMOSE_DP=native, default
+    # on NCCL), or one torch.distributed all-reduce after backward (=torch,
+    # and always under the gloo test backend)
+    dp = None
+    if world > 1 and os.environ.get("MIMOSE_DP", "native") == "native":
+        import torch.distributed as dist
+        if dist.get_backend() == "nccl":
+            from paper_2209_02478_b200.dp import NativeDP
+            dp = NativeDP(local, rank, world)
+    bucket_mb = float(os.environ.get("MIMOSE_DP_BUCKET_MB", "32"))
 
     def allreduce_hook(tr):
-        if world == 1:
+        if world == 1 or dp is not None:
             return None
         import torch.distributed as dist
         grads = tr.grads()
@@ -288,7 +313,7 @@ def run_gpu_arm(args, rank, world, local):
     def timed_run(tr, host_batches, dev_batches):
         """W warm-up + K timed device-input steps; returns (ms list, rows)."""
         hook = allreduce_hook(tr)
-        scale = 1.0 / world
+        scale = 1.0 / world if hook else 1.0  # native DP averages by itself
 
         def one(db):
             tr.step_device(db, optimizer=False, stream=stream)
@@ -316,6 +341,8 @@ def run_gpu_arm(args, rank, world, local):
 
     # 2. Mimose trainer under the budget; sheltered calibration window first
     tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="mimose"), budget, local)
+    if dp is not None:
+        tr.attach_dp(dp, bucket_mb)
     calib = tr.train.max_sheltered_iters + 2
     cal_batches = batches(seqs[:calib], args.seed + 7 * rank + 1)
     t_cal0 = time.perf_counter()
@@ -368,7 +395,7 @@ def run_gpu_arm(args, rank, world, local):
     losses = []
 
     def e2e_run(group):
-        if world == 1:
+        if world == 1 or dp is not None:
             prev = None
             for b in group:
                 row = tr.step_async(*b, stream=stream)
@@ -401,6 +428,8 @@ def run_gpu_arm(args, rank, world, local):
     if not args.no_baseline and not args.profile_only:
         base = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"),
                        int(peak_none * 1.15) + GiB, local)
+        if dp is not None:
+            base.attach_dp(dp, bucket_mb)
         ms_none, _ = timed_run(base, hb, db)
         ms_none = allmax(ms_none, world)
         nock = samples / (ms_none / 1000.0)
@@ -412,9 +441,11 @@ def run_gpu_arm(args, rank, world, local):
         threads = os.cpu_count() or 1
         g = np.random.default_rng(1)
         S_s = run_seqs[:3]
-        tot = sum(cpu_step_sample(model_cfg, S, 4, g, threads) for S in S_s)
-        cpu = {"value": 4 * len(S_s) / tot, "unit": "samples/s", "cores": threads, "kind": "port",
-               "sample": f"3 steps x 4 sequences (one question) at S={S_s}; oracle/bert_ref.py "
+        sub = model_cfg.num_choices if model_cfg.head == 0 else 1
+        tot = sum(cpu_step_sample(model_cfg, S, sub, g, threads) for S in S_s)
+        cpu = {"value": sub * len(S_s) / tot, "unit": "samples/s", "cores": threads,
+               "kind": "port",
+               "sample": f"3 steps x {sub} sequence(s) at S={S_s}; oracle/bert_ref.py "
                          f"PyTorch-CPU fp32 fwd+bwd + AdamW, {threads} threads"}
 
     info = tr.info()
@@ -425,8 +456,7 @@ def run_gpu_arm(args, rank, world, local):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (uniform token ids, N(0,0.02) random-init weights)",
             "config": {
-                "workload": "bert-base-mc: BERT-base (L12 H768 A12 F3072 V30522) multiple-choice "
-                            "fine-tune, SWAG-shaped 16x4 choices (BASELINE configs[1])",
+                "workload": PRESET_INFO[args.preset][0],
                 "global_batch": B * world, "seq_len": args.dist, "parallelism": f"dp{world}",
                 "dp_size_stream": args.size_stream,
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
@@ -445,8 +475,12 @@ def run_gpu_arm(args, rank, world, local):
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_per_step,
                     "d2h_bytes_per_step": 4,
                     "api": "mimose_trainer_step_async + mimose_trainer_loss (1-step lag)"
-                    if world == 1 else "mimose_trainer_forward_backward + NCCL all-reduce + "
-                                       "mimose_trainer_optimizer_step",
+                    if world == 1 or dp is not None else
+                    "mimose_trainer_forward_backward + NCCL all-reduce + "
+                    "mimose_trainer_optimizer_step",
+                    "dp": ("native bucketed NCCL all-reduce overlapping backward "
+                           f"({bucket_mb:g} MB buckets)") if dp is not None else
+                          ("torch.distributed all-reduce after backward" if world > 1 else None),
                     "host_ms_per_step": sum(host_ms) / len(host_ms),
                     "losses_finite": all(l == l for l in losses)},
             "gpu_launches": int(launches),
@@ -466,6 +500,8 @@ def run_gpu_arm(args, rank, world, local):
         }
         print(json.dumps(line), flush=True)
     tr.close()
+    if dp is not None:
+        dp.close()
 
 
 def main():

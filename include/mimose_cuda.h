@@ -26,10 +26,11 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 1
+#define MIMOSE_ABI_VERSION 2
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
+typedef struct mimose_dp mimose_dp;
 
 int mimose_abi_version(void);
 const char* mimose_last_error(void);
@@ -247,6 +248,28 @@ void mimose_free_string(char* s);
  * word-embedding gradient. perm: [T], seg: [T+1], uid: [T]. */
 int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32_t* perm,
                               int32_t* seg, int32_t* uid, int* n_unique);
+
+/* ---- data parallelism (§8(b2) mimose_dp_*) --------------
+ * One NCCL communicator per rank (NCCL resolved at run time). The unique id
+ * (128 bytes) is made on rank 0 and broadcast by the caller (the reference
+ * has no DP: SPEC.md:196 - this is new surface). */
+int mimose_dp_unique_id(void* out128);
+int mimose_dp_create(int device, const void* unique_id128, int rank, int world, mimose_dp** out);
+int mimose_dp_destroy(mimose_dp* dp);
+/* in-place all-reduce of n elements; dtype 0 fp32 / 1 bf16, op 0 sum / 1 max */
+int mimose_dp_allreduce(mimose_dp* dp, void* buf, int64_t n, int dtype, int op, void* stream);
+/* Attach (dp != NULL) or detach: the trainer then sums its gradients across
+ * ranks in buckets of >= bucket_bytes on the communicator's own stream as the
+ * backward finishes each layer, and the optimizer waits for the last bucket
+ * and scales by 1/world. */
+int mimose_trainer_attach_dp(mimose_trainer* tr, mimose_dp* dp, int64_t bucket_bytes);
+/* The bucket schedule in use: triples {after_unit, begin, end} (elements of
+ * the flat gradient buffer; unit 0 = embeddings, 1..L = blocks, L+1 = head).
+ * Returns the count in *n (at most cap triples written). */
+int mimose_trainer_dp_buckets(mimose_trainer* tr, int64_t* triples, int cap, int* n);
+/* Host-only: the same schedule for arbitrary unit offsets (n_units + 1 values). */
+int mimose_dp_plan_buckets(const int64_t* unit_off, int n_units, int64_t bucket_elems,
+                           int64_t* triples, int cap, int* n);
 
 #ifdef __cplusplus
 }

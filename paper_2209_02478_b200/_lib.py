@@ -168,7 +168,19 @@ CUDA_SYMBOLS = [
     ("mimose_free_string", None, [_P]),
     ("mimose_build_token_tables", C.c_int,
      [_P, C.c_int64, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]),
+    ("mimose_dp_unique_id", C.c_int, [_P]),
+    ("mimose_dp_create", C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("mimose_dp_destroy", C.c_int, [_P]),
+    ("mimose_dp_allreduce", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, _P]),
+    ("mimose_trainer_attach_dp", C.c_int, [_P, _P, C.c_int64]),
+    ("mimose_trainer_dp_buckets", C.c_int,
+     [_P, C.POINTER(C.c_int64), C.c_int, C.POINTER(C.c_int)]),
+    ("mimose_dp_plan_buckets", C.c_int,
+     [C.POINTER(C.c_int64), C.c_int, C.c_int64, C.POINTER(C.c_int64), C.c_int,
+      C.POINTER(C.c_int)]),
 ]
+
+ABI_VERSION = 2
 
 
 def _bind(lib, symbols):
@@ -186,6 +198,9 @@ def cuda_lib():
             raise MimoseError(f"{CUDA_LIB_PATH} missing: run `make` (no CPU fallback exists)")
         lib = C.CDLL(CUDA_LIB_PATH)
         _bind(lib, CUDA_SYMBOLS)
+        if lib.mimose_abi_version() != ABI_VERSION:
+            raise MimoseError(f"{CUDA_LIB_PATH}: ABI {lib.mimose_abi_version()} != {ABI_VERSION}"
+                              " (stale build: run make)")
         _cuda = lib
     return _cuda
 

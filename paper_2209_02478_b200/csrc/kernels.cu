@@ -607,7 +607,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
                                                     float* __restrict__ v,
                                                     const float* __restrict__ g,
                                                     bf16* __restrict__ p16, int64_t n,
-                                                    int64_t n_decay, const float* __restrict__ norm2,
+                                                    const uint8_t* __restrict__ decay_chunk,
+                                                    const float* __restrict__ norm2,
                                                     mimose_ops::AdamWArgs a) {
   float clip = 1.f;
   if (a.max_grad_norm > 0.f) {
@@ -615,7 +616,8 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     clip = fminf(1.f, a.max_grad_norm / (nrm * a.grad_scale + 1e-6f));
   }
   const float gs = clip * a.grad_scale;
-  // n and n_decay are multiples of 4 (64-element aligned parameter tensors)
+  // n is a multiple of 4; decay_chunk[e / 64] = 1 when element e belongs to a
+  // decayed tensor (tensors are 64-element aligned)
   const int64_t n4 = n / 4;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -623,7 +625,7 @@ __global__ void __launch_bounds__(256) adamw_kernel(float* __restrict__ p, float
     float4 mv = reinterpret_cast<const float4*>(m)[i];
     float4 vv = reinterpret_cast<const float4*>(v)[i];
     const float4 gv = reinterpret_cast<const float4*>(g)[i];
-    const bool decay = 4 * i < n_decay;
+    const bool decay = decay_chunk[(4 * i) >> 6] != 0;
     float* pp = &pv.x;
     float* mp = &mv.x;
     float* vp = &vv.x;
@@ -1120,9 +1122,10 @@ cudaError_t grad_norm2(const float* g, int64_t n, float* partial, float* out, cu
 }
 
 cudaError_t adamw(float* p, float* m, float* v, const float* g, void* p16, int64_t n,
-                  int64_t n_decay, const float* norm2, const AdamWArgs& a, cudaStream_t s) {
+                  const uint8_t* decay_chunk, const float* norm2, const AdamWArgs& a,
+                  cudaStream_t s) {
   mimose_dev::adamw_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
-      p, m, v, g, static_cast<bf16*>(p16), n, n_decay, norm2, a);
+      p, m, v, g, static_cast<bf16*>(p16), n, decay_chunk, norm2, a);
   count_launch();
   return cudaGetLastError();
 }

@@ -108,7 +108,8 @@ cudaError_t mc_head(const void* pre, int B, int H, int C, const float* wc, const
                     void* dpre, float* dwc, float* dbc, cudaStream_t s);
 cudaError_t grad_norm2(const float* g, int64_t n, float* partial, float* out, cudaStream_t s);
 cudaError_t adamw(float* p, float* m, float* v, const float* g, void* p16, int64_t n,
-                  int64_t n_decay, const float* norm2, const AdamWArgs& a, cudaStream_t s);
+                  const uint8_t* decay_chunk, const float* norm2, const AdamWArgs& a,
+                  cudaStream_t s);
 cudaError_t f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s);
 cudaError_t init_normal(float* p, int64_t n, float mean, float std, uint64_t seed,
                         uint64_t stream, cudaStream_t s);

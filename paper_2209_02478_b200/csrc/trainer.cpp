@@ -326,50 +326,44 @@ Trainer::~Trainer() {
 ParamRef Trainer::add_param(const std::string& name, int64_t n, bool decay,
                             std::vector<ParamRef*>& fix) {
   (void)fix;
-  (void)decay;
   ParamRef r;
   r.n = n;
   r.off = nparam_;
   nparam_ += (n + kAlignElems - 1) / kAlignElems * kAlignElems;
   param_names_.push_back(name);
   param_refs_.push_back(r);
+  param_decay_.push_back(decay ? 1 : 0);
   return r;
 }
 
 // Parameter names follow oracle/bert_ref.py param_shapes (HF BERT / GPT-2
 // tensors with fused QKV). Tied LM / MLM decoders reuse embeddings.word.
+// Layout: contiguous gradient units in forward order - [embeddings]
+// [layer 0] ... [layer L-1] [final LN + head] - so that the backward finishes
+// them back to front and the data-parallel all-reduce can ship each bucket
+// while earlier layers are still differentiating. Weight decay is a
+// per-64-element chunk flag (tensors are 64-aligned).
 void Trainer::build_params() {
   std::vector<ParamRef*> fix;
   const int64_t H = H_, F = F_;
   const bool bert = m_.arch == MIMOSE_ARCH_BERT;
   lp_.resize(L_);
-  // decayed tensors first (matrices + embeddings), then biases / LayerNorm
+  unit_off_.clear();
+  unit_off_.push_back(nparam_);
   word_ = add_param("embeddings.word", (int64_t)m_.vocab * H, true, fix);
   pos_ = add_param("embeddings.position", (int64_t)m_.max_pos * H, true, fix);
   if (m_.type_vocab > 0) type_ = add_param("embeddings.token_type", (int64_t)m_.type_vocab * H, true, fix);
-  for (int l = 0; l < L_; ++l) {
-    const std::string p = "layer." + std::to_string(l) + ".";
-    lp_[l].wqkv = add_param(p + "attn.qkv.weight", 3 * H * H, true, fix);
-    lp_[l].wo = add_param(p + "attn.out.weight", H * H, true, fix);
-    lp_[l].w1 = add_param(p + "ffn.in.weight", F * H, true, fix);
-    lp_[l].w2 = add_param(p + "ffn.out.weight", H * F, true, fix);
-  }
-  switch (m_.head) {
-    case MIMOSE_HEAD_MC:
-      wp_ = add_param("pooler.weight", H * H, true, fix);
-      wc_ = add_param("classifier.weight", H, true, fix);
-      break;
-    case MIMOSE_HEAD_QA: qaw_ = add_param("qa.weight", 2 * H, true, fix); break;
-    case MIMOSE_HEAD_MLM: mlmw_ = add_param("mlm.transform.weight", H * H, true, fix); break;
-    default: break;
-  }
-  n_decay_ = nparam_;
   if (bert) {
     eln_g_ = add_param("embeddings.ln.weight", H, false, fix);
     eln_b_ = add_param("embeddings.ln.bias", H, false, fix);
   }
   for (int l = 0; l < L_; ++l) {
+    unit_off_.push_back(nparam_);
     const std::string p = "layer." + std::to_string(l) + ".";
+    lp_[l].wqkv = add_param(p + "attn.qkv.weight", 3 * H * H, true, fix);
+    lp_[l].wo = add_param(p + "attn.out.weight", H * H, true, fix);
+    lp_[l].w1 = add_param(p + "ffn.in.weight", F * H, true, fix);
+    lp_[l].w2 = add_param(p + "ffn.out.weight", H * F, true, fix);
     lp_[l].bqkv = add_param(p + "attn.qkv.bias", 3 * H, false, fix);
     lp_[l].bo = add_param(p + "attn.out.bias", H, false, fix);
     lp_[l].ln1_g = add_param(p + "attn.ln.weight", H, false, fix);
@@ -379,17 +373,24 @@ void Trainer::build_params() {
     lp_[l].ln2_g = add_param(p + "ffn.ln.weight", H, false, fix);
     lp_[l].ln2_b = add_param(p + "ffn.ln.bias", H, false, fix);
   }
+  unit_off_.push_back(nparam_);
   if (!bert) {
     fln_g_ = add_param("final_ln.weight", H, false, fix);
     fln_b_ = add_param("final_ln.bias", H, false, fix);
   }
   switch (m_.head) {
     case MIMOSE_HEAD_MC:
+      wp_ = add_param("pooler.weight", H * H, true, fix);
       bp_ = add_param("pooler.bias", H, false, fix);
+      wc_ = add_param("classifier.weight", H, true, fix);
       bc_ = add_param("classifier.bias", 1, false, fix);
       break;
-    case MIMOSE_HEAD_QA: qab_ = add_param("qa.bias", 2, false, fix); break;
+    case MIMOSE_HEAD_QA:
+      qaw_ = add_param("qa.weight", 2 * H, true, fix);
+      qab_ = add_param("qa.bias", 2, false, fix);
+      break;
     case MIMOSE_HEAD_MLM:
+      mlmw_ = add_param("mlm.transform.weight", H * H, true, fix);
       mlmb_ = add_param("mlm.transform.bias", H, false, fix);
       mlm_g_ = add_param("mlm.ln.weight", H, false, fix);
       mlm_beta_ = add_param("mlm.ln.bias", H, false, fix);
@@ -397,12 +398,22 @@ void Trainer::build_params() {
       break;
     default: break;
   }
+  unit_off_.push_back(nparam_);
 
   p32_ = static_cast<float*>(take(nparam_ * 4, kTagParam));
   p16_ = take(nparam_ * 2, kTagParam);
   g32_ = static_cast<float*>(take(nparam_ * 4, kTagGrad));
   am_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
   av_ = static_cast<float*>(take(nparam_ * 4, kTagOptim));
+  // decay flag per 64-element chunk
+  std::vector<uint8_t> chunk(static_cast<size_t>(nparam_ / kAlignElems), 0);
+  for (size_t i = 0; i < param_refs_.size(); ++i)
+    if (param_decay_[i])
+      for (int64_t c = param_refs_[i].off / kAlignElems;
+           c < (param_refs_[i].off + param_refs_[i].n + kAlignElems - 1) / kAlignElems; ++c)
+        chunk[static_cast<size_t>(c)] = 1;
+  decay_chunk_ = static_cast<uint8_t*>(take(static_cast<int64_t>(chunk.size()) + 64, kTagParam));
+  ck(cudaMemcpy(decay_chunk_, chunk.data(), chunk.size(), cudaMemcpyHostToDevice), "memcpy");
 }
 
 bool Trainer::fused_attn(int S) const {
@@ -1369,6 +1380,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     drop(stf);
     dy = dl;
   }
+  dp_unit_done(L_ + 1, s);
 
   // ---- backward through the blocks (recompute dropped ones first)
   for (int l = L_ - 1; l >= 0; --l) {
@@ -1380,6 +1392,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     }
     if (dropped[l]) layer_fwd(l, hin, out[l], &saves[l], g, s);  // recompute, same streams
     void* dx = layer_bwd(l, hin, saves[l], dy, g, s);
+    dp_unit_done(l + 1, s);
     drop(out[l]);
     dy = dx;
   }
@@ -1412,6 +1425,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
                           m_.type_vocab, col_partial_, G + type_.off, s),
        "colsum");
   drop(de);
+  dp_unit_done(0, s);
 
   r->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0)
                    .count();
@@ -1443,7 +1457,26 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   iter_ += 1;
 }
 
+void Trainer::attach_dp(DataParallel* dp, int64_t bucket_bytes) {
+  dp_ = dp;
+  buckets_.clear();
+  if (dp_ != nullptr) buckets_ = plan_buckets(unit_off_, std::max<int64_t>(bucket_bytes / 4, 1));
+}
+
+// Gradient unit `unit` is final on stream s: ship the bucket that ends here.
+void Trainer::dp_unit_done(int unit, cudaStream_t s) {
+  if (dp_ == nullptr) return;
+  for (const Bucket& b : buckets_)
+    if (b.after_unit == unit) dp_->allreduce_after(g32_ + b.begin, b.end - b.begin, s);
+}
+
+// With a native DP communicator attached the gradients were summed across
+// ranks during backward: wait for the last bucket and average (1 / world).
 void Trainer::optimizer_step(float grad_scale, cudaStream_t s) {
+  if (dp_ != nullptr) {
+    dp_->join(s);
+    grad_scale /= static_cast<float>(dp_->world());
+  }
   adam_t_ += 1;
   mimose_ops::AdamWArgs a;
   a.lr = t_.lr;
@@ -1456,7 +1489,7 @@ void Trainer::optimizer_step(float grad_scale, cudaStream_t s) {
   a.bc1 = 1.f - std::pow(t_.beta1, (float)adam_t_);
   a.bc2 = 1.f - std::pow(t_.beta2, (float)adam_t_);
   if (a.max_grad_norm > 0.f) ck(mimose_ops::grad_norm2(g32_, nparam_, norm_partial_, norm2_, s), "grad_norm2");
-  ck(mimose_ops::adamw(p32_, am_, av_, g32_, p16_, nparam_, n_decay_, norm2_, a, s), "adamw");
+  ck(mimose_ops::adamw(p32_, am_, av_, g32_, p16_, nparam_, decay_chunk_, norm2_, a, s), "adamw");
 }
 
 // Checks host labels against the head's layout; for MLM writes the masked
@@ -1612,6 +1645,9 @@ using mimose_rt::Trainer;
 
 struct mimose_trainer {
   Trainer* impl = nullptr;
+};
+struct mimose_dp {
+  mimose_rt::DataParallel* impl = nullptr;
 };
 
 namespace {
@@ -1791,6 +1827,75 @@ int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32
                               int32_t* seg, int32_t* uid, int* n_unique) {
   return guarded("mimose_build_token_tables", [&] {
     *n_unique = mimose_rt::build_token_tables(tokens, T, vocab, perm, seg, uid);
+  });
+}
+
+int mimose_dp_unique_id(void* out128) {
+  if (!out128) return fail("mimose_dp_unique_id: null argument");
+  return guarded("mimose_dp_unique_id", [&] { mimose_rt::DataParallel::unique_id(out128); });
+}
+
+int mimose_dp_create(int device, const void* uid, int rank, int world, mimose_dp** out) {
+  if (!uid || !out) return fail("mimose_dp_create: null argument");
+  return guarded("mimose_dp_create", [&] {
+    auto* dp = new mimose_dp();
+    try {
+      dp->impl = new mimose_rt::DataParallel(device, uid, rank, world);
+    } catch (...) {
+      delete dp;
+      throw;
+    }
+    *out = dp;
+  });
+}
+
+int mimose_dp_destroy(mimose_dp* dp) {
+  if (!dp) return 0;
+  return guarded("mimose_dp_destroy", [&] {
+    delete dp->impl;
+    delete dp;
+  });
+}
+
+int mimose_dp_allreduce(mimose_dp* dp, void* buf, int64_t n, int dtype, int op, void* stream) {
+  if (!dp || (!buf && n > 0)) return fail("mimose_dp_allreduce: null argument");
+  return guarded("mimose_dp_allreduce", [&] {
+    dp->impl->allreduce(buf, n, dtype, op, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int mimose_trainer_attach_dp(mimose_trainer* tr, mimose_dp* dp, int64_t bucket_bytes) {
+  if (!tr) return fail("mimose_trainer_attach_dp: null trainer");
+  return guarded("mimose_trainer_attach_dp", [&] {
+    tr->impl->attach_dp(dp ? dp->impl : nullptr, bucket_bytes);
+  });
+}
+
+static void write_triples(const std::vector<mimose_rt::Bucket>& b, int64_t* out, int cap, int* n) {
+  *n = static_cast<int>(b.size());
+  for (int i = 0; i < cap && i < static_cast<int>(b.size()); ++i) {
+    out[3 * i] = b[static_cast<size_t>(i)].after_unit;
+    out[3 * i + 1] = b[static_cast<size_t>(i)].begin;
+    out[3 * i + 2] = b[static_cast<size_t>(i)].end;
+  }
+}
+
+int mimose_trainer_dp_buckets(mimose_trainer* tr, int64_t* triples, int cap, int* n) {
+  if (!tr || !n || (cap > 0 && !triples)) return fail("mimose_trainer_dp_buckets: null argument");
+  write_triples(tr->impl->dp_buckets(), triples, cap, n);
+  return 0;
+}
+
+int mimose_dp_plan_buckets(const int64_t* unit_off, int n_units, int64_t bucket_elems,
+                           int64_t* triples, int cap, int* n) {
+  if (!unit_off || !n || n_units < 0 || (cap > 0 && !triples))
+    return fail("mimose_dp_plan_buckets: bad argument");
+  return guarded("mimose_dp_plan_buckets", [&] {
+    std::vector<int64_t> off(unit_off, unit_off + n_units + 1);
+    for (int u = 0; u < n_units; ++u)
+      if (off[static_cast<size_t>(u) + 1] < off[static_cast<size_t>(u)])
+        throw std::runtime_error("unit offsets must be non-decreasing");
+    write_triples(mimose_rt::plan_buckets(off, std::max<int64_t>(bucket_elems, 1)), triples, cap, n);
   });
 }
 

@@ -21,6 +21,7 @@
 #include "capi_common.hpp"
 #include "mimose/mimose.hpp"
 #include "mimose_cuda.h"
+#include "dp.hpp"
 
 namespace mimose_rt {
 
@@ -69,6 +70,9 @@ class Trainer {
   void forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
                         mimose_step_report* rep);
   void optimizer_step(float grad_scale, cudaStream_t s);
+  // native bucketed gradient all-reduce during backward (nullptr detaches)
+  void attach_dp(DataParallel* dp, int64_t bucket_bytes);
+  const std::vector<Bucket>& dp_buckets() const { return buckets_; }
 
   // host inputs -> staged H2D -> forward_backward (+ hook + optimizer) -> loss D2H
   void step_host(const int32_t* tokens, const int32_t* types, const int32_t* labels, int B,
@@ -151,7 +155,13 @@ class Trainer {
   float* g32_ = nullptr;
   float* am_ = nullptr;
   float* av_ = nullptr;
-  int64_t nparam_ = 0, n_decay_ = 0;
+  int64_t nparam_ = 0;
+  std::vector<char> param_decay_;
+  uint8_t* decay_chunk_ = nullptr;
+  std::vector<int64_t> unit_off_;  // gradient units: embeddings, layers, head (+ end)
+  DataParallel* dp_ = nullptr;     // not owned
+  std::vector<Bucket> buckets_;
+  void dp_unit_done(int unit, cudaStream_t s);
   std::vector<std::string> param_names_;
   std::vector<ParamRef> param_refs_;
   ParamRef word_, pos_, type_, eln_g_, eln_b_, wp_, bp_, wc_, bc_;

@@ -76,6 +76,59 @@ class DataParallelTrainer:
         return row
 
 
+class NativeDP:
+    """The library's own NCCL communicator (C ABI mimose_dp_*).
+
+    Rank 0 makes the NCCL unique id; it is broadcast over the already
+    initialised torch.distributed group (any backend: it is 128 host bytes).
+    Attach to a Trainer with ``trainer.attach_dp(dp, bucket_mb)``: gradients
+    are then summed in buckets on the communicator's high-priority stream as
+    the backward finishes each block (overlapping the remaining backward),
+    and the optimizer waits for the last bucket and scales by 1/world.
+    """
+
+    def __init__(self, device: int, rank: int, world: int, group=None, unique_id: bytes = None):
+        import ctypes as C
+        from ._lib import check, cuda_lib
+        self.lib = cuda_lib()
+        self.rank, self.world = rank, world
+        if unique_id is None:
+            buf = (C.c_char * 128)()
+            if rank == 0:
+                check(self.lib.mimose_dp_unique_id(buf))
+            unique_id = bytes(buf)
+            if world > 1:
+                import torch.distributed as dist
+                obj = [unique_id]
+                dist.broadcast_object_list(obj, src=0, group=group)
+                unique_id = obj[0]
+        uid = (C.c_char * 128).from_buffer_copy(unique_id)
+        h = C.c_void_p()
+        check(self.lib.mimose_dp_create(int(device), uid, int(rank), int(world), C.byref(h)))
+        self.handle = h
+
+    def allreduce_(self, tensor, op: str = "sum", stream=None):
+        """In-place all-reduce of a CUDA fp32 / bf16 tensor on `stream`."""
+        import torch
+        from ._lib import check
+        dt = {torch.float32: 0, torch.bfloat16: 1}[tensor.dtype]
+        s = stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        check(self.lib.mimose_dp_allreduce(self.handle, tensor.data_ptr(), tensor.numel(), dt,
+                                           {"sum": 0, "max": 1}[op], s))
+        return tensor
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.mimose_dp_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def timed(fn, *args, **kw):
     t0 = time.perf_counter()
     out = fn(*args, **kw)

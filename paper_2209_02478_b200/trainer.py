@@ -108,6 +108,26 @@ PRESETS = {
                        TrainConfig(batch=8, seq_min=128, seq_max=2048)),
 }
 
+# Workload description, default size distribution (reference workload.hpp
+# syntax) and default budget fraction per preset. QA runs at
+# 60 %: with B = 12 the constant footprint (weights, grads, AdamW state) is
+# already ~40 % of the no-checkpoint peak, so 40 % is infeasible.
+PRESET_INFO = {
+    "small4-h256": ("small BERT-like encoder L4 H256 A4 F1024, MC head, B=8 (BASELINE configs[0])",
+                    "uniform:32:256", 0.75),
+    "bert-base-mc": ("bert-base-mc: BERT-base (L12 H768 A12 F3072 V30522) multiple-choice "
+                     "fine-tune, SWAG-shaped 16x4 choices (BASELINE configs[1])",
+                     "uniform:64:512", 0.4),
+    "roberta-base-qa": ("roberta-base-qa: RoBERTa-base (L12 H768 V50265) extractive QA, "
+                        "SQuAD-shaped B=12 (BASELINE configs[2])", "normal:300:100:153:512", 0.6),
+    "roberta-large-qa": ("roberta-large-qa: RoBERTa-large (L24 H1024 V50265) extractive QA, "
+                         "SQuAD-shaped B=12 (BASELINE configs[2])", "normal:300:100:153:512", 0.6),
+    "gpt2-medium-lm": ("gpt2-medium-lm: GPT-2 medium (L24 H1024 A16 V50257) causal LM, B=8 "
+                       "(BASELINE configs[3])", "uniform:128:1024", 0.4),
+    "bert-large-mlm": ("bert-large-mlm: BERT-large (L24 H1024 A16 V30522) MLM 15%, B=8, "
+                       "positions to 2048 (BASELINE configs[4])", "uniform:128:2048", 0.3),
+}
+
 
 class _DevArray:
     """__cuda_array_interface__ view of library-owned device memory."""
@@ -252,6 +272,20 @@ class Trainer:
         self._hook = _lib.GRAD_HOOK(_cb)
         check(self.lib.mimose_trainer_set_grad_hook(self.handle, self._hook, None))
 
+    def attach_dp(self, dp, bucket_mb: float = 32.0):
+        """Native bucketed all-reduce during backward (dp: dp.NativeDP or None).
+        With it attached, optimizer steps average over ranks by themselves."""
+        self._dp = dp
+        check(self.lib.mimose_trainer_attach_dp(self.handle, dp.handle if dp else None,
+                                                int(bucket_mb * (1 << 20))))
+
+    def dp_buckets(self):
+        """[(after_unit, begin, end)] of the attached schedule (flat grad elements)."""
+        out = (C.c_int64 * (3 * 512))()
+        n = C.c_int()
+        check(self.lib.mimose_trainer_dp_buckets(self.handle, out, 512, C.byref(n)))
+        return [tuple(out[3 * i:3 * i + 3]) for i in range(min(n.value, 512))]
+
     # ------------------------------------------------------------ buffers
     def _buffers(self):
         p32, p16, g32, dl, dlg = (C.c_void_p() for _ in range(5))
@@ -343,6 +377,9 @@ class Trainer:
 
     def close(self):
         if getattr(self, "handle", None):
+            if getattr(self, "_dp", None) is not None:
+                self.lib.mimose_trainer_attach_dp(self.handle, None, 0)
+                self._dp = None
             self.lib.mimose_trainer_destroy(self.handle)
             self.handle = None
         self.ctx.close()

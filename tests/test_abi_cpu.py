@@ -41,7 +41,7 @@ def test_cuda_lib_exports_exactly_the_header():
     assert all(s.startswith("mimose_") for s in exp), [s for s in exp if not s.startswith("mimose_")]
     bound = {name for name, _, _ in _lib.CUDA_SYMBOLS}
     assert set(decl) == bound, set(decl) ^ bound
-    assert lib.mimose_abi_version() == 1
+    assert lib.mimose_abi_version() == _lib.ABI_VERSION == 2
 
 
 def test_host_lib_exports_exactly_the_header():
@@ -126,3 +126,50 @@ def test_token_tables_stable_counting_sort():
         assert np.all(tok[pos] == uid[u])
         assert np.all(np.diff(pos) > 0)  # ascending positions -> fixed summation order
     assert sorted(perm.tolist()) == list(range(1000))
+
+
+def _plan(off, bucket):
+    from paper_2209_02478_b200 import _lib
+    lib = _lib.cuda_lib()
+    arr = (C.c_int64 * len(off))(*off)
+    out = (C.c_int64 * (3 * len(off)))()
+    n = C.c_int()
+    _lib.check(lib.mimose_dp_plan_buckets(arr, len(off) - 1, bucket, out, len(off), C.byref(n)))
+    return [tuple(out[3 * i:3 * i + 3]) for i in range(n.value)]
+
+
+def test_dp_bucket_schedule_covers_grads_back_to_front():
+    """Buckets tile the flat gradient buffer exactly once, are issued in
+    backward completion order (head, last block, ..., embeddings), each
+    >= the bucket size except the final one, and only ever cover units that
+    are already final when issued."""
+    rng = random.Random(3)
+    for _ in range(200):
+        U = rng.randint(1, 30)
+        sizes = [rng.choice([0, 64, 640, 7_000_000 // 64 * 64]) for _ in range(U)]
+        off = [0]
+        for s in sizes:
+            off.append(off[-1] + s)
+        bucket = rng.choice([1, 64, 1000, 5_000_000, 10 ** 9])
+        b = _plan(off, bucket)
+        covered = sorted((beg, end) for _, beg, end in b)
+        pos = 0
+        for beg, end in covered:
+            assert beg == pos and end > beg
+            pos = end
+        assert pos == off[-1] or (pos == 0 and off[-1] == 0)
+        units = [u for u, _, _ in b]
+        assert units == sorted(units, reverse=True)
+        for k, (u, beg, end) in enumerate(b):
+            assert beg == off[u]  # the bucket starts at the unit just finished
+            if k < len(b) - 1:
+                assert end - beg >= bucket
+
+
+def test_dp_bucket_schedule_examples():
+    # 3 units of 100 elements, 150-element buckets: after unit 1 -> [100, 300), after unit 0
+    assert _plan([0, 100, 200, 300], 150) == [(1, 100, 300), (0, 0, 100)]
+    # one big bucket: only at the end
+    assert _plan([0, 100, 200, 300], 10 ** 6) == [(0, 0, 300)]
+    # per-unit buckets
+    assert _plan([0, 100, 200, 300], 1) == [(2, 200, 300), (1, 100, 200), (0, 0, 100)]

@@ -297,3 +297,38 @@ def test_dtr_reactive_eviction_on_the_arena(cuda_device):
     assert r1["loss"] == r0["loss"]
     assert torch.equal(tr.grads(), g0)
     tr.close()
+
+
+def test_native_dp_world1_bucketed_allreduce_is_identity(cuda_device):
+    """The native NCCL path (comm stream, per-block buckets, join before the
+    optimizer) on a 1-rank communicator leaves every step bit-identical to the
+    plain run, and the bucket schedule tiles the gradient buffer."""
+    from paper_2209_02478_b200.dp import NativeDP
+    rng = np.random.default_rng(31)
+    batches = [synthetic_batch(rng, 8, s, TINY["vocab"], 4) for s in (32, 40, 24)]
+    runs = []
+    for native in (False, True):
+        tr = _tiny_trainer(dropout=0.1, lr=1e-3)
+        dp = None
+        if native:
+            dp = NativeDP(0, 0, 1)
+            tr.attach_dp(dp, bucket_mb=0.5)
+            b = tr.dp_buckets()
+            assert len(b) >= 2
+            spans = sorted((x[1], x[2]) for x in b)
+            assert spans[0][0] == 0 and all(spans[i][1] == spans[i + 1][0]
+                                            for i in range(len(spans) - 1))
+            assert spans[-1][1] == tr.grads().numel()
+        losses = [tr.step(*bt)["loss"] for bt in batches]
+        torch.cuda.synchronize()
+        runs.append((losses, tr.params().clone()))
+        tr.close()
+        if dp is not None:
+            x = torch.arange(1000, device="cuda", dtype=torch.float32)
+            y = x.clone()
+            dp.allreduce_(y)
+            torch.cuda.synchronize()
+            assert torch.equal(x, y)
+            dp.close()
+    assert runs[0][0] == runs[1][0]
+    assert torch.equal(runs[0][1], runs[1][1])
