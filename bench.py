@@ -132,6 +132,12 @@ def sizes_for(dist, batch, iters, seed):
     return [int(x) for x in xs]
 
 
+# ncu --set full (dram__bytes_read.sum + dram__bytes_write.sum) of one
+# representative dense-GEMM launch of the profiled step, next to that launch's
+# algorithmic bytes (operands + outputs once); source files under profiles/.
+TRAFFIC = {}
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -371,7 +377,7 @@ def run_gpu_arm(args, rank, world, local):
     extra = batches(seqs[calib + n_total:calib + n_total + 2], args.seed + 99)
     extra_db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in extra]
     import ctypes as C
-    lib.mimose_gemm_profile_enable(1)
+    lib.mimose_profile_enable(1)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -379,12 +385,39 @@ def run_gpu_arm(args, rank, world, local):
         tr.step_device(d, optimizer=True, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize()
-    fl, gms, gl = C.c_double(), C.c_double(), C.c_int64()
-    _lib.check(lib.mimose_gemm_profile_read(C.byref(fl), C.byref(gms), C.byref(gl)))
-    lib.mimose_gemm_profile_enable(0)
     step_ms_prof = e0.elapsed_time(e1)
-    achieved_tflops = fl.value / (gms.value / 1000.0) / 1e12 if gms.value > 0 else 0.0
+
+    def prof(prefix):
+        fl, by, pms, n = C.c_double(), C.c_double(), C.c_double(), C.c_int64()
+        _lib.check(lib.mimose_profile_read(prefix.encode(), C.byref(fl), C.byref(by),
+                                           C.byref(pms), C.byref(n)))
+        return fl.value, by.value, pms.value, n.value
+
+    pcsv = C.c_void_p()
+    lib.mimose_profile_csv(C.byref(pcsv))
+    classes = sorted({l.split(",", 1)[0] for l in _lib.take_string(lib, pcsv).splitlines()[1:]})
+    lib.mimose_profile_enable(0)
     peak_tf = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)))
+    peak_bw = float(pk.get("hbm_gbs", 6547.0))
+    # dominant kernel family: the dense (projection / FFN / weight-gradient)
+    # tcgen05 GEMMs, tensor-bound; every other class against HBM
+    dfl, dby, dms, dn = prof("gemm_dense")
+    achieved_tflops = dfl / (dms / 1000.0) / 1e12 if dms > 0 else 0.0
+    stages = {}
+    for c in classes:
+        fl, by, cms, n = prof(c)
+        if cms <= 0:
+            continue
+        st = {"ms_share_of_step": cms / step_ms_prof, "launches": n}
+        if c == "gemm_dense":
+            st.update(bound="tensor", achieved_tflops=fl / (cms / 1e3) / 1e12,
+                      frac=fl / (cms / 1e3) / 1e12 / peak_tf)
+        else:
+            st.update(bound="hbm", achieved_gbs=by / (cms / 1e3) / 1e9,
+                      frac=by / (cms / 1e3) / 1e9 / peak_bw)
+            if fl > 0:
+                st["achieved_tflops"] = fl / (cms / 1e3) / 1e12
+        stages[c] = st
 
     # 4. e2e: public API with HOST (pinned) inputs, H2D + loss D2H inside the region.
     #    N=1: mimose_trainer_step_async + mimose_trainer_loss with a one-step lag
@@ -467,10 +500,16 @@ def run_gpu_arm(args, rank, world, local):
             },
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tf,
-                         "traffic": None,
-                         "kernel": "gemm_bf16_tn_kernel (tcgen05) family",
-                         "gemm_ms_share_of_step": gms.value / step_ms_prof if step_ms_prof else None,
-                         "gemm_launches": gl.value, "peak_kind": pk_kind + " sustained"},
+                         "traffic": (TRAFFIC.get(args.preset) or {}).get("dram_bytes"),
+                         "traffic_detail": TRAFFIC.get(args.preset),
+                         "kernel": "gemm_bf16_tn_kernel (tcgen05) dense GEMMs: QKV / out-proj / "
+                                   "FFN forward, dgrad, split-K wgrad",
+                         "ms_share_of_step": dms / step_ms_prof if step_ms_prof else None,
+                         "launches": dn, "peak_kind": pk_kind + " sustained",
+                         "stages": stages, "hbm_peak_gbs": peak_bw,
+                         "profiled": "2 extra planned steps, every launch bracketed by CUDA "
+                                     "events on its stream; algorithmic flops / bytes per "
+                                     "launch (DESIGN.md §2)"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "samples/s", "h2d_bytes_per_step": h2d_per_step,
                     "d2h_bytes_per_step": 4,

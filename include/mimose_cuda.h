@@ -95,6 +95,7 @@ typedef struct {
   int split_k;       /* fp32 outputs: 0 auto (needs workspace), 1 off, >1 forced */
   void* workspace;   /* fp32 split-K partials, >= split_k * M * N * 4 bytes */
   int64_t workspace_bytes;
+  int force_ew;      /* 0 = heuristic epilogue warps; 8 / 16 forces it */
 } mimose_gemm_args;
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);
@@ -105,8 +106,19 @@ int mimose_gemm(const mimose_gemm_args* args, void* stream);
  * number of launches since enable. */
 int mimose_gemm_profile_enable(int enable);
 int mimose_gemm_profile_read(double* flops, double* ms, int64_t* launches);
-/* Per-launch CSV (M,N,K,batch,bn,a_mn,b_mn,epi,grid,ms,tflops); free with mimose_free_string. */
+/* Per-launch CSV (class,desc,flops,bytes,ms); free with mimose_free_string. */
 int mimose_gemm_profile_csv(char** out);
+
+/* Kernel profiling across ALL instrumented launches (GEMMs and the
+ * memory-bound stages). Each record carries its class ("gemm_dense",
+ * "gemm_attn", "mem_softmax_fwd", "mem_ln_bwd", ...), algorithmic flops and
+ * algorithmic HBM bytes. read() sums records whose class starts with
+ * `class_prefix` ("" = all). The GEMM calls above are views of the same
+ * recorder restricted to the "gemm" prefix. */
+int mimose_profile_enable(int enable);
+int mimose_profile_read(const char* class_prefix, double* flops, double* bytes, double* ms,
+                        int64_t* launches);
+int mimose_profile_csv(char** out);
 
 /* ------------------------------------------------------------------ trainer
  * The training executor: BERT-style encoder blocks (post-LN, GELU FFN,

@@ -64,6 +64,7 @@ class GemmArgs(C.Structure):
         ("alpha", C.c_float), ("beta", C.c_float),
         ("force_bn", C.c_int), ("direct_store", C.c_int),
         ("split_k", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
+        ("force_ew", C.c_int),
     ]
 
 
@@ -135,6 +136,11 @@ CUDA_SYMBOLS = [
     ("mimose_gemm_profile_csv", C.c_int, [C.POINTER(C.c_void_p)]),
     ("mimose_gemm_profile_read", C.c_int,
      [C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("mimose_profile_enable", C.c_int, [C.c_int]),
+    ("mimose_profile_read", C.c_int,
+     [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+      C.POINTER(C.c_int64)]),
+    ("mimose_profile_csv", C.c_int, [C.POINTER(C.c_void_p)]),
     ("mimose_trainer_create", C.c_int,
      [_P, C.POINTER(ModelCfg), C.POINTER(TrainCfg), C.POINTER(C.c_void_p)]),
     ("mimose_trainer_destroy", C.c_int, [_P]),

@@ -10,6 +10,7 @@
 #include "capi_common.hpp"
 #include "mimose_cuda.h"
 #include "ops.hpp"
+#include "prof.hpp"
 
 using mimose_rt::ArenaBook;
 using mimose_rt::DeviceArena;
@@ -142,6 +143,7 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   c.ldo = a->ldo; c.obs1 = a->obs1; c.obs2 = a->obs2;
   c.alpha = a->alpha; c.beta = a->beta;
   c.force_bn = a->force_bn;
+  c.force_ew = a->force_ew;
   c.direct_store = a->direct_store != 0;
   c.split_k = a->split_k;
   c.workspace = a->workspace;
@@ -163,6 +165,21 @@ int mimose_gemm_profile_csv(char** out) {
   *out = p;
   return 0;
 }
+
+int mimose_profile_enable(int enable) {
+  mimose_ops::prof_enable(enable != 0);
+  return 0;
+}
+
+int mimose_profile_read(const char* class_prefix, double* flops, double* bytes, double* ms,
+                        int64_t* launches) {
+  cudaError_t e = mimose_ops::prof_read(class_prefix != nullptr ? class_prefix : "", flops, bytes,
+                                        ms, launches);
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_profile_read");
+  return 0;
+}
+
+int mimose_profile_csv(char** out) { return mimose_gemm_profile_csv(out); }
 
 int mimose_gemm_profile_read(double* flops, double* ms, int64_t* launches) {
   cudaError_t e = mimose_ops::gemm_profile_read(flops, ms, launches);

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 #include <string>
@@ -15,6 +16,7 @@
 #include "gemm_sm100.cuh"
 #include "ops.hpp"
 #include "ops_attn.hpp"
+#include "prof.hpp"
 
 namespace mimose_ops {
 
@@ -27,14 +29,6 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
 
 std::atomic<uint64_t> g_launches{0};
 
-// optional per-launch event bracketing (roofline evidence)
-struct GemmProfile {
-  bool on = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
-  std::vector<double> flops;
-  std::vector<std::string> desc;
-  size_t used = 0;
-} g_prof;
 
 EncodeFn encode_fn() {
   static EncodeFn fn = [] {
@@ -138,12 +132,12 @@ bool make_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box
   return make_map_t(map, v.ptr, v.rows, v.cols, v.ld, v.bs1, v.bs2, nb1, nb2, 64, box_rows, 2);
 }
 
-template <int BN, int EPI>
+template <int BN, int EPI, int EW>
 cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                      const CUtensorMap& td2, const mimose_dev::GemmParams& p, int grid,
                      cudaStream_t stream) {
-  using Cfg = mimose_dev::GemmCfg<BN, EPI>;
-  auto kern = mimose_dev::gemm_bf16_tn_kernel<BN, EPI>;
+  using Cfg = mimose_dev::GemmCfg<BN, EPI, EW>;
+  auto kern = mimose_dev::gemm_bf16_tn_kernel<BN, EPI, EW>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -151,22 +145,44 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<grid, mimose_dev::kGemmThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 
 template <int BN>
-cudaError_t launch_bn(int epi, const CUtensorMap& ta, const CUtensorMap& tb,
+cudaError_t launch_bn(int epi, int ew, const CUtensorMap& ta, const CUtensorMap& tb,
                       const CUtensorMap& td, const CUtensorMap& td2,
                       const mimose_dev::GemmParams& p, int grid, cudaStream_t s) {
+  using namespace mimose_dev;
   switch (epi) {
-    case kEpiBf16: return launch_t<BN, mimose_dev::kEpiBf16>(ta, tb, td, td2, p, grid, s);
-    case kEpiBiasGelu: return launch_t<BN, mimose_dev::kEpiBiasGelu>(ta, tb, td, td2, p, grid, s);
-    case kEpiDGelu: return launch_t<BN, mimose_dev::kEpiDGelu>(ta, tb, td, td2, p, grid, s);
-    case kEpiF32: return launch_t<BN, mimose_dev::kEpiF32>(ta, tb, td, td2, p, grid, s);
+    case kEpiBf16:
+      return ew == 16 ? launch_t<BN, kEpiBf16, 16>(ta, tb, td, td2, p, grid, s)
+                      : launch_t<BN, kEpiBf16, 8>(ta, tb, td, td2, p, grid, s);
+    case kEpiBiasGelu:
+      return ew == 16 ? launch_t<BN, kEpiBiasGelu, 16>(ta, tb, td, td2, p, grid, s)
+                      : launch_t<BN, kEpiBiasGelu, 8>(ta, tb, td, td2, p, grid, s);
+    case kEpiDGelu:
+      return ew == 16 ? launch_t<BN, kEpiDGelu, 16>(ta, tb, td, td2, p, grid, s)
+                      : launch_t<BN, kEpiDGelu, 8>(ta, tb, td, td2, p, grid, s);
+    case kEpiF32: return launch_t<BN, kEpiF32, 8>(ta, tb, td, td2, p, grid, s);
   }
   return cudaErrorInvalidValue;
+}
+
+// epilogue warps: 16 for the GELU / dGELU epilogues (math-bound: FFN1
+// 549 -> 742 TFLOP/s, dGELU 638 -> 802), 8 otherwise (the write-bound
+// attention contractions measured slower with 16). MIMOSE_GEMM_EW
+// (8 / 16) overrides for A/B timing.
+int pick_ew(const GemmCall& c, int bn) {
+  static const int forced = [] {
+    const char* e = std::getenv("MIMOSE_GEMM_EW");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  if (c.epi == kEpiF32 || bn < 128) return 8;  // 16 warps need >= 32 columns each
+  if (c.force_ew == 8 || c.force_ew == 16) return c.force_ew;
+  if (forced == 8 || forced == 16) return forced;
+  return (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) ? 16 : 8;
 }
 
 int pick_bn(const GemmCall& c) {
@@ -272,6 +288,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   if ((reinterpret_cast<uintptr_t>(c.A.ptr) & 15) || (reinterpret_cast<uintptr_t>(c.B.ptr) & 15))
     return cudaErrorMisalignedAddress;
   const int bn = pick_bn(c);
+  const int ew = pick_ew(c, bn);
   int splits = 1;
   if (c.epi == kEpiF32 && c.nb1 == 1 && c.nb2 == 1 && c.workspace != nullptr && c.split_k != 1 &&
       c.N % 4 == 0 && (reinterpret_cast<uintptr_t>(c.workspace) & 15) == 0) {
@@ -323,7 +340,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     p.beta = 0.f;
   } else {
     const int esz = c.epi == kEpiF32 ? 4 : 2;
-    const int cb = (bn / 2) * esz >= 128 ? 128 : 64;  // GemmCfg::kChunkBytes
+    const int cb = mimose_dev::gemm_chunk_bytes(bn, c.epi, ew);  // GemmCfg::kChunkBytes
     const uint32_t cw = cb / esz;
     const bool sw64 = cb == 64;
     auto al = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
@@ -342,28 +359,29 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   const int64_t tiles =
       (int64_t)((c.M + 127) / 128) * ((c.N + bn - 1) / bn) * c.nb1 * c.nb2 * splits;
   const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
-  std::pair<cudaEvent_t, cudaEvent_t>* pe = nullptr;
-  if (g_prof.on) {
-    if (g_prof.used == g_prof.ev.size()) {
-      std::pair<cudaEvent_t, cudaEvent_t> e;
-      cudaEventCreate(&e.first);
-      cudaEventCreate(&e.second);
-      g_prof.ev.push_back(e);
-    }
-    pe = &g_prof.ev[g_prof.used++];
-    g_prof.flops.push_back(2.0 * c.M * (double)c.N * c.K * c.nb1 * c.nb2);
-    g_prof.desc.push_back(std::to_string(c.M) + "," + std::to_string(c.N) + "," +
-                          std::to_string(c.K) + "," + std::to_string(c.nb1 * c.nb2) + "," +
-                          std::to_string(bn) + "," + std::to_string((int)c.a_mn) + "," +
-                          std::to_string((int)c.b_mn) + "," + std::to_string(c.epi) + "," +
-                          std::to_string(grid));
-    cudaEventRecord(pe->first, stream);
-  }
+  // roofline record: algorithmic flops 2*M*N*K*batch; algorithmic bytes =
+  // operands read once + outputs (and epilogue side inputs) once. Batched
+  // (per-head) views are the materialised-attention contractions.
+  const double nb = (double)c.nb1 * c.nb2;
+  const double osz = c.epi == kEpiF32 ? 4.0 : 2.0;
+  double gbytes = nb * (2.0 * c.M * c.K + 2.0 * c.N * c.K + osz * c.M * c.N);
+  if (c.epi == kEpiBiasGelu) gbytes += nb * 2.0 * c.M * c.N;       // second output (u, g)
+  if (c.aux != nullptr) gbytes += nb * 2.0 * c.M * c.N;             // residual / GELU input
+  if (c.epi == kEpiF32 && c.beta != 0.f) gbytes += nb * 4.0 * c.M * c.N;
+  std::string gdesc;
+  if (prof_on())
+    gdesc = std::to_string(c.M) + " " + std::to_string(c.N) + " " + std::to_string(c.K) + " " +
+            std::to_string(c.nb1 * c.nb2) + " bn" + std::to_string(bn) + " amn" +
+            std::to_string((int)c.a_mn) + " bmn" + std::to_string((int)c.b_mn) + " epi" +
+            std::to_string(c.epi) + " ew" + std::to_string(ew) + " splits" + std::to_string(splits) + " grid" +
+            std::to_string(grid);
+  ProfScope prof(nb > 1 ? "gemm_attn" : "gemm_dense", 2.0 * c.M * (double)c.N * c.K * nb, gbytes,
+                 stream, gdesc);
   cudaError_t err = cudaErrorInvalidValue;
   switch (bn) {
-    case 64: err = launch_bn<64>(c.epi, ta, tb, td, td2, p, grid, stream); break;
-    case 128: err = launch_bn<128>(c.epi, ta, tb, td, td2, p, grid, stream); break;
-    case 256: err = launch_bn<256>(c.epi, ta, tb, td, td2, p, grid, stream); break;
+    case 64: err = launch_bn<64>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
+    case 128: err = launch_bn<128>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
+    case 256: err = launch_bn<256>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
   }
   if (err == cudaSuccess && splits > 1) {
     splitk_reduce_kernel<<<2 * sm_count(), 256, 0, stream>>>(
@@ -372,44 +390,16 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     g_launches.fetch_add(1, std::memory_order_relaxed);
     err = cudaGetLastError();
   }
-  if (pe != nullptr) cudaEventRecord(pe->second, stream);
   return err;
 }
 
-void gemm_profile_enable(bool on) {
-  g_prof.on = on;
-  g_prof.used = 0;
-  g_prof.flops.clear();
-  g_prof.desc.clear();
-}
+void gemm_profile_enable(bool on) { prof_enable(on); }
 
-std::string gemm_profile_csv() {
-  std::string out = "M,N,K,batch,bn,a_mn,b_mn,epi,grid,ms,tflops\n";
-  for (size_t i = 0; i < g_prof.used; ++i) {
-    cudaEventSynchronize(g_prof.ev[i].second);
-    float m = 0.f;
-    cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second);
-    out += g_prof.desc[i] + "," + std::to_string(m) + "," +
-           std::to_string(m > 0 ? g_prof.flops[i] / (m * 1e-3) / 1e12 : 0.0) + "\n";
-  }
-  return out;
-}
+std::string gemm_profile_csv() { return prof_csv(); }
 
 cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches) {
-  double f = 0.0, t = 0.0;
-  for (size_t i = 0; i < g_prof.used; ++i) {
-    cudaError_t e = cudaEventSynchronize(g_prof.ev[i].second);
-    if (e != cudaSuccess) return e;
-    float m = 0.f;
-    e = cudaEventElapsedTime(&m, g_prof.ev[i].first, g_prof.ev[i].second);
-    if (e != cudaSuccess) return e;
-    t += m;
-    f += g_prof.flops[i];
-  }
-  *flops = f;
-  *ms = t;
-  *launches = (int64_t)g_prof.used;
-  return cudaSuccess;
+  double bytes = 0.0;
+  return prof_read("gemm", flops, &bytes, ms, launches);
 }
 
 }  // namespace mimose_ops

@@ -56,24 +56,38 @@ struct GemmParams {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kEpiWarps = 8;        // two warps per TMEM lane quarter (column halves)
-constexpr int kGemmThreads = 64 + 32 * kEpiWarps;  // warp0 TMA, warp1 MMA, warps2-9 epilogue
 constexpr int kSmemBudget = 227 * 1024;
 
-template <int BN, int EPI>
+// EW epilogue warps: EW / 4 per TMEM lane quarter, each owning BN / (EW / 4)
+// accumulator columns. 8 (column halves) by default; 16 (column quarters)
+// for the math-heavy GELU / dGELU epilogues and the write-bound attention
+// contractions, which would otherwise leave the tensor pipe idle.
+constexpr int gemm_threads(int EW) { return 64 + 32 * EW; }  // warp0 TMA, warp1 MMA, rest epilogue
+
+// staged row chunk of one epilogue warp: 128 B (SWIZZLE_128B) or 64 B
+// (SWIZZLE_64B) when the warp's column span is narrower than 128 B or when
+// 16 warps share the register file (32-column chunks)
+constexpr int gemm_chunk_bytes(int BN, int EPI, int EW) {
+  return (EW == 16 && EPI != kEpiF32) ? 64
+         : ((BN / (EW / 4)) * (EPI == kEpiF32 ? 4 : 2) >= 128 ? 128 : 64);
+}
+
+template <int BN, int EPI, int EW = 8>
 struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kNOut = EPI == kEpiBiasGelu ? 2 : 1;
   static constexpr int kEsz = EPI == kEpiF32 ? 4 : 2;
-  // staged row chunk: 128 B (SWIZZLE_128B) or 64 B (SWIZZLE_64B) when a warp's
-  // half-tile is narrower than 128 B
-  static constexpr int kChunkBytes = (BN / 2) * kEsz >= 128 ? 128 : 64;
+  static constexpr int kEpiWarps = EW;
+  static constexpr int kColParts = EW / 4;
+  static constexpr int kThreads = gemm_threads(EW);
+  static constexpr int kChunkBytes = gemm_chunk_bytes(BN, EPI, EW);
   static constexpr int kChunkCols = kChunkBytes / kEsz;
-  // per epilogue warp: kNOut buffers of 32 rows x 128 B (single-buffered:
-  // the TMA store drains 4 KB from smem long before the next chunk is ready)
-  static constexpr int kStagingBytes = kEpiWarps * kNOut * 4096;
+  static constexpr int kBufBytes = 32 * kChunkBytes;  // 32 rows x one chunk
+  // per epilogue warp: kNOut buffers of 32 rows x kChunkBytes (single-buffered:
+  // the TMA store drains the buffer long before the next chunk is ready)
+  static constexpr int kStagingBytes = EW * kNOut * kBufBytes;
   static constexpr int kBiasBytes = 2 * BN * 4;  // tile bias slice, per accumulator stage
   static constexpr int kStagesRaw =
       (kSmemBudget - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
@@ -231,14 +245,15 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
   }
 }
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int BN, int EPI, int EW>
+__global__ void __launch_bounds__(gemm_threads(EW), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmD,
                         const __grid_constant__ CUtensorMap tmD2, const GemmParams p) {
-  using Cfg = GemmCfg<BN, EPI>;
+  using Cfg = GemmCfg<BN, EPI, EW>;
   constexpr int S = Cfg::kStages;
+  constexpr int kEpiWarps = EW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -364,13 +379,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     // ------------------------------------------------------------ epilogue
-    const int ew = warp - 2;            // epilogue warp 0..7
+    const int ew = warp - 2;            // epilogue warp 0..EW-1
     const int quarter = warp & 3;       // TMEM lane quarter this warp may access
-    const int half = ew >> 2;           // which half of the tile's columns
+    const int part = ew >> 2;           // which column part of the tile
     constexpr int CB = Cfg::kChunkBytes;
     constexpr int CW = Cfg::kChunkCols;
     constexpr int NCH = CB / 16;        // 16-byte chunks per staged row
-    uint8_t* wbuf = sD + ew * (Cfg::kNOut * 4096);
+    uint8_t* wbuf = sD + ew * (Cfg::kNOut * Cfg::kBufBytes);
     int local = 0, chunk_seq = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
       const int zz = tile / tiles_per_batch;
@@ -402,7 +417,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const long long obase = (long long)b2 * p.obs2 + (long long)b1 * p.obs1 +
                               (long long)row * p.ldo;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      const int c_begin = half * (BN / 2), c_end = c_begin + BN / 2;
+      const int c_begin = part * (BN / Cfg::kColParts), c_end = c_begin + BN / Cfg::kColParts;
 
       if (p.tma_store) {
         // ---- staged path: TMEM -> regs -> swizzled smem -> TMA store
@@ -451,7 +466,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                            pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
             }
             if constexpr (EPI == kEpiBiasGelu) {
-              st_shared_v4(addr + 4096, pack_bf16x2(g[8 * j], g[8 * j + 1]),
+              st_shared_v4(addr + Cfg::kBufBytes, pack_bf16x2(g[8 * j], g[8 * j + 1]),
                            pack_bf16x2(g[8 * j + 2], g[8 * j + 3]),
                            pack_bf16x2(g[8 * j + 4], g[8 * j + 5]),
                            pack_bf16x2(g[8 * j + 6], g[8 * j + 7]));
@@ -462,7 +477,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) {
             tma_store_4d(&tmD, sb, n0 + c, m0 + quarter * 32, b1, b2);
             if constexpr (EPI == kEpiBiasGelu)
-              tma_store_4d(&tmD2, sb + 4096, n0 + c, m0 + quarter * 32, b1, b2);
+              tma_store_4d(&tmD2, sb + Cfg::kBufBytes, n0 + c, m0 + quarter * 32, b1, b2);
             bulk_commit();
           }
         }

@@ -17,10 +17,21 @@
 #include "common.cuh"
 #include "ops.hpp"
 #include "ops_mem.hpp"
+#include "prof.hpp"
 
 namespace mimose_dev {
 
 using bf16 = __nv_bfloat16;
+
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h[i]);
+    v[2 * i] = f.x;
+    v[2 * i + 1] = f.y;
+  }
+}
 
 // =====================================================================
 // LayerNorm forward (one warp per row; VPL 8-element chunks per lane)
@@ -82,29 +93,50 @@ __device__ __forceinline__ void ln_row_finish(float (&z)[VPL][8], int row, int l
   }
 }
 
-// z = res + dropout(branch); y = LN(z)
-template <int VPL>
-__global__ void __launch_bounds__(256) add_ln_fwd_kernel(const mimose_ops::LnFwdArgs a) {
+// z = res + dropout(branch); y = LN(z). Warp w of block b walks rows
+// b * 8 + w, + gridDim * 8, ...; the next row's branch / residual loads are
+// issued before the current row's reductions (register double-buffering).
+template <int VPL, bool RES>
+__global__ void __launch_bounds__(256, 2) add_ln_fwd_kernel(const mimose_ops::LnFwdArgs a) {
   constexpr int H = VPL * 256;
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= a.rows) return;
-  float z[VPL][8];
+  const int stride = gridDim.x * 8;
+  int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  uint4 br[VPL], rs[VPL], nbr[VPL], nrs[VPL];
+  auto load = [&](int r, uint4 (&b)[VPL], uint4 (&q)[VPL]) {
 #pragma unroll
-  for (int c = 0; c < VPL; ++c) {
-    const int col = 8 * (lane + 32 * c);
-    const uint64_t idx = (uint64_t)row * H + col;
-    float br[8];
-    load8(static_cast<const bf16*>(a.br) + idx, br);
-    const uint32_t m = dropout_mask8(a.br_drop, idx);
-    float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (a.res != nullptr) load8(static_cast<const bf16*>(a.res) + idx, r);
+    for (int c = 0; c < VPL; ++c) {
+      const uint64_t idx = (uint64_t)r * H + 8 * (lane + 32 * c);
+      b[c] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.br) + idx));
+      if constexpr (RES)
+        q[c] = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.res) + idx));
+    }
+  };
+  if (row < a.rows) load(row, br, rs);
+  for (; row < a.rows; row += stride) {
+    if (row + stride < a.rows) load(row + stride, nbr, nrs);
+    float z[VPL][8];
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      z[c][e] = bf16r(r[e] + (((m >> e) & 1u) ? br[e] * a.br_drop.scale : 0.f));
-    if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + idx, z[c]);
+    for (int c = 0; c < VPL; ++c) {
+      const int col = 8 * (lane + 32 * c);
+      const uint64_t idx = (uint64_t)row * H + col;
+      float b[8];
+      unpack8(br[c], b);
+      const uint32_t m = dropout_mask8(a.br_drop, idx);
+      float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      if constexpr (RES) unpack8(rs[c], r);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        z[c][e] = bf16r(r[e] + (((m >> e) & 1u) ? b[e] * a.br_drop.scale : 0.f));
+      if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + idx, z[c]);
+    }
+    ln_row_finish<VPL>(z, row, lane, a);
+#pragma unroll
+    for (int c = 0; c < VPL; ++c) {
+      br[c] = nbr[c];
+      if constexpr (RES) rs[c] = nrs[c];
+    }
   }
-  ln_row_finish<VPL>(z, row, lane, a);
 }
 
 // z = word[tok] + pos[s] + type[tt]; y = dropout(LN(z))
@@ -141,96 +173,153 @@ __global__ void __launch_bounds__(256) embed_ln_fwd_kernel(const mimose_ops::LnF
 //   dz     = rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy_eff * gamma
 //   dbr    = dz * branch-dropout mask * scale
 // per-block partials: [3][H] = {sum dy_eff*xhat, sum dy_eff, sum dbr}
+//
+// Layout: a row is owned by TPR = H / 8 threads (one 16-byte chunk each, so
+// a thread's column accumulators are 3 x 8 floats); a block holds G such row
+// groups, each walking rows r = blockIdx * G + grp + k * gridDim * G. The
+// next row's operands are loaded before the current row is reduced
+// (register double-buffering), so every thread keeps two rows of loads in
+// flight. Row reductions: warp shuffles, then (H > 256) one float2 per warp
+// through a parity-buffered smem slot behind a per-group named barrier.
+// Fixed row -> group assignment + fixed-order combines: deterministic.
 // =====================================================================
-template <int VPL>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const mimose_ops::LnBwdArgs a) {
-  constexpr int H = VPL * 256;
-  extern __shared__ float red[];  // [8 warps][3][H]
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  float acc_g[VPL][8], acc_b[VPL][8], acc_d[VPL][8];
-#pragma unroll
-  for (int c = 0; c < VPL; ++c)
-#pragma unroll
-    for (int e = 0; e < 8; ++e) acc_g[c][e] = acc_b[c][e] = acc_d[c][e] = 0.f;
 
-  for (int row = blockIdx.x * 8 + warp; row < a.rows; row += gridDim.x * 8) {
-    const float2 st = reinterpret_cast<const float2*>(a.stats)[row];
-    float xh[VPL][8], dy[VPL][8], gg[VPL][8];
+template <int WPR>
+struct LnBwdGeo {
+  static constexpr int TPR = WPR * 32;
+  static constexpr int H = TPR * 8;
+  static constexpr int G = WPR == 1 ? 8 : (WPR == 2 ? 4 : 2);  // <= 256 threads, 2 blocks / SM
+  static constexpr int THREADS = G * TPR;
+};
+
+struct LnBwdRaw {
+  uint4 z, dy, dy2, dres;
+};
+
+template <bool DY2, bool DRES>
+__device__ __forceinline__ void ln_bwd_load(const mimose_ops::LnBwdArgs& a, int64_t idx,
+                                            LnBwdRaw& r) {
+  r.z = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.z) + idx));
+  r.dy = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.dy) + idx));
+  if (DY2)
+    r.dy2 = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.dy2) + idx));
+  if (DRES)
+    r.dres = __ldcs(reinterpret_cast<const uint4*>(static_cast<const bf16*>(a.dres) + idx));
+}
+
+template <int WPR, bool DY2, bool DRES>
+__global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, 2)
+    ln_bwd_kernel(const mimose_ops::LnBwdArgs a) {
+  using Geo = LnBwdGeo<WPR>;
+  constexpr int TPR = Geo::TPR, H = Geo::H, G = Geo::G;
+  __shared__ float2 red[2][G][WPR];
+  __shared__ float comb[G][3][H];
+  const int grp = threadIdx.x / TPR;
+  const int t = threadIdx.x % TPR;
+  const int w = t >> 5, lane = t & 31;
+  const int col = 8 * t;
+  float gam[8];
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(a.gamma + col);
+    *reinterpret_cast<float4*>(gam) = g4[0];
+    *reinterpret_cast<float4*>(gam + 4) = g4[1];
+  }
+  float acc_g[8], acc_b[8], acc_d[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc_g[e] = acc_b[e] = acc_d[e] = 0.f;
+
+  const int64_t step = (int64_t)gridDim.x * G;
+  int64_t row = (int64_t)blockIdx.x * G + grp;
+  LnBwdRaw cur{}, nxt{};
+  float2 st_cur = make_float2(0.f, 0.f), st_nxt = st_cur;
+  if (row < a.rows) {
+    ln_bwd_load<DY2, DRES>(a, row * H + col, cur);
+    st_cur = reinterpret_cast<const float2*>(a.stats)[row];
+  }
+  for (int it = 0; row < a.rows; row += step, ++it) {
+    const int64_t idx = row * H + col;
+    const int64_t nrow = row + step;
+    if (nrow < a.rows) {  // prefetch the next row of this group
+      ln_bwd_load<DY2, DRES>(a, nrow * H + col, nxt);
+      st_nxt = reinterpret_cast<const float2*>(a.stats)[nrow];
+    }
+    float zz[8], dy[8];
+    unpack8(cur.z, zz);
+    unpack8(cur.dy, dy);
+    if constexpr (DY2) {
+      float d2[8];
+      unpack8(cur.dy2, d2);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dy[e] += d2[e];
+    }
+    if (a.in_drop.threshold != 0) {
+      const uint32_t m = dropout_mask8(a.in_drop, idx);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dy[e] = ((m >> e) & 1u) ? dy[e] * a.in_drop.scale : 0.f;
+    }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int c = 0; c < VPL; ++c) {
-      const int col = 8 * (lane + 32 * c);
-      const uint64_t idx = (uint64_t)row * H + col;
-      float zz[8], g[8];
-      load8(static_cast<const bf16*>(a.z) + idx, zz);
-      load8(static_cast<const bf16*>(a.dy) + idx, dy[c]);
-      if (a.dy2 != nullptr) {
-        float d2[8];
-        load8(static_cast<const bf16*>(a.dy2) + idx, d2);
+    for (int e = 0; e < 8; ++e) {
+      const float xh = (zz[e] - st_cur.x) * st_cur.y;
+      const float gg = dy[e] * gam[e];
+      s1 += gg;
+      s2 += gg * xh;
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if constexpr (WPR > 1) {
+      if (lane == 0) red[it & 1][grp][w] = make_float2(s1, s2);
+      asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(TPR) : "memory");
+      s1 = 0.f;
+      s2 = 0.f;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dy[c][e] += d2[e];
-      }
-      const uint32_t m = dropout_mask8(a.in_drop, idx);
-      const float4* g4 = reinterpret_cast<const float4*>(a.gamma + col);
-      *reinterpret_cast<float4*>(g) = g4[0];
-      *reinterpret_cast<float4*>(g + 4) = g4[1];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        if (a.in_drop.threshold != 0) dy[c][e] = ((m >> e) & 1u) ? dy[c][e] * a.in_drop.scale : 0.f;
-        xh[c][e] = (zz[e] - st.x) * st.y;
-        gg[c][e] = dy[c][e] * g[e];
-        s1 += gg[c][e];
-        s2 += gg[c][e] * xh[c][e];
+      for (int k = 0; k < WPR; ++k) {
+        const float2 v = red[it & 1][grp][k];
+        s1 += v.x;
+        s2 += v.y;
       }
     }
-    const float mg = warp_sum(s1) * (1.f / H);
-    const float mgx = warp_sum(s2) * (1.f / H);
-#pragma unroll
-    for (int c = 0; c < VPL; ++c) {
-      const int col = 8 * (lane + 32 * c);
-      const uint64_t idx = (uint64_t)row * H + col;
-      float dz[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) dz[e] = st.y * (gg[c][e] - mg - xh[c][e] * mgx);
-      if (a.dres != nullptr) {
-        float rr[8];
-        load8(static_cast<const bf16*>(a.dres) + idx, rr);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) dz[e] += rr[e];
-      }
-      store8(static_cast<bf16*>(a.dz) + idx, dz);
-      const uint32_t m = dropout_mask8(a.br_drop, idx);
-      float db[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e)
-        db[e] = bf16r(((m >> e) & 1u) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
-      if (a.dbr != nullptr) store8(static_cast<bf16*>(a.dbr) + idx, db);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        acc_g[c][e] += dy[c][e] * xh[c][e];
-        acc_b[c][e] += dy[c][e];
-        acc_d[c][e] += db[e];
-      }
-    }
-  }
-  // fixed-order block reduction -> partial[blockIdx.x][3][H]
-#pragma unroll
-  for (int c = 0; c < VPL; ++c) {
-    const int col = 8 * (lane + 32 * c);
+    const float mg = s1 * (1.f / H);
+    const float mgx = s2 * (1.f / H);
+    float dz[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      red[(warp * 3 + 0) * H + col + e] = acc_g[c][e];
-      red[(warp * 3 + 1) * H + col + e] = acc_b[c][e];
-      red[(warp * 3 + 2) * H + col + e] = acc_d[c][e];
+      const float xh = (zz[e] - st_cur.x) * st_cur.y;
+      dz[e] = st_cur.y * (dy[e] * gam[e] - mg - xh * mgx);
+      acc_g[e] += dy[e] * xh;
+      acc_b[e] += dy[e];
     }
+    if constexpr (DRES) {
+      float rr[8];
+      unpack8(cur.dres, rr);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) dz[e] += rr[e];
+    }
+    store8(static_cast<bf16*>(a.dz) + idx, dz);
+    const uint32_t m = dropout_mask8(a.br_drop, idx);
+    float db[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      db[e] = bf16r(((m >> e) & 1u) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
+      acc_d[e] += db[e];
+    }
+    if (a.dbr != nullptr) store8(static_cast<bf16*>(a.dbr) + idx, db);
+    cur = nxt;
+    st_cur = st_nxt;
+  }
+  // fixed-order combine of the G row groups -> partial[blockIdx.x][3][H]
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    comb[grp][0][col + e] = acc_g[e];
+    comb[grp][1][col + e] = acc_b[e];
+    comb[grp][2][col + e] = acc_d[e];
   }
   __syncthreads();
   float* out = a.partial + (size_t)blockIdx.x * 3 * H;
-  for (int i = threadIdx.x; i < 3 * H; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 3 * H; i += Geo::THREADS) {
     float s = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s += red[w * 3 * H + i];
+    for (int g = 0; g < G; ++g) s += (&comb[g][0][0])[i];
     out[i] = s;
   }
 }
@@ -271,7 +360,27 @@ __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restr
   const int col = (blockIdx.x * 32 + tx) * 8;
   float acc[2][8] = {};
   if (col < N) {
-    for (int r = blockIdx.y * 8 + ty; r < rows; r += gridDim.y * 8) {
+    // four rows per iteration, loads issued first (fixed summation order)
+    const int step = gridDim.y * 8;
+    int r = blockIdx.y * 8 + ty;
+    for (; r + 3 * step < rows; r += 4 * step) {
+      uint4 raw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        raw[u] = __ldcs(reinterpret_cast<const uint4*>(x + (int64_t)(r + u * step) * ld + col));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float v[8];
+        unpack8(raw[u], v);
+        const int g = grp != nullptr ? grp[r + u * step] : 0;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc[0][e] += g == 0 ? v[e] : 0.f;
+          acc[1][e] += g == 1 ? v[e] : 0.f;
+        }
+      }
+    }
+    for (; r < rows; r += step) {
       float v[8];
       load8(x + (int64_t)r * ld + col, v);
       const int g = grp != nullptr ? grp[r] : 0;
@@ -319,15 +428,6 @@ __device__ __forceinline__ float group_max(float v) {
   return v;
 }
 
-__device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
-  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 f = __bfloat1622float2(h[i]);
-    v[2 * i] = f.x;
-    v[2 * i + 1] = f.y;
-  }
-}
 
 // All loads of a lane are issued before any arithmetic; exp is evaluated once.
 template <int L, int MAXC>
@@ -914,19 +1014,38 @@ int persistent_blocks() {
 }
 }  // namespace
 
+// blocks of the LayerNorm backward: >= ~4 rows per row group, at most two
+// blocks per SM; a function of `rows` only (deterministic partial layout)
 int ln_bwd_blocks(int rows) {
-  const int want = (rows + 7) / 8;
+  const int want = (rows + 31) / 32;
   const int cap = 2 * persistent_blocks();
-  return want < cap ? want : cap;
+  return want < 1 ? 1 : (want < cap ? want : cap);
 }
 
 cudaError_t add_ln_fwd(const LnFwdArgs& a, int H, cudaStream_t s) {
-  const int g = grid_for(a.rows, 8);
+  const int want = grid_for(a.rows, 8), cap = 2 * persistent_blocks();
+  const int g = want < cap ? want : cap;
+  // bytes/row: branch (+ residual) read, z (if saved) + y written, stats
+  const double rb = 2.0 * H * (1 + (a.res != nullptr) + (a.z != nullptr) + 1) +
+                    (a.stats != nullptr ? 8 : 0);
+  ProfScope prof(a.skip_ln ? "mem_add" : "mem_ln_fwd", 0, rb * a.rows, s);
   switch (H) {
-    case 256: mimose_dev::add_ln_fwd_kernel<1><<<g, 256, 0, s>>>(a); break;
-    case 512: mimose_dev::add_ln_fwd_kernel<2><<<g, 256, 0, s>>>(a); break;
-    case 768: mimose_dev::add_ln_fwd_kernel<3><<<g, 256, 0, s>>>(a); break;
-    case 1024: mimose_dev::add_ln_fwd_kernel<4><<<g, 256, 0, s>>>(a); break;
+    case 256:
+      if (a.res) mimose_dev::add_ln_fwd_kernel<1, true><<<g, 256, 0, s>>>(a);
+      else mimose_dev::add_ln_fwd_kernel<1, false><<<g, 256, 0, s>>>(a);
+      break;
+    case 512:
+      if (a.res) mimose_dev::add_ln_fwd_kernel<2, true><<<g, 256, 0, s>>>(a);
+      else mimose_dev::add_ln_fwd_kernel<2, false><<<g, 256, 0, s>>>(a);
+      break;
+    case 768:
+      if (a.res) mimose_dev::add_ln_fwd_kernel<3, true><<<g, 256, 0, s>>>(a);
+      else mimose_dev::add_ln_fwd_kernel<3, false><<<g, 256, 0, s>>>(a);
+      break;
+    case 1024:
+      if (a.res) mimose_dev::add_ln_fwd_kernel<4, true><<<g, 256, 0, s>>>(a);
+      else mimose_dev::add_ln_fwd_kernel<4, false><<<g, 256, 0, s>>>(a);
+      break;
     default: return cudaErrorInvalidValue;
   }
   count_launch();
@@ -937,6 +1056,8 @@ cudaError_t embed_ln_fwd(const LnFwdArgs& a, int H, const int32_t* tok, const in
                          const void* word, const void* pos, const void* type, int S,
                          cudaStream_t s) {
   const int g = grid_for(a.rows, 8);
+  ProfScope prof("mem_embed_ln_fwd", 0,
+                 (2.0 * H * (3 + (a.z != nullptr)) + 8.0) * a.rows, s);
   auto w = static_cast<const bf16*>(word);
   auto p = static_cast<const bf16*>(pos);
   auto t = static_cast<const bf16*>(type);
@@ -951,23 +1072,25 @@ cudaError_t embed_ln_fwd(const LnFwdArgs& a, int H, const int32_t* tok, const in
   return cudaGetLastError();
 }
 
-template <int VPL>
+template <int WPR>
 static cudaError_t ln_bwd_t(const LnBwdArgs& a, int nblk, cudaStream_t s) {
-  constexpr int H = VPL * 256;
-  const int smem = 8 * 3 * H * (int)sizeof(float);
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(mimose_dev::ln_bwd_kernel<VPL>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    configured = true;
-  }
-  mimose_dev::ln_bwd_kernel<VPL><<<nblk, 256, smem, s>>>(a);
+  constexpr int T = mimose_dev::LnBwdGeo<WPR>::THREADS;
+  const bool d2 = a.dy2 != nullptr, dr = a.dres != nullptr;
+  if (d2 && dr) mimose_dev::ln_bwd_kernel<WPR, true, true><<<nblk, T, 0, s>>>(a);
+  else if (d2) mimose_dev::ln_bwd_kernel<WPR, true, false><<<nblk, T, 0, s>>>(a);
+  else if (dr) mimose_dev::ln_bwd_kernel<WPR, false, true><<<nblk, T, 0, s>>>(a);
+  else mimose_dev::ln_bwd_kernel<WPR, false, false><<<nblk, T, 0, s>>>(a);
   return cudaGetLastError();
 }
 
 cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float* dbias,
                    cudaStream_t s) {
   const int nblk = ln_bwd_blocks(a.rows);
+  // bytes/row: z, dy (+ dy2, + dres) read, stats, dz (+ dbr) written
+  ProfScope prof("mem_ln_bwd", 0,
+                 (2.0 * H * (3 + (a.dy2 != nullptr) + (a.dres != nullptr) + (a.dbr != nullptr)) +
+                  8.0) * a.rows,
+                 s);
   cudaError_t e;
   switch (H) {
     case 256: e = ln_bwd_t<1>(a, nblk, s); break;
@@ -993,6 +1116,7 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
                    float* partial, float* out, cudaStream_t s) {
   if (N % 8 || ld % 8 || G < 1 || G > 2) return cudaErrorInvalidValue;
   const int rb = colsum_row_blocks(rows);
+  ProfScope prof("mem_colsum", 0, 2.0 * rows * N, s);
   dim3 grid((N + 255) / 256, rb);
   mimose_dev::colsum_partial_kernel<<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N, ld,
                                                          groups, G, partial);
@@ -1033,6 +1157,8 @@ static void softmax_bwd_t(const bf16* p, bf16* dp, int64_t rows, int S, int ld,
     default: FN(8); break;                                                         \
   }
 
+// lanes per row: 8 up to 256 columns, 16 up to 512, 32 beyond, so rows up to
+// 1024 need <= 4 chunks per lane (the prefetching variants)
 static bool softmax_geometry(int ld, int* L, int* maxc) {
   const int chunks = ld / 8;
   if (ld <= 512) *L = 8;
@@ -1046,6 +1172,11 @@ static bool softmax_geometry(int ld, int* L, int* maxc) {
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, cudaStream_t s, bool causal) {
   const int cz = causal ? 1 : 0;
+  // scores read (live region), P and dropped P written over the row pitch
+  ProfScope prof("mem_softmax_fwd", 0,
+                 (double)rows * (2.0 * (causal ? 0.5 * (S + 1) : S) +
+                                 2.0 * ld * (1 + (Pd != nullptr))),
+                 s);
   auto in = static_cast<const bf16*>(scores);
   auto p = static_cast<bf16*>(P);
   auto pd = static_cast<bf16*>(Pd);
@@ -1066,6 +1197,7 @@ cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int
 
 cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
+  ProfScope prof("mem_softmax_bwd", 0, (double)rows * 6.0 * S, s);  // P, dPd read; dS written
   auto p = static_cast<const bf16*>(P);
   auto dp = static_cast<bf16*>(dPd);
   int L = 0, maxc = 0;
@@ -1114,6 +1246,7 @@ int sumsq_blocks() { return 2 * persistent_blocks(); }
 
 cudaError_t grad_norm2(const float* g, int64_t n, float* partial, float* out, cudaStream_t s) {
   const int nb = sumsq_blocks();
+  ProfScope prof("mem_gradnorm", 0, 4.0 * n, s);
   mimose_dev::sumsq_partial_kernel<<<nb, 256, 0, s>>>(g, n, partial);
   count_launch();
   mimose_dev::sum_partials_kernel<<<1, 32, 0, s>>>(partial, nb, out);
@@ -1124,6 +1257,7 @@ cudaError_t grad_norm2(const float* g, int64_t n, float* partial, float* out, cu
 cudaError_t adamw(float* p, float* m, float* v, const float* g, void* p16, int64_t n,
                   const uint8_t* decay_chunk, const float* norm2, const AdamWArgs& a,
                   cudaStream_t s) {
+  ProfScope prof("mem_adamw", 0, 30.0 * n, s);  // p, m, v, g read; p, m, v, p16 written
   mimose_dev::adamw_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
       p, m, v, g, static_cast<bf16*>(p16), n, decay_chunk, norm2, a);
   count_launch();
@@ -1148,6 +1282,7 @@ cudaError_t f32_to_bf16(const float* in, void* out, int64_t n, cudaStream_t s) {
 cudaError_t dropout_apply(const void* in, void* out, int64_t n, const DropoutCfg& d,
                           cudaStream_t s) {
   if (n % 8) return cudaErrorInvalidValue;
+  ProfScope prof("mem_dropout", 0, 4.0 * n, s);
   mimose_dev::dropout_apply_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
       static_cast<const bf16*>(in), static_cast<bf16*>(out), n / 8, d);
   count_launch();
@@ -1157,6 +1292,7 @@ cudaError_t dropout_apply(const void* in, void* out, int64_t n, const DropoutCfg
 cudaError_t dgelu_apply(const void* dg, const void* u, void* out, int64_t n, bool tanh_form,
                         cudaStream_t s) {
   if (n % 8) return cudaErrorInvalidValue;
+  ProfScope prof("mem_dgelu", 0, 6.0 * n, s);
   mimose_dev::dgelu_apply_kernel<<<4 * persistent_blocks(), 256, 0, s>>>(
       static_cast<const bf16*>(dg), static_cast<const bf16*>(u), static_cast<bf16*>(out), n / 8,
       tanh_form ? 1 : 0);
@@ -1217,6 +1353,7 @@ cudaError_t qa_head_bwd(const void* x, const float* dlogits, int T, int H, const
 cudaError_t ce_rows(void* logits, int rows, int V, int ld, const int32_t* labels,
                     float grad_scale, float* loss_rows, cudaStream_t s) {
   if (ld % 8) return cudaErrorInvalidValue;
+  ProfScope prof("mem_ce_rows", 0, 4.0 * rows * (double)V, s);
   mimose_dev::ce_rows_kernel<<<rows, 512, 0, s>>>(static_cast<bf16*>(logits), V, ld, labels,
                                                   grad_scale, loss_rows);
   count_launch();

@@ -38,6 +38,7 @@ struct GemmCall {
   int64_t ldo = 0, obs1 = 0, obs2 = 0;
   float alpha = 1.f, beta = 0.f;
   int force_bn = 0;  // 0 = heuristic; 64/128/256 for tests
+  int force_ew = 0;  // 0 = heuristic; 8 / 16 epilogue warps for tests
   bool direct_store = false;  // tests: force the per-thread store epilogue
   // deterministic split-K for fp32 (weight-gradient) outputs: partials go to
   // `workspace` ([splits][M][N] fp32) and are summed in a fixed order.

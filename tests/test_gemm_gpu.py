@@ -37,12 +37,13 @@ def _rand(*shape, dev="cuda"):
     return torch.randn(*shape, device=dev).to(torch.bfloat16)
 
 
+@pytest.mark.parametrize("ew", [8, 16])
 @pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("bn", [64, 128, 256])
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 256, 128), (200, 72, 80), (1000, 770, 768), (128, 2304, 64)])
-def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct):
+def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct, ew):
     ops = _ops()
     torch.manual_seed(0)
     M, N, K = shape
@@ -53,7 +54,8 @@ def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct):
     if (a_arg.stride(0) * 2) % 16 or (b_arg.stride(0) * 2) % 16:
         pytest.skip("TMA needs 16-byte row pitch")
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
-    ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn, direct_store=direct)
+    ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn, direct_store=direct,
+             force_ew=ew)
     torch.cuda.synchronize()
     _check_bf16(out, A.float() @ B.float().t())
 
@@ -74,8 +76,9 @@ def test_gemm_f32_beta(cuda_device, bn, beta):
     _check_f32(out, ref, K)
 
 
+@pytest.mark.parametrize("ew", [8, 16])
 @pytest.mark.parametrize("M", [517, 1024])
-def test_gemm_bias_gelu_and_dgelu(cuda_device, M):
+def test_gemm_bias_gelu_and_dgelu(cuda_device, M, ew):
     ops = _ops()
     torch.manual_seed(2)
     N, K = 3072, 768
@@ -84,7 +87,7 @@ def test_gemm_bias_gelu_and_dgelu(cuda_device, M):
     bias = torch.randn(N, device="cuda")
     u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     g = torch.empty_like(u)
-    ops.gemm(X, W, u, epi=ops.EPI_BIAS_GELU, out2=g, bias=bias)
+    ops.gemm(X, W, u, epi=ops.EPI_BIAS_GELU, out2=g, bias=bias, force_ew=ew)
     torch.cuda.synchronize()
     u_ref = X.float() @ W.float().t() + bias
     _check_bf16(u, u_ref)
@@ -95,7 +98,7 @@ def test_gemm_bias_gelu_and_dgelu(cuda_device, M):
     dY = _rand(M, K)
     du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     W2 = _rand(K, N) * 0.05  # FFN2 weight [H, 4H]: dgrad B operand is MN-major view [K=H, N=4H]
-    ops.gemm(dY, W2, du, b_mn=True, epi=ops.EPI_DGELU, aux=u)
+    ops.gemm(dY, W2, du, b_mn=True, epi=ops.EPI_DGELU, aux=u, force_ew=ew)
     torch.cuda.synchronize()
     uf = u.float().requires_grad_(True)
     torch.nn.functional.gelu(uf).backward(torch.ones_like(uf))

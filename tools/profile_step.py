@@ -11,6 +11,36 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def summarize(text, top=30):
+    """Per-(class, shape) aggregate of the profiler CSV: ms, share, TFLOP/s
+    (GEMMs) or algorithmic GB/s (memory-bound stages)."""
+    import csv
+    import io
+    rows = list(csv.DictReader(io.StringIO(text)))
+    agg = {}
+    for r in rows:
+        key = (r["class"], r["desc"])
+        a = agg.setdefault(key, [0, 0.0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += float(r["ms"])
+        a[2] += float(r["flops"])
+        a[3] += float(r["bytes"])
+    tot = sum(v[1] for v in agg.values())
+    out = [f"instrumented total {tot:.3f} ms over {len(rows)} launches"]
+    cls = {}
+    for (c, _), (n, ms, fl, by) in agg.items():
+        x = cls.setdefault(c, [0, 0.0, 0.0, 0.0])
+        x[0] += n; x[1] += ms; x[2] += fl; x[3] += by
+    for c, (n, ms, fl, by) in sorted(cls.items(), key=lambda kv: -kv[1][1]):
+        out.append(f"{ms:8.3f} ms {100 * ms / tot:5.1f}%  x{n:4d}  {c:18s} "
+                   f"{fl / (ms * 1e-3) / 1e12:7.1f} TFLOP/s  {by / (ms * 1e-3) / 1e9:7.0f} GB/s")
+    out.append("-- per shape --")
+    for (c, d), (n, ms, fl, by) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+        out.append(f"{ms:8.3f} ms  x{n:3d}  {c:18s} {d:48s} "
+                   f"{fl / (ms * 1e-3) / 1e12:7.1f} TFLOP/s  {by / (ms * 1e-3) / 1e9:7.0f} GB/s")
+    return "\n".join(out)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--preset", default="bert-base-mc")
@@ -24,31 +54,39 @@ def main():
     import numpy as np
     import torch
     from paper_2209_02478_b200 import _lib
-    from paper_2209_02478_b200.trainer import PRESETS, DeviceBatch, Trainer, synthetic_batch
+    from paper_2209_02478_b200.trainer import PRESETS, DeviceBatch, Trainer, synthetic_task_batch
     m, t = PRESETS[args.preset]
     GiB = 1 << 30
     rng = np.random.default_rng(0)
     probe = Trainer(m, dataclasses.replace(t, planner="none"), 60 * GiB)
-    probe.step(*synthetic_batch(rng, t.batch, t.seq_max, m.vocab, m.num_choices), optimizer=False)
+    probe.step(*synthetic_task_batch(rng, m, t.batch, t.seq_max), optimizer=False)
     peak = probe.rows[-1]["peak_reserved"]
     probe.close()
     budget = int(args.budget_frac * peak) if args.planner == "mimose" else int(1.2 * peak)
     tr = Trainer(m, dataclasses.replace(t, planner=args.planner, attn_fused=args.attn_fused),
                  budget)
-    for s in [64, 512, 200, 350, 128, 480, 300, 96, 420, 256, 160, 384]:
-        tr.step(*synthetic_batch(rng, t.batch, s, m.vocab, m.num_choices))
-    db = DeviceBatch.from_host(*synthetic_batch(rng, t.batch, args.seq, m.vocab, m.num_choices),
-                               m.vocab)
+    lo, hi = t.seq_min, t.seq_max
+    for f in [0.0, 1.0, 0.3, 0.6, 0.15, 0.9, 0.5, 0.05, 0.8, 0.4, 0.2, 0.7]:
+        tr.step(*synthetic_task_batch(rng, m, t.batch, int(lo + f * (hi - lo)) // 8 * 8 or 8))
+    db = DeviceBatch.from_host(*synthetic_task_batch(rng, m, t.batch, args.seq), m.vocab)
     tr.step_device(db)  # warm
     torch.cuda.synchronize()
     lib = _lib.cuda_lib()
     if args.gemm_csv:
-        lib.mimose_gemm_profile_enable(1)
+        lib.mimose_profile_enable(1)
     torch.cuda.nvtx.range_push("timed_step")
     r = tr.step_device(db)
     torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     print({k: r[k] for k in ("seq", "phase_name", "plan_size", "peak_reserved")})
+    if args.gemm_csv:
+        p = C.c_void_p()
+        lib.mimose_profile_csv(C.byref(p))
+        text = _lib.take_string(lib, p)
+        lib.mimose_profile_enable(0)
+        with open(args.gemm_csv, "w") as f:
+            f.write(text)
+        print(summarize(text))
     if args.time_steps:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -58,27 +96,6 @@ def main():
         torch.cuda.synchronize()
         print(f"seq {args.seq} attn_fused={args.attn_fused}: "
               f"{e0.elapsed_time(e1) / args.time_steps:.3f} ms/step (plan_size {r['plan_size']})")
-    if args.gemm_csv:
-        p = C.c_void_p()
-        lib.mimose_gemm_profile_csv(C.byref(p))
-        text = _lib.take_string(lib, p)
-        lib.mimose_gemm_profile_enable(0)
-        with open(args.gemm_csv, "w") as f:
-            f.write(text)
-        rows = [l.split(",") for l in text.strip().splitlines()[1:]]
-        agg = {}
-        for row in rows:
-            key = tuple(row[:9])
-            a = agg.setdefault(key, [0, 0.0])
-            a[0] += 1
-            a[1] += float(row[9])
-        tot = sum(v[1] for v in agg.values())
-        print(f"GEMM total {tot:.3f} ms over {len(rows)} launches")
-        for key, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1])[:25]:
-            M, N, K, b = map(int, key[:4])
-            tf = 2.0 * M * N * K * b * n / (ms * 1e-3) / 1e12
-            print(f"{ms:8.3f} ms  x{n:3d}  M={M:6d} N={N:5d} K={K:6d} batch={b:4d} bn={key[4]} "
-                  f"amn={key[5]} bmn={key[6]} epi={key[7]} grid={key[8]}  {tf:7.1f} TFLOP/s")
     tr.close()
 
 
