@@ -5,6 +5,7 @@
 #include "attn_sm100.cuh"
 #include "ops.hpp"
 #include "ops_attn.hpp"
+#include "prof.hpp"
 
 namespace mimose_ops {
 
@@ -34,7 +35,7 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   }
   const int tiles = ((p.S + 127) / 128) * p.nh * p.B;
   const int grid = tiles < attn_sm_count() ? tiles : attn_sm_count();
-  kern<<<grid, 320, Cfg::kSmemBytes, s>>>(a, b, o1, o2, p);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(a, b, o1, o2, p);
   count_launch();
   return cudaGetLastError();
 }
@@ -47,13 +48,17 @@ cudaError_t attn_scores_fwd(const MatView& q, const MatView& k, void* P, void* P
                             int nh, int B, float alpha, const mimose_dev::DropoutCfg& drop,
                             cudaStream_t s) {
   if (!attn_fused_supported(S)) return cudaErrorInvalidValue;
+  const double nz = (double)nh * B;
+  // Q, K read; P (+ Pd) written
+  ProfScope prof("attn_fused_fwd", 2.0 * S * (double)S * 64 * nz,
+                 nz * (4.0 * S * 64 + 2.0 * S * (double)ld * (Pd != nullptr ? 2 : 1)), s);
   CUtensorMap ta, tb, t1, t2;
   if (!make_operand_map(&ta, q, nh, B, 128) || !make_operand_map(&tb, k, nh, B, 256))
     return cudaErrorInvalidValue;
-  if (!make_output_map(&t1, P, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B))
+  if (!make_output_map(&t1, P, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B, 32, true))
     return cudaErrorInvalidValue;
   if (Pd != nullptr &&
-      !make_output_map(&t2, Pd, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B))
+      !make_output_map(&t2, Pd, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B, 32, true))
     return cudaErrorInvalidValue;
   if (Pd == nullptr) t2 = t1;
   mimose_dev::AttnParams p{};
@@ -68,10 +73,14 @@ cudaError_t attn_scores_bwd(const MatView& dout, const MatView& v, const void* P
                             int ld, int nh, int B, float ds_scale,
                             const mimose_dev::DropoutCfg& drop, cudaStream_t s) {
   if (!attn_fused_supported(S)) return cudaErrorInvalidValue;
+  const double nz = (double)nh * B;
+  // dO, V, P read; dS written
+  ProfScope prof("attn_fused_bwd", 2.0 * S * (double)S * 64 * nz,
+                 nz * (4.0 * S * 64 + 4.0 * S * (double)S), s);
   CUtensorMap ta, tb, t1;
   if (!make_operand_map(&ta, dout, nh, B, 128) || !make_operand_map(&tb, v, nh, B, 256))
     return cudaErrorInvalidValue;
-  if (!make_output_map(&t1, dS, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B))
+  if (!make_output_map(&t1, dS, S, S, ld, (int64_t)S * ld, (int64_t)nh * S * ld, nh, B, 32, true))
     return cudaErrorInvalidValue;
   mimose_dev::AttnParams p{};
   p.S = S; p.ld = ld; p.nh = nh; p.B = B;

@@ -7,10 +7,13 @@
 //   backward: dPd = dO V^T       ->  dS = P * (dP - rowsum(dP * P)) * scale,
 //                                    dP = dPd * mask / (1 - p)           (dS stored)
 //
-// Row statistics: the 8 epilogue warps split each row into two column
-// halves (TMEM lane quarter x half); partial max / sum / dot are exchanged
-// through shared memory with a named barrier. Output chunks go through
-// 128B-swizzled staging buffers and TMA bulk stores, like the GEMM epilogue.
+// Row statistics: 16 epilogue warps split each row into four column parts
+// (TMEM lane quarter x part); partial max / sum / dot are exchanged through
+// shared memory behind a named barrier. Forward: pass 1 row max, pass 2
+// exp + row sum with the exponentials written back into TMEM (tcgen05.st),
+// pass 3 normalise + Philox dropout, so every score costs one ex2. Backward:
+// the keep masks of pass 1 stay in registers for pass 2. Output chunks (32
+// columns) go through 64B-swizzled staging buffers and TMA bulk stores.
 // The materialised P / Pd / dS keep the reference's quadratic activation term
 // (reference proj/models/bert12.model c2) exactly as the unfused path does.
 #pragma once
@@ -37,13 +40,17 @@ struct AttnParams {
 
 template <int NC>
 struct AttnCfg {
+  static constexpr int kEW = 16;                 // epilogue warps
+  static constexpr int kThreads = 64 + 32 * kEW;
+  static constexpr int kQ = NC / 4;              // accumulator columns per epilogue warp
   static constexpr int kABytes = 128 * 64 * 2;
   static constexpr int kBBytes = NC * 64 * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kStages = NC == 512 ? 1 : 2;
   static constexpr int kAcc = NC == 512 ? 1 : 2;  // TMEM accumulators (512 columns total)
-  static constexpr int kStagingBytes = 8 * 2 * 4096;
-  static constexpr int kRedBytes = 2 * 2 * 2 * 128 * 4;  // [tile parity][max|sum][half][row]
+  static constexpr int kBufBytes = 32 * 64;       // 32 rows x 64 B (32 bf16 columns)
+  static constexpr int kStagingBytes = kEW * 2 * kBufBytes;
+  static constexpr int kRedBytes = 2 * 2 * 4 * 128 * 4;  // [tile parity][max|sum][part][row]
   static constexpr int kSmemBytes =
       kStages * kStageBytes + kStagingBytes + kRedBytes + 1024 + 256;
 };
@@ -60,18 +67,28 @@ __device__ __forceinline__ uint32_t pack_bf16x2_(float a, float b) {
 }
 
 __device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, 256;" ::: "memory");
+  asm volatile("bar.sync 1, 512;" ::: "memory");
+}
+
+__device__ __forceinline__ void unpack_bf16x8(const uint4& raw, float (&v)[8]) {
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h2[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
 }
 
 template <int NC, bool BWD>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
     attn_scores_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmB,
                        const __grid_constant__ CUtensorMap tmO1,
                        const __grid_constant__ CUtensorMap tmO2, const AttnParams p) {
   using Cfg = AttnCfg<NC>;
   constexpr int NS = Cfg::kStages;
-  constexpr int HALF = NC / 2;
+  constexpr int Q = Cfg::kQ;
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -79,7 +96,7 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + NS * Cfg::kABytes;
   uint8_t* sD = smem + NS * Cfg::kStageBytes;
-  float* red = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [2][2][2][128]
+  float* red = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [2][2][4][128]
   uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes + Cfg::kRedBytes);
   uint64_t* empty = full + NS;
   uint64_t* tfull = empty + NS;
@@ -101,7 +118,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], Cfg::kEW);
     }
     fence_barrier_init();
   }
@@ -163,16 +180,18 @@ __global__ void __launch_bounds__(320, 1)
   } else {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 2;
-    const int quarter = warp & 3;
-    const int half = ew >> 2;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int part = ew >> 2;      // column part 0..3
     const int r_local = quarter * 32 + static_cast<int>(lane);
-    uint8_t* wbuf = sD + ew * (2 * 4096);
+    uint8_t* wbuf = sD + ew * (2 * Cfg::kBufBytes);
+    const uint32_t rbase = smem_u32(wbuf) + lane * 64;
+    const uint32_t sw = (lane >> 1) & 3;  // SWIZZLE_64B: 16 B chunk j of row r at j ^ ((r >> 1) & 3)
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       // row-statistic exchange buffers, double-buffered by tile parity so a
-      // warp running ahead cannot overwrite what its partner has yet to read
-      float* red_a = red + (it & 1) * 512;  // [2][128] max / dot
-      float* red_b = red_a + 256;           // [2][128] sum
+      // warp running ahead cannot overwrite what another has yet to read
+      float* red_a = red + (it & 1) * 1024;  // [4][128] max / dot
+      float* red_b = red_a + 512;            // [4][128] sum
       const int z = tile / tiles_m;
       const int m0 = (tile % tiles_m) * 128;
       const int b1 = z % p.nh, b2 = z / p.nh;
@@ -183,153 +202,145 @@ __global__ void __launch_bounds__(320, 1)
       const int64_t grow = ((int64_t)z * p.S + (row_ok ? i : 0));  // row of the [B*nh*S][ld] view
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NC + half * HALF;
-      const int c0 = half * HALF;  // first column of this warp's half
+      const int c0 = part * Q;  // first column of this warp's part
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NC + c0;
 
       if constexpr (!BWD) {
-        // ---- pass 1: row max (log2 domain)
+        // ---- pass 1: row max of the raw scores (alpha > 0 commutes with max)
         const float sc = p.alpha * kLog2e;
         float mx = -INFINITY;
 #pragma unroll 1
-        for (int c = 0; c < HALF; c += 32) {
-          if (c0 + c >= p.S) break;
-          uint32_t r[32];
-          tmem_ld32_nowait(t_row + c, r);
-          tmem_wait_ld();
+        for (int c = 0; c < Q; c += 32) {
+          if (c0 + c < p.S) {
+            uint32_t r[32];
+            tmem_ld32_nowait(t_row + c, r);
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c0 + c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]) * sc);
+            for (int e = 0; e < 32; ++e)
+              if (c0 + c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]));
+          }
         }
-        red_a[half * 128 + r_local] = mx;
+        red_a[part * 128 + r_local] = mx * sc;
         epi_bar();
-        mx = fmaxf(red_a[r_local], red_a[128 + r_local]);
-        // ---- pass 2: row sum of exp
+        mx = fmaxf(fmaxf(red_a[r_local], red_a[128 + r_local]),
+                   fmaxf(red_a[256 + r_local], red_a[384 + r_local]));
+        // ---- pass 2: e = 2^(s * sc - max) written back to TMEM; row sum
         float sum = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < HALF; c += 32) {
-          if (c0 + c >= p.S) break;
-          uint32_t r[32];
-          tmem_ld32_nowait(t_row + c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (c0 + c + e < p.S) sum += ex2f(__uint_as_float(r[e]) * sc - mx);
-        }
-        red_b[half * 128 + r_local] = sum;
-        epi_bar();
-        const float inv = 1.f / (red_b[r_local] + red_b[128 + r_local]);
-        // ---- pass 3: normalise, dropout, stage, TMA store (64-column chunks)
-#pragma unroll 1
-        for (int c = 0; c < HALF; c += 64) {
-          if (c0 + c >= p.S) break;
-          if (lane == 0) bulk_wait_read<0>();
-          __syncwarp();
-          float v[64];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+        for (int c = 0; c < Q; c += 32) {
+          if (c0 + c < p.S) {
             uint32_t r[32];
-            tmem_ld32_nowait(t_row + c + 32 * h, r);
+            tmem_ld32_nowait(t_row + c, r);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 32; ++e) {
-              const int col = c0 + c + 32 * h + e;
-              v[32 * h + e] = col < p.S ? ex2f(__uint_as_float(r[e]) * sc - mx) * inv : 0.f;
+              const float x = c0 + c + e < p.S ? ex2f(__uint_as_float(r[e]) * sc - mx) : 0.f;
+              sum += x;
+              r[e] = __float_as_uint(x);
             }
+            tmem_st32(t_row + c, r);
           }
-          const uint32_t rbase = smem_u32(wbuf) + lane * 128;
+        }
+        tmem_wait_st();
+        red_b[part * 128 + r_local] = sum;
+        epi_bar();
+        const float inv = 1.f / ((red_b[r_local] + red_b[128 + r_local]) +
+                                 (red_b[256 + r_local] + red_b[384 + r_local]));
+        // ---- pass 3: normalise, dropout, stage, TMA store (32-column chunks)
+#pragma unroll 1
+        for (int c = 0; c < Q; c += 32) {
+          if (c0 + c >= p.S) break;
+          if (lane == 0) bulk_wait_read<0>();
+          __syncwarp();
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
+          for (int j = 0; j < 4; ++j) {
             float pv[8], dv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pv[e] = bf16r(v[8 * j + e]);
-            const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * j)
-                                      : 0xFFu;
+            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * j + e]) * inv);
+            const uint32_t m =
+                row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * j) : 0xFFu;
 #pragma unroll
             for (int e = 0; e < 8; ++e) dv[e] = ((m >> e) & 1u) ? pv[e] * p.drop.scale : 0.f;
-            const uint32_t addr = rbase + ((j ^ (lane & 7)) << 4);
+            const uint32_t addr = rbase + ((j ^ sw) << 4);
             st_shared_v4(addr, pack_bf16x2_(pv[0], pv[1]), pack_bf16x2_(pv[2], pv[3]),
                          pack_bf16x2_(pv[4], pv[5]), pack_bf16x2_(pv[6], pv[7]));
             if (p.store_pd)
-              st_shared_v4(addr + 4096, pack_bf16x2_(dv[0], dv[1]), pack_bf16x2_(dv[2], dv[3]),
-                           pack_bf16x2_(dv[4], dv[5]), pack_bf16x2_(dv[6], dv[7]));
+              st_shared_v4(addr + Cfg::kBufBytes, pack_bf16x2_(dv[0], dv[1]),
+                           pack_bf16x2_(dv[2], dv[3]), pack_bf16x2_(dv[4], dv[5]),
+                           pack_bf16x2_(dv[6], dv[7]));
           }
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
             tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
-            if (p.store_pd) tma_store_4d(&tmO2, wbuf + 4096, c0 + c, m0 + quarter * 32, b1, b2);
+            if (p.store_pd)
+              tma_store_4d(&tmO2, wbuf + Cfg::kBufBytes, c0 + c, m0 + quarter * 32, b1, b2);
             bulk_commit();
           }
         }
       } else {
         // ---- backward: pass 1 dot = sum_j dP_j P_j (dP = dPd * mask * scale)
         const __nv_bfloat16* prow = p.P + grow * p.ld;
+        uint32_t mk[Q / 8];
         float dot = 0.f;
-#pragma unroll 1
-        for (int c = 0; c < HALF; c += 32) {
-          if (c0 + c >= p.S) break;
-          uint4 pr[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            pr[q] = (row_ok && c0 + c + 8 * q < p.S)
-                        ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
-                        : make_uint4(0, 0, 0, 0);
-          uint32_t r[32];
-          tmem_ld32_nowait(t_row + c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * q)
-                                      : 0u;
-            float pf[8];
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pr[q]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h2[e]);
-              pf[2 * e] = f.x;
-              pf[2 * e + 1] = f.y;
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int col = c0 + c + 8 * q + e;
-              if (col < p.S && ((m >> e) & 1u))
-                dot += __uint_as_float(r[8 * q + e]) * p.drop.scale * pf[e];
-            }
-          }
-        }
-        red_a[half * 128 + r_local] = dot;
-        epi_bar();
-        dot = red_a[r_local] + red_a[128 + r_local];
-        // ---- pass 2: dS = P * (dP - dot) * scale -> stage -> TMA store
-#pragma unroll 1
-        for (int c = 0; c < HALF; c += 64) {
-          if (c0 + c >= p.S) break;
-          if (lane == 0) bulk_wait_read<0>();
-          __syncwarp();
-          const uint32_t rbase = smem_u32(wbuf) + lane * 128;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+        for (int c = 0; c < Q; c += 32) {
+          if (c0 + c < p.S) {
             uint4 pr[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              pr[q] = (row_ok && c0 + c + 32 * h + 8 * q < p.S)
-                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 32 * h + 8 * q)
+              pr[q] = (row_ok && c0 + c + 8 * q < p.S)
+                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
                           : make_uint4(0, 0, 0, 0);
             uint32_t r[32];
-            tmem_ld32_nowait(t_row + c + 32 * h, r);
+            tmem_ld32_nowait(t_row + c, r);
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int colq = c0 + c + 32 * h + 8 * q;
-              const uint32_t m = row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + colq) : 0u;
-              float pf[8], ds[8];
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&pr[q]);
+              const uint32_t m =
+                  row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * q) : 0u;
+              mk[c / 8 + q] = m;
+              float pf[8];
+              unpack_bf16x8(pr[q], pf);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                pf[2 * e] = f.x;
-                pf[2 * e + 1] = f.y;
+              for (int e = 0; e < 8; ++e) {
+                const int col = c0 + c + 8 * q + e;
+                if (col < p.S && ((m >> e) & 1u))
+                  dot += __uint_as_float(r[8 * q + e]) * p.drop.scale * pf[e];
               }
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) mk[c / 8 + q] = 0u;
+          }
+        }
+        red_a[part * 128 + r_local] = dot;
+        epi_bar();
+        dot = (red_a[r_local] + red_a[128 + r_local]) + (red_a[256 + r_local] + red_a[384 + r_local]);
+        // ---- pass 2: dS = P * (dP - dot) * scale -> stage -> TMA store
+#pragma unroll
+        for (int c = 0; c < Q; c += 32) {
+          if (c0 + c < p.S) {
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+            uint4 pr[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              pr[q] = (row_ok && c0 + c + 8 * q < p.S)
+                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
+                          : make_uint4(0, 0, 0, 0);
+            uint32_t r[32];
+            tmem_ld32_nowait(t_row + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int colq = c0 + c + 8 * q;
+              const uint32_t m = mk[c / 8 + q];
+              float pf[8], ds[8];
+              unpack_bf16x8(pr[q], pf);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const bool in = colq + e < p.S;
@@ -337,17 +348,16 @@ __global__ void __launch_bounds__(320, 1)
                                                         : 0.f;
                 ds[e] = in ? pf[e] * (g - dot) * p.ds_scale : 0.f;
               }
-              const int j = 4 * h + q;  // 16-byte chunk index inside the 128-byte row
-              st_shared_v4(rbase + ((j ^ (lane & 7)) << 4), pack_bf16x2_(ds[0], ds[1]),
+              st_shared_v4(rbase + ((q ^ sw) << 4), pack_bf16x2_(ds[0], ds[1]),
                            pack_bf16x2_(ds[2], ds[3]), pack_bf16x2_(ds[4], ds[5]),
                            pack_bf16x2_(ds[6], ds[7]));
             }
-          }
-          fence_async_shared();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
-            bulk_commit();
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
+              bulk_commit();
+            }
           }
         }
       }

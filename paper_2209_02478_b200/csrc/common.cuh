@@ -53,6 +53,67 @@ __device__ __forceinline__ uint32_t dropout_mask8(const DropoutCfg& d, uint64_t 
   return m;
 }
 
+// N independent Philox4x32-10 blocks (same key, counters (stream, group[i]))
+// computed round-major: the key schedule is evaluated once per round for all
+// N blocks, and the N multiply chains interleave. Bit-identical to Philox.
+template <int N>
+__device__ __forceinline__ void philox_n(uint64_t seed, uint64_t stream, const uint64_t (&group)[N],
+                                         uint32_t (&out)[N][4]) {
+  uint32_t c0[N], c1[N], c2[N], c3[N];
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    c0[n] = (uint32_t)group[n];
+    c1[n] = (uint32_t)(group[n] >> 32);
+    c2[n] = (uint32_t)stream;
+    c3[n] = (uint32_t)(stream >> 32);
+  }
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+      const uint64_t p0 = (uint64_t)0xD2511F53u * c0[n];
+      const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2[n];
+      c0[n] = (uint32_t)(p1 >> 32) ^ c1[n] ^ k0;
+      c1[n] = (uint32_t)p1;
+      c2[n] = (uint32_t)(p0 >> 32) ^ c3[n] ^ k1;
+      c3[n] = (uint32_t)p0;
+    }
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+#pragma unroll
+  for (int n = 0; n < N; ++n) {
+    out[n][0] = c0[n];
+    out[n][1] = c1[n];
+    out[n][2] = c2[n];
+    out[n][3] = c3[n];
+  }
+}
+
+// keep predicate from a raw Philox block (see philox_keep)
+__device__ __forceinline__ bool philox_keep_w(const uint32_t (&r)[4], int e, uint32_t thr_hi) {
+  const uint32_t w = r[e >> 1];
+  return ((e & 1) ? w : (w << 16)) >= thr_hi;
+}
+
+// 2^x for x <= 0 (softmax exponentials): ex2.approx.ftz, no range fix-up
+__device__ __forceinline__ float exp2_neg(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// keep predicate of element e (0..7) of a Philox group without building the
+// 8-bit mask: the 16-bit half (e & 1) of word (e >> 1) is >= threshold
+// <=> (word << 16) >= thr_hi (even e) / word >= thr_hi (odd e), with
+// thr_hi = threshold << 16 (threshold 0 keeps everything). Same decision as
+// dropout_mask8 bit e.
+__device__ __forceinline__ bool philox_keep(const Philox& a, int e, uint32_t thr_hi) {
+  const uint32_t w = a.r[e >> 1];
+  return ((e & 1) ? w : (w << 16)) >= thr_hi;
+}
+
 // keep decision for a single element (head kernel)
 __device__ __forceinline__ bool dropout_keep1(const DropoutCfg& d, uint64_t idx) {
   if (d.threshold == 0) return true;

@@ -248,9 +248,9 @@ bool make_operand_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint
 }
 
 bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                     int64_t bs1, int64_t bs2, int nb1, int nb2) {
+                     int64_t bs1, int64_t bs2, int nb1, int nb2, uint32_t box_cols, bool sw64) {
   if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * 2) % 16) return false;
-  return make_map_t(map, ptr, rows, cols, ld, bs1, bs2, nb1, nb2, 64, 32, 2);
+  return make_map_t(map, ptr, rows, cols, ld, bs1, bs2, nb1, nb2, box_cols, 32, 2, sw64);
 }
 
 int pick_split_k(int M, int N, int K, int bn) {

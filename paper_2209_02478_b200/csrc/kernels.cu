@@ -116,18 +116,28 @@ __global__ void __launch_bounds__(256, 2) add_ln_fwd_kernel(const mimose_ops::Ln
   for (; row < a.rows; row += stride) {
     if (row + stride < a.rows) load(row + stride, nbr, nrs);
     float z[VPL][8];
+    uint32_t rnd[VPL][4];
+    if (a.br_drop.threshold != 0) {
+      uint64_t grp[VPL];
+#pragma unroll
+      for (int c = 0; c < VPL; ++c) grp[c] = ((uint64_t)row * H + 8 * (lane + 32 * c)) >> 3;
+      philox_n<VPL>(a.br_drop.seed, a.br_drop.stream, grp, rnd);
+    } else {
+#pragma unroll
+      for (int c = 0; c < VPL; ++c) rnd[c][0] = rnd[c][1] = rnd[c][2] = rnd[c][3] = 0xFFFFFFFFu;
+    }
+    const uint32_t thr_hi = a.br_drop.threshold << 16;
 #pragma unroll
     for (int c = 0; c < VPL; ++c) {
       const int col = 8 * (lane + 32 * c);
       const uint64_t idx = (uint64_t)row * H + col;
       float b[8];
       unpack8(br[c], b);
-      const uint32_t m = dropout_mask8(a.br_drop, idx);
       float r[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       if constexpr (RES) unpack8(rs[c], r);
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        z[c][e] = bf16r(r[e] + (((m >> e) & 1u) ? b[e] * a.br_drop.scale : 0.f));
+        z[c][e] = bf16r(r[e] + (philox_keep_w(rnd[c], e, thr_hi) ? b[e] * a.br_drop.scale : 0.f));
       if (a.z != nullptr) store8(static_cast<bf16*>(a.z) + idx, z[c]);
     }
     ln_row_finish<VPL>(z, row, lane, a);
@@ -190,6 +200,7 @@ struct LnBwdGeo {
   static constexpr int H = TPR * 8;
   static constexpr int G = WPR == 1 ? 8 : (WPR == 2 ? 4 : 2);  // <= 256 threads, 2 blocks / SM
   static constexpr int THREADS = G * TPR;
+  static constexpr int MINB = 2;  // resident blocks per SM (3 measured slower: spills)
 };
 
 struct LnBwdRaw {
@@ -208,7 +219,7 @@ __device__ __forceinline__ void ln_bwd_load(const mimose_ops::LnBwdArgs& a, int6
 }
 
 template <int WPR, bool DY2, bool DRES>
-__global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, 2)
+__global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     ln_bwd_kernel(const mimose_ops::LnBwdArgs a) {
   using Geo = LnBwdGeo<WPR>;
   constexpr int TPR = Geo::TPR, H = Geo::H, G = Geo::G;
@@ -253,9 +264,10 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, 2)
       for (int e = 0; e < 8; ++e) dy[e] += d2[e];
     }
     if (a.in_drop.threshold != 0) {
-      const uint32_t m = dropout_mask8(a.in_drop, idx);
+      const Philox ph(a.in_drop.seed, a.in_drop.stream, (uint64_t)idx >> 3);
+      const uint32_t thr_hi = a.in_drop.threshold << 16;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) dy[e] = ((m >> e) & 1u) ? dy[e] * a.in_drop.scale : 0.f;
+      for (int e = 0; e < 8; ++e) dy[e] = philox_keep(ph, e, thr_hi) ? dy[e] * a.in_drop.scale : 0.f;
     }
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -296,13 +308,19 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, 2)
       for (int e = 0; e < 8; ++e) dz[e] += rr[e];
     }
     store8(static_cast<bf16*>(a.dz) + idx, dz);
-    const uint32_t m = dropout_mask8(a.br_drop, idx);
     float db[8];
+    if (a.br_drop.threshold != 0) {
+      const Philox ph(a.br_drop.seed, a.br_drop.stream, (uint64_t)idx >> 3);
+      const uint32_t thr_hi = a.br_drop.threshold << 16;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      db[e] = bf16r(((m >> e) & 1u) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
-      acc_d[e] += db[e];
+      for (int e = 0; e < 8; ++e)
+        db[e] = bf16r(philox_keep(ph, e, thr_hi) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) db[e] = bf16r(bf16r(dz[e]) * a.br_drop.scale);
     }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc_d[e] += db[e];
     if (a.dbr != nullptr) store8(static_cast<bf16*>(a.dbr) + idx, db);
     cur = nxt;
     st_cur = st_nxt;
@@ -430,6 +448,10 @@ __device__ __forceinline__ float group_max(float v) {
 
 
 // All loads of a lane are issued before any arithmetic; exp is evaluated once.
+// Instruction economy (the kernel is issue-bound, not HBM-bound, once Philox
+// is counted): whole 8-column chunks skip per-element bounds checks, the
+// max is taken on raw scores and folded into one FFMA before ex2, and the
+// keep predicates come straight from the Philox words (philox_keep).
 template <int L, int MAXC>
 __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict__ s_in,
                                                           bf16* __restrict__ p_out,
@@ -444,12 +466,12 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
   const bool live = row < rows;
   const bf16* in = s_in + (live ? row : 0) * ld;
   // causal: keys j > query i (= row within its sequence) are masked out
-  const int jmax = causal ? static_cast<int>(row % S) + 1 : S;
+  const int jmax = live ? (causal ? static_cast<int>(row % S) + 1 : S) : 0;
   uint4 raw[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    raw[c] = (live && j0 < jmax) ? *reinterpret_cast<const uint4*>(in + j0) : make_uint4(0, 0, 0, 0);
+    raw[c] = j0 < jmax ? __ldcs(reinterpret_cast<const uint4*>(in + j0)) : make_uint4(0, 0, 0, 0);
   }
   float v[MAXC][8];
   float mx = -INFINITY;
@@ -457,36 +479,58 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(const bf16* __restrict
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
     unpack8(raw[c], v[c]);
+    if (j0 + 8 <= jmax) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      v[c][e] = (live && j0 + e < jmax) ? v[c][e] * kLog2e : -INFINITY;
-      mx = fmaxf(mx, v[c][e]);
+      for (int e = 0; e < 8; ++e) mx = fmaxf(mx, v[c][e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        v[c][e] = j0 + e < jmax ? v[c][e] : -INFINITY;
+        mx = fmaxf(mx, v[c][e]);
+      }
     }
   }
   mx = group_max<L>(mx);
+  const float nmx = -mx * kLog2e;  // exp(s - max) = 2^(s log2e - max log2e)
   float sum = 0.f;
 #pragma unroll
   for (int c = 0; c < MAXC; ++c)
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      v[c][e] = exp2f(v[c][e] - mx);
+      v[c][e] = exp2_neg(fmaf(v[c][e], kLog2e, nmx));
       sum += v[c][e];
     }
   const float inv = 1.f / group_sum<L>(sum);
   if (!live) return;
+  const uint32_t thr_hi = drop.threshold << 16;
+  // chunks in pairs: one Philox key schedule per pair, two interleaved chains
 #pragma unroll
-  for (int c = 0; c < MAXC; ++c) {
-    const int j0 = 8 * (sub + L * c);
-    if (j0 >= ld) continue;
-    float p[8], pd[8];
-    const uint32_t m = dropout_mask8(drop, (uint64_t)row * ld + j0);
+  for (int c2 = 0; c2 < MAXC; c2 += 2) {
+    constexpr int W = 2;
+    uint32_t rnd[W][4];
+    if (pd_out != nullptr) {
+      uint64_t grp[W];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      p[e] = bf16r(v[c][e] * inv);
-      pd[e] = ((m >> e) & 1u) ? p[e] * drop.scale : 0.f;
+      for (int u = 0; u < W; ++u) grp[u] = ((uint64_t)row * ld + 8 * (sub + L * (c2 + u))) >> 3;
+      philox_n<W>(drop.seed, drop.stream, grp, rnd);
     }
-    store8(p_out + row * ld + j0, p);
-    if (pd_out != nullptr) store8(pd_out + row * ld + j0, pd);
+#pragma unroll
+    for (int u = 0; u < W; ++u) {
+      const int c = c2 + u;
+      if (c >= MAXC) break;
+      const int j0 = 8 * (sub + L * c);
+      if (j0 >= ld) continue;
+      float p[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) p[e] = bf16r(v[c][e] * inv);
+      store8(p_out + row * ld + j0, p);
+      if (pd_out != nullptr) {
+        float pd[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) pd[e] = philox_keep_w(rnd[u], e, thr_hi) ? p[e] * drop.scale : 0.f;
+        store8(pd_out + row * ld + j0, pd);
+      }
+    }
   }
 }
 
@@ -502,29 +546,45 @@ __global__ void __launch_bounds__(256, (MAXC > 4) ? 1 : 2) softmax_bwd_kernel(co
   const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
   const bool live = row < rows;
   const int64_t base = (live ? row : 0) * ld;
+  const int jmax = live ? S : 0;
   uint4 praw[MAXC], draw[MAXC];
-  uint32_t mbits = 0;  // keep bits, 8 per chunk... packed 4 chunks per word below
-  uint32_t mk[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    const bool in = live && j0 < S;
-    praw[c] = in ? *reinterpret_cast<const uint4*>(P + base + j0) : make_uint4(0, 0, 0, 0);
-    draw[c] = in ? *reinterpret_cast<const uint4*>(dpd + base + j0) : make_uint4(0, 0, 0, 0);
+    const bool in = j0 < jmax;
+    praw[c] = in ? __ldcs(reinterpret_cast<const uint4*>(P + base + j0)) : make_uint4(0, 0, 0, 0);
+    draw[c] = in ? __ldcs(reinterpret_cast<const uint4*>(dpd + base + j0)) : make_uint4(0, 0, 0, 0);
   }
-  (void)mbits;
+  // g = dP = dPd * keep * scale (0 outside the row); P is 0 outside (zero-filled loads)
+  const uint32_t thr_hi = drop.threshold << 16;
+  float g[MAXC][8];
   float dot = 0.f;
+  uint32_t rnd[MAXC][4];
+  {
+    uint64_t grp[MAXC];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) grp[c] = ((uint64_t)row * ld + 8 * (sub + L * c)) >> 3;
+    philox_n<MAXC>(drop.seed, drop.stream, grp, rnd);
+  }
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
-    mk[c] = (live && j0 < S) ? dropout_mask8(drop, (uint64_t)row * ld + j0) : 0u;
-    if (!(live && j0 < S)) continue;
     float p[8], dp[8];
     unpack8(praw[c], p);
     unpack8(draw[c], dp);
+    if (j0 + 8 <= jmax) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e)
-      if (j0 + e < S && ((mk[c] >> e) & 1u)) dot += dp[e] * drop.scale * p[e];
+      for (int e = 0; e < 8; ++e) {
+        g[c][e] = philox_keep_w(rnd[c], e, thr_hi) ? dp[e] * drop.scale : 0.f;
+        dot += g[c][e] * p[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        g[c][e] = (j0 + e < jmax && philox_keep_w(rnd[c], e, thr_hi)) ? dp[e] * drop.scale : 0.f;
+        dot += g[c][e] * p[e];
+      }
+    }
   }
   dot = group_sum<L>(dot);
   if (!live) return;
@@ -532,16 +592,10 @@ __global__ void __launch_bounds__(256, (MAXC > 4) ? 1 : 2) softmax_bwd_kernel(co
   for (int c = 0; c < MAXC; ++c) {
     const int j0 = 8 * (sub + L * c);
     if (j0 >= ld) continue;
-    float p[8], dp[8], ds[8];
+    float p[8], ds[8];
     unpack8(praw[c], p);
-    unpack8(draw[c], dp);
-    const uint32_t m = mk[c];
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const bool in = j0 + e < S;
-      const float g = (in && ((m >> e) & 1u)) ? dp[e] * drop.scale : 0.f;
-      ds[e] = in ? p[e] * (g - dot) * scale : 0.f;
-    }
+    for (int e = 0; e < 8; ++e) ds[e] = j0 + e < S ? p[e] * (g[c][e] - dot) * scale : 0.f;
     store8(dpd + base + j0, ds);
   }
 }

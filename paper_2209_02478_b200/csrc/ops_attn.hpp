@@ -14,9 +14,11 @@ namespace mimose_ops {
 
 // bf16 operand map over a 4-D view with a {64, box_rows} SWIZZLE_128B box
 bool make_operand_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box_rows);
-// bf16 output map (rows x cols, pitch ld, batch strides) with a {64, 32} box
+// bf16 output map (rows x cols, pitch ld, batch strides) with a {box_cols, 32}
+// box, SWIZZLE_128B (64 columns) or SWIZZLE_64B (32 columns)
 bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, int64_t ld,
-                     int64_t bs1, int64_t bs2, int nb1, int nb2);
+                     int64_t bs1, int64_t bs2, int nb1, int nb2, uint32_t box_cols = 64,
+                     bool sw64 = false);
 
 bool attn_fused_supported(int S);
 // P = softmax(alpha * Q K^T), Pd = dropout(P) (Pd may be null when p = 0)
