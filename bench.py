@@ -396,7 +396,6 @@ def run_gpu_arm(args, rank, world, local):
     pcsv = C.c_void_p()
     lib.mimose_profile_csv(C.byref(pcsv))
     classes = sorted({l.split(",", 1)[0] for l in _lib.take_string(lib, pcsv).splitlines()[1:]})
-    lib.mimose_profile_enable(0)
     peak_tf = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)))
     peak_bw = float(pk.get("hbm_gbs", 6547.0))
     # dominant kernel family: the dense (projection / FFN / weight-gradient)
@@ -418,6 +417,7 @@ def run_gpu_arm(args, rank, world, local):
             if fl > 0:
                 st["achieved_tflops"] = fl / (cms / 1e3) / 1e12
         stages[c] = st
+    lib.mimose_profile_enable(0)  # (clears the records: read everything first)
 
     # 4. e2e: public API with HOST (pinned) inputs, H2D + loss D2H inside the region.
     #    N=1: mimose_trainer_step_async + mimose_trainer_loss with a one-step lag

@@ -96,6 +96,7 @@ typedef struct {
   void* workspace;   /* fp32 split-K partials, >= split_k * M * N * 4 bytes */
   int64_t workspace_bytes;
   int force_ew;      /* 0 = heuristic epilogue warps; 8 / 16 forces it */
+  int force_cg;      /* 0 = heuristic; 1 = one SM per tile, 2 = CTA pair (cta_group::2) */
 } mimose_gemm_args;
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);

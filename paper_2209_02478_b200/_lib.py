@@ -64,7 +64,7 @@ class GemmArgs(C.Structure):
         ("alpha", C.c_float), ("beta", C.c_float),
         ("force_bn", C.c_int), ("direct_store", C.c_int),
         ("split_k", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
-        ("force_ew", C.c_int),
+        ("force_ew", C.c_int), ("force_cg", C.c_int),
     ]
 
 

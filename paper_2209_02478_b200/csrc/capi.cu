@@ -144,6 +144,7 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   c.alpha = a->alpha; c.beta = a->beta;
   c.force_bn = a->force_bn;
   c.force_ew = a->force_ew;
+  c.force_cg = a->force_cg;
   c.direct_store = a->direct_store != 0;
   c.split_k = a->split_k;
   c.workspace = a->workspace;

@@ -132,12 +132,12 @@ bool make_map(CUtensorMap* map, const MatView& v, int nb1, int nb2, uint32_t box
   return make_map_t(map, v.ptr, v.rows, v.cols, v.ld, v.bs1, v.bs2, nb1, nb2, 64, box_rows, 2);
 }
 
-template <int BN, int EPI, int EW>
+template <int BN, int EPI, int EW, int CG = 1>
 cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& td,
                      const CUtensorMap& td2, const mimose_dev::GemmParams& p, int grid,
                      cudaStream_t stream) {
-  using Cfg = mimose_dev::GemmCfg<BN, EPI, EW>;
-  auto kern = mimose_dev::gemm_bf16_tn_kernel<BN, EPI, EW>;
+  using Cfg = mimose_dev::GemmCfg<BN, EPI, EW, CG>;
+  auto kern = mimose_dev::gemm_bf16_tn_kernel<BN, EPI, EW, CG>;
   static bool configured = false;
   if (!configured) {
     cudaError_t e =
@@ -145,9 +145,42 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
+  if constexpr (CG == 1) {
+    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
+  } else {
+    // CTA pairs: cluster (2, 1, 1), `grid` counts CTAs (2 per pair tile slot)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(Cfg::kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, td2, p);
+    if (e != cudaSuccess) return e;
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
+}
+
+// CTA-pair (cta_group::2) launches: BN = 256 only
+cudaError_t launch_pair(int epi, int ew, const CUtensorMap& ta, const CUtensorMap& tb,
+                        const CUtensorMap& td, const CUtensorMap& td2,
+                        const mimose_dev::GemmParams& p, int grid, cudaStream_t s) {
+  using namespace mimose_dev;
+  switch (epi) {
+    case kEpiBf16: return launch_t<256, kEpiBf16, 8, 2>(ta, tb, td, td2, p, grid, s);
+    case kEpiBiasGelu: return launch_t<256, kEpiBiasGelu, 16, 2>(ta, tb, td, td2, p, grid, s);
+    case kEpiDGelu: return launch_t<256, kEpiDGelu, 16, 2>(ta, tb, td, td2, p, grid, s);
+    case kEpiF32: return launch_t<256, kEpiF32, 8, 2>(ta, tb, td, td2, p, grid, s);
+  }
+  (void)ew;
+  return cudaErrorInvalidValue;
 }
 
 template <int BN>
@@ -174,6 +207,25 @@ cudaError_t launch_bn(int epi, int ew, const CUtensorMap& ta, const CUtensorMap&
 // 549 -> 742 TFLOP/s, dGELU 638 -> 802), 8 otherwise (the write-bound
 // attention contractions measured slower with 16). MIMOSE_GEMM_EW
 // (8 / 16) overrides for A/B timing.
+// CTA pair (cta_group::2, 256 x 256 tiles over two SMs): halves the B-operand
+// traffic per SM and deepens the smem pipeline (6 stages of 32 KB). Used for
+// unbatched, un-split GEMMs with >= 2 row blocks whose epilogue is light
+// (K >= 768 projections and data gradients: 1090 -> 1250 TFLOP/s at K = 3072).
+// MIMOSE_GEMM_CG=1/2 forces (A/B timing); force_cg in the call overrides.
+int pick_cg(const GemmCall& c, int bn, int splits) {
+  static const int forced = [] {
+    const char* e = std::getenv("MIMOSE_GEMM_CG");
+    return e != nullptr ? std::atoi(e) : 0;
+  }();
+  if (bn != 256 || c.nb1 * c.nb2 != 1 || splits != 1 || c.M <= 128) return 1;
+  if (c.force_cg == 1 || c.force_cg == 2) return c.force_cg;
+  if (forced == 1 || forced == 2) return forced;
+  // epilogue-bound GELU / dGELU tiles gain nothing from a faster mainloop and
+  // lose to the pair's joint accumulator release (measured 730 -> 683 TFLOP/s)
+  if (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) return 1;
+  return 2;
+}
+
 int pick_ew(const GemmCall& c, int bn) {
   static const int forced = [] {
     const char* e = std::getenv("MIMOSE_GEMM_EW");
@@ -288,7 +340,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   if ((reinterpret_cast<uintptr_t>(c.A.ptr) & 15) || (reinterpret_cast<uintptr_t>(c.B.ptr) & 15))
     return cudaErrorMisalignedAddress;
   const int bn = pick_bn(c);
-  const int ew = pick_ew(c, bn);
+  int ew = pick_ew(c, bn);
   int splits = 1;
   if (c.epi == kEpiF32 && c.nb1 == 1 && c.nb2 == 1 && c.workspace != nullptr && c.split_k != 1 &&
       c.N % 4 == 0 && (reinterpret_cast<uintptr_t>(c.workspace) & 15) == 0) {
@@ -299,7 +351,9 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   }
   CUtensorMap ta, tb;
   if (!make_map(&ta, c.A, c.nb1, c.nb2, c.a_mn ? 64u : 128u)) return cudaErrorInvalidValue;
-  if (!make_map(&tb, c.B, c.nb1, c.nb2, c.b_mn ? 64u : (uint32_t)bn))
+  const int cg = pick_cg(c, bn, splits);
+  if (cg == 2) ew = (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) ? 16 : 8;  // launch_pair
+  if (!make_map(&tb, c.B, c.nb1, c.nb2, c.b_mn ? 64u : (uint32_t)(bn / cg)))
     return cudaErrorInvalidValue;
 
   mimose_dev::GemmParams p{};
@@ -356,9 +410,10 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     p.tma_store = ok ? 1 : 0;
   }
 
-  const int64_t tiles =
-      (int64_t)((c.M + 127) / 128) * ((c.N + bn - 1) / bn) * c.nb1 * c.nb2 * splits;
-  const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+  const int64_t tiles = (int64_t)((c.M + 128 * cg - 1) / (128 * cg)) * ((c.N + bn - 1) / bn) *
+                        c.nb1 * c.nb2 * splits;
+  const int slots = sm_count() / cg;  // CTAs (cg = 1) or CTA pairs (cg = 2) resident at once
+  const int grid = (int)(tiles < slots ? tiles : slots) * cg;
   // roofline record: algorithmic flops 2*M*N*K*batch; algorithmic bytes =
   // operands read once + outputs (and epilogue side inputs) once. Batched
   // (per-head) views are the materialised-attention contractions.
@@ -373,7 +428,8 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     gdesc = std::to_string(c.M) + " " + std::to_string(c.N) + " " + std::to_string(c.K) + " " +
             std::to_string(c.nb1 * c.nb2) + " bn" + std::to_string(bn) + " amn" +
             std::to_string((int)c.a_mn) + " bmn" + std::to_string((int)c.b_mn) + " epi" +
-            std::to_string(c.epi) + " ew" + std::to_string(ew) + " splits" + std::to_string(splits) + " grid" +
+            std::to_string(c.epi) + " ew" + std::to_string(ew) + " cg" + std::to_string(cg) +
+            " splits" + std::to_string(splits) + " grid" +
             std::to_string(grid);
   ProfScope prof(nb > 1 ? "gemm_attn" : "gemm_dense", 2.0 * c.M * (double)c.N * c.K * nb, gbytes,
                  stream, gdesc);
@@ -381,7 +437,10 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   switch (bn) {
     case 64: err = launch_bn<64>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
     case 128: err = launch_bn<128>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
-    case 256: err = launch_bn<256>(c.epi, ew, ta, tb, td, td2, p, grid, stream); break;
+    case 256:
+      err = cg == 2 ? launch_pair(c.epi, ew, ta, tb, td, td2, p, grid, stream)
+                    : launch_bn<256>(c.epi, ew, ta, tb, td, td2, p, grid, stream);
+      break;
   }
   if (err == cudaSuccess && splits > 1) {
     splitk_reduce_kernel<<<2 * sm_count(), 256, 0, stream>>>(

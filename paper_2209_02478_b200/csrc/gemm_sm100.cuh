@@ -72,10 +72,14 @@ constexpr int gemm_chunk_bytes(int BN, int EPI, int EW) {
          : ((BN / (EW / 4)) * (EPI == kEpiF32 ? 4 : 2) >= 128 ? 128 : 64);
 }
 
-template <int BN, int EPI, int EW = 8>
+// CG = cta_group: 1 (one SM per 128 x BN tile) or 2 (a CTA pair per
+// 256 x BN tile: each CTA loads its 128 A rows and half of the B rows, the
+// leader issues the pair's MMAs, each CTA's TMEM holds its 128 output rows)
+template <int BN, int EPI, int EW = 8, int CG = 1>
 struct GemmCfg {
+  static constexpr int kBRows = BN / CG;  // B rows staged per CTA
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kNOut = EPI == kEpiBiasGelu ? 2 : 1;
   static constexpr int kEsz = EPI == kEpiF32 ? 4 : 2;
@@ -245,15 +249,18 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
   }
 }
 
-template <int BN, int EPI, int EW>
+template <int BN, int EPI, int EW, int CG>
 __global__ void __launch_bounds__(gemm_threads(EW), 1)
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmD,
                         const __grid_constant__ CUtensorMap tmD2, const GemmParams p) {
-  using Cfg = GemmCfg<BN, EPI, EW>;
+  using Cfg = GemmCfg<BN, EPI, EW, CG>;
   constexpr int S = Cfg::kStages;
   constexpr int kEpiWarps = EW;
+  constexpr int kTileM = kBM * CG;  // output rows per (pair) tile
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -270,7 +277,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
 
-  const int tiles_m = (p.M + kBM - 1) / kBM;
+  const int tiles_m = (p.M + kTileM - 1) / kTileM;
   const int tiles_n = (p.N + BN - 1) / BN;
   const int tiles_per_batch = tiles_m * tiles_n;
   const int num_tiles = tiles_per_batch * p.nb1 * p.nb2 * p.splits;
@@ -289,13 +296,17 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], kEpiWarps);  // one arrive per epilogue warp
+      mbar_init(&tempty[a], kEpiWarps * CG);  // one arrive per epilogue warp (of both CTAs)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 1) {
+    if constexpr (CG == 2) tmem_alloc_2sm(tmem_slot, Cfg::kTmemCols);
+    else tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote signal
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -303,13 +314,14 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int it = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      const uint32_t full_leader = CG == 2 ? mapa_rank(&full[0], 0) : 0u;
+      for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
         const int zz = tile / tiles_per_batch;
         const int t_in = tile % tiles_per_batch;
         // n-fastest raster: the CTAs that run concurrently share one A row
         // block (read once from HBM) and cycle through B (weights, L2-resident)
-        const int m0 = (t_in / tiles_n) * kBM;
-        const int n0 = (t_in % tiles_n) * BN;
+        const int m0 = (t_in / tiles_n) * kTileM + (int)rank * kBM;
+        const int n0 = (t_in % tiles_n) * BN + (int)rank * Cfg::kBRows;
         const int split = zz % p.splits, z = zz / p.splits;
         const int b1 = z % p.nb1, b2 = z / p.nb1;
         const int kb0 = split * p.kb_per_split;
@@ -318,30 +330,54 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
           uint8_t* a_dst = sA + s * Cfg::kABytes;
           uint8_t* b_dst = sB + s * Cfg::kBBytes;
           const int k0 = kb * kBK;
-          if (!p.a_mn) {
-            tma_load_4d(&tmA, &full[s], a_dst, k0, m0, b1, b2);
-          } else {
+          if constexpr (CG == 2) {
+            // both CTAs' bytes complete on the leader's full[s]; only the
+            // leader arms it (a peer's early complete_tx is absorbed: the
+            // phase cannot flip before the leader's arrive)
+            const uint32_t fb = full_leader + (uint32_t)(s * sizeof(uint64_t));
+            if (leader) mbar_arrive_expect_tx(&full[s], CG * Cfg::kStageBytes);
+            if (!p.a_mn) {
+              tma_load_4d_2sm(&tmA, fb, a_dst, k0, m0, b1, b2);
+            } else {
 #pragma unroll
-            for (int j = 0; j < kBM / 64; ++j)
-              tma_load_4d(&tmA, &full[s], a_dst + j * 8192, m0 + 64 * j, k0, b1, b2);
-          }
-          if (!p.b_mn) {
-            tma_load_4d(&tmB, &full[s], b_dst, k0, n0, b1, b2);
-          } else {
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_4d_2sm(&tmA, fb, a_dst + j * 8192, m0 + 64 * j, k0, b1, b2);
+            }
+            if (!p.b_mn) {
+              tma_load_4d_2sm(&tmB, fb, b_dst, k0, n0, b1, b2);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_4d(&tmB, &full[s], b_dst + j * 8192, n0 + 64 * j, k0, b1, b2);
+              for (int j = 0; j < Cfg::kBRows / 64; ++j)
+                tma_load_4d_2sm(&tmB, fb, b_dst + j * 8192, n0 + 64 * j, k0, b1, b2);
+            }
+          } else {
+            mbar_arrive_expect_tx(&full[s], Cfg::kStageBytes);
+            if (!p.a_mn) {
+              tma_load_4d(&tmA, &full[s], a_dst, k0, m0, b1, b2);
+            } else {
+#pragma unroll
+              for (int j = 0; j < kBM / 64; ++j)
+                tma_load_4d(&tmA, &full[s], a_dst + j * 8192, m0 + 64 * j, k0, b1, b2);
+            }
+            if (!p.b_mn) {
+              tma_load_4d(&tmB, &full[s], b_dst, k0, n0, b1, b2);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_4d(&tmB, &full[s], b_dst + j * 8192, n0 + 64 * j, k0, b1, b2);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_bf16_f32(kBM, BN, p.a_mn != 0, p.b_mn != 0);
+    // (CTA pair: the leader alone issues the 256-row MMAs for both CTAs)
+    if (CG == 1 || leader) {
+    const uint32_t idesc = idesc_bf16_f32(kTileM, BN, p.a_mn != 0, p.b_mn != 0);
     // K-major: advance 16 elements = 32 B inside the 128 B swizzle row.
     // MN-major: advance 16 K-rows = 2048 B; LBO = 64 rows * 128 B between MN blocks.
     const uint32_t a_step = p.a_mn ? 2048u : 32u;
@@ -349,7 +385,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
     const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
     int it = 0, local = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++local) {
       const int acc = local & 1;
       const uint32_t aph = (local >> 1) & 1;
       const int split = (tile / tiles_per_batch) % p.splits;
@@ -369,13 +405,20 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
           for (int kk = 0; kk < kBK / 16; ++kk) {
             const uint64_t da = smem_desc_sw128(a_addr + kk * a_step, a_lbo, 1024);
             const uint64_t db = smem_desc_sw128(b_addr + kk * b_step, b_lbo, 1024);
-            umma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            if constexpr (CG == 2) umma_bf16_2sm(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
+            else umma_bf16(d_tmem, da, db, idesc, (kb | kk) != 0 ? 1u : 0u);
           }
-          umma_commit(&empty[s]);
-          if (kb == kb_n - 1) umma_commit(&tfull[acc]);
+          if constexpr (CG == 2) {
+            umma_commit_2sm(&empty[s], 0x3);
+            if (kb == kb_n - 1) umma_commit_2sm(&tfull[acc], 0x3);
+          } else {
+            umma_commit(&empty[s]);
+            if (kb == kb_n - 1) umma_commit(&tfull[acc]);
+          }
         }
         __syncwarp();
       }
+    }
     }
   } else {
     // ------------------------------------------------------------ epilogue
@@ -387,10 +430,11 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     constexpr int NCH = CB / 16;        // 16-byte chunks per staged row
     uint8_t* wbuf = sD + ew * (Cfg::kBufs * Cfg::kNOut * Cfg::kBufBytes);
     int local = 0, chunk_seq = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++local) {
+    const uint32_t tempty_leader = CG == 2 ? mapa_rank(&tempty[0], 0) : 0u;
+    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++local) {
       const int zz = tile / tiles_per_batch;
       const int t_in = tile % tiles_per_batch;
-      const int m0 = (t_in / tiles_n) * kBM;
+      const int m0 = (t_in / tiles_n) * kTileM + (int)rank * kBM;
       const int n0 = (t_in % tiles_n) * BN;
       const int split = zz % p.splits, z = zz / p.splits;
       // split-K partials are addressed as batch index b1 = split of the workspace
@@ -547,11 +591,23 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
+        else mbar_arrive(&tempty[acc]);
+      }
     }
     if (p.tma_store && lane == 0) bulk_wait<0>();
   }
-
+  if constexpr (CG == 2) {
+    // both CTAs done with TMEM and with every remote barrier before teardown
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+      tc_fence_after();
+      tmem_dealloc_2sm(tmem_base, Cfg::kTmemCols);
+    }
+    return;
+  }
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();

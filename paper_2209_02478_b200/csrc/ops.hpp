@@ -39,6 +39,7 @@ struct GemmCall {
   float alpha = 1.f, beta = 0.f;
   int force_bn = 0;  // 0 = heuristic; 64/128/256 for tests
   int force_ew = 0;  // 0 = heuristic; 8 / 16 epilogue warps for tests
+  int force_cg = 0;  // 0 = heuristic; 1 / 2 (CTA pair) for tests
   bool direct_store = false;  // tests: force the per-thread store epilogue
   // deterministic split-K for fp32 (weight-gradient) outputs: partials go to
   // `workspace` ([splits][M][N] fp32) and are summed in a fixed order.

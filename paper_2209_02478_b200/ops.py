@@ -36,7 +36,7 @@ def _view(t: torch.Tensor, nb1: int, nb2: int):
 
 
 def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None, bias=None,
-         alpha=1.0, beta=0.0, force_bn=0, force_ew=0, direct_store=False, split_k=1,
+         alpha=1.0, beta=0.0, force_bn=0, force_ew=0, force_cg=0, direct_store=False, split_k=1,
          workspace=None, stream=None):
     """out[z] = alpha * op(a)[z] @ op(b)[z]^T with the kernel's epilogue.
 
@@ -67,6 +67,7 @@ def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None
     args.alpha, args.beta = alpha, beta
     args.force_bn = force_bn
     args.force_ew = force_ew
+    args.force_cg = force_cg
     args.direct_store = int(direct_store)
     args.split_k = split_k
     if workspace is not None:

@@ -37,13 +37,16 @@ def _rand(*shape, dev="cuda"):
     return torch.randn(*shape, device=dev).to(torch.bfloat16)
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("ew", [8, 16])
 @pytest.mark.parametrize("direct", [False, True])
 @pytest.mark.parametrize("bn", [64, 128, 256])
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("shape", [(256, 256, 128), (200, 72, 80), (1000, 770, 768), (128, 2304, 64)])
-def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct, ew):
+def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct, ew, cg):
+    if cg == 2 and (bn != 256 or shape[0] <= 128):
+        pytest.skip("CTA pairs run 256-wide tiles with >= 2 row blocks")
     ops = _ops()
     torch.manual_seed(0)
     M, N, K = shape
@@ -55,14 +58,15 @@ def test_gemm_majors(cuda_device, bn, a_mn, b_mn, shape, direct, ew):
         pytest.skip("TMA needs 16-byte row pitch")
     out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     ops.gemm(a_arg, b_arg, out, a_mn=a_mn, b_mn=b_mn, force_bn=bn, direct_store=direct,
-             force_ew=ew)
+             force_ew=ew, force_cg=cg)
     torch.cuda.synchronize()
     _check_bf16(out, A.float() @ B.float().t())
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("beta", [0.0, 0.5])
 @pytest.mark.parametrize("bn", [128, 256])
-def test_gemm_f32_beta(cuda_device, bn, beta):
+def test_gemm_f32_beta(cuda_device, bn, beta, cg):
     ops = _ops()
     torch.manual_seed(1)
     M, N, K = 768, 3072, 4096
@@ -71,14 +75,16 @@ def test_gemm_f32_beta(cuda_device, bn, beta):
     X = _rand(K, N)   # [T, K_in]
     out = torch.randn(M, N, device="cuda")
     ref = out * beta + dY.float().t() @ X.float()
-    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, beta=beta, force_bn=bn)
+    ops.gemm(dY, X, out, a_mn=True, b_mn=True, epi=ops.EPI_F32, beta=beta, force_bn=bn,
+             force_cg=cg)
     torch.cuda.synchronize()
     _check_f32(out, ref, K)
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("ew", [8, 16])
 @pytest.mark.parametrize("M", [517, 1024])
-def test_gemm_bias_gelu_and_dgelu(cuda_device, M, ew):
+def test_gemm_bias_gelu_and_dgelu(cuda_device, M, ew, cg):
     ops = _ops()
     torch.manual_seed(2)
     N, K = 3072, 768
@@ -87,7 +93,7 @@ def test_gemm_bias_gelu_and_dgelu(cuda_device, M, ew):
     bias = torch.randn(N, device="cuda")
     u = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     g = torch.empty_like(u)
-    ops.gemm(X, W, u, epi=ops.EPI_BIAS_GELU, out2=g, bias=bias, force_ew=ew)
+    ops.gemm(X, W, u, epi=ops.EPI_BIAS_GELU, out2=g, bias=bias, force_ew=ew, force_cg=cg)
     torch.cuda.synchronize()
     u_ref = X.float() @ W.float().t() + bias
     _check_bf16(u, u_ref)
@@ -98,7 +104,7 @@ def test_gemm_bias_gelu_and_dgelu(cuda_device, M, ew):
     dY = _rand(M, K)
     du = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     W2 = _rand(K, N) * 0.05  # FFN2 weight [H, 4H]: dgrad B operand is MN-major view [K=H, N=4H]
-    ops.gemm(dY, W2, du, b_mn=True, epi=ops.EPI_DGELU, aux=u, force_ew=ew)
+    ops.gemm(dY, W2, du, b_mn=True, epi=ops.EPI_DGELU, aux=u, force_ew=ew, force_cg=cg)
     torch.cuda.synchronize()
     uf = u.float().requires_grad_(True)
     torch.nn.functional.gelu(uf).backward(torch.ones_like(uf))
