@@ -212,12 +212,12 @@ cudaError_t launch_bn(int epi, int ew, const CUtensorMap& ta, const CUtensorMap&
 // unbatched, un-split GEMMs with >= 2 row blocks whose epilogue is light
 // (K >= 768 projections and data gradients: 1090 -> 1250 TFLOP/s at K = 3072).
 // MIMOSE_GEMM_CG=1/2 forces (A/B timing); force_cg in the call overrides.
-int pick_cg(const GemmCall& c, int bn, int splits) {
+int pick_cg(const GemmCall& c, int bn) {
   static const int forced = [] {
     const char* e = std::getenv("MIMOSE_GEMM_CG");
     return e != nullptr ? std::atoi(e) : 0;
   }();
-  if (bn != 256 || c.nb1 * c.nb2 != 1 || splits != 1 || c.M <= 128) return 1;
+  if (bn != 256 || c.nb1 * c.nb2 != 1 || c.M <= 128) return 1;
   if (c.force_cg == 1 || c.force_cg == 2) return c.force_cg;
   if (forced == 1 || forced == 2) return forced;
   // epilogue-bound GELU / dGELU tiles gain nothing from a faster mainloop and
@@ -286,11 +286,10 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-// wave efficiency of `tiles` CTAs on the SMs
-double wave_eff(int64_t tiles) {
-  const int64_t sm = sm_count();
-  const int64_t waves = (tiles + sm - 1) / sm;
-  return (double)tiles / (double)(waves * sm);
+// wave efficiency of `tiles` work units on `slots` resident CTAs (or pairs)
+double wave_eff(int64_t tiles, int64_t slots) {
+  const int64_t waves = (tiles + slots - 1) / slots;
+  return (double)tiles / (double)(waves * slots);
 }
 
 }  // namespace
@@ -305,14 +304,15 @@ bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, in
   return make_map_t(map, ptr, rows, cols, ld, bs1, bs2, nb1, nb2, box_cols, 32, 2, sw64);
 }
 
-int pick_split_k(int M, int N, int K, int bn) {
-  const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + bn - 1) / bn);
+int pick_split_k(int M, int N, int K, int bn, int cg) {
+  const int64_t tiles = (int64_t)((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
+  const int64_t slots = sm_count() / cg;
   const int kb = (K + 63) / 64;
   int best = 1;
-  double best_eff = wave_eff(tiles);
+  double best_eff = wave_eff(tiles, slots);
   for (int s = 2; s <= 8; ++s) {
     if (kb / s < 8) break;  // keep >= 8 k-blocks per split
-    const double e = wave_eff(tiles * s);
+    const double e = wave_eff(tiles * s, slots);
     if (e > best_eff + 0.05) {
       best = s;
       best_eff = e;
@@ -327,7 +327,7 @@ int64_t splitk_workspace_bytes(int M, int N, int K) {
   int dummy = 0;
   c.workspace = &dummy;  // "a workspace will be provided"
   const int bn = pick_bn(c);
-  int s = pick_split_k(M, N, K, bn);
+  int s = pick_split_k(M, N, K, bn, pick_cg(c, bn));
   return s > 1 ? (int64_t)s * M * N * 4 : 0;
 }
 
@@ -341,18 +341,18 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     return cudaErrorMisalignedAddress;
   const int bn = pick_bn(c);
   int ew = pick_ew(c, bn);
+  const int cg = pick_cg(c, bn);
+  if (cg == 2) ew = (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) ? 16 : 8;  // launch_pair
   int splits = 1;
   if (c.epi == kEpiF32 && c.nb1 == 1 && c.nb2 == 1 && c.workspace != nullptr && c.split_k != 1 &&
       c.N % 4 == 0 && (reinterpret_cast<uintptr_t>(c.workspace) & 15) == 0) {
-    splits = c.split_k > 1 ? c.split_k : pick_split_k(c.M, c.N, c.K, bn);
+    splits = c.split_k > 1 ? c.split_k : pick_split_k(c.M, c.N, c.K, bn, cg);
     const int kb = (c.K + 63) / 64;
     if (splits > kb) splits = kb;
     while (splits > 1 && (int64_t)splits * c.M * c.N * 4 > c.workspace_bytes) --splits;
   }
   CUtensorMap ta, tb;
   if (!make_map(&ta, c.A, c.nb1, c.nb2, c.a_mn ? 64u : 128u)) return cudaErrorInvalidValue;
-  const int cg = pick_cg(c, bn, splits);
-  if (cg == 2) ew = (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) ? 16 : 8;  // launch_pair
   if (!make_map(&tb, c.B, c.nb1, c.nb2, c.b_mn ? 64u : (uint32_t)(bn / cg)))
     return cudaErrorInvalidValue;
 

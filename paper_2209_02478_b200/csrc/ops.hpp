@@ -53,7 +53,7 @@ struct GemmCall {
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);
 // split-K choice for an fp32 (weight-gradient) GEMM and the workspace it needs
-int pick_split_k(int M, int N, int K, int bn);
+int pick_split_k(int M, int N, int K, int bn, int cg = 1);
 int64_t splitk_workspace_bytes(int M, int N, int K);
 void gemm_profile_enable(bool on);
 cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches);
