@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
                        const __grid_constant__ CUtensorMap tmO2, const AttnParams p) {
   using Cfg = AttnCfg<NC>;
   constexpr int NS = Cfg::kStages;
-  constexpr int Q = Cfg::kQ;
+  constexpr int NCH = NC / 128;  // 32-column chunks per column part
   constexpr float kLog2e = 1.4426950408889634f;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -202,119 +202,137 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
       const int64_t grow = ((int64_t)z * p.S + (row_ok ? i : 0));  // row of the [B*nh*S][ld] view
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
-      const int c0 = part * Q;  // first column of this warp's part
-      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NC + c0;
+      // 32-column chunks are dealt round-robin to the 4 column parts (chunk
+      // ch -> part ch % 4), so every warp gets within one chunk of S / 4
+      // columns whatever S is
+      const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * NC;
+      const uint32_t thr_hi = p.drop.threshold << 16;
 
       if constexpr (!BWD) {
         // ---- pass 1: row max of the raw scores (alpha > 0 commutes with max)
         const float sc = p.alpha * kLog2e;
         float mx = -INFINITY;
 #pragma unroll 1
-        for (int c = 0; c < Q; c += 32) {
-          if (c0 + c < p.S) {
-            uint32_t r[32];
-            tmem_ld32_nowait(t_row + c, r);
-            tmem_wait_ld();
+        for (int j = 0; j < NCH; ++j) {
+          const int c = (part + 4 * j) * 32;
+          if (c >= p.S) break;
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
+          if (c + 32 <= p.S) {
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(r[e]));
+          } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (c0 + c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]));
+              if (c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]));
           }
         }
         red_a[part * 128 + r_local] = mx * sc;
         epi_bar();
-        mx = fmaxf(fmaxf(red_a[r_local], red_a[128 + r_local]),
-                   fmaxf(red_a[256 + r_local], red_a[384 + r_local]));
+        const float nmx = -fmaxf(fmaxf(red_a[r_local], red_a[128 + r_local]),
+                                 fmaxf(red_a[256 + r_local], red_a[384 + r_local]));
         // ---- pass 2: e = 2^(s * sc - max) written back to TMEM; row sum
         float sum = 0.f;
 #pragma unroll 1
-        for (int c = 0; c < Q; c += 32) {
-          if (c0 + c < p.S) {
-            uint32_t r[32];
-            tmem_ld32_nowait(t_row + c, r);
-            tmem_wait_ld();
+        for (int j = 0; j < NCH; ++j) {
+          const int c = (part + 4 * j) * 32;
+          if (c >= p.S) break;
+          uint32_t r[32];
+          tmem_ld32_nowait(t_row + c, r);
+          tmem_wait_ld();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) {
-              const float x = c0 + c + e < p.S ? ex2f(__uint_as_float(r[e]) * sc - mx) : 0.f;
-              sum += x;
-              r[e] = __float_as_uint(x);
-            }
-            tmem_st32(t_row + c, r);
+          for (int e = 0; e < 32; ++e) {
+            const float x = c + e < p.S ? ex2f(fmaf(__uint_as_float(r[e]), sc, nmx)) : 0.f;
+            sum += x;
+            r[e] = __float_as_uint(x);
           }
+          tmem_st32(t_row + c, r);
         }
         tmem_wait_st();
         red_b[part * 128 + r_local] = sum;
         epi_bar();
         const float inv = 1.f / ((red_b[r_local] + red_b[128 + r_local]) +
                                  (red_b[256 + r_local] + red_b[384 + r_local]));
-        // ---- pass 3: normalise, dropout, stage, TMA store (32-column chunks)
+        // ---- pass 3: normalise, dropout, stage, TMA store
 #pragma unroll 1
-        for (int c = 0; c < Q; c += 32) {
-          if (c0 + c >= p.S) break;
+        for (int j = 0; j < NCH; ++j) {
+          const int c = (part + 4 * j) * 32;
+          if (c >= p.S) break;
+          uint32_t rnd[4][4];
+          if (p.store_pd) {
+            uint64_t grp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)grow * p.ld + c + 8 * q) >> 3;
+            philox_n<4>(p.drop.seed, p.drop.stream, grp, rnd);
+          }
           if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
           uint32_t r[32];
           tmem_ld32_nowait(t_row + c, r);
           tmem_wait_ld();
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
+          for (int q = 0; q < 4; ++q) {
             float pv[8], dv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * j + e]) * inv);
-            const uint32_t m =
-                row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * j) : 0xFFu;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dv[e] = ((m >> e) & 1u) ? pv[e] * p.drop.scale : 0.f;
-            const uint32_t addr = rbase + ((j ^ sw) << 4);
+            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * q + e]) * inv);
+            const uint32_t addr = rbase + ((q ^ sw) << 4);
             st_shared_v4(addr, pack_bf16x2_(pv[0], pv[1]), pack_bf16x2_(pv[2], pv[3]),
                          pack_bf16x2_(pv[4], pv[5]), pack_bf16x2_(pv[6], pv[7]));
-            if (p.store_pd)
+            if (p.store_pd) {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                dv[e] = philox_keep_w(rnd[q], e, thr_hi) ? pv[e] * p.drop.scale : 0.f;
               st_shared_v4(addr + Cfg::kBufBytes, pack_bf16x2_(dv[0], dv[1]),
                            pack_bf16x2_(dv[2], dv[3]), pack_bf16x2_(dv[4], dv[5]),
                            pack_bf16x2_(dv[6], dv[7]));
+            }
           }
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
-            tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
-            if (p.store_pd)
-              tma_store_4d(&tmO2, wbuf + Cfg::kBufBytes, c0 + c, m0 + quarter * 32, b1, b2);
+            tma_store_4d(&tmO1, wbuf, c, m0 + quarter * 32, b1, b2);
+            if (p.store_pd) tma_store_4d(&tmO2, wbuf + Cfg::kBufBytes, c, m0 + quarter * 32, b1, b2);
             bulk_commit();
           }
         }
       } else {
-        // ---- backward: pass 1 dot = sum_j dP_j P_j (dP = dPd * mask * scale)
+        // ---- backward: pass 1 dot = sum_j dP_j P_j (dP = dPd * keep * scale);
+        // the keep decisions of each 32-column chunk stay in one register
+        // (km) for pass 2, dP is re-read from TMEM
         const __nv_bfloat16* prow = p.P + grow * p.ld;
-        uint32_t mk[Q / 8];
+        uint32_t km[NCH];
         float dot = 0.f;
 #pragma unroll
-        for (int c = 0; c < Q; c += 32) {
-          if (c0 + c < p.S) {
+        for (int j = 0; j < NCH; ++j) {
+          const int c = (part + 4 * j) * 32;
+          if (c < p.S) {
+            uint64_t grp[4];
+            uint32_t rnd[4][4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)grow * p.ld + c + 8 * q) >> 3;
+            philox_n<4>(p.drop.seed, p.drop.stream, grp, rnd);
+            km[j] = 0u;
             uint4 pr[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              pr[q] = (row_ok && c0 + c + 8 * q < p.S)
-                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
-                          : make_uint4(0, 0, 0, 0);
+              pr[q] = (row_ok && c + 8 * q < p.S) ? *reinterpret_cast<const uint4*>(prow + c + 8 * q)
+                                                  : make_uint4(0, 0, 0, 0);
             uint32_t r[32];
             tmem_ld32_nowait(t_row + c, r);
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const uint32_t m =
-                  row_ok ? dropout_mask8(p.drop, (uint64_t)grow * p.ld + c0 + c + 8 * q) : 0u;
-              mk[c / 8 + q] = m;
               float pf[8];
               unpack_bf16x8(pr[q], pf);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                const int col = c0 + c + 8 * q + e;
-                if (col < p.S && ((m >> e) & 1u))
-                  dot += __uint_as_float(r[8 * q + e]) * p.drop.scale * pf[e];
+                const bool keep = c + 8 * q + e < p.S && philox_keep_w(rnd[q], e, thr_hi);
+                km[j] |= (keep ? 1u : 0u) << (8 * q + e);
+                const float g = keep ? __uint_as_float(r[8 * q + e]) * p.drop.scale : 0.f;
+                dot += g * pf[e];
               }
             }
-          } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) mk[c / 8 + q] = 0u;
           }
         }
         red_a[part * 128 + r_local] = dot;
@@ -322,30 +340,30 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
         dot = (red_a[r_local] + red_a[128 + r_local]) + (red_a[256 + r_local] + red_a[384 + r_local]);
         // ---- pass 2: dS = P * (dP - dot) * scale -> stage -> TMA store
 #pragma unroll
-        for (int c = 0; c < Q; c += 32) {
-          if (c0 + c < p.S) {
+        for (int j = 0; j < NCH; ++j) {
+          const int c = (part + 4 * j) * 32;
+          if (c < p.S) {
             if (lane == 0) bulk_wait_read<0>();
             __syncwarp();
             uint4 pr[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q)
-              pr[q] = (row_ok && c0 + c + 8 * q < p.S)
-                          ? *reinterpret_cast<const uint4*>(prow + c0 + c + 8 * q)
-                          : make_uint4(0, 0, 0, 0);
+              pr[q] = (row_ok && c + 8 * q < p.S) ? *reinterpret_cast<const uint4*>(prow + c + 8 * q)
+                                                  : make_uint4(0, 0, 0, 0);
             uint32_t r[32];
             tmem_ld32_nowait(t_row + c, r);
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int colq = c0 + c + 8 * q;
-              const uint32_t m = mk[c / 8 + q];
+              const int colq = c + 8 * q;
               float pf[8], ds[8];
               unpack_bf16x8(pr[q], pf);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const bool in = colq + e < p.S;
-                const float g = (in && ((m >> e) & 1u)) ? __uint_as_float(r[8 * q + e]) * p.drop.scale
-                                                        : 0.f;
+                const float g = ((km[j] >> (8 * q + e)) & 1u)
+                                    ? __uint_as_float(r[8 * q + e]) * p.drop.scale
+                                    : 0.f;
                 ds[e] = in ? pf[e] * (g - dot) * p.ds_scale : 0.f;
               }
               st_shared_v4(rbase + ((q ^ sw) << 4), pack_bf16x2_(ds[0], ds[1]),
@@ -355,7 +373,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
             fence_async_shared();
             __syncwarp();
             if (lane == 0) {
-              tma_store_4d(&tmO1, wbuf, c0 + c, m0 + quarter * 32, b1, b2);
+              tma_store_4d(&tmO1, wbuf, c, m0 + quarter * 32, b1, b2);
               bulk_commit();
             }
           }

@@ -48,7 +48,8 @@ def main():
     ap.add_argument("--seq", type=int, default=288)
     ap.add_argument("--planner", default="mimose")
     ap.add_argument("--gemm-csv", default="")
-    ap.add_argument("--attn-fused", action="store_true")
+    ap.add_argument("--attn-fused", action="store_true", help="(default) fused score kernels")
+    ap.add_argument("--attn-unfused", action="store_true", help="GEMM + softmax kernel pair")
     ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
     args = ap.parse_args()
     import numpy as np
@@ -63,7 +64,8 @@ def main():
     peak = probe.rows[-1]["peak_reserved"]
     probe.close()
     budget = int(args.budget_frac * peak) if args.planner == "mimose" else int(1.2 * peak)
-    tr = Trainer(m, dataclasses.replace(t, planner=args.planner, attn_fused=args.attn_fused),
+    fused = not args.attn_unfused
+    tr = Trainer(m, dataclasses.replace(t, planner=args.planner, attn_fused=fused),
                  budget)
     lo, hi = t.seq_min, t.seq_max
     for f in [0.0, 1.0, 0.3, 0.6, 0.15, 0.9, 0.5, 0.05, 0.8, 0.4, 0.2, 0.7]:
@@ -94,7 +96,7 @@ def main():
             tr.step_device(db)
         e1.record()
         torch.cuda.synchronize()
-        print(f"seq {args.seq} attn_fused={args.attn_fused}: "
+        print(f"seq {args.seq} attn_fused={fused}: "
               f"{e0.elapsed_time(e1) / args.time_steps:.3f} ms/step (plan_size {r['plan_size']})")
     tr.close()
 
