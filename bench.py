@@ -135,7 +135,15 @@ def sizes_for(dist, batch, iters, seed):
 # ncu --set full (dram__bytes_read.sum + dram__bytes_write.sum) of one
 # representative dense-GEMM launch of the profiled step, next to that launch's
 # algorithmic bytes (operands + outputs once); source files under profiles/.
-TRAFFIC = {}
+TRAFFIC = {
+    # FFN2 forward, 18432 x 768 x 3072 (S = 288, 64 sequences), CTA-pair tile;
+    # profiles/r1b_ncu_full_fwd_summary.txt. Algorithmic = A + B read once +
+    # C written once = 146.2 MB; DRAM traffic is lower because part of the
+    # output is still dirty in the 126 MB L2 when the kernel ends: no re-reads.
+    "bert-base-mc": {"dram_bytes": 132.4e6, "algorithmic_bytes": 146.2e6,
+                     "launch": "gemm_bf16_tn_kernel<256,0,8,2> FFN2 fwd M=18432 N=768 K=3072",
+                     "source": "profiles/r1b_ncu_full_fwd_summary.txt"},
+}
 
 
 def peaks():
