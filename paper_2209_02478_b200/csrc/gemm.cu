@@ -249,6 +249,20 @@ int pick_bn(const GemmCall& c) {
   // column chunks, so padding costs only idle MMA slots)
   const int64_t t256 = tm * ((c.N + 255) / 256) * batches;
   if (c.N > 128 && t256 >= 2 * sm_count()) return 256;
+  // light-epilogue unbatched GEMMs run 256-wide tiles on CTA pairs (see
+  // pick_cg): take them whenever the pair grid is not clearly worse-filled
+  // than the 128-wide single-SM grid (pair tiles are ~1.3x faster per flop)
+  if (c.N > 128 && batches == 1 && c.M > 128 && c.epi != kEpiBiasGelu && c.epi != kEpiDGelu &&
+      c.force_cg != 1) {
+    const int64_t pairs = sm_count() / 2;
+    const int64_t tp = ((c.M + 255) / 256) * ((c.N + 255) / 256);
+    const int64_t t128 = tm * ((c.N + 127) / 128);
+    auto eff = [](int64_t t, int64_t slots) {
+      const int64_t w = (t + slots - 1) / slots;
+      return (double)t / (double)(w * slots);
+    };
+    if (1.3 * eff(tp, pairs) >= eff(t128, sm_count())) return 256;
+  }
   return 128;
 }
 
@@ -286,11 +300,6 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
   }
 }
 
-// wave efficiency of `tiles` work units on `slots` resident CTAs (or pairs)
-double wave_eff(int64_t tiles, int64_t slots) {
-  const int64_t waves = (tiles + slots - 1) / slots;
-  return (double)tiles / (double)(waves * slots);
-}
 
 }  // namespace
 
@@ -304,18 +313,28 @@ bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, in
   return make_map_t(map, ptr, rows, cols, ld, bs1, bs2, nb1, nb2, box_cols, 32, 2, sw64);
 }
 
+// split-K count by a small cost model: mainloop time ~ waves * k-blocks per
+// split (one k-block of a 128x256 tile or a 256x256 pair tile ~ 512 tensor
+// cycles ~ 0.27 us), plus writing and re-reading the fp32 partials at HBM
+// speed. Keeps >= 8 k-blocks per split.
 int pick_split_k(int M, int N, int K, int bn, int cg) {
   const int64_t tiles = (int64_t)((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
   const int64_t slots = sm_count() / cg;
   const int kb = (K + 63) / 64;
+  const double t_kb = 0.27e-6 * bn / 256.0, hbm = 6.0e12;
+  auto cost = [&](int s) {
+    const int64_t waves = (tiles * s + slots - 1) / slots;
+    const double main = (double)waves * ((kb + s - 1) / s) * t_kb;
+    return main + (s > 1 ? (double)s * M * N * 8.0 / hbm : 0.0);
+  };
   int best = 1;
-  double best_eff = wave_eff(tiles, slots);
+  double best_cost = cost(1);
   for (int s = 2; s <= 8; ++s) {
     if (kb / s < 8) break;  // keep >= 8 k-blocks per split
-    const double e = wave_eff(tiles * s, slots);
-    if (e > best_eff + 0.05) {
+    const double c = cost(s);
+    if (c < 0.97 * best_cost) {
       best = s;
-      best_eff = e;
+      best_cost = c;
     }
   }
   return best;

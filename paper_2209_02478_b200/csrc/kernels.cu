@@ -1068,10 +1068,11 @@ int persistent_blocks() {
 }
 }  // namespace
 
-// blocks of the LayerNorm backward: >= ~4 rows per row group, at most two
-// blocks per SM; a function of `rows` only (deterministic partial layout)
+// blocks of the LayerNorm backward: enough to fill two blocks per SM even for
+// small token counts (GPT-2 at short S), at most two per SM; a function of
+// `rows` only (deterministic partial layout)
 int ln_bwd_blocks(int rows) {
-  const int want = (rows + 31) / 32;
+  const int want = (rows + 7) / 8;
   const int cap = 2 * persistent_blocks();
   return want < 1 ? 1 : (want < cap ? want : cap);
 }
@@ -1162,8 +1163,8 @@ cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float
 }
 
 int colsum_row_blocks(int rows) {
-  const int want = (rows + 63) / 64;
-  return want < 64 ? (want < 1 ? 1 : want) : 64;
+  const int want = (rows + 31) / 32;
+  return want < 128 ? (want < 1 ? 1 : want) : 128;
 }
 
 cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <set>
@@ -582,7 +583,11 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   void* Pm = take(quad, act_tag);
   void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  if (fused_attn(S)) {
+  static const int fwd_max = [] {
+    const char* e = std::getenv("MIMOSE_ATTN_FWD_MAX");
+    return e != nullptr ? std::atoi(e) : 512;
+  }();
+  if (fused_attn(S) && S <= fwd_max) {
     // fused: scores stay in TMEM, softmax + dropout in the epilogue
     ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, s),

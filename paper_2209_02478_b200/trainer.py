@@ -115,7 +115,7 @@ PRESETS = {
 # already ~40 % of the no-checkpoint peak, so 40 % is infeasible.
 PRESET_INFO = {
     "small4-h256": ("small BERT-like encoder L4 H256 A4 F1024, MC head, B=8 (BASELINE configs[0])",
-                    "uniform:32:256", 0.75),
+                    "uniform:32:256", 0.8),
     "bert-base-mc": ("bert-base-mc: BERT-base (L12 H768 A12 F3072 V30522) multiple-choice "
                      "fine-tune, SWAG-shaped 16x4 choices (BASELINE configs[1])",
                      "uniform:64:512", 0.4),
