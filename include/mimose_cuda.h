@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 2
+#define MIMOSE_ABI_VERSION 3
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
@@ -166,6 +166,8 @@ typedef struct {
   int estimator_order;         /* harness.hpp:53 */
   float lr, beta1, beta2, adam_eps, weight_decay, max_grad_norm;
   int attn_fused;              /* 1: fused score+softmax kernels (S <= 512); 0: GEMM + softmax kernels */
+  int reserve_per_size;        /* automatic reserve: 1 = extras at this step's S + margin (the
+                                  planner then keeps more blocks for short inputs), 0 = at seq_max */
 } mimose_train_cfg;
 
 enum {
@@ -197,6 +199,7 @@ typedef struct {
   double pred_err_max;
   int pred_layers;             /* kept blocks the error was measured on */
   double host_ms;              /* host wall time spent issuing this step's work */
+  int64_t reserve_bytes;       /* scheduler reserve the plan was generated with */
 } mimose_step_report;
 
 typedef void (*mimose_grad_hook)(void* user, float* grads, int64_t n, void* stream);

@@ -89,7 +89,7 @@ class TrainCfg(C.Structure):
         ("estimator_order", C.c_int),
         ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
         ("weight_decay", C.c_float), ("max_grad_norm", C.c_float),
-        ("attn_fused", C.c_int),
+        ("attn_fused", C.c_int), ("reserve_per_size", C.c_int),
     ]
 
 
@@ -103,7 +103,7 @@ class StepReport(C.Structure):
         ("plan_us", C.c_double), ("fit_us", C.c_double),
         ("dropped_mask_lo", C.c_uint64),
         ("pred_err_mean", C.c_double), ("pred_err_max", C.c_double), ("pred_layers", C.c_int),
-        ("host_ms", C.c_double),
+        ("host_ms", C.c_double), ("reserve_bytes", C.c_int64),
     ]
 
     def as_dict(self):
@@ -186,7 +186,7 @@ CUDA_SYMBOLS = [
       C.POINTER(C.c_int)]),
 ]
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 def _bind(lib, symbols):

@@ -1008,8 +1008,19 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
     trained_ = true;
   }
   if (ccfg_.collect_new_sizes_always && unseen) return Mode::Collect;
+  // reserve for this input size: the transients outside the planned blocks
+  // (inputs, head, retained boundaries, one block's backward workspace) scale
+  // with S, so sizing them at S_max would over-checkpoint short inputs. The
+  // plan cache is keyed by x, so each entry is consistent with its reserve.
+  mimose::SchedulerConfig sc = sched_;
+  if (t_.reserve_bytes < 0 && t_.reserve_per_size) {
+    const int64_t S = x / t_.batch;
+    sc.reserve_bytes = std::min<int64_t>(extras_bytes(S) + sched_.budget_bytes / 50,
+                                         sched_.budget_bytes - 1);
+  }
+  rep->reserve_bytes = sc.effective_reserve();
   const auto t0 = std::chrono::steady_clock::now();
-  auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, x, sched_);
+  auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, x, sc);
   const auto t1 = std::chrono::steady_clock::now();
   rep->plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   if (!hit) {

@@ -74,6 +74,9 @@ class TrainConfig:
     # scores never reach HBM. Full BERT-base step, B = 64: 0.6 % slower at
     # S = 128, 1.7-4.6 % faster for S >= 256 (profiles/README.md) -> default.
     attn_fused: bool = True
+    # automatic reserve sized for each step's S (extras_bytes(S) + 2 %) instead
+    # of seq_max: short inputs then keep more blocks (fewer recomputes)
+    reserve_per_size: int = 1
 
     def to_c(self):
         c = _lib.TrainCfg()

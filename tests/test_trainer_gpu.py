@@ -207,7 +207,8 @@ def test_repeated_steps_train_and_are_deterministic(cuda_device):
     assert all(math.isfinite(x) for x in losses[0])
 
 
-def test_mimose_phases_budget_and_plan_parity(cuda_device):
+@pytest.mark.parametrize("per_size", [1, 0])
+def test_mimose_phases_budget_and_plan_parity(cuda_device, per_size):
     """Sheltered collection -> fit -> responsive plans; never over budget;
     GPU plans bit-identical to the host planner fed the GPU's own samples."""
     from paper_2209_02478_b200 import planner as host
@@ -226,7 +227,7 @@ def test_mimose_phases_budget_and_plan_parity(cuda_device):
     peak_none = rep["peak_reserved"]
     probe.close()
     budget = int(0.6 * peak_none)
-    tr = make("mimose", budget, max_sheltered_iters=4)
+    tr = make("mimose", budget, max_sheltered_iters=4, reserve_per_size=per_size)
     seqs = [32, 100, 256, 180, 100, 256, 200, 32, 150, 256, 77, 133, 256, 180, 240]
     rows = [tr.step(*synthetic_batch(rng, B, s, TINY["vocab"], 4)) for s in seqs]
     st = tr.mem_stats()
@@ -245,13 +246,21 @@ def test_mimose_phases_budget_and_plan_parity(cuda_device):
     assert est_text == tr.estimator_text()
     planned = [r for r in rows if r["phase_name"] == "planned"]
     info = tr.info()
-    cfg = host.SchedCfg(budget_bytes=info["budget"], reserve_bytes=info["reserve_bytes"])
-    masks, insuff, hits = host.plan_sequence(est_text, tr.model_text(), cfg,
-                                             [r["x"] for r in planned], tr.model.layers)
-    for r, m, i, h in zip(planned, masks, insuff, hits):
+    # the reserve is sized per input (extras at this step's S): replay each
+    # planned step on the host with the reserve it was planned with; the
+    # cache is keyed by x (tolerance 0), so a repeated x must be a hit
+    seen = set()
+    for r in planned:
+        assert 0 < r["reserve_bytes"] <= info["reserve_bytes"]
+        if not per_size:
+            assert r["reserve_bytes"] == info["reserve_bytes"]
+        cfg = host.SchedCfg(budget_bytes=info["budget"], reserve_bytes=r["reserve_bytes"])
+        (m,), (i,), _ = host.plan_sequence(est_text, tr.model_text(), cfg, [r["x"]],
+                                           tr.model.layers)
         assert r["dropped_mask_lo"] == m
         assert r["insufficient"] == i
-        assert r["cache_hit"] == h
+        assert r["cache_hit"] == (r["x"] in seen)
+        seen.add(r["x"])
     # the run through the reference's own report writers (harness.hpp:339-379)
     summary, csv = tr.report()
     lines = csv.strip().splitlines()
