@@ -417,9 +417,13 @@ void Trainer::build_params() {
   ck(cudaMemcpy(decay_chunk_, chunk.data(), chunk.size(), cudaMemcpyHostToDevice), "memcpy");
 }
 
-bool Trainer::fused_attn(int S) const {
-  // the fused score kernels have no causal mask: causal models use the pair
-  return t_.attn_fused && !m_.causal && mimose_ops::attn_fused_supported(S);
+// attn_fused: 0 = QK^T GEMM + softmax kernels; 1 = block-looped fused score
+// kernels (attn2_sm100.cuh: any S <= 2048, causal too); 2 = single-row fused
+// kernels (attn_sm100.cuh: bidirectional, S <= 512)
+int Trainer::fused_attn(int S) const {
+  if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
+  if (t_.attn_fused == 2 && !m_.causal && mimose_ops::attn_fused_supported(S)) return 2;
+  return 0;
 }
 
 void Trainer::init_params(cudaStream_t s) {
@@ -493,7 +497,8 @@ int64_t Trainer::block_work_bytes(int S) const {
   // post-LN: dy, dz2, df, du | dz1, da, dctx, dx, dP, dqkv
   // pre-LN:  dy, df, du, dh1, da, dx2 | dh1, da, dctx, dP, dqkv, dx, dx1
   const int64_t s1 = act * (pre ? 5 : 3) + 2 * T * F;
-  const int64_t s2 = act * (pre ? 5 : 4) + quad + 2 * T * 3 * H;
+  // (+ act: the block-looped attention backward keeps ctx until dS is done)
+  const int64_t s2 = act * (pre ? 6 : 5) + quad + 2 * T * 3 * H;
   return std::max(s1, s2);
 }
 
@@ -587,8 +592,14 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
     const char* e = std::getenv("MIMOSE_ATTN_FWD_MAX");
     return e != nullptr ? std::atoi(e) : 512;
   }();
-  if (fused_attn(S) && S <= fwd_max) {
-    // fused: scores stay in TMEM, softmax + dropout in the epilogue
+  const int fused = S <= fwd_max ? fused_attn(S) : 0;
+  if (fused == 1) {
+    // fused, block-looped: scores stay in TMEM, softmax + dropout in the epilogue
+    ck(mimose_ops::attn2_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
+                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, m_.causal != 0, s),
+       "attn2_scores_fwd");
+  } else if (fused == 2) {
+    // fused, whole key row in TMEM
     ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, s),
        "attn_scores_fwd");
@@ -649,10 +660,16 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
     c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
     run_gemm(c, s);
   }
+  const int fused = fused_attn(S);
   drop(sv.Pd);
   void* dP = take(quad, kTagTransient);
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  if (fused_attn(S)) {
+  if (fused == 1) {
+    ck(mimose_ops::attn2_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
+                                    sv.ctx, sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop,
+                                    m_.causal != 0, s),
+       "attn2_scores_bwd");
+  } else if (fused == 2) {
     // fused: dPd stays in TMEM; softmax backward in the epilogue writes dS
     ck(mimose_ops::attn_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
                                    sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop, s),
@@ -894,11 +911,12 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   void* dap = da ? da : dh1;
   // output projection: dWo = da^T ctx ; dctx = da Wo
   run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
-  drop(sv.ctx);
+  if (fused_attn(g.S) != 1) drop(sv.ctx);  // else attn_bwd reads it (rowsum(dP o P) = dO . ctx)
   void* dctx = take(T * H * 2, kTagTransient);
   run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
   drop(da);
   void* dqkv = attn_bwd(l, sv, dctx, g, s);
+  if (fused_attn(g.S) == 1) drop(sv.ctx);
   // QKV projection: dbqkv, dWqkv = dqkv^T xin
   ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
      "colsum");

@@ -70,10 +70,13 @@ class TrainConfig:
     adam_eps: float = 1e-8
     weight_decay: float = 0.01
     max_grad_norm: float = 1.0
-    # fused score+softmax kernels (attn_sm100.cuh, bidirectional S <= 512):
-    # scores never reach HBM. Full BERT-base step, B = 64: 0.6 % slower at
-    # S = 128, 1.7-4.6 % faster for S >= 256 (profiles/README.md) -> default.
-    attn_fused: bool = True
+    # attention scores: 2 = single-row fused kernels (attn_sm100.cuh: the key
+    # row of a 128-query tile in TMEM, softmax / dropout / softmax-backward in
+    # the epilogue; bidirectional S <= 512, else the pair below); 1 =
+    # block-looped fused kernels (attn2_sm100.cuh: any S <= 2048, causal too;
+    # correct but slower than both others today - profiles/README.md);
+    # 0 = QK^T GEMM + softmax kernels
+    attn_fused: int = 2
     # automatic reserve sized for each step's S (extras_bytes(S) + 2 %) instead
     # of seq_max: short inputs then keep more blocks (fewer recomputes)
     reserve_per_size: int = 1

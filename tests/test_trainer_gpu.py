@@ -53,7 +53,7 @@ def _grads_by_name(tr):
     return {name: g[off:off + n].copy() for name, (off, n) in tr.param_table().items()}
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [16, 45, 96])
 def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
@@ -175,7 +175,7 @@ def test_variant_device_inputs_match_host(cuda_device, variant):
     assert torch.equal(out[0][1], out[1][1])
 
 
-@pytest.mark.parametrize("fused", [False, True])
+@pytest.mark.parametrize("fused", [0, 1, 2])
 def test_checkpointed_grads_bitwise_equal_plain(cuda_device, fused):
     """Recompute is deterministic: dropping any subset of blocks gives the
     exact same gradients (dropout on, so Philox regeneration is exercised)."""
@@ -341,3 +341,52 @@ def test_native_dp_world1_bucketed_allreduce_is_identity(cuda_device):
             dp.close()
     assert runs[0][0] == runs[1][0]
     assert torch.equal(runs[0][1], runs[1][1])
+
+
+# Block-looped fused attention (attn2_sm100.cuh) walks keys in 256-column
+# blocks: S > 256 exercises the online max / sum across blocks, S > 512 the
+# sequences the single-row kernel cannot hold, causal the masked blocks.
+LONG = dict(TINY, layers=1, max_pos=640)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("dropout", [0.0, 0.1])
+@pytest.mark.parametrize("S", [300, 520])
+def test_long_sequence_attention_vs_cpu_oracle(cuda_device, S, dropout, causal, mode):
+    from oracle import bert_ref
+    shape = dict(LONG, type_vocab=0, arch=1, head=2, causal=1, gelu_tanh=1) if causal else LONG
+    m = ModelConfig(hidden_dropout=dropout, attn_dropout=dropout, seed=91, **shape)
+    t = TrainConfig(planner="none", batch=4, seq_min=S, seq_max=S, attn_fused=mode)
+    tr = Trainer(m, t, 4 * GiB)
+    rng = np.random.default_rng(31)
+    tok, typ, lab = synthetic_task_batch(rng, tr.model, 4, S)
+    params = _oracle_params(tr)
+    rep = tr.step(tok, typ, lab, optimizer=False)
+    ref_loss, _, ref_grads = bert_ref.loss_and_grads(params, tok, typ, lab, tr.model, step=0)
+    assert math.isfinite(rep["loss"])
+    assert abs(rep["loss"] - ref_loss) <= 2e-2 * max(1.0, abs(ref_loss)), (rep["loss"], ref_loss)
+    _check_grads(_grads_by_name(tr), ref_grads)
+    tr.close()
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("causal", [False, True])
+def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode):
+    """Recompute through the block-looped kernels is bit-exact at S > 512."""
+    shape = dict(LONG, layers=2, type_vocab=0, arch=1, head=2, causal=1, gelu_tanh=1) if causal \
+        else dict(LONG, layers=2)
+    S = 600
+    grads = []
+    for forced in ([], [0, 1]):
+        m = ModelConfig(hidden_dropout=0.1, attn_dropout=0.1, seed=92, **shape)
+        t = TrainConfig(planner="none", batch=4, seq_min=S, seq_max=S, attn_fused=mode)
+        tr = Trainer(m, t, 4 * GiB)
+        tok, typ, lab = synthetic_task_batch(np.random.default_rng(7), tr.model, 4, S)
+        tr.force_plan(forced)
+        rep = tr.step(tok, typ, lab, optimizer=False)
+        torch.cuda.synchronize()
+        grads.append((rep["loss"], tr.grads().clone()))
+        tr.close()
+    assert grads[0][0] == grads[1][0]
+    assert torch.equal(grads[0][1], grads[1][1])

@@ -50,6 +50,8 @@ def main():
     ap.add_argument("--gemm-csv", default="")
     ap.add_argument("--attn-fused", action="store_true", help="(default) fused score kernels")
     ap.add_argument("--attn-unfused", action="store_true", help="GEMM + softmax kernel pair")
+    ap.add_argument("--attn-mode", type=int, default=2,
+                    help="TrainConfig.attn_fused when fused: 2 single-row, 1 block-looped")
     ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
     args = ap.parse_args()
     import numpy as np
@@ -64,7 +66,7 @@ def main():
     peak = probe.rows[-1]["peak_reserved"]
     probe.close()
     budget = int(args.budget_frac * peak) if args.planner == "mimose" else int(1.2 * peak)
-    fused = not args.attn_unfused
+    fused = 0 if args.attn_unfused else args.attn_mode
     tr = Trainer(m, dataclasses.replace(t, planner=args.planner, attn_fused=fused),
                  budget)
     lo, hi = t.seq_min, t.seq_max
