@@ -36,7 +36,18 @@ cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap
   }
   const int tiles = ((p.S + 127) / 128) * p.nh * p.B;
   const int grid = tiles < attn_sm_count() ? tiles : attn_sm_count();
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(a, b, o1, o2, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, o1, o2, p);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }
@@ -55,7 +66,18 @@ cudaError_t launch2(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMa
   }
   const int tiles = ((p.S + 127) / 128) * p.nh * p.B;
   const int grid = tiles < attn_sm_count() ? tiles : attn_sm_count();
-  kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, s>>>(a, b, o1, o2, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, o1, o2, p);
+  if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
 }

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(Attn2Cfg::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // inputs of this launch are complete from here on
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer

@@ -29,6 +29,19 @@ using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, voi
 
 std::atomic<uint64_t> g_launches{0};
 
+}  // namespace
+
+// PDL for the tcgen05 kernels (MIMOSE_PDL=0 disables, for A/B timing)
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MIMOSE_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+namespace {
+
 
 EncodeFn encode_fn() {
   static EncodeFn fn = [] {
@@ -145,25 +158,31 @@ cudaError_t launch_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtenso
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  if constexpr (CG == 1) {
-    kern<<<grid, Cfg::kThreads, Cfg::kSmemBytes, stream>>>(ta, tb, td, td2, p);
-  } else {
-    // CTA pairs: cluster (2, 1, 1), `grid` counts CTAs (2 per pair tile slot)
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(Cfg::kThreads);
-    cfg.dynamicSmemBytes = Cfg::kSmemBytes;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, td2, p);
-    if (e != cudaSuccess) return e;
+  // programmatic dependent launch (the kernel calls pdl_wait() before its
+  // first dependent access) + cluster (2, 1, 1) for CTA pairs; `grid` counts CTAs
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmemBytes;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
+  if constexpr (CG > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CG;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, td, td2, p);
+  if (e != cudaSuccess) return e;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -52,6 +52,8 @@ struct GemmCall {
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);
+// programmatic dependent launch for the tcgen05 kernels (env MIMOSE_PDL=0 off)
+bool pdl_enabled();
 // split-K choice for an fp32 (weight-gradient) GEMM and the workspace it needs
 int pick_split_k(int M, int N, int K, int bn, int cg = 1);
 int64_t splitk_workspace_bytes(int M, int N, int K);

@@ -109,6 +109,15 @@ __device__ __forceinline__ void fence_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start (barrier init,
+// TMEM alloc, tensor-map prefetch) while the previous kernel drains; it must
+// wait here before touching anything that kernel produced.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- CTA pair
 // (cta_group::2: two SMs of one TPC run one 256-row MMA tile; the leader,
 // cluster rank 0, issues every tcgen05.mma / commit)
