@@ -258,6 +258,13 @@ int pick_ew(const GemmCall& c, int bn) {
 
 int pick_bn(const GemmCall& c) {
   if (c.force_bn) return c.force_bn;
+  if (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) {  // A/B knob for the GELU epilogues
+    static const int gelu_bn = [] {
+      const char* e = std::getenv("MIMOSE_GELU_BN");
+      return e != nullptr ? std::atoi(e) : 0;
+    }();
+    if (gelu_bn == 128 || gelu_bn == 256) return gelu_bn;
+  }
   if (c.N <= 64) return 64;
   const int64_t batches = (int64_t)c.nb1 * c.nb2;
   const int64_t tm = (c.M + 127) / 128;

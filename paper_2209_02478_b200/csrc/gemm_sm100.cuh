@@ -92,11 +92,14 @@ struct GemmCfg {
   // per epilogue warp: kBufs sets of kNOut buffers of 32 rows x kChunkBytes
   static constexpr int kBufs = 1;  // 2 measured: attention unchanged, dense -4 %
   static constexpr int kStagingBytes = EW * kBufs * kNOut * kBufBytes;
-  static constexpr int kBiasBytes = 2 * BN * 4;  // tile bias slice, per accumulator stage
+  // TMEM accumulators: as many BN-column tiles as fit 512 columns (max 4), so
+  // the MMA can run up to kAcc - 1 tiles ahead of the epilogue
+  static constexpr int kAcc = (512 / BN) > 4 ? 4 : (512 / BN);
+  static constexpr int kBiasBytes = kAcc * BN * 4;  // tile bias slice, per accumulator
   static constexpr int kStagesRaw =
       (kSmemBudget - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr int kTmemCols = kAcc * BN;
   static constexpr int kSmemBytes =
       kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 256;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
@@ -308,12 +311,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
   uint8_t* sD = smem + S * Cfg::kStageBytes;  // epilogue staging (1024-aligned)
-  float* sBias = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [2][BN]
+  float* sBias = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [kAcc][BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes + Cfg::kBiasBytes);
   uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tfull = empty + S;             // [kAcc]
+  uint64_t* tempty = tfull + Cfg::kAcc;    // [kAcc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + Cfg::kAcc);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < Cfg::kAcc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);  // one arrive per epilogue warp (of both CTAs)
     }
@@ -428,8 +431,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
     int it = 0, local = 0;
     for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++local) {
-      const int acc = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
+      const int acc = local % Cfg::kAcc;
+      const uint32_t aph = (local / Cfg::kAcc) & 1;
       const int split = (tile / tiles_per_batch) % p.splits;
       const int kb_n = min(num_kb, (split + 1) * p.kb_per_split) - split * p.kb_per_split;
       mbar_wait(&tempty[acc], aph ^ 1);
@@ -482,8 +485,8 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       // split-K partials are addressed as batch index b1 = split of the workspace
       const int b1 = p.splits > 1 ? split : z % p.nb1;
       const int b2 = p.splits > 1 ? 0 : z / p.nb1;
-      const int acc = local & 1;
-      const uint32_t aph = (local >> 1) & 1;
+      const int acc = local % Cfg::kAcc;
+      const uint32_t aph = (local / Cfg::kAcc) & 1;
       // stage this tile's bias slice once (all 8 epilogue warps, then a named
       // barrier); double-buffered by accumulator stage
       float* tb = nullptr;
