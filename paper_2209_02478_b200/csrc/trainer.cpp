@@ -486,20 +486,58 @@ int64_t Trainer::head_bytes(int S) const {
   return head + 64 * 1024;
 }
 
-// Worst live set of one block's backward outside its saved tensors (mirrors
-// the allocation order of layer_bwd / attn_bwd).
+// Worst extra live set of one block's backward: transients allocated minus
+// saved tensors already released, replayed in layer_bwd / attn_bwd's exact
+// allocation order (a saved tensor freed early is reused by later transients,
+// so summing every transient would over-reserve by ~3x at S = 512). Also
+// covers the forward's transient score buffer of the unfused attention path.
 int64_t Trainer::block_work_bytes(int S) const {
   const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
   const int64_t ld = round8(S);
   const int64_t quad = B * nh_ * (int64_t)S * ld * 2;
-  const int64_t act = 2 * T * H;
+  const int64_t act = 2 * T * H, fact = 2 * T * F, qkv3 = 2 * T * 3 * H, st = 8 * T;
   const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
-  // post-LN: dy, dz2, df, du | dz1, da, dctx, dx, dP, dqkv
-  // pre-LN:  dy, df, du, dh1, da, dx2 | dh1, da, dctx, dP, dqkv, dx, dx1
-  const int64_t s1 = act * (pre ? 5 : 3) + 2 * T * F;
-  // (+ act: the block-looped attention backward keeps ctx until dS is done)
-  const int64_t s2 = act * (pre ? 6 : 5) + quad + 2 * T * 3 * H;
-  return std::max(s1, s2);
+  const bool hid = m_.hidden_dropout > 0.f;
+  const int64_t pd = m_.attn_dropout > 0.f ? quad : 0;
+  const int fused = fused_attn(S);
+  int64_t live = act, peak = act;  // dy
+  auto take_b = [&](int64_t n) { live += n; peak = std::max(peak, live); };
+  auto drop_b = [&](int64_t n) { live -= n; };
+  if (pre) {
+    if (hid) take_b(act);                       // df
+    drop_b(fact); take_b(fact);                 // g -> du
+    if (hid) drop_b(act);                       // df
+    drop_b(fact); drop_b(act);                  // u, z2 (x2)
+    take_b(act); if (hid) take_b(act);          // dh1, da
+    take_b(act);                                // dx2
+    drop_b(fact); drop_b(act); drop_b(act);     // du, dx2, dy
+    drop_b(act); drop_b(st);                    // h1, st2
+  } else {
+    take_b(act); if (hid) take_b(act);          // dres (dz2), df
+    drop_b(act); drop_b(act); drop_b(st);       // dy, z2, st2
+    drop_b(fact); take_b(fact);                 // g -> du
+    if (hid) drop_b(act);                       // df
+    drop_b(fact); drop_b(act);                  // u, h1 (x2)
+    take_b(act); if (hid) take_b(act);          // dh1, da
+    drop_b(fact); drop_b(act);                  // du, dres
+    take_b(act);                                // dz1
+    drop_b(act); drop_b(act); drop_b(st);       // dh1, z1, st1
+  }
+  if (fused != 1) drop_b(act);                  // ctx
+  take_b(act);                                  // dctx
+  if (hid) drop_b(act);                         // da
+  take_b(qkv3);                                 // dqkv
+  if (fused != 1) drop_b(pd);                   // Pd
+  take_b(quad);                                 // dP
+  if (fused == 1) drop_b(pd);
+  drop_b(act); drop_b(quad);                    // dctx, P
+  drop_b(quad); drop_b(qkv3);                   // dP, qkv
+  if (fused == 1) drop_b(act);                  // ctx
+  take_b(act);                                  // dx
+  if (pre) take_b(act);                         // dx1
+  // forward: the unfused path's score buffer lives next to the block's saves
+  const int64_t fwd = fused ? 0 : quad;
+  return std::max(peak, fwd);
 }
 
 int64_t Trainer::extras_bytes(int S) const {
@@ -547,7 +585,7 @@ void Trainer::build_spec() {
 
   sched_ = mimose::SchedulerConfig{};
   sched_.budget_bytes = ctx_->arena.stats().budget;
-  const int64_t margin = sched_.budget_bytes / 50;  // 2% fragmentation margin
+  const int64_t margin = sched_.budget_bytes * 3 / 100;  // 3% fragmentation margin
   sched_.reserve_bytes = t_.reserve_bytes >= 0 ? t_.reserve_bytes : extras_bytes(t_.seq_max) + margin;
   if (sched_.reserve_bytes >= sched_.budget_bytes) sched_.reserve_bytes = sched_.budget_bytes - 1;
   sched_.bucket_tolerance = t_.bucket_tolerance;
@@ -1033,7 +1071,7 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
   mimose::SchedulerConfig sc = sched_;
   if (t_.reserve_bytes < 0 && t_.reserve_per_size) {
     const int64_t S = x / t_.batch;
-    sc.reserve_bytes = std::min<int64_t>(extras_bytes(S) + sched_.budget_bytes / 50,
+    sc.reserve_bytes = std::min<int64_t>(extras_bytes(S) + sched_.budget_bytes * 3 / 100,
                                          sched_.budget_bytes - 1);
   }
   rep->reserve_bytes = sc.effective_reserve();
