@@ -88,7 +88,7 @@ bool attn_fused_supported(int S) { return S >= 1 && S <= 512; }
 
 cudaError_t attn_scores_fwd(const MatView& q, const MatView& k, void* P, void* Pd, int S, int ld,
                             int nh, int B, float alpha, const mimose_dev::DropoutCfg& drop,
-                            cudaStream_t s) {
+                            cudaStream_t s, bool causal) {
   if (!attn_fused_supported(S)) return cudaErrorInvalidValue;
   const double nz = (double)nh * B;
   // Q, K read; P (+ Pd) written
@@ -108,6 +108,7 @@ cudaError_t attn_scores_fwd(const MatView& q, const MatView& k, void* P, void* P
   p.alpha = alpha;
   p.drop = drop;
   p.store_pd = Pd != nullptr;
+  p.causal = causal ? 1 : 0;
   return S <= 256 ? launch<256, false>(ta, tb, t1, t2, p, s) : launch<512, false>(ta, tb, t1, t2, p, s);
 }
 

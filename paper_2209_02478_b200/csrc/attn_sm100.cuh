@@ -36,6 +36,8 @@ struct AttnParams {
   DropoutCfg drop;
   const __nv_bfloat16* P;     // bwd: saved probabilities [B][nh][S][ld]
   int store_pd;               // fwd: also store the dropped-out probabilities
+  int causal;                 // fwd: keys j > query i masked (P = 0 there, so the
+                              // backward needs no mask: dS = P * (...) = 0)
 };
 
 template <int NC>
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
       const uint32_t thr_hi = p.drop.threshold << 16;
 
       if constexpr (!BWD) {
+        const int jmax = p.causal ? min(p.S, i + 1) : p.S;  // valid keys of this row
         // ---- pass 1: row max of the raw scores (alpha > 0 commutes with max)
         const float sc = p.alpha * kLog2e;
         float mx = -INFINITY;
@@ -220,13 +223,13 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
           uint32_t r[32];
           tmem_ld32_nowait(t_row + c, r);
           tmem_wait_ld();
-          if (c + 32 <= p.S) {
+          if (c + 32 <= jmax) {
 #pragma unroll
             for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(r[e]));
           } else {
 #pragma unroll
             for (int e = 0; e < 32; ++e)
-              if (c + e < p.S) mx = fmaxf(mx, __uint_as_float(r[e]));
+              if (c + e < jmax) mx = fmaxf(mx, __uint_as_float(r[e]));
           }
         }
         red_a[part * 128 + r_local] = mx * sc;
@@ -244,7 +247,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const float x = c + e < p.S ? ex2f(fmaf(__uint_as_float(r[e]), sc, nmx)) : 0.f;
+            const float x = c + e < jmax ? ex2f(fmaf(__uint_as_float(r[e]), sc, nmx)) : 0.f;
             sum += x;
             r[e] = __float_as_uint(x);
           }

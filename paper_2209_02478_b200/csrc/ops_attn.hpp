@@ -22,9 +22,10 @@ bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, in
 
 bool attn_fused_supported(int S);
 // P = softmax(alpha * Q K^T), Pd = dropout(P) (Pd may be null when p = 0)
+// (causal: keys j > query i get P = 0)
 cudaError_t attn_scores_fwd(const MatView& q, const MatView& k, void* P, void* Pd, int S, int ld,
                             int nh, int B, float alpha, const mimose_dev::DropoutCfg& drop,
-                            cudaStream_t s);
+                            cudaStream_t s, bool causal = false);
 // dS = P * (dP - rowsum(dP * P)) * ds_scale with dP = dropout'(dO V^T)
 cudaError_t attn_scores_bwd(const MatView& dout, const MatView& v, const void* P, void* dS, int S,
                             int ld, int nh, int B, float ds_scale,

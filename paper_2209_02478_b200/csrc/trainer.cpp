@@ -419,10 +419,10 @@ void Trainer::build_params() {
 
 // attn_fused: 0 = QK^T GEMM + softmax kernels; 1 = block-looped fused score
 // kernels (attn2_sm100.cuh: any S <= 2048, causal too); 2 = single-row fused
-// kernels (attn_sm100.cuh: bidirectional, S <= 512)
+// kernels (attn_sm100.cuh: S <= 512, causal too)
 int Trainer::fused_attn(int S) const {
   if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
-  if (t_.attn_fused == 2 && !m_.causal && mimose_ops::attn_fused_supported(S)) return 2;
+  if (t_.attn_fused == 2 && mimose_ops::attn_fused_supported(S)) return 2;
   return 0;
 }
 
@@ -639,7 +639,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   } else if (fused == 2) {
     // fused, whole key row in TMEM
     ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
-                                   Pd, S, ld, nh, g.B, 0.125f, pdrop, s),
+                                   Pd, S, ld, nh, g.B, 0.125f, pdrop, s, m_.causal != 0),
        "attn_scores_fwd");
   } else {
     // scores = q k^T / sqrt(64), batched over (head, sequence); then softmax

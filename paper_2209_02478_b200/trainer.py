@@ -72,7 +72,7 @@ class TrainConfig:
     max_grad_norm: float = 1.0
     # attention scores: 2 = single-row fused kernels (attn_sm100.cuh: the key
     # row of a 128-query tile in TMEM, softmax / dropout / softmax-backward in
-    # the epilogue; bidirectional S <= 512, else the pair below); 1 =
+    # the epilogue; S <= 512, causal too, else the pair below); 1 =
     # block-looped fused kernels (attn2_sm100.cuh: any S <= 2048, causal too;
     # correct but slower than both others today - profiles/README.md);
     # 0 = QK^T GEMM + softmax kernels

@@ -370,13 +370,13 @@ def test_long_sequence_attention_vs_cpu_oracle(cuda_device, S, dropout, causal, 
     tr.close()
 
 
+@pytest.mark.parametrize("S", [300, 600])
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("causal", [False, True])
-def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode):
+def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode, S):
     """Recompute through the block-looped kernels is bit-exact at S > 512."""
     shape = dict(LONG, layers=2, type_vocab=0, arch=1, head=2, causal=1, gelu_tanh=1) if causal \
         else dict(LONG, layers=2)
-    S = 600
     grads = []
     for forced in ([], [0, 1]):
         m = ModelConfig(hidden_dropout=0.1, attn_dropout=0.1, seed=92, **shape)
