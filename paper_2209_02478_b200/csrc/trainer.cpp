@@ -420,6 +420,21 @@ void Trainer::build_params() {
 // attn_fused: 0 = QK^T GEMM + softmax kernels; 1 = block-looped fused score
 // kernels (attn2_sm100.cuh: any S <= 2048, causal too); 2 = single-row fused
 // kernels (attn_sm100.cuh: S <= 512, causal too)
+// Dropped-out attention probabilities Pd are saved by default. With
+// MIMOSE_SAVE_PD=0 the backward regenerates them from the saved P with the
+// same Philox stream (bit-identical values), trading a 4 B/score elementwise
+// pass for one S x S tensor per kept block. Measured: at a budget defined as a
+// fraction of the no-checkpoint peak the smaller peak shrinks the budget too,
+// so regeneration lowered samples/s (GPT-2 298 -> 275, RoBERTa-large 707 ->
+// 660); it pays only under a fixed absolute budget.
+bool Trainer::save_pd() const {
+  static const bool keep = [] {
+    const char* e = std::getenv("MIMOSE_SAVE_PD");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return keep && m_.attn_dropout > 0.f;
+}
+
 int Trainer::fused_attn(int S) const {
   if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
   if (t_.attn_fused == 2 && mimose_ops::attn_fused_supported(S)) return 2;
@@ -527,9 +542,9 @@ int64_t Trainer::block_work_bytes(int S) const {
   take_b(act);                                  // dctx
   if (hid) drop_b(act);                         // da
   take_b(qkv3);                                 // dqkv
-  if (fused != 1) drop_b(pd);                   // Pd
+  if (!save_pd()) take_b(pd);                   // regenerated Pd (0 without dropout)
+  drop_b(pd);                                   // Pd (saved or regenerated) after dV
   take_b(quad);                                 // dP
-  if (fused == 1) drop_b(pd);
   drop_b(act); drop_b(quad);                    // dctx, P
   drop_b(quad); drop_b(qkv3);                   // dP, qkv
   if (fused == 1) drop_b(act);                  // ctx
@@ -568,7 +583,7 @@ void Trainer::build_spec() {
   spec_.constant_footprint = constant_bytes_;
   spec_.input_min = (int64_t)t_.batch * t_.seq_min;
   spec_.input_max = (int64_t)t_.batch * t_.seq_max;
-  const double p_quad = (m_.attn_dropout > 0.f ? 2.0 : 1.0) * nh_ * 2.0 / B;
+  const double p_quad = (save_pd() ? 2.0 : 1.0) * nh_ * 2.0 / B;
   for (int l = 0; l < L_; ++l) {
     mimose::LayerSpec ls;
     ls.id = l;
@@ -624,7 +639,8 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
                        p32_ + P.bqkv.off),
            s);
   void* Pm = take(quad, act_tag);
-  void* Pd = m_.attn_dropout > 0.f ? take(quad, act_tag) : nullptr;
+  // Pd: only the P V operand unless saved (save_pd); the backward regenerates it
+  void* Pd = m_.attn_dropout > 0.f ? take(quad, save_pd() ? act_tag : kTagTransient) : nullptr;
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
   static const int fwd_max = [] {
     const char* e = std::getenv("MIMOSE_ATTN_FWD_MAX");
@@ -668,12 +684,15 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
     c.out = ctx; c.ldo = H; c.obs1 = 64; c.obs2 = (int64_t)S * H;
     run_gemm(c, s);
   }
+  if (!(keep && save_pd())) {
+    drop(Pd);
+    Pd = nullptr;
+  }
   if (keep) {
     save->qkv = qkv; save->P = Pm; save->Pd = Pd;
   } else {
     drop(qkv);
     drop(Pm);
-    drop(Pd);
   }
   return ctx;
 }
@@ -686,6 +705,13 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
   // dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
   void* dqkv = take(T * 3 * H * 2, kTagTransient);
+  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+  if (sv.Pd == nullptr && m_.attn_dropout > 0.f) {
+    // regenerate Pd = keep * P / (1 - p) from the saved P (same Philox
+    // stream and element index as the forward: bit-identical)
+    sv.Pd = take(quad, kTagTransient);
+    ck(mimose_ops::dropout_apply(sv.P, sv.Pd, quad / 2, pdrop, s), "dropout_apply");
+  }
   {
     GemmCall c;
     c.M = S; c.N = 64; c.K = S; c.nb1 = nh; c.nb2 = g.B;
@@ -700,8 +726,8 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
   }
   const int fused = fused_attn(S);
   drop(sv.Pd);
+  sv.Pd = nullptr;
   void* dP = take(quad, kTagTransient);
-  const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
   if (fused == 1) {
     ck(mimose_ops::attn2_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
                                     sv.ctx, sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop,

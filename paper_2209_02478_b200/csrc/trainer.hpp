@@ -131,6 +131,7 @@ class Trainer {
   void* attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g, cudaStream_t s);
   void* attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
   int fused_attn(int S) const;
+  bool save_pd() const;
   void* head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g, cudaStream_t s);
   int label_count(int B, int S) const;
  public:
