@@ -9,9 +9,10 @@
 //
 // Row statistics: 16 epilogue warps split each row into four column parts
 // (TMEM lane quarter x part); partial max / sum / dot are exchanged through
-// shared memory behind a named barrier. Forward: pass 1 row max, pass 2
-// exp + row sum with the exponentials written back into TMEM (tcgen05.st),
-// pass 3 normalise + Philox dropout, so every score costs one ex2. Backward:
+// shared memory behind a named barrier. Forward: pass 1 online row max / sum
+// with the exponentials written back into TMEM (tcgen05.st) relative to the
+// running max, pass 2 normalise (per-chunk max correction) + Philox dropout,
+// so every score costs one ex2 and two TMEM reads. Backward:
 // the keep masks of pass 1 stay in registers for pass 2. Output chunks (32
 // columns) go through 64B-swizzled staging buffers and TMA bulk stores.
 // The materialised P / Pd / dS keep the reference's quadratic activation term
@@ -213,56 +214,70 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
 
       if constexpr (!BWD) {
         const int jmax = p.causal ? min(p.S, i + 1) : p.S;  // valid keys of this row
-        // ---- pass 1: row max of the raw scores (alpha > 0 commutes with max)
+        // ---- pass 1 (online): per chunk, the running row max m of this part
+        // and the running sum of 2^(s sc - m) (rescaled when m grows); the
+        // exponentials go back into TMEM relative to the max current at that
+        // chunk (mch[j]), corrected in pass 2 by 2^(mch[j] - m_row)
         const float sc = p.alpha * kLog2e;
-        float mx = -INFINITY;
-#pragma unroll 1
+        float m_run = -INFINITY, l_run = 0.f;
+        float mch[NCH];
+#pragma unroll
         for (int j = 0; j < NCH; ++j) {
+          mch[j] = -INFINITY;
           const int c = (part + 4 * j) * 32;
-          if (c >= p.S) break;
-          uint32_t r[32];
-          tmem_ld32_nowait(t_row + c, r);
-          tmem_wait_ld();
-          if (c + 32 <= jmax) {
+          if (c < p.S) {
+            uint32_t r[32];
+            tmem_ld32_nowait(t_row + c, r);
+            tmem_wait_ld();
+            float cm = -INFINITY;
+            if (c + 32 <= jmax) {
 #pragma unroll
-            for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(r[e]));
-          } else {
+              for (int e = 0; e < 32; ++e) cm = fmaxf(cm, __uint_as_float(r[e]));
+            } else {
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (c + e < jmax) mx = fmaxf(mx, __uint_as_float(r[e]));
+              for (int e = 0; e < 32; ++e)
+                if (c + e < jmax) cm = fmaxf(cm, __uint_as_float(r[e]));
+            }
+            const float m_new = fmaxf(m_run, cm * sc);
+            if (m_new != -INFINITY) {
+              if (m_run != -INFINITY) l_run *= ex2f(m_run - m_new);
+              const float nm = -m_new;
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                const float x = c + e < jmax ? ex2f(fmaf(__uint_as_float(r[e]), sc, nm)) : 0.f;
+                l_run += x;
+                r[e] = __float_as_uint(x);
+              }
+              m_run = m_new;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) r[e] = 0u;
+            }
+            mch[j] = m_run;
+            tmem_st32(t_row + c, r);
           }
-        }
-        red_a[part * 128 + r_local] = mx * sc;
-        epi_bar();
-        const float nmx = -fmaxf(fmaxf(red_a[r_local], red_a[128 + r_local]),
-                                 fmaxf(red_a[256 + r_local], red_a[384 + r_local]));
-        // ---- pass 2: e = 2^(s * sc - max) written back to TMEM; row sum
-        float sum = 0.f;
-#pragma unroll 1
-        for (int j = 0; j < NCH; ++j) {
-          const int c = (part + 4 * j) * 32;
-          if (c >= p.S) break;
-          uint32_t r[32];
-          tmem_ld32_nowait(t_row + c, r);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = c + e < jmax ? ex2f(fmaf(__uint_as_float(r[e]), sc, nmx)) : 0.f;
-            sum += x;
-            r[e] = __float_as_uint(x);
-          }
-          tmem_st32(t_row + c, r);
         }
         tmem_wait_st();
-        red_b[part * 128 + r_local] = sum;
+        red_a[part * 128 + r_local] = m_run;
+        red_b[part * 128 + r_local] = l_run;
         epi_bar();
-        const float inv = 1.f / ((red_b[r_local] + red_b[128 + r_local]) +
-                                 (red_b[256 + r_local] + red_b[384 + r_local]));
-        // ---- pass 3: normalise, dropout, stage, TMA store
-#pragma unroll 1
+        float m_row = red_a[r_local];
+#pragma unroll
+        for (int q = 1; q < 4; ++q) m_row = fmaxf(m_row, red_a[q * 128 + r_local]);
+        float l_row = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float mq = red_a[q * 128 + r_local];
+          if (mq != -INFINITY) l_row += red_b[q * 128 + r_local] * ex2f(mq - m_row);
+        }
+        const float inv = l_row > 0.f ? 1.f / l_row : 0.f;
+        // ---- pass 2: normalise (with the chunk's max correction), dropout,
+        // stage, TMA store
+#pragma unroll
         for (int j = 0; j < NCH; ++j) {
           const int c = (part + 4 * j) * 32;
           if (c >= p.S) break;
+          const float f = mch[j] != -INFINITY ? ex2f(mch[j] - m_row) * inv : 0.f;
           uint32_t rnd[4][4];
           if (p.store_pd) {
             uint64_t grp[4];
@@ -279,7 +294,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
           for (int q = 0; q < 4; ++q) {
             float pv[8], dv[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * q + e]) * inv);
+            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * q + e]) * f);
             const uint32_t addr = rbase + ((q ^ sw) << 4);
             st_shared_v4(addr, pack_bf16x2_(pv[0], pv[1]), pack_bf16x2_(pv[2], pv[3]),
                          pack_bf16x2_(pv[4], pv[5]), pack_bf16x2_(pv[6], pv[7]));
