@@ -411,6 +411,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   p.alpha = c.alpha; p.beta = c.beta;
   p.gelu_tanh = c.gelu_tanh;
   p.drop = c.drop;
+  p.causal_tiles = c.causal_tiles ? 1 : 0;
   if (c.drop.threshold != 0 && (c.epi != kEpiBf16 || c.nb1 != 1 || c.nb2 != 1 || c.N % 8 != 0))
     return cudaErrorInvalidValue;  // dropout index = row * ldo + col, 8-column groups
   {

@@ -52,6 +52,8 @@ struct GemmParams {
   int kb_per_split;         // k-blocks per split
   int gelu_tanh;            // GELU flavour of kEpiBiasGelu / kEpiDGelu: 0 erf, 1 tanh
   DropoutCfg drop;          // kEpiBf16: dropout on (alpha*acc + bias) before adding aux
+  int causal_tiles;         // batched S x S score GEMMs of a causal model: skip tiles
+                            // whose columns (keys) all exceed their rows (queries)
 };
 
 constexpr int kBM = 128;
@@ -363,6 +365,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
         const int zz = tile / tiles_per_batch;
         const int t_in = tile % tiles_per_batch;
+        if (p.causal_tiles && (t_in % tiles_n) * BN >= (t_in / tiles_n) * kTileM + kTileM) continue;
         // n-fastest raster: the CTAs that run concurrently share one A row
         // block (read once from HBM) and cycle through B (weights, L2-resident)
         const int m0 = (t_in / tiles_n) * kTileM + (int)rank * kBM;
@@ -429,8 +432,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     const uint32_t b_step = p.b_mn ? 2048u : 32u;
     const uint32_t a_lbo = p.a_mn ? 8192u : 16u;
     const uint32_t b_lbo = p.b_mn ? 8192u : 16u;
-    int it = 0, local = 0;
-    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++local) {
+    int it = 0, local = 0;  // local counts processed tiles only (accumulator phases)
+    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
+      {
+        const int t_in = tile % tiles_per_batch;
+        if (p.causal_tiles && (t_in % tiles_n) * BN >= (t_in / tiles_n) * kTileM + kTileM) continue;
+      }
       const int acc = local % Cfg::kAcc;
       const uint32_t aph = (local / Cfg::kAcc) & 1;
       const int split = (tile / tiles_per_batch) % p.splits;
@@ -463,6 +470,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         }
         __syncwarp();
       }
+      ++local;
     }
     }
   } else {
@@ -476,9 +484,10 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
     uint8_t* wbuf = sD + ew * (Cfg::kBufs * Cfg::kNOut * Cfg::kBufBytes);
     int local = 0, chunk_seq = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_rank(&tempty[0], 0) : 0u;
-    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG, ++local) {
+    for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
       const int zz = tile / tiles_per_batch;
       const int t_in = tile % tiles_per_batch;
+      if (p.causal_tiles && (t_in % tiles_n) * BN >= (t_in / tiles_n) * kTileM + kTileM) continue;
       const int m0 = (t_in / tiles_n) * kTileM + (int)rank * kBM;
       const int n0 = (t_in % tiles_n) * BN;
       const int split = zz % p.splits, z = zz / p.splits;
@@ -640,6 +649,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
         else mbar_arrive(&tempty[acc]);
       }
+      ++local;
     }
     if (p.tma_store && lane == 0) bulk_wait<0>();
   }

@@ -539,14 +539,16 @@ template <int L, int MAXC>
 __global__ void __launch_bounds__(256, (MAXC > 4) ? 1 : 2) softmax_bwd_kernel(const bf16* __restrict__ P,
                                                           bf16* __restrict__ dpd, int64_t rows,
                                                           int S, int ld, DropoutCfg drop,
-                                                          float scale) {
+                                                          float scale, int causal) {
   constexpr int R = 32 / L;
   const int lane = threadIdx.x & 31;
   const int sub = lane % L;
   const int64_t row = ((int64_t)blockIdx.x * 8 + (threadIdx.x >> 5)) * R + lane / L;
   const bool live = row < rows;
   const int64_t base = (live ? row : 0) * ld;
-  const int jmax = live ? S : 0;
+  // causal: keys above the diagonal carry P = 0 and may hold unwritten dPd
+  // (their score tiles were skipped): never read them
+  const int jmax = live ? (causal ? static_cast<int>(row % S) + 1 : S) : 0;
   uint4 praw[MAXC], draw[MAXC];
 #pragma unroll
   for (int c = 0; c < MAXC; ++c) {
@@ -1191,10 +1193,10 @@ static void softmax_fwd_t(const bf16* in, bf16* p, bf16* pd, int64_t rows, int S
 }
 template <int L, int MAXC>
 static void softmax_bwd_t(const bf16* p, bf16* dp, int64_t rows, int S, int ld,
-                          const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
+                          const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s, int causal) {
   const int64_t rows_per_block = 8 * (32 / L);
   const int g = (int)((rows + rows_per_block - 1) / rows_per_block);
-  mimose_dev::softmax_bwd_kernel<L, MAXC><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale);
+  mimose_dev::softmax_bwd_kernel<L, MAXC><<<g, 256, 0, s>>>(p, dp, rows, S, ld, d, scale, causal);
 }
 
 // Dispatch: L lanes per row (8 for rows up to 512, 16 up to 1024, 32 up to
@@ -1251,15 +1253,16 @@ cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int
 }
 
 cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
-                        const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s) {
+                        const mimose_dev::DropoutCfg& d, float scale, cudaStream_t s, bool causal) {
+  const int cz = causal ? 1 : 0;
   ProfScope prof("mem_softmax_bwd", 0, (double)rows * 6.0 * S, s);  // P, dPd read; dS written
   auto p = static_cast<const bf16*>(P);
   auto dp = static_cast<bf16*>(dPd);
   int L = 0, maxc = 0;
   if (!softmax_geometry(ld, &L, &maxc)) return cudaErrorInvalidValue;
-#define BWD8(M) softmax_bwd_t<8, M>(p, dp, rows, S, ld, d, scale, s)
-#define BWD16(M) softmax_bwd_t<16, M>(p, dp, rows, S, ld, d, scale, s)
-#define BWD32(M) softmax_bwd_t<32, M>(p, dp, rows, S, ld, d, scale, s)
+#define BWD8(M) softmax_bwd_t<8, M>(p, dp, rows, S, ld, d, scale, s, cz)
+#define BWD16(M) softmax_bwd_t<16, M>(p, dp, rows, S, ld, d, scale, s, cz)
+#define BWD32(M) softmax_bwd_t<32, M>(p, dp, rows, S, ld, d, scale, s, cz)
   if (L == 8) { MIMOSE_SOFTMAX_CASES(BWD8) }
   else if (L == 16) { MIMOSE_SOFTMAX_CASES(BWD16) }
   else { MIMOSE_SOFTMAX_CASES(BWD32) }

@@ -49,6 +49,7 @@ struct GemmCall {
   int64_t workspace_bytes = 0;
   int gelu_tanh = 0;              // GELU flavour for kEpiBiasGelu / kEpiDGelu
   mimose_dev::DropoutCfg drop;    // kEpiBf16: dropout on the product before adding aux
+  bool causal_tiles = false;      // skip tiles above the diagonal (causal S x S scores)
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);

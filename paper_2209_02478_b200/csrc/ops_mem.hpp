@@ -67,7 +67,7 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,
                         const DropoutCfg& d, cudaStream_t s, bool causal = false);
 cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
-                        const DropoutCfg& d, float scale, cudaStream_t s);
+                        const DropoutCfg& d, float scale, cudaStream_t s, bool causal = false);
 cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
                             const int32_t* uid, int n_unique, float* dword, cudaStream_t s,
                             bool accumulate = false);

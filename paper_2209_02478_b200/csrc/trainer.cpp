@@ -667,6 +667,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
     c.epi = mimose_ops::kEpiBf16;
     c.out = sc; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
     c.alpha = 0.125f;
+    c.causal_tiles = m_.causal != 0;  // the softmax never reads keys above the diagonal
     run_gemm(c, s);
     ck(mimose_ops::softmax_fwd(sc, Pm, Pd, (int64_t)g.B * nh * S, S, ld, pdrop, s, m_.causal != 0),
        "softmax_fwd");
@@ -746,8 +747,10 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
     c.B = head_view(sv.qkv, 2 * H, S, 3 * H);
     c.epi = mimose_ops::kEpiBf16;
     c.out = dP; c.ldo = ld; c.obs1 = (int64_t)S * ld; c.obs2 = (int64_t)nh * S * ld;
+    c.causal_tiles = m_.causal != 0;
     run_gemm(c, s);
-    ck(mimose_ops::softmax_bwd(sv.P, dP, (int64_t)g.B * nh * S, S, ld, pdrop, 0.125f, s),
+    ck(mimose_ops::softmax_bwd(sv.P, dP, (int64_t)g.B * nh * S, S, ld, pdrop, 0.125f, s,
+                               m_.causal != 0),
        "softmax_bwd");
   }
   drop(dctx);

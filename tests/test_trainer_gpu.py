@@ -94,9 +94,10 @@ VARIANTS = {
 }
 
 
-def _variant_trainer(shape, dropout=0.0, planner="none", batch=8, seq=(16, 96)):
+def _variant_trainer(shape, dropout=0.0, planner="none", batch=8, seq=(16, 96), attn_fused=2):
     m = ModelConfig(hidden_dropout=dropout, attn_dropout=dropout, seed=77, **shape)
-    t = TrainConfig(planner=planner, batch=batch, seq_min=seq[0], seq_max=seq[1])
+    t = TrainConfig(planner=planner, batch=batch, seq_min=seq[0], seq_max=seq[1],
+                    attn_fused=attn_fused)
     return Trainer(m, t, 4 * GiB)
 
 
@@ -114,12 +115,19 @@ def _check_grads(got, ref_grads):
             assert cos >= 0.995, f"{name}: cosine {cos}"
 
 
+@pytest.mark.parametrize("attn", [2, 0])
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
-@pytest.mark.parametrize("S", [24, 61])
-def test_variant_parity_vs_cpu_oracle(cuda_device, variant, dropout, S):
+@pytest.mark.parametrize("S", [24, 61, 200])
+def test_variant_parity_vs_cpu_oracle(cuda_device, variant, dropout, S, attn):
+    """attn 0 exercises the GEMM + softmax pair (causal: score tiles above the
+    diagonal skipped, softmax backward masked); attn 2 the fused kernels."""
     from oracle import bert_ref
-    tr = _variant_trainer(VARIANTS[variant], dropout=dropout)
+    if S > 96:
+        shape = dict(VARIANTS[variant], max_pos=256)
+        tr = _variant_trainer(shape, dropout=dropout, seq=(16, 256), attn_fused=attn)
+    else:
+        tr = _variant_trainer(VARIANTS[variant], dropout=dropout, attn_fused=attn)
     rng = np.random.default_rng(21)
     tok, typ, lab = synthetic_task_batch(rng, tr.model, 8, S)
     params = _oracle_params(tr)
