@@ -412,6 +412,8 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   p.gelu_tanh = c.gelu_tanh;
   p.drop = c.drop;
   p.causal_tiles = c.causal_tiles ? 1 : 0;
+  p.causal_k = c.causal_k;
+  if (c.causal_k != 0 && splits > 1) return cudaErrorInvalidValue;
   if (c.drop.threshold != 0 && (c.epi != kEpiBf16 || c.nb1 != 1 || c.nb2 != 1 || c.N % 8 != 0))
     return cudaErrorInvalidValue;  // dropout index = row * ldo + col, 8-column groups
   {

@@ -54,6 +54,9 @@ struct GemmParams {
   DropoutCfg drop;          // kEpiBf16: dropout on (alpha*acc + bias) before adding aux
   int causal_tiles;         // batched S x S score GEMMs of a causal model: skip tiles
                             // whose columns (keys) all exceed their rows (queries)
+  int causal_k;             // causal contractions over S: 1 = only k <= row contributes
+                            // (P V, dS K), 2 = only k >= row (P^T dO, dS^T Q); the
+                            // k-blocks outside are exact zeros and are skipped
 };
 
 constexpr int kBM = 128;
@@ -372,8 +375,13 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
         const int n0 = (t_in % tiles_n) * BN + (int)rank * Cfg::kBRows;
         const int split = zz % p.splits, z = zz / p.splits;
         const int b1 = z % p.nb1, b2 = z / p.nb1;
-        const int kb0 = split * p.kb_per_split;
-        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        int kb0 = split * p.kb_per_split;
+        int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        {
+          const int mb = (t_in / tiles_n) * kTileM;
+          if (p.causal_k == 1) kb1 = min(kb1, (mb + kTileM + kBK - 1) / kBK);
+          if (p.causal_k == 2) kb0 = max(kb0, mb / kBK);
+        }
         for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
@@ -441,7 +449,16 @@ __global__ void __launch_bounds__(gemm_threads(EW), 1)
       const int acc = local % Cfg::kAcc;
       const uint32_t aph = (local / Cfg::kAcc) & 1;
       const int split = (tile / tiles_per_batch) % p.splits;
-      const int kb_n = min(num_kb, (split + 1) * p.kb_per_split) - split * p.kb_per_split;
+      int kb_n = min(num_kb, (split + 1) * p.kb_per_split) - split * p.kb_per_split;
+      if (p.causal_k != 0) {  // same k-block range as the producer
+        const int t_in = tile % tiles_per_batch;
+        const int mb = (t_in / tiles_n) * kTileM;
+        int kb0 = split * p.kb_per_split;
+        int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        if (p.causal_k == 1) kb1 = min(kb1, (mb + kTileM + kBK - 1) / kBK);
+        if (p.causal_k == 2) kb0 = max(kb0, mb / kBK);
+        kb_n = kb1 - kb0;
+      }
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;

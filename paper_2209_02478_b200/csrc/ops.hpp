@@ -50,6 +50,7 @@ struct GemmCall {
   int gelu_tanh = 0;              // GELU flavour for kEpiBiasGelu / kEpiDGelu
   mimose_dev::DropoutCfg drop;    // kEpiBf16: dropout on the product before adding aux
   bool causal_tiles = false;      // skip tiles above the diagonal (causal S x S scores)
+  int causal_k = 0;               // 1: only k <= row contributes, 2: only k >= row (causal)
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);

@@ -683,6 +683,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
     c.b_mn = true;
     c.epi = mimose_ops::kEpiBf16;
     c.out = ctx; c.ldo = H; c.obs1 = 64; c.obs2 = (int64_t)S * H;
+    c.causal_k = m_.causal ? 1 : 0;  // keys j <= query i only
     run_gemm(c, s);
   }
   if (!(keep && save_pd())) {
@@ -721,6 +722,7 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
     c.B = head_view(dctx, 0, S, H);
     c.b_mn = true;
     c.epi = mimose_ops::kEpiBf16;
+    c.causal_k = m_.causal ? 2 : 0;  // dV_j: queries i >= key j only
     c.out = static_cast<bf16raw*>(dqkv) + 2 * H;
     c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
     run_gemm(c, s);
@@ -763,10 +765,12 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
     c.b_mn = true;
     c.epi = mimose_ops::kEpiBf16;
     c.out = dqkv; c.ldo = 3 * H; c.obs1 = 64; c.obs2 = (int64_t)S * 3 * H;
+    c.causal_k = m_.causal ? 1 : 0;  // keys j <= query i
     run_gemm(c, s);
     // dK = dS^T Q
     c.A = sq_view(dP, S, ld, nh);
     c.a_mn = true;
+    c.causal_k = m_.causal ? 2 : 0;  // queries i >= key j
     c.B = head_view(sv.qkv, 0, S, 3 * H);
     c.out = static_cast<bf16raw*>(dqkv) + H;
     run_gemm(c, s);
