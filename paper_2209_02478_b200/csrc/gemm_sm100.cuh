@@ -241,12 +241,22 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
   if constexpr (EPI == kEpiBf16) {
     // branch dropout (pre-LN residual: out = aux + dropout(x W^T + b))
     if (p.drop.threshold != 0) {
+      // Philox blocks two groups at a time (round-major), keep predicates
+      // straight from the words (same masks as dropout_mask8)
+      const uint32_t thr_hi = p.drop.threshold << 16;
 #pragma unroll
-      for (int q = 0; q < NV / 8; ++q) {
-        const uint32_t m = dropout_mask8(p.drop, (uint64_t)obase + col0 + 8 * q);
+      for (int q = 0; q < NV / 8; q += 2) {
+        uint64_t grp[2];
+        uint32_t rnd[2][4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
-          v[8 * q + e] = ((m >> e) & 1u) ? v[8 * q + e] * p.drop.scale : 0.f;
+        for (int u = 0; u < 2; ++u) grp[u] = ((uint64_t)obase + col0 + 8 * (q + u)) >> 3;
+        philox_n<2>(p.drop.seed, p.drop.stream, grp, rnd);
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            v[8 * (q + u) + e] =
+                philox_keep_w(rnd[u], e, thr_hi) ? v[8 * (q + u) + e] * p.drop.scale : 0.f;
       }
     }
   }
