@@ -242,11 +242,20 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
             if (m_new != -INFINITY) {
               if (m_run != -INFINITY) l_run *= ex2f(m_run - m_new);
               const float nm = -m_new;
+              if (c + 32 <= jmax) {  // whole chunk valid: no per-element masking
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const float x = c + e < jmax ? ex2f(fmaf(__uint_as_float(r[e]), sc, nm)) : 0.f;
-                l_run += x;
-                r[e] = __float_as_uint(x);
+                for (int e = 0; e < 32; ++e) {
+                  const float x = ex2f(fmaf(__uint_as_float(r[e]), sc, nm));
+                  l_run += x;
+                  r[e] = __float_as_uint(x);
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 32; ++e) {
+                  const float x = c + e < jmax ? ex2f(fmaf(__uint_as_float(r[e]), sc, nm)) : 0.f;
+                  l_run += x;
+                  r[e] = __float_as_uint(x);
+                }
               }
               m_run = m_new;
             } else {
@@ -293,11 +302,16 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             float pv[8], dv[8];
+            uint32_t ph[4];  // P rounded once to bf16 pairs; pv = the same values widened
 #pragma unroll
-            for (int e = 0; e < 8; ++e) pv[e] = bf16r(__uint_as_float(r[8 * q + e]) * f);
+            for (int e = 0; e < 8; e += 2) {
+              ph[e >> 1] = pack_bf16x2_(__uint_as_float(r[8 * q + e]) * f,
+                                        __uint_as_float(r[8 * q + e + 1]) * f);
+              pv[e] = __uint_as_float(ph[e >> 1] << 16);
+              pv[e + 1] = __uint_as_float(ph[e >> 1] & 0xFFFF0000u);
+            }
             const uint32_t addr = rbase + ((q ^ sw) << 4);
-            st_shared_v4(addr, pack_bf16x2_(pv[0], pv[1]), pack_bf16x2_(pv[2], pv[3]),
-                         pack_bf16x2_(pv[4], pv[5]), pack_bf16x2_(pv[6], pv[7]));
+            st_shared_v4(addr, ph[0], ph[1], ph[2], ph[3]);
             if (p.store_pd) {
 #pragma unroll
               for (int e = 0; e < 8; ++e)
