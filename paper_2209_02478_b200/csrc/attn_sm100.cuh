@@ -388,16 +388,16 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
             tmem_wait_ld();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int colq = c + 8 * q;
               float pf[8], ds[8];
               unpack_bf16x8(pr[q], pf);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                const bool in = colq + e < p.S;
+                // (columns >= S: g = 0 by the keep mask, and the TMA store
+                // clips them, so no per-element bounds test is needed)
                 const float g = ((km[j] >> (8 * q + e)) & 1u)
                                     ? __uint_as_float(r[8 * q + e]) * p.drop.scale
                                     : 0.f;
-                ds[e] = in ? pf[e] * (g - dot) * p.ds_scale : 0.f;
+                ds[e] = pf[e] * (g - dot) * p.ds_scale;
               }
               st_shared_v4(rbase + ((q ^ sw) << 4), pack_bf16x2_(ds[0], ds[1]),
                            pack_bf16x2_(ds[2], ds[3]), pack_bf16x2_(ds[4], ds[5]),
