@@ -158,6 +158,33 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int s = it % NS;
       const uint32_t ph = (it / NS) & 1;
+      if constexpr (NC == 512) {
+        // one 512-column accumulator released in two halves: the lower half
+        // of tile i + 1 is computed while the epilogue still works through
+        // the upper half of tile i (tfull / tempty index = half)
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        const uint32_t hph = it & 1;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          mbar_wait(&tempty[half], hph ^ 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(sA + s * Cfg::kABytes);
+            const uint32_t b_addr = smem_u32(sB + s * Cfg::kBBytes);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t da = smem_desc_sw128(a_addr + kk * 32, 16, 1024);
+              const uint64_t db = smem_desc_sw128(b_addr + half * 256 * 128 + kk * 32, 16, 1024);
+              umma_bf16(tmem_base + half * 256, da, db, idesc, kk != 0 ? 1u : 0u);
+            }
+            umma_commit(&tfull[half]);
+            if (half == 1) umma_commit(&empty[s]);
+          }
+          __syncwarp();
+        }
+        continue;
+      }
       const int acc = it % Cfg::kAcc;
       const uint32_t aph = (it / Cfg::kAcc) & 1;
       mbar_wait(&tempty[acc], aph ^ 1);
@@ -204,8 +231,29 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
       const int i = m0 + r_local;  // query row
       const bool row_ok = i < p.S;
       const int64_t grow = ((int64_t)z * p.S + (row_ok ? i : 0));  // row of the [B*nh*S][ld] view
-      mbar_wait(&tfull[acc], aph);
-      tc_fence_after();
+      if constexpr (NC != 512) {
+        mbar_wait(&tfull[acc], aph);
+        tc_fence_after();
+      }
+      // NC = 512: half h of the row lands on tfull[h] and is released on
+      // tempty[h]; chunks j = 0, 1 are the lower half, j = 2, 3 the upper
+      auto half_wait = [&](int j) {
+        if constexpr (NC == 512) {
+          if (j == 0 || j == 2) {
+            mbar_wait(&tfull[j >> 1], it & 1);
+            tc_fence_after();
+          }
+        }
+      };
+      auto half_release = [&](int j) {
+        if constexpr (NC == 512) {
+          if (j == 1 || j == 3) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[j >> 1]);
+          }
+        }
+      };
       // 32-column chunks are dealt round-robin to the 4 column parts (chunk
       // ch -> part ch % 4), so every warp gets within one chunk of S / 4
       // columns whatever S is
@@ -223,6 +271,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
         float mch[NCH];
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
+          half_wait(j);
           mch[j] = -INFINITY;
           const int c = (part + 4 * j) * 32;
           if (c < p.S) {
@@ -285,7 +334,10 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
           const int c = (part + 4 * j) * 32;
-          if (c >= p.S) break;
+          if (c >= p.S) {
+            half_release(j);
+            continue;
+          }
           const float f = mch[j] != -INFINITY ? ex2f(mch[j] - m_row) * inv : 0.f;
           uint32_t rnd[4][4];
           if (p.store_pd) {
@@ -328,6 +380,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
             if (p.store_pd) tma_store_4d(&tmO2, wbuf + Cfg::kBufBytes, c, m0 + quarter * 32, b1, b2);
             bulk_commit();
           }
+          half_release(j);
         }
       } else {
         // ---- backward: pass 1 dot = sum_j dP_j P_j (dP = dPd * keep * scale);
@@ -338,6 +391,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
         float dot = 0.f;
 #pragma unroll
         for (int j = 0; j < NCH; ++j) {
+          half_wait(j);
           const int c = (part + 4 * j) * 32;
           if (c < p.S) {
             uint64_t grp[4];
@@ -410,11 +464,14 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
               bulk_commit();
             }
           }
+          half_release(j);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if constexpr (NC != 512) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
     }
     if (lane == 0) bulk_wait<0>();
   }
