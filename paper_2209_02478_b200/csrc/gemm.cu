@@ -460,7 +460,9 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
 
   const int64_t tiles = (int64_t)((c.M + 128 * cg - 1) / (128 * cg)) * ((c.N + bn - 1) / bn) *
                         c.nb1 * c.nb2 * splits;
-  const int slots = sm_count() / cg;  // CTAs (cg = 1) or CTA pairs (cg = 2) resident at once
+  // CTAs (cg = 1) or CTA pairs (cg = 2) resident at once (64-wide tiles: two per SM)
+  const int slots =
+      sm_count() * ((bn == 64 && ew == 8 && c.epi == kEpiBf16 && cg == 1) ? 2 : 1) / cg;
   const int grid = (int)(tiles < slots ? tiles : slots) * cg;
   // roofline record: algorithmic flops 2*M*N*K*batch; algorithmic bytes =
   // operands read once + outputs (and epilogue side inputs) once. Batched

@@ -101,8 +101,12 @@ struct GemmCfg {
   // the MMA can run up to kAcc - 1 tiles ahead of the epilogue
   static constexpr int kAcc = (512 / BN) > 4 ? 4 : (512 / BN);
   static constexpr int kBiasBytes = kAcc * BN * 4;  // tile bias slice, per accumulator
+  // 64-wide tiles (the streaming attention contractions, K = S) run two CTAs
+  // per SM: two independent load / MMA / epilogue pipelines, each with half
+  // the shared memory and TMEM
+  static constexpr int kMinBlocks = (BN == 64 && EW == 8 && EPI == kEpiBf16 && CG == 1) ? 2 : 1;
   static constexpr int kStagesRaw =
-      (kSmemBudget - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
+      (kSmemBudget / kMinBlocks - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
   static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
   static constexpr int kTmemCols = kAcc * BN;
   static constexpr int kSmemBytes =
@@ -309,7 +313,7 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
 }
 
 template <int BN, int EPI, int EW, int CG>
-__global__ void __launch_bounds__(gemm_threads(EW), 1)
+__global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::kMinBlocks))
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmD,
