@@ -153,7 +153,15 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_bf16_f32(128, 256, false, false);
+    // MMA width trimmed to the key columns that exist (multiple of 16): keys
+    // >= S are zero-filled by the TMA and never read, so computing them only
+    // burns tensor cycles (and power) - e.g. S = 288 needs 256 + 32 columns
+    auto n_eff = [&](int col0) {
+      const int n = min(256, ((p.S - col0 + 15) / 16) * 16);
+      return n < 16 ? 16 : n;
+    };
+    const uint32_t idesc = idesc_bf16_f32(128, n_eff(0), false, false);
+    const uint32_t idesc_hi = idesc_bf16_f32(128, n_eff(256), false, false);
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int s = it % NS;
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(AttnCfg<NC>::kThreads, 1)
             for (int kk = 0; kk < 4; ++kk) {
               const uint64_t da = smem_desc_sw128(a_addr + kk * 32, 16, 1024);
               const uint64_t db = smem_desc_sw128(b_addr + half * 256 * 128 + kk * 32, 16, 1024);
-              umma_bf16(tmem_base + half * 256, da, db, idesc, kk != 0 ? 1u : 0u);
+              umma_bf16(tmem_base + half * 256, da, db, half ? idesc_hi : idesc, kk != 0 ? 1u : 0u);
             }
             umma_commit(&tfull[half]);
             if (half == 1) umma_commit(&empty[s]);
