@@ -44,3 +44,6 @@ clean:
 	rm -rf $(BUILD) $(PKG)/*.so
 
 .PHONY: all clean
+
+print-nvflags:
+	@echo $(NVFLAGS)

@@ -231,6 +231,15 @@ cudaError_t launch_bn(int epi, int ew, const CUtensorMap& ta, const CUtensorMap&
 // unbatched, un-split GEMMs with >= 2 row blocks whose epilogue is light
 // (K >= 768 projections and data gradients: 1090 -> 1250 TFLOP/s at K = 3072).
 // MIMOSE_GEMM_CG=1/2 forces (A/B timing); force_cg in the call overrides.
+// MIMOSE_AUX_TMA=0: aux rows through per-thread loads (A/B timing)
+bool aux_tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MIMOSE_AUX_TMA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 int pick_cg(const GemmCall& c, int bn) {
   static const int forced = [] {
     const char* e = std::getenv("MIMOSE_GEMM_CG");
@@ -239,9 +248,11 @@ int pick_cg(const GemmCall& c, int bn) {
   if (bn != 256 || c.nb1 * c.nb2 != 1 || c.M <= 128) return 1;
   if (c.force_cg == 1 || c.force_cg == 2) return c.force_cg;
   if (forced == 1 || forced == 2) return forced;
-  // epilogue-bound GELU / dGELU tiles gain nothing from a faster mainloop and
-  // lose to the pair's joint accumulator release (measured 730 -> 683 TFLOP/s)
-  if (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) return 1;
+  // the dGELU epilogue (aux tile in, one output) is the slower side of its
+  // pipeline, and the pair's joint accumulator release costs it (852 -> 794
+  // TFLOP/s); the GELU GEMM's mainloop is the slower side and the pair's
+  // halved B traffic helps it (887 -> 909)
+  if (c.epi == kEpiDGelu) return 1;
   return 2;
 }
 
@@ -278,7 +289,7 @@ int pick_bn(const GemmCall& c) {
   // light-epilogue unbatched GEMMs run 256-wide tiles on CTA pairs (see
   // pick_cg): take them whenever the pair grid is not clearly worse-filled
   // than the 128-wide single-SM grid (pair tiles are ~1.3x faster per flop)
-  if (c.N > 128 && batches == 1 && c.M > 128 && c.epi != kEpiBiasGelu && c.epi != kEpiDGelu &&
+  if (c.N > 128 && batches == 1 && c.M > 128 && c.epi != kEpiDGelu &&
       c.force_cg != 1) {
     const int64_t pairs = sm_count() / 2;
     const int64_t tp = ((c.M + 255) / 256) * ((c.N + 255) / 256);
@@ -456,6 +467,12 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
       ok = make_map_t(&td2, c.out2, c.M, c.N, c.ldo, c.obs1, c.obs2, c.nb1, c.nb2, cw, 32, esz,
                       sw64);
     p.tma_store = ok ? 1 : 0;
+    // aux (dGELU input / residual) tiles by TMA into the staging buffers: same
+    // addressing as the output, so the same box and swizzle
+    if (ok && c.aux != nullptr && (c.epi == kEpiDGelu || c.epi == kEpiBf16) && al(c.aux) &&
+        aux_tma_enabled())
+      p.aux_tma = make_map_t(&td2, const_cast<void*>(c.aux), c.M, c.N, c.ldo, c.obs1, c.obs2,
+                             c.nb1, c.nb2, cw, 32, esz, sw64) ? 1 : 0;
   }
 
   const int64_t tiles = (int64_t)((c.M + 128 * cg - 1) / (128 * cg)) * ((c.N + bn - 1) / bn) *
@@ -512,3 +529,15 @@ cudaError_t gemm_profile_read(double* flops, double* ms, int64_t* launches) {
 }
 
 }  // namespace mimose_ops
+
+#ifdef MIMOSE_GEMM_TRACE
+extern "C" int mimose_debug_trace(void* dst, int n, int clear) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(dst, mimose_dev::g_gemm_trace, n * 8);
+  if (clear) {
+    static unsigned long long z[1 << 15];
+    cudaMemcpyToSymbol(mimose_dev::g_gemm_trace, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

@@ -54,6 +54,8 @@ struct GemmParams {
   DropoutCfg drop;          // kEpiBf16: dropout on (alpha*acc + bias) before adding aux
   int causal_tiles;         // batched S x S score GEMMs of a causal model: skip tiles
                             // whose columns (keys) all exceed their rows (queries)
+  int aux_tma;              // 1: the aux tile arrives by TMA (map in the tmD2 slot) into
+                            // the warp's staging buffers instead of per-row loads
   int causal_k;             // causal contractions over S: 1 = only k <= row contributes
                             // (P V, dS K), 2 = only k >= row (P^T dO, dS^T Q); the
                             // k-blocks outside are exact zeros and are skipped
@@ -87,6 +89,8 @@ struct GemmCfg {
   static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kNOut = EPI == kEpiBiasGelu ? 2 : 1;
+  // the GELU epilogue's two outputs go through the same staging buffer one
+  // after the other: one fewer buffer per warp buys a pipeline stage
   static constexpr int kEsz = EPI == kEpiF32 ? 4 : 2;
   static constexpr int kEpiWarps = EW;
   static constexpr int kColParts = EW / 4;
@@ -95,22 +99,30 @@ struct GemmCfg {
   static constexpr int kChunkCols = kChunkBytes / kEsz;
   static constexpr int kBufBytes = 32 * kChunkBytes;  // 32 rows x one chunk
   // per epilogue warp: kBufs sets of kNOut buffers of 32 rows x kChunkBytes
-  static constexpr int kBufs = 1;  // 2 measured: attention unchanged, dense -4 %
-  static constexpr int kStagingBytes = EW * kBufs * kNOut * kBufBytes;
+  // (2 measured for plain outputs: attention unchanged, dense -4 %; the dGELU
+  // epilogue takes 2 so both chunks' aux tiles are requested by TMA before
+  // the accumulator is ready)
+  static constexpr int kBufs = EPI == kEpiDGelu ? 2 : 1;
+  static constexpr int kStagingBytes = EW * kBufs * kBufBytes;
   // TMEM accumulators: as many BN-column tiles as fit 512 columns (max 4), so
   // the MMA can run up to kAcc - 1 tiles ahead of the epilogue
   static constexpr int kAcc = (512 / BN) > 4 ? 4 : (512 / BN);
-  static constexpr int kBiasBytes = kAcc * BN * 4;  // tile bias slice, per accumulator
+  // bias is read straight from global memory (uniform across the warp: one
+  // L1 broadcast per float4) rather than staged per tile in shared memory
+  static constexpr int kBiasBytes = 0;
   // 64-wide tiles (the streaming attention contractions, K = S) run two CTAs
   // per SM: two independent load / MMA / epilogue pipelines, each with half
   // the shared memory and TMEM
   static constexpr int kMinBlocks = (BN == 64 && EW == 8 && EPI == kEpiBf16 && CG == 1) ? 2 : 1;
   static constexpr int kStagesRaw =
-      (kSmemBudget / kMinBlocks - 1024 - 256 - kStagingBytes - kBiasBytes) / kStageBytes;
-  static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
+      (kSmemBudget / kMinBlocks - 1024 - 512 - kStagingBytes - kBiasBytes) / kStageBytes;
+  // two-CTA-per-SM contractions measured fastest with 3 stages (S = 288
+  // step, P.V / dV / dK / dQ: 2 stages 2.40 ms, 3 stages 2.12, 4 stages 2.69)
+  static constexpr int kMaxStages = kMinBlocks == 2 ? 3 : 8;
+  static constexpr int kStages = kStagesRaw > kMaxStages ? kMaxStages : kStagesRaw;
   static constexpr int kTmemCols = kAcc * BN;
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 256;
+      kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 512;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
 };
 
@@ -216,8 +228,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // Epilogue math on NV consecutive accumulator columns of one row (values in
-// v, first column col0). `bias_t` points at this chunk's slice of the tile's
-// bias staged in shared memory (or is null); `aux_pre` holds the chunk's aux
+// v, first column col0). `bias_t` points at this chunk's slice of the bias
+// in global memory, p.bias + col0 (or is null); `aux_pre` holds the chunk's aux
 // row prefetched before the TMEM load (or is null: load here). Results in v
 // (and g for the GELU output).
 template <int EPI, int NV>
@@ -232,13 +244,19 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
   }
   if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
     if (bias_t != nullptr) {
+      if (col0 + NV <= p.N && (reinterpret_cast<uintptr_t>(bias_t) & 15) == 0) {
 #pragma unroll
-      for (int q = 0; q < NV / 4; ++q) {
-        const float4 b = *reinterpret_cast<const float4*>(bias_t + 4 * q);  // smem broadcast
-        v[4 * q] += b.x;
-        v[4 * q + 1] += b.y;
-        v[4 * q + 2] += b.z;
-        v[4 * q + 3] += b.w;
+        for (int q = 0; q < NV / 4; ++q) {
+          const float4 b = __ldg(reinterpret_cast<const float4*>(bias_t) + q);  // warp-uniform
+          v[4 * q] += b.x;
+          v[4 * q + 1] += b.y;
+          v[4 * q + 2] += b.z;
+          v[4 * q + 3] += b.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+          if (col0 + i < p.N) v[i] += __ldg(bias_t + i);
       }
     }
   }
@@ -312,6 +330,24 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
   }
 }
 
+// Pipeline trace (build with -DMIMOSE_GEMM_TRACE; tools/gemm_trace.py): CTA 0
+// records SM clocks per tile -- MMA start / last issue / cycles waiting for
+// operands, and per epilogue warp the accumulator wait and the release. Off
+// by default: every GT / GT_CLK compiles to nothing.
+#ifdef MIMOSE_GEMM_TRACE
+__device__ unsigned long long g_gemm_trace[1 << 15];
+__device__ __forceinline__ unsigned long long clk64() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+#define GT(i, v) if (blockIdx.x == 0 && (i) < (1 << 15)) g_gemm_trace[i] = (v)
+#define GT_CLK() clk64()
+#else
+#define GT(i, v)
+#define GT_CLK() 0ull
+#endif
+
 template <int BN, int EPI, int EW, int CG>
 __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::kMinBlocks))
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -330,12 +366,12 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
   uint8_t* sA = smem;
   uint8_t* sB = smem + S * Cfg::kABytes;
   uint8_t* sD = smem + S * Cfg::kStageBytes;  // epilogue staging (1024-aligned)
-  float* sBias = reinterpret_cast<float*>(sD + Cfg::kStagingBytes);  // [kAcc][BN]
   uint64_t* full = reinterpret_cast<uint64_t*>(sD + Cfg::kStagingBytes + Cfg::kBiasBytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;             // [kAcc]
   uint64_t* tempty = tfull + Cfg::kAcc;    // [kAcc]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + Cfg::kAcc);
+  uint64_t* abar = tempty + Cfg::kAcc + 1;  // [EW][kBufs] aux-tile arrivals
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -351,7 +387,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
     tma_prefetch(&tmB);
     if (p.tma_store) {
       tma_prefetch(&tmD);
-      if (EPI == kEpiBiasGelu) tma_prefetch(&tmD2);
+      if (EPI == kEpiBiasGelu || p.aux_tma) tma_prefetch(&tmD2);
     }
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
@@ -361,6 +397,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps * CG);  // one arrive per epilogue warp (of both CTAs)
     }
+    for (int i = 0; i < kEpiWarps * Cfg::kBufs; ++i) mbar_init(&abar[i], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -475,11 +512,15 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       }
       mbar_wait(&tempty[acc], aph ^ 1);
       tc_fence_after();
+      if (lane == 0 && local < 64) GT(local * 8 + 0, GT_CLK());
+      unsigned long long fw = 0;
       const uint32_t d_tmem = tmem_base + acc * BN;
       for (int kb = 0; kb < kb_n; ++kb, ++it) {
         const int s = it % S;
         const uint32_t ph = (it / S) & 1;
+        const unsigned long long w0 = GT_CLK();
         mbar_wait(&full[s], ph);
+        fw += GT_CLK() - w0;
         tc_fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(sA + s * Cfg::kABytes);
@@ -501,6 +542,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
         }
         __syncwarp();
       }
+      if (lane == 0 && local < 64) { GT(local * 8 + 1, GT_CLK()); GT(local * 8 + 2, fw); }
       ++local;
     }
     }
@@ -512,7 +554,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
     constexpr int CB = Cfg::kChunkBytes;
     constexpr int CW = Cfg::kChunkCols;
     constexpr int NCH = CB / 16;        // 16-byte chunks per staged row
-    uint8_t* wbuf = sD + ew * (Cfg::kBufs * Cfg::kNOut * Cfg::kBufBytes);
+    uint8_t* wbuf = sD + ew * (Cfg::kBufs * Cfg::kBufBytes);
     int local = 0, chunk_seq = 0;
     const uint32_t tempty_leader = CG == 2 ? mapa_rank(&tempty[0], 0) : 0u;
     for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
@@ -527,41 +569,62 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       const int b2 = p.splits > 1 ? 0 : z / p.nb1;
       const int acc = local % Cfg::kAcc;
       const uint32_t aph = (local / Cfg::kAcc) & 1;
-      // stage this tile's bias slice once (all 8 epilogue warps, then a named
-      // barrier); double-buffered by accumulator stage
-      float* tb = nullptr;
+      const float* tb = nullptr;  // this tile's bias slice (global)
       if constexpr (EPI == kEpiBf16 || EPI == kEpiBiasGelu) {
-        if (p.bias != nullptr) {
-          tb = sBias + acc * BN;
-          for (int i = ew * 32 + static_cast<int>(lane); i < BN; i += kEpiWarps * 32)
-            tb[i] = n0 + i < p.N ? __ldg(p.bias + n0 + i) : 0.f;
-          asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");
+        if (p.bias != nullptr) tb = p.bias + n0;
+      }
+      const int c_begin = part * (BN / Cfg::kColParts), c_end = c_begin + BN / Cfg::kColParts;
+      // aux tiles by TMA: request the first kBufs chunks now (the buffers are
+      // free once every earlier store has read them), so the loads overlap
+      // the wait for the accumulator
+      const bool aux_tma = (EPI == kEpiBf16 || EPI == kEpiDGelu) && p.aux_tma;
+      auto issue_aux = [&](int c, int seq) {
+        uint64_t* bar = &abar[ew * Cfg::kBufs + seq % Cfg::kBufs];
+        mbar_arrive_expect_tx(bar, Cfg::kBufBytes);
+        tma_load_4d(&tmD2, bar, wbuf + (seq % Cfg::kBufs) * Cfg::kBufBytes, n0 + c,
+                    m0 + quarter * 32, b1, b2);
+      };
+      if (aux_tma && lane == 0) {
+        bulk_wait_read<0>();
+        for (int k = 0; k < Cfg::kBufs; ++k) {
+          const int c = c_begin + k * CW;
+          if (c >= c_end || n0 + c >= p.N) break;
+          issue_aux(c, chunk_seq + k);
         }
       }
+      if (lane == 0 && local < 64) GT(4096 + (local * 16 + ew) * 2, GT_CLK());
       mbar_wait(&tfull[acc], aph);
       tc_fence_after();
+      if (lane == 0 && local < 64) GT(4096 + (local * 16 + ew) * 2 + 1, GT_CLK());
 
       const int row = m0 + quarter * 32 + static_cast<int>(lane);
       const bool row_ok = row < p.M;
       const long long obase = (long long)b2 * p.obs2 + (long long)b1 * p.obs1 +
                               (long long)row * p.ldo;
       const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-      const int c_begin = part * (BN / Cfg::kColParts), c_end = c_begin + BN / Cfg::kColParts;
 
       if (p.tma_store) {
         // ---- staged path: TMEM -> regs -> swizzled smem -> TMA store
 #pragma unroll 1
         for (int c = c_begin; c < c_end; c += CW, ++chunk_seq) {
           if (n0 + c >= p.N) break;
-          uint8_t* sb = wbuf + (chunk_seq % Cfg::kBufs) * (Cfg::kNOut * Cfg::kBufBytes);
-          // the store that last used this buffer has read it
-          if (lane == 0) bulk_wait_read<Cfg::kBufs - 1>();
+          uint8_t* sb = wbuf + (chunk_seq % Cfg::kBufs) * Cfg::kBufBytes;
+          // the store that last used this buffer has read it (aux by TMA: the
+          // buffer was freed before its load was issued)
+          if (!aux_tma && lane == 0) bulk_wait_read<Cfg::kBufs - 1>();
           __syncwarp();
           float v[CW], g[CW];
           // issue the aux-row loads before waiting on TMEM so the two latencies overlap
           uint4 aux_pre[CW / 8];
           bool have_pre = false;
-          if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
+          const uint32_t rbase = smem_u32(sb) + lane * CB;
+          const uint32_t sw = CB == 128 ? (lane & 7) : ((lane >> 1) & 3);
+          if (aux_tma) {
+            mbar_wait(&abar[ew * Cfg::kBufs + chunk_seq % Cfg::kBufs], (chunk_seq / Cfg::kBufs) & 1);
+#pragma unroll
+            for (int j = 0; j < NCH; ++j) aux_pre[j] = ld_shared_v4(rbase + ((j ^ sw) << 4));
+            have_pre = true;
+          } else if constexpr (EPI == kEpiBf16 || EPI == kEpiDGelu) {
             if (p.aux != nullptr && row_ok && p.vec && n0 + c + CW <= p.N) {
               const __nv_bfloat16* ax = p.aux + obase + n0 + c;
 #pragma unroll
@@ -581,8 +644,6 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
           }
           epilogue_math<EPI, CW>(v, g, p, obase, n0 + c, row_ok, tb ? tb + c : nullptr,
                                  have_pre ? aux_pre : nullptr);
-          const uint32_t rbase = smem_u32(sb) + lane * CB;
-          const uint32_t sw = CB == 128 ? (lane & 7) : ((lane >> 1) & 3);
 #pragma unroll
           for (int j = 0; j < NCH; ++j) {
             const uint32_t addr = rbase + ((j ^ sw) << 4);
@@ -595,20 +656,35 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
                            pack_bf16x2(v[8 * j + 4], v[8 * j + 5]),
                            pack_bf16x2(v[8 * j + 6], v[8 * j + 7]));
             }
-            if constexpr (EPI == kEpiBiasGelu) {
-              st_shared_v4(addr + Cfg::kBufBytes, pack_bf16x2(g[8 * j], g[8 * j + 1]),
-                           pack_bf16x2(g[8 * j + 2], g[8 * j + 3]),
-                           pack_bf16x2(g[8 * j + 4], g[8 * j + 5]),
-                           pack_bf16x2(g[8 * j + 6], g[8 * j + 7]));
-            }
           }
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
             tma_store_4d(&tmD, sb, n0 + c, m0 + quarter * 32, b1, b2);
-            if constexpr (EPI == kEpiBiasGelu)
-              tma_store_4d(&tmD2, sb + Cfg::kBufBytes, n0 + c, m0 + quarter * 32, b1, b2);
             bulk_commit();
+            // the next chunk's aux tile into this buffer once the store has read it
+            const int cn = c + Cfg::kBufs * CW;
+            if (aux_tma && cn < c_end && n0 + cn < p.N) {
+              bulk_wait_read<0>();
+              issue_aux(cn, chunk_seq + Cfg::kBufs);
+            }
+          }
+          if constexpr (EPI == kEpiBiasGelu) {
+            // second output through the same buffer once the first store has read it
+            if (lane == 0) bulk_wait_read<0>();
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < NCH; ++j)
+              st_shared_v4(rbase + ((j ^ sw) << 4), pack_bf16x2(g[8 * j], g[8 * j + 1]),
+                           pack_bf16x2(g[8 * j + 2], g[8 * j + 3]),
+                           pack_bf16x2(g[8 * j + 4], g[8 * j + 5]),
+                           pack_bf16x2(g[8 * j + 6], g[8 * j + 7]));
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_store_4d(&tmD2, sb, n0 + c, m0 + quarter * 32, b1, b2);
+              bulk_commit();
+            }
           }
         }
       } else {
@@ -676,6 +752,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       }
       tc_fence_before();
       __syncwarp();
+      if (lane == 0 && local < 64) GT(8192 + (local * 16 + ew), GT_CLK());
       if (lane == 0) {
         if constexpr (CG == 2) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * sizeof(uint64_t)));
         else mbar_arrive(&tempty[acc]);

@@ -39,6 +39,23 @@ def main():
     for name, (fn, fl) in cases.items():
         ms = t(fn)
         print(f"{name}: {ms*1e3:8.1f} us  {fl / ms / 1e9:8.1f} TFLOP/s")
+    if "--variants" in sys.argv:
+        # epilogue-warp count x CTA pairing for the epilogue-heavy shapes
+        for cg in (1, 2):
+            for ew in (8, 16):
+                for name, fn in (
+                        ("ffn1 gelu", lambda: ops.gemm(X, W1, out_f, epi=ops.EPI_BIAS_GELU, out2=out2,
+                                                       bias=b1, force_ew=ew, force_cg=cg)),
+                        ("ffn1 plain", lambda: ops.gemm(X, W1, out_f, force_ew=ew, force_cg=cg)),
+                        ("dgelu", lambda: ops.gemm(dY, W2, out_f, b_mn=True, epi=ops.EPI_DGELU,
+                                                   aux=U, force_ew=ew, force_cg=cg))):
+                    try:
+                        ms = t(fn)
+                    except Exception as e:  # configuration not instantiated
+                        print(f"{name:10s} cg{cg} ew{ew}: n/a ({e})")
+                        continue
+                    print(f"{name:10s} cg{cg} ew{ew}: {ms*1e3:8.1f} us  "
+                          f"{2 * T * F * H / ms / 1e9:8.1f} TFLOP/s")
 
 
 if __name__ == "__main__":
