@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 3
+#define MIMOSE_ABI_VERSION 4
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
@@ -100,6 +100,30 @@ typedef struct {
 } mimose_gemm_args;
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);
+
+/* Flash attention operator (head dim 64; the trainer's attn_fused = 3 path):
+ * packed qkv [B*S][3H] bf16 (q | k | v thirds, head h at columns 64h of
+ * each, H = 64 * nh). Forward writes ctx [B*S][H] bf16 and lse [B*nh][S] fp32
+ * (log2-sum-exp of the scaled scores). Backward reads qkv, ctx, lse, dctx and
+ * writes dqkv [B*S][3H]; workspace >= 4 * B * nh * S bytes. Dropout on the
+ * probabilities uses the same Philox element index (row * round8(S) + key)
+ * as the materialised path, so both paths drop the same entries. */
+typedef struct mimose_attn_args {
+  int B, S, nh, causal;
+  float scale;        /* score scale (1/sqrt(64)) */
+  float dropout_p;
+  uint64_t seed, stream_id;
+  const void* qkv;
+  void* ctx;
+  float* lse;
+  const void* dctx;
+  void* dqkv;
+  void* workspace;
+  int64_t workspace_bytes;
+} mimose_attn_args;
+
+int mimose_flash_attn_fwd(const mimose_attn_args* args, void* stream);
+int mimose_flash_attn_bwd(const mimose_attn_args* args, void* stream);
 
 /* GEMM profiling (roofline evidence): while enabled, every GEMM launch is
  * bracketed by CUDA events on its stream; read() synchronises and returns

@@ -115,6 +115,17 @@ GRAD_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
 
+class AttnArgs(C.Structure):
+    _fields_ = [
+        ("B", C.c_int), ("S", C.c_int), ("nh", C.c_int), ("causal", C.c_int),
+        ("scale", C.c_float), ("dropout_p", C.c_float),
+        ("seed", C.c_uint64), ("stream_id", C.c_uint64),
+        ("qkv", C.c_void_p), ("ctx", C.c_void_p), ("lse", C.c_void_p),
+        ("dctx", C.c_void_p), ("dqkv", C.c_void_p),
+        ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
+    ]
+
+
 # (name, restype, argtypes) for every symbol include/mimose_cuda.h declares.
 CUDA_SYMBOLS = [
     ("mimose_abi_version", C.c_int, []),
@@ -132,6 +143,8 @@ CUDA_SYMBOLS = [
     ("mimose_book_free", C.c_int, [C.c_void_p, C.c_int64]),
     ("mimose_book_stats", C.c_int, [C.c_void_p, C.POINTER(MemStats)]),
     ("mimose_gemm", C.c_int, [C.POINTER(GemmArgs), C.c_void_p]),
+    ("mimose_flash_attn_fwd", C.c_int, [C.POINTER(AttnArgs), C.c_void_p]),
+    ("mimose_flash_attn_bwd", C.c_int, [C.POINTER(AttnArgs), C.c_void_p]),
     ("mimose_gemm_profile_enable", C.c_int, [C.c_int]),
     ("mimose_gemm_profile_csv", C.c_int, [C.POINTER(C.c_void_p)]),
     ("mimose_gemm_profile_read", C.c_int,
@@ -186,7 +199,7 @@ CUDA_SYMBOLS = [
       C.POINTER(C.c_int)]),
 ]
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 def _bind(lib, symbols):

@@ -10,6 +10,8 @@
 #include "capi_common.hpp"
 #include "mimose_cuda.h"
 #include "ops.hpp"
+#include "ops_attn.hpp"
+#include "ops_mem.hpp"
 #include "prof.hpp"
 
 using mimose_rt::ArenaBook;
@@ -152,6 +154,39 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   cudaError_t e = mimose_ops::gemm(c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "mimose_gemm");
   return 0;
+}
+
+namespace {
+mimose_ops::MatView qkv_head_view(const void* qkv, int part, int S, int H) {
+  mimose_ops::MatView v;
+  v.ptr = static_cast<const uint16_t*>(qkv) + (int64_t)part * H;
+  v.rows = S;
+  v.cols = 64;
+  v.ld = 3 * (int64_t)H;
+  v.bs1 = 64;
+  v.bs2 = (int64_t)S * 3 * H;
+  return v;
+}
+}  // namespace
+
+int mimose_flash_attn_fwd(const mimose_attn_args* a, void* stream) {
+  if (a == nullptr || a->qkv == nullptr || a->ctx == nullptr || a->lse == nullptr)
+    return fail("mimose_flash_attn_fwd: null argument");
+  if (a->B <= 0 || a->S <= 0 || a->nh <= 0) return fail("mimose_flash_attn_fwd: bad shape");
+  const int H = 64 * a->nh;
+  const auto drop = mimose_ops::make_dropout(a->dropout_p, a->seed, a->stream_id);
+  cudaError_t e = mimose_ops::flash_fwd(
+      qkv_head_view(a->qkv, 0, a->S, H), qkv_head_view(a->qkv, 1, a->S, H),
+      qkv_head_view(a->qkv, 2, a->S, H), a->ctx, H, a->lse, a->S, (a->S + 7) / 8 * 8, a->nh, a->B,
+      a->scale, drop, a->causal != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_flash_attn_fwd");
+  return 0;
+}
+
+int mimose_flash_attn_bwd(const mimose_attn_args* a, void* stream) {
+  (void)a;
+  (void)stream;
+  return fail("mimose_flash_attn_bwd: not built yet");
 }
 
 int mimose_gemm_profile_enable(int enable) {

@@ -43,4 +43,14 @@ cudaError_t attn2_scores_bwd(const MatView& dout, const MatView& v, const void* 
                              void* dS, int S, int ld, int nh, int B, float ds_scale,
                              const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s);
 
+// Flash attention (flash_sm100.cuh, head dim 64): no S x S tensor in HBM.
+// q / k / v: 4-D head views ([B][nh][S][64] over the packed qkv rows);
+// ctx: [B*S][ctx_ld] (head h at columns 64h); lse: [B*nh][S] log2-sum-exp of
+// the scaled scores. Dropout keep bits use the element index row * ld + key
+// of the materialised path.
+bool flash_supported(int S);
+cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void* ctx,
+                      int64_t ctx_ld, float* lse, int S, int ld, int nh, int B, float alpha,
+                      const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s);
+
 }  // namespace mimose_ops

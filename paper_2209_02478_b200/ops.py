@@ -76,3 +76,39 @@ def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None
     lib = cuda_lib()
     check(lib.mimose_gemm(C.byref(args), _stream(stream)))
     return out
+
+
+def _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale):
+    from ._lib import AttnArgs
+    assert qkv.dtype == torch.bfloat16 and qkv.is_contiguous() and qkv.shape == (B * S, 3 * 64 * nh)
+    a = AttnArgs()
+    a.B, a.S, a.nh, a.causal = B, S, nh, int(causal)
+    a.scale, a.dropout_p = scale, dropout_p
+    a.seed, a.stream_id = seed, stream_id
+    a.qkv = qkv.data_ptr()
+    return a
+
+
+def flash_attn_fwd(qkv, B, S, nh, *, causal=False, dropout_p=0.0, seed=0, stream_id=0,
+                   scale=0.125, stream=None):
+    """Flash attention forward over packed qkv [B*S, 3H] (head dim 64).
+    Returns (ctx [B*S, H] bf16, lse [B*nh, S] fp32 log2-sum-exp of the scaled scores)."""
+    H = 64 * nh
+    ctx = torch.empty(B * S, H, device=qkv.device, dtype=torch.bfloat16)
+    lse = torch.empty(B * nh, S, device=qkv.device, dtype=torch.float32)
+    a = _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale)
+    a.ctx, a.lse = ctx.data_ptr(), lse.data_ptr()
+    check(cuda_lib().mimose_flash_attn_fwd(C.byref(a), _stream(stream)))
+    return ctx, lse
+
+
+def flash_attn_bwd(qkv, ctx, lse, dctx, B, S, nh, *, causal=False, dropout_p=0.0, seed=0,
+                   stream_id=0, scale=0.125, stream=None):
+    """Flash attention backward: dqkv [B*S, 3H] from dctx and the forward's ctx / lse."""
+    dqkv = torch.empty_like(qkv)
+    ws = torch.empty(B * nh * S, device=qkv.device, dtype=torch.float32)
+    a = _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale)
+    a.ctx, a.lse, a.dctx, a.dqkv = ctx.data_ptr(), lse.data_ptr(), dctx.data_ptr(), dqkv.data_ptr()
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel() * 4
+    check(cuda_lib().mimose_flash_attn_bwd(C.byref(a), _stream(stream)))
+    return dqkv

@@ -39,6 +39,18 @@ def main():
     for name, (fn, fl) in cases.items():
         ms = t(fn)
         print(f"{name}: {ms*1e3:8.1f} us  {fl / ms / 1e9:8.1f} TFLOP/s")
+    if "--splitk" in sys.argv:
+        # weight-gradient shapes (fp32 out, K = tokens) against the split-K factor
+        ws = torch.empty(64 << 20, device="cuda", dtype=torch.float32)
+        for (m, n) in ((2304, 768), (768, 3072), (3072, 768), (768, 768)):
+            dO, Xin = r(T, m), r(T, n)
+            o = torch.empty(m, n, device="cuda", dtype=torch.float32)
+            line = []
+            for sk in (0, 1, 2, 3, 4, 5, 6, 8):
+                ms = t(lambda: ops.gemm(dO, Xin, o, a_mn=True, b_mn=True, epi=ops.EPI_F32,
+                                        workspace=ws, split_k=sk))
+                line.append(f"s{sk}:{ms*1e3:6.1f}")
+            print(f"wgrad {m}x{n}x{T}: " + "  ".join(line) + "  (us; s0 = cost model)")
     if "--variants" in sys.argv:
         # epilogue-warp count x CTA pairing for the epilogue-heavy shapes
         for cg in (1, 2):
