@@ -105,7 +105,8 @@ int mimose_gemm(const mimose_gemm_args* args, void* stream);
  * packed qkv [B*S][3H] bf16 (q | k | v thirds, head h at columns 64h of
  * each, H = 64 * nh). Forward writes ctx [B*S][H] bf16 and lse [B*nh][S] fp32
  * (log2-sum-exp of the scaled scores). Backward reads qkv, ctx, lse, dctx and
- * writes dqkv [B*S][3H]; workspace >= 4 * B * nh * S bytes. Dropout on the
+ * writes dqkv [B*S][3H]; workspace >= 4 * B * nh * S bytes. With dropout the
+ * forward also writes one keep bit per score (keep_mask) for the backward. Dropout on the
  * probabilities uses the same Philox element index (row * round8(S) + key)
  * as the materialised path, so both paths drop the same entries. */
 typedef struct mimose_attn_args {
@@ -116,6 +117,7 @@ typedef struct mimose_attn_args {
   const void* qkv;
   void* ctx;
   float* lse;
+  uint32_t* keep_mask; /* dropout_p > 0: keep bits [B*nh*S][ceil(S/32)] (fwd out, bwd in) */
   const void* dctx;
   void* dqkv;
   void* workspace;

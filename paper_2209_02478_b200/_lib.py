@@ -120,7 +120,7 @@ class AttnArgs(C.Structure):
         ("B", C.c_int), ("S", C.c_int), ("nh", C.c_int), ("causal", C.c_int),
         ("scale", C.c_float), ("dropout_p", C.c_float),
         ("seed", C.c_uint64), ("stream_id", C.c_uint64),
-        ("qkv", C.c_void_p), ("ctx", C.c_void_p), ("lse", C.c_void_p),
+        ("qkv", C.c_void_p), ("ctx", C.c_void_p), ("lse", C.c_void_p), ("keep_mask", C.c_void_p),
         ("dctx", C.c_void_p), ("dqkv", C.c_void_p),
         ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
     ]

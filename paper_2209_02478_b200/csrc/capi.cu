@@ -177,16 +177,31 @@ int mimose_flash_attn_fwd(const mimose_attn_args* a, void* stream) {
   const auto drop = mimose_ops::make_dropout(a->dropout_p, a->seed, a->stream_id);
   cudaError_t e = mimose_ops::flash_fwd(
       qkv_head_view(a->qkv, 0, a->S, H), qkv_head_view(a->qkv, 1, a->S, H),
-      qkv_head_view(a->qkv, 2, a->S, H), a->ctx, H, a->lse, a->S, (a->S + 7) / 8 * 8, a->nh, a->B,
-      a->scale, drop, a->causal != 0, static_cast<cudaStream_t>(stream));
+      qkv_head_view(a->qkv, 2, a->S, H), a->ctx, H, a->lse, a->keep_mask, a->S,
+      (a->S + 7) / 8 * 8, a->nh, a->B, a->scale, drop, a->causal != 0,
+      static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "mimose_flash_attn_fwd");
   return 0;
 }
 
 int mimose_flash_attn_bwd(const mimose_attn_args* a, void* stream) {
-  (void)a;
-  (void)stream;
-  return fail("mimose_flash_attn_bwd: not built yet");
+  if (a == nullptr || a->qkv == nullptr || a->ctx == nullptr || a->lse == nullptr ||
+      a->dctx == nullptr || a->dqkv == nullptr)
+    return fail("mimose_flash_attn_bwd: null argument");
+  if (a->B <= 0 || a->S <= 0 || a->nh <= 0) return fail("mimose_flash_attn_bwd: bad shape");
+  if (a->dropout_p > 0.f && a->keep_mask == nullptr)
+    return fail("mimose_flash_attn_bwd: dropout needs the forward's keep_mask");
+  if (a->workspace == nullptr || a->workspace_bytes < (int64_t)4 * a->B * a->nh * a->S)
+    return fail("mimose_flash_attn_bwd: workspace < 4 * B * nh * S bytes");
+  const int H = 64 * a->nh;
+  const auto drop = mimose_ops::make_dropout(a->dropout_p, a->seed, a->stream_id);
+  cudaError_t e = mimose_ops::flash_bwd(
+      qkv_head_view(a->qkv, 0, a->S, H), qkv_head_view(a->qkv, 1, a->S, H),
+      qkv_head_view(a->qkv, 2, a->S, H), a->ctx, a->dctx, H, a->lse, a->keep_mask,
+      static_cast<float*>(a->workspace), a->dqkv, a->S, (a->S + 7) / 8 * 8, a->nh, a->B, a->scale,
+      drop, a->causal != 0, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_flash_attn_bwd");
+  return 0;
 }
 
 int mimose_gemm_profile_enable(int enable) {

@@ -7,6 +7,8 @@
 #include "ops_attn.hpp"
 #include "prof.hpp"
 
+#include <algorithm>
+
 namespace mimose_ops {
 
 namespace {
@@ -47,19 +49,49 @@ cudaError_t launch_flash(Kern kern, int smem, int threads, int tiles, const CUte
   return cudaGetLastError();
 }
 
+template <typename Kern>
+cudaError_t launch_flash4(Kern kern, int smem, int threads, int tiles, const CUtensorMap& a,
+                          const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
+                          const mimose_dev::FlashParams& p, cudaStream_t s, bool& configured) {
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  const int grid = tiles < flash_sm_count() ? tiles : flash_sm_count();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, d, p);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool flash_supported(int S) { return S >= 1 && S <= 8192; }
 
 cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void* ctx,
-                      int64_t ctx_ld, float* lse, int S, int ld, int nh, int B, float alpha,
-                      const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s) {
+                      int64_t ctx_ld, float* lse, uint32_t* mask, int S, int ld, int nh, int B,
+                      float alpha, const mimose_dev::DropoutCfg& drop, bool causal,
+                      cudaStream_t s) {
   if (!flash_supported(S) || (ctx_ld * 2) % 16 || (reinterpret_cast<uintptr_t>(ctx) & 15))
     return cudaErrorInvalidValue;
   const double nz = (double)nh * B;
   const double pairs = causal ? 0.5 * S * (double)(S + 1) : (double)S * S;
   // QK^T and P V; q, k, v read, ctx + lse written
-  ProfScope prof("attn_flash_fwd", 4.0 * 64 * pairs * nz, nz * (8.0 * S * 64 + 4.0 * S), s);
+  const int mw = (S + 31) / 32;
+  const bool with_mask = mask != nullptr && drop.threshold != 0;
+  ProfScope prof("attn_flash_fwd", 4.0 * 64 * pairs * nz,
+                 nz * (8.0 * S * 64 + 4.0 * S + (with_mask ? 4.0 * S * mw : 0.0)), s);
   CUtensorMap tq, tk, tv;
   if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
       !make_operand_map(&tv, v, nh, B, 64))
@@ -72,10 +104,86 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   p.ctx = static_cast<__nv_bfloat16*>(ctx);
   p.ctx_ld = ctx_ld;
   p.lse = lse;
+  p.mask = with_mask ? mask : nullptr;
+  p.mw = mw;
   static bool configured = false;
   using Cfg = mimose_dev::FlashFwdCfg;
   return launch_flash(mimose_dev::flash_fwd_kernel, Cfg::kSmemBytes, Cfg::kThreads,
                       ((S + 127) / 128) * nh * B, tq, tk, tv, p, s, configured);
 }
 
+cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, const void* ctx,
+                      const void* dctx, int64_t ctx_ld, const float* lse, const uint32_t* mask,
+                      float* dvec, void* dqkv, int S, int ld, int nh, int B, float alpha,
+                      const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s) {
+  if (!flash_supported(S) || (ctx_ld * 2) % 16 || (drop.threshold != 0 && mask == nullptr))
+    return cudaErrorInvalidValue;
+  const double nz = (double)nh * B;
+  const double pairs = causal ? 0.5 * S * (double)(S + 1) : (double)S * S;
+  const int mw = (S + 31) / 32;
+  {
+    // D = rowsum(dO o O): dctx and ctx read, one float per row written
+    ProfScope prof("attn_flash_rowdot", 0.0, nz * (4.0 * S * 64 + 4.0 * S), s);
+    const int64_t n = (int64_t)B * S * nh;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * flash_sm_count());
+    mimose_dev::flash_rowdot_kernel<<<blocks, 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(dctx), static_cast<const __nv_bfloat16*>(ctx), ctx_ld,
+        S, nh, B, dvec);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  MatView dov;
+  dov.ptr = dctx;
+  dov.rows = S;
+  dov.cols = 64;
+  dov.ld = ctx_ld;
+  dov.bs1 = 64;
+  dov.bs2 = (int64_t)S * ctx_ld;
+  CUtensorMap tq, tk, tv, to;
+  if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
+      !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128))
+    return cudaErrorInvalidValue;
+  mimose_dev::FlashParams p{};
+  p.S = S; p.nh = nh; p.B = B; p.ld = ld;
+  p.sc = alpha * 1.4426950408889634f;
+  p.drop = drop;
+  p.causal = causal ? 1 : 0;
+  p.ctx_ld = ctx_ld;
+  p.lse = const_cast<float*>(lse);
+  p.mask = const_cast<uint32_t*>(mask);
+  p.mw = mw;
+  p.dvec = dvec;
+  p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
+  p.ds_scale = alpha;
+  using Cfg = mimose_dev::FlashBwdCfg;
+  const int items = ((S + 127) / 128) * nh * B;
+  const double mbytes = drop.threshold != 0 ? 4.0 * S * mw : 0.0;
+  {
+    // S, dPd recomputed; dV, dK accumulated: 4 MMAs per (query, key) block pair
+    ProfScope prof("attn_flash_bwd_kv", 8.0 * 64 * pairs * nz,
+                   nz * (8.0 * S * 64 + 8.0 * S + mbytes + 4.0 * S * 64), s);
+    static bool configured = false;
+    cudaError_t e = launch_flash4(mimose_dev::flash_bwd_kernel<0>, Cfg::kSmemKV, Cfg::kThreads,
+                                  items, tq, tk, tv, to, p, s, configured);
+    if (e != cudaSuccess) return e;
+  }
+  {
+    // S, dPd recomputed; dQ accumulated: 3 MMAs per block pair
+    ProfScope prof("attn_flash_bwd_q", 6.0 * 64 * pairs * nz,
+                   nz * (8.0 * S * 64 + 8.0 * S + mbytes + 2.0 * S * 64), s);
+    static bool configured = false;
+    return launch_flash4(mimose_dev::flash_bwd_kernel<1>, Cfg::kSmemQ, Cfg::kThreads, items, tq,
+                         tk, tv, to, p, s, configured);
+  }
+}
+
 }  // namespace mimose_ops
+
+#ifdef MIMOSE_FLASH_TRACE
+extern "C" int mimose_debug_flash_trace(void* dst) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(dst, mimose_dev::g_flash_trace, 4096 * 8);
+  return 0;
+}
+#endif

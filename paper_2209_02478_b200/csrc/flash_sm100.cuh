@@ -42,6 +42,8 @@ struct FlashParams {
   __nv_bfloat16* ctx;   // fwd out: [B*S][ctx_ld], head h at columns 64h
   long long ctx_ld;
   float* lse;           // fwd out / bwd in: [B*nh][S]
+  uint32_t* mask;       // fwd out / bwd in (dropout only): keep bits [B*nh*S][mw],
+  int mw;               //   bit e of word (row, k) = key 32k + e kept
   // backward
   const __nv_bfloat16* dctx;  // [B*S][ctx_ld]
   const float* dvec;          // [B*nh][S] rowsum(dO o O)
@@ -74,6 +76,21 @@ __device__ __forceinline__ uint32_t fl_pack(float a, float b) {
 }
 
 __device__ __forceinline__ void fl_epi_bar() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+
+// Pipeline trace (build with -DMIMOSE_FLASH_TRACE): CTA 0 stamps SM clocks.
+#ifdef MIMOSE_FLASH_TRACE
+__device__ unsigned long long g_flash_trace[4096];
+__device__ __forceinline__ unsigned long long fl_clk() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+#define FT(i, v) if (blockIdx.x == 0 && (i) < 4096) g_flash_trace[i] = (v)
+#define FT_CLK() fl_clk()
+#else
+#define FT(i, v)
+#define FT_CLK() 0ull
+#endif
 
 __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -164,6 +181,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     int kv = 0, jb = 0, tc = 0;
     // O_w += P_b[:, 32w..32w+31] V[32w..32w+31, :] for block b (j-th of its tile)
     auto issue_pv = [&](int b, int j, int stage) {
+      if (lane == 0 && b < 256) FT(b * 4 + 1, FT_CLK());
       if (j == 0) {
         mbar_wait(oempty, (tc & 1) ^ 1);  // the previous tile's O has been read
         tc_fence_after();
@@ -187,6 +205,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         __syncwarp();
       }
       if (lane == 0) umma_commit(&empty[stage]);
+      if (lane == 0 && b < 256) FT(b * 4 + 2, FT_CLK());
       __syncwarp();
     };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
@@ -199,6 +218,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         mbar_wait(&full[s], (kv / NS) & 1);
         mbar_wait(&sempty[jb & 1], ((jb >> 1) & 1) ^ 1);
         tc_fence_after();
+        if (lane == 0 && jb < 256) FT(jb * 4 + 0, FT_CLK());
         if (lane == 0) {
           const uint32_t qa = smem_u32(sQ), ka = smem_u32(sKV + s * Cfg::kKVBytes);
 #pragma unroll
@@ -235,27 +255,46 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
       const int i = qt * 128 + r;
       const bool row_ok = i < p.S;
       const int64_t grow = (int64_t)z * p.S + (row_ok ? i : 0);
+      const bool warp_dead = qt * 128 + quarter * 32 >= p.S;  // all 32 rows past the end
       float m_used = kNegInf, l = 0.f;
       for (int j = 0; j < nkb; ++j, ++jb) {
         const int sb = jb & 1;
+        const bool trw = lane == 0 && (ew == 0 || ew == 15) && jb < 128;
+        [[maybe_unused]] const int tro = 1024 + jb * 8 + (ew == 15 ? 4 : 0);
+        if (trw) FT(tro + 0, FT_CLK());
         mbar_wait(&sfull[sb], (jb >> 1) & 1);
         tc_fence_after();
         uint32_t raw[32];
         tmem_ld32_nowait(lane_base + sb * 128 + 32 * w, raw);
         tmem_wait_ld();
+        if (trw) FT(tro + 1, FT_CLK());
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
         const int c0 = j * 128 + 32 * w;
         int lim = p.S - c0;  // valid keys of the slice: c0 + e < S (and <= i if causal)
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
-        float s[32];
-        float mb = kNegInf;
+        if (warp_dead) lim = 0;
+        // warp-uniform paths: every key valid (no per-score test) / none valid
+        // (past the sequence end or above the diagonal: P = 0, no Philox)
+        const bool all_full = __all_sync(0xffffffffu, lim >= 32);
+        const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
+        float x[32];
+        float mraw = kNegInf;
+        if (all_full) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          s[e] = e < lim ? __uint_as_float(raw[e]) * p.sc : kNegInf;
-          mb = fmaxf(mb, s[e]);
+          for (int e = 0; e < 32; ++e) {
+            x[e] = __uint_as_float(raw[e]);
+            mraw = fmaxf(mraw, x[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            x[e] = e < lim ? __uint_as_float(raw[e]) : kNegInf;
+            mraw = fmaxf(mraw, x[e]);
+          }
         }
+        const float mb = mraw * p.sc;
         if (j == 0) {
           m_used = mb;
         } else {
@@ -284,26 +323,40 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         // this P buffer is free once the P V of two blocks ago has run
         mbar_wait(&pvdone[sb * 4 + w], ((jb >> 1) & 1) ^ 1);
         const float m_eff = m_used == kNegInf ? 0.f : m_used;
-        uint32_t rnd[4][4];
-        if (thr_hi != 0) {
-          uint64_t grp[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)grow * p.ld + c0 + 8 * q) >> 3;
-          philox_n<4>(p.drop.seed, p.drop.stream, grp, rnd);
-        }
         float psum = 0.f;
         uint32_t pk[16];
+        if (all_dead) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float a0 = fl_ex2(s[e] - m_eff), a1 = fl_ex2(s[e + 1] - m_eff);
-          psum += a0 + a1;
+          for (int e = 0; e < 16; ++e) pk[e] = 0u;
+        } else {
+          uint32_t rnd[4][4];
           if (thr_hi != 0) {
-            if (!philox_keep_w(rnd[e >> 3], e & 7, thr_hi)) a0 = 0.f;
-            if (!philox_keep_w(rnd[e >> 3], (e & 7) + 1, thr_hi)) a1 = 0.f;
+            uint64_t grp[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)grow * p.ld + c0 + 8 * q) >> 3;
+            philox_n<4>(p.drop.seed, p.drop.stream, grp, rnd);
           }
-          pk[e >> 1] = fl_pack(a0, a1);
+          uint32_t kw = 0;
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            // p = 2^(s * sc - m): one FFMA + ex2 per score
+            float a0 = fl_ex2(fmaf(x[e], p.sc, -m_eff)), a1 = fl_ex2(fmaf(x[e + 1], p.sc, -m_eff));
+            psum += a0 + a1;
+            if (thr_hi != 0) {
+              const bool k0 = philox_keep_w(rnd[e >> 3], e & 7, thr_hi);
+              const bool k1 = philox_keep_w(rnd[e >> 3], (e & 7) + 1, thr_hi);
+              if (!k0) a0 = 0.f;
+              if (!k1) a1 = 0.f;
+              kw |= (k0 ? 1u : 0u) << e;
+              kw |= (k1 ? 2u : 0u) << e;
+            }
+            pk[e >> 1] = fl_pack(a0, a1);
+          }
+          // keep bits for the backward (no Philox there)
+          if (p.mask != nullptr && row_ok) p.mask[grow * p.mw + (c0 >> 5)] = kw;
         }
         l += psum;
+        if (trw) FT(tro + 2, FT_CLK());
         const uint32_t rowa = smem_u32(sP + sb * Cfg::kPBytes + (w >> 1) * 16384) + r * 128;
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -313,10 +366,14 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[sb * 4 + w]);
+        if (trw) FT(tro + 3, FT_CLK());
       }
       // ---- tile end: combine the four slices of each row
+      const bool trf = lane == 0 && ew == 0 && tc < 64;
+      if (trf) FT(2048 + tc * 4 + 0, FT_CLK());
       mbar_wait(ofull, tc & 1);
       tc_fence_after();
+      if (trf) FT(2048 + tc * 4 + 1, FT_CLK());
       float* xm = xch + (tc & 1) * 1024;  // [4 slices][128 rows]
       float* xl = xm + 512;
       xm[w * 128 + r] = m_used;
@@ -355,6 +412,385 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
                             fl_pack(acc[12] * inv, acc[13] * inv),
                             fl_pack(acc[14] * inv, acc[15] * inv));
         if (w == 0) p.lse[grow] = M + __log2f(L);
+      }
+      if (trf) FT(2048 + tc * 4 + 2, FT_CLK());
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ============================================================ backward
+// Deterministic (no atomics), two kernels over the same per-score algebra,
+// with the keep bits the forward stored (no Philox here):
+//   P   = 2^(s sc - lse_i)                 (masked keys: 0)
+//   Pd  = keep ? P / (1-p) : 0             dPd = dO_i . v_j  (TMEM)
+//   dP  = keep ? dPd / (1-p) : 0           dS  = P (dP - D_i) * scale,
+// D_i = dO_i . O_i (flash_rowdot_kernel). Both kernels compute S = Q K^T and
+// dPd = dO V^T into TMEM with the query rows on the TMEM lanes (16 warps:
+// lane quarter x 32-key slice, as the forward), then
+//   flash_bwd_kv_kernel (one 128-key block per work item, loop over query
+//   blocks): dV += Pd^T dO, dK += dS^T Q -- Pd / dS staged in smem as
+//   [query][key] tiles and read by the MMA as MN-major A operands;
+//   flash_bwd_q_kernel (one 128-query block per work item, loop over key
+//   blocks): dQ += dS K with K read as an MN-major B operand.
+struct FlashBwdCfg {
+  static constexpr int kEW = 16;
+  static constexpr int kThreads = 64 + 32 * kEW;
+  static constexpr int kTile = 128 * 64 * 2;      // one 128-row x 64-dim bf16 tile
+  static constexpr int kStages = 2;
+  static constexpr int kSqBytes = 128 * 128 * 2;  // one [query][key] bf16 tile (2 sub-tiles)
+  // kv kernel: K, V + stages of (Q, dO) + Pd + dS ; q kernel: Q, dO + stages of (K, V) + dS
+  static constexpr int kSmemKV = 2 * kTile + kStages * 2 * kTile + 2 * kSqBytes + 1024 + 512;
+  static constexpr int kSmemQ = 2 * kTile + kStages * 2 * kTile + kSqBytes + 1024 + 512;
+};
+
+// per-score backward algebra for one thread's 32-key slice of a query row;
+// Pd (optional) and dS packed as bf16 pairs
+template <bool WITH_PD>
+__device__ __forceinline__ void flash_bwd_slice(const uint32_t (&sraw)[32],
+                                                const uint32_t (&dpraw)[32], int lim, bool all_full,
+                                                float lse, float dvec, uint32_t kw, bool dropout,
+                                                const FlashParams& p, uint32_t (&pk_pd)[16],
+                                                uint32_t (&pk_ds)[16]) {
+  const float neg_inf = -__int_as_float(0x7f800000);
+#pragma unroll
+  for (int e = 0; e < 32; e += 2) {
+    float P[2], dP[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float x = (all_full || e + u < lim) ? __uint_as_float(sraw[e + u]) : neg_inf;
+      P[u] = fl_ex2(fmaf(x, p.sc, -lse));
+      dP[u] = __uint_as_float(dpraw[e + u]);
+      if (dropout) {
+        const bool keep = (kw >> (e + u)) & 1u;
+        dP[u] = keep ? dP[u] * p.drop.scale : 0.f;
+      }
+    }
+    if constexpr (WITH_PD) {
+      float d0 = P[0], d1 = P[1];
+      if (dropout) {
+        d0 = ((kw >> e) & 1u) ? d0 * p.drop.scale : 0.f;
+        d1 = ((kw >> (e + 1)) & 1u) ? d1 * p.drop.scale : 0.f;
+      }
+      pk_pd[e >> 1] = fl_pack(d0, d1);
+    }
+    pk_ds[e >> 1] = fl_pack(P[0] * (dP[0] - dvec) * p.ds_scale, P[1] * (dP[1] - dvec) * p.ds_scale);
+  }
+}
+
+// row r's 32-key slice w of a [query][key] tile (two 64-key SWIZZLE_128B sub-tiles)
+__device__ __forceinline__ void flash_st_slice(uint8_t* tile, int r, int w,
+                                               const uint32_t (&pk)[16]) {
+  const uint32_t rowa = smem_u32(tile + (w >> 1) * 16384) + r * 128;
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    st_shared_v4(rowa + ((((w & 1) * 4 + c) ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1],
+                 pk[4 * c + 2], pk[4 * c + 3]);
+}
+
+// D_i = dO_i . O_i for every (token, head): one thread per pair
+__global__ void flash_rowdot_kernel(const __nv_bfloat16* __restrict__ dctx,
+                                    const __nv_bfloat16* __restrict__ ctx, long long ld, int S,
+                                    int nh, int B, float* __restrict__ dvec) {
+  const long long n = (long long)B * S * nh;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int h = (int)(t % nh);
+    const long long tok = t / nh;
+    const uint4* a = reinterpret_cast<const uint4*>(dctx + tok * ld + h * 64);
+    const uint4* c = reinterpret_cast<const uint4*>(ctx + tok * ld + h * 64);
+    float acc = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const uint4 x = __ldg(a + q), y = __ldg(c + q);
+      const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 fx = __bfloat1622float2(x2[e]), fy = __bfloat1622float2(y2[e]);
+        acc = fmaf(fx.x, fy.x, acc);
+        acc = fmaf(fx.y, fy.y, acc);
+      }
+    }
+    const int b = (int)(tok / S), i = (int)(tok % S);
+    dvec[((long long)b * nh + h) * S + i] = acc;
+  }
+}
+
+// MODE 0: dK / dV kernel (work item = key block); MODE 1: dQ kernel (work item = query block)
+template <int MODE>
+__global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
+    flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ,
+                     const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV,
+                     const __grid_constant__ CUtensorMap tmO, const FlashParams p) {
+  using Cfg = FlashBwdCfg;
+  constexpr int NS = Cfg::kStages;
+  constexpr bool KV = MODE == 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  // fixed pair: KV ? (K, V) : (Q, dO); streamed pairs: KV ? (Q, dO) : (K, V)
+  uint8_t* sFix = smem;
+  uint8_t* sStr = smem + 2 * Cfg::kTile;
+  uint8_t* sDS = sStr + NS * 2 * Cfg::kTile;
+  uint8_t* sPD = sDS + Cfg::kSqBytes;  // KV only
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (KV ? 2 : 1) * Cfg::kSqBytes);
+  uint64_t* full = bars;             // [NS]
+  uint64_t* empty = full + NS;       // [NS]
+  uint64_t* fixfull = empty + NS;
+  uint64_t* fixempty = fixfull + 1;
+  uint64_t* sfull = fixempty + 1;
+  uint64_t* sempty = sfull + 1;
+  uint64_t* pfull = sempty + 1;
+  uint64_t* pdone = pfull + 1;
+  uint64_t* accfull = pdone + 1;
+  uint64_t* accempty = accfull + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  const int nblk = (p.S + 127) / 128;
+  const int num_items = nblk * p.nh * p.B;
+  // inner blocks of work item `blk`: KV: query blocks [causal ? blk : 0, nblk);
+  // Q: key blocks [0, causal ? blk + 1 : nblk)
+  auto inner_range = [&](int blk, int& lo, int& hi) {
+    if (KV) {
+      lo = p.causal ? blk : 0;
+      hi = nblk;
+    } else {
+      lo = 0;
+      hi = p.causal ? blk + 1 : nblk;
+    }
+  };
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ);
+    tma_prefetch(&tmK);
+    tma_prefetch(&tmV);
+    tma_prefetch(&tmO);
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(fixfull, 1);
+    mbar_init(fixempty, 1);
+    mbar_init(sfull, 1);
+    mbar_init(sempty, Cfg::kEW);
+    mbar_init(pfull, Cfg::kEW);
+    mbar_init(pdone, 1);
+    mbar_init(accfull, 1);
+    mbar_init(accempty, Cfg::kEW);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int st = 0, ic = 0;
+      for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
+        const int z = item / nblk, blk = item % nblk;
+        const int h = z % p.nh, b = z / p.nh;
+        mbar_wait(fixempty, (ic & 1) ^ 1);
+        mbar_arrive_expect_tx(fixfull, 2 * Cfg::kTile);
+        tma_load_4d(KV ? &tmK : &tmQ, fixfull, sFix, 0, blk * 128, h, b);
+        tma_load_4d(KV ? &tmV : &tmO, fixfull, sFix + Cfg::kTile, 0, blk * 128, h, b);
+        int lo, hi;
+        inner_range(blk, lo, hi);
+        for (int j = lo; j < hi; ++j, ++st) {
+          const int s = st % NS;
+          mbar_wait(&empty[s], ((st / NS) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], 2 * Cfg::kTile);
+          uint8_t* d = sStr + s * 2 * Cfg::kTile;
+          tma_load_4d(KV ? &tmQ : &tmK, &full[s], d, 0, j * 128, h, b);
+          tma_load_4d(KV ? &tmO : &tmV, &full[s], d + Cfg::kTile, 0, j * 128, h, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
+    // KV: dV += Pd^T dO, dK += dS^T Q (A MN-major [query][key] tiles, B MN-major)
+    // Q : dQ += dS K (A K-major [query][key] tile, B = K MN-major)
+    const uint32_t idesc_acc = idesc_bf16_f32(128, 64, KV, true);
+    int st = 0, ic = 0, blkc = 0;  // blkc: inner blocks processed (barrier phases)
+    auto issue_sdp = [&](int s) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
+      const uint32_t q = smem_u32(KV ? sStr + s * 2 * Cfg::kTile : sFix);
+      const uint32_t k = smem_u32(KV ? sFix : sStr + s * 2 * Cfg::kTile);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem_base, smem_desc_sw128(q + kk * 32, 16, 1024),
+                  smem_desc_sw128(k + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        umma_bf16(tmem_base + 128, smem_desc_sw128(q + Cfg::kTile + kk * 32, 16, 1024),
+                  smem_desc_sw128(k + Cfg::kTile + kk * 32, 16, 1024), idesc_s,
+                  kk != 0 ? 1u : 0u);
+      umma_commit(sfull);
+    };
+    auto issue_acc = [&](int s, bool first) {
+      if (KV) {
+        const uint32_t pd = smem_u32(sPD), ds = smem_u32(sDS);
+        const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kTile);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries, 16 per MMA
+          umma_bf16(tmem_base + 256, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
+                    smem_desc_sw128(q + Cfg::kTile + kk * 2048, 8192, 1024), idesc_acc,
+                    (first && kk == 0) ? 0u : 1u);
+          umma_bf16(tmem_base + 320, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
+                    smem_desc_sw128(q + kk * 2048, 8192, 1024), idesc_acc,
+                    (first && kk == 0) ? 0u : 1u);
+        }
+      } else {
+        const uint32_t ds = smem_u32(sDS);
+        const uint32_t k = smem_u32(sStr + s * 2 * Cfg::kTile);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // K = 128 keys
+          umma_bf16(tmem_base + 256,
+                    smem_desc_sw128(ds + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
+                    smem_desc_sw128(k + kk * 2048, 8192, 1024), idesc_acc,
+                    (first && kk == 0) ? 0u : 1u);
+      }
+      umma_commit(pdone);
+      umma_commit(&empty[s]);
+    };
+    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
+      int lo, hi;
+      inner_range(item % nblk, lo, hi);
+      mbar_wait(fixfull, ic & 1);
+      tc_fence_after();
+      // S / dPd of block j + 1 go in before the accumulation of block j
+      int prev_s = 0;
+      for (int j = lo; j < hi; ++j, ++st, ++blkc) {
+        const int s = st % NS;
+        mbar_wait(&full[s], (st / NS) & 1);
+        mbar_wait(sempty, (blkc & 1) ^ 1);
+        tc_fence_after();
+        if (lane == 0) issue_sdp(s);
+        __syncwarp();
+        if (j > lo) {
+          mbar_wait(pfull, (blkc - 1) & 1);
+          tc_fence_after();
+          if (lane == 0) issue_acc(prev_s, j - 1 == lo);
+          __syncwarp();
+        }
+        prev_s = s;
+        if (j == lo) {
+          // the accumulators are free once the previous item's were read
+          mbar_wait(accempty, (ic & 1) ^ 1);
+          tc_fence_after();
+        }
+      }
+      mbar_wait(pfull, (blkc - 1) & 1);
+      tc_fence_after();
+      if (lane == 0) {
+        issue_acc(prev_s, hi - 1 == lo);
+        umma_commit(accfull);
+        umma_commit(fixempty);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ score warps
+    const int ew = warp - 2;
+    const int quarter = warp & 3;
+    const int w = ew >> 2;
+    const int r = quarter * 32 + static_cast<int>(lane);
+    const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
+    const bool dropout = p.drop.threshold != 0;
+    int ic = 0, blkc = 0;
+    for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
+      const int z = item / nblk, blk = item % nblk;
+      const int h = z % p.nh, b = z / p.nh;
+      int lo, hi;
+      inner_range(blk, lo, hi);
+      for (int j = lo; j < hi; ++j, ++blkc) {
+        const int qb = KV ? j : blk, kb = KV ? blk : j;  // query / key block
+        const int i = qb * 128 + r;
+        const bool row_ok = i < p.S;
+        const int64_t grow = (int64_t)z * p.S + (row_ok ? i : 0);
+        // per-row scalars and keep bits first: their loads overlap the MMA
+        const float lse = p.lse[grow], dv = p.dvec[grow];
+        const int c0 = kb * 128 + 32 * w;
+        int lim = p.S - c0;
+        if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
+        if (!row_ok) lim = 0;
+        const uint32_t kw = (dropout && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
+        mbar_wait(sfull, blkc & 1);
+        tc_fence_after();
+        uint32_t sraw[32], dpraw[32];
+        tmem_ld32_nowait(lane_base + 32 * w, sraw);
+        tmem_ld32_nowait(lane_base + 128 + 32 * w, dpraw);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty);
+        const bool all_full = __all_sync(0xffffffffu, lim >= 32);
+        const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
+        uint32_t pk_pd[16], pk_ds[16];
+        if (all_dead) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk_pd[e] = pk_ds[e] = 0u;
+        } else {
+          flash_bwd_slice<KV>(sraw, dpraw, lim, all_full, lse, dv, kw, dropout, p, pk_pd, pk_ds);
+        }
+        // the previous block's accumulation MMAs have read the staged tiles
+        mbar_wait(pdone, (blkc & 1) ^ 1);
+        if (KV) flash_st_slice(sPD, r, w, pk_pd);
+        flash_st_slice(sDS, r, w, pk_ds);
+        fence_async_shared();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(pfull);
+      }
+      // ---- item end: accumulators out (TMEM lanes = the item's 128 rows)
+      mbar_wait(accfull, ic & 1);
+      tc_fence_after();
+      const int row = blk * 128 + r;  // key (KV) or query (Q) row of this lane
+      if (KV) {
+        uint32_t o[32];
+        tmem_ld32_nowait(lane_base + 256 + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(accempty);
+        if (row < p.S) {
+          const long long H = p.ctx_ld;
+          __nv_bfloat16* dst = p.dqkv + ((long long)b * p.S + row) * 3 * H + (w < 2 ? 2 * H : H) +
+                               h * 64 + 32 * (w & 1);
+          uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            d4[q] = make_uint4(fl_pack(__uint_as_float(o[8 * q]), __uint_as_float(o[8 * q + 1])),
+                               fl_pack(__uint_as_float(o[8 * q + 2]), __uint_as_float(o[8 * q + 3])),
+                               fl_pack(__uint_as_float(o[8 * q + 4]), __uint_as_float(o[8 * q + 5])),
+                               fl_pack(__uint_as_float(o[8 * q + 6]), __uint_as_float(o[8 * q + 7])));
+        }
+      } else {
+        float o[16];
+        tmem_ld16(lane_base + 256 + 16 * w, o);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(accempty);
+        if (row < p.S) {
+          const long long H = p.ctx_ld;
+          uint4* d4 = reinterpret_cast<uint4*>(p.dqkv + ((long long)b * p.S + row) * 3 * H +
+                                               h * 64 + 16 * w);
+          d4[0] = make_uint4(fl_pack(o[0], o[1]), fl_pack(o[2], o[3]), fl_pack(o[4], o[5]),
+                             fl_pack(o[6], o[7]));
+          d4[1] = make_uint4(fl_pack(o[8], o[9]), fl_pack(o[10], o[11]), fl_pack(o[12], o[13]),
+                             fl_pack(o[14], o[15]));
+        }
       }
     }
   }

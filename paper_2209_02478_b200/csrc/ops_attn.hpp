@@ -49,8 +49,16 @@ cudaError_t attn2_scores_bwd(const MatView& dout, const MatView& v, const void* 
 // the scaled scores. Dropout keep bits use the element index row * ld + key
 // of the materialised path.
 bool flash_supported(int S);
+// mask (dropout only, may be null): keep bits [B*nh*S][ceil(S/32)] uint32 for
+// the backward
 cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void* ctx,
-                      int64_t ctx_ld, float* lse, int S, int ld, int nh, int B, float alpha,
+                      int64_t ctx_ld, float* lse, uint32_t* mask, int S, int ld, int nh, int B,
+                      float alpha, const mimose_dev::DropoutCfg& drop, bool causal,
+                      cudaStream_t s);
+// dqkv from dctx and the forward's ctx / lse / mask; dvec: [B*nh*S] fp32 workspace
+cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, const void* ctx,
+                      const void* dctx, int64_t ctx_ld, const float* lse, const uint32_t* mask,
+                      float* dvec, void* dqkv, int S, int ld, int nh, int B, float alpha,
                       const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s);
 
 }  // namespace mimose_ops

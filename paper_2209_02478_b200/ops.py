@@ -92,23 +92,28 @@ def _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale):
 def flash_attn_fwd(qkv, B, S, nh, *, causal=False, dropout_p=0.0, seed=0, stream_id=0,
                    scale=0.125, stream=None):
     """Flash attention forward over packed qkv [B*S, 3H] (head dim 64).
-    Returns (ctx [B*S, H] bf16, lse [B*nh, S] fp32 log2-sum-exp of the scaled scores)."""
+    Returns (ctx [B*S, H] bf16, lse [B*nh, S] fp32 log2-sum-exp of the scaled scores,
+    keep mask [B*nh*S, ceil(S/32)] int32 bits or None without dropout)."""
     H = 64 * nh
     ctx = torch.empty(B * S, H, device=qkv.device, dtype=torch.bfloat16)
     lse = torch.empty(B * nh, S, device=qkv.device, dtype=torch.float32)
+    mask = (torch.zeros(B * nh * S, (S + 31) // 32, device=qkv.device, dtype=torch.int32)
+            if dropout_p > 0 else None)
     a = _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale)
     a.ctx, a.lse = ctx.data_ptr(), lse.data_ptr()
+    a.keep_mask = mask.data_ptr() if mask is not None else None
     check(cuda_lib().mimose_flash_attn_fwd(C.byref(a), _stream(stream)))
-    return ctx, lse
+    return ctx, lse, mask
 
 
-def flash_attn_bwd(qkv, ctx, lse, dctx, B, S, nh, *, causal=False, dropout_p=0.0, seed=0,
+def flash_attn_bwd(qkv, ctx, lse, mask, dctx, B, S, nh, *, causal=False, dropout_p=0.0, seed=0,
                    stream_id=0, scale=0.125, stream=None):
     """Flash attention backward: dqkv [B*S, 3H] from dctx and the forward's ctx / lse."""
     dqkv = torch.empty_like(qkv)
     ws = torch.empty(B * nh * S, device=qkv.device, dtype=torch.float32)
     a = _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale)
     a.ctx, a.lse, a.dctx, a.dqkv = ctx.data_ptr(), lse.data_ptr(), dctx.data_ptr(), dqkv.data_ptr()
+    a.keep_mask = mask.data_ptr() if mask is not None else None
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel() * 4
     check(cuda_lib().mimose_flash_attn_bwd(C.byref(a), _stream(stream)))
     return dqkv

@@ -47,7 +47,7 @@ def test_flash_fwd_matches_fp32(cuda_device, S, causal, p):
     g = torch.Generator(device="cpu").manual_seed(S * 7 + causal)
     qkv = (torch.randn(B * S, 3 * 64 * nh, generator=g) * 1.5).to(torch.bfloat16).to(cuda_device)
     seed, stream = 1234, 77
-    ctx, lse = ops.flash_attn_fwd(qkv, B, S, nh, causal=causal, dropout_p=p, seed=seed,
+    ctx, lse, _ = ops.flash_attn_fwd(qkv, B, S, nh, causal=causal, dropout_p=p, seed=seed,
                                   stream_id=stream)
     torch.cuda.synchronize()
     ref, lse_ref = _ref(qkv, B, S, nh, causal, p, seed, stream)
@@ -63,3 +63,49 @@ def test_flash_fwd_deterministic(cuda_device):
     a = ops.flash_attn_fwd(qkv, B, S, nh, dropout_p=0.1, seed=5, stream_id=9)
     b = ops.flash_attn_fwd(qkv, B, S, nh, dropout_p=0.1, seed=5, stream_id=9)
     assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def _ref_grads(qkv, dctx, B, S, nh, causal, p, seed, stream, scale=0.125):
+    x = qkv.float().clone().requires_grad_(True)
+    ctx, _ = _ref(x, B, S, nh, causal, p, seed, stream, scale)
+    ctx.backward(dctx.float())
+    return x.grad
+
+
+@pytest.mark.parametrize("S", [64, 128, 200, 288, 512, 700])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_flash_bwd_matches_fp32(cuda_device, S, causal, p):
+    """dqkv through the two backward kernels vs autograd of the fp32 restatement
+    (bf16 P / dS operands and bf16 dqkv: 2e-2 of the largest gradient)."""
+    from paper_2209_02478_b200 import ops
+    B, nh = 2, 3
+    g = torch.Generator(device="cpu").manual_seed(S * 11 + causal)
+    qkv = (torch.randn(B * S, 3 * 64 * nh, generator=g) * 1.5).to(torch.bfloat16).to(cuda_device)
+    dctx = torch.randn(B * S, 64 * nh, generator=g).to(torch.bfloat16).to(cuda_device)
+    seed, stream = 99, 5
+    ctx, lse, mask = ops.flash_attn_fwd(qkv, B, S, nh, causal=causal, dropout_p=p, seed=seed,
+                                        stream_id=stream)
+    dqkv = ops.flash_attn_bwd(qkv, ctx, lse, mask, dctx, B, S, nh, causal=causal, dropout_p=p,
+                              seed=seed, stream_id=stream)
+    torch.cuda.synchronize()
+    ref = _ref_grads(qkv, dctx, B, S, nh, causal, p, seed, stream)
+    for t in range(3):  # q, k, v thirds
+        got = dqkv[:, t * 64 * nh:(t + 1) * 64 * nh].float()
+        exp = ref[:, t * 64 * nh:(t + 1) * 64 * nh]
+        err = (got - exp).abs().max().item()
+        assert err <= 2e-2 * exp.abs().max().item(), (t, err, exp.abs().max().item())
+
+
+def test_flash_keep_mask_matches_oracle(cuda_device):
+    """The forward's keep bits are the oracle's Philox keep mask at the
+    materialised path's element index."""
+    from paper_2209_02478_b200 import ops
+    B, S, nh, p = 2, 200, 2, 0.1
+    qkv = torch.randn(B * S, 3 * 64 * nh, device=cuda_device).to(torch.bfloat16)
+    _, _, mask = ops.flash_attn_fwd(qkv, B, S, nh, dropout_p=p, seed=3, stream_id=4)
+    m = mask.cpu().numpy().view(np.uint32)
+    bits = ((m[:, :, None] >> np.arange(32, dtype=np.uint32)) & 1).reshape(B * nh * S, -1)[:, :S]
+    ld = (S + 7) // 8 * 8
+    idx = np.arange(B * nh * S, dtype=np.int64)[:, None] * ld + np.arange(S, dtype=np.int64)
+    assert np.array_equal(bits.astype(bool), bert_ref.keep_mask(p, 3, 4, idx))
