@@ -122,6 +122,19 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
   const int tiles_m = (p.S + 127) / 128;
   const int num_tiles = tiles_m * p.nh * p.B;
   auto nkb_of = [&](int qt) { return p.causal ? (qt + 1 < tiles_m ? qt + 1 : tiles_m) : tiles_m; };
+  // tile -> (head z, query tile qt). Causal: longest tiles first, heads
+  // fastest, so the static round-robin over CTAs stays balanced (with
+  // z-major order and 148 % tiles_m == 0 a CTA would always get the same qt)
+  auto decode = [&](int tile, int& z, int& qt) {
+    if (p.causal) {
+      const int nz = p.nh * p.B;
+      qt = tiles_m - 1 - tile / nz;
+      z = tile % nz;
+    } else {
+      z = tile / tiles_m;
+      qt = tile % tiles_m;
+    }
+  };
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmQ);
@@ -157,7 +170,8 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     if (lane == 0) {
       int kv = 0, tc = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
-        const int z = tile / tiles_m, qt = tile % tiles_m;
+        int z, qt;
+        decode(tile, z, qt);
         const int h = z % p.nh, b = z / p.nh;
         mbar_wait(qempty, (tc & 1) ^ 1);
         mbar_arrive_expect_tx(qfull, Cfg::kQBytes);
@@ -209,7 +223,9 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
       __syncwarp();
     };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
-      const int nkb = nkb_of(tile % tiles_m);
+      int z_, qt_;
+      decode(tile, z_, qt_);
+      const int nkb = nkb_of(qt_);
       mbar_wait(qfull, tc & 1);
       tc_fence_after();
       int prev_stage = 0;
@@ -249,7 +265,8 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     const float kNegInf = -__int_as_float(0x7f800000);
     int jb = 0, tc = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
-      const int z = tile / tiles_m, qt = tile % tiles_m;
+      int z, qt;
+      decode(tile, z, qt);
       const int h = z % p.nh, b = z / p.nh;
       const int nkb = nkb_of(qt);
       const int i = qt * 128 + r;
@@ -558,6 +575,17 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
   const int num_items = nblk * p.nh * p.B;
   // inner blocks of work item `blk`: KV: query blocks [causal ? blk : 0, nblk);
   // Q: key blocks [0, causal ? blk + 1 : nblk)
+  // item -> (head z, block). Causal: most inner blocks first, heads fastest
+  auto decode = [&](int item, int& z, int& blk) {
+    if (p.causal) {
+      const int nz = p.nh * p.B;
+      blk = KV ? item / nz : nblk - 1 - item / nz;
+      z = item % nz;
+    } else {
+      z = item / nblk;
+      blk = item % nblk;
+    }
+  };
   auto inner_range = [&](int blk, int& lo, int& hi) {
     if (KV) {
       lo = p.causal ? blk : 0;
@@ -599,7 +627,8 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     if (lane == 0) {
       int st = 0, ic = 0;
       for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
-        const int z = item / nblk, blk = item % nblk;
+        int z, blk;
+        decode(item, z, blk);
         const int h = z % p.nh, b = z / p.nh;
         mbar_wait(fixempty, (ic & 1) ^ 1);
         mbar_arrive_expect_tx(fixfull, 2 * Cfg::kTile);
@@ -666,7 +695,9 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     };
     for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
       int lo, hi;
-      inner_range(item % nblk, lo, hi);
+      int z_, blk_;
+      decode(item, z_, blk_);
+      inner_range(blk_, lo, hi);
       mbar_wait(fixfull, ic & 1);
       tc_fence_after();
       // S / dPd of block j + 1 go in before the accumulation of block j
@@ -710,7 +741,8 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     const bool dropout = p.drop.threshold != 0;
     int ic = 0, blkc = 0;
     for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
-      const int z = item / nblk, blk = item % nblk;
+      int z, blk;
+      decode(item, z, blk);
       const int h = z % p.nh, b = z / p.nh;
       int lo, hi;
       inner_range(blk, lo, hi);

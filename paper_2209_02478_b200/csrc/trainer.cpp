@@ -419,7 +419,9 @@ void Trainer::build_params() {
 
 // attn_fused: 0 = QK^T GEMM + softmax kernels; 1 = block-looped fused score
 // kernels (attn2_sm100.cuh: any S <= 2048, causal too); 2 = single-row fused
-// kernels (attn_sm100.cuh: S <= 512, causal too)
+// kernels (attn_sm100.cuh: S <= 512, causal too); 3 = flash attention
+// (flash_sm100.cuh: no S x S tensor at all -- the block saves one fp32
+// log-sum-exp per row and, with dropout, one keep bit per score)
 // Dropped-out attention probabilities Pd are saved by default. With
 // MIMOSE_SAVE_PD=0 the backward regenerates them from the saved P with the
 // same Philox stream (bit-identical values), trading a 4 B/score elementwise
@@ -438,6 +440,7 @@ bool Trainer::save_pd() const {
 int Trainer::fused_attn(int S) const {
   if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
   if (t_.attn_fused == 2 && mimose_ops::attn_fused_supported(S)) return 2;
+  if (t_.attn_fused == 3 && mimose_ops::flash_supported(S)) return 3;
   return 0;
 }
 
@@ -515,6 +518,9 @@ int64_t Trainer::block_work_bytes(int S) const {
   const bool hid = m_.hidden_dropout > 0.f;
   const int64_t pd = m_.attn_dropout > 0.f ? quad : 0;
   const int fused = fused_attn(S);
+  const bool flash = fused == 3;
+  const int64_t lse = 4 * B * nh_ * (int64_t)S;
+  const int64_t kmask = m_.attn_dropout > 0.f ? 4 * B * nh_ * (int64_t)S * ((S + 31) / 32) : 0;
   int64_t live = act, peak = act;  // dy
   auto take_b = [&](int64_t n) { live += n; peak = std::max(peak, live); };
   auto drop_b = [&](int64_t n) { live -= n; };
@@ -538,6 +544,13 @@ int64_t Trainer::block_work_bytes(int S) const {
     take_b(act);                                // dz1
     drop_b(act); drop_b(act); drop_b(st);       // dh1, z1, st1
   }
+  if (flash) {
+    take_b(act);                                // dctx
+    if (hid) drop_b(act);                       // da
+    take_b(qkv3); take_b(lse);                  // dqkv, D = rowsum(dO o O)
+    drop_b(lse); drop_b(act); drop_b(lse);      // D, dctx, saved lse
+    drop_b(kmask); drop_b(qkv3); drop_b(act);   // keep bits, qkv, ctx
+  } else {
   if (fused != 1) drop_b(act);                  // ctx
   take_b(act);                                  // dctx
   if (hid) drop_b(act);                         // da
@@ -548,10 +561,12 @@ int64_t Trainer::block_work_bytes(int S) const {
   drop_b(act); drop_b(quad);                    // dctx, P
   drop_b(quad); drop_b(qkv3);                   // dP, qkv
   if (fused == 1) drop_b(act);                  // ctx
+  }
   take_b(act);                                  // dx
   if (pre) take_b(act);                         // dx1
   // forward: the unfused path's score buffer lives next to the block's saves
   const int64_t fwd = fused ? 0 : quad;
+  (void)lse;
   return std::max(peak, fwd);
 }
 
@@ -583,15 +598,22 @@ void Trainer::build_spec() {
   spec_.constant_footprint = constant_bytes_;
   spec_.input_min = (int64_t)t_.batch * t_.seq_min;
   spec_.input_max = (int64_t)t_.batch * t_.seq_max;
-  const double p_quad = (save_pd() ? 2.0 : 1.0) * nh_ * 2.0 / B;
+  const bool flash = t_.attn_fused == 3;
+  // per-layer quadratic term: P (+ Pd) for the materialised paths, the keep
+  // bits (1 bit per score) for flash attention; flash adds 4 B per row (lse)
+  const double p_quad = flash ? (m_.attn_dropout > 0.f ? nh_ / (8.0 * B) : 0.0)
+                              : (save_pd() ? 2.0 : 1.0) * nh_ * 2.0 / B;
+  const double lin_extra = flash ? 4.0 * nh_ : 0.0;
   for (int l = 0; l < L_; ++l) {
     mimose::LayerSpec ls;
     ls.id = l;
     ls.position = l;
     ls.stage_id = l;
-    ls.category = mimose::LayerCategory::QuadraticStructure;
+    // flash attention without dropout saves nothing quadratic: a(x) is linear
+    ls.category = p_quad > 0.0 ? mimose::LayerCategory::QuadraticStructure
+                               : mimose::LayerCategory::ImplicitReduction;
     // prior a(x): saved tensors per token + materialised probabilities
-    ls.activation_coeffs = {0.0, static_cast<double>(16 * H + 4 * F + 16), p_quad};
+    ls.activation_coeffs = {0.0, static_cast<double>(16 * H + 4 * F + 16) + lin_extra, p_quad};
     ls.boundary_coeffs = {0.0, static_cast<double>(2 * H)};
     ls.forward_time_coeffs = {0.01, 1e-6};
     spec_.layers.push_back(ls);
@@ -638,6 +660,27 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   run_gemm(linear_call(x, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
                        p32_ + P.bqkv.off),
            s);
+  if (fused_attn(S) == 3) {
+    // flash: ctx plus one fp32 log-sum-exp per row (and keep bits) instead of P / Pd
+    const auto fdrop =
+        mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+    void* lse = take(4 * (int64_t)g.B * nh * S, act_tag);
+    void* kmask = m_.attn_dropout > 0.f
+                      ? take(4 * (int64_t)g.B * nh * S * ((S + 31) / 32), act_tag)
+                      : nullptr;
+    void* ctx = take(T * H * 2, act_tag);
+    ck(mimose_ops::flash_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H),
+                             head_view(qkv, 2 * H, S, 3 * H), ctx, H, static_cast<float*>(lse),
+                             static_cast<uint32_t*>(kmask), S, ld, nh, g.B, 0.125f, fdrop,
+                             m_.causal != 0, s),
+       "flash_fwd");
+    if (keep) {
+      save->qkv = qkv; save->lse = lse; save->mask = kmask;
+    } else {
+      drop(qkv); drop(lse); drop(kmask);
+    }
+    return ctx;
+  }
   void* Pm = take(quad, act_tag);
   // Pd: only the P V operand unless saved (save_pd); the backward regenerates it
   void* Pd = m_.attn_dropout > 0.f ? take(quad, save_pd() ? act_tag : kTagTransient) : nullptr;
@@ -707,6 +750,23 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
   // dPd = dctx V^T ; dV = Pd^T dctx ; dS = softmax'(dP) ; dQ = dS K ; dK = dS^T Q
   void* dqkv = take(T * 3 * H * 2, kTagTransient);
+  if (fused_attn(S) == 3) {
+    const auto fdrop =
+        mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+    void* dvec = take(4 * (int64_t)g.B * nh * S, kTagTransient);
+    ck(mimose_ops::flash_bwd(head_view(sv.qkv, 0, S, 3 * H), head_view(sv.qkv, H, S, 3 * H),
+                             head_view(sv.qkv, 2 * H, S, 3 * H), sv.ctx, dctx, H,
+                             static_cast<const float*>(sv.lse),
+                             static_cast<const uint32_t*>(sv.mask), static_cast<float*>(dvec),
+                             dqkv, S, ld, nh, g.B, 0.125f, fdrop, m_.causal != 0, s),
+       "flash_bwd");
+    drop(dvec);
+    drop(dctx);
+    drop(sv.lse);
+    drop(sv.mask);
+    drop(sv.qkv);
+    return dqkv;
+  }
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
   if (sv.Pd == nullptr && m_.attn_dropout > 0.f) {
     // regenerate Pd = keep * P / (1 - p) from the saved P (same Philox
@@ -891,7 +951,7 @@ void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const St
 
 void Trainer::free_save(LayerSave& sv) {
   drop(sv.qkv); drop(sv.P); drop(sv.Pd); drop(sv.ctx); drop(sv.z1); drop(sv.st1); drop(sv.h1);
-  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2);
+  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2); drop(sv.lse); drop(sv.mask);
 }
 
 // ----------------------------------------------------------- layer backward
@@ -982,12 +1042,13 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   void* dap = da ? da : dh1;
   // output projection: dWo = da^T ctx ; dctx = da Wo
   run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
-  if (fused_attn(g.S) != 1) drop(sv.ctx);  // else attn_bwd reads it (rowsum(dP o P) = dO . ctx)
+  // attn_fused 1 / 3 read ctx in attn_bwd (rowsum(dP o P) = dO . ctx)
+  if (fused_attn(g.S) != 1 && fused_attn(g.S) != 3) drop(sv.ctx);
   void* dctx = take(T * H * 2, kTagTransient);
   run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
   drop(da);
   void* dqkv = attn_bwd(l, sv, dctx, g, s);
-  if (fused_attn(g.S) == 1) drop(sv.ctx);
+  if (fused_attn(g.S) == 1 || fused_attn(g.S) == 3) drop(sv.ctx);
   // QKV projection: dbqkv, dWqkv = dqkv^T xin
   ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
      "colsum");

@@ -38,6 +38,7 @@ struct LayerSave {
   void *qkv = nullptr, *P = nullptr, *Pd = nullptr, *ctx = nullptr, *z1 = nullptr,
        *h1 = nullptr, *u = nullptr, *g = nullptr, *z2 = nullptr, *st1 = nullptr,
        *st2 = nullptr;
+  void *lse = nullptr, *mask = nullptr;  // flash attention (attn_fused = 3) instead of P / Pd
 };
 
 struct StepGeo {

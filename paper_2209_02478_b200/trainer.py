@@ -75,7 +75,8 @@ class TrainConfig:
     # the epilogue; S <= 512, causal too, else the pair below); 1 =
     # block-looped fused kernels (attn2_sm100.cuh: any S <= 2048, causal too;
     # correct but slower than both others today - profiles/README.md);
-    # 0 = QK^T GEMM + softmax kernels
+    # 0 = QK^T GEMM + softmax kernels; 3 = flash attention (flash_sm100.cuh:
+    # no S x S tensor saved or written -- lse per row + keep bits; any S)
     attn_fused: int = 2
     # automatic reserve sized for each step's S (extras_bytes(S) + 2 %) instead
     # of seq_max: short inputs then keep more blocks (fewer recomputes)

@@ -53,7 +53,7 @@ def _grads_by_name(tr):
     return {name: g[off:off + n].copy() for name, (off, n) in tr.param_table().items()}
 
 
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [16, 45, 96])
 def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
@@ -115,7 +115,7 @@ def _check_grads(got, ref_grads):
             assert cos >= 0.995, f"{name}: cosine {cos}"
 
 
-@pytest.mark.parametrize("attn", [2, 0])
+@pytest.mark.parametrize("attn", [2, 0, 3])
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [24, 61, 200])
@@ -183,7 +183,7 @@ def test_variant_device_inputs_match_host(cuda_device, variant):
     assert torch.equal(out[0][1], out[1][1])
 
 
-@pytest.mark.parametrize("fused", [0, 1, 2])
+@pytest.mark.parametrize("fused", [0, 1, 2, 3])
 def test_checkpointed_grads_bitwise_equal_plain(cuda_device, fused):
     """Recompute is deterministic: dropping any subset of blocks gives the
     exact same gradients (dropout on, so Philox regeneration is exercised)."""
@@ -357,7 +357,7 @@ def test_native_dp_world1_bucketed_allreduce_is_identity(cuda_device):
 LONG = dict(TINY, layers=1, max_pos=640)
 
 
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [300, 520])
@@ -379,7 +379,7 @@ def test_long_sequence_attention_vs_cpu_oracle(cuda_device, S, dropout, causal, 
 
 
 @pytest.mark.parametrize("S", [300, 600])
-@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("mode", [1, 2, 3])
 @pytest.mark.parametrize("causal", [False, True])
 def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode, S):
     """Recompute through the block-looped kernels is bit-exact at S > 512."""

@@ -40,6 +40,23 @@ def main():
                                                   dropout_p=0.1, seed=1, stream_id=2))
                 line += f"  bwd {ub:8.1f} us {2.5 * fl / ub / 1e6:7.1f} TFLOP/s"
             print(line, flush=True)
+            if "--classes" in sys.argv:
+                import ctypes as C
+                from paper_2209_02478_b200 import _lib
+                lib = _lib.cuda_lib()
+                lib.mimose_profile_enable(1)
+                ctx, lse, mask = f()
+                d = torch.randn_like(ctx)
+                ops.flash_attn_bwd(qkv, ctx, lse, mask, d, B, S, nh, causal=causal, dropout_p=0.1,
+                                   seed=1, stream_id=2)
+                torch.cuda.synchronize()
+                p = C.c_void_p()
+                lib.mimose_profile_csv(C.byref(p))
+                text = _lib.take_string(lib, p)
+                lib.mimose_profile_enable(0)
+                for row in text.strip().splitlines()[1:]:
+                    c = row.split(",")
+                    print(f"    {c[0]:22s} {float(c[-1]) * 1e3:8.1f} us")
 
 
 if __name__ == "__main__":
