@@ -64,6 +64,11 @@ def parse():
                          "stream (length-synchronised sampling, no stragglers; data differs per "
                          "rank); 'per-rank' = seed base+rank (independent lengths, max-over-"
                          "ranks straggler cost)")
+    ap.add_argument("--attn", default="flash", choices=["flash", "materialised"],
+                    help="attention kernels of the measured runs: flash (attn_fused 3, no S x S "
+                         "tensor) or materialised (attn_fused 2, P / Pd saved like the reference "
+                         "model). The budget denominator is always the materialised model's "
+                         "no-ckpt peak (the reference model's memory semantics)")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu (no comparison arms, no cpu baseline)")
     args = ap.parse_args()
@@ -277,6 +282,7 @@ def run_gpu_arm(args, rank, world, local):
 
     lib = _lib.cuda_lib()
     model_cfg, train_cfg = PRESETS[args.preset]
+    train_cfg = dataclasses.replace(train_cfg, attn_fused=3 if args.attn == "flash" else 2)
     B = train_cfg.batch
     S_max = train_cfg.seq_max
     stream = torch.cuda.current_stream()
@@ -286,7 +292,11 @@ def run_gpu_arm(args, rank, world, local):
     free, total = torch.cuda.mem_get_info()
     ranks_here = max(1, world // max(1, torch.cuda.device_count()))
     probe_budget = int(min(free * 0.85 / ranks_here, 150 * GiB))
-    probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"), probe_budget, local)
+    # the reference model (HF BERT / GPT-2) materialises P and dropout(P): the
+    # budget is a fraction of THAT model's no-checkpoint peak, whichever
+    # attention kernels the measured runs use
+    probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none", attn_fused=2),
+                    probe_budget, local)
     rng = np.random.default_rng(args.seed + 1000 * rank)
     probe.step(*synthetic_task_batch(rng, model_cfg, B, S_max), optimizer=False, stream=stream)
     peak_none = int(allmax(probe.rows[-1]["peak_reserved"], world))
@@ -502,6 +512,9 @@ def run_gpu_arm(args, rank, world, local):
                 "dp_size_stream": args.size_stream,
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
                 "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
+                "attention": args.attn,
+                "budget_basis": "no-ckpt peak of the materialised-attention model at S_max "
+                                "(reference memory semantics)",
                 "l2": "not flushed: per-step working set (GBs of activations) >> 126 MB L2",
                 "calibration": f"{calib} planner-calibration steps (sheltered collection window "
                                f"+ fit) run before warm-up, {calib_s:.2f} s",

@@ -50,8 +50,8 @@ def main():
     ap.add_argument("--gemm-csv", default="")
     ap.add_argument("--attn-fused", action="store_true", help="(default) fused score kernels")
     ap.add_argument("--attn-unfused", action="store_true", help="GEMM + softmax kernel pair")
-    ap.add_argument("--attn-mode", type=int, default=2,
-                    help="TrainConfig.attn_fused when fused: 2 single-row, 1 block-looped")
+    ap.add_argument("--attn-mode", type=int, default=3,
+                    help="TrainConfig.attn_fused when fused: 3 flash, 2 single-row, 1 block-looped")
     ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
     args = ap.parse_args()
     import numpy as np
@@ -61,7 +61,8 @@ def main():
     m, t = PRESETS[args.preset]
     GiB = 1 << 30
     rng = np.random.default_rng(0)
-    probe = Trainer(m, dataclasses.replace(t, planner="none"), 60 * GiB)
+    # budget basis: the materialised-attention model's no-ckpt peak (as bench.py)
+    probe = Trainer(m, dataclasses.replace(t, planner="none", attn_fused=2), 60 * GiB)
     probe.step(*synthetic_task_batch(rng, m, t.batch, t.seq_max), optimizer=False)
     peak = probe.rows[-1]["peak_reserved"]
     probe.close()
