@@ -50,9 +50,10 @@ cudaError_t launch_flash(Kern kern, int smem, int threads, int tiles, const CUte
 }
 
 template <typename Kern>
-cudaError_t launch_flash4(Kern kern, int smem, int threads, int tiles, const CUtensorMap& a,
+cudaError_t launch_flash5(Kern kern, int smem, int threads, int tiles, const CUtensorMap& a,
                           const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
-                          const mimose_dev::FlashParams& p, cudaStream_t s, bool& configured) {
+                          const CUtensorMap& e5, const mimose_dev::FlashParams& p,
+                          cudaStream_t s, bool& configured) {
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
@@ -69,7 +70,7 @@ cudaError_t launch_flash4(Kern kern, int smem, int threads, int tiles, const CUt
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, d, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, d, e5, p);
   if (e != cudaSuccess) return e;
   count_launch();
   return cudaGetLastError();
@@ -121,18 +122,6 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   const double nz = (double)nh * B;
   const double pairs = causal ? 0.5 * S * (double)(S + 1) : (double)S * S;
   const int mw = (S + 31) / 32;
-  {
-    // D = rowsum(dO o O): dctx and ctx read, one float per row written
-    ProfScope prof("attn_flash_rowdot", 0.0, nz * (4.0 * S * 64 + 4.0 * S), s);
-    const int64_t n = (int64_t)B * S * nh;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * flash_sm_count());
-    mimose_dev::flash_rowdot_kernel<<<blocks, 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(dctx), static_cast<const __nv_bfloat16*>(ctx), ctx_ld,
-        S, nh, B, dvec);
-    count_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-  }
   MatView dov;
   dov.ptr = dctx;
   dov.rows = S;
@@ -140,9 +129,12 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   dov.ld = ctx_ld;
   dov.bs1 = 64;
   dov.bs2 = (int64_t)S * ctx_ld;
-  CUtensorMap tq, tk, tv, to;
+  MatView cv = dov;
+  cv.ptr = ctx;
+  CUtensorMap tq, tk, tv, to, tc;
   if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
-      !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128))
+      !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128) ||
+      !make_operand_map(&tc, cv, nh, B, 128))
     return cudaErrorInvalidValue;
   mimose_dev::FlashParams p{};
   p.S = S; p.nh = nh; p.B = B; p.ld = ld;
@@ -160,21 +152,23 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   const int items = ((S + 127) / 128) * nh * B;
   const double mbytes = drop.threshold != 0 ? 4.0 * S * mw : 0.0;
   {
+    // S, dPd recomputed; dQ accumulated: 3 MMAs per block pair; also
+    // D = dO . O per row (dO, O tiles read once per query block)
+    ProfScope prof("attn_flash_bwd_q", 6.0 * 64 * pairs * nz,
+                   nz * (10.0 * S * 64 + 8.0 * S + mbytes + 2.0 * S * 64), s);
+    static bool configured = false;
+    cudaError_t e = launch_flash5(mimose_dev::flash_bwd_kernel<1>, Cfg::kSmemQ, Cfg::kThreads,
+                                  items, tq, tk, tv, to, tc, p, s, configured);
+    if (e != cudaSuccess) return e;
+  }
+
+  {
     // S, dPd recomputed; dV, dK accumulated: 4 MMAs per (query, key) block pair
     ProfScope prof("attn_flash_bwd_kv", 8.0 * 64 * pairs * nz,
                    nz * (8.0 * S * 64 + 8.0 * S + mbytes + 4.0 * S * 64), s);
     static bool configured = false;
-    cudaError_t e = launch_flash4(mimose_dev::flash_bwd_kernel<0>, Cfg::kSmemKV, Cfg::kThreads,
-                                  items, tq, tk, tv, to, p, s, configured);
-    if (e != cudaSuccess) return e;
-  }
-  {
-    // S, dPd recomputed; dQ accumulated: 3 MMAs per block pair
-    ProfScope prof("attn_flash_bwd_q", 6.0 * 64 * pairs * nz,
-                   nz * (8.0 * S * 64 + 8.0 * S + mbytes + 2.0 * S * 64), s);
-    static bool configured = false;
-    return launch_flash4(mimose_dev::flash_bwd_kernel<1>, Cfg::kSmemQ, Cfg::kThreads, items, tq,
-                         tk, tv, to, p, s, configured);
+    return launch_flash5(mimose_dev::flash_bwd_kernel<0>, Cfg::kSmemKV, Cfg::kThreads, items,
+                         tq, tk, tv, to, to, p, s, configured);
   }
 }
 

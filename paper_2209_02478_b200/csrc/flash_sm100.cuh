@@ -46,7 +46,7 @@ struct FlashParams {
   int mw;               //   bit e of word (row, k) = key 32k + e kept
   // backward
   const __nv_bfloat16* dctx;  // [B*S][ctx_ld]
-  const float* dvec;          // [B*nh][S] rowsum(dO o O)
+  float* dvec;                // [B*nh][S] rowsum(dO o O) (dQ kernel writes, dK/dV reads)
   __nv_bfloat16* dqkv;        // [B*S][3 * ctx_ld]
   float ds_scale;             // score scale folded into dS (1/sqrt(64))
 };
@@ -446,7 +446,8 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
 //   P   = 2^(s sc - lse_i)                 (masked keys: 0)
 //   Pd  = keep ? P / (1-p) : 0             dPd = dO_i . v_j  (TMEM)
 //   dP  = keep ? dPd / (1-p) : 0           dS  = P (dP - D_i) * scale,
-// D_i = dO_i . O_i (flash_rowdot_kernel). Both kernels compute S = Q K^T and
+// D_i = dO_i . O_i (the dQ kernel, which runs first, computes it from its
+// staged dO / O tiles and stores it for the dK / dV kernel). Both kernels compute S = Q K^T and
 // dPd = dO V^T into TMEM with the query rows on the TMEM lanes (16 warps:
 // lane quarter x 32-key slice, as the forward), then
 //   flash_bwd_kv_kernel (one 128-key block per work item, loop over query
@@ -460,42 +461,38 @@ struct FlashBwdCfg {
   static constexpr int kTile = 128 * 64 * 2;      // one 128-row x 64-dim bf16 tile
   static constexpr int kStages = 2;
   static constexpr int kSqBytes = 128 * 128 * 2;  // one [query][key] bf16 tile (2 sub-tiles)
-  // kv kernel: K, V + stages of (Q, dO) + Pd + dS ; q kernel: Q, dO + stages of (K, V) + dS
+  // kv kernel: K, V + stages of (Q, dO) + Pd + dS ; q kernel: Q, dO, O + stages of (K, V) + dS
   static constexpr int kSmemKV = 2 * kTile + kStages * 2 * kTile + 2 * kSqBytes + 1024 + 512;
-  static constexpr int kSmemQ = 2 * kTile + kStages * 2 * kTile + kSqBytes + 1024 + 512;
+  static constexpr int kSmemQ = 3 * kTile + kStages * 2 * kTile + kSqBytes + 1024 + 512;
 };
 
 // per-score backward algebra for one thread's 32-key slice of a query row;
-// Pd (optional) and dS packed as bf16 pairs
+// Pd (optional) and dS packed as bf16 pairs. The dS scale is folded into the
+// exponent (lse_s = lse - log2(ds_scale): P' = P * ds_scale) and the keep bit
+// into one factor f = keep / (1 - p):
+//   dS = P' (dPd f - D),   Pd = P' f / ds_scale
 template <bool WITH_PD>
 __device__ __forceinline__ void flash_bwd_slice(const uint32_t (&sraw)[32],
                                                 const uint32_t (&dpraw)[32], int lim, bool all_full,
-                                                float lse, float dvec, uint32_t kw, bool dropout,
+                                                float lse_s, float dvec, uint32_t kw, bool dropout,
                                                 const FlashParams& p, uint32_t (&pk_pd)[16],
                                                 uint32_t (&pk_ds)[16]) {
   const float neg_inf = -__int_as_float(0x7f800000);
+  const float fk = dropout ? p.drop.scale : 1.f;  // f of a kept score
+  const float inv_ds = 1.f / p.ds_scale;
 #pragma unroll
   for (int e = 0; e < 32; e += 2) {
-    float P[2], dP[2];
+    float P[2], dS[2], Pd[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const float x = (all_full || e + u < lim) ? __uint_as_float(sraw[e + u]) : neg_inf;
-      P[u] = fl_ex2(fmaf(x, p.sc, -lse));
-      dP[u] = __uint_as_float(dpraw[e + u]);
-      if (dropout) {
-        const bool keep = (kw >> (e + u)) & 1u;
-        dP[u] = keep ? dP[u] * p.drop.scale : 0.f;
-      }
+      P[u] = fl_ex2(fmaf(x, p.sc, -lse_s));
+      const float f = (!dropout || ((kw >> (e + u)) & 1u)) ? fk : 0.f;
+      dS[u] = P[u] * fmaf(__uint_as_float(dpraw[e + u]), f, -dvec);
+      if constexpr (WITH_PD) Pd[u] = P[u] * (f * inv_ds);
     }
-    if constexpr (WITH_PD) {
-      float d0 = P[0], d1 = P[1];
-      if (dropout) {
-        d0 = ((kw >> e) & 1u) ? d0 * p.drop.scale : 0.f;
-        d1 = ((kw >> (e + 1)) & 1u) ? d1 * p.drop.scale : 0.f;
-      }
-      pk_pd[e >> 1] = fl_pack(d0, d1);
-    }
-    pk_ds[e >> 1] = fl_pack(P[0] * (dP[0] - dvec) * p.ds_scale, P[1] * (dP[1] - dvec) * p.ds_scale);
+    if constexpr (WITH_PD) pk_pd[e >> 1] = fl_pack(Pd[0], Pd[1]);
+    pk_ds[e >> 1] = fl_pack(dS[0], dS[1]);
   }
 }
 
@@ -509,51 +506,24 @@ __device__ __forceinline__ void flash_st_slice(uint8_t* tile, int r, int w,
                  pk[4 * c + 2], pk[4 * c + 3]);
 }
 
-// D_i = dO_i . O_i for every (token, head): one thread per pair
-__global__ void flash_rowdot_kernel(const __nv_bfloat16* __restrict__ dctx,
-                                    const __nv_bfloat16* __restrict__ ctx, long long ld, int S,
-                                    int nh, int B, float* __restrict__ dvec) {
-  const long long n = (long long)B * S * nh;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int h = (int)(t % nh);
-    const long long tok = t / nh;
-    const uint4* a = reinterpret_cast<const uint4*>(dctx + tok * ld + h * 64);
-    const uint4* c = reinterpret_cast<const uint4*>(ctx + tok * ld + h * 64);
-    float acc = 0.f;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const uint4 x = __ldg(a + q), y = __ldg(c + q);
-      const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
-      const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 fx = __bfloat1622float2(x2[e]), fy = __bfloat1622float2(y2[e]);
-        acc = fmaf(fx.x, fy.x, acc);
-        acc = fmaf(fx.y, fy.y, acc);
-      }
-    }
-    const int b = (int)(tok / S), i = (int)(tok % S);
-    dvec[((long long)b * nh + h) * S + i] = acc;
-  }
-}
-
 // MODE 0: dK / dV kernel (work item = key block); MODE 1: dQ kernel (work item = query block)
 template <int MODE>
 __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                      const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV,
-                     const __grid_constant__ CUtensorMap tmO, const FlashParams p) {
+                     const __grid_constant__ CUtensorMap tmO,
+                     const __grid_constant__ CUtensorMap tmC, const FlashParams p) {
   using Cfg = FlashBwdCfg;
   constexpr int NS = Cfg::kStages;
   constexpr bool KV = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  // fixed pair: KV ? (K, V) : (Q, dO); streamed pairs: KV ? (Q, dO) : (K, V)
+  // fixed tiles: KV ? (K, V) : (Q, dO, O); streamed pairs: KV ? (Q, dO) : (K, V)
+  constexpr int kFix = KV ? 2 : 3;
   uint8_t* sFix = smem;
-  uint8_t* sStr = smem + 2 * Cfg::kTile;
+  uint8_t* sStr = smem + kFix * Cfg::kTile;
   uint8_t* sDS = sStr + NS * 2 * Cfg::kTile;
   uint8_t* sPD = sDS + Cfg::kSqBytes;  // KV only
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (KV ? 2 : 1) * Cfg::kSqBytes);
@@ -601,6 +571,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     tma_prefetch(&tmK);
     tma_prefetch(&tmV);
     tma_prefetch(&tmO);
+    if (!KV) tma_prefetch(&tmC);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -631,9 +602,10 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
         decode(item, z, blk);
         const int h = z % p.nh, b = z / p.nh;
         mbar_wait(fixempty, (ic & 1) ^ 1);
-        mbar_arrive_expect_tx(fixfull, 2 * Cfg::kTile);
+        mbar_arrive_expect_tx(fixfull, kFix * Cfg::kTile);
         tma_load_4d(KV ? &tmK : &tmQ, fixfull, sFix, 0, blk * 128, h, b);
         tma_load_4d(KV ? &tmV : &tmO, fixfull, sFix + Cfg::kTile, 0, blk * 128, h, b);
+        if (!KV) tma_load_4d(&tmC, fixfull, sFix + 2 * Cfg::kTile, 0, blk * 128, h, b);
         int lo, hi;
         inner_range(blk, lo, hi);
         for (int j = lo; j < hi; ++j, ++st) {
@@ -746,13 +718,36 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
       const int h = z % p.nh, b = z / p.nh;
       int lo, hi;
       inner_range(blk, lo, hi);
+      // dQ kernel: D_i = dO_i . O_i of this lane's query row from the staged
+      // dO / O tiles (this kernel runs first and stores D for the dK / dV one)
+      float d_row = 0.f;
+      if (!KV) {
+        mbar_wait(fixfull, ic & 1);
+        const uint32_t ra = smem_u32(sFix + Cfg::kTile) + r * 128;
+        const uint32_t rc = smem_u32(sFix + 2 * Cfg::kTile) + r * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
+          const uint4 x = ld_shared_v4(ra + off), y = ld_shared_v4(rc + off);
+          const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&x);
+          const __nv_bfloat162* y2 = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 fx = __bfloat1622float2(x2[e]), fy = __bfloat1622float2(y2[e]);
+            d_row = fmaf(fx.x, fy.x, d_row);
+            d_row = fmaf(fx.y, fy.y, d_row);
+          }
+        }
+        const int i = blk * 128 + r;
+        if (w == 0 && i < p.S) p.dvec[(int64_t)z * p.S + i] = d_row;
+      }
       for (int j = lo; j < hi; ++j, ++blkc) {
         const int qb = KV ? j : blk, kb = KV ? blk : j;  // query / key block
         const int i = qb * 128 + r;
         const bool row_ok = i < p.S;
         const int64_t grow = (int64_t)z * p.S + (row_ok ? i : 0);
         // per-row scalars and keep bits first: their loads overlap the MMA
-        const float lse = p.lse[grow], dv = p.dvec[grow];
+        const float lse = p.lse[grow], dv = KV ? p.dvec[grow] : d_row;
         const int c0 = kb * 128 + 32 * w;
         int lim = p.S - c0;
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
@@ -774,7 +769,8 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk_pd[e] = pk_ds[e] = 0u;
         } else {
-          flash_bwd_slice<KV>(sraw, dpraw, lim, all_full, lse, dv, kw, dropout, p, pk_pd, pk_ds);
+          flash_bwd_slice<KV>(sraw, dpraw, lim, all_full, lse - __log2f(p.ds_scale), dv, kw,
+                              dropout, p, pk_pd, pk_ds);
         }
         // the previous block's accumulation MMAs have read the staged tiles
         mbar_wait(pdone, (blkc & 1) ^ 1);
