@@ -466,33 +466,34 @@ struct FlashBwdCfg {
   static constexpr int kSmemQ = 3 * kTile + kStages * 2 * kTile + kSqBytes + 1024 + 512;
 };
 
-// per-score backward algebra for one thread's 32-key slice of a query row;
-// Pd (optional) and dS packed as bf16 pairs. The dS scale is folded into the
-// exponent (lse_s = lse - log2(ds_scale): P' = P * ds_scale) and the keep bit
-// into one factor f = keep / (1 - p):
+// per-score backward algebra for 16 keys (columns e0..e0+15 of the thread's
+// 32-key slice) of a query row; Pd (optional) and dS packed as bf16 pairs.
+// The dS scale is folded into the exponent (lse_s = lse - log2(ds_scale):
+// P' = P * ds_scale) and the keep bit into one factor f = keep / (1 - p):
 //   dS = P' (dPd f - D),   Pd = P' f / ds_scale
-template <bool WITH_PD>
-__device__ __forceinline__ void flash_bwd_slice(const uint32_t (&sraw)[32],
-                                                const uint32_t (&dpraw)[32], int lim, bool all_full,
-                                                float lse_s, float dvec, uint32_t kw, bool dropout,
-                                                const FlashParams& p, uint32_t (&pk_pd)[16],
-                                                uint32_t (&pk_ds)[16]) {
+// FULL: every key valid (no per-score test); DROP: dropout on.
+template <bool FULL, bool WITH_PD, bool DROP>
+__device__ __forceinline__ void flash_bwd_half(const uint32_t (&sraw)[16],
+                                               const uint32_t (&dpraw)[16], int e0, int lim,
+                                               float lse_s, float dvec, uint32_t kw, float fk,
+                                               float fkd, float sc, uint32_t* pk_pd,
+                                               uint32_t* pk_ds) {
   const float neg_inf = -__int_as_float(0x7f800000);
-  const float fk = dropout ? p.drop.scale : 1.f;  // f of a kept score
-  const float inv_ds = 1.f / p.ds_scale;
 #pragma unroll
-  for (int e = 0; e < 32; e += 2) {
-    float P[2], dS[2], Pd[2];
+  for (int e = 0; e < 16; e += 2) {
+    float dS[2], Pd[2];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const float x = (all_full || e + u < lim) ? __uint_as_float(sraw[e + u]) : neg_inf;
-      P[u] = fl_ex2(fmaf(x, p.sc, -lse_s));
-      const float f = (!dropout || ((kw >> (e + u)) & 1u)) ? fk : 0.f;
-      dS[u] = P[u] * fmaf(__uint_as_float(dpraw[e + u]), f, -dvec);
-      if constexpr (WITH_PD) Pd[u] = P[u] * (f * inv_ds);
+      const int col = e0 + e + u;
+      float x = __uint_as_float(sraw[e + u]);
+      if (!FULL) x = col < lim ? x : neg_inf;
+      const float P = fl_ex2(fmaf(x, sc, -lse_s));
+      const bool keep = !DROP || ((kw >> col) & 1u);
+      dS[u] = P * fmaf(__uint_as_float(dpraw[e + u]), keep ? fk : 0.f, -dvec);
+      if constexpr (WITH_PD) Pd[u] = P * (keep ? fkd : 0.f);
     }
-    if constexpr (WITH_PD) pk_pd[e >> 1] = fl_pack(Pd[0], Pd[1]);
-    pk_ds[e >> 1] = fl_pack(dS[0], dS[1]);
+    if constexpr (WITH_PD) pk_pd[(e0 + e) >> 1] = fl_pack(Pd[0], Pd[1]);
+    pk_ds[(e0 + e) >> 1] = fl_pack(dS[0], dS[1]);
   }
 }
 
@@ -755,23 +756,41 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
         const uint32_t kw = (dropout && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
         mbar_wait(sfull, blkc & 1);
         tc_fence_after();
-        uint32_t sraw[32], dpraw[32];
-        tmem_ld32_nowait(lane_base + 32 * w, sraw);
-        tmem_ld32_nowait(lane_base + 128 + 32 * w, dpraw);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sempty);
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
         const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
         uint32_t pk_pd[16], pk_ds[16];
-        if (all_dead) {
+        // two 16-key halves (S and dPd of a half in registers at a time); the
+        // TMEM buffers are released after the second half
+        const float lse_s = lse - __log2f(p.ds_scale);
+        const float fk = dropout ? p.drop.scale : 1.f, fkd = fk / p.ds_scale;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk_pd[e] = pk_ds[e] = 0u;
-        } else {
-          flash_bwd_slice<KV>(sraw, dpraw, lim, all_full, lse - __log2f(p.ds_scale), dv, kw,
-                              dropout, p, pk_pd, pk_ds);
+        for (int half = 0; half < 2; ++half) {
+          uint32_t sr[16], dr[16];
+          tmem_ld16u_nowait(lane_base + 32 * w + 16 * half, sr);
+          tmem_ld16u_nowait(lane_base + 128 + 32 * w + 16 * half, dr);
+          tmem_wait_ld();
+          if (all_dead) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) pk_pd[8 * half + e] = pk_ds[8 * half + e] = 0u;
+          } else if (all_full) {
+            if (dropout)
+              flash_bwd_half<true, KV, true>(sr, dr, 16 * half, lim, lse_s, dv, kw, fk, fkd, p.sc,
+                                             pk_pd, pk_ds);
+            else
+              flash_bwd_half<true, KV, false>(sr, dr, 16 * half, lim, lse_s, dv, kw, fk, fkd, p.sc,
+                                              pk_pd, pk_ds);
+          } else {
+            if (dropout)
+              flash_bwd_half<false, KV, true>(sr, dr, 16 * half, lim, lse_s, dv, kw, fk, fkd, p.sc,
+                                              pk_pd, pk_ds);
+            else
+              flash_bwd_half<false, KV, false>(sr, dr, 16 * half, lim, lse_s, dv, kw, fk, fkd,
+                                               p.sc, pk_pd, pk_ds);
+          }
         }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sempty);
         // the previous block's accumulation MMAs have read the staged tiles
         mbar_wait(pdone, (blkc & 1) ^ 1);
         if (KV) flash_st_slice(sPD, r, w, pk_pd);
