@@ -19,7 +19,8 @@
 //   Tile end: the four slices of a row are combined once (max / sum through
 //   shared memory), O = sum_w O_w 2^(m_w - M) / L * 1/(1-p) -> ctx, and
 //   lse = M + log2 L (log2 units of the scaled scores) is stored for the
-//   backward.
+//   backward -- deferred until after the next tile's first block, so the
+//   wait for the tile's last P V MMA overlaps softmax work.
 #pragma once
 
 #include <cuda.h>
@@ -264,6 +265,55 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     const uint32_t thr_hi = p.drop.threshold << 16;
     const float kNegInf = -__int_as_float(0x7f800000);
     int jb = 0, tc = 0;
+    // Tile end, software-pipelined: a tile's four slices are combined after
+    // the NEXT tile's first block, so the wait for its last P V overlaps work
+    bool pend = false, pend_ok = false;
+    int pend_tc = 0;
+    int64_t pend_ctx = 0, pend_grow = 0;
+    auto finish = [&]() {
+      mbar_wait(ofull, pend_tc & 1);
+      tc_fence_after();
+      fl_epi_bar();  // every warp has stored its slice statistics
+      const float* xm = xch + (pend_tc & 1) * 1024;
+      const float* xl = xm + 512;
+      float M = kNegInf;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) M = fmaxf(M, xm[t * 128 + r]);
+      float f[4], L = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const float mt = xm[t * 128 + r];
+        f[t] = mt == kNegInf ? 0.f : fl_ex2(mt - M);
+        L += f[t] * xl[t * 128 + r];
+      }
+      const float inv = p.drop.scale / L;
+      float acc[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int t = 0; t < 4; t += 2) {
+        uint32_t o0[16], o1[16];
+        tmem_ld16u_nowait(lane_base + 256 + 64 * t + 16 * w, o0);
+        tmem_ld16u_nowait(lane_base + 256 + 64 * (t + 1) + 16 * w, o1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+          acc[e] = fmaf(__uint_as_float(o1[e]), f[t + 1], fmaf(__uint_as_float(o0[e]), f[t], acc[e]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(oempty);
+      if (pend_ok) {
+        uint4* dst = reinterpret_cast<uint4*>(p.ctx + pend_ctx);
+        dst[0] = make_uint4(fl_pack(acc[0] * inv, acc[1] * inv), fl_pack(acc[2] * inv, acc[3] * inv),
+                            fl_pack(acc[4] * inv, acc[5] * inv), fl_pack(acc[6] * inv, acc[7] * inv));
+        dst[1] = make_uint4(fl_pack(acc[8] * inv, acc[9] * inv), fl_pack(acc[10] * inv, acc[11] * inv),
+                            fl_pack(acc[12] * inv, acc[13] * inv),
+                            fl_pack(acc[14] * inv, acc[15] * inv));
+        if (w == 0) p.lse[pend_grow] = M + __log2f(L);
+      }
+      pend = false;
+    };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       int z, qt;
       decode(tile, z, qt);
@@ -384,54 +434,21 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[sb * 4 + w]);
         if (trw) FT(tro + 3, FT_CLK());
+        if (j == 0 && pend) finish();  // the previous tile's combine
       }
-      // ---- tile end: combine the four slices of each row
-      const bool trf = lane == 0 && ew == 0 && tc < 64;
-      if (trf) FT(2048 + tc * 4 + 0, FT_CLK());
-      mbar_wait(ofull, tc & 1);
-      tc_fence_after();
-      if (trf) FT(2048 + tc * 4 + 1, FT_CLK());
-      float* xm = xch + (tc & 1) * 1024;  // [4 slices][128 rows]
-      float* xl = xm + 512;
-      xm[w * 128 + r] = m_used;
-      xl[w * 128 + r] = l;
-      fl_epi_bar();
-      float M = kNegInf;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) M = fmaxf(M, xm[t * 128 + r]);
-      float f[4], L = 0.f;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const float mt = xm[t * 128 + r];
-        f[t] = mt == kNegInf ? 0.f : fl_ex2(mt - M);
-        L += f[t] * xl[t * 128 + r];
+      // this tile's row statistics for its (deferred) combine
+      {
+        float* xm = xch + (tc & 1) * 1024;  // [4 slices][128 rows]
+        xm[w * 128 + r] = m_used;
+        xm[512 + w * 128 + r] = l;
       }
-      const float inv = p.drop.scale / L;
-      float acc[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        float o[16];
-        tmem_ld16(lane_base + 256 + 64 * t + 16 * w, o);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) acc[e] = fmaf(o[e], f[t], acc[e]);
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(oempty);
-      if (row_ok) {
-        uint4* dst = reinterpret_cast<uint4*>(p.ctx + ((int64_t)b * p.S + i) * p.ctx_ld + h * 64 +
-                                              16 * w);
-        dst[0] = make_uint4(fl_pack(acc[0] * inv, acc[1] * inv), fl_pack(acc[2] * inv, acc[3] * inv),
-                            fl_pack(acc[4] * inv, acc[5] * inv), fl_pack(acc[6] * inv, acc[7] * inv));
-        dst[1] = make_uint4(fl_pack(acc[8] * inv, acc[9] * inv), fl_pack(acc[10] * inv, acc[11] * inv),
-                            fl_pack(acc[12] * inv, acc[13] * inv),
-                            fl_pack(acc[14] * inv, acc[15] * inv));
-        if (w == 0) p.lse[grow] = M + __log2f(L);
-      }
-      if (trf) FT(2048 + tc * 4 + 2, FT_CLK());
+      pend = true;
+      pend_tc = tc;
+      pend_ok = row_ok;
+      pend_ctx = ((int64_t)b * p.S + i) * p.ctx_ld + h * 64 + 16 * w;
+      pend_grow = grow;
     }
+    if (pend) finish();
   }
   __syncthreads();
   if (warp == 1) {
