@@ -175,7 +175,13 @@ int mimose_flash_attn_fwd(const mimose_attn_args* a, void* stream) {
   if (a->B <= 0 || a->S <= 0 || a->nh <= 0) return fail("mimose_flash_attn_fwd: bad shape");
   const int H = 64 * a->nh;
   const auto drop = mimose_ops::make_dropout(a->dropout_p, a->seed, a->stream_id);
-  cudaError_t e = mimose_ops::flash_fwd(
+  if (drop.threshold != 0 && a->keep_mask == nullptr)
+    return fail("mimose_flash_attn_fwd: dropout needs keep_mask");
+  cudaError_t e = mimose_ops::flash_keep_mask(a->keep_mask, a->S, (a->S + 7) / 8 * 8, a->nh, a->B,
+                                              drop, a->causal != 0,
+                                              static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "mimose_flash_attn_fwd");
+  e = mimose_ops::flash_fwd(
       qkv_head_view(a->qkv, 0, a->S, H), qkv_head_view(a->qkv, 1, a->S, H),
       qkv_head_view(a->qkv, 2, a->S, H), a->ctx, H, a->lse, a->keep_mask, a->S,
       (a->S + 7) / 8 * 8, a->nh, a->B, a->scale, drop, a->causal != 0,

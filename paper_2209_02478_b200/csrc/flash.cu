@@ -90,7 +90,8 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   const double pairs = causal ? 0.5 * S * (double)(S + 1) : (double)S * S;
   // QK^T and P V; q, k, v read, ctx + lse written
   const int mw = (S + 31) / 32;
-  const bool with_mask = mask != nullptr && drop.threshold != 0;
+  const bool with_mask = drop.threshold != 0;
+  if (with_mask && mask == nullptr) return cudaErrorInvalidValue;
   ProfScope prof("attn_flash_fwd", 4.0 * 64 * pairs * nz,
                  nz * (8.0 * S * 64 + 4.0 * S + (with_mask ? 4.0 * S * mw : 0.0)), s);
   CUtensorMap tq, tk, tv;
@@ -111,6 +112,21 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   using Cfg = mimose_dev::FlashFwdCfg;
   return launch_flash(mimose_dev::flash_fwd_kernel, Cfg::kSmemBytes, Cfg::kThreads,
                       ((S + 127) / 128) * nh * B, tq, tk, tv, p, s, configured);
+}
+
+cudaError_t flash_keep_mask(uint32_t* mask, int S, int ld, int nh, int B,
+                            const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s) {
+  if (drop.threshold == 0) return cudaSuccess;
+  if (mask == nullptr || !flash_supported(S)) return cudaErrorInvalidValue;
+  const int mw = (S + 31) / 32;
+  ProfScope prof("attn_flash_mask", 0.0, (double)nh * B * 4.0 * S * mw, s);
+  const int64_t n = (int64_t)B * nh * S * mw;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 16 * flash_sm_count());
+  mimose_dev::flash_keep_mask_kernel<<<blocks, 256, 0, s>>>(
+      drop.seed, drop.stream, drop.threshold, (long long)B * nh * S, S, ld, mw, causal ? 1 : 0,
+      mask);
+  count_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, const void* ctx,

@@ -43,7 +43,7 @@ struct FlashParams {
   __nv_bfloat16* ctx;   // fwd out: [B*S][ctx_ld], head h at columns 64h
   long long ctx_ld;
   float* lse;           // fwd out / bwd in: [B*nh][S]
-  uint32_t* mask;       // fwd out / bwd in (dropout only): keep bits [B*nh*S][mw],
+  uint32_t* mask;       // fwd / bwd in (dropout only): keep bits [B*nh*S][mw],
   int mw;               //   bit e of word (row, k) = key 32k + e kept
   // backward
   const __nv_bfloat16* dctx;  // [B*S][ctx_ld]
@@ -92,6 +92,34 @@ __device__ __forceinline__ unsigned long long fl_clk() {
 #define FT(i, v)
 #define FT_CLK() 0ull
 #endif
+
+// Dropout keep bits of the attention probabilities, one uint32 per (row, 32
+// keys): bit e of word (row, k) keeps key 32k + e. Philox4x32-10 at the
+// materialised path's element index row * ld + key (one call per 8 keys,
+// 16-bit halves against the threshold: the same decisions as dropout_mask8).
+// The bits depend only on (seed, stream, shape), so this runs at full
+// occupancy ahead of the forward, which then tests one bit per score.
+__global__ void flash_keep_mask_kernel(uint64_t seed, uint64_t stream, uint32_t threshold,
+                                       long long rows, int S, int ld, int mw, int causal,
+                                       uint32_t* __restrict__ mask) {
+  const long long n = rows * mw;
+  const uint32_t thr_hi = threshold << 16;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long row = t / mw;
+    const int k = (int)(t % mw);
+    if (causal && 32 * k > (int)(row % S)) continue;  // all keys above the diagonal: never read
+    uint64_t grp[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)row * ld + 32 * k + 8 * q) >> 3;
+    uint32_t rnd[4][4];
+    philox_n<4>(seed, stream, grp, rnd);
+    uint32_t kw = 0;
+#pragma unroll
+    for (int e = 0; e < 32; ++e) kw |= (philox_keep_w(rnd[e >> 3], e & 7, thr_hi) ? 1u : 0u) << e;
+    mask[t] = kw;
+  }
+}
 
 __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -328,6 +356,12 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         const int sb = jb & 1;
         const bool trw = lane == 0 && (ew == 0 || ew == 15) && jb < 128;
         [[maybe_unused]] const int tro = 1024 + jb * 8 + (ew == 15 ? 4 : 0);
+        // keep bits first: the load overlaps the wait for S
+        const int c0 = j * 128 + 32 * w;
+        int lim = p.S - c0;  // valid keys of the slice: c0 + e < S (and <= i if causal)
+        if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
+        if (warp_dead) lim = 0;
+        const uint32_t kw = (thr_hi != 0 && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
         if (trw) FT(tro + 0, FT_CLK());
         mbar_wait(&sfull[sb], (jb >> 1) & 1);
         tc_fence_after();
@@ -338,10 +372,6 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[sb]);
-        const int c0 = j * 128 + 32 * w;
-        int lim = p.S - c0;  // valid keys of the slice: c0 + e < S (and <= i if causal)
-        if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
-        if (warp_dead) lim = 0;
         // warp-uniform paths: every key valid (no per-score test) / none valid
         // (past the sequence end or above the diagonal: P = 0, no Philox)
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
@@ -396,31 +426,17 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk[e] = 0u;
         } else {
-          uint32_t rnd[4][4];
-          if (thr_hi != 0) {
-            uint64_t grp[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)grow * p.ld + c0 + 8 * q) >> 3;
-            philox_n<4>(p.drop.seed, p.drop.stream, grp, rnd);
-          }
-          uint32_t kw = 0;
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             // p = 2^(s * sc - m): one FFMA + ex2 per score
             float a0 = fl_ex2(fmaf(x[e], p.sc, -m_eff)), a1 = fl_ex2(fmaf(x[e + 1], p.sc, -m_eff));
             psum += a0 + a1;
-            if (thr_hi != 0) {
-              const bool k0 = philox_keep_w(rnd[e >> 3], e & 7, thr_hi);
-              const bool k1 = philox_keep_w(rnd[e >> 3], (e & 7) + 1, thr_hi);
-              if (!k0) a0 = 0.f;
-              if (!k1) a1 = 0.f;
-              kw |= (k0 ? 1u : 0u) << e;
-              kw |= (k1 ? 2u : 0u) << e;
+            if (thr_hi != 0) {  // keep bits from flash_keep_mask_kernel
+              if (!((kw >> e) & 1u)) a0 = 0.f;
+              if (!((kw >> (e + 1)) & 1u)) a1 = 0.f;
             }
             pk[e >> 1] = fl_pack(a0, a1);
           }
-          // keep bits for the backward (no Philox there)
-          if (p.mask != nullptr && row_ok) p.mask[grow * p.mw + (c0 >> 5)] = kw;
         }
         l += psum;
         if (trw) FT(tro + 2, FT_CLK());

@@ -49,8 +49,13 @@ cudaError_t attn2_scores_bwd(const MatView& dout, const MatView& v, const void* 
 // the scaled scores. Dropout keep bits use the element index row * ld + key
 // of the materialised path.
 bool flash_supported(int S);
-// mask (dropout only, may be null): keep bits [B*nh*S][ceil(S/32)] uint32 for
-// the backward
+// Dropout keep bits [B*nh*S][ceil(S/32)] uint32 (bit e of word (row, k) =
+// key 32k + e kept), Philox at the materialised path's element index; they
+// depend only on (seed, stream, shape), so the trainer generates them on a
+// side stream while the QKV projection runs. Read by flash_fwd / flash_bwd.
+cudaError_t flash_keep_mask(uint32_t* mask, int S, int ld, int nh, int B,
+                            const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s);
+// mask: required with dropout (flash_keep_mask output)
 cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void* ctx,
                       int64_t ctx_ld, float* lse, uint32_t* mask, int S, int ld, int nh, int B,
                       float alpha, const mimose_dev::DropoutCfg& drop, bool causal,

@@ -229,6 +229,8 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   }
   ev_.resize(2 * L_);
   for (auto& e : ev_) ck(cudaEventCreate(&e), "cudaEventCreate");
+  ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
+  for (auto& e : side_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   ck(cudaStreamSynchronize(s), "init sync");
 
   constant_bytes_ = ctx_->arena.stats().requested;
@@ -314,6 +316,9 @@ Trainer::~Trainer() {
     cudaEventDestroy(e.second);
   }
   for (auto& e : ev_) cudaEventDestroy(e);
+  for (auto& e : side_ev_)
+    if (e) cudaEventDestroy(e);
+  if (side_) cudaStreamDestroy(side_);
   if (h_loss_) cudaFreeHost(h_loss_);
   for (int k = 0; k < 2; ++k) {
     if (h_stage_[k]) cudaFreeHost(h_stage_[k]);
@@ -656,18 +661,30 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   const int act_tag = keep ? kTagAct : kTagTransient;
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
 
+  const bool flash = fused_attn(S) == 3;
+  // flash keep bits: generated on the side stream while the QKV GEMM runs
+  // (they depend only on the Philox stream and the shape)
+  const auto fdrop =
+      mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+  void* kmask = flash && m_.attn_dropout > 0.f
+                    ? take(4 * (int64_t)g.B * nh * S * ((S + 31) / 32), act_tag)
+                    : nullptr;
+  if (kmask != nullptr) {
+    ck(cudaEventRecord(side_ev_[0], s), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(side_, side_ev_[0], 0), "cudaStreamWaitEvent");
+    ck(mimose_ops::flash_keep_mask(static_cast<uint32_t*>(kmask), S, ld, nh, g.B, fdrop,
+                                   m_.causal != 0, side_),
+       "flash_keep_mask");
+    ck(cudaEventRecord(side_ev_[1], side_), "cudaEventRecord");
+  }
   void* qkv = take(T * 3 * H * 2, act_tag);
   run_gemm(linear_call(x, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
                        p32_ + P.bqkv.off),
            s);
-  if (fused_attn(S) == 3) {
+  if (flash) {
     // flash: ctx plus one fp32 log-sum-exp per row (and keep bits) instead of P / Pd
-    const auto fdrop =
-        mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
+    if (kmask != nullptr) ck(cudaStreamWaitEvent(s, side_ev_[1], 0), "cudaStreamWaitEvent");
     void* lse = take(4 * (int64_t)g.B * nh * S, act_tag);
-    void* kmask = m_.attn_dropout > 0.f
-                      ? take(4 * (int64_t)g.B * nh * S * ((S + 31) / 32), act_tag)
-                      : nullptr;
     void* ctx = take(T * H * 2, act_tag);
     ck(mimose_ops::flash_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H),
                              head_view(qkv, 2 * H, S, 3 * H), ctx, H, static_cast<float*>(lse),

@@ -190,6 +190,9 @@ class Trainer {
   int64_t stage_elems_ = 0;
 
   std::vector<cudaEvent_t> ev_;  // 2 per layer (collector timing)
+  // side stream: flash attention keep bits generated during the QKV GEMM
+  cudaStream_t side_ = nullptr;
+  cudaEvent_t side_ev_[2] = {};
 
   mimose::ModelSpec spec_;
   mimose::SchedulerConfig sched_;

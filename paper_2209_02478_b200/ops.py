@@ -97,7 +97,7 @@ def flash_attn_fwd(qkv, B, S, nh, *, causal=False, dropout_p=0.0, seed=0, stream
     H = 64 * nh
     ctx = torch.empty(B * S, H, device=qkv.device, dtype=torch.bfloat16)
     lse = torch.empty(B * nh, S, device=qkv.device, dtype=torch.float32)
-    mask = (torch.zeros(B * nh * S, (S + 31) // 32, device=qkv.device, dtype=torch.int32)
+    mask = (torch.empty(B * nh * S, (S + 31) // 32, device=qkv.device, dtype=torch.int32)
             if dropout_p > 0 else None)
     a = _attn_args(qkv, B, S, nh, causal, dropout_p, seed, stream_id, scale)
     a.ctx, a.lse = ctx.data_ptr(), lse.data_ptr()
