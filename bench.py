@@ -69,6 +69,10 @@ def parse():
                          "tensor) or materialised (attn_fused 2, P / Pd saved like the reference "
                          "model). The budget denominator is always the materialised model's "
                          "no-ckpt peak (the reference model's memory semantics)")
+    ap.add_argument("--budget-basis", default="materialised", choices=["materialised", "self"],
+                    help="no-ckpt peak the budget fraction applies to: the materialised-attention "
+                         "model's (reference memory semantics, default) or the measured "
+                         "configuration's own")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu (no comparison arms, no cpu baseline)")
     args = ap.parse_args()
@@ -295,8 +299,10 @@ def run_gpu_arm(args, rank, world, local):
     # the reference model (HF BERT / GPT-2) materialises P and dropout(P): the
     # budget is a fraction of THAT model's no-checkpoint peak, whichever
     # attention kernels the measured runs use
-    probe = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none", attn_fused=2),
-                    probe_budget, local)
+    probe_cfg = dataclasses.replace(train_cfg, planner="none")
+    if args.budget_basis == "materialised":
+        probe_cfg = dataclasses.replace(probe_cfg, attn_fused=2)
+    probe = Trainer(model_cfg, probe_cfg, probe_budget, local)
     rng = np.random.default_rng(args.seed + 1000 * rank)
     probe.step(*synthetic_task_batch(rng, model_cfg, B, S_max), optimizer=False, stream=stream)
     peak_none = int(allmax(probe.rows[-1]["peak_reserved"], world))
@@ -513,8 +519,10 @@ def run_gpu_arm(args, rank, world, local):
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
                 "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
                 "attention": args.attn,
-                "budget_basis": "no-ckpt peak of the materialised-attention model at S_max "
-                                "(reference memory semantics)",
+                "budget_basis": ("no-ckpt peak of the materialised-attention model at S_max "
+                                 "(reference memory semantics)"
+                                 if args.budget_basis == "materialised"
+                                 else "no-ckpt peak of the measured configuration at S_max"),
                 "l2": "not flushed: per-step working set (GBs of activations) >> 126 MB L2",
                 "calibration": f"{calib} planner-calibration steps (sheltered collection window "
                                f"+ fit) run before warm-up, {calib_s:.2f} s",
