@@ -8,6 +8,7 @@
 #include "prof.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace mimose_ops {
 
@@ -32,7 +33,7 @@ cudaError_t launch_flash(Kern kern, int smem, int threads, int tiles, const CUte
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int grid = tiles < flash_sm_count() ? tiles : flash_sm_count();
+  const int grid = tiles;  // callers cap it at the resident CTAs
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -94,8 +95,13 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   if (with_mask && mask == nullptr) return cudaErrorInvalidValue;
   ProfScope prof("attn_flash_fwd", 4.0 * 64 * pairs * nz,
                  nz * (8.0 * S * 64 + 4.0 * S + (with_mask ? 4.0 * S * mw : 0.0)), s);
+  // key block: 64 (two CTAs per SM) unless MIMOSE_FLASH_KB=128
+  static const int kb = [] {
+    const char* e = std::getenv("MIMOSE_FLASH_KB");
+    return e != nullptr && std::atoi(e) == 128 ? 128 : 64;
+  }();
   CUtensorMap tq, tk, tv;
-  if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
+  if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, kb) ||
       !make_operand_map(&tv, v, nh, B, 64))
     return cudaErrorInvalidValue;
   mimose_dev::FlashParams p{};
@@ -108,10 +114,17 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   p.lse = lse;
   p.mask = with_mask ? mask : nullptr;
   p.mw = mw;
+  const int tiles = ((S + 127) / 128) * nh * B;
+  if (kb == 128) {
+    using Cfg = mimose_dev::FlashFwdCfg<128>;
+    static bool configured = false;
+    return launch_flash(mimose_dev::flash_fwd_kernel<128>, Cfg::kSmemBytes, Cfg::kThreads,
+                        std::min(tiles, flash_sm_count()), tq, tk, tv, p, s, configured);
+  }
+  using Cfg = mimose_dev::FlashFwdCfg<64>;
   static bool configured = false;
-  using Cfg = mimose_dev::FlashFwdCfg;
-  return launch_flash(mimose_dev::flash_fwd_kernel, Cfg::kSmemBytes, Cfg::kThreads,
-                      ((S + 127) / 128) * nh * B, tq, tk, tv, p, s, configured);
+  return launch_flash(mimose_dev::flash_fwd_kernel<64>, Cfg::kSmemBytes, Cfg::kThreads,
+                      std::min(tiles, 2 * flash_sm_count()), tq, tk, tv, p, s, configured);
 }
 
 cudaError_t flash_keep_mask(uint32_t* mask, int S, int ld, int nh, int B,

@@ -52,15 +52,24 @@ struct FlashParams {
   float ds_scale;             // score scale folded into dS (1/sqrt(64))
 };
 
+// KB keys per block: 128 (one CTA per SM, 16 softmax warps = 4 lane quarters
+// x 4 key slices, all 512 TMEM columns) or 64 (two CTAs per SM, 8 softmax
+// warps each, 256 TMEM columns: two independent pipelines per SM hide each
+// other's MMA / barrier latencies)
+template <int KB>
 struct FlashFwdCfg {
-  static constexpr int kEW = 16;
+  static constexpr int kNSL = KB / 32;             // 32-key slices per block
+  static constexpr int kEW = 4 * kNSL;             // softmax warps
   static constexpr int kThreads = 64 + 32 * kEW;
+  static constexpr int kMinBlocks = KB == 64 ? 2 : 1;
   static constexpr int kQBytes = 128 * 64 * 2;
-  static constexpr int kKBytes = 128 * 64 * 2;
-  static constexpr int kKVBytes = 2 * kKBytes;  // K block + V block
+  static constexpr int kKBytes = KB * 64 * 2;
+  static constexpr int kKVBytes = 2 * kKBytes;     // K block + V block
   static constexpr int kStages = 3;
-  static constexpr int kPBytes = 128 * 128 * 2;  // two 64-key swizzled sub-tiles
-  static constexpr int kXchBytes = 2 * 2 * 4 * 128 * 4;  // [tile parity][m|l][slice][row]
+  static constexpr int kPBytes = 128 * KB * 2;     // KB / 64 swizzled 64-key sub-tiles
+  static constexpr int kXchBytes = 2 * 2 * kNSL * 128 * 4;  // [tile parity][m|l][slice][row]
+  static constexpr int kTmemCols = 4 * KB;         // 2 S buffers (KB) + kNSL O slices (64)
+  static constexpr int kOCols = 64 / kNSL;         // output columns per warp in the combine
   static constexpr int kSmemBytes =
       kQBytes + kStages * kKVBytes + 2 * kPBytes + kXchBytes + 1024 + 512;
 };
@@ -76,7 +85,8 @@ __device__ __forceinline__ uint32_t fl_pack(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-__device__ __forceinline__ void fl_epi_bar() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void fl_epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
 // Pipeline trace (build with -DMIMOSE_FLASH_TRACE): CTA 0 stamps SM clocks.
 #ifdef MIMOSE_FLASH_TRACE
@@ -121,12 +131,14 @@ __global__ void flash_keep_mask_kernel(uint64_t seed, uint64_t stream, uint32_t 
   }
 }
 
-__global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
+template <int KB>
+__global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kMinBlocks)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                      const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV, const FlashParams p) {
-  using Cfg = FlashFwdCfg;
+  using Cfg = FlashFwdCfg<KB>;
   constexpr int NS = Cfg::kStages;
+  constexpr int NSL = Cfg::kNSL;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -140,17 +152,22 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
   uint64_t* qempty = qfull + 1;
   uint64_t* sfull = qempty + 1;   // [2] S buffers
   uint64_t* sempty = sfull + 2;   // [2]
-  uint64_t* pfull = sempty + 2;   // [2 P buffers][4 slices]
-  uint64_t* pvdone = pfull + 8;   // [2][4]
-  uint64_t* ofull = pvdone + 8;
+  uint64_t* pfull = sempty + 2;         // [2 P buffers][NSL slices]
+  uint64_t* pvdone = pfull + 2 * NSL;   // [2][NSL]
+  uint64_t* ofull = pvdone + 2 * NSL;
   uint64_t* oempty = ofull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 1);
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
   const int tiles_m = (p.S + 127) / 128;
+  const int tiles_k = (p.S + KB - 1) / KB;
   const int num_tiles = tiles_m * p.nh * p.B;
-  auto nkb_of = [&](int qt) { return p.causal ? (qt + 1 < tiles_m ? qt + 1 : tiles_m) : tiles_m; };
+  // key blocks of query tile qt (causal: up to the tile's last row)
+  auto nkb_of = [&](int qt) {
+    const int c = (qt + 1) * (128 / KB);
+    return p.causal ? (c < tiles_k ? c : tiles_k) : tiles_k;
+  };
   // tile -> (head z, query tile qt). Causal: longest tiles first, heads
   // fastest, so the static round-robin over CTAs stays balanced (with
   // z-major order and 148 % tiles_m == 0 a CTA would always get the same qt)
@@ -179,7 +196,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
       mbar_init(&sfull[b], 1);
       mbar_init(&sempty[b], Cfg::kEW);
     }
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 2 * NSL; ++i) {
       mbar_init(&pfull[i], 4);  // the four lane-quarter warps of a slice
       mbar_init(&pvdone[i], 1);
     }
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     mbar_init(oempty, Cfg::kEW);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -211,15 +228,16 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
           mbar_wait(&empty[s], ((kv / NS) & 1) ^ 1);
           mbar_arrive_expect_tx(&full[s], Cfg::kKVBytes);
           uint8_t* kd = sKV + s * Cfg::kKVBytes;
-          tma_load_4d(&tmK, &full[s], kd, 0, j * 128, h, b);
-          tma_load_4d(&tmV, &full[s], kd + Cfg::kKBytes, 0, j * 128, h, b);
-          tma_load_4d(&tmV, &full[s], kd + Cfg::kKBytes + 8192, 0, j * 128 + 64, h, b);
+          tma_load_4d(&tmK, &full[s], kd, 0, j * KB, h, b);
+#pragma unroll
+          for (int v = 0; v < KB / 64; ++v)
+            tma_load_4d(&tmV, &full[s], kd + Cfg::kKBytes + v * 8192, 0, j * KB + 64 * v, h, b);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
+    const uint32_t idesc_s = idesc_bf16_f32(128, KB, false, false);
     const uint32_t idesc_pv = idesc_bf16_f32(128, 64, false, true);
     int kv = 0, jb = 0, tc = 0;
     // O_w += P_b[:, 32w..32w+31] V[32w..32w+31, :] for block b (j-th of its tile)
@@ -230,8 +248,8 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         tc_fence_after();
       }
 #pragma unroll 1
-      for (int w = 0; w < 4; ++w) {
-        mbar_wait(&pfull[(b & 1) * 4 + w], (b >> 1) & 1);
+      for (int w = 0; w < NSL; ++w) {
+        mbar_wait(&pfull[(b & 1) * NSL + w], (b >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t pa =
@@ -240,10 +258,10 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
                                        (w >> 1) * 8192) + (w & 1) * 4096;
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem_base + 256 + 64 * w, smem_desc_sw128(pa + kk * 32, 16, 1024),
+            umma_bf16(tmem_base + 2 * KB + 64 * w, smem_desc_sw128(pa + kk * 32, 16, 1024),
                       smem_desc_sw128(va + kk * 2048, 8192, 1024), idesc_pv,
                       (j > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&pvdone[(b & 1) * 4 + w]);
+          umma_commit(&pvdone[(b & 1) * NSL + w]);
         }
         __syncwarp();
       }
@@ -268,7 +286,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
           const uint32_t qa = smem_u32(sQ), ka = smem_u32(sKV + s * Cfg::kKVBytes);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tmem_base + (jb & 1) * 128, smem_desc_sw128(qa + kk * 32, 16, 1024),
+            umma_bf16(tmem_base + (jb & 1) * KB, smem_desc_sw128(qa + kk * 32, 16, 1024),
                       smem_desc_sw128(ka + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
           umma_commit(&sfull[jb & 1]);
           if (j == nkb - 1) umma_commit(qempty);
@@ -301,43 +319,46 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
     auto finish = [&]() {
       mbar_wait(ofull, pend_tc & 1);
       tc_fence_after();
-      fl_epi_bar();  // every warp has stored its slice statistics
-      const float* xm = xch + (pend_tc & 1) * 1024;
-      const float* xl = xm + 512;
+      fl_epi_bar<32 * Cfg::kEW>();  // every warp has stored its slice statistics
+      const float* xm = xch + (pend_tc & 1) * (2 * NSL * 128);
+      const float* xl = xm + NSL * 128;
       float M = kNegInf;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) M = fmaxf(M, xm[t * 128 + r]);
-      float f[4], L = 0.f;
+      for (int t = 0; t < NSL; ++t) M = fmaxf(M, xm[t * 128 + r]);
+      float f[NSL], L = 0.f;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
+      for (int t = 0; t < NSL; ++t) {
         const float mt = xm[t * 128 + r];
         f[t] = mt == kNegInf ? 0.f : fl_ex2(mt - M);
         L += f[t] * xl[t * 128 + r];
       }
       const float inv = p.drop.scale / L;
-      float acc[16];
+      constexpr int OC = Cfg::kOCols;  // this warp's output columns [OC w, OC w + OC)
+      float acc[OC];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) acc[e] = 0.f;
+      for (int e = 0; e < OC; ++e) acc[e] = 0.f;
 #pragma unroll
-      for (int t = 0; t < 4; t += 2) {
-        uint32_t o0[16], o1[16];
-        tmem_ld16u_nowait(lane_base + 256 + 64 * t + 16 * w, o0);
-        tmem_ld16u_nowait(lane_base + 256 + 64 * (t + 1) + 16 * w, o1);
-        tmem_wait_ld();
+      for (int t = 0; t < NSL; ++t) {
 #pragma unroll
-        for (int e = 0; e < 16; ++e)
-          acc[e] = fmaf(__uint_as_float(o1[e]), f[t + 1], fmaf(__uint_as_float(o0[e]), f[t], acc[e]));
+        for (int q = 0; q < OC / 16; ++q) {
+          uint32_t o[16];
+          tmem_ld16u_nowait(lane_base + 2 * KB + 64 * t + OC * w + 16 * q, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) acc[16 * q + e] = fmaf(__uint_as_float(o[e]), f[t], acc[16 * q + e]);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(oempty);
       if (pend_ok) {
         uint4* dst = reinterpret_cast<uint4*>(p.ctx + pend_ctx);
-        dst[0] = make_uint4(fl_pack(acc[0] * inv, acc[1] * inv), fl_pack(acc[2] * inv, acc[3] * inv),
-                            fl_pack(acc[4] * inv, acc[5] * inv), fl_pack(acc[6] * inv, acc[7] * inv));
-        dst[1] = make_uint4(fl_pack(acc[8] * inv, acc[9] * inv), fl_pack(acc[10] * inv, acc[11] * inv),
-                            fl_pack(acc[12] * inv, acc[13] * inv),
-                            fl_pack(acc[14] * inv, acc[15] * inv));
+#pragma unroll
+        for (int q = 0; q < OC / 8; ++q)
+          dst[q] = make_uint4(fl_pack(acc[8 * q] * inv, acc[8 * q + 1] * inv),
+                              fl_pack(acc[8 * q + 2] * inv, acc[8 * q + 3] * inv),
+                              fl_pack(acc[8 * q + 4] * inv, acc[8 * q + 5] * inv),
+                              fl_pack(acc[8 * q + 6] * inv, acc[8 * q + 7] * inv));
         if (w == 0) p.lse[pend_grow] = M + __log2f(L);
       }
       pend = false;
@@ -354,10 +375,10 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
       float m_used = kNegInf, l = 0.f;
       for (int j = 0; j < nkb; ++j, ++jb) {
         const int sb = jb & 1;
-        const bool trw = lane == 0 && (ew == 0 || ew == 15) && jb < 128;
-        [[maybe_unused]] const int tro = 1024 + jb * 8 + (ew == 15 ? 4 : 0);
+        const bool trw = lane == 0 && (ew == 0 || ew == Cfg::kEW - 1) && jb < 128;
+        [[maybe_unused]] const int tro = 1024 + jb * 8 + (ew == Cfg::kEW - 1 ? 4 : 0);
         // keep bits first: the load overlaps the wait for S
-        const int c0 = j * 128 + 32 * w;
+        const int c0 = j * KB + 32 * w;
         int lim = p.S - c0;  // valid keys of the slice: c0 + e < S (and <= i if causal)
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
         if (warp_dead) lim = 0;
@@ -366,7 +387,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         mbar_wait(&sfull[sb], (jb >> 1) & 1);
         tc_fence_after();
         uint32_t raw[32];
-        tmem_ld32_nowait(lane_base + sb * 128 + 32 * w, raw);
+        tmem_ld32_nowait(lane_base + sb * KB + 32 * w, raw);
         tmem_wait_ld();
         if (trw) FT(tro + 1, FT_CLK());
         tc_fence_before();
@@ -401,12 +422,12 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
             const float alpha = mn == kNegInf ? 1.f : fl_ex2(m_used - mn);
             // O_w holds P V of the blocks so far: wait for the last one to land
             const int pb = jb - 1;
-            mbar_wait(&pvdone[(pb & 1) * 4 + w], (pb >> 1) & 1);
+            mbar_wait(&pvdone[(pb & 1) * NSL + w], (pb >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int part = 0; part < 4; ++part) {
               float o[16];
-              const uint32_t ta = lane_base + 256 + 64 * w + 16 * part;
+              const uint32_t ta = lane_base + 2 * KB + 64 * w + 16 * part;
               tmem_ld16(ta, o);
 #pragma unroll
               for (int e = 0; e < 16; ++e) o[e] *= alpha;
@@ -418,7 +439,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
           }
         }
         // this P buffer is free once the P V of two blocks ago has run
-        mbar_wait(&pvdone[sb * 4 + w], ((jb >> 1) & 1) ^ 1);
+        mbar_wait(&pvdone[sb * NSL + w], ((jb >> 1) & 1) ^ 1);
         const float m_eff = m_used == kNegInf ? 0.f : m_used;
         float psum = 0.f;
         uint32_t pk[16];
@@ -448,20 +469,20 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
         fence_async_shared();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[sb * 4 + w]);
+        if (lane == 0) mbar_arrive(&pfull[sb * NSL + w]);
         if (trw) FT(tro + 3, FT_CLK());
         if (j == 0 && pend) finish();  // the previous tile's combine
       }
       // this tile's row statistics for its (deferred) combine
       {
-        float* xm = xch + (tc & 1) * 1024;  // [4 slices][128 rows]
+        float* xm = xch + (tc & 1) * (2 * NSL * 128);  // [m | l][slice][row]
         xm[w * 128 + r] = m_used;
-        xm[512 + w * 128 + r] = l;
+        xm[NSL * 128 + w * 128 + r] = l;
       }
       pend = true;
       pend_tc = tc;
       pend_ok = row_ok;
-      pend_ctx = ((int64_t)b * p.S + i) * p.ctx_ld + h * 64 + 16 * w;
+      pend_ctx = ((int64_t)b * p.S + i) * p.ctx_ld + h * 64 + Cfg::kOCols * w;
       pend_grow = grow;
     }
     if (pend) finish();
@@ -469,7 +490,7 @@ __global__ void __launch_bounds__(FlashFwdCfg::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 }
 
