@@ -60,7 +60,7 @@ cudaError_t launch_flash5(Kern kern, int smem, int threads, int tiles, const CUt
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  const int grid = tiles < flash_sm_count() ? tiles : flash_sm_count();
+  const int grid = tiles;  // callers cap it at the resident CTAs
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(threads);
@@ -160,10 +160,11 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   dov.bs2 = (int64_t)S * ctx_ld;
   MatView cv = dov;
   cv.ptr = ctx;
-  CUtensorMap tq, tk, tv, to, tc;
+  CUtensorMap tq, tk, tv, to, tc, tk64, tv64;
   if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
       !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128) ||
-      !make_operand_map(&tc, cv, nh, B, 128))
+      !make_operand_map(&tc, cv, nh, B, 128) || !make_operand_map(&tk64, k, nh, B, 64) ||
+      !make_operand_map(&tv64, v, nh, B, 64))
     return cudaErrorInvalidValue;
   mimose_dev::FlashParams p{};
   p.S = S; p.nh = nh; p.B = B; p.ld = ld;
@@ -177,7 +178,8 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   p.dvec = dvec;
   p.dqkv = static_cast<__nv_bfloat16*>(dqkv);
   p.ds_scale = alpha;
-  using Cfg = mimose_dev::FlashBwdCfg;
+  using CfgQ = mimose_dev::FlashBwdCfg<1, 64>;
+  using CfgKV = mimose_dev::FlashBwdCfg<0, 128>;
   const int items = ((S + 127) / 128) * nh * B;
   const double mbytes = drop.threshold != 0 ? 4.0 * S * mw : 0.0;
   {
@@ -186,8 +188,9 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
     ProfScope prof("attn_flash_bwd_q", 6.0 * 64 * pairs * nz,
                    nz * (10.0 * S * 64 + 8.0 * S + mbytes + 2.0 * S * 64), s);
     static bool configured = false;
-    cudaError_t e = launch_flash5(mimose_dev::flash_bwd_kernel<1>, Cfg::kSmemQ, Cfg::kThreads,
-                                  items, tq, tk, tv, to, tc, p, s, configured);
+    cudaError_t e = launch_flash5(mimose_dev::flash_bwd_kernel<1, 64>, CfgQ::kSmemBytes,
+                                  CfgQ::kThreads, std::min(items, 2 * flash_sm_count()), tq,
+                                  tk64, tv64, to, tc, p, s, configured);
     if (e != cudaSuccess) return e;
   }
 
@@ -196,8 +199,9 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
     ProfScope prof("attn_flash_bwd_kv", 8.0 * 64 * pairs * nz,
                    nz * (8.0 * S * 64 + 8.0 * S + mbytes + 4.0 * S * 64), s);
     static bool configured = false;
-    return launch_flash5(mimose_dev::flash_bwd_kernel<0>, Cfg::kSmemKV, Cfg::kThreads, items,
-                         tq, tk, tv, to, to, p, s, configured);
+    return launch_flash5(mimose_dev::flash_bwd_kernel<0, 128>, CfgKV::kSmemBytes,
+                         CfgKV::kThreads, std::min(items, flash_sm_count()), tq, tk, tv, to, to,
+                         p, s, configured);
   }
 }
 

@@ -509,15 +509,24 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
 //   [query][key] tiles and read by the MMA as MN-major A operands;
 //   flash_bwd_q_kernel (one 128-query block per work item, loop over key
 //   blocks): dQ += dS K with K read as an MN-major B operand.
+// MODE 0 (dK / dV): 128-key items, 128-query inner blocks, 16 score warps,
+// one CTA per SM. MODE 1 (dQ): 128-query items, KB-key inner blocks; KB = 64
+// runs two CTAs per SM (8 score warps, 256 TMEM columns each).
+template <int MODE, int KB>
 struct FlashBwdCfg {
-  static constexpr int kEW = 16;
+  static constexpr int kKB = MODE == 0 ? 128 : KB;  // keys per S tile
+  static constexpr int kNSL = kKB / 32;              // 32-key slices
+  static constexpr int kEW = 4 * kNSL;
   static constexpr int kThreads = 64 + 32 * kEW;
-  static constexpr int kTile = 128 * 64 * 2;      // one 128-row x 64-dim bf16 tile
+  static constexpr int kMinBlocks = (MODE == 1 && KB == 64) ? 2 : 1;
+  static constexpr int kTile = 128 * 64 * 2;       // one 128-row x 64-dim bf16 tile
+  static constexpr int kStrTile = (MODE == 0 ? 128 : KB) * 64 * 2;  // streamed tile
   static constexpr int kStages = 2;
-  static constexpr int kSqBytes = 128 * 128 * 2;  // one [query][key] bf16 tile (2 sub-tiles)
-  // kv kernel: K, V + stages of (Q, dO) + Pd + dS ; q kernel: Q, dO, O + stages of (K, V) + dS
-  static constexpr int kSmemKV = 2 * kTile + kStages * 2 * kTile + 2 * kSqBytes + 1024 + 512;
-  static constexpr int kSmemQ = 3 * kTile + kStages * 2 * kTile + kSqBytes + 1024 + 512;
+  static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
+  static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
+  static constexpr int kTmemCols = MODE == 0 ? 512 : (KB == 64 ? 256 : 512);
+  static constexpr int kSmemBytes = kFix * kTile + kStages * 2 * kStrTile +
+                                    (MODE == 0 ? 2 : 1) * kSqBytes + 1024 + 512;
 };
 
 // per-score backward algebra for 16 keys (columns e0..e0+15 of the thread's
@@ -562,24 +571,26 @@ __device__ __forceinline__ void flash_st_slice(uint8_t* tile, int r, int w,
 }
 
 // MODE 0: dK / dV kernel (work item = key block); MODE 1: dQ kernel (work item = query block)
-template <int MODE>
-__global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
+template <int MODE, int KB>
+__global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
+                                  FlashBwdCfg<MODE, KB>::kMinBlocks)
     flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                      const __grid_constant__ CUtensorMap tmK,
                      const __grid_constant__ CUtensorMap tmV,
                      const __grid_constant__ CUtensorMap tmO,
                      const __grid_constant__ CUtensorMap tmC, const FlashParams p) {
-  using Cfg = FlashBwdCfg;
+  using Cfg = FlashBwdCfg<MODE, KB>;
   constexpr int NS = Cfg::kStages;
+  constexpr int KBL = Cfg::kKB;  // keys per S tile
   constexpr bool KV = MODE == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   // fixed tiles: KV ? (K, V) : (Q, dO, O); streamed pairs: KV ? (Q, dO) : (K, V)
-  constexpr int kFix = KV ? 2 : 3;
+  constexpr int kFix = Cfg::kFix;
   uint8_t* sFix = smem;
   uint8_t* sStr = smem + kFix * Cfg::kTile;
-  uint8_t* sDS = sStr + NS * 2 * Cfg::kTile;
+  uint8_t* sDS = sStr + NS * 2 * Cfg::kStrTile;
   uint8_t* sPD = sDS + Cfg::kSqBytes;  // KV only
   uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (KV ? 2 : 1) * Cfg::kSqBytes);
   uint64_t* full = bars;             // [NS]
@@ -596,7 +607,8 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
-  const int nblk = (p.S + 127) / 128;
+  const int nblk = (p.S + 127) / 128;       // 128-row item blocks
+  const int nkb = (p.S + KBL - 1) / KBL;    // Q mode: KBL-key inner blocks
   const int num_items = nblk * p.nh * p.B;
   // inner blocks of work item `blk`: KV: query blocks [causal ? blk : 0, nblk);
   // Q: key blocks [0, causal ? blk + 1 : nblk)
@@ -617,7 +629,8 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
       hi = nblk;
     } else {
       lo = 0;
-      hi = p.causal ? blk + 1 : nblk;
+      const int c = (blk + 1) * (128 / KBL);
+      hi = p.causal ? (c < nkb ? c : nkb) : nkb;
     }
   };
 
@@ -641,7 +654,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
     mbar_init(accempty, Cfg::kEW);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -666,53 +679,55 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
         for (int j = lo; j < hi; ++j, ++st) {
           const int s = st % NS;
           mbar_wait(&empty[s], ((st / NS) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], 2 * Cfg::kTile);
-          uint8_t* d = sStr + s * 2 * Cfg::kTile;
-          tma_load_4d(KV ? &tmQ : &tmK, &full[s], d, 0, j * 128, h, b);
-          tma_load_4d(KV ? &tmO : &tmV, &full[s], d + Cfg::kTile, 0, j * 128, h, b);
+          mbar_arrive_expect_tx(&full[s], 2 * Cfg::kStrTile);
+          uint8_t* d = sStr + s * 2 * Cfg::kStrTile;
+          const int rows = KV ? 128 : KBL;
+          tma_load_4d(KV ? &tmQ : &tmK, &full[s], d, 0, j * rows, h, b);
+          tma_load_4d(KV ? &tmO : &tmV, &full[s], d + Cfg::kStrTile, 0, j * rows, h, b);
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc_s = idesc_bf16_f32(128, 128, false, false);
+    const uint32_t idesc_s = idesc_bf16_f32(128, KBL, false, false);
     // KV: dV += Pd^T dO, dK += dS^T Q (A MN-major [query][key] tiles, B MN-major)
     // Q : dQ += dS K (A K-major [query][key] tile, B = K MN-major)
     const uint32_t idesc_acc = idesc_bf16_f32(128, 64, KV, true);
     int st = 0, ic = 0, blkc = 0;  // blkc: inner blocks processed (barrier phases)
     auto issue_sdp = [&](int s) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
-      const uint32_t q = smem_u32(KV ? sStr + s * 2 * Cfg::kTile : sFix);
-      const uint32_t k = smem_u32(KV ? sFix : sStr + s * 2 * Cfg::kTile);
+      const uint32_t q = smem_u32(KV ? sStr + s * 2 * Cfg::kStrTile : sFix);
+      const uint32_t k = smem_u32(KV ? sFix : sStr + s * 2 * Cfg::kStrTile);
+      constexpr int kQ2 = KV ? Cfg::kStrTile : Cfg::kTile;   // dO follows Q
+      constexpr int kK2 = KV ? Cfg::kTile : Cfg::kStrTile;   // V follows K
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
         umma_bf16(tmem_base, smem_desc_sw128(q + kk * 32, 16, 1024),
                   smem_desc_sw128(k + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem_base + 128, smem_desc_sw128(q + Cfg::kTile + kk * 32, 16, 1024),
-                  smem_desc_sw128(k + Cfg::kTile + kk * 32, 16, 1024), idesc_s,
-                  kk != 0 ? 1u : 0u);
+        umma_bf16(tmem_base + KBL, smem_desc_sw128(q + kQ2 + kk * 32, 16, 1024),
+                  smem_desc_sw128(k + kK2 + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
       umma_commit(sfull);
     };
     auto issue_acc = [&](int s, bool first) {
       if (KV) {
         const uint32_t pd = smem_u32(sPD), ds = smem_u32(sDS);
-        const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kTile);
+        const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries, 16 per MMA
-          umma_bf16(tmem_base + 256, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
-                    smem_desc_sw128(q + Cfg::kTile + kk * 2048, 8192, 1024), idesc_acc,
+          umma_bf16(tmem_base + 2 * KBL, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
+                    smem_desc_sw128(q + Cfg::kStrTile + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
-          umma_bf16(tmem_base + 320, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
+          umma_bf16(tmem_base + 2 * KBL + 64, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
                     smem_desc_sw128(q + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
         }
       } else {
         const uint32_t ds = smem_u32(sDS);
-        const uint32_t k = smem_u32(sStr + s * 2 * Cfg::kTile);
+        const uint32_t k = smem_u32(sStr + s * 2 * Cfg::kStrTile);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)  // K = 128 keys
-          umma_bf16(tmem_base + 256,
+        for (int kk = 0; kk < KBL / 16; ++kk)  // K = the block's keys
+          umma_bf16(tmem_base + 2 * KBL,
                     smem_desc_sw128(ds + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                     smem_desc_sw128(k + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
@@ -803,7 +818,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
         const int64_t grow = (int64_t)z * p.S + (row_ok ? i : 0);
         // per-row scalars and keep bits first: their loads overlap the MMA
         const float lse = p.lse[grow], dv = KV ? p.dvec[grow] : d_row;
-        const int c0 = kb * 128 + 32 * w;
+        const int c0 = kb * KBL + 32 * w;
         int lim = p.S - c0;
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
         if (!row_ok) lim = 0;
@@ -821,7 +836,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
         for (int half = 0; half < 2; ++half) {
           uint32_t sr[16], dr[16];
           tmem_ld16u_nowait(lane_base + 32 * w + 16 * half, sr);
-          tmem_ld16u_nowait(lane_base + 128 + 32 * w + 16 * half, dr);
+          tmem_ld16u_nowait(lane_base + KBL + 32 * w + 16 * half, dr);
           tmem_wait_ld();
           if (all_dead) {
 #pragma unroll
@@ -860,7 +875,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
       const int row = blk * 128 + r;  // key (KV) or query (Q) row of this lane
       if (KV) {
         uint32_t o[32];
-        tmem_ld32_nowait(lane_base + 256 + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
+        tmem_ld32_nowait(lane_base + 2 * KBL + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -878,19 +893,28 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
                                fl_pack(__uint_as_float(o[8 * q + 6]), __uint_as_float(o[8 * q + 7])));
         }
       } else {
-        float o[16];
-        tmem_ld16(lane_base + 256 + 16 * w, o);
+        constexpr int OC = 64 / Cfg::kNSL;  // dQ columns of this warp
+        float o[OC];
+#pragma unroll
+        for (int q = 0; q < OC / 16; ++q) {
+          uint32_t u[16];
+          tmem_ld16u_nowait(lane_base + 2 * KBL + OC * w + 16 * q, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[16 * q + e] = __uint_as_float(u[e]);
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(accempty);
         if (row < p.S) {
           const long long H = p.ctx_ld;
           uint4* d4 = reinterpret_cast<uint4*>(p.dqkv + ((long long)b * p.S + row) * 3 * H +
-                                               h * 64 + 16 * w);
-          d4[0] = make_uint4(fl_pack(o[0], o[1]), fl_pack(o[2], o[3]), fl_pack(o[4], o[5]),
-                             fl_pack(o[6], o[7]));
-          d4[1] = make_uint4(fl_pack(o[8], o[9]), fl_pack(o[10], o[11]), fl_pack(o[12], o[13]),
-                             fl_pack(o[14], o[15]));
+                                               h * 64 + OC * w);
+#pragma unroll
+          for (int q = 0; q < OC / 8; ++q)
+            d4[q] = make_uint4(fl_pack(o[8 * q], o[8 * q + 1]), fl_pack(o[8 * q + 2], o[8 * q + 3]),
+                               fl_pack(o[8 * q + 4], o[8 * q + 5]),
+                               fl_pack(o[8 * q + 6], o[8 * q + 7]));
         }
       }
     }
@@ -898,7 +922,7 @@ __global__ void __launch_bounds__(FlashBwdCfg::kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, 512);
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 }
 
