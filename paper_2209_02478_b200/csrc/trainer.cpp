@@ -14,6 +14,7 @@
 #include "ops_attn.hpp"
 #include "ops_mem.hpp"
 #include "trainer.hpp"
+#include "prof.hpp"
 
 namespace mimose_rt {
 
@@ -669,13 +670,18 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   void* kmask = flash && m_.attn_dropout > 0.f
                     ? take(4 * (int64_t)g.B * nh * S * ((S + 31) / 32), act_tag)
                     : nullptr;
-  if (kmask != nullptr) {
+  // (serialised on the main stream while the kernel profiler records, so
+  // every kernel's event time is its own)
+  const bool overlap = kmask != nullptr && !mimose_ops::prof_on();
+  if (overlap) {
     ck(cudaEventRecord(side_ev_[0], s), "cudaEventRecord");
     ck(cudaStreamWaitEvent(side_, side_ev_[0], 0), "cudaStreamWaitEvent");
+  }
+  if (kmask != nullptr) {
     ck(mimose_ops::flash_keep_mask(static_cast<uint32_t*>(kmask), S, ld, nh, g.B, fdrop,
-                                   m_.causal != 0, side_),
+                                   m_.causal != 0, overlap ? side_ : s),
        "flash_keep_mask");
-    ck(cudaEventRecord(side_ev_[1], side_), "cudaEventRecord");
+    if (overlap) ck(cudaEventRecord(side_ev_[1], side_), "cudaEventRecord");
   }
   void* qkv = take(T * 3 * H * 2, act_tag);
   run_gemm(linear_call(x, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
@@ -683,7 +689,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
            s);
   if (flash) {
     // flash: ctx plus one fp32 log-sum-exp per row (and keep bits) instead of P / Pd
-    if (kmask != nullptr) ck(cudaStreamWaitEvent(s, side_ev_[1], 0), "cudaStreamWaitEvent");
+    if (overlap) ck(cudaStreamWaitEvent(s, side_ev_[1], 0), "cudaStreamWaitEvent");
     void* lse = take(4 * (int64_t)g.B * nh * S, act_tag);
     void* ctx = take(T * H * 2, act_tag);
     ck(mimose_ops::flash_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H),
