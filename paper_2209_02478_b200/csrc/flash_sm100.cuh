@@ -829,7 +829,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
         uint32_t pk_pd[16], pk_ds[16];
         // two 16-key halves (S and dPd of a half in registers at a time); the
-        // TMEM buffers are released after the second half
+        // TMEM buffers are released once the second half is loaded
         const float lse_s = lse - __log2f(p.ds_scale);
         const float fk = dropout ? p.drop.scale : 1.f, fkd = fk / p.ds_scale;
 #pragma unroll
@@ -838,6 +838,13 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
           tmem_ld16u_nowait(lane_base + 32 * w + 16 * half, sr);
           tmem_ld16u_nowait(lane_base + KBL + 32 * w + 16 * half, dr);
           tmem_wait_ld();
+          if (half == 1) {
+            // S / dPd fully in registers: the MMA may overwrite them (next block)
+            // while this warp still computes its second half
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(sempty);
+          }
           if (all_dead) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) pk_pd[8 * half + e] = pk_ds[8 * half + e] = 0u;
@@ -857,9 +864,6 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                                                p.sc, pk_pd, pk_ds);
           }
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(sempty);
         // the previous block's accumulation MMAs have read the staged tiles
         mbar_wait(pdone, (blkc & 1) ^ 1);
         if (KV) flash_st_slice(sPD, r, w, pk_pd);
