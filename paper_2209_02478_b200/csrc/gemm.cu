@@ -308,7 +308,24 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
                                      float* __restrict__ out, long long ldo, float beta) {
   const long long total = (long long)M * N;
   const bool v4 = (N % 4 == 0) && (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
-  if (v4) {
+  if (v4 && ldo == N) {
+    // dense output: linear index, no row / column division
+    const long long n4 = total / 4;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+      float4 acc = reinterpret_cast<const float4*>(ws)[i];
+      for (int s = 1; s < splits; ++s) {
+        const float4 t = reinterpret_cast<const float4*>(ws + (long long)s * total)[i];
+        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      }
+      float4* o = reinterpret_cast<float4*>(out) + i;
+      if (beta != 0.f) {
+        const float4 old = *o;
+        acc.x += beta * old.x; acc.y += beta * old.y; acc.z += beta * old.z; acc.w += beta * old.w;
+      }
+      *o = acc;
+    }
+  } else if (v4) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total / 4;
          i += (long long)gridDim.x * blockDim.x) {
       const long long e = i * 4;

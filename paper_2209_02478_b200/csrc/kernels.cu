@@ -351,8 +351,18 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
   const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
   const int i = blockIdx.x * 32 + x;
   float s = 0.f;
-  if (i < W)
-    for (int b = y; b < nblk; b += 8) s += partial[(size_t)b * W + i];
+  if (i < W) {
+    // four independent chains (four loads in flight per thread), combined in
+    // a fixed order: deterministic
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    int b = y;
+    for (; b + 24 < nblk; b += 32) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s4[u] += partial[(size_t)(b + 8 * u) * W + i];
+    }
+    for (int u = 0; b < nblk; b += 8, ++u) s4[u & 3] += partial[(size_t)b * W + i];
+    s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  }
   red[y][x] = s;
   __syncthreads();
   if (y == 0 && i < W) {
