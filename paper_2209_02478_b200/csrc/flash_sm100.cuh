@@ -524,6 +524,7 @@ struct FlashBwdCfg {
   static constexpr int kStages = 2;
   static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
   static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
+  // S double buffer (2 kKB) + dPd (kKB) + accumulators (128 for dK / dV, 64 for dQ)
   static constexpr int kTmemCols = MODE == 0 ? 512 : (KB == 64 ? 256 : 512);
   static constexpr int kSmemBytes = kFix * kTile + kStages * 2 * kStrTile +
                                     (MODE == 0 ? 2 : 1) * kSqBytes + 1024 + 512;
@@ -597,9 +598,12 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
   uint64_t* empty = full + NS;       // [NS]
   uint64_t* fixfull = empty + NS;
   uint64_t* fixempty = fixfull + 1;
-  uint64_t* sfull = fixempty + 1;
-  uint64_t* sempty = sfull + 1;
-  uint64_t* pfull = sempty + 1;
+  // S double-buffered in TMEM, dPd single: the score warps read dPd first and
+  // release it, so the next block's S and dPd MMAs run while they compute
+  uint64_t* sfull = fixempty + 1;  // [2] S[b] and dPd of a block landed
+  uint64_t* sempty = sfull + 2;    // [2] S buffer b read
+  uint64_t* dpempty = sempty + 2;  // dPd read
+  uint64_t* pfull = dpempty + 1;
   uint64_t* pdone = pfull + 1;
   uint64_t* accfull = pdone + 1;
   uint64_t* accempty = accfull + 1;
@@ -646,8 +650,11 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     }
     mbar_init(fixfull, 1);
     mbar_init(fixempty, 1);
-    mbar_init(sfull, 1);
-    mbar_init(sempty, Cfg::kEW);
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(&sfull[b2], 1);
+      mbar_init(&sempty[b2], Cfg::kEW);
+    }
+    mbar_init(dpempty, Cfg::kEW);
     mbar_init(pfull, Cfg::kEW);
     mbar_init(pdone, 1);
     mbar_init(accfull, 1);
@@ -694,20 +701,20 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     // Q : dQ += dS K (A K-major [query][key] tile, B = K MN-major)
     const uint32_t idesc_acc = idesc_bf16_f32(128, 64, KV, true);
     int st = 0, ic = 0, blkc = 0;  // blkc: inner blocks processed (barrier phases)
-    auto issue_sdp = [&](int s) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
+    auto issue_sdp = [&](int s, int sb) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
       const uint32_t q = smem_u32(KV ? sStr + s * 2 * Cfg::kStrTile : sFix);
       const uint32_t k = smem_u32(KV ? sFix : sStr + s * 2 * Cfg::kStrTile);
       constexpr int kQ2 = KV ? Cfg::kStrTile : Cfg::kTile;   // dO follows Q
       constexpr int kK2 = KV ? Cfg::kTile : Cfg::kStrTile;   // V follows K
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem_base, smem_desc_sw128(q + kk * 32, 16, 1024),
+        umma_bf16(tmem_base + sb * KBL, smem_desc_sw128(q + kk * 32, 16, 1024),
                   smem_desc_sw128(k + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem_base + KBL, smem_desc_sw128(q + kQ2 + kk * 32, 16, 1024),
+        umma_bf16(tmem_base + 2 * KBL, smem_desc_sw128(q + kQ2 + kk * 32, 16, 1024),
                   smem_desc_sw128(k + kK2 + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
-      umma_commit(sfull);
+      umma_commit(&sfull[sb]);
     };
     auto issue_acc = [&](int s, bool first) {
       if (KV) {
@@ -715,10 +722,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries, 16 per MMA
-          umma_bf16(tmem_base + 2 * KBL, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
+          umma_bf16(tmem_base + 3 * KBL, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
                     smem_desc_sw128(q + Cfg::kStrTile + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
-          umma_bf16(tmem_base + 2 * KBL + 64, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
+          umma_bf16(tmem_base + 3 * KBL + 64, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
                     smem_desc_sw128(q + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
         }
@@ -727,7 +734,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         const uint32_t k = smem_u32(sStr + s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < KBL / 16; ++kk)  // K = the block's keys
-          umma_bf16(tmem_base + 2 * KBL,
+          umma_bf16(tmem_base + 3 * KBL,
                     smem_desc_sw128(ds + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
                     smem_desc_sw128(k + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
@@ -747,9 +754,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       for (int j = lo; j < hi; ++j, ++st, ++blkc) {
         const int s = st % NS;
         mbar_wait(&full[s], (st / NS) & 1);
-        mbar_wait(sempty, (blkc & 1) ^ 1);
+        mbar_wait(&sempty[blkc & 1], ((blkc >> 1) & 1) ^ 1);
+        mbar_wait(dpempty, (blkc & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) issue_sdp(s);
+        if (lane == 0) issue_sdp(s, blkc & 1);
         __syncwarp();
         if (j > lo) {
           mbar_wait(pfull, (blkc - 1) & 1);
@@ -823,27 +831,33 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
         if (!row_ok) lim = 0;
         const uint32_t kw = (dropout && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
-        mbar_wait(sfull, blkc & 1);
+        const int sbuf = blkc & 1;
+        mbar_wait(&sfull[sbuf], (blkc >> 1) & 1);
         tc_fence_after();
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
         const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
         uint32_t pk_pd[16], pk_ds[16];
-        // two 16-key halves (S and dPd of a half in registers at a time); the
-        // TMEM buffers are released once the second half is loaded
+        // dPd first (whole slice, then its buffer is released), then S in two
+        // 16-key halves; S buffer released once the second half is loaded
+        uint32_t dpr[2][16];
+        tmem_ld16u_nowait(lane_base + 2 * KBL + 32 * w, dpr[0]);
+        tmem_ld16u_nowait(lane_base + 2 * KBL + 32 * w + 16, dpr[1]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(dpempty);
         const float lse_s = lse - __log2f(p.ds_scale);
         const float fk = dropout ? p.drop.scale : 1.f, fkd = fk / p.ds_scale;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          uint32_t sr[16], dr[16];
-          tmem_ld16u_nowait(lane_base + 32 * w + 16 * half, sr);
-          tmem_ld16u_nowait(lane_base + KBL + 32 * w + 16 * half, dr);
+          uint32_t sr[16];
+          const uint32_t (&dr)[16] = dpr[half];
+          tmem_ld16u_nowait(lane_base + sbuf * KBL + 32 * w + 16 * half, sr);
           tmem_wait_ld();
           if (half == 1) {
-            // S / dPd fully in registers: the MMA may overwrite them (next block)
-            // while this warp still computes its second half
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(sempty);
+            if (lane == 0) mbar_arrive(&sempty[sbuf]);
           }
           if (all_dead) {
 #pragma unroll
@@ -879,7 +893,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       const int row = blk * 128 + r;  // key (KV) or query (Q) row of this lane
       if (KV) {
         uint32_t o[32];
-        tmem_ld32_nowait(lane_base + 2 * KBL + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
+        tmem_ld32_nowait(lane_base + 3 * KBL + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
@@ -902,7 +916,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
 #pragma unroll
         for (int q = 0; q < OC / 16; ++q) {
           uint32_t u[16];
-          tmem_ld16u_nowait(lane_base + 2 * KBL + OC * w + 16 * q, u);
+          tmem_ld16u_nowait(lane_base + 3 * KBL + OC * w + 16 * q, u);
           tmem_wait_ld();
 #pragma unroll
           for (int e = 0; e < 16; ++e) o[16 * q + e] = __uint_as_float(u[e]);
