@@ -757,7 +757,13 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         mbar_wait(&sempty[blkc & 1], ((blkc >> 1) & 1) ^ 1);
         mbar_wait(dpempty, (blkc & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) issue_sdp(s, blkc & 1);
+        if (lane == 0) {
+          issue_sdp(s, blkc & 1);
+          // the fixed tiles feed only the S / dPd MMAs (the accumulation reads
+          // the staged tiles and the streamed pair): release them after the
+          // item's last S / dPd, so the next item's loads overlap this one's tail
+          if (j == hi - 1) umma_commit(fixempty);
+        }
         __syncwarp();
         if (j > lo) {
           mbar_wait(pfull, (blkc - 1) & 1);
@@ -777,7 +783,6 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       if (lane == 0) {
         issue_acc(prev_s, hi - 1 == lo);
         umma_commit(accfull);
-        umma_commit(fixempty);
       }
       __syncwarp();
     }
