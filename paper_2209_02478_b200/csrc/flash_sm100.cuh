@@ -759,10 +759,14 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         tc_fence_after();
         if (lane == 0) {
           issue_sdp(s, blkc & 1);
-          // the fixed tiles feed only the S / dPd MMAs (the accumulation reads
-          // the staged tiles and the streamed pair): release them after the
-          // item's last S / dPd, so the next item's loads overlap this one's tail
-          if (j == hi - 1) umma_commit(fixempty);
+          // dK / dV: the fixed K, V tiles feed only the S / dPd MMAs (the
+          // accumulation reads the staged tiles and the streamed pair), so they
+          // are released after the item's last S / dPd and the next item's
+          // loads overlap this one's tail. (dQ: the score warps read the fixed
+          // dO / O tiles and wait on fixfull, so those are released only after
+          // the item's last accumulation -- an earlier release would let the
+          // producer overwrite them, and lap fixfull, before the warps read.)
+          if (KV && j == hi - 1) umma_commit(fixempty);
         }
         __syncwarp();
         if (j > lo) {
@@ -783,6 +787,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       if (lane == 0) {
         issue_acc(prev_s, hi - 1 == lo);
         umma_commit(accfull);
+        if (!KV) umma_commit(fixempty);
       }
       __syncwarp();
     }
