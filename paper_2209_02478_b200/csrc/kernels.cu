@@ -270,12 +270,13 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
       for (int e = 0; e < 8; ++e) dy[e] = philox_keep(ph, e, thr_hi) ? dy[e] * a.in_drop.scale : 0.f;
     }
     float s1 = 0.f, s2 = 0.f;
+    float xh[8];  // x-hat, reused below
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float xh = (zz[e] - st_cur.x) * st_cur.y;
+      xh[e] = (zz[e] - st_cur.x) * st_cur.y;
       const float gg = dy[e] * gam[e];
       s1 += gg;
-      s2 += gg * xh;
+      s2 += gg * xh[e];
     }
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
@@ -296,9 +297,8 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     float dz[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float xh = (zz[e] - st_cur.x) * st_cur.y;
-      dz[e] = st_cur.y * (dy[e] * gam[e] - mg - xh * mgx);
-      acc_g[e] += dy[e] * xh;
+      dz[e] = st_cur.y * (dy[e] * gam[e] - mg - xh[e] * mgx);
+      acc_g[e] += dy[e] * xh[e];
       acc_b[e] += dy[e];
     }
     if constexpr (DRES) {
@@ -307,17 +307,34 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
 #pragma unroll
       for (int e = 0; e < 8; ++e) dz[e] += rr[e];
     }
-    store8(static_cast<bf16*>(a.dz) + idx, dz);
+    // one rounding pass: the stored bf16 dz, widened back with bit ops, is the
+    // value the branch gradient starts from (same as bf16r(dz))
+    uint4 dzp;
+    {
+      __nv_bfloat162* hp = reinterpret_cast<__nv_bfloat162*>(&dzp);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) hp[q] = __floats2bfloat162_rn(dz[2 * q], dz[2 * q + 1]);
+      *reinterpret_cast<uint4*>(static_cast<bf16*>(a.dz) + idx) = dzp;
+    }
+    float dzr[8];
+    {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(&dzp);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        dzr[2 * q] = __uint_as_float(w[q] << 16);
+        dzr[2 * q + 1] = __uint_as_float(w[q] & 0xFFFF0000u);
+      }
+    }
     float db[8];
     if (a.br_drop.threshold != 0) {
       const Philox ph(a.br_drop.seed, a.br_drop.stream, (uint64_t)idx >> 3);
       const uint32_t thr_hi = a.br_drop.threshold << 16;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        db[e] = bf16r(philox_keep(ph, e, thr_hi) ? bf16r(dz[e]) * a.br_drop.scale : 0.f);
+        db[e] = bf16r(philox_keep(ph, e, thr_hi) ? dzr[e] * a.br_drop.scale : 0.f);
     } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) db[e] = bf16r(bf16r(dz[e]) * a.br_drop.scale);
+      for (int e = 0; e < 8; ++e) db[e] = bf16r(dzr[e] * a.br_drop.scale);
     }
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc_d[e] += db[e];
