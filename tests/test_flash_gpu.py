@@ -127,3 +127,31 @@ def test_flash_bwd_many_items_per_cta(cuda_device, S):
     ref = _ref_grads(qkv, dctx, B, S, nh, False, 0.1, 7, 1)
     err = (dqkv.float() - ref).abs().max().item()
     assert err <= 2e-2 * ref.abs().max().item(), err
+
+
+def test_flash_fwd_kb128_variant(cuda_device):
+    """The one-CTA-per-SM 128-key-block forward (MIMOSE_FLASH_KB=128, read once
+    per process, hence the subprocess) against the same fp32 restatement."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import torch, sys, importlib.util; sys.path.insert(0, '.');"
+        "spec = importlib.util.spec_from_file_location('tfg', 'tests/test_flash_gpu.py');"
+        "tfg = importlib.util.module_from_spec(spec); spec.loader.exec_module(tfg); _ref = tfg._ref;"
+        "from paper_2209_02478_b200 import ops;"
+        "B, nh = 2, 3\n"
+        "for S in (200, 512):\n"
+        "  for causal in (False, True):\n"
+        "    g = torch.Generator(device='cpu').manual_seed(S)\n"
+        "    qkv = (torch.randn(B * S, 3 * 64 * nh, generator=g) * 1.5).to(torch.bfloat16).cuda()\n"
+        "    ctx, lse, _ = ops.flash_attn_fwd(qkv, B, S, nh, causal=causal, dropout_p=0.1, seed=3, stream_id=4)\n"
+        "    ref, lref = _ref(qkv, B, S, nh, causal, 0.1, 3, 4)\n"
+        "    assert (ctx.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()\n"
+        "    assert (lse - lref).abs().max().item() < 1e-3\n"
+        "print('kb128 ok')\n")
+    env = dict(os.environ, MIMOSE_FLASH_KB="128")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and "kb128 ok" in r.stdout, r.stderr[-2000:]
