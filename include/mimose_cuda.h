@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 4
+#define MIMOSE_ABI_VERSION 5
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
@@ -170,6 +170,8 @@ typedef struct {
   int head;               /* MIMOSE_HEAD_* */
   int causal;             /* causal self-attention mask */
   int gelu_tanh;          /* GELU tanh approximation (GPT-2 "gelu_new") instead of erf */
+  int pad_token_id;       /* word-embedding row that receives no gradient (HF BERT
+                             padding_idx = pad_token_id = 0); -1 = none (GPT-2) */
 } mimose_model_cfg;
 
 enum {
@@ -191,9 +193,16 @@ typedef struct {
   int collect_new_sizes_always;/* collector.hpp:93 */
   int estimator_order;         /* harness.hpp:53 */
   float lr, beta1, beta2, adam_eps, weight_decay, max_grad_norm;
-  int attn_fused;              /* 1: fused score+softmax kernels (S <= 512); 0: GEMM + softmax kernels */
-  int reserve_per_size;        /* automatic reserve: 1 = extras at this step's S + margin (the
-                                  planner then keeps more blocks for short inputs), 0 = at seq_max */
+  int attn_fused;              /* 3: flash attention (default; no S x S tensor); 2: fused
+                                  score + softmax kernels, whole key row in TMEM (S <= 512);
+                                  1: block-looped fused score kernels (S <= 2048); 0: QK^T GEMM
+                                  + softmax kernels */
+  int reserve_per_size;        /* automatic reserve: 1 = sized for this step's S and verified
+                                  against the plan's own replay (simulate_iteration) - short
+                                  inputs keep more units; 0 = worst case at seq_max */
+  int ckpt_unit;               /* checkpoint unit the planner schedules: 0 = transformer block
+                                  (the reference's layer granularity), 1 = block half (attention
+                                  half, FFN half: 2 x layers units, finer-grained drops) */
 } mimose_train_cfg;
 
 enum {

@@ -82,14 +82,24 @@ def keep_mask(p: float, seed: int, stream: int, idx: np.ndarray) -> np.ndarray:
     thr = dropout_threshold(p)
     if thr == 0:
         return np.ones(idx.shape, dtype=bool)
-    flat = idx.reshape(-1).astype(np.uint64)
-    groups = flat >> np.uint64(3)
-    ug, inv = np.unique(groups, return_inverse=True)
-    r = philox4x32_10(seed, stream, ug)
-    e = (flat & np.uint64(7)).astype(np.int64)
-    words = r[inv, e >> 1].astype(np.uint64)
-    half = ((words >> (np.uint64(16) * (e & 1).astype(np.uint64))) & np.uint64(0xFFFF))
-    return (half >= np.uint64(thr)).reshape(idx.shape)
+    flat = idx.reshape(-1)
+    out = np.empty(flat.size, dtype=bool)
+    chunk = 1 << 23  # bounded temporaries for S x S masks at S = 2048
+    for c0 in range(0, flat.size, chunk):
+        f = flat[c0:c0 + chunk].astype(np.uint64)
+        groups = f >> np.uint64(3)
+        g0, g1 = int(groups.min()), int(groups.max())
+        if g1 - g0 < 2 * f.size:  # dense index range: one Philox call per group in it
+            r = philox4x32_10(seed, stream, np.arange(g0, g1 + 1, dtype=np.uint64))
+            inv = (groups - np.uint64(g0)).astype(np.int64)
+        else:
+            ug, inv = np.unique(groups, return_inverse=True)
+            r = philox4x32_10(seed, stream, ug)
+        e = (f & np.uint64(7)).astype(np.int64)
+        words = r[inv, e >> 1].astype(np.uint64)
+        half = (words >> (np.uint64(16) * (e & 1).astype(np.uint64))) & np.uint64(0xFFFF)
+        out[c0:c0 + chunk] = half >= np.uint64(thr)
+    return out.reshape(idx.shape)
 
 
 def stream_id(step: int, layer: int, site: int) -> int:
@@ -175,7 +185,13 @@ def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.
     def ln(x, w, b):
         return torch.nn.functional.layer_norm(x, (H,), P[w], P[b], eps=cfg.ln_eps)
 
-    e = P["embeddings.word"][tok] + P["embeddings.position"][pos]
+    # HF BertEmbeddings: nn.Embedding(..., padding_idx=pad_token_id) - the
+    # padding row gets no gradient from the lookup (a tied decoder still
+    # contributes to it); GPT-2 has no padding index (pad_token_id -1)
+    pad = _c(cfg, "pad_token_id", -1)
+    e = torch.nn.functional.embedding(tok, P["embeddings.word"],
+                                      padding_idx=pad if pad >= 0 else None) \
+        + P["embeddings.position"][pos]
     if cfg.type_vocab > 0:
         typ = torch.from_numpy(types.astype(np.int64)).reshape(-1)
         e = e + P["embeddings.token_type"][typ]

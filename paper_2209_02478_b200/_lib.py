@@ -77,6 +77,7 @@ class ModelCfg(C.Structure):
         ("init_std", C.c_float),
         ("seed", C.c_uint64),
         ("arch", C.c_int), ("head", C.c_int), ("causal", C.c_int), ("gelu_tanh", C.c_int),
+        ("pad_token_id", C.c_int),
     ]
 
 
@@ -89,7 +90,7 @@ class TrainCfg(C.Structure):
         ("estimator_order", C.c_int),
         ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
         ("weight_decay", C.c_float), ("max_grad_norm", C.c_float),
-        ("attn_fused", C.c_int), ("reserve_per_size", C.c_int),
+        ("attn_fused", C.c_int), ("reserve_per_size", C.c_int), ("ckpt_unit", C.c_int),
     ]
 
 
@@ -199,7 +200,7 @@ CUDA_SYMBOLS = [
       C.POINTER(C.c_int)]),
 ]
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 
 def _bind(lib, symbols):

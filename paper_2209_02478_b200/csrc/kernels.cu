@@ -640,10 +640,12 @@ __global__ void __launch_bounds__(256) embed_word_grad_kernel(const bf16* __rest
                                                               const int32_t* __restrict__ uid,
                                                               int n_unique,
                                                               float* __restrict__ dword,
-                                                              int accumulate) {
+                                                              int accumulate, int pad) {
   const int lane = threadIdx.x & 31;
   const int u = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (u >= n_unique) return;
+  // the padding row gets no embedding gradient (HF padding_idx); a tied
+  // decoder's own gradient for it stays in place
+  if (u >= n_unique || uid[u] == pad) return;
   const int b = seg[u], e = seg[u + 1];
   float* out = dword + (int64_t)uid[u] * H;
   for (int c0 = lane * 8; c0 < H; c0 += 256) {
@@ -1302,10 +1304,10 @@ cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
 
 cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
                             const int32_t* uid, int n_unique, float* dword, cudaStream_t s,
-                            bool accumulate) {
+                            bool accumulate, int pad) {
   if (n_unique == 0) return cudaSuccess;
   mimose_dev::embed_word_grad_kernel<<<grid_for(n_unique, 8), 256, 0, s>>>(
-      static_cast<const bf16*>(de), H, perm, seg, uid, n_unique, dword, accumulate ? 1 : 0);
+      static_cast<const bf16*>(de), H, perm, seg, uid, n_unique, dword, accumulate ? 1 : 0, pad);
   count_launch();
   return cudaGetLastError();
 }

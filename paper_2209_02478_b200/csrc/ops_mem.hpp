@@ -70,7 +70,7 @@ cudaError_t softmax_bwd(const void* P, void* dPd, int64_t rows, int S, int ld,
                         const DropoutCfg& d, float scale, cudaStream_t s, bool causal = false);
 cudaError_t embed_word_grad(const void* de, int H, const int32_t* perm, const int32_t* seg,
                             const int32_t* uid, int n_unique, float* dword, cudaStream_t s,
-                            bool accumulate = false);
+                            bool accumulate = false, int pad = -1);
 
 // out = in * keep-mask * scale over n (multiple of 8) bf16 elements; element
 // index = position in the buffer (the forward's dropout index)

@@ -155,6 +155,7 @@ int build_token_tables(const int32_t* tokens, int64_t T, int V, int32_t* perm, i
 // ------------------------------------------------------------------ setup
 void* Trainer::take(int64_t bytes, int tag) {
   void* p = ctx_->arena.alloc(bytes, tag);
+  if (p != nullptr && in_step_) step_live_.insert(p);
   if (p == nullptr) {
     const auto& st = ctx_->arena.stats();
     throw std::runtime_error("budget exceeded: request " + std::to_string(bytes) + " B with " +
@@ -168,6 +169,7 @@ void* Trainer::take(int64_t bytes, int tag) {
 void Trainer::drop(void*& p) {
   if (p != nullptr) {
     if (!ctx_->arena.free(p)) throw std::runtime_error("arena free of unknown pointer");
+    if (in_step_) step_live_.erase(p);
     p = nullptr;
   }
 }
@@ -178,6 +180,9 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   nh_ = m.heads;
   F_ = m.ffn;
   L_ = m.layers;
+  if (t.ckpt_unit != 0 && t.ckpt_unit != 1) throw std::runtime_error("ckpt_unit must be 0 (block) or 1 (half)");
+  half_ = t.ckpt_unit == 1;
+  if (units() > 64) throw std::runtime_error("at most 64 checkpoint units (layers <= 32 with half units)");
   if (H_ % 256 || H_ > 1024 || H_ / nh_ != 64 || F_ % 64 || L_ < 1 || L_ > 64)
     throw std::runtime_error("unsupported model shape (need hidden % 256 == 0, <= 1024, head dim 64)");
   if (m.arch != MIMOSE_ARCH_BERT && m.arch != MIMOSE_ARCH_GPT2) throw std::runtime_error("unknown arch");
@@ -186,6 +191,7 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   if (m.head == MIMOSE_HEAD_MC && (m.num_choices < 1 || t.batch % m.num_choices))
     throw std::runtime_error("batch must be a multiple of num_choices");
   if (m.vocab < 2) throw std::runtime_error("bad vocab");
+  if (m.pad_token_id < -1 || m.pad_token_id >= m.vocab) throw std::runtime_error("bad pad_token_id");
   if (t.seq_min < 1 || t.seq_max < t.seq_min || t.seq_max > m.max_pos || round8(t.seq_max) > 2048)
     throw std::runtime_error("bad sequence range");
 
@@ -228,8 +234,13 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
     ck(cudaMallocHost(&h_stage_[k], stage_elems_ * sizeof(int32_t)), "cudaMallocHost");
     ck(cudaEventCreateWithFlags(&stage_ev_[k], cudaEventDisableTiming), "event");
   }
-  ev_.resize(2 * L_);
+  ev_.resize(2 * static_cast<size_t>(units()));
   for (auto& e : ev_) ck(cudaEventCreate(&e), "cudaEventCreate");
+  for (int k = 0; k < kEvRing; ++k) {
+    ck(cudaEventCreate(&step_ev_[k][0]), "cudaEventCreate");
+    ck(cudaEventCreate(&step_ev_[k][1]), "cudaEventCreate");
+    step_ev_iter_[k] = -1;
+  }
   ck(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking), "cudaStreamCreate");
   for (auto& e : side_ev_) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
   ck(cudaStreamSynchronize(s), "init sync");
@@ -247,6 +258,7 @@ mimose::SimReport Trainer::report() {
   rep.budget_bytes = sched_.budget_bytes;
   rep.reserve_bytes = sched_.effective_reserve();
   rep.iterations = static_cast<int64_t>(history_.size());
+  for (int k = 0; k < kEvRing; ++k) resolve_step_ms(k);
   std::set<int64_t> distinct;
   for (size_t i = 0; i < history_.size(); ++i) {
     const mimose_step_report& h = history_[i];
@@ -256,12 +268,7 @@ mimose::SimReport Trainer::report() {
     row.planner = rep.planner;
     row.cache_hit = h.cache_hit != 0;
     row.peak_bytes = h.peak_reserved;  // measured (arena), not simulated
-    float ms = 0.f;
-    if (i < step_ev_.size()) {
-      ck(cudaEventSynchronize(step_ev_[i].second), "event");
-      ck(cudaEventElapsedTime(&ms, step_ev_[i].first, step_ev_[i].second), "event");
-    }
-    row.iteration_ms = ms;
+    row.iteration_ms = std::max(0.f, history_ms_[i]);
     // recompute cost from the measured per-block forward-time model
     double rc = 0.0;
     for (const auto& l : spec_.layers)
@@ -312,10 +319,9 @@ mimose::SimReport Trainer::report() {
 }
 
 Trainer::~Trainer() {
-  for (auto& e : step_ev_) {
-    cudaEventDestroy(e.first);
-    cudaEventDestroy(e.second);
-  }
+  for (auto& e : step_ev_)
+    for (cudaEvent_t ev : e)
+      if (ev) cudaEventDestroy(ev);
   for (auto& e : ev_) cudaEventDestroy(e);
   for (auto& e : side_ev_)
     if (e) cudaEventDestroy(e);
@@ -443,6 +449,8 @@ bool Trainer::save_pd() const {
   return keep && m_.attn_dropout > 0.f;
 }
 
+// The forward, the backward and the byte model (block_work_bytes) all ask
+// this one function, so they always agree on the path for a given S.
 int Trainer::fused_attn(int S) const {
   if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
   if (t_.attn_fused == 2 && mimose_ops::attn_fused_supported(S)) return 2;
@@ -510,11 +518,14 @@ int64_t Trainer::head_bytes(int S) const {
   return head + 64 * 1024;
 }
 
-// Worst extra live set of one block's backward: transients allocated minus
-// saved tensors already released, replayed in layer_bwd / attn_bwd's exact
-// allocation order (a saved tensor freed early is reused by later transients,
-// so summing every transient would over-reserve by ~3x at S = 512). Also
-// covers the forward's transient score buffer of the unfused attention path.
+// Worst extra live set of one unit's backward above its saved set and the
+// incoming gradient: transients allocated minus saved tensors already
+// released, replayed in ffn_half_bwd / attn_half_bwd / attn_bwd's exact
+// allocation order (a saved tensor freed early is reused by later
+// transients, so summing every transient would over-reserve by ~3x at
+// S = 512). Whole-block units replay both halves back to back; half units
+// take the larger of the two. Also covers the forward's transient score
+// buffer of the unfused attention path.
 int64_t Trainer::block_work_bytes(int S) const {
   const int64_t B = t_.batch, T = B * S, H = H_, F = F_;
   const int64_t ld = round8(S);
@@ -527,70 +538,100 @@ int64_t Trainer::block_work_bytes(int S) const {
   const bool flash = fused == 3;
   const int64_t lse = 4 * B * nh_ * (int64_t)S;
   const int64_t kmask = m_.attn_dropout > 0.f ? 4 * B * nh_ * (int64_t)S * ((S + 31) / 32) : 0;
-  int64_t live = act, peak = act;  // dy
+  int64_t live = 0, peak = 0;
   auto take_b = [&](int64_t n) { live += n; peak = std::max(peak, live); };
   auto drop_b = [&](int64_t n) { live -= n; };
-  if (pre) {
-    if (hid) take_b(act);                       // df
-    drop_b(fact); take_b(fact);                 // g -> du
-    if (hid) drop_b(act);                       // df
-    drop_b(fact); drop_b(act);                  // u, z2 (x2)
-    take_b(act); if (hid) take_b(act);          // dh1, da
-    take_b(act);                                // dx2
-    drop_b(fact); drop_b(act); drop_b(act);     // du, dx2, dy
-    drop_b(act); drop_b(st);                    // h1, st2
-  } else {
-    take_b(act); if (hid) take_b(act);          // dres (dz2), df
-    drop_b(act); drop_b(act); drop_b(st);       // dy, z2, st2
-    drop_b(fact); take_b(fact);                 // g -> du
-    if (hid) drop_b(act);                       // df
-    drop_b(fact); drop_b(act);                  // u, h1 (x2)
-    take_b(act); if (hid) take_b(act);          // dh1, da
-    drop_b(fact); drop_b(act);                  // du, dres
-    take_b(act);                                // dz1
-    drop_b(act); drop_b(act); drop_b(st);       // dh1, z1, st1
-  }
-  if (flash) {
+  auto ffn = [&] {  // ffn_half_bwd: dy live -> dh1 (+ da) live
+    if (pre) {
+      if (hid) take_b(act);                     // df
+      drop_b(fact); take_b(fact);               // g -> du
+      if (hid) drop_b(act);                     // df
+      drop_b(fact);                             // u
+      take_b(act); drop_b(act);                 // dh1, x2
+      if (hid) take_b(act);                     // da
+      take_b(act);                              // dx2
+      drop_b(fact); drop_b(act); drop_b(act);   // du, dx2, dy
+      drop_b(st);                               // st2
+    } else {
+      take_b(act); if (hid) take_b(act);        // dres (dz2), df
+      drop_b(act); drop_b(act); drop_b(st);     // dy, z2, st2
+      drop_b(fact); take_b(fact);               // g -> du
+      if (hid) drop_b(act);                     // df
+      drop_b(fact);                             // u
+      take_b(act);                              // dh1
+      drop_b(fact); drop_b(act);                // du, dres
+    }
+  };
+  auto attn = [&] {  // attn_half_bwd: dh1 (+ da) live -> dx live
+    if (!pre) {
+      take_b(act); if (hid) take_b(act);        // dz1, da
+      drop_b(act); drop_b(act); drop_b(st);     // dh1, z1, st1
+    }
+    if (fused != 1 && !flash) drop_b(act);      // ctx
     take_b(act);                                // dctx
     if (hid) drop_b(act);                       // da
-    take_b(qkv3); take_b(lse);                  // dqkv, D = rowsum(dO o O)
-    drop_b(lse); drop_b(act); drop_b(lse);      // D, dctx, saved lse
-    drop_b(kmask); drop_b(qkv3); drop_b(act);   // keep bits, qkv, ctx
+    if (flash) {
+      take_b(qkv3); take_b(lse);                // dqkv, D = rowsum(dO o O)
+      drop_b(lse); drop_b(act); drop_b(lse);    // D, dctx, saved lse
+      drop_b(kmask); drop_b(qkv3); drop_b(act); // keep bits, qkv, ctx
+    } else {
+      take_b(qkv3);                             // dqkv
+      if (!save_pd()) take_b(pd);               // regenerated Pd (0 without dropout)
+      drop_b(pd);                               // Pd (saved or regenerated) after dV
+      take_b(quad);                             // dP
+      drop_b(act); drop_b(quad);                // dctx, P
+      drop_b(quad); drop_b(qkv3);               // dP, qkv
+      if (fused == 1) drop_b(act);              // ctx
+    }
+    take_b(act);                                // dx
+    if (pre) {
+      take_b(act);                              // dx1
+      drop_b(qkv3); drop_b(act); drop_b(act);   // dqkv, x1, dx1
+      drop_b(st); drop_b(act);                  // st1, dh1
+    } else {
+      drop_b(qkv3); drop_b(act);                // dqkv, dz1
+    }
+  };
+  int64_t work = 0;
+  if (half_) {
+    live = peak = act;                          // dy
+    ffn();
+    work = peak;
+    live = peak = act + (pre && hid ? act : 0); // dh1 (+ da)
+    attn();
+    work = std::max(work, peak);
   } else {
-  if (fused != 1) drop_b(act);                  // ctx
-  take_b(act);                                  // dctx
-  if (hid) drop_b(act);                         // da
-  take_b(qkv3);                                 // dqkv
-  if (!save_pd()) take_b(pd);                   // regenerated Pd (0 without dropout)
-  drop_b(pd);                                   // Pd (saved or regenerated) after dV
-  take_b(quad);                                 // dP
-  drop_b(act); drop_b(quad);                    // dctx, P
-  drop_b(quad); drop_b(qkv3);                   // dP, qkv
-  if (fused == 1) drop_b(act);                  // ctx
+    live = peak = act;                          // dy
+    ffn();
+    drop_b(act);                                // h1 (block-internal, saved)
+    attn();
+    work = peak;
   }
-  take_b(act);                                  // dx
-  if (pre) take_b(act);                         // dx1
-  // forward: the unfused path's score buffer lives next to the block's saves
+  // forward: the unfused path's score buffer lives next to the unit's saves
   const int64_t fwd = fused ? 0 : quad;
-  (void)lse;
-  return std::max(peak, fwd);
+  return std::max(work, fwd);
 }
 
-int64_t Trainer::extras_bytes(int S) const {
-  // bytes outside the planner-managed blocks that can be live at once:
-  // inputs + token tables, embedding saves (z0, stats, h0), head tensors,
-  // the output boundaries of every block (the scheduler's excess does not
-  // count a dropped block's retained output), and one block's backward
-  // workspace.
+// Bytes outside the planner-managed units that can be live at once: inputs
+// + token tables, embedding saves (z0, stats, h0), head tensors and one
+// unit's backward workspace.
+int64_t Trainer::nonunit_bytes(int S) const {
   const int64_t B = t_.batch, T = B * S, H = H_;
   const int64_t act = 2 * T * H;
   const int64_t inputs = 4 * (7 * T + 2 * B + 8);
   const int64_t embed = m_.arch == MIMOSE_ARCH_BERT ? 2 * act + 8 * T : act;
-  const int64_t bounds = (int64_t)L_ * act;
-  return inputs + embed + head_bytes(S) + bounds + block_work_bytes(S);
+  return inputs + embed + head_bytes(S) + block_work_bytes(S);
 }
 
-// Bytes that appear only transiently after the forward (head + one block's
+// ... plus the retained outputs of n_dropped dropped units (every unit when
+// n_dropped < 0: the scheduler's excess formula credits a dropped unit with
+// its whole a(x), but the unit keeps its output, simulator.hpp:131-135).
+int64_t Trainer::extras_bytes(int S, int n_dropped) const {
+  const int n = n_dropped < 0 ? units() : n_dropped;
+  return nonunit_bytes(S) + (int64_t)n * unit_out_bytes(S);
+}
+
+// Bytes that appear only transiently after the forward (head + one unit's
 // backward workspace) plus a 2 % fragmentation margin: what the reactive
 // evictor must leave free.
 int64_t Trainer::dtr_headroom(int S) const {
@@ -605,26 +646,34 @@ void Trainer::build_spec() {
   spec_.input_min = (int64_t)t_.batch * t_.seq_min;
   spec_.input_max = (int64_t)t_.batch * t_.seq_max;
   const bool flash = t_.attn_fused == 3;
-  // per-layer quadratic term: P (+ Pd) for the materialised paths, the keep
-  // bits (1 bit per score) for flash attention; flash adds 4 B per row (lse)
+  // attention-half quadratic term: P (+ Pd) for the materialised paths, the
+  // keep bits (1 bit per score) for flash attention; flash adds 4 B per row
+  // (lse)
   const double p_quad = flash ? (m_.attn_dropout > 0.f ? nh_ / (8.0 * B) : 0.0)
                               : (save_pd() ? 2.0 : 1.0) * nh_ * 2.0 / B;
   const double lin_extra = flash ? 4.0 * nh_ : 0.0;
-  for (int l = 0; l < L_; ++l) {
+  // prior a(x) per token: attention half qkv + ctx + z1 + st1 + output h1;
+  // FFN half u + g + z2 + st2 + output y
+  const double attn_lin = static_cast<double>(12 * H + 8) + lin_extra;
+  const double ffn_lin = static_cast<double>(4 * F + 4 * H + 8);
+  for (int u = 0; u < units(); ++u) {
+    const bool attn_part = !half_ || u % 2 == 0;
+    const bool ffn_part = !half_ || u % 2 == 1;
+    const double quad = attn_part ? p_quad : 0.0;
     mimose::LayerSpec ls;
-    ls.id = l;
-    ls.position = l;
-    ls.stage_id = l;
+    ls.id = u;
+    ls.position = u;
+    ls.stage_id = unit_block(u);
     // flash attention without dropout saves nothing quadratic: a(x) is linear
-    ls.category = p_quad > 0.0 ? mimose::LayerCategory::QuadraticStructure
-                               : mimose::LayerCategory::ImplicitReduction;
-    // prior a(x): saved tensors per token + materialised probabilities
-    ls.activation_coeffs = {0.0, static_cast<double>(16 * H + 4 * F + 16) + lin_extra, p_quad};
+    ls.category = quad > 0.0 ? mimose::LayerCategory::QuadraticStructure
+                             : mimose::LayerCategory::ImplicitReduction;
+    ls.activation_coeffs = {0.0, (attn_part ? attn_lin : 0.0) + (ffn_part ? ffn_lin : 0.0), quad};
     ls.boundary_coeffs = {0.0, static_cast<double>(2 * H)};
     ls.forward_time_coeffs = {0.01, 1e-6};
     spec_.layers.push_back(ls);
   }
   mimose::validate_model(spec_);
+  sim_spec_ = spec_;
 
   sched_ = mimose::SchedulerConfig{};
   sched_.budget_bytes = ctx_->arena.stats().budget;
@@ -653,7 +702,7 @@ void Trainer::set_forced_plan(const int* ids, int n, int active) {
 // ------------------------------------------------------------ attention
 // qkv = x Wqkv^T + bqkv ; P = softmax(q k^T / 8 [causal]) ; Pd = dropout(P) ;
 // ctx = Pd v (head-interleaved [T, H]). Saved tensors go to *save when kept.
-void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g, cudaStream_t s) {
+void* Trainer::attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_;
   const int S = g.S, ld = g.ld, nh = nh_;
@@ -708,11 +757,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
   // Pd: only the P V operand unless saved (save_pd); the backward regenerates it
   void* Pd = m_.attn_dropout > 0.f ? take(quad, save_pd() ? act_tag : kTagTransient) : nullptr;
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
-  static const int fwd_max = [] {
-    const char* e = std::getenv("MIMOSE_ATTN_FWD_MAX");
-    return e != nullptr ? std::atoi(e) : 512;
-  }();
-  const int fused = S <= fwd_max ? fused_attn(S) : 0;
+  const int fused = fused_attn(S);
   if (fused == 1) {
     // fused, block-looped: scores stay in TMEM, softmax + dropout in the epilogue
     ck(mimose_ops::attn2_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
@@ -767,7 +812,7 @@ void* Trainer::attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g,
 
 // Attention backward from dctx (consumed) through the saved qkv / P / Pd
 // (freed); returns dqkv [T, 3H].
-void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cudaStream_t s) {
+void* Trainer::attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaStream_t s) {
   const int64_t T = g.T, H = H_;
   const int S = g.S, ld = g.ld, nh = nh_;
   const int64_t quad = (int64_t)g.B * nh * S * ld * 2;
@@ -863,124 +908,160 @@ void* Trainer::attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cuda
   return dqkv;
 }
 
-// ------------------------------------------------------------ layer forward
-// BERT (post-LN):  h1 = LN1(h + drop(attn(h))) ; y = LN2(h1 + drop(ffn(h1)))
-// GPT-2 (pre-LN):  h1 = h + drop(attn(LN1(h))) ; y = h1 + drop(ffn(LN2(h1)))
-// LayerSave slots: post-LN z1/st1 = LN1 input/stats, h1 = LN1 output, z2/st2 =
-// LN2 input/stats; pre-LN z1 = LN1 output x1, st1, h1, z2 = LN2 output x2, st2.
-void Trainer::layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
-                        cudaStream_t s) {
+// ------------------------------------------------------------ block halves
+// Each transformer block is two halves; the residual add (with its branch
+// dropout) is the epilogue of the projection GEMM that ends each half.
+//   BERT (post-LN)   attention  z1 = h + drop(attn(h) Wo + bo), h1 = LN1(z1)
+//                    FFN        z2 = h1 + drop(gelu(h1 W1 + b1) W2 + b2), y = LN2(z2)
+//   GPT-2 (pre-LN)   attention  x1 = LN1(h), h1 = h + drop(attn(x1) Wo + bo)
+//                    FFN        x2 = LN2(h1), y = h1 + drop(gelu(x2 W1 + b1) W2 + b2)
+// Saved sets: attention {qkv, lse (+ keep bits) | P (+ Pd), ctx, z1|x1, st1},
+// FFN {z2|x2, st2, u, g}.
+void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, const StepGeo& g,
+                            cudaStream_t s) {
   const LayerParams& P = lp_[l];
-  const int64_t T = g.T, H = H_, F = F_;
+  const int64_t T = g.T, H = H_;
   auto* W = static_cast<bf16raw*>(p16_);
   const bool keep = save != nullptr;
   const int act_tag = keep ? kTagAct : kTagTransient;
   const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
   const auto attn_out_drop =
       mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
-  const auto ffn_out_drop =
-      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
-
-  void* z1 = nullptr;
+  void* x1 = nullptr;
   void* st1 = nullptr;
   const void* ain = h;
   if (pre) {
-    z1 = take(T * H * 2, act_tag);  // x1 = LN1(h)
+    x1 = take(T * H * 2, act_tag);
     st1 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
     la.rows = (int)T; la.br = h;
     la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
-    la.stats = st1; la.y = z1;
+    la.stats = st1; la.y = x1;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    ain = z1;
+    ain = x1;
   }
   void* ctx = attn_fwd(l, ain, save, g, s);
-  if (pre && !keep) drop(z1);
-  // attention output projection, residual, LayerNorm
-  void* a = take(T * H * 2, kTagTransient);
-  run_gemm(linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, a, mimose_ops::kEpiBf16, p32_ + P.bo.off), s);
+  if (pre && !keep) drop(x1);
+  // output projection; residual + branch dropout in the epilogue
+  void* z1 = pre ? h1 : take(T * H * 2, act_tag);
+  {
+    GemmCall c = linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, z1, mimose_ops::kEpiBf16,
+                             p32_ + P.bo.off);
+    c.aux = h;
+    c.drop = attn_out_drop;
+    run_gemm(c, s);
+  }
   if (!keep) drop(ctx);
-  void* h1 = nullptr;
-  void* x2 = nullptr;  // FFN input
-  void* z2 = nullptr;
+  if (!pre) {
+    st1 = keep ? take(T * 8, act_tag) : nullptr;
+    mimose_ops::LnFwdArgs la;
+    la.rows = (int)T; la.br = z1;
+    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
+    la.stats = st1; la.y = h1;
+    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+    if (!keep) drop(z1);
+  }
+  if (keep) {
+    save->ctx = ctx;
+    save->z1 = pre ? x1 : z1;
+    save->st1 = st1;
+  }
+}
+
+void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const StepGeo& g,
+                           cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_, F = F_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  const bool keep = save != nullptr;
+  const int act_tag = keep ? kTagAct : kTagTransient;
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  const auto ffn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
+  void* x2 = nullptr;
   void* st2 = nullptr;
+  const void* fin = h1;
   if (pre) {
-    h1 = take(T * H * 2, act_tag);
     x2 = take(T * H * 2, act_tag);
     st2 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
+    la.rows = (int)T; la.br = h1;
     la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
-    la.z = h1; la.stats = st2; la.y = x2;
+    la.stats = st2; la.y = x2;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    z2 = x2;
-  } else {
-    z1 = keep ? take(T * H * 2, act_tag) : nullptr;
-    st1 = keep ? take(T * 8, act_tag) : nullptr;
-    h1 = take(T * H * 2, act_tag);
-    mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
-    la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
-    la.z = z1; la.stats = st1; la.y = h1;
-    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    x2 = h1;
+    fin = x2;
   }
-  drop(a);
-  // FFN
   void* u = take(T * F * 2, act_tag);
   void* gg = take(T * F * 2, act_tag);
   {
-    GemmCall c = linear_call(x2, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
+    GemmCall c = linear_call(fin, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
                              p32_ + P.b1.off);
     c.out2 = gg;
     c.gelu_tanh = m_.gelu_tanh;
     run_gemm(c, s);
   }
-  if (!keep) drop(u);
-  if (pre) {
-    if (!keep) drop(x2);
-    // y = h1 + dropout(g W2^T + b2): dropout + residual in the GEMM epilogue
-    GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, y, mimose_ops::kEpiBf16,
+  if (!keep) {
+    drop(u);
+    if (pre) drop(x2);
+  }
+  void* z2 = pre ? y : take(T * H * 2, act_tag);
+  {
+    GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, z2, mimose_ops::kEpiBf16,
                              p32_ + P.b2.off);
     c.aux = h1;
     c.drop = ffn_out_drop;
     run_gemm(c, s);
-    if (!keep) {
-      drop(gg);
-      drop(h1);
-      return;
-    }
-  } else {
-    void* f = take(T * H * 2, kTagTransient);
-    run_gemm(linear_call(gg, W + P.w2.off, T, (int)H, (int)F, f, mimose_ops::kEpiBf16, p32_ + P.b2.off), s);
-    if (!keep) drop(gg);
-    z2 = keep ? take(T * H * 2, act_tag) : nullptr;
+  }
+  if (!keep) drop(gg);
+  if (!pre) {
     st2 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.res = h1; la.br = f; la.br_drop = ffn_out_drop;
+    la.rows = (int)T; la.br = z2;
     la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
-    la.z = z2; la.stats = st2; la.y = y;
+    la.stats = st2; la.y = y;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    drop(f);
-    if (!keep) {
-      drop(h1);
-      return;
-    }
+    if (!keep) drop(z2);
   }
-  save->ctx = ctx;
-  save->z1 = z1; save->st1 = st1; save->h1 = h1;
-  save->u = u; save->g = gg; save->z2 = z2; save->st2 = st2;
+  if (keep) {
+    save->z2 = pre ? x2 : z2;
+    save->st2 = st2;
+    save->u = u;
+    save->g = gg;
+  }
 }
 
-void Trainer::free_save(LayerSave& sv) {
-  drop(sv.qkv); drop(sv.P); drop(sv.Pd); drop(sv.ctx); drop(sv.z1); drop(sv.st1); drop(sv.h1);
-  drop(sv.u); drop(sv.g); drop(sv.z2); drop(sv.st2); drop(sv.lse); drop(sv.mask);
+void Trainer::unit_fwd(int u, const void* in, void* out, UnitSave* save, const StepGeo& g,
+                       cudaStream_t s) {
+  if (u < 0 || u >= units()) throw std::runtime_error("unit index out of range");
+  if (save != nullptr) save->live = true;
+  if (half_) {
+    if (u % 2 == 0) attn_half_fwd(u / 2, in, out, save ? &save->a : nullptr, g, s);
+    else ffn_half_fwd(u / 2, in, out, save ? &save->f : nullptr, g, s);
+    return;
+  }
+  void* h1 = take(g.T * H_ * 2, save ? kTagAct : kTagTransient);
+  attn_half_fwd(u, in, h1, save ? &save->a : nullptr, g, s);
+  ffn_half_fwd(u, h1, out, save ? &save->f : nullptr, g, s);
+  if (save != nullptr) save->h1 = h1;
+  else drop(h1);
 }
 
-// ----------------------------------------------------------- layer backward
-// Consumes dy (freed) and the saved set (freed); returns dx (grad of h).
-void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
-                         cudaStream_t s) {
+void Trainer::free_save(UnitSave& sv) {
+  AttnSave& a = sv.a;
+  FfnSave& f = sv.f;
+  drop(a.qkv); drop(a.P); drop(a.Pd); drop(a.ctx); drop(a.z1); drop(a.st1); drop(a.lse);
+  drop(a.mask);
+  drop(f.z2); drop(f.st2); drop(f.u); drop(f.g);
+  drop(sv.h1);
+  sv.live = false;
+}
+
+// ----------------------------------------------------------- half backward
+// FFN half: consumes dy (grad of y) and the saved set, returns d h1. Pre-LN
+// blocks also return (*da) the attention branch's dropped-out gradient and
+// accumulate dbo: both come out of LN2's backward, which already reads d h1.
+void* Trainer::ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void** da_out,
+                            const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_, F = F_;
   auto* W = static_cast<bf16raw*>(p16_);
@@ -991,12 +1072,11 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
       mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
   const auto ffn_out_drop =
       mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteFfnOut));
-
-  // FFN-output residual / dropout / LN2 backward -> df (grad of the FFN output)
+  *da_out = nullptr;
   void* dres = nullptr;  // gradient reaching h1 through the residual
-  void* df = nullptr;
+  void* df = nullptr;    // gradient of the FFN output (after the branch dropout)
   if (pre) {
-    dres = dy;  // y = h1 + drop(f): d h1 (residual part) = dy
+    dres = dy;  // y = h1 + drop(f)
     if (hid_drop) {
       df = take(T * H * 2, kTagTransient);
       ck(mimose_ops::dropout_apply(dy, df, T * H, ffn_out_drop, s), "dropout_apply");
@@ -1027,32 +1107,52 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
   drop(df);
   drop(sv.u);
   ck(mimose_ops::colsum(du, (int)T, (int)F, F, nullptr, 1, col_partial_, G + P.b1.off, s), "colsum");
-  // FFN1: dW1 = du^T x2
-  void*& x2 = pre ? sv.z2 : sv.h1;
-  run_gemm(wgrad_call(du, x2, T, (int)F, (int)H, G + P.w1.off), s);
-  drop(x2);
+  // FFN1: dW1 = du^T (FFN input)
+  run_gemm(wgrad_call(du, pre ? sv.z2 : h1, T, (int)F, (int)H, G + P.w1.off), s);
   void* dh1 = take(T * H * 2, kTagTransient);
-  void* da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
   if (pre) {
+    drop(sv.z2);
+    void* da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
     // dx2 = du W1 ; d h1 = LN2'(dx2) + dy ; da = drop'(d h1), dbo
     void* dx2 = take(T * H * 2, kTagTransient);
     run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dx2, mimose_ops::kEpiBf16, nullptr), s);
     drop(du);
     mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dx2; a.z = sv.h1; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
+    a.rows = (int)T; a.dy = dx2; a.z = h1; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
     a.dres = dres;
     a.dz = dh1; a.dbr = da; a.br_drop = attn_out_drop;
     a.partial = ln_partial_;
     ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.bo.off, s), "ln_bwd");
     drop(dx2);
     drop(dy);
-    drop(sv.h1); drop(sv.st2);
+    drop(sv.st2);
+    *da_out = da;
   } else {
-    // d h1 = du W1 + dz2 (residual) ; LN1 backward (+ attention-output dropout, dbo)
+    // d h1 = du W1 + dz2 (residual)
     run_gemm(dgrad_call(du, W + P.w1.off, T, (int)F, (int)H, dh1, mimose_ops::kEpiBf16, dres), s);
     drop(du);
     drop(dres);
-    void* dz1 = take(T * H * 2, kTagTransient);
+  }
+  return dh1;
+}
+
+// Attention half: consumes d h1 (and, pre-LN, the FFN half's da), returns
+// d h (grad of the block input).
+void* Trainer::attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void* da,
+                             const StepGeo& g, cudaStream_t s) {
+  const LayerParams& P = lp_[l];
+  const int64_t T = g.T, H = H_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  float* G = g32_;
+  const bool hid_drop = m_.hidden_dropout > 0.f;
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  const auto attn_out_drop =
+      mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, l, kSiteAttnOut));
+  void* dz1 = nullptr;  // post-LN: gradient reaching h through the residual
+  if (!pre) {
+    // LN1 backward (+ attention-output dropout, dbo)
+    dz1 = take(T * H * 2, kTagTransient);
+    da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
     mimose_ops::LnBwdArgs a;
     a.rows = (int)T; a.dy = dh1; a.z = sv.z1; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
     a.dz = dz1; a.dbr = da; a.br_drop = attn_out_drop;
@@ -1060,18 +1160,18 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
     ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, G + P.bo.off, s), "ln_bwd");
     drop(dh1);
     drop(sv.z1); drop(sv.st1);
-    dh1 = dz1;  // gradient reaching the block input through the residual
   }
-  void* dap = da ? da : dh1;
+  void* dap = da ? da : (pre ? dh1 : dz1);
   // output projection: dWo = da^T ctx ; dctx = da Wo
   run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
   // attn_fused 1 / 3 read ctx in attn_bwd (rowsum(dP o P) = dO . ctx)
-  if (fused_attn(g.S) != 1 && fused_attn(g.S) != 3) drop(sv.ctx);
+  const int fused = fused_attn(g.S);
+  if (fused != 1 && fused != 3) drop(sv.ctx);
   void* dctx = take(T * H * 2, kTagTransient);
   run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
   drop(da);
   void* dqkv = attn_bwd(l, sv, dctx, g, s);
-  if (fused_attn(g.S) == 1 || fused_attn(g.S) == 3) drop(sv.ctx);
+  if (fused == 1 || fused == 3) drop(sv.ctx);
   // QKV projection: dbqkv, dWqkv = dqkv^T xin
   ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
      "colsum");
@@ -1091,15 +1191,31 @@ void* Trainer::layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const St
     ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, nullptr, s), "ln_bwd");
     drop(dx1);
     drop(sv.st1);
+    drop(dh1);
   } else {
     // dx = dqkv Wqkv + dz1 (residual)
-    run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx, mimose_ops::kEpiBf16, dh1), s);
+    run_gemm(dgrad_call(dqkv, W + P.wqkv.off, T, 3 * (int)H, (int)H, dx, mimose_ops::kEpiBf16, dz1), s);
     drop(dqkv);
+    drop(dz1);
   }
-  drop(dh1);
   return dx;
 }
 
+void* Trainer::unit_bwd(int u, const void* in, UnitSave& sv, void* dy, void** aux,
+                        const StepGeo& g, cudaStream_t s) {
+  if (u < 0 || u >= units()) throw std::runtime_error("unit index out of range");
+  sv.live = false;
+  if (half_) {
+    if (u % 2 == 1) return ffn_half_bwd(u / 2, in, sv.f, dy, aux, g, s);
+    void* da = *aux;
+    *aux = nullptr;
+    return attn_half_bwd(u / 2, in, sv.a, dy, da, g, s);
+  }
+  void* da = nullptr;
+  void* dh1 = ffn_half_bwd(u, sv.h1, sv.f, dy, &da, g, s);
+  drop(sv.h1);
+  return attn_half_bwd(u, in, sv.a, dh1, da, g, s);
+}
 // ------------------------------------------------------------ phase machine
 void Trainer::refit(mimose_step_report* rep) {
   const int order = std::min(t_.estimator_order, cstate_.distinct_sizes() - 1);
@@ -1113,6 +1229,13 @@ void Trainer::refit(mimose_step_report* rep) {
   // the plan cache is kept across refits, as the reference harness does
   // measured profile -> model document (activation coefficients = the fit
   // padded to order 2 when possible, forward time = per-layer linear fit)
+  sim_spec_ = spec_;
+  for (auto& ls : sim_spec_.layers) {
+    const auto& c = est_.per_layer_coeffs.at(ls.id);
+    std::array<double, 3> a{0, 0, 0};
+    for (size_t k = 0; k < c.size() && k < 3; ++k) a[k] = c[k];
+    ls.activation_coeffs = a;
+  }
   for (auto& ls : spec_.layers) {
     const auto& c = est_.per_layer_coeffs.at(ls.id);
     std::array<double, 3> a{0, 0, 0};
@@ -1181,24 +1304,47 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
     trained_ = true;
   }
   if (ccfg_.collect_new_sizes_always && unseen) return Mode::Collect;
-  // reserve for this input size: the transients outside the planned blocks
-  // (inputs, head, retained boundaries, one block's backward workspace) scale
-  // with S, so sizing them at S_max would over-checkpoint short inputs. The
-  // plan cache is keyed by x, so each entry is consistent with its reserve.
+  // Reserve for this input size (reserve_per_size, default). The scheduler
+  // bounds the END-OF-FORWARD residency of the kept units
+  // (scheduler.hpp:125-126); what it does not see scales with S: inputs,
+  // embedding and head tensors, one unit's backward workspace, a 3 %
+  // fragmentation margin (nonunit_bytes), and what the plan itself adds -
+  // the retained outputs of dropped units, their forward transients and the
+  // recompute before their backward. The latter is measured with the
+  // reference's own iteration replay (simulate_iteration, simulator.hpp:104)
+  // over the FITTED a(x): the reserve is raised by the replay's overshoot
+  // and the size re-planned until the plan fits (a fixed point, a few
+  // generate_plan calls of ~1 us). The plan cache is keyed by x and each
+  // entry keeps the reserve it was generated with, so a hit replays exactly.
   mimose::SchedulerConfig sc = sched_;
+  const auto t0 = std::chrono::steady_clock::now();
   if (t_.reserve_bytes < 0 && t_.reserve_per_size) {
-    const int64_t S = x / t_.batch;
-    sc.reserve_bytes = std::min<int64_t>(extras_bytes(S) + sched_.budget_bytes * 3 / 100,
-                                         sched_.budget_bytes - 1);
+    const int64_t budget = sched_.budget_bytes;
+    const auto known = plan_reserve_.find(x);
+    if (known != plan_reserve_.end() && cache_.entries.count(x)) {
+      sc.reserve_bytes = known->second;
+    } else {
+      const int64_t fixed = nonunit_bytes(static_cast<int>(x / t_.batch)) + budget * 3 / 100;
+      int64_t R = std::min<int64_t>(fixed, budget - 1);
+      for (int it = 0; it <= units() + 1; ++it) {
+        sc.reserve_bytes = R;
+        const mimose::CheckpointPlan trial = mimose::generate_plan(est_, spec_, x, sc);
+        if (trial.insufficient_budget) break;
+        const int64_t over = mimose::simulate_iteration(sim_spec_, trial, x).peak_bytes + fixed - budget;
+        if (over <= 0 || R >= budget - 1) break;
+        R = std::min<int64_t>(R + over, budget - 1);
+      }
+      sc.reserve_bytes = R;
+    }
   }
   rep->reserve_bytes = sc.effective_reserve();
-  const auto t0 = std::chrono::steady_clock::now();
   auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, x, sc);
   const auto t1 = std::chrono::steady_clock::now();
   rep->plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   if (!hit) {
     cache_.entries[x].generated_at_iter = iter_;
     p.generated_at_iter = iter_;
+    plan_reserve_[x] = sc.reserve_bytes;
   }
   rep->cache_hit = hit ? 1 : 0;
   rep->predicted_kept = mimose::detail::estimated_kept_bytes(est_, spec_, p, x);
@@ -1391,6 +1537,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   g.step = static_cast<uint64_t>(iter_);
   const int64_t x = g.T;
   const int64_t T = g.T, H = H_;
+  const int U = units();
   auto* W = static_cast<bf16raw*>(p16_);
   float* G = g32_;
 
@@ -1411,30 +1558,28 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   if (mode == Mode::Collect && r->phase != MIMOSE_PHASE_FALLBACK) r->phase = MIMOSE_PHASE_COLLECT;
   if (mode == Mode::AllLayers) r->phase = MIMOSE_PHASE_SHELTERED;
   if (mode == Mode::Planned) r->phase = MIMOSE_PHASE_PLANNED;
-  std::vector<char> dropped(L_, 0);
+  // an insufficient_budget plan already holds every unit
+  // (scheduler.hpp:153-156): it runs all-dropped and the arena decides
+  std::vector<char> dropped(U, 0);
   if (mode == Mode::Collect || mode == Mode::AllLayers) {
     std::fill(dropped.begin(), dropped.end(), 1);
   } else {
     for (int id : plan.dropped_layers)
-      if (id >= 0 && id < L_) dropped[id] = 1;
+      if (id >= 0 && id < U) dropped[id] = 1;
   }
-  for (int l = 0; l < L_; ++l)
-    if (dropped[l]) {
+  for (int u = 0; u < U; ++u)
+    if (dropped[u]) {
       r->plan_size += 1;
-      if (l < 64) r->dropped_mask_lo |= (uint64_t)1 << l;
+      if (u < 64) r->dropped_mask_lo |= (uint64_t)1 << u;
     }
   r->insufficient = plan.insufficient_budget ? 1 : 0;
   if (mode != Mode::Planned)
     r->predicted_kept = constant_bytes_;  // informational only
 
   ctx_->arena.reset_peak();
-  {
-    std::pair<cudaEvent_t, cudaEvent_t> ev;
-    ck(cudaEventCreate(&ev.first), "event");
-    ck(cudaEventCreate(&ev.second), "event");
-    ck(cudaEventRecord(ev.first, s), "event");
-    step_ev_.push_back(ev);
-  }
+  const int slot = static_cast<int>(iter_ % kEvRing);
+  resolve_step_ms(slot);
+  ck(cudaEventRecord(step_ev_[slot][0], s), "event");
   g_wgrad_ws = wgrad_ws_;
   g_wgrad_ws_bytes = wgrad_ws_bytes_;
 
@@ -1459,21 +1604,21 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
        "embed_ln_fwd");
   }
 
-  // ---- encoder blocks
-  std::vector<void*> out(L_, nullptr);
-  std::vector<LayerSave> saves(L_);
-  std::vector<int64_t> measured(L_, 0);
+  // ---- checkpoint units (blocks or block halves)
+  std::vector<void*> out(U, nullptr);
+  std::vector<UnitSave> saves(U);
+  std::vector<int64_t> measured(U, 0);
   const bool collect = mode == Mode::Collect;
   // ---- DTR-style reactive eviction (reference baselines.hpp:62-159) on the
-  // real arena: before a block needs a_l(x) more bytes than fit under the
+  // real arena: before a unit needs a_u(x) more bytes than fit under the
   // budget minus the backward headroom, evict the resident saved set that
   // maximises staleness * bytes / forward_ms down to its boundary output.
   const bool dtr = t_.planner == MIMOSE_PLANNER_DTR && !forced_active_;
   int64_t tick = 0;
-  std::vector<int64_t> last_use(L_, 0);
+  std::vector<int64_t> last_use(U, 0);
   const int64_t dtr_room = ctx_->arena.stats().budget - dtr_headroom(S);
-  auto need_of = [&](int l) {
-    const auto& ls = spec_.layers[static_cast<size_t>(l)];
+  auto need_of = [&](int u) {
+    const auto& ls = spec_.layers[static_cast<size_t>(u)];
     return static_cast<int64_t>(ls.activation_at(static_cast<double>(x)));
   };
   auto evict_until = [&](int64_t need, int upto) {
@@ -1481,7 +1626,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
       int victim = -1;
       double best = -1.0;
       for (int j = 0; j < upto; ++j) {
-        if (dropped[j] || saves[j].qkv == nullptr) continue;
+        if (dropped[j] || !saves[j].live) continue;
         const double ms = std::max(1e-3, spec_.layers[static_cast<size_t>(j)].forward_ms(x));
         const double score = static_cast<double>(tick - last_use[j]) *
                              static_cast<double>(std::max<int64_t>(measured[j], 1)) / ms;
@@ -1497,42 +1642,42 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
       if (victim < 64) r->dropped_mask_lo |= (uint64_t)1 << victim;
     }
   };
-  for (int l = 0; l < L_; ++l) {
-    const void* hin = l == 0 ? h0 : out[l - 1];
+  for (int u = 0; u < U; ++u) {
+    const void* hin = u == 0 ? h0 : out[u - 1];
     if (dtr) {
       ++tick;
-      evict_until(need_of(l), l);
-      last_use[l] = tick;
+      evict_until(need_of(u), u);
+      last_use[u] = tick;
     }
     if (collect) {
       // measuring pass: full save set; the arena's requested-bytes delta is
-      // the block's activation footprint a_l(x) (output included), then
+      // the unit's activation footprint a_u(x) (output included), then
       // everything but the output (the checkpoint boundary) is released.
       const int64_t before = ctx_->arena.stats().requested;
-      ck(cudaEventRecord(ev_[2 * l], s), "event");
-      out[l] = take(T * H * 2, kTagBoundary);
-      layer_fwd(l, hin, out[l], &saves[l], g, s);
-      ck(cudaEventRecord(ev_[2 * l + 1], s), "event");
-      measured[l] = ctx_->arena.stats().requested - before;
-      free_save(saves[l]);
-    } else if (dropped[l]) {
-      out[l] = take(T * H * 2, kTagBoundary);
-      layer_fwd(l, hin, out[l], nullptr, g, s);
+      ck(cudaEventRecord(ev_[2 * u], s), "event");
+      out[u] = take(T * H * 2, kTagBoundary);
+      unit_fwd(u, hin, out[u], &saves[u], g, s);
+      ck(cudaEventRecord(ev_[2 * u + 1], s), "event");
+      measured[u] = ctx_->arena.stats().requested - before;
+      free_save(saves[u]);
+    } else if (dropped[u]) {
+      out[u] = take(T * H * 2, kTagBoundary);
+      unit_fwd(u, hin, out[u], nullptr, g, s);
     } else {
       const int64_t before = ctx_->arena.stats().requested;
-      out[l] = take(T * H * 2, kTagAct);
-      layer_fwd(l, hin, out[l], &saves[l], g, s);
-      measured[l] = ctx_->arena.stats().requested - before;
+      out[u] = take(T * H * 2, kTagAct);
+      unit_fwd(u, hin, out[u], &saves[u], g, s);
+      measured[u] = ctx_->arena.stats().requested - before;
     }
   }
-  // memory-prediction error on the kept blocks (allocator-measured a_l(x))
+  // memory-prediction error on the kept units (allocator-measured a_u(x))
   if (trained_) {
     double sum = 0.0, mx = 0.0;
     int n = 0;
-    for (int l = 0; l < L_; ++l) {
-      if (dropped[l] || measured[l] <= 0) continue;
-      const double pred = static_cast<double>(mimose::predict(est_, l, x));
-      const double err = std::abs(pred - static_cast<double>(measured[l])) / static_cast<double>(measured[l]);
+    for (int u = 0; u < U; ++u) {
+      if (dropped[u] || measured[u] <= 0) continue;
+      const double pred = static_cast<double>(mimose::predict(est_, u, x));
+      const double err = std::abs(pred - static_cast<double>(measured[u])) / static_cast<double>(measured[u]);
       sum += err;
       mx = std::max(mx, err);
       ++n;
@@ -1543,14 +1688,14 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   }
 
   // ---- final LayerNorm (pre-LN / GPT-2) and the task head (forward + backward)
-  void* hidden = out[L_ - 1];
+  void* hidden = out[U - 1];
   void* xf = nullptr;
   void* stf = nullptr;
   if (!bert) {
     xf = take(T * H * 2, kTagAct);
     stf = take(T * 8, kTagAct);
     mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.br = out[L_ - 1];
+    la.rows = (int)T; la.br = out[U - 1];
     la.gamma = p32_ + fln_g_.off; la.beta = p32_ + fln_b_.off; la.eps = m_.ln_eps;
     la.stats = stf; la.y = xf;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
@@ -1560,7 +1705,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   if (!bert) {
     void* dl = take(T * H * 2, kTagTransient);
     mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dy; a.z = out[L_ - 1]; a.stats = stf; a.gamma = p32_ + fln_g_.off;
+    a.rows = (int)T; a.dy = dy; a.z = out[U - 1]; a.stats = stf; a.gamma = p32_ + fln_g_.off;
     a.dz = dl;
     a.partial = ln_partial_;
     ck(mimose_ops::ln_bwd(a, (int)H, G + fln_g_.off, G + fln_b_.off, nullptr, s), "ln_bwd");
@@ -1571,18 +1716,20 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   }
   dp_unit_done(L_ + 1, s);
 
-  // ---- backward through the blocks (recompute dropped ones first)
-  for (int l = L_ - 1; l >= 0; --l) {
-    const void* hin = l == 0 ? h0 : out[l - 1];
+  // ---- backward through the units (recompute dropped ones first)
+  void* aux = nullptr;  // pre-LN attention-branch gradient handed FFN half -> attention half
+  for (int u = U - 1; u >= 0; --u) {
+    const void* hin = u == 0 ? h0 : out[u - 1];
     if (dtr) {
       ++tick;
-      if (dropped[l]) evict_until(need_of(l) - 2 * T * H, l);
-      last_use[l] = tick;
+      if (dropped[u]) evict_until(need_of(u) - 2 * T * H, u);
+      last_use[u] = tick;
     }
-    if (dropped[l]) layer_fwd(l, hin, out[l], &saves[l], g, s);  // recompute, same streams
-    void* dx = layer_bwd(l, hin, saves[l], dy, g, s);
-    dp_unit_done(l + 1, s);
-    drop(out[l]);
+    if (dropped[u]) unit_fwd(u, hin, out[u], &saves[u], g, s);  // recompute, same streams
+    void* dx = unit_bwd(u, hin, saves[u], dy, &aux, g, s);
+    // a block's parameters are final once its attention half is done
+    if (!half_ || u % 2 == 0) dp_unit_done(unit_block(u) + 1, s);
+    drop(out[u]);
     dy = dx;
   }
 
@@ -1606,7 +1753,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   drop(z0); drop(st0); drop(h0);
   // tied decoders (LM / MLM) already wrote their [V, H] weight gradient: add
   ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s,
-                                 tied),
+                                 tied, m_.pad_token_id),
      "embed_word_grad");
   ck(mimose_ops::embed_pos_grad(de, B, S, (int)H, G + pos_.off, s), "embed_pos_grad");
   if (m_.type_vocab > 0)
@@ -1624,26 +1771,71 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
 
   // ---- commit collector measurements (reference collector.hpp:129-184)
   if (collect) {
-    ck(cudaEventSynchronize(ev_[2 * L_ - 1]), "event sync");
+    ck(cudaEventSynchronize(ev_[2 * U - 1]), "event sync");
     const bool fresh = cstate_.seen_sizes.count(x) == 0;
-    for (int l = 0; l < L_ && fresh; ++l) {
+    for (int u = 0; u < U && fresh; ++u) {
       float ms = 0.f;
-      ck(cudaEventElapsedTime(&ms, ev_[2 * l], ev_[2 * l + 1]), "event elapsed");
+      ck(cudaEventElapsedTime(&ms, ev_[2 * u], ev_[2 * u + 1]), "event elapsed");
       mimose::CollectedSample smp;
-      smp.layer_id = l;
+      smp.layer_id = u;
       smp.input_size = x;
-      smp.measured_activation_bytes = measured[l];
+      smp.measured_activation_bytes = measured[u];
       smp.measured_forward_ms = ms;
-      smp.valid = true;  // blocks are flat: no nested checkpoint scopes to filter
+      smp.valid = true;  // units are flat: no nested checkpoint scopes to filter
       cstate_.samples.push_back(smp);
     }
     cstate_.seen_sizes.insert(x);
     cstate_.collected_iterations += 1;
     if (trained_ && ccfg_.collect_new_sizes_always) refit(r);
   }
-  ck(cudaEventRecord(step_ev_.back().second, s), "event");
+  ck(cudaEventRecord(step_ev_[slot][1], s), "event");
+  step_ev_iter_[slot] = iter_;
   history_.push_back(*r);
+  history_ms_.push_back(-1.f);
+  while (history_.size() > kHistoryCap) {
+    history_.pop_front();
+    history_ms_.pop_front();
+    history_first_ += 1;
+  }
   iter_ += 1;
+}
+
+// Device milliseconds of the step recorded in ring slot `slot` -> its
+// history row (the ring is recycled every kEvRing steps).
+void Trainer::resolve_step_ms(int slot) {
+  const int64_t it = step_ev_iter_[slot];
+  if (it < 0) return;
+  step_ev_iter_[slot] = -1;
+  float ms = 0.f;
+  ck(cudaEventSynchronize(step_ev_[slot][1]), "event");
+  ck(cudaEventElapsedTime(&ms, step_ev_[slot][0], step_ev_[slot][1]), "event");
+  const int64_t k = it - history_first_;
+  if (k >= 0 && k < static_cast<int64_t>(history_ms_.size())) history_ms_[static_cast<size_t>(k)] = ms;
+}
+
+mimose_step_report* Trainer::history_row(int64_t iter) {
+  const int64_t k = iter - history_first_;
+  if (k < 0 || k >= static_cast<int64_t>(history_.size())) return nullptr;
+  return &history_[static_cast<size_t>(k)];
+}
+
+// Step scope: arena blocks taken while a step runs are tracked; a step that
+// throws (budget breach, bad input, CUDA error) releases them, so the next
+// step starts from the post-constructor arena state.
+void Trainer::begin_step() {
+  step_live_.clear();
+  in_step_ = true;
+}
+
+void Trainer::end_step(bool ok) {
+  in_step_ = false;
+  if (!ok) {
+    for (void* p : step_live_) ctx_->arena.free(p);
+    // the event slot of the failed step is recorded-but-unfinished at most
+    for (int k = 0; k < kEvRing; ++k)
+      if (step_ev_iter_[k] == iter_) step_ev_iter_[k] = -1;
+  }
+  step_live_.clear();
 }
 
 void Trainer::attach_dp(DataParallel* dp, int64_t bucket_bytes) {
@@ -1800,7 +1992,13 @@ void Trainer::step_host(const int32_t* tokens, const int32_t* types, const int32
   void* dv = d;
   drop(dv);
   if (do_optimizer) {
-    if (hook_) hook_(hook_user_, g32_, nparam_, s);
+    if (hook_) {
+      // the hook sees final gradients: bucketed all-reduces still in flight
+      // on the communicator's stream are joined first (the optimizer's own
+      // join then has nothing left to wait for)
+      if (dp_ != nullptr) dp_->join(s);
+      hook_(hook_user_, g32_, nparam_, s);
+    }
     optimizer_step(1.f, s);
   }
   // loss read-back into a pinned ring slot (read later by loss(iter) or now)
@@ -1821,8 +2019,7 @@ float Trainer::loss(int64_t iter) {
     throw std::runtime_error("loss of iteration " + std::to_string(iter) + " is not available");
   ck(cudaEventSynchronize(loss_ev_[j]), "loss wait");
   const float v = h_loss_[j];
-  for (auto& h : history_)
-    if (h.iter == iter) h.loss = v;
+  if (mimose_step_report* h = history_row(iter)) h->loss = v;
   return v;
 }
 
@@ -1848,6 +2045,18 @@ int guarded(const char* what, Fn&& fn) {
   } catch (const std::exception& e) {
     return fail(std::string(what) + ": " + e.what());
   }
+}
+// one training step inside the trainer's step scope (see begin_step)
+template <typename Fn>
+void in_step(Trainer* t, Fn&& fn) {
+  t->begin_step();
+  try {
+    fn();
+  } catch (...) {
+    t->end_step(false);
+    throw;
+  }
+  t->end_step(true);
 }
 char* dup_string(const std::string& s) {
   char* p = static_cast<char*>(std::malloc(s.size() + 1));
@@ -1885,7 +2094,9 @@ int mimose_trainer_step(mimose_trainer* tr, const int32_t* tokens, const int32_t
                         const int32_t* labels, int batch, int seq, void* stream,
                         mimose_step_report* rep) {
   return guarded("mimose_trainer_step", [&] {
-    tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep);
+    in_step(tr->impl, [&] {
+      tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep);
+    });
   });
 }
 
@@ -1893,8 +2104,10 @@ int mimose_trainer_step_async(mimose_trainer* tr, const int32_t* tokens, const i
                               const int32_t* labels, int batch, int seq, void* stream,
                               mimose_step_report* rep) {
   return guarded("mimose_trainer_step_async", [&] {
-    tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream), rep,
-                        /*sync=*/false);
+    in_step(tr->impl, [&] {
+      tr->impl->step_host(tokens, types, labels, batch, seq, 1, static_cast<cudaStream_t>(stream),
+                          rep, /*sync=*/false);
+    });
   });
 }
 
@@ -1906,7 +2119,9 @@ int mimose_trainer_forward_backward(mimose_trainer* tr, const int32_t* tokens,
                                     const int32_t* types, const int32_t* labels, int batch,
                                     int seq, void* stream, mimose_step_report* rep) {
   return guarded("mimose_trainer_forward_backward", [&] {
-    tr->impl->step_host(tokens, types, labels, batch, seq, 0, static_cast<cudaStream_t>(stream), rep);
+    in_step(tr->impl, [&] {
+      tr->impl->step_host(tokens, types, labels, batch, seq, 0, static_cast<cudaStream_t>(stream), rep);
+    });
   });
 }
 
@@ -1919,9 +2134,11 @@ int mimose_trainer_step_device(mimose_trainer* tr, const int32_t* tokens, const 
     in.tokens = tokens; in.types = types; in.labels = labels;
     in.perm = perm; in.seg = seg; in.uid = uid; in.n_unique = n_unique;
     auto s = static_cast<cudaStream_t>(stream);
-    tr->impl->device_labels(in, batch, seq, s);
-    tr->impl->forward_backward(in, batch, seq, s, rep);
-    tr->impl->release_device_labels(in);
+    in_step(tr->impl, [&] {
+      tr->impl->device_labels(in, batch, seq, s);
+      tr->impl->forward_backward(in, batch, seq, s, rep);
+      tr->impl->release_device_labels(in);
+    });
     if (do_optimizer) tr->impl->optimizer_step(1.f, s);
   });
 }

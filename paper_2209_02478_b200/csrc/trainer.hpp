@@ -15,7 +15,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
+#include <map>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "capi_common.hpp"
@@ -34,11 +37,26 @@ struct LayerParams {
   ParamRef wqkv, bqkv, wo, bo, ln1_g, ln1_b, w1, b1, w2, b2, ln2_g, ln2_b;
 };
 
-struct LayerSave {
+// Saved tensors of the attention half of a block. z1: post-LN = LN1 input
+// (h + dropout(attn)), pre-LN = LN1 output x1; st1 = LN1 {mean, rstd}.
+struct AttnSave {
   void *qkv = nullptr, *P = nullptr, *Pd = nullptr, *ctx = nullptr, *z1 = nullptr,
-       *h1 = nullptr, *u = nullptr, *g = nullptr, *z2 = nullptr, *st1 = nullptr,
-       *st2 = nullptr;
+       *st1 = nullptr;
   void *lse = nullptr, *mask = nullptr;  // flash attention (attn_fused = 3) instead of P / Pd
+};
+// Saved tensors of the FFN half. z2: post-LN = LN2 input, pre-LN = LN2
+// output x2 (the FFN input); u = FFN1 pre-activation, g = GELU(u).
+struct FfnSave {
+  void *z2 = nullptr, *st2 = nullptr, *u = nullptr, *g = nullptr;
+};
+// Saved set of one checkpoint unit (a whole block, or one half of it). For
+// whole-block units h1 - the block-internal attention-half output - is saved
+// too; for half units it is the attention unit's output (a boundary).
+struct UnitSave {
+  AttnSave a;
+  FfnSave f;
+  void* h1 = nullptr;
+  bool live = false;
 };
 
 struct StepGeo {
@@ -101,36 +119,59 @@ class Trainer {
   bool trained() const { return trained_; }
   const mimose::PlanCache& cache() const { return cache_; }
   const mimose::SchedulerConfig& sched() const { return sched_; }
-  const std::vector<mimose_step_report>& history() const { return history_; }
+  const std::deque<mimose_step_report>& history() const { return history_; }
   int64_t constant_bytes() const { return constant_bytes_; }
   int64_t reserve_bytes() const { return sched_.effective_reserve(); }
   int param_count() const { return static_cast<int>(param_names_.size()); }
   void param_info(int i, const char** name, int64_t* off, int64_t* n) const;
-  int64_t extras_bytes(int S) const;
+  // bytes outside the planner-managed units that can be live at once; with
+  // n_dropped >= 0 the retained outputs of exactly that many dropped units,
+  // else of every unit
+  int64_t extras_bytes(int S, int n_dropped = -1) const;
+  int64_t unit_out_bytes(int S) const { return 2LL * t_.batch * S * H_; }
   int64_t head_bytes(int S) const;
   int64_t block_work_bytes(int S) const;
+  int64_t nonunit_bytes(int S) const;
   int64_t dtr_headroom(int S) const;
   // the run so far in the reference's report schema (harness.hpp:57-118):
   // per-iteration rows with MEASURED peak bytes and device milliseconds
   mimose::SimReport report();
 
  private:
-  // arena helpers (throw on budget breach)
-  void* take(int64_t bytes, int tag);
-  void drop(void*& p);
   ParamRef add_param(const std::string& name, int64_t n, bool decay, std::vector<ParamRef*>& fix);
 
   void build_params();
   void init_params(cudaStream_t s);
   void build_spec();
 
-  // layer executor
-  void layer_fwd(int l, const void* h, void* y, LayerSave* save, const StepGeo& g,
+  // unit executor. Checkpoint units are whole blocks (ckpt_unit 0, the
+  // reference's layer granularity) or block halves (ckpt_unit 1: unit 2l =
+  // attention half of block l, 2l + 1 = its FFN half). A unit forward with
+  // save == nullptr keeps only its output; the backward consumes dy (and the
+  // pre-LN attention-branch gradient *aux handed from an FFN half) and the
+  // saved set, and returns the gradient of the unit input.
+ public:
+  int units() const { return half_ ? 2 * L_ : L_; }
+  int unit_block(int u) const { return half_ ? u / 2 : u; }
+  void unit_fwd(int u, const void* in, void* out, UnitSave* save, const StepGeo& g,
+                cudaStream_t s);
+  void* unit_bwd(int u, const void* in, UnitSave& sv, void* dy, void** aux, const StepGeo& g,
                  cudaStream_t s);
-  void* layer_bwd(int l, const void* h, LayerSave& sv, void* dy, const StepGeo& g,
-                  cudaStream_t s);
-  void* attn_fwd(int l, const void* x, LayerSave* save, const StepGeo& g, cudaStream_t s);
-  void* attn_bwd(int l, LayerSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
+  void free_save(UnitSave& sv);
+  void* take(int64_t bytes, int tag);
+  void drop(void*& p);
+
+ private:
+  void attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, const StepGeo& g,
+                     cudaStream_t s);
+  void ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const StepGeo& g,
+                    cudaStream_t s);
+  void* ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void** da, const StepGeo& g,
+                     cudaStream_t s);
+  void* attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void* da, const StepGeo& g,
+                      cudaStream_t s);
+  void* attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, cudaStream_t s);
+  void* attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
   int fused_attn(int S) const;
   bool save_pd() const;
   void* head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g, cudaStream_t s);
@@ -140,8 +181,6 @@ class Trainer {
   void release_device_labels(StepInputs& in);
 
  private:
-  void free_save(LayerSave& sv);
-
   // phase machine (reference harness.hpp:215-296)
   enum class Mode { Plain, Collect, AllLayers, Planned };
   Mode decide(int64_t x, mimose::CheckpointPlan& plan, mimose_step_report* rep);
@@ -151,6 +190,7 @@ class Trainer {
   mimose_model_cfg m_;
   mimose_train_cfg t_;
   int H_, nh_, F_, L_;
+  bool half_ = false;  // checkpoint units = block halves
 
   float* p32_ = nullptr;
   void* p16_ = nullptr;
@@ -195,6 +235,9 @@ class Trainer {
   cudaEvent_t side_ev_[2] = {};
 
   mimose::ModelSpec spec_;
+  // spec_ with the FITTED activation polynomials (unvalidated): the replay
+  // (simulate_iteration) that checks a plan's true peak before it runs
+  mimose::ModelSpec sim_spec_;
   mimose::SchedulerConfig sched_;
   mimose::CollectorConfig ccfg_;
   mimose::CollectorState cstate_;
@@ -204,9 +247,31 @@ class Trainer {
   int64_t iter_ = 0;
   int adam_t_ = 0;
   int64_t constant_bytes_ = 0;
-  std::vector<mimose_step_report> history_;
-  // per-step device time (events on the step's stream), for the report
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> step_ev_;
+  // per-iteration rows (bounded: the oldest are dropped past kHistoryCap) and
+  // their device milliseconds, resolved lazily from a fixed ring of event
+  // pairs recorded on the step's stream (-1 = not resolved yet)
+  static constexpr size_t kHistoryCap = size_t(1) << 18;
+  static constexpr int kEvRing = 16;
+  std::deque<mimose_step_report> history_;
+  std::deque<float> history_ms_;
+  int64_t history_first_ = 0;  // iter of history_.front()
+  cudaEvent_t step_ev_[kEvRing][2] = {};
+  int64_t step_ev_iter_[kEvRing] = {};
+  void resolve_step_ms(int slot);
+  mimose_step_report* history_row(int64_t iter);
+  // reserve the plan of each input size was generated with (cache entries)
+  std::map<int64_t, int64_t> plan_reserve_;
+
+  // exception safety: arena blocks taken during a step are tracked and
+  // released if the step throws (budget breach, bad input), so a failed step
+  // does not shrink the arena for the next one
+  bool in_step_ = false;
+  std::unordered_set<void*> step_live_;
+  friend struct StepScope;
+ public:
+  void begin_step();
+  void end_step(bool ok);
+ private:
 
   bool forced_active_ = false;
   std::vector<int> forced_;

@@ -41,6 +41,9 @@ class ModelConfig:
     head: int = 0        # 0 multiple choice, 1 extractive QA, 2 causal LM (tied), 3 masked LM (tied)
     causal: int = 0
     gelu_tanh: int = 0
+    # HF BertEmbeddings: nn.Embedding(vocab, H, padding_idx=pad_token_id = 0) -
+    # the padding row never receives a gradient; GPT-2 has none (-1)
+    pad_token_id: int = 0
 
     def to_c(self):
         c = _lib.ModelCfg()
@@ -81,6 +84,11 @@ class TrainConfig:
     # automatic reserve sized for each step's S (extras_bytes(S) + 2 %) instead
     # of seq_max: short inputs then keep more blocks (fewer recomputes)
     reserve_per_size: int = 1
+    # checkpoint unit the planner schedules: 0 = whole transformer block (the
+    # reference's layer granularity), 1 = block half (attention half / FFN
+    # half, 2 x layers units): an FFN half frees ~60 % of a block's bytes for
+    # ~45 % of its forward time, so tight budgets recompute less
+    ckpt_unit: int = 1
 
     def to_c(self):
         c = _lib.TrainCfg()
@@ -108,7 +116,7 @@ PRESETS = {
     # configs[3]: GPT-2 medium causal LM, S 128-1024
     "gpt2-medium-lm": (ModelConfig(layers=24, hidden=1024, heads=16, ffn=4096, vocab=50257,
                                    max_pos=1024, type_vocab=0, ln_eps=1e-5, arch=1, head=2,
-                                   causal=1, gelu_tanh=1),
+                                   causal=1, gelu_tanh=1, pad_token_id=-1),
                        TrainConfig(batch=8, seq_min=128, seq_max=1024)),
     # configs[4]: BERT-large MLM pretraining-shaped, S 128-2048 (extended position table)
     "bert-large-mlm": (ModelConfig(layers=24, hidden=1024, heads=16, ffn=4096, max_pos=2048,

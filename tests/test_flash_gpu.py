@@ -155,3 +155,36 @@ def test_flash_fwd_kb128_variant(cuda_device):
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0 and "kb128 ok" in r.stdout, r.stderr[-2000:]
+
+
+# BASELINE sequence lengths and head counts (configs[3] GPT-2 medium S <= 1024,
+# configs[4] BERT-large S <= 2048; 16 heads): forward and backward against the
+# same fp32 restatement.
+@pytest.mark.parametrize("S,B", [(1024, 2), (2048, 1)])
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("p", [0.0, 0.1])
+def test_flash_fwd_bwd_long_16_heads(cuda_device, S, B, causal, p):
+    from paper_2209_02478_b200 import ops
+    nh = 16
+    g = torch.Generator(device="cpu").manual_seed(S + causal)
+    qkv = (torch.randn(B * S, 3 * 64 * nh, generator=g) * 1.5).to(torch.bfloat16).to(cuda_device)
+    dctx = torch.randn(B * S, 64 * nh, generator=g).to(torch.bfloat16).to(cuda_device)
+    seed, stream = 31, 17
+    ctx, lse, mask = ops.flash_attn_fwd(qkv, B, S, nh, causal=causal, dropout_p=p, seed=seed,
+                                        stream_id=stream)
+    dqkv = ops.flash_attn_bwd(qkv, ctx, lse, mask, dctx, B, S, nh, causal=causal, dropout_p=p,
+                              seed=seed, stream_id=stream)
+    torch.cuda.synchronize()
+    x = qkv.float().clone().requires_grad_(True)
+    ref, lse_ref = _ref(x, B, S, nh, causal, p, seed, stream)
+    ref.backward(dctx.float())
+    ref = ref.detach()
+    assert (ctx.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+    assert (lse - lse_ref).abs().max().item() < 1e-3
+    for t in range(3):
+        got = dqkv[:, t * 64 * nh:(t + 1) * 64 * nh].float()
+        exp = x.grad[:, t * 64 * nh:(t + 1) * 64 * nh]
+        err = (got - exp).abs().max().item()
+        assert err <= 2e-2 * exp.abs().max().item(), (t, err, exp.abs().max().item())
+        rel = ((got - exp).norm() / exp.norm()).item()
+        assert rel <= 1e-2, (t, rel)

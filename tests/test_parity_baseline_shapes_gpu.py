@@ -1,0 +1,87 @@
+"""Parity at the shapes the bench runs (BASELINE.json configs[1], [3], [4]):
+the full GPU training step (flash attention, tcgen05 GEMMs, fused LayerNorm /
+dropout / heads) against the fp32 CPU oracle (oracle/bert_ref.py, itself
+pinned to HF transformers in tests/test_oracle_vs_hf.py) on the same
+bf16-rounded weights and the same Philox dropout masks.
+
+Shapes (fewer layers than the bench models - every layer is the same code -
+but the bench's hidden size, head count, vocabulary and sequence length):
+  bert-base-mc   H 768,  12 heads, V 30522, L 2, B 4 (one 4-choice question), S 512
+  gpt2-medium-lm H 1024, 16 heads, V 50257, L 2, B 2, S 1024, causal, tanh GELU, pre-LN
+  bert-large-mlm H 1024, 16 heads, V 30522, L 1, B 1, S 2048, MLM 15 %
+
+Tolerances (bf16 activations and GEMM operands, fp32 accumulation and
+statistics; the smoke step shows ~1e-2):
+  loss           |gpu - cpu| <= 1e-2 * max(1, |cpu|)
+  every gradient ||g_gpu - g_cpu|| <= 2.5e-2 * ||g_cpu|| + 5e-4, cosine >= 0.999
+Checkpointed (every unit dropped and recomputed) == plain, bitwise.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from _helpers import check_grads, grads_by_name, oracle_params
+
+pytestmark = pytest.mark.gpu
+
+from paper_2209_02478_b200.trainer import ModelConfig, TrainConfig, Trainer, synthetic_task_batch  # noqa: E402
+
+GiB = 1 << 30
+SHAPES = {
+    "bert-base-mc": (dict(layers=2, hidden=768, heads=12, ffn=3072, vocab=30522, max_pos=512,
+                          type_vocab=2, num_choices=4), 4, 512),
+    "gpt2-medium-lm": (dict(layers=2, hidden=1024, heads=16, ffn=4096, vocab=50257, max_pos=1024,
+                            type_vocab=0, ln_eps=1e-5, arch=1, head=2, causal=1, gelu_tanh=1,
+                            pad_token_id=-1), 2, 1024),
+    "bert-large-mlm": (dict(layers=1, hidden=1024, heads=16, ffn=4096, vocab=30522, max_pos=2048,
+                            head=3), 1, 2048),
+}
+
+
+def _make(shape, B, S, dropout, unit=1):
+    m = ModelConfig(hidden_dropout=dropout, attn_dropout=dropout, seed=4242, **shape)
+    t = TrainConfig(planner="none", batch=B, seq_min=S, seq_max=S, ckpt_unit=unit)
+    return Trainer(m, t, 40 * GiB)
+
+
+@pytest.mark.parametrize("dropout", [0.0, 0.1])
+@pytest.mark.parametrize("name", list(SHAPES))
+def test_step_parity_at_baseline_shapes(cuda_device, name, dropout):
+    from oracle import bert_ref
+    shape, B, S = SHAPES[name]
+    tr = _make(shape, B, S, dropout)
+    tok, typ, lab = synthetic_task_batch(np.random.default_rng(13), tr.model, B, S)
+    params = oracle_params(tr)
+    rep = tr.step(tok, typ, lab, optimizer=False)
+    got = grads_by_name(tr)
+    tr.close()
+    ref_loss, _, ref_grads = bert_ref.loss_and_grads(params, tok, typ, lab, tr.model, step=0)
+    assert math.isfinite(rep["loss"])
+    assert abs(rep["loss"] - ref_loss) <= 1e-2 * max(1.0, abs(ref_loss)), (rep["loss"], ref_loss)
+    worst = check_grads(got, ref_grads, rel=2.5e-2, min_cos=0.999)
+    print(f"{name} dropout={dropout}: loss {rep['loss']:.6f} vs {ref_loss:.6f}; "
+          f"worst grad rel err {worst[0]:.3e} ({worst[1]})")
+
+
+@pytest.mark.parametrize("unit", [0, 1])
+@pytest.mark.parametrize("name", list(SHAPES))
+def test_checkpointed_bitwise_at_baseline_shapes(cuda_device, name, unit):
+    """Every unit dropped (forward no-save, recompute before backward) gives
+    the plain run's loss and gradients bit for bit, at the bench shapes."""
+    shape, B, S = SHAPES[name]
+    tok, typ, lab = synthetic_task_batch(np.random.default_rng(3), ModelConfig(**shape), B, S)
+    out = []
+    for drop_all in (False, True):
+        tr = _make(shape, B, S, 0.1, unit)
+        n_units = shape["layers"] * (2 if unit else 1)
+        if drop_all:
+            tr.force_plan(range(n_units))
+        rep = tr.step(tok, typ, lab, optimizer=False)
+        assert rep["plan_size"] == (n_units if drop_all else 0)
+        torch.cuda.synchronize()
+        out.append((rep["loss"], tr.grads().clone()))
+        tr.close()
+    assert out[0][0] == out[1][0]
+    assert torch.equal(out[0][1], out[1][1])
