@@ -39,6 +39,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -59,7 +61,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-baseline", action="store_true", help="skip no-ckpt throughput arm")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--size-stream", default="shared", choices=["shared", "per-rank"],
+    ap.add_argument("--size-stream", default="per-rank", choices=["shared", "per-rank"],
                     help="DP length policy: 'shared' = every rank draws S from the same seeded "
                          "stream (length-synchronised sampling, no stragglers; data differs per "
                          "rank); 'per-rank' = seed base+rank (independent lengths, max-over-"
@@ -73,6 +75,8 @@ def parse():
                     help="no-ckpt peak the budget fraction applies to: the materialised-attention "
                          "model's (reference memory semantics, default) or the measured "
                          "configuration's own")
+    ap.add_argument("--ckpt-unit", type=int, default=1, choices=[0, 1],
+                    help="checkpoint unit: 1 = block half (attention / FFN, default), 0 = block")
     ap.add_argument("--profile-only", action="store_true",
                     help="short run for ncu (no comparison arms, no cpu baseline)")
     args = ap.parse_args()
@@ -136,23 +140,12 @@ class ClockSampler:
 
 
 def sizes_for(dist, batch, iters, seed):
+    """Per-step sequence lengths from the product's copy of the reference
+    sampler (include/mimose/workload.hpp sample_workload, bit-exact with it:
+    tests/test_planner_golden.py)."""
     from paper_2209_02478_b200 import planner
     xs = planner.host_lib().workload(dist, 1, iters, seed)
     return [int(x) for x in xs]
-
-
-# ncu --set full (dram__bytes_read.sum + dram__bytes_write.sum) of one
-# representative dense-GEMM launch of the profiled step, next to that launch's
-# algorithmic bytes (operands + outputs once); source files under profiles/.
-TRAFFIC = {
-    # FFN2 forward, 18432 x 768 x 3072 (S = 288, 64 sequences), CTA-pair tile;
-    # profiles/r1b_ncu_full_fwd_summary.txt. Algorithmic = A + B read once +
-    # C written once = 146.2 MB; DRAM traffic is lower because part of the
-    # output is still dirty in the 126 MB L2 when the kernel ends: no re-reads.
-    "bert-base-mc": {"dram_bytes": 132.4e6, "algorithmic_bytes": 146.2e6,
-                     "launch": "gemm_bf16_tn_kernel<256,0,8,2> FFN2 fwd M=18432 N=768 K=3072",
-                     "source": "profiles/r1b_ncu_full_fwd_summary.txt"},
-}
 
 
 def peaks():
@@ -212,9 +205,62 @@ def barrier(world):
 
 
 # ----------------------------------------------------------------- CPU arm
-def cpu_step_sample(model_cfg, S, sub_batch, rng, threads):
-    """One bounded CPU training step (oracle fp32 fwd+bwd + AdamW) of
-    `sub_batch` sequences of length S; returns seconds."""
+def ref_planner_lib():
+    """The UNMODIFIED reference planner (proj/include compiled by
+    oracle/Makefile into oracle/_ref/libmimose_ref.so; built here, shipped to
+    the GPU box with the snapshot) - the reference arm's sizes and plans come
+    from it, not from this repo's product libraries."""
+    from paper_2209_02478_b200.planner import PlannerLib
+    path = os.path.join(ROOT, "oracle", "_ref", "libmimose_ref.so")
+    if not os.path.exists(path):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "_ref/libmimose_ref.so"],
+                       check=True, capture_output=True)
+    return PlannerLib(path, "ref_planner_")
+
+
+def cpu_model_document(model_cfg, batch, s_min, s_max):
+    """The CPU step's memory profile in the reference's own `.model` format,
+    with the reference's own per-block semantics (proj/models/bert12.model:
+    fp32 BERT block = 16 hidden-sized fp32 tensors per token + 3 S x S fp32
+    tensors per head, output = one fp32 hidden state; constant = 16 B/param)."""
+    H, nh, L = model_cfg.hidden, model_cfg.heads, model_cfg.layers
+    from oracle import bert_ref
+    n_param = sum(int(np.prod(s)) for s in bert_ref.param_shapes(model_cfg).values())
+    lines = ["version: 1", f"constant_footprint: {16 * n_param}",
+             f"input_range: {batch * s_min} {batch * s_max}", ""]
+    for l in range(L):
+        lines += ["[layer]", f"id: {l}", f"position: {l}", f"stage: {l}",
+                  "category: quadratic-structure",
+                  f"activation_coeffs: 0 {16 * H * 4} {3 * nh * 4 / batch!r}",
+                  f"boundary_coeffs: 0 {H * 4}", "forward_time_coeffs: 1 0.0006", ""]
+    return "\n".join(lines)
+
+
+def cpu_plans(model_cfg, batch, s_min, s_max, xs, frac):
+    """Mimose on the CPU path: the reference's fit + lookup_or_plan over the
+    CPU model document at a budget of frac x its no-checkpoint peak at S_max."""
+    import numpy as np  # noqa: F401
+    from paper_2209_02478_b200.planner import SchedCfg
+    ref = ref_planner_lib()
+    doc = cpu_model_document(model_cfg, batch, s_min, s_max)
+    # the sheltered collector's samples of this profile at three sizes (exact)
+    H, nh = model_cfg.hidden, model_cfg.heads
+    rows = ["layer_id,input_size,bytes,ms,valid"]
+    for S in (s_min, (s_min + s_max) // 2, s_max):
+        x = batch * S
+        a = round(16 * H * 4 * x + 3 * nh * 4 / batch * x * x)
+        rows += [f"{l},{x},{a},{1 + 0.0006 * x!r},1" for l in range(model_cfg.layers)]
+    est = ref.fit_text("\n".join(rows) + "\n", 2)
+    peak, _, _ = ref.simulate_plan(doc, [], batch * s_max)
+    cfg = SchedCfg(budget_bytes=int(frac * peak))
+    masks, _, _ = ref.plan_seq(est, doc, cfg, [batch * S for S in xs], model_cfg.layers)
+    return [[l for l in range(model_cfg.layers) if (m >> l) & 1] for m in masks], int(frac * peak)
+
+
+def cpu_step_sample(model_cfg, S, sub_batch, rng, threads, ckpt=()):
+    """One bounded CPU training step (oracle fp32 fwd+bwd with the planned
+    blocks under torch.utils.checkpoint, + AdamW) of `sub_batch` sequences of
+    length S; returns seconds."""
     import numpy as np
     import torch
     from oracle import bert_ref
@@ -230,7 +276,8 @@ def cpu_step_sample(model_cfg, S, sub_batch, rng, threads):
               for k, s in shapes.items()}
     tok, typ, lab = synthetic_task_batch(rng, model_cfg, sub_batch, S)
     t0 = time.perf_counter()
-    _, _, grads = bert_ref.loss_and_grads(params, tok, typ, lab, model_cfg, step=0)
+    _, _, grads = bert_ref.loss_and_grads(params, tok, typ, lab, model_cfg, step=0,
+                                          checkpoint_layers=ckpt)
     # AdamW update of every parameter (what the GPU step also does)
     for k, gr in grads.items():
         p = torch.from_numpy(params[k])
@@ -251,24 +298,38 @@ def run_reference_arm(args, rank, world):
     model_cfg, train_cfg = PRESETS[args.preset]
     threads = os.cpu_count() or 1
     sub = model_cfg.num_choices if model_cfg.head == 0 else 1  # one question / sequence
-    xs = sizes_for(args.dist, train_cfg.batch, args.warmup + args.steps, args.seed)
+    # sizes: the reference's own sampler (workload.hpp sample_workload), seed base
+    xs = [int(x) for x in ref_planner_lib().workload(args.dist, 1, args.warmup + args.steps,
+                                                     args.seed)]
+    plans, cpu_budget = cpu_plans(model_cfg, sub, train_cfg.seq_min, train_cfg.seq_max, xs,
+                                  args.budget_frac)
     rng = np.random.default_rng(args.seed)
-    for S in xs[:args.warmup]:
-        cpu_step_sample(model_cfg, S, sub, rng, threads)
+    for S, ck in zip(xs[:args.warmup], plans[:args.warmup]):
+        cpu_step_sample(model_cfg, S, sub, rng, threads, ck)
     tot = 0.0
-    for S in xs[args.warmup:]:
-        tot += cpu_step_sample(model_cfg, S, sub, rng, threads)
+    for S, ck in zip(xs[args.warmup:], plans[args.warmup:]):
+        tot += cpu_step_sample(model_cfg, S, sub, rng, threads, ck)
     value = sub * args.steps / tot
+    timed_plans = plans[args.warmup:]
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "samples/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * tot / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-        "config": {"workload": f"{PRESET_INFO[args.preset][0]} - CPU port", "global_batch": sub,
-                   "seq_len": args.dist, "parallelism": "cpu"},
+        "config": {"workload": f"{PRESET_INFO[args.preset][0]} - CPU path", "global_batch": sub,
+                   "seq_len": args.dist, "parallelism": "cpu",
+                   "budget_frac_of_no_ckpt_peak": args.budget_frac,
+                   "cpu_budget_bytes": cpu_budget},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": threads, "kind": "port",
-                         "sample": f"{sub} sequence(s) per step at the step's drawn S; "
-                                   f"oracle/bert_ref.py fp32 fwd+bwd + AdamW"},
+                         "sample": f"{sub} sequence(s) per step at the step's drawn S "
+                                   f"(reference sampler, oracle/_ref); plans from the compiled "
+                                   f"reference planner (fit + lookup_or_plan) over the fp32 CPU "
+                                   f"profile in bert12.model semantics; oracle/bert_ref.py fp32 "
+                                   f"fwd+bwd with the planned blocks under torch.utils.checkpoint "
+                                   f"+ AdamW",
+                         "avg_checkpointed_blocks": sum(len(p) for p in timed_plans) /
+                                                    max(1, len(timed_plans)),
+                         "seqs": xs[args.warmup:]},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -276,8 +337,18 @@ def run_reference_arm(args, rank, world):
 
 
 # ----------------------------------------------------------------- GPU arm
+def traffic_record(preset):
+    """ncu --set full DRAM traffic (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the dominant dense-GEMM launch, captured at this commit by
+    tools/ncu_traffic.py into profiles/traffic.json (None when absent)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(preset)
+    except Exception:
+        return None
+
+
 def run_gpu_arm(args, rank, world, local):
-    import numpy as np
     import torch
     from paper_2209_02478_b200 import _lib
     from paper_2209_02478_b200.trainer import (PRESETS, PRESET_INFO, DeviceBatch, Trainer,
@@ -286,27 +357,50 @@ def run_gpu_arm(args, rank, world, local):
 
     lib = _lib.cuda_lib()
     model_cfg, train_cfg = PRESETS[args.preset]
-    train_cfg = dataclasses.replace(train_cfg, attn_fused=3 if args.attn == "flash" else 2)
+    train_cfg = dataclasses.replace(train_cfg, attn_fused=3 if args.attn == "flash" else 2,
+                                    ckpt_unit=args.ckpt_unit)
     B = train_cfg.batch
     S_max = train_cfg.seq_max
     stream = torch.cuda.current_stream()
     pk, pk_kind = peaks()
 
-    # 1. no-checkpoint peak at S_max (defines the budget denominator)
+    # gradient exchange for N > 1: the library's own NCCL communicator with
+    # bucketed all-reduce overlapping the backward (MIMOSE_DP=native, default
+    # on NCCL), or one torch.distributed all-reduce after backward (=torch,
+    # and always under the gloo test backend). Its device buffers live
+    # outside the arena, so they are taken off each rank's budget.
+    dp = None
+    if world > 1 and os.environ.get("MIMOSE_DP", "native") == "native":
+        import torch.distributed as dist
+        if dist.get_backend() == "nccl":
+            from paper_2209_02478_b200.dp import NativeDP
+            dp = NativeDP(local, rank, world)
+    nccl_bytes = int(allmax(dp.device_bytes(), world)) if dp is not None else 0
+    bucket_mb = float(os.environ.get("MIMOSE_DP_BUCKET_MB", "32"))
+
+    # 1. no-checkpoint peaks at S_max: the measured configuration's own
+    #    (flash attention: "self") and the materialised-attention model's
+    #    (attention probabilities and their dropout output saved, as HF BERT /
+    #    GPT-2 and the reference's bert12.model do). The budget is
+    #    budget_frac x the --budget-basis one; the other basis is measured too.
     free, total = torch.cuda.mem_get_info()
     ranks_here = max(1, world // max(1, torch.cuda.device_count()))
     probe_budget = int(min(free * 0.85 / ranks_here, 150 * GiB))
-    # the reference model (HF BERT / GPT-2) materialises P and dropout(P): the
-    # budget is a fraction of THAT model's no-checkpoint peak, whichever
-    # attention kernels the measured runs use
-    probe_cfg = dataclasses.replace(train_cfg, planner="none")
-    if args.budget_basis == "materialised":
-        probe_cfg = dataclasses.replace(probe_cfg, attn_fused=2)
-    probe = Trainer(model_cfg, probe_cfg, probe_budget, local)
     rng = np.random.default_rng(args.seed + 1000 * rank)
-    probe.step(*synthetic_task_batch(rng, model_cfg, B, S_max), optimizer=False, stream=stream)
-    peak_none = int(allmax(probe.rows[-1]["peak_reserved"], world))
-    probe.close()
+    probe_batch = synthetic_task_batch(rng, model_cfg, B, S_max)
+
+    def probe_peak(attn_fused):
+        p = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none", attn_fused=attn_fused),
+                    probe_budget, local)
+        p.step(*probe_batch, optimizer=False, stream=stream)
+        v = int(allmax(p.rows[-1]["peak_reserved"], world))
+        p.close()
+        return v
+
+    peak_self = probe_peak(train_cfg.attn_fused)
+    peak_mat = probe_peak(2) if train_cfg.attn_fused != 2 else peak_self
+    bases = {"materialised": peak_mat, "self": peak_self}
+    peak_none = bases[args.budget_basis]
     budget = int(args.budget_frac * peak_none)
 
     n_total = args.warmup + args.steps
@@ -318,18 +412,6 @@ def run_gpu_arm(args, rank, world, local):
         g = np.random.default_rng(seed)
         return [synthetic_task_batch(g, model_cfg, B, s) for s in seq_list]
 
-    # gradient exchange for N > 1: the library's own NCCL communicator with
-    # bucketed all-reduce overlapping the backward (MIMOSE_DP=native, default
-    # on NCCL), or one torch.distributed all-reduce after backward (=torch,
-    # and always under the gloo test backend)
-    dp = None
-    if world > 1 and os.environ.get("MIMOSE_DP", "native") == "native":
-        import torch.distributed as dist
-        if dist.get_backend() == "nccl":
-            from paper_2209_02478_b200.dp import NativeDP
-            dp = NativeDP(local, rank, world)
-    bucket_mb = float(os.environ.get("MIMOSE_DP_BUCKET_MB", "32"))
-
     def allreduce_hook(tr):
         if world == 1 or dp is not None:
             return None
@@ -340,8 +422,8 @@ def run_gpu_arm(args, rank, world, local):
             dist.all_reduce(grads)
         return hook
 
-    def timed_run(tr, host_batches, dev_batches):
-        """W warm-up + K timed device-input steps; returns (ms list, rows)."""
+    def timed_run(tr, dev_batches):
+        """W warm-up + K timed device-input steps; returns (ms, launches)."""
         hook = allreduce_hook(tr)
         scale = 1.0 / world if hook else 1.0  # native DP averages by itself
 
@@ -369,35 +451,56 @@ def run_gpu_arm(args, rank, world, local):
         launches = lib.mimose_launch_count() - l0
         return ms, launches
 
-    # 2. Mimose trainer under the budget; sheltered calibration window first
-    tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="mimose"), budget, local)
-    if dp is not None:
-        tr.attach_dp(dp, bucket_mb)
-    calib = tr.train.max_sheltered_iters + 2
-    cal_batches = batches(seqs[:calib], args.seed + 7 * rank + 1)
-    t_cal0 = time.perf_counter()
-    for b in cal_batches:
-        tr.step(*b, stream=stream)
-    calib_s = time.perf_counter() - t_cal0
+    calib = train_cfg.max_sheltered_iters + 2
     run_seqs = seqs[calib:calib + n_total]
     hb = batches(run_seqs, args.seed + 7 * rank + 2)
     db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in hb]
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ms, launches = timed_run(tr, hb, db)
-    ms_max = allmax(ms, world)
-    rows = tr.rows[-args.steps:]
     samples = B * args.steps * world
-    value = samples / (ms_max / 1000.0)
 
-    # memory discipline + prediction error + planning overhead over the timed steps
-    max_peak = max(r["peak_reserved"] for r in rows)
-    over = [r for r in rows if r["peak_reserved"] > budget]
-    pred = [r["pred_err_max"] for r in rows if r["pred_layers"] > 0]
-    plan_us = sum(r["plan_us"] + r["fit_us"] for r in rows)
-    dropped_avg = sum(r["plan_size"] for r in rows) / len(rows)
+    def mimose_run(run_budget, clocks=False):
+        """Mimose trainer under run_budget: sheltered calibration window, then
+        W + K timed steps; returns (trainer, value, ms, launches, summary, clk)."""
+        tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="mimose"),
+                     run_budget - nccl_bytes, local)
+        if dp is not None:
+            tr.attach_dp(dp, bucket_mb)
+        t_cal0 = time.perf_counter()
+        for b in batches(seqs[:calib], args.seed + 7 * rank + 1):
+            tr.step(*b, stream=stream)
+        calib_s = time.perf_counter() - t_cal0
+        torch.cuda.synchronize()
+        clk = None
+        if clocks:
+            with ClockSampler(local) as clk:
+                ms, launches = timed_run(tr, db)
+        else:
+            ms, launches = timed_run(tr, db)
+        ms = allmax(ms, world)
+        rows = tr.rows[-args.steps:]
+        over = [r for r in rows if r["peak_reserved"] > r["budget"]]
+        pred = [r["pred_err_max"] for r in rows if r["pred_layers"] > 0]
+        plan_us = sum(r["plan_us"] + r["fit_us"] for r in rows)
+        units = sum(r["plan_size"] for r in rows) / len(rows)
+        info = tr.info()
+        summary = {
+            "budget_bytes": run_budget, "arena_bytes": run_budget - nccl_bytes,
+            "max_peak_bytes": max(r["peak_reserved"] for r in rows),
+            "steps_over_budget": len(over), "arena_failures": tr.mem_stats()["n_failures"],
+            "mem_pred_err_max": max(pred) if pred else None,
+            "mem_pred_err_mean": (sum(pred) / len(pred)) if pred else None,
+            "planning_overhead_frac": (plan_us / 1000.0) / ms if ms else None,
+            "avg_dropped_units": units,
+            "avg_dropped_blocks": units / (2 if train_cfg.ckpt_unit == 1 else 1),
+            "constant_bytes": info["constant_bytes"], "reserve_bytes_seq_max": info["reserve_bytes"],
+            "cache_hits": info["cache_hits"], "cache_misses": info["cache_misses"],
+            "calibration_s": calib_s,
+        }
+        return tr, samples / (ms / 1000.0), ms, launches, summary, clk
 
-    # 3. roofline: GEMM family timed per launch (CUDA events) on 2 extra steps
+    # 2. Mimose under the headline budget
+    tr, value, ms_max, launches, summ, clk = mimose_run(budget, clocks=True)
+
+    # 3. roofline: every instrumented launch timed by CUDA events on 2 extra steps
     extra = batches(seqs[calib + n_total:calib + n_total + 2], args.seed + 99)
     extra_db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in extra]
     import ctypes as C
@@ -421,9 +524,11 @@ def run_gpu_arm(args, rank, world, local):
     lib.mimose_profile_csv(C.byref(pcsv))
     classes = sorted({l.split(",", 1)[0] for l in _lib.take_string(lib, pcsv).splitlines()[1:]})
     peak_tf = float(pk.get("bf16_tflops_sustained", pk.get("bf16_tflops", 1400.0)))
+    peak_tf_burst = float(pk.get("bf16_tflops", peak_tf))
     peak_bw = float(pk.get("hbm_gbs", 6547.0))
     # dominant kernel family: the dense (projection / FFN / weight-gradient)
-    # tcgen05 GEMMs, tensor-bound; every other class against HBM
+    # tcgen05 GEMMs, tensor-bound; every other class against HBM (and the
+    # attention kernels also against the tensor burst peak)
     dfl, dby, dms, dn = prof("gemm_dense")
     achieved_tflops = dfl / (dms / 1000.0) / 1e12 if dms > 0 else 0.0
     stages = {}
@@ -440,6 +545,7 @@ def run_gpu_arm(args, rank, world, local):
                       frac=by / (cms / 1e3) / 1e9 / peak_bw)
             if fl > 0:
                 st["achieved_tflops"] = fl / (cms / 1e3) / 1e12
+                st["tensor_frac_burst"] = fl / (cms / 1e3) / 1e12 / peak_tf_burst
         stages[c] = st
     lib.mimose_profile_enable(0)  # (clears the records: read everything first)
 
@@ -479,34 +585,49 @@ def run_gpu_arm(args, rank, world, local):
     e2e_value = samples / e2e_s
     h2d_per_step = sum(x.numel() * 4 for b in pinned[args.warmup:] for x in b) // args.steps
     host_ms = [r["host_ms"] for r in tr.rows[-args.steps:]]
+    tr.close()
 
-    # 5. no-checkpoint, unlimited-memory throughput on the same size stream
+    # 5. the other budget basis, same size stream (the claim on both bases)
+    other = {}
+    if not args.profile_only:
+        ob = "self" if args.budget_basis == "materialised" else "materialised"
+        t2, v2, _, _, s2, _ = mimose_run(int(args.budget_frac * bases[ob]))
+        t2.close()
+        other = {"basis": ob, "value": v2, "no_ckpt_peak_bytes": bases[ob], **s2}
+
+    # 6. no-checkpoint, unlimited-memory throughput on the same size stream
     nock = None
     if not args.no_baseline and not args.profile_only:
         base = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="none"),
-                       int(peak_none * 1.15) + GiB, local)
+                       int(max(peak_self, peak_mat) * 1.15) + GiB, local)
         if dp is not None:
             base.attach_dp(dp, bucket_mb)
-        ms_none, _ = timed_run(base, hb, db)
+        ms_none, _ = timed_run(base, db)
         ms_none = allmax(ms_none, world)
         nock = samples / (ms_none / 1000.0)
         base.close()
+    if other and nock:
+        other["frac_of_no_ckpt"] = other["value"] / nock
 
-    # 6. CPU baseline (rank 0, N=1 only): bounded sample of the same workload
+    # 7. CPU baseline (rank 0, N=1 only): bounded sample of the same workload
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile_only:
         threads = os.cpu_count() or 1
         g = np.random.default_rng(1)
         S_s = run_seqs[:3]
         sub = model_cfg.num_choices if model_cfg.head == 0 else 1
-        tot = sum(cpu_step_sample(model_cfg, S, sub, g, threads) for S in S_s)
+        plans, _ = cpu_plans(model_cfg, sub, train_cfg.seq_min, train_cfg.seq_max, S_s,
+                             args.budget_frac)
+        tot = sum(cpu_step_sample(model_cfg, S, sub, g, threads, ck) for S, ck in zip(S_s, plans))
         cpu = {"value": sub * len(S_s) / tot, "unit": "samples/s", "cores": threads,
                "kind": "port",
                "sample": f"3 steps x {sub} sequence(s) at S={S_s}; oracle/bert_ref.py "
-                         f"PyTorch-CPU fp32 fwd+bwd + AdamW, {threads} threads"}
+                         f"PyTorch-CPU fp32 fwd+bwd (reference-planned blocks under "
+                         f"torch.utils.checkpoint) + AdamW, {threads} threads"}
 
-    info = tr.info()
+    timed_S = run_seqs[args.warmup:]
     if rank == 0:
+        traffic = traffic_record(args.preset)
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -519,18 +640,23 @@ def run_gpu_arm(args, rank, world, local):
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
                 "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
                 "attention": args.attn,
+                "ckpt_unit": "block half (attention / FFN)" if train_cfg.ckpt_unit == 1
+                             else "transformer block",
                 "budget_basis": ("no-ckpt peak of the materialised-attention model at S_max "
                                  "(reference memory semantics)"
                                  if args.budget_basis == "materialised"
                                  else "no-ckpt peak of the measured configuration at S_max"),
+                "nccl_bytes_outside_arena": nccl_bytes,
+                "timed_seq_lens": {"values": timed_S, "mean": sum(timed_S) / len(timed_S),
+                                   "distribution_mean": _dist_mean(args.dist)},
                 "l2": "not flushed: per-step working set (GBs of activations) >> 126 MB L2",
                 "calibration": f"{calib} planner-calibration steps (sheltered collection window "
-                               f"+ fit) run before warm-up, {calib_s:.2f} s",
+                               f"+ fit) run before warm-up, {summ['calibration_s']:.2f} s",
             },
             "roofline": {"bound": "tensor", "achieved": achieved_tflops, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tf,
-                         "traffic": (TRAFFIC.get(args.preset) or {}).get("dram_bytes"),
-                         "traffic_detail": TRAFFIC.get(args.preset),
+                         "traffic": traffic["dram_bytes"] if traffic else None,
+                         "traffic_detail": traffic,
                          "kernel": "gemm_bf16_tn_kernel (tcgen05) dense GEMMs: QKV / out-proj / "
                                    "FFN forward, dgrad, split-K wgrad",
                          "ms_share_of_step": dms / step_ms_prof if step_ms_prof else None,
@@ -552,24 +678,24 @@ def run_gpu_arm(args, rank, world, local):
                     "host_ms_per_step": sum(host_ms) / len(host_ms),
                     "losses_finite": all(l == l for l in losses)},
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
-            "mimose": {
-                "no_ckpt_samples_per_s": nock,
-                "frac_of_no_ckpt": (value / nock) if nock else None,
-                "max_peak_bytes": max_peak, "budget_bytes": budget,
-                "steps_over_budget": len(over), "arena_failures": tr.mem_stats()["n_failures"],
-                "mem_pred_err_max": max(pred) if pred else None,
-                "mem_pred_err_mean": (sum(pred) / len(pred)) if pred else None,
-                "planning_overhead_frac": (plan_us / 1000.0) / ms if ms else None,
-                "avg_dropped_blocks": dropped_avg,
-                "constant_bytes": info["constant_bytes"], "reserve_bytes": info["reserve_bytes"],
-                "cache_hits": info["cache_hits"], "cache_misses": info["cache_misses"],
-            },
+            "clocks": clk.summary() if clk else None,
+            "mimose": {"no_ckpt_samples_per_s": nock,
+                       "frac_of_no_ckpt": (value / nock) if nock else None,
+                       "basis": args.budget_basis, **summ},
+            "mimose_other_basis": other or None,
         }
         print(json.dumps(line), flush=True)
-    tr.close()
     if dp is not None:
         dp.close()
+
+
+def _dist_mean(dist):
+    f = dist.split(":")
+    if f[0] == "uniform":
+        return (float(f[1]) + float(f[2])) / 2
+    if f[0] == "normal":
+        return float(f[1])
+    return None
 
 
 def main():

@@ -306,6 +306,19 @@ int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32
  * has no DP: SPEC.md:196 - this is new surface). */
 int mimose_dp_unique_id(void* out128);
 int mimose_dp_create(int device, const void* unique_id128, int rank, int world, mimose_dp** out);
+/* Injectable transport: the same bucket schedule and comm-stream ordering,
+ * but every reduction is handed to `fn` (buf: device pointer of n elements,
+ * dtype 0 fp32 / 1 bf16, op 0 sum / 1 max, stream: the comm stream, already
+ * ordered behind the backward work that produced the bucket). fn must leave
+ * the cross-rank result in place (stream-ordered or synchronously) and
+ * return 0. Used to run several ranks on one GPU (tests). */
+typedef int (*mimose_dp_reduce_fn)(void* user, void* buf, int64_t n, int dtype, int op,
+                                   void* stream);
+int mimose_dp_create_custom(int device, int rank, int world, mimose_dp_reduce_fn fn, void* user,
+                            mimose_dp** out);
+/* Device bytes the NCCL communicator holds outside the budget arena (measured
+ * around its init and first collective); 0 for custom transports. */
+int mimose_dp_device_bytes(mimose_dp* dp, int64_t* out);
 int mimose_dp_destroy(mimose_dp* dp);
 /* in-place all-reduce of n elements; dtype 0 fp32 / 1 bf16, op 0 sum / 1 max */
 int mimose_dp_allreduce(mimose_dp* dp, void* buf, int64_t n, int dtype, int op, void* stream);

@@ -17,9 +17,14 @@ BertForMultipleChoice as of transformers v4.18 on PyTorch 1.11
   block:  h1 = LN(h + dropout(Wo . attn(h)))  attn probs dropped out
           h2 = LN(h1 + dropout(W2 . gelu(W1 . h1)))       (exact erf GELU)
   head:   logits = dropout(tanh(Wp . h[:, 0])) . wc + bc ; CE over choices
-"parity unpinned" against the reference itself (no reference vectors exist
-for tensors); loss/grad agreement with the GPU is checked at stated
-tolerances in tests/test_trainer_gpu.py.
+Pinned to the third-party implementation itself: tests/test_oracle_vs_hf.py
+loads identical weights into HF BertForMultipleChoice /
+BertForQuestionAnswering / BertForMaskedLM / GPT2LMHeadModel (transformers
+5.5.0, float64, dropout 0) and requires this oracle's loss and every
+gradient to agree to 1e-9 relative; the reference repository itself has no
+tensor vectors. Loss/grad agreement with the GPU is checked at stated
+tolerances in tests/test_trainer_gpu.py and
+tests/test_parity_baseline_shapes_gpu.py.
 
 Dropout masks are reproduced bit-exactly with a numpy restatement of the
 Philox4x32-10 counter scheme the kernels use, so parity holds with dropout on.
@@ -154,8 +159,14 @@ def _drop(x: torch.Tensor, p: float, seed: int, stream: int, idx: np.ndarray) ->
 
 
 def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.ndarray,
-                   labels: np.ndarray, cfg, step: int = 0, dtype=torch.float32):
+                   labels: np.ndarray, cfg, step: int = 0, dtype=torch.float32,
+                   checkpoint_layers=()):
     """Forward + backward on CPU. Returns (loss, logits, {name: grad ndarray}).
+
+    checkpoint_layers: blocks run under torch.utils.checkpoint (the paper's
+    mechanism) - forward without saving, recomputed in the
+    backward; the Philox masks are regenerated identically, so the result
+    does not change (the CPU arm of bench.py times Mimose plans this way).
 
     Architectures (cfg.arch): 0 post-LN BERT block, 1 pre-LN GPT-2 block
     (attention causal when cfg.causal). Heads (cfg.head) and label layouts:
@@ -219,19 +230,26 @@ def loss_and_grads(params: Dict[str, np.ndarray], tokens: np.ndarray, types: np.
         return torch.nn.functional.gelu(u, approximate=gelu_kind) @ P[p + "ffn.out.weight"].T \
             + P[p + "ffn.out.bias"]
 
-    for l in range(L):
+    def block(h, l):
         p = f"layer.{l}."
         if arch == ARCH_BERT:
             a = attention(h, p, l)
             h1 = ln(h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx),
                     p + "attn.ln.weight", p + "attn.ln.bias")
-            h = ln(h1 + _drop(ffn(h1, p), ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx),
-                   p + "ffn.ln.weight", p + "ffn.ln.bias")
+            return ln(h1 + _drop(ffn(h1, p), ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx),
+                      p + "ffn.ln.weight", p + "ffn.ln.bias")
+        a = attention(ln(h, p + "attn.ln.weight", p + "attn.ln.bias"), p, l)
+        h1 = h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx)
+        f = ffn(ln(h1, p + "ffn.ln.weight", p + "ffn.ln.bias"), p)
+        return h1 + _drop(f, ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx)
+
+    ckpt = set(checkpoint_layers)
+    for l in range(L):
+        if l in ckpt:
+            import torch.utils.checkpoint as tuc
+            h = tuc.checkpoint(block, h, l, use_reentrant=False)
         else:
-            a = attention(ln(h, p + "attn.ln.weight", p + "attn.ln.bias"), p, l)
-            h1 = h + _drop(a, ph, seed, stream_id(step, l, SITE_ATTN_OUT), hid_idx)
-            f = ffn(ln(h1, p + "ffn.ln.weight", p + "ffn.ln.bias"), p)
-            h = h1 + _drop(f, ph, seed, stream_id(step, l, SITE_FFN_OUT), hid_idx)
+            h = block(h, l)
     if arch == ARCH_GPT2:
         h = ln(h, "final_ln.weight", "final_ln.bias")
 

@@ -112,6 +112,7 @@ class StepReport(C.Structure):
 
 
 GRAD_HOOK = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+DP_REDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_void_p)
 
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
@@ -190,6 +191,9 @@ CUDA_SYMBOLS = [
      [_P, C.c_int64, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]),
     ("mimose_dp_unique_id", C.c_int, [_P]),
     ("mimose_dp_create", C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.POINTER(_P)]),
+    ("mimose_dp_create_custom", C.c_int,
+     [C.c_int, C.c_int, C.c_int, DP_REDUCE, _P, C.POINTER(_P)]),
+    ("mimose_dp_device_bytes", C.c_int, [_P, C.POINTER(C.c_int64)]),
     ("mimose_dp_destroy", C.c_int, [_P]),
     ("mimose_dp_allreduce", C.c_int, [_P, _P, C.c_int64, C.c_int, C.c_int, _P]),
     ("mimose_trainer_attach_dp", C.c_int, [_P, _P, C.c_int64]),

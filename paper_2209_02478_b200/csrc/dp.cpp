@@ -78,7 +78,31 @@ DataParallel::DataParallel(int device, const void* uid, int rank, int world)
   cck(cudaSetDevice(device), "cudaSetDevice");
   UniqueId id;
   std::memcpy(&id, uid, sizeof(id));
+  size_t free0 = 0, free1 = 0, total = 0;
+  cck(cudaDeviceSynchronize(), "sync");
+  cck(cudaMemGetInfo(&free0, &total), "cudaMemGetInfo");
   nck(*api_, api_->comm_init_rank(&comm_, world, id, rank), "ncclCommInitRank");
+  init_streams();
+  // first collective: NCCL sets up its channel / proxy buffers lazily
+  float* probe = nullptr;
+  cck(cudaMalloc(&probe, 4096), "cudaMalloc");
+  cck(cudaMemsetAsync(probe, 0, 4096, stream_), "memset");
+  allreduce(probe, 1024, 0, 0, stream_);
+  cck(cudaStreamSynchronize(stream_), "sync");
+  cck(cudaFree(probe), "cudaFree");
+  cck(cudaMemGetInfo(&free1, &total), "cudaMemGetInfo");
+  device_bytes_ = free0 > free1 ? static_cast<int64_t>(free0 - free1) : 0;
+}
+
+DataParallel::DataParallel(int device, int rank, int world, ReduceFn fn, void* user)
+    : fn_(fn), user_(user), rank_(rank), world_(world), device_(device) {
+  if (world < 1 || rank < 0 || rank >= world) throw std::runtime_error("bad rank / world");
+  if (fn == nullptr) throw std::runtime_error("null reduce callback");
+  cck(cudaSetDevice(device), "cudaSetDevice");
+  init_streams();
+}
+
+void DataParallel::init_streams() {
   int lo = 0, hi = 0;
   cck(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
   cck(cudaStreamCreateWithPriority(&stream_, cudaStreamNonBlocking, hi), "comm stream");
@@ -88,7 +112,7 @@ DataParallel::DataParallel(int device, const void* uid, int rank, int world)
 
 DataParallel::~DataParallel() {
   if (stream_) cudaStreamSynchronize(stream_);
-  if (comm_ && api_->comm_destroy) api_->comm_destroy(comm_);
+  if (comm_ && api_ && api_->comm_destroy) api_->comm_destroy(comm_);
   if (ready_) cudaEventDestroy(ready_);
   if (done_) cudaEventDestroy(done_);
   if (stream_) cudaStreamDestroy(stream_);
@@ -96,6 +120,10 @@ DataParallel::~DataParallel() {
 
 void DataParallel::allreduce(void* buf, int64_t n, int dtype, int op, cudaStream_t s) {
   if (n <= 0) return;
+  if (fn_ != nullptr) {
+    if (fn_(user_, buf, n, dtype, op, s) != 0) throw std::runtime_error("reduce callback failed");
+    return;
+  }
   const int dt = dtype == 1 ? kNcclBfloat16 : kNcclFloat32;
   nck(*api_, api_->all_reduce(buf, buf, static_cast<size_t>(n), dt, op == 1 ? kNcclMax : kNcclSum,
                               comm_, s),

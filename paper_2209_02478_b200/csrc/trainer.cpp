@@ -1216,6 +1216,53 @@ void* Trainer::unit_bwd(int u, const void* in, UnitSave& sv, void* dy, void** au
   drop(sv.h1);
   return attn_half_bwd(u, in, sv.a, dh1, da, g, s);
 }
+// ------------------------------------------------------------ replay
+// Peak residency of one iteration under `plan` as THIS executor runs it:
+// the reference's iteration semantics (simulate_iteration, simulator.hpp:
+// 104-160: a dropped unit's forward transient a(x), then its own output o(x)
+// kept; recompute +(a - o) right before its backward; the backward frees
+// a(x)) plus the half-unit rule - a block whose two halves are both dropped
+// keeps only the FFN half's output and recomputes its attention half (whole
+// a(x), output included) right before the FFN half. a(x) is the fitted
+// polynomial (sim_spec_), o(x) the unit output.
+int64_t Trainer::replay_peak(const mimose::CheckpointPlan& plan, int64_t x) const {
+  const int U = units();
+  const double xd = static_cast<double>(x);
+  std::vector<int64_t> a(U), o(U);
+  std::vector<char> d(U, 0), rec(U, 0);
+  for (int u = 0; u < U; ++u) {
+    a[u] = mimose::round_bytes(sim_spec_.layers[static_cast<size_t>(u)].activation_at(xd));
+    o[u] = mimose::round_bytes(sim_spec_.layers[static_cast<size_t>(u)].boundary_at(xd));
+  }
+  for (int id : plan.dropped_layers)
+    if (id >= 0 && id < U) d[id] = 1;
+  int64_t res = sim_spec_.constant_footprint, peak = res;
+  for (int u = 0; u < U; ++u) {
+    if (d[u]) {
+      peak = std::max(peak, res + a[u]);
+      res += o[u];
+      if (pair_dropped(u, d)) res -= o[u - 1];
+    } else {
+      res += a[u];
+      peak = std::max(peak, res);
+    }
+  }
+  for (int u = U - 1; u >= 0; --u) {
+    if (d[u] && !rec[u]) {
+      if (pair_dropped(u, d)) {
+        res += a[u - 1];
+        rec[u - 1] = 1;
+        peak = std::max(peak, res);
+      }
+      res += a[u] - o[u];
+      rec[u] = 1;
+      peak = std::max(peak, res);
+    }
+    res -= a[u];
+  }
+  return peak;
+}
+
 // ------------------------------------------------------------ phase machine
 void Trainer::refit(mimose_step_report* rep) {
   const int order = std::min(t_.estimator_order, cstate_.distinct_sizes() - 1);
@@ -1330,7 +1377,7 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
         sc.reserve_bytes = R;
         const mimose::CheckpointPlan trial = mimose::generate_plan(est_, spec_, x, sc);
         if (trial.insufficient_budget) break;
-        const int64_t over = mimose::simulate_iteration(sim_spec_, trial, x).peak_bytes + fixed - budget;
+        const int64_t over = replay_peak(trial, x) + fixed - budget;
         if (over <= 0 || R >= budget - 1) break;
         R = std::min<int64_t>(R + over, budget - 1);
       }
@@ -1669,6 +1716,10 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
       unit_fwd(u, hin, out[u], &saves[u], g, s);
       measured[u] = ctx_->arena.stats().requested - before;
     }
+    // both halves of a block dropped: its FFN half's output is the only
+    // boundary kept; h1 is regenerated with the attention half's recompute
+    // right before the FFN half's (see the backward loop and replay_peak)
+    if (pair_dropped(u, dropped) && !dtr) drop(out[u - 1]);
   }
   // memory-prediction error on the kept units (allocator-measured a_u(x))
   if (trained_) {
@@ -1719,14 +1770,22 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   // ---- backward through the units (recompute dropped ones first)
   void* aux = nullptr;  // pre-LN attention-branch gradient handed FFN half -> attention half
   for (int u = U - 1; u >= 0; --u) {
-    const void* hin = u == 0 ? h0 : out[u - 1];
     if (dtr) {
       ++tick;
       if (dropped[u]) evict_until(need_of(u) - 2 * T * H, u);
       last_use[u] = tick;
     }
-    if (dropped[u]) unit_fwd(u, hin, out[u], &saves[u], g, s);  // recompute, same streams
-    void* dx = unit_bwd(u, hin, saves[u], dy, &aux, g, s);
+    if (dropped[u] && !saves[u].live) {
+      if (out[u - (u > 0 ? 1 : 0)] == nullptr) {
+        // the attention half of a doubly-dropped block first (regenerates h1)
+        const void* ha = u == 1 ? h0 : out[u - 2];
+        out[u - 1] = take(T * H * 2, kTagBoundary);
+        unit_fwd(u - 1, ha, out[u - 1], &saves[u - 1], g, s);
+      }
+      // recompute, same kernels and Philox streams as the forward
+      unit_fwd(u, u == 0 ? h0 : out[u - 1], out[u], &saves[u], g, s);
+    }
+    void* dx = unit_bwd(u, u == 0 ? h0 : out[u - 1], saves[u], dy, &aux, g, s);
     // a block's parameters are final once its attention half is done
     if (!half_ || u % 2 == 0) dp_unit_done(unit_block(u) + 1, s);
     drop(out[u]);
@@ -2253,6 +2312,27 @@ int mimose_dp_create(int device, const void* uid, int rank, int world, mimose_dp
     }
     *out = dp;
   });
+}
+
+int mimose_dp_create_custom(int device, int rank, int world, mimose_dp_reduce_fn fn, void* user,
+                            mimose_dp** out) {
+  if (!fn || !out) return fail("mimose_dp_create_custom: null argument");
+  return guarded("mimose_dp_create_custom", [&] {
+    auto* dp = new mimose_dp();
+    try {
+      dp->impl = new mimose_rt::DataParallel(device, rank, world, fn, user);
+    } catch (...) {
+      delete dp;
+      throw;
+    }
+    *out = dp;
+  });
+}
+
+int mimose_dp_device_bytes(mimose_dp* dp, int64_t* out) {
+  if (!dp || !out) return fail("mimose_dp_device_bytes: null argument");
+  *out = dp->impl->device_bytes();
+  return 0;
 }
 
 int mimose_dp_destroy(mimose_dp* dp) {

@@ -132,6 +132,12 @@ class Trainer {
   int64_t head_bytes(int S) const;
   int64_t block_work_bytes(int S) const;
   int64_t nonunit_bytes(int S) const;
+  // peak residency of an iteration under `plan`, as this executor runs it
+  int64_t replay_peak(const mimose::CheckpointPlan& plan, int64_t x) const;
+  // FFN-half unit u whose attention half is dropped too (half units only)
+  bool pair_dropped(int u, const std::vector<char>& d) const {
+    return half_ && u % 2 == 1 && d[static_cast<size_t>(u)] && d[static_cast<size_t>(u) - 1];
+  }
   int64_t dtr_headroom(int S) const;
   // the run so far in the reference's report schema (harness.hpp:57-118):
   // per-iteration rows with MEASURED peak bytes and device milliseconds

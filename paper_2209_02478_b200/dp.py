@@ -18,6 +18,8 @@ from typing import Callable, List, Optional, Sequence
 
 import numpy as np
 
+from .trainer import _DevArray
+
 
 def rank_sizes(dist: str, iterations: int, base_seed: int, rank: int) -> List[int]:
     """Per-rank sequence lengths: the reference sampler with seed base + rank."""
@@ -61,17 +63,31 @@ class DataParallelTrainer:
             self._grads = self.tr.grads()
         return self._grads
 
+    def _exchange(self, stream):
+        if getattr(self.tr, "_dp", None) is not None:
+            raise RuntimeError("trainer has a NativeDP attached: gradients would be reduced "
+                               "(and scaled by 1/world) twice")
+        if self.world > 1:
+            import torch
+            # the all-reduce runs on torch's current stream: order it behind
+            # the backward issued on `stream`
+            if stream is not None and torch.cuda.is_available():
+                s = stream if isinstance(stream, torch.cuda.Stream) else \
+                    torch.cuda.ExternalStream(stream)
+                with torch.cuda.stream(s):
+                    self._allreduce(self.grads())
+            else:
+                self._allreduce(self.grads())
+
     def step(self, tokens, types, labels, stream=None) -> dict:
         row = self.tr.step(tokens, types, labels, optimizer=False, stream=stream)
-        if self.world > 1:
-            self._allreduce(self.grads())
+        self._exchange(stream)
         self.tr.optimizer_step(1.0 / self.world, stream=stream)
         return row
 
     def step_device(self, batch, stream=None) -> dict:
         row = self.tr.step_device(batch, optimizer=False, stream=stream)
-        if self.world > 1:
-            self._allreduce(self.grads())
+        self._exchange(stream)
         self.tr.optimizer_step(1.0 / self.world, stream=stream)
         return row
 
@@ -87,11 +103,40 @@ class NativeDP:
     and the optimizer waits for the last bucket and scales by 1/world.
     """
 
-    def __init__(self, device: int, rank: int, world: int, group=None, unique_id: bytes = None):
+    def __init__(self, device: int, rank: int, world: int, group=None, unique_id: bytes = None,
+                 reduce_fn: Optional[Callable] = None):
+        """reduce_fn(tensor, op, stream) -> None: custom transport instead of
+        NCCL (tensor = CUDA view of the bucket, op 'sum' / 'max', stream =
+        torch.cuda.ExternalStream of the communicator's stream, already
+        ordered behind the backward that produced the bucket); it must leave
+        the cross-rank result in `tensor`."""
         import ctypes as C
-        from ._lib import check, cuda_lib
+        from ._lib import DP_REDUCE, check, cuda_lib
         self.lib = cuda_lib()
         self.rank, self.world = rank, world
+        self.reduce_calls = 0
+        if reduce_fn is not None:
+            import torch
+
+            def _cb(user, buf, n, dtype, op, stream):
+                try:
+                    typestr = "<f4" if dtype == 0 else "<i2"
+                    t = torch.as_tensor(_DevArray(buf, n, typestr), device="cuda")
+                    if dtype == 1:
+                        t = t.view(torch.bfloat16)
+                    reduce_fn(t, "max" if op == 1 else "sum",
+                              torch.cuda.ExternalStream(stream, device=torch.device("cuda", device)))
+                    self.reduce_calls += 1
+                    return 0
+                except Exception as e:  # noqa: BLE001 - reported through the C status
+                    self.error = e
+                    return 1
+            self._cb = DP_REDUCE(_cb)
+            h = C.c_void_p()
+            check(self.lib.mimose_dp_create_custom(int(device), int(rank), int(world), self._cb,
+                                                   None, C.byref(h)))
+            self.handle = h
+            return
         if unique_id is None:
             buf = (C.c_char * 128)()
             if rank == 0:
@@ -106,6 +151,14 @@ class NativeDP:
         h = C.c_void_p()
         check(self.lib.mimose_dp_create(int(device), uid, int(rank), int(world), C.byref(h)))
         self.handle = h
+
+    def device_bytes(self) -> int:
+        """Device memory the NCCL communicator holds outside the budget arena."""
+        import ctypes as C
+        from ._lib import check
+        out = C.c_int64()
+        check(self.lib.mimose_dp_device_bytes(self.handle, C.byref(out)))
+        return out.value
 
     def allreduce_(self, tensor, op: str = "sum", stream=None):
         """In-place all-reduce of a CUDA fp32 / bf16 tensor on `stream`."""

@@ -31,6 +31,13 @@ def check_grads(got, ref_grads, rel, floor=5e-4, min_cos=0.995):
     """Every gradient within rel * ||ref|| + floor (L2) and cosine >= min_cos.
     Returns the worst relative error seen (for the failure message / logs)."""
     worst = (0.0, None)
+    import os
+    log = os.environ.get("MIMOSE_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            for name, ref in ref_grads.items():
+                nr = float(np.linalg.norm(ref))
+                f.write(f"{name} {float(np.linalg.norm(got[name] - ref)) / max(nr, 1e-12):.4e} {nr:.4e}\n")
     for name, ref in ref_grads.items():
         g = got[name]
         nr = np.linalg.norm(ref)

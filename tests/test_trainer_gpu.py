@@ -71,15 +71,10 @@ def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
     assert abs(rep["loss"] - ref_loss) <= 2e-2 * max(1.0, abs(ref_loss)), (rep["loss"], ref_loss)
     logits = tr.logits_device().cpu().numpy()
     assert np.allclose(logits, ref_logits, atol=5e-2, rtol=5e-2)
-    got = _grads_by_name(tr)
-    for name, ref in ref_grads.items():
-        g = got[name]
-        nr = np.linalg.norm(ref)
-        err = np.linalg.norm(g - ref)
-        assert err <= 8e-2 * nr + 1e-6, f"{name}: rel err {err / max(nr, 1e-12):.3e}"
-        if nr > 1e-6:
-            cos = float(np.dot(g, ref) / (np.linalg.norm(g) * nr + 1e-30))
-            assert cos >= 0.995, f"{name}: cosine {cos}"
+    # absolute floor as in _check_grads: the key third of qkv.bias has an
+    # exactly-zero gradient (softmax is shift-invariant per row), so only
+    # bf16 rounding noise remains there on the GPU
+    _check_grads(_grads_by_name(tr), ref_grads)
     tr.close()
 
 
@@ -259,7 +254,9 @@ def test_mimose_phases_budget_and_plan_parity(cuda_device, per_size):
     # cache is keyed by x (tolerance 0), so a repeated x must be a hit
     seen = set()
     for r in planned:
-        assert 0 < r["reserve_bytes"] <= info["reserve_bytes"]
+        # per-size reserves are verified against the plan's own replay and may
+        # exceed the static seq_max figure (recompute transients)
+        assert 0 < r["reserve_bytes"] < info["budget"]
         if not per_size:
             assert r["reserve_bytes"] == info["reserve_bytes"]
         cfg = host.SchedCfg(budget_bytes=info["budget"], reserve_bytes=r["reserve_bytes"])
