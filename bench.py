@@ -9,20 +9,32 @@ reference's own sampler (include/mimose/workload.hpp sample_workload, seed
 base+rank), random-init weights (N(0, 0.02)), AdamW, dropout 0.1, bf16
 compute. Budget = 40 % of the measured no-checkpoint peak at S_max
 (everything - weights, grads, AdamW state, activations, workspace - lives in
-the budget arena). --preset picks the other BASELINE configs (parity /
-reporting runs): small4-h256, roberta-{base,large}-qa, gpt2-medium-lm,
-bert-large-mlm, each with its own default size distribution and budget.
+the budget arena). The peak is measured twice: for the materialised-
+attention model (the reference's / HF's memory semantics, --budget-basis
+materialised, the headline default) and for the measured flash-attention
+configuration itself ("self"); the line carries the Mimose run on BOTH
+budgets (mimose / mimose_other_basis) against the same no-checkpoint
+throughput. --preset picks the other BASELINE configs (parity / reporting
+runs): small4-h256, roberta-{base,large}-qa, gpt2-medium-lm, bert-large-mlm,
+each with its own default size distribution and budget; --planner static-max
+| dtr runs the reference's baseline planners under the same budget.
 
-N > 1: one rank per GPU; the gradient exchange is the library's own NCCL
-communicator (mimose_dp_*) with bucketed all-reduce issued as the backward
-finishes each block (MIMOSE_DP=torch: one torch all-reduce after backward).
+N > 1: one rank per GPU, each drawing its own sequence lengths (seed base +
+rank) and planning under its own budget; the gradient exchange is the
+library's own NCCL communicator (mimose_dp_*) with bucketed all-reduce
+issued as the backward finishes each block (MIMOSE_DP=torch: one torch
+all-reduce after backward). NCCL's own device buffers are measured and
+taken off each rank's arena.
 
 Arms
   default            this repo's B200 path (python bench.py --gpus N ...)
-  --impl reference   the CPU path: the oracle's PyTorch-CPU fp32 restatement
-                     of the same training step (the reference itself is a
-                     byte/ms simulator with no tensor code), all host cores,
-                     bounded sub-batch per step, rank 0 only.
+  --impl reference   the CPU path: sizes and plans from the compiled
+                     UNMODIFIED reference (oracle/_ref), the oracle's
+                     PyTorch-CPU fp32 restatement of the step with the
+                     planned blocks under torch.utils.checkpoint (the
+                     reference itself is a byte/ms simulator with no tensor
+                     code), all host cores, bounded sub-batch per step, rank 0
+                     only.
 
 One JSON line on rank 0. Timing: W untimed warm-up steps after the planner's
 sheltered calibration window, then exactly K steps bracketed by barrier +
@@ -75,6 +87,12 @@ def parse():
                     help="no-ckpt peak the budget fraction applies to: the materialised-attention "
                          "model's (reference memory semantics, default) or the measured "
                          "configuration's own")
+    ap.add_argument("--planner", default="mimose", choices=["mimose", "static-max", "dtr"],
+                    help="planner of the measured runs under the budget: Mimose (the product), "
+                         "static-max (plan once for S_max, reference baselines.hpp:20-23) or "
+                         "dtr (reactive eviction on the real arena, baselines.hpp:62-159)")
+    ap.add_argument("--cache-tol", type=float, default=0.0,
+                    help="plan-cache tolerance (reference scheduler.hpp:27, 204-221)")
     ap.add_argument("--ckpt-unit", type=int, default=1, choices=[0, 1],
                     help="checkpoint unit: 1 = block half (attention / FFN, default), 0 = block")
     ap.add_argument("--profile-only", action="store_true",
@@ -358,7 +376,7 @@ def run_gpu_arm(args, rank, world, local):
     lib = _lib.cuda_lib()
     model_cfg, train_cfg = PRESETS[args.preset]
     train_cfg = dataclasses.replace(train_cfg, attn_fused=3 if args.attn == "flash" else 2,
-                                    ckpt_unit=args.ckpt_unit)
+                                    ckpt_unit=args.ckpt_unit, cache_tolerance=args.cache_tol)
     B = train_cfg.batch
     S_max = train_cfg.seq_max
     stream = torch.cuda.current_stream()
@@ -460,7 +478,7 @@ def run_gpu_arm(args, rank, world, local):
     def mimose_run(run_budget, clocks=False):
         """Mimose trainer under run_budget: sheltered calibration window, then
         W + K timed steps; returns (trainer, value, ms, launches, summary, clk)."""
-        tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner="mimose"),
+        tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner=args.planner),
                      run_budget - nccl_bytes, local)
         if dp is not None:
             tr.attach_dp(dp, bucket_mb)
@@ -679,7 +697,8 @@ def run_gpu_arm(args, rank, world, local):
                     "losses_finite": all(l == l for l in losses)},
             "gpu_launches": int(launches),
             "clocks": clk.summary() if clk else None,
-            "mimose": {"no_ckpt_samples_per_s": nock,
+            "mimose": {"planner": args.planner, "cache_tolerance": args.cache_tol,
+                       "no_ckpt_samples_per_s": nock,
                        "frac_of_no_ckpt": (value / nock) if nock else None,
                        "basis": args.budget_basis, **summ},
             "mimose_other_basis": other or None,

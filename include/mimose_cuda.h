@@ -300,6 +300,61 @@ void mimose_free_string(char* s);
 int mimose_build_token_tables(const int32_t* tokens, int64_t T, int vocab, int32_t* perm,
                               int32_t* seg, int32_t* uid, int* n_unique);
 
+/* ------------------------------------------------------- layer-level ABI
+ * the per-unit operations of one training iteration, so a
+ * caller can run the reference's training loop itself - the Mimose branch of
+ * reference harness.hpp:215-296 with its simulate_iteration /
+ * collect_iteration calls (harness.hpp:189,196,221,231,240,265,286) replaced
+ * by these (tests/host/harness_gpu.cpp does exactly that, with the planner
+ * from mimose_planner.h). Every buffer is a block of the trainer's budget
+ * arena; buffers the library allocates are released with mimose_free.
+ * A checkpoint unit is a transformer block (mimose_train_cfg.ckpt_unit 0) or
+ * a block half (1: unit 2l = attention half of block l, 2l + 1 = FFN half). */
+typedef struct mimose_saved mimose_saved;  /* saved set of one unit / the embeddings */
+typedef struct {
+  const int32_t* tokens;        /* device [batch*seq] */
+  const int32_t* types;         /* device [batch*seq] (zeros when type_vocab == 0) */
+  const int32_t* labels;        /* device, the head's layout (mimose_trainer_step) */
+  const int32_t* perm;          /* device token tables (mimose_build_token_tables) */
+  const int32_t* seg;
+  const int32_t* uid;
+  int n_unique;
+  int batch, seq;
+  int64_t step;                 /* iteration index: selects the dropout (Philox) streams */
+} mimose_layer_io;
+
+int mimose_trainer_units(mimose_trainer* tr, int* n_units);
+/* *h0 = dropout(LN(word + pos + type)) (BERT) | dropout(word + pos) (GPT-2); *saved
+ * receives the embedding's saved set. */
+int mimose_embed_fwd(mimose_trainer* tr, const mimose_layer_io* io, void** h0,
+                     mimose_saved** saved, void* stream);
+/* Unit forward x_in -> x_out ([batch*seq][hidden] bf16, caller's arena block).
+ * saved == NULL: no-save forward (the unit is dropped: only x_out stays);
+ * else *saved receives the unit's saved set. Recompute = the same call with
+ * saved != NULL (same kernels, same Philox streams: bit-identical). */
+int mimose_layer_fwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,
+                     void* x_out, mimose_saved** saved, void* stream);
+/* Unit backward: consumes dy (arena block, grad of x_out) and saved; *dx =
+ * grad of x_in (arena block). Units are differentiated last to first. */
+int mimose_layer_bwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,
+                     mimose_saved* saved, void* dy, void** dx, void* stream);
+/* Final LayerNorm (GPT-2) + task head forward, loss (mimose_trainer_buffers
+ * d_loss) and head backward; *dlast = grad of the last unit's output. */
+int mimose_head_fwd_bwd(mimose_trainer* tr, const mimose_layer_io* io, const void* last,
+                        void** dlast, void* stream);
+/* Embedding backward: consumes dh0, h0 and the embedding's saved set. */
+int mimose_embed_bwd(mimose_trainer* tr, const mimose_layer_io* io, mimose_saved* saved,
+                     void* h0, void* dh0, void* stream);
+int mimose_saved_free(mimose_trainer* tr, mimose_saved* saved);
+/* Fused AdamW over the flat parameters (global-norm clipping; grad_scale on
+ * the raw gradients). Same as mimose_trainer_optimizer_step. */
+int mimose_adamw_step(mimose_trainer* tr, float grad_scale, void* stream);
+/* Timing for the collector (cudaEvent wrappers; elapsed synchronises on end). */
+int mimose_event_create(void** ev);
+int mimose_event_record(void* ev, void* stream);
+int mimose_event_elapsed(void* start, void* end, float* ms);
+int mimose_event_destroy(void* ev);
+
 /* ---- data parallelism (§8(b2) mimose_dp_*) --------------
  * One NCCL communicator per rank (NCCL resolved at run time). The unique id
  * (128 bytes) is made on rank 0 and broadcast by the caller (the reference

@@ -47,6 +47,21 @@ int mimose_planner_plan_sequence(const char* estimator_text, const char* model_t
                                  uint64_t* dropped_masks, int mask_words, int* insufficient,
                                  int* cache_hit);
 
+/* A planning session: the estimator, the model document, the scheduler
+ * config and ONE persistent PlanCache (scheduler.hpp:169-227), as the
+ * reference harness keeps them across iterations (harness.hpp:277-293).
+ * set_estimator swaps in a refit estimator and keeps the cache, as
+ * harness.hpp:264-276 does. reserve_bytes >= 0 overrides the session's
+ * reserve for this call (per-input-size reserves). */
+typedef struct mimose_plan_session mimose_plan_session;
+int mimose_planner_session_create(const char* estimator_text, const char* model_text,
+                                  const mimose_sched_cfg* cfg, mimose_plan_session** out);
+int mimose_planner_session_set_estimator(mimose_plan_session* s, const char* estimator_text);
+int mimose_planner_session_plan(mimose_plan_session* s, int64_t x, int64_t reserve_bytes,
+                                uint64_t* dropped_mask, int mask_words, int* insufficient,
+                                int* cache_hit);
+int mimose_planner_session_destroy(mimose_plan_session* s);
+
 int mimose_planner_simulate(const char* model_text, const int* dropped, int n_dropped,
                             int64_t x, int64_t* peak_bytes, double* iteration_ms,
                             double* recompute_ms);

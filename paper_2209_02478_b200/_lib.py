@@ -117,6 +117,14 @@ DP_REDUCE = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c
 _P = C.c_void_p
 _I32P = C.POINTER(C.c_int32)
 
+class LayerIO(C.Structure):
+    _fields_ = [
+        ("tokens", C.c_void_p), ("types", C.c_void_p), ("labels", C.c_void_p),
+        ("perm", C.c_void_p), ("seg", C.c_void_p), ("uid", C.c_void_p), ("n_unique", C.c_int),
+        ("batch", C.c_int), ("seq", C.c_int), ("step", C.c_int64),
+    ]
+
+
 class AttnArgs(C.Structure):
     _fields_ = [
         ("B", C.c_int), ("S", C.c_int), ("nh", C.c_int), ("causal", C.c_int),
@@ -189,6 +197,19 @@ CUDA_SYMBOLS = [
     ("mimose_free_string", None, [_P]),
     ("mimose_build_token_tables", C.c_int,
      [_P, C.c_int64, C.c_int, _P, _P, _P, C.POINTER(C.c_int)]),
+    ("mimose_trainer_units", C.c_int, [_P, C.POINTER(C.c_int)]),
+    ("mimose_embed_fwd", C.c_int, [_P, C.POINTER(LayerIO), C.POINTER(_P), C.POINTER(_P), _P]),
+    ("mimose_layer_fwd", C.c_int, [_P, C.c_int, C.POINTER(LayerIO), _P, _P, C.POINTER(_P), _P]),
+    ("mimose_layer_bwd", C.c_int,
+     [_P, C.c_int, C.POINTER(LayerIO), _P, _P, _P, C.POINTER(_P), _P]),
+    ("mimose_head_fwd_bwd", C.c_int, [_P, C.POINTER(LayerIO), _P, C.POINTER(_P), _P]),
+    ("mimose_embed_bwd", C.c_int, [_P, C.POINTER(LayerIO), _P, _P, _P, _P]),
+    ("mimose_saved_free", C.c_int, [_P, _P]),
+    ("mimose_adamw_step", C.c_int, [_P, C.c_float, _P]),
+    ("mimose_event_create", C.c_int, [C.POINTER(_P)]),
+    ("mimose_event_record", C.c_int, [_P, _P]),
+    ("mimose_event_elapsed", C.c_int, [_P, _P, C.POINTER(C.c_float)]),
+    ("mimose_event_destroy", C.c_int, [_P]),
     ("mimose_dp_unique_id", C.c_int, [_P]),
     ("mimose_dp_create", C.c_int, [C.c_int, _P, C.c_int, C.c_int, C.POINTER(_P)]),
     ("mimose_dp_create_custom", C.c_int,

@@ -398,20 +398,23 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
         const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
         float x[32];
-        float mraw = kNegInf;
+        // four independent max chains (a single 32-deep chain serialises on
+        // the FMNMX latency)
+        float mr[4] = {kNegInf, kNegInf, kNegInf, kNegInf};
         if (all_full) {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             x[e] = __uint_as_float(raw[e]);
-            mraw = fmaxf(mraw, x[e]);
+            mr[e & 3] = fmaxf(mr[e & 3], x[e]);
           }
         } else {
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
             x[e] = e < lim ? __uint_as_float(raw[e]) : kNegInf;
-            mraw = fmaxf(mraw, x[e]);
+            mr[e & 3] = fmaxf(mr[e & 3], x[e]);
           }
         }
+        const float mraw = fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3]));
         const float mb = mraw * p.sc;
         if (j == 0) {
           m_used = mb;
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         // this P buffer is free once the P V of two blocks ago has run
         mbar_wait(&pvdone[sb * NSL + w], ((jb >> 1) & 1) ^ 1);
         const float m_eff = m_used == kNegInf ? 0.f : m_used;
-        float psum = 0.f;
+        float ps[4] = {0.f, 0.f, 0.f, 0.f};  // four independent row-sum chains
         uint32_t pk[16];
         if (all_dead) {
 #pragma unroll
@@ -451,7 +454,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
           for (int e = 0; e < 32; e += 2) {
             // p = 2^(s * sc - m): one FFMA + ex2 per score
             float a0 = fl_ex2(fmaf(x[e], p.sc, -m_eff)), a1 = fl_ex2(fmaf(x[e + 1], p.sc, -m_eff));
-            psum += a0 + a1;
+            ps[(e >> 1) & 3] += a0 + a1;
             if (thr_hi != 0) {  // keep bits from flash_keep_mask_kernel
               if (!((kw >> e) & 1u)) a0 = 0.f;
               if (!((kw >> (e + 1)) & 1u)) a1 = 0.f;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
             pk[e >> 1] = fl_pack(a0, a1);
           }
         }
-        l += psum;
+        l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
         if (trw) FT(tro + 2, FT_CLK());
         const uint32_t rowa = smem_u32(sP + sb * Cfg::kPBytes + (w >> 1) * 16384) + r * 128;
 #pragma unroll

@@ -70,7 +70,56 @@ mimose::SchedulerConfig to_sched(const mimose_sched_cfg* c) {
 
 }  // namespace
 
+struct mimose_plan_session {
+  mimose::EstimatorModel est;
+  mimose::ModelSpec model;
+  mimose::SchedulerConfig sched;
+  mimose::PlanCache cache;
+};
+
 extern "C" {
+
+int mimose_planner_session_create(const char* estimator_text, const char* model_text,
+                                  const mimose_sched_cfg* cfg, mimose_plan_session** out) {
+  return guard([&] {
+    auto* s = new mimose_plan_session();
+    try {
+      s->est = mimose::estimator_from_string(estimator_text);
+      s->model = mimose::load_model_from_string(model_text);
+      s->sched = to_sched(cfg);
+    } catch (...) {
+      delete s;
+      throw;
+    }
+    *out = s;
+  });
+}
+
+int mimose_planner_session_set_estimator(mimose_plan_session* s, const char* estimator_text) {
+  return guard([&] { s->est = mimose::estimator_from_string(estimator_text); });
+}
+
+int mimose_planner_session_plan(mimose_plan_session* s, int64_t x, int64_t reserve_bytes,
+                                uint64_t* dropped_mask, int mask_words, int* insufficient,
+                                int* cache_hit) {
+  return guard([&] {
+    mimose::SchedulerConfig sc = s->sched;
+    if (reserve_bytes >= 0) sc.reserve_bytes = reserve_bytes;
+    auto [plan, hit] = mimose::lookup_or_plan(s->cache, s->est, s->model, x, sc);
+    for (int w = 0; w < mask_words; ++w) dropped_mask[w] = 0;
+    for (int id : plan.dropped_layers) {
+      if (id < 0 || id >= 64 * mask_words) throw mimose::Error("layer id beyond mask width");
+      dropped_mask[id / 64] |= uint64_t{1} << (id % 64);
+    }
+    *insufficient = plan.insufficient_budget ? 1 : 0;
+    *cache_hit = hit ? 1 : 0;
+  });
+}
+
+int mimose_planner_session_destroy(mimose_plan_session* s) {
+  delete s;
+  return 0;
+}
 
 const char* mimose_planner_last_error(void) { return g_err.c_str(); }
 void mimose_planner_free(char* s) { std::free(s); }

@@ -1327,16 +1327,12 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
     case MIMOSE_PLANNER_DTR:
       return Mode::Plain;
     case MIMOSE_PLANNER_ALL:
-      for (int l = 0; l < L_; ++l) plan.dropped_layers.push_back(l);
+      for (int u = 0; u < units(); ++u) plan.dropped_layers.push_back(u);
       return Mode::Plain;
-    case MIMOSE_PLANNER_STATIC: {
-      // provisioned once for the largest input from the analytic profile
-      static_cast<void>(0);
-      mimose::EstimatorModel ex = mimose::exact_estimator(spec_);
-      plan = mimose::static_max_plan(ex, spec_, spec_.input_max, sched_);
-      return Mode::Plain;
-    }
     default:
+      // MIMOSE and STATIC share the sheltered collection and the fit; the
+      // static planner (reference baselines.hpp:20-23 static_max_plan) then
+      // provisions every step for the largest input instead of this one
       break;
   }
   const bool unseen = cstate_.seen_sizes.count(x) == 0;
@@ -1365,19 +1361,20 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
   // entry keeps the reserve it was generated with, so a hit replays exactly.
   mimose::SchedulerConfig sc = sched_;
   const auto t0 = std::chrono::steady_clock::now();
+  const int64_t xp = t_.planner == MIMOSE_PLANNER_STATIC ? spec_.input_max : x;
   if (t_.reserve_bytes < 0 && t_.reserve_per_size) {
     const int64_t budget = sched_.budget_bytes;
-    const auto known = plan_reserve_.find(x);
-    if (known != plan_reserve_.end() && cache_.entries.count(x)) {
+    const auto known = plan_reserve_.find(xp);
+    if (known != plan_reserve_.end() && cache_.entries.count(xp)) {
       sc.reserve_bytes = known->second;
     } else {
-      const int64_t fixed = nonunit_bytes(static_cast<int>(x / t_.batch)) + budget * 3 / 100;
+      const int64_t fixed = nonunit_bytes(static_cast<int>(xp / t_.batch)) + budget * 3 / 100;
       int64_t R = std::min<int64_t>(fixed, budget - 1);
       for (int it = 0; it <= units() + 1; ++it) {
         sc.reserve_bytes = R;
-        const mimose::CheckpointPlan trial = mimose::generate_plan(est_, spec_, x, sc);
+        const mimose::CheckpointPlan trial = mimose::generate_plan(est_, spec_, xp, sc);
         if (trial.insufficient_budget) break;
-        const int64_t over = replay_peak(trial, x) + fixed - budget;
+        const int64_t over = replay_peak(trial, xp) + fixed - budget;
         if (over <= 0 || R >= budget - 1) break;
         R = std::min<int64_t>(R + over, budget - 1);
       }
@@ -1385,16 +1382,16 @@ Trainer::Mode Trainer::decide(int64_t x, mimose::CheckpointPlan& plan, mimose_st
     }
   }
   rep->reserve_bytes = sc.effective_reserve();
-  auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, x, sc);
+  auto [p, hit] = mimose::lookup_or_plan(cache_, est_, spec_, xp, sc);
   const auto t1 = std::chrono::steady_clock::now();
   rep->plan_us = std::chrono::duration<double, std::micro>(t1 - t0).count();
   if (!hit) {
-    cache_.entries[x].generated_at_iter = iter_;
+    cache_.entries[xp].generated_at_iter = iter_;
     p.generated_at_iter = iter_;
-    plan_reserve_[x] = sc.reserve_bytes;
+    plan_reserve_[xp] = sc.reserve_bytes;
   }
   rep->cache_hit = hit ? 1 : 0;
-  rep->predicted_kept = mimose::detail::estimated_kept_bytes(est_, spec_, p, x);
+  rep->predicted_kept = mimose::detail::estimated_kept_bytes(est_, spec_, p, xp);
   plan = p;
   return Mode::Planned;
 }
@@ -1572,8 +1569,94 @@ void* Trainer::head_fwd_bwd(const StepInputs& in, const void* hidden, const Step
 }
 
 // ------------------------------------------------------------------- step
-void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
-                               mimose_step_report* rep) {
+// ------------------------------------------------------ model ends
+// Embeddings: BERT z0 = word + pos (+ type), h0 = dropout(LN(z0)); GPT-2
+// h0 = dropout(word + pos) (no LayerNorm). Returns h0; z0 / stats saved.
+void* Trainer::embed_fwd(const StepInputs& in, const StepGeo& g, EmbedSave& es, cudaStream_t s) {
+  const int64_t T = g.T, H = H_;
+  auto* W = static_cast<bf16raw*>(p16_);
+  const bool bert = m_.arch == MIMOSE_ARCH_BERT;
+  es.z0 = bert ? take(T * H * 2, kTagAct) : nullptr;
+  es.st0 = bert ? take(T * 8, kTagAct) : nullptr;
+  void* h0 = take(T * H * 2, kTagAct);
+  mimose_ops::LnFwdArgs la;
+  la.rows = (int)T;
+  la.skip_ln = !bert;
+  la.gamma = bert ? p32_ + eln_g_.off : nullptr;
+  la.beta = bert ? p32_ + eln_b_.off : nullptr;
+  la.eps = m_.ln_eps;
+  la.z = es.z0; la.stats = es.st0; la.y = h0;
+  la.out_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+  ck(mimose_ops::embed_ln_fwd(la, (int)H, in.tokens, m_.type_vocab > 0 ? in.types : nullptr,
+                              W + word_.off, W + pos_.off,
+                              m_.type_vocab > 0 ? W + type_.off : nullptr, g.S, s),
+     "embed_ln_fwd");
+  return h0;
+}
+
+// Final LayerNorm (pre-LN / GPT-2) + task head forward, loss (-> d_loss_),
+// head backward; returns the gradient of the last unit's output.
+void* Trainer::head_block(const StepInputs& in, const void* last, const StepGeo& g,
+                          cudaStream_t s) {
+  const int64_t T = g.T, H = H_;
+  float* G = g32_;
+  if (m_.arch == MIMOSE_ARCH_BERT) return head_fwd_bwd(in, last, g, s);
+  void* xf = take(T * H * 2, kTagAct);
+  void* stf = take(T * 8, kTagAct);
+  mimose_ops::LnFwdArgs la;
+  la.rows = (int)T; la.br = last;
+  la.gamma = p32_ + fln_g_.off; la.beta = p32_ + fln_b_.off; la.eps = m_.ln_eps;
+  la.stats = stf; la.y = xf;
+  ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
+  void* dy = head_fwd_bwd(in, xf, g, s);
+  void* dl = take(T * H * 2, kTagTransient);
+  mimose_ops::LnBwdArgs a;
+  a.rows = (int)T; a.dy = dy; a.z = last; a.stats = stf; a.gamma = p32_ + fln_g_.off;
+  a.dz = dl;
+  a.partial = ln_partial_;
+  ck(mimose_ops::ln_bwd(a, (int)H, G + fln_g_.off, G + fln_b_.off, nullptr, s), "ln_bwd");
+  drop(dy);
+  drop(xf);
+  drop(stf);
+  return dl;
+}
+
+// Embedding backward: consumes dy (grad of h0), h0 and the saves.
+void Trainer::embed_bwd(const StepInputs& in, const StepGeo& g, EmbedSave& es, void* h0, void* dy,
+                        cudaStream_t s) {
+  const int64_t T = g.T, H = H_;
+  float* G = g32_;
+  const bool bert = m_.arch == MIMOSE_ARCH_BERT;
+  const bool tied = m_.head == MIMOSE_HEAD_LM || m_.head == MIMOSE_HEAD_MLM;
+  if (!tied) ck(cudaMemsetAsync(G + word_.off, 0, word_.n * 4, s), "memset");
+  ck(cudaMemsetAsync(G + pos_.off, 0, pos_.n * 4, s), "memset");
+  void* de = take(T * H * 2, kTagTransient);
+  const auto edrop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
+  if (bert) {
+    mimose_ops::LnBwdArgs a;
+    a.rows = (int)T; a.dy = dy; a.z = es.z0; a.stats = es.st0; a.gamma = p32_ + eln_g_.off;
+    a.in_drop = edrop;
+    a.dz = de;
+    a.partial = ln_partial_;
+    ck(mimose_ops::ln_bwd(a, (int)H, G + eln_g_.off, G + eln_b_.off, nullptr, s), "ln_bwd");
+  } else {
+    ck(mimose_ops::dropout_apply(dy, de, T * H, edrop, s), "dropout_apply");
+  }
+  drop(dy);
+  drop(es.z0); drop(es.st0); drop(h0);
+  // tied decoders (LM / MLM) already wrote their [V, H] weight gradient: add
+  ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s,
+                                 tied, m_.pad_token_id),
+     "embed_word_grad");
+  ck(mimose_ops::embed_pos_grad(de, g.B, g.S, (int)H, G + pos_.off, s), "embed_pos_grad");
+  if (m_.type_vocab > 0)
+    ck(mimose_ops::colsum(de, (int)T, (int)H, H, m_.type_vocab == 2 ? in.types : nullptr,
+                          m_.type_vocab, col_partial_, G + type_.off, s),
+       "colsum");
+  drop(de);
+}
+
+StepGeo Trainer::geometry(int B, int S, int64_t step) const {
   if (B != t_.batch) throw std::runtime_error("batch differs from the configured batch");
   if (S < t_.seq_min || S > t_.seq_max) throw std::runtime_error("sequence length outside range");
   StepGeo g;
@@ -1581,12 +1664,18 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   g.S = S;
   g.ld = round8(S);
   g.T = (int64_t)B * S;
-  g.step = static_cast<uint64_t>(iter_);
+  g.step = static_cast<uint64_t>(step);
+  g_wgrad_ws = wgrad_ws_;
+  g_wgrad_ws_bytes = wgrad_ws_bytes_;
+  return g;
+}
+
+void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t s,
+                               mimose_step_report* rep) {
+  const StepGeo g = geometry(B, S, iter_);
   const int64_t x = g.T;
   const int64_t T = g.T, H = H_;
   const int U = units();
-  auto* W = static_cast<bf16raw*>(p16_);
-  float* G = g32_;
 
   const auto host_t0 = std::chrono::steady_clock::now();
   mimose_step_report local{};
@@ -1627,29 +1716,9 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   const int slot = static_cast<int>(iter_ % kEvRing);
   resolve_step_ms(slot);
   ck(cudaEventRecord(step_ev_[slot][0], s), "event");
-  g_wgrad_ws = wgrad_ws_;
-  g_wgrad_ws_bytes = wgrad_ws_bytes_;
 
-  // ---- embeddings: BERT z0 = word + pos (+ type), h0 = dropout(LN(z0));
-  //                  GPT-2 h0 = dropout(word + pos) (no LayerNorm)
-  const bool bert = m_.arch == MIMOSE_ARCH_BERT;
-  void* z0 = bert ? take(T * H * 2, kTagAct) : nullptr;
-  void* st0 = bert ? take(T * 8, kTagAct) : nullptr;
-  void* h0 = take(T * H * 2, kTagAct);
-  {
-    mimose_ops::LnFwdArgs la;
-    la.rows = (int)T;
-    la.skip_ln = !bert;
-    la.gamma = bert ? p32_ + eln_g_.off : nullptr;
-    la.beta = bert ? p32_ + eln_b_.off : nullptr;
-    la.eps = m_.ln_eps;
-    la.z = z0; la.stats = st0; la.y = h0;
-    la.out_drop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
-    ck(mimose_ops::embed_ln_fwd(la, (int)H, in.tokens, m_.type_vocab > 0 ? in.types : nullptr,
-                                W + word_.off, W + pos_.off,
-                                m_.type_vocab > 0 ? W + type_.off : nullptr, S, s),
-       "embed_ln_fwd");
-  }
+  EmbedSave es;
+  void* h0 = embed_fwd(in, g, es, s);
 
   // ---- checkpoint units (blocks or block halves)
   std::vector<void*> out(U, nullptr);
@@ -1739,32 +1808,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   }
 
   // ---- final LayerNorm (pre-LN / GPT-2) and the task head (forward + backward)
-  void* hidden = out[U - 1];
-  void* xf = nullptr;
-  void* stf = nullptr;
-  if (!bert) {
-    xf = take(T * H * 2, kTagAct);
-    stf = take(T * 8, kTagAct);
-    mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.br = out[U - 1];
-    la.gamma = p32_ + fln_g_.off; la.beta = p32_ + fln_b_.off; la.eps = m_.ln_eps;
-    la.stats = stf; la.y = xf;
-    ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    hidden = xf;
-  }
-  void* dy = head_fwd_bwd(in, hidden, g, s);
-  if (!bert) {
-    void* dl = take(T * H * 2, kTagTransient);
-    mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dy; a.z = out[U - 1]; a.stats = stf; a.gamma = p32_ + fln_g_.off;
-    a.dz = dl;
-    a.partial = ln_partial_;
-    ck(mimose_ops::ln_bwd(a, (int)H, G + fln_g_.off, G + fln_b_.off, nullptr, s), "ln_bwd");
-    drop(dy);
-    drop(xf);
-    drop(stf);
-    dy = dl;
-  }
+  void* dy = head_block(in, out[U - 1], g, s);
   dp_unit_done(L_ + 1, s);
 
   // ---- backward through the units (recompute dropped ones first)
@@ -1793,33 +1837,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   }
 
   // ---- embedding backward
-  const bool tied = m_.head == MIMOSE_HEAD_LM || m_.head == MIMOSE_HEAD_MLM;
-  if (!tied) ck(cudaMemsetAsync(G + word_.off, 0, word_.n * 4, s), "memset");
-  ck(cudaMemsetAsync(G + pos_.off, 0, pos_.n * 4, s), "memset");
-  void* de = take(T * H * 2, kTagTransient);
-  const auto edrop = mimose_ops::make_dropout(m_.hidden_dropout, m_.seed, stream_id(g.step, L_, kSiteEmbed));
-  if (bert) {
-    mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dy; a.z = z0; a.stats = st0; a.gamma = p32_ + eln_g_.off;
-    a.in_drop = edrop;
-    a.dz = de;
-    a.partial = ln_partial_;
-    ck(mimose_ops::ln_bwd(a, (int)H, G + eln_g_.off, G + eln_b_.off, nullptr, s), "ln_bwd");
-  } else {
-    ck(mimose_ops::dropout_apply(dy, de, T * H, edrop, s), "dropout_apply");
-  }
-  drop(dy);
-  drop(z0); drop(st0); drop(h0);
-  // tied decoders (LM / MLM) already wrote their [V, H] weight gradient: add
-  ck(mimose_ops::embed_word_grad(de, (int)H, in.perm, in.seg, in.uid, in.n_unique, G + word_.off, s,
-                                 tied, m_.pad_token_id),
-     "embed_word_grad");
-  ck(mimose_ops::embed_pos_grad(de, B, S, (int)H, G + pos_.off, s), "embed_pos_grad");
-  if (m_.type_vocab > 0)
-    ck(mimose_ops::colsum(de, (int)T, (int)H, H, m_.type_vocab == 2 ? in.types : nullptr,
-                          m_.type_vocab, col_partial_, G + type_.off, s),
-       "colsum");
-  drop(de);
+  embed_bwd(in, g, es, h0, dy, s);
   dp_unit_done(0, s);
 
   r->host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0)
@@ -2094,6 +2112,11 @@ struct mimose_trainer {
 struct mimose_dp {
   mimose_rt::DataParallel* impl = nullptr;
 };
+struct mimose_saved {
+  bool embed = false;
+  mimose_rt::UnitSave unit;
+  mimose_rt::EmbedSave emb;
+};
 
 namespace {
 template <typename Fn>
@@ -2312,6 +2335,152 @@ int mimose_dp_create(int device, const void* uid, int rank, int world, mimose_dp
     }
     *out = dp;
   });
+}
+
+// ------------------------------------------------------- layer-level ABI
+static mimose_rt::StepInputs io_inputs(const mimose_layer_io* io) {
+  mimose_rt::StepInputs in;
+  in.tokens = io->tokens; in.types = io->types; in.labels = io->labels;
+  in.perm = io->perm; in.seg = io->seg; in.uid = io->uid; in.n_unique = io->n_unique;
+  return in;
+}
+
+int mimose_trainer_units(mimose_trainer* tr, int* n_units) {
+  if (!tr || !n_units) return fail("mimose_trainer_units: null argument");
+  *n_units = tr->impl->units();
+  return 0;
+}
+
+int mimose_embed_fwd(mimose_trainer* tr, const mimose_layer_io* io, void** h0,
+                     mimose_saved** saved, void* stream) {
+  if (!tr || !io || !h0 || !saved) return fail("mimose_embed_fwd: null argument");
+  return guarded("mimose_embed_fwd", [&] {
+    Trainer* t = tr->impl;
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    auto* sv = new mimose_saved();
+    sv->embed = true;
+    try {
+      *h0 = t->embed_fwd(io_inputs(io), g, sv->emb, static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      delete sv;
+      throw;
+    }
+    *saved = sv;
+  });
+}
+
+int mimose_layer_fwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,
+                     void* x_out, mimose_saved** saved, void* stream) {
+  if (!tr || !io || !x_in || !x_out) return fail("mimose_layer_fwd: null argument");
+  return guarded("mimose_layer_fwd", [&] {
+    Trainer* t = tr->impl;
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    if (saved == nullptr) {
+      t->unit_fwd(unit, x_in, x_out, nullptr, g, static_cast<cudaStream_t>(stream));
+      return;
+    }
+    auto* sv = new mimose_saved();
+    try {
+      t->unit_fwd(unit, x_in, x_out, &sv->unit, g, static_cast<cudaStream_t>(stream));
+    } catch (...) {
+      t->free_save(sv->unit);
+      delete sv;
+      throw;
+    }
+    *saved = sv;
+  });
+}
+
+int mimose_layer_bwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,
+                     mimose_saved* saved, void* dy, void** dx, void* stream) {
+  if (!tr || !io || !x_in || !saved || saved->embed || !dy || !dx)
+    return fail("mimose_layer_bwd: bad argument");
+  return guarded("mimose_layer_bwd", [&] {
+    Trainer* t = tr->impl;
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    *dx = t->unit_bwd(unit, x_in, saved->unit, dy, &t->pending_aux_, g,
+                      static_cast<cudaStream_t>(stream));
+    delete saved;
+  });
+}
+
+int mimose_head_fwd_bwd(mimose_trainer* tr, const mimose_layer_io* io, const void* last,
+                        void** dlast, void* stream) {
+  if (!tr || !io || !last || !dlast) return fail("mimose_head_fwd_bwd: null argument");
+  return guarded("mimose_head_fwd_bwd", [&] {
+    Trainer* t = tr->impl;
+    auto s = static_cast<cudaStream_t>(stream);
+    auto in = io_inputs(io);
+    t->device_labels(in, io->batch, io->seq, s);
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    try {
+      *dlast = t->head_block(in, last, g, s);
+    } catch (...) {
+      t->release_device_labels(in);
+      throw;
+    }
+    t->release_device_labels(in);
+  });
+}
+
+int mimose_embed_bwd(mimose_trainer* tr, const mimose_layer_io* io, mimose_saved* saved,
+                     void* h0, void* dh0, void* stream) {
+  if (!tr || !io || !saved || !saved->embed || !h0 || !dh0)
+    return fail("mimose_embed_bwd: bad argument");
+  return guarded("mimose_embed_bwd", [&] {
+    Trainer* t = tr->impl;
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    t->embed_bwd(io_inputs(io), g, saved->emb, h0, dh0, static_cast<cudaStream_t>(stream));
+    delete saved;
+  });
+}
+
+int mimose_saved_free(mimose_trainer* tr, mimose_saved* saved) {
+  if (!tr || !saved) return 0;
+  return guarded("mimose_saved_free", [&] {
+    if (saved->embed) {
+      tr->impl->drop(saved->emb.z0);
+      tr->impl->drop(saved->emb.st0);
+    } else {
+      tr->impl->free_save(saved->unit);
+    }
+    delete saved;
+  });
+}
+
+int mimose_adamw_step(mimose_trainer* tr, float grad_scale, void* stream) {
+  return mimose_trainer_optimizer_step(tr, grad_scale, stream);
+}
+
+int mimose_event_create(void** ev) {
+  if (!ev) return fail("mimose_event_create: null argument");
+  return guarded("mimose_event_create", [&] {
+    cudaEvent_t e = nullptr;
+    mimose_rt::ck(cudaEventCreate(&e), "cudaEventCreate");
+    *ev = e;
+  });
+}
+
+int mimose_event_record(void* ev, void* stream) {
+  return guarded("mimose_event_record", [&] {
+    mimose_rt::ck(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)),
+                  "cudaEventRecord");
+  });
+}
+
+int mimose_event_elapsed(void* start, void* end, float* ms) {
+  if (!ms) return fail("mimose_event_elapsed: null argument");
+  return guarded("mimose_event_elapsed", [&] {
+    mimose_rt::ck(cudaEventSynchronize(static_cast<cudaEvent_t>(end)), "cudaEventSynchronize");
+    mimose_rt::ck(cudaEventElapsedTime(ms, static_cast<cudaEvent_t>(start),
+                                       static_cast<cudaEvent_t>(end)),
+                  "cudaEventElapsedTime");
+  });
+}
+
+int mimose_event_destroy(void* ev) {
+  if (ev) cudaEventDestroy(static_cast<cudaEvent_t>(ev));
+  return 0;
 }
 
 int mimose_dp_create_custom(int device, int rank, int world, mimose_dp_reduce_fn fn, void* user,

@@ -59,6 +59,10 @@ struct UnitSave {
   bool live = false;
 };
 
+struct EmbedSave {
+  void *z0 = nullptr, *st0 = nullptr;  // BERT: LN input and {mean, rstd}
+};
+
 struct StepGeo {
   int B = 0, S = 0, ld = 0;
   int64_t T = 0;
@@ -181,6 +185,20 @@ class Trainer {
   int fused_attn(int S) const;
   bool save_pd() const;
   void* head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g, cudaStream_t s);
+
+ public:
+  // model ends, used by forward_backward and the layer-level C ABI
+  StepGeo geometry(int B, int S, int64_t step) const;
+  void* embed_fwd(const StepInputs& in, const StepGeo& g, EmbedSave& es, cudaStream_t s);
+  void* head_block(const StepInputs& in, const void* last, const StepGeo& g, cudaStream_t s);
+  void embed_bwd(const StepInputs& in, const StepGeo& g, EmbedSave& es, void* h0, void* dy,
+                 cudaStream_t s);
+  int64_t iter() const { return iter_; }
+  // pre-LN attention-branch gradient between an FFN half's and its attention
+  // half's backward when driven unit by unit through the C ABI
+  void* pending_aux_ = nullptr;
+
+ private:
   int label_count(int B, int S) const;
  public:
   void device_labels(StepInputs& in, int B, int S, cudaStream_t s);

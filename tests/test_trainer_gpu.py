@@ -395,3 +395,89 @@ def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode, S):
         tr.close()
     assert grads[0][0] == grads[1][0]
     assert torch.equal(grads[0][1], grads[1][1])
+
+
+# ---------------------------------------------------------------- policies
+def _policy_trainer(budget_frac=0.6, **kw):
+    rng = np.random.default_rng(11)
+    shape = dict(TINY, layers=6, max_pos=256)
+
+    def make(planner, budget, **k):
+        m = ModelConfig(hidden_dropout=0.1, attn_dropout=0.1, seed=77, **shape)
+        t = TrainConfig(planner=planner, batch=32, seq_min=32, seq_max=256, **k)
+        return Trainer(m, t, budget)
+
+    probe = make("none", 8 * GiB)
+    peak = probe.step(*synthetic_batch(rng, 32, 256, TINY["vocab"], 4))["peak_reserved"]
+    probe.close()
+    return make, int(budget_frac * peak), rng
+
+
+def test_tolerant_plan_cache_matches_host(cuda_device):
+    """cache_tolerance 0.02 (reference scheduler.hpp:204-221): near sizes hit
+    a neighbour's plan when its estimated kept bytes still fit; the GPU run's
+    hit / miss and plan sequence equals the host planner replaying the same
+    sizes with the same estimator, reserve and tolerance."""
+    from paper_2209_02478_b200 import planner as host
+    make, budget, rng = _policy_trainer()
+    seqs = [32, 100, 256, 180, 250, 251, 252, 254, 180, 182, 100, 101, 256, 255, 33, 240]
+    hits = {}
+    for tol in (0.0, 0.02):
+        tr = make("mimose", budget, max_sheltered_iters=4, reserve_per_size=0,
+                  cache_tolerance=tol)
+        rows = [tr.step(*synthetic_batch(rng, 32, s, TINY["vocab"], 4)) for s in seqs]
+        assert all(r["peak_reserved"] <= budget for r in rows)
+        planned = [r for r in rows if r["phase_name"] == "planned"]
+        info = tr.info()
+        cfg = host.SchedCfg(budget_bytes=info["budget"], reserve_bytes=info["reserve_bytes"],
+                            cache_tolerance=tol)
+        masks, ins, hit = host.plan_sequence(tr.estimator_text(), tr.model_text(), cfg,
+                                             [r["x"] for r in planned], 2 * 6)
+        assert [r["dropped_mask_lo"] for r in planned] == masks
+        assert [r["insufficient"] for r in planned] == ins
+        assert [r["cache_hit"] for r in planned] == hit
+        hits[tol] = sum(hit)
+        tr.close()
+    assert hits[0.02] > hits[0.0]
+
+
+def test_collect_new_sizes_always(cuda_device):
+    """Every-new-size mode (reference collector.hpp:190-196, harness.hpp:264-276):
+    after the window an unseen size runs a collection step and refits; seen
+    sizes plan. The refit estimator is the host fit of the GPU samples."""
+    from paper_2209_02478_b200 import planner as host
+    make, budget, rng = _policy_trainer()
+    tr = make("mimose", budget, max_sheltered_iters=3, collect_new_sizes_always=True)
+    seqs = [32, 128, 256, 100, 100, 200, 128, 200, 64, 64]
+    rows = [tr.step(*synthetic_batch(rng, 32, s, TINY["vocab"], 4)) for s in seqs]
+    phases = [r["phase_name"] for r in rows]
+    assert phases[:3] == ["collect"] * 3
+    assert phases[3] == "collect" and phases[4] == "planned"      # 100 new, then seen
+    assert phases[5] == "collect" and phases[6] == "planned"      # 200 new; 128 seen
+    assert phases[7] == "planned" and phases[8] == "collect" and phases[9] == "planned"
+    assert all(r["fit_order"] == 2 for r in (rows[5], rows[8]))   # refit on each new size
+    assert all(r["peak_reserved"] <= budget for r in rows)
+    assert host.fit(tr.samples_csv(), order=2) == tr.estimator_text()
+    assert len(tr.samples_csv().strip().splitlines()) == 1 + 12 * 6  # 6 sizes x 12 units
+    tr.close()
+
+
+def test_static_planner_plans_for_the_largest_input(cuda_device):
+    """static-max (reference baselines.hpp:20-23): after the same collection
+    and fit, every step runs the plan generated for S_max - never fewer drops
+    than Mimose's input-aware plan, and never over budget."""
+    make, budget, rng = _policy_trainer(0.55)
+    seqs = [32, 100, 256, 180, 64, 128, 256, 40, 200, 96]
+    runs = {}
+    for planner in ("static-max", "mimose"):
+        tr = make(planner, budget, max_sheltered_iters=4)
+        runs[planner] = [tr.step(*synthetic_batch(np.random.default_rng(5), 32, s,
+                                                  TINY["vocab"], 4)) for s in seqs]
+        assert all(r["peak_reserved"] <= budget for r in runs[planner])
+        tr.close()
+    st = [r for r in runs["static-max"] if r["phase_name"] == "planned"]
+    mi = [r for r in runs["mimose"] if r["phase_name"] == "planned"]
+    assert len({r["dropped_mask_lo"] for r in st}) == 1 and st[0]["plan_size"] > 0
+    for a, b in zip(st, mi):
+        assert a["plan_size"] >= b["plan_size"]
+    assert any(a["plan_size"] > b["plan_size"] for a, b in zip(st, mi))

@@ -17,12 +17,18 @@ def main():
     by_op = collections.Counter()
     hot = []
     seen = set()
+    src = ""
+    by_src = collections.Counter()
     for row in csv.reader(lines[hi + 1:]):
         if len(row) != len(hdr) or row[0] == "Line No":
             continue
         d = dict(zip(hdr, row))
         addr = d.get("Address", "")
-        if not addr or addr in seen:
+        if not addr:
+            # a CUDA source line (the SASS rows that follow belong to it)
+            src = (row[0] + ": " + (row[1] if len(row) > 1 else "")).strip()[:90]
+            continue
+        if addr in seen:
             continue
         seen.add(addr)
         sass = row[3]
@@ -39,7 +45,8 @@ def main():
                 by_reason[r] += int(d[r] or 0)
             except ValueError:
                 pass
-        hot.append((n, addr, sass, {r: d[r] for r in reasons if d[r] not in ("", "0")}))
+        by_src[src] += n
+        hot.append((n, addr, sass, {r: d[r] for r in reasons if d[r] not in ("", "0")}, src))
     tot = sum(by_reason.values()) or 1
     print("samples by stall reason:")
     for r, n in by_reason.most_common():
@@ -48,9 +55,12 @@ def main():
     print("samples by opcode:")
     for o, n in by_op.most_common(top):
         print(f"  {o:12s} {n:8d} {100 * n / tot:5.1f}%")
+    print("hottest source lines:")
+    for s, n in by_src.most_common(top):
+        print(f"  {n:7d} {100 * n / tot:5.1f}%  {s}")
     print("hottest instructions:")
-    for n, a, s, r in sorted(hot, reverse=True)[:top]:
-        print(f"  {n:7d} {a} {s[:60]:60s} {r}")
+    for n, a, s, r, src in sorted(hot, reverse=True)[:top]:
+        print(f"  {n:7d} {a} {s[:60]:60s} {r}  <- {src[:60]}")
 
 
 if __name__ == "__main__":
