@@ -8,8 +8,15 @@ ARCH    := -gencode arch=compute_100a,code=sm_100a
 PKG     := paper_2209_02478_b200
 CSRC    := $(PKG)/csrc
 BUILD   := build
+# mbarrier watchdog (~35 s, traps a pipeline that never completes instead of
+# hanging the GPU): on by default; `make WATCHDOG=0` for a build that waits
+# indefinitely (preempted / time-sliced contexts)
+WATCHDOG ?= 1
 NVFLAGS := $(ARCH) -O3 -std=c++20 -lineinfo -Xcompiler -fPIC -Iinclude -I$(CSRC) \
            --expt-relaxed-constexpr -Xcompiler -Wall
+ifeq ($(WATCHDOG),1)
+NVFLAGS += -DMIMOSE_MBAR_WATCHDOG
+endif
 CXXFLAGS:= -O2 -std=c++20 -fPIC -Wall -Wextra -Iinclude
 
 CU_SRCS := $(wildcard $(CSRC)/*.cu)

@@ -117,14 +117,18 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
   const int tiles = ((S + 127) / 128) * nh * B;
   if (kb == 128) {
     using Cfg = mimose_dev::FlashFwdCfg<128>;
-    static bool configured = false;
-    return launch_flash(mimose_dev::flash_fwd_kernel<128>, Cfg::kSmemBytes, Cfg::kThreads,
-                        std::min(tiles, flash_sm_count()), tq, tk, tv, p, s, configured);
+    static bool configured[2] = {false, false};
+    return launch_flash(with_mask ? mimose_dev::flash_fwd_kernel<128, true>
+                                  : mimose_dev::flash_fwd_kernel<128, false>,
+                        Cfg::kSmemBytes, Cfg::kThreads, std::min(tiles, flash_sm_count()), tq, tk,
+                        tv, p, s, configured[with_mask]);
   }
   using Cfg = mimose_dev::FlashFwdCfg<64>;
-  static bool configured = false;
-  return launch_flash(mimose_dev::flash_fwd_kernel<64>, Cfg::kSmemBytes, Cfg::kThreads,
-                      std::min(tiles, 2 * flash_sm_count()), tq, tk, tv, p, s, configured);
+  static bool configured[2] = {false, false};
+  return launch_flash(with_mask ? mimose_dev::flash_fwd_kernel<64, true>
+                                : mimose_dev::flash_fwd_kernel<64, false>,
+                      Cfg::kSmemBytes, Cfg::kThreads, std::min(tiles, 2 * flash_sm_count()), tq, tk,
+                      tv, p, s, configured[with_mask]);
 }
 
 cudaError_t flash_keep_mask(uint32_t* mask, int S, int ld, int nh, int B,

@@ -131,7 +131,8 @@ __global__ void flash_keep_mask_kernel(uint64_t seed, uint64_t stream, uint32_t 
   }
 }
 
-template <int KB>
+// DROP: dropout on (keep bits read and applied); off = no per-score mask work
+template <int KB, bool DROP>
 __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kMinBlocks)
     flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ,
                      const __grid_constant__ CUtensorMap tmK,
@@ -308,7 +309,6 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     const int w = ew >> 2;         // key slice of every block
     const int r = quarter * 32 + static_cast<int>(lane);
     const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
-    const uint32_t thr_hi = p.drop.threshold << 16;
     const float kNegInf = -__int_as_float(0x7f800000);
     int jb = 0, tc = 0;
     // Tile end, software-pipelined: a tile's four slices are combined after
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         int lim = p.S - c0;  // valid keys of the slice: c0 + e < S (and <= i if causal)
         if (p.causal && i - c0 + 1 < lim) lim = i - c0 + 1;
         if (warp_dead) lim = 0;
-        const uint32_t kw = (thr_hi != 0 && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
+        const uint32_t kw = (DROP && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
         if (trw) FT(tro + 0, FT_CLK());
         mbar_wait(&sfull[sb], (jb >> 1) & 1);
         tc_fence_after();
@@ -444,25 +444,28 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         // this P buffer is free once the P V of two blocks ago has run
         mbar_wait(&pvdone[sb * NSL + w], ((jb >> 1) & 1) ^ 1);
         const float m_eff = m_used == kNegInf ? 0.f : m_used;
-        float ps[4] = {0.f, 0.f, 0.f, 0.f};  // four independent row-sum chains
+        // row sums: two paired (f32x2) accumulators = four independent chains
+        float2 ps2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
         uint32_t pk[16];
         if (all_dead) {
 #pragma unroll
           for (int e = 0; e < 16; ++e) pk[e] = 0u;
         } else {
+          const float2 sc2 = make_float2(p.sc, p.sc), nm2 = make_float2(-m_eff, -m_eff);
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
-            // p = 2^(s * sc - m): one FFMA + ex2 per score
-            float a0 = fl_ex2(fmaf(x[e], p.sc, -m_eff)), a1 = fl_ex2(fmaf(x[e + 1], p.sc, -m_eff));
-            ps[(e >> 1) & 3] += a0 + a1;
-            if (thr_hi != 0) {  // keep bits from flash_keep_mask_kernel
+            // p = 2^(s * sc - m): one paired FFMA2 per two scores, then ex2 each
+            const float2 t = __ffma2_rn(make_float2(x[e], x[e + 1]), sc2, nm2);
+            float a0 = fl_ex2(t.x), a1 = fl_ex2(t.y);
+            ps2[(e >> 1) & 1] = __fadd2_rn(ps2[(e >> 1) & 1], make_float2(a0, a1));
+            if (DROP) {  // keep bits from flash_keep_mask_kernel
               if (!((kw >> e) & 1u)) a0 = 0.f;
               if (!((kw >> (e + 1)) & 1u)) a1 = 0.f;
             }
             pk[e >> 1] = fl_pack(a0, a1);
           }
         }
-        l += (ps[0] + ps[1]) + (ps[2] + ps[3]);
+        l += (ps2[0].x + ps2[0].y) + (ps2[1].x + ps2[1].y);
         if (trw) FT(tro + 2, FT_CLK());
         const uint32_t rowa = smem_u32(sP + sb * Cfg::kPBytes + (w >> 1) * 16384) + r * 128;
 #pragma unroll
@@ -546,21 +549,30 @@ __device__ __forceinline__ void flash_bwd_half(const uint32_t (&sraw)[16],
                                                float fkd, float sc, uint32_t* pk_pd,
                                                uint32_t* pk_ds) {
   const float neg_inf = -__int_as_float(0x7f800000);
+  // paired f32x2 math (FFMA2 / FMUL2): two scores per instruction
+  const float2 sc2 = make_float2(sc, sc), nl2 = make_float2(-lse_s, -lse_s);
+  const float2 nd2 = make_float2(-dvec, -dvec);
 #pragma unroll
   for (int e = 0; e < 16; e += 2) {
-    float dS[2], Pd[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int col = e0 + e + u;
-      float x = __uint_as_float(sraw[e + u]);
-      if (!FULL) x = col < lim ? x : neg_inf;
-      const float P = fl_ex2(fmaf(x, sc, -lse_s));
-      const bool keep = !DROP || ((kw >> col) & 1u);
-      dS[u] = P * fmaf(__uint_as_float(dpraw[e + u]), keep ? fk : 0.f, -dvec);
-      if constexpr (WITH_PD) Pd[u] = P * (keep ? fkd : 0.f);
+    float2 x = make_float2(__uint_as_float(sraw[e]), __uint_as_float(sraw[e + 1]));
+    if (!FULL) {
+      if (e0 + e >= lim) x.x = neg_inf;
+      if (e0 + e + 1 >= lim) x.y = neg_inf;
     }
-    if constexpr (WITH_PD) pk_pd[(e0 + e) >> 1] = fl_pack(Pd[0], Pd[1]);
-    pk_ds[(e0 + e) >> 1] = fl_pack(dS[0], dS[1]);
+    const float2 t = __ffma2_rn(x, sc2, nl2);
+    const float2 P = make_float2(fl_ex2(t.x), fl_ex2(t.y));
+    float2 f = make_float2(fk, fk), fd = make_float2(fkd, fkd);
+    if (DROP) {
+      if (!((kw >> (e0 + e)) & 1u)) f.x = fd.x = 0.f;
+      if (!((kw >> (e0 + e + 1)) & 1u)) f.y = fd.y = 0.f;
+    }
+    const float2 dp = make_float2(__uint_as_float(dpraw[e]), __uint_as_float(dpraw[e + 1]));
+    const float2 dS = __fmul2_rn(P, __ffma2_rn(dp, f, nd2));
+    if constexpr (WITH_PD) {
+      const float2 Pd = __fmul2_rn(P, fd);
+      pk_pd[(e0 + e) >> 1] = fl_pack(Pd.x, Pd.y);
+    }
+    pk_ds[(e0 + e) >> 1] = fl_pack(dS.x, dS.y);
   }
 }
 

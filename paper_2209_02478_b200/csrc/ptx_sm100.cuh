@@ -56,15 +56,39 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   return ok != 0;
 }
 
-// Blocking wait with a watchdog: a barrier that never completes (a pipeline
-// bug) traps after ~4 s instead of hanging the GPU.
+// try_wait with a suspend-time hint: a waiting warp sleeps in hardware
+// instead of re-issuing the test, leaving the issue slots to the math warps
+// of the same SM sub-partition
+__device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, P1;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+
+// Blocking wait. With MIMOSE_MBAR_WATCHDOG (debug builds) a barrier that
+// never completes (a pipeline bug) traps after ~2^36 cycles (~35 s) instead
+// of hanging; release builds wait (a preempted or time-sliced context must
+// not be killed by a clock-based trap).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
+#ifdef MIMOSE_MBAR_WATCHDOG
   const long long t0 = clock64();
-  while (!mbar_try_wait(addr, parity)) {
-    if (clock64() - t0 > (8LL << 30)) __trap();
+  while (!mbar_try_wait_sleep(addr, parity)) {
+    if (clock64() - t0 > (1LL << 36)) __trap();
   }
+#else
+  while (!mbar_try_wait_sleep(addr, parity)) {
+  }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA

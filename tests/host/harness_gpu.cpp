@@ -159,6 +159,7 @@ int main(int argc, char** argv) {
   const int order_cfg = t.estimator_order;
   const int window = t.max_sheltered_iters;
   const bool every_new = t.collect_new_sizes_always != 0;
+  const bool half = t.ckpt_unit == 1;
 
   auto refit = [&]() {
     const int order = std::min(order_cfg, static_cast<int>(seen.size()) - 1);
@@ -275,11 +276,23 @@ int main(int argc, char** argv) {
         ck(mimose_alloc(ctx, 2 * T * m.hidden, 3, &out[u]), "alloc out");
         ck(mimose_layer_fwd(tr, u, &io, in, out[u], &sv[u], s), "layer fwd");
       }
+      // half units: a block whose attention AND FFN halves are both dropped
+      // keeps only the FFN half's output (the executor's rule, see
+      // Trainer::replay_peak); h1 is regenerated before the FFN half's recompute
+      if (half && u % 2 == 1 && (collect || (dropped[u] && dropped[u - 1]))) {
+        ck(mimose_free(ctx, out[u - 1]), "free h1");
+        out[u - 1] = nullptr;
+      }
     }
     void* dy = nullptr;
     ck(mimose_head_fwd_bwd(tr, &io, out[U - 1], &dy, s), "head");
     // ---- backward (dropped units recomputed right before their backward)
     for (int u = U - 1; u >= 0; --u) {
+      if (u > 0 && out[u - 1] == nullptr) {  // h1 of a doubly-dropped block
+        ck(mimose_alloc(ctx, 2 * T * m.hidden, 4, &out[u - 1]), "alloc h1");
+        ck(mimose_layer_fwd(tr, u - 1, &io, u == 1 ? h0 : out[u - 2], out[u - 1], &sv[u - 1], s),
+           "recompute attention half");
+      }
       const void* in = u == 0 ? h0 : out[u - 1];
       if (sv[u] == nullptr) ck(mimose_layer_fwd(tr, u, &io, in, out[u], &sv[u], s), "recompute");
       void* dx = nullptr;
