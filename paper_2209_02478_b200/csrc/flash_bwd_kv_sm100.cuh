@@ -260,8 +260,10 @@ __global__ void __launch_bounds__(FlashBwdKvCfg::kThreads, 1)
         uint32_t kw = 0xffffffffu;
         if (DROP) {
           const int qi = q0 + static_cast<int>(lane);
-          const uint32_t row =
-              qi < p.S ? p.mask[((int64_t)z * p.S + qi) * p.mw + (kb * 4 + quarter)] : 0u;
+          const int chunk = kb * 4 + quarter;  // keys 32 chunk .. (past S: padding keys)
+          const uint32_t row = (qi < p.S && chunk < p.mw)
+                                   ? p.mask[((int64_t)z * p.S + qi) * p.mw + chunk]
+                                   : 0u;
           kw = warp_bit_transpose(row, lane);
         }
         // causal: query q0 + i valid iff q0 + i >= key

@@ -66,12 +66,11 @@ struct FlashFwdCfg {
   static constexpr int kKBytes = KB * 64 * 2;
   static constexpr int kKVBytes = 2 * kKBytes;     // K block + V block
   static constexpr int kStages = 3;
-  static constexpr int kPBytes = 128 * KB * 2;     // KB / 64 swizzled 64-key sub-tiles
   static constexpr int kXchBytes = 2 * 2 * kNSL * 128 * 4;  // [tile parity][m|l][slice][row]
   static constexpr int kTmemCols = 4 * KB;         // 2 S buffers (KB) + kNSL O slices (64)
   static constexpr int kOCols = 64 / kNSL;         // output columns per warp in the combine
   static constexpr int kSmemBytes =
-      kQBytes + kStages * kKVBytes + 2 * kPBytes + kXchBytes + 1024 + 512;
+      kQBytes + kStages * kKVBytes + kXchBytes + 1024 + 512;
 };
 
 __device__ __forceinline__ float fl_ex2(float x) {
@@ -145,8 +144,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   uint8_t* sQ = smem;
   uint8_t* sKV = smem + Cfg::kQBytes;
-  uint8_t* sP = sKV + NS * Cfg::kKVBytes;
-  float* xch = reinterpret_cast<float*>(sP + 2 * Cfg::kPBytes);
+  float* xch = reinterpret_cast<float*>(sKV + NS * Cfg::kKVBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + Cfg::kXchBytes);
   uint64_t* empty = full + NS;
   uint64_t* qfull = empty + NS;
@@ -195,7 +193,9 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     mbar_init(qempty, 1);
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sfull[b], 1);
-      mbar_init(&sempty[b], Cfg::kEW);
+      // S buffer b also carries P (bf16, written back over S) until its P V
+      // MMAs have read it: released by their commit
+      mbar_init(&sempty[b], 1);
     }
     for (int i = 0; i < 2 * NSL; ++i) {
       mbar_init(&pfull[i], 4);  // the four lane-quarter warps of a slice
@@ -253,20 +253,24 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         mbar_wait(&pfull[(b & 1) * NSL + w], (b >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t pa =
-              smem_u32(sP + (b & 1) * Cfg::kPBytes + (w >> 1) * 16384) + (w & 1) * 64;
+          // A = P_b[:, slice w] from TMEM (bf16 pairs over the slice's first
+          // 16 columns of S buffer b), B = V rows of the slice (MN-major)
+          const uint32_t pa = tmem_base + (b & 1) * KB + 32 * w;
           const uint32_t va = smem_u32(sKV + stage * Cfg::kKVBytes + Cfg::kKBytes +
                                        (w >> 1) * 8192) + (w & 1) * 4096;
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk)
-            umma_bf16(tmem_base + 2 * KB + 64 * w, smem_desc_sw128(pa + kk * 32, 16, 1024),
-                      smem_desc_sw128(va + kk * 2048, 8192, 1024), idesc_pv,
-                      (j > 0 || kk > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem_base + 2 * KB + 64 * w, pa + 8 * kk,
+                         smem_desc_sw128(va + kk * 2048, 8192, 1024), idesc_pv,
+                         (j > 0 || kk > 0) ? 1u : 0u);
           umma_commit(&pvdone[(b & 1) * NSL + w]);
         }
         __syncwarp();
       }
-      if (lane == 0) umma_commit(&empty[stage]);
+      if (lane == 0) {
+        umma_commit(&sempty[b & 1]);
+        umma_commit(&empty[stage]);
+      }
       if (lane == 0 && b < 256) FT(b * 4 + 2, FT_CLK());
       __syncwarp();
     };
@@ -390,9 +394,6 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         tmem_ld32_nowait(lane_base + sb * KB + 32 * w, raw);
         tmem_wait_ld();
         if (trw) FT(tro + 1, FT_CLK());
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sempty[sb]);
         // warp-uniform paths: every key valid (no per-score test) / none valid
         // (past the sequence end or above the diagonal: P = 0, no Philox)
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
@@ -441,8 +442,6 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
             m_used = mn;
           }
         }
-        // this P buffer is free once the P V of two blocks ago has run
-        mbar_wait(&pvdone[sb * NSL + w], ((jb >> 1) & 1) ^ 1);
         const float m_eff = m_used == kNegInf ? 0.f : m_used;
         // row sums: two paired (f32x2) accumulators = four independent chains
         float2 ps2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -467,12 +466,10 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         }
         l += (ps2[0].x + ps2[0].y) + (ps2[1].x + ps2[1].y);
         if (trw) FT(tro + 2, FT_CLK());
-        const uint32_t rowa = smem_u32(sP + sb * Cfg::kPBytes + (w >> 1) * 16384) + r * 128;
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-          st_shared_v4(rowa + ((((w & 1) * 4 + c) ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1],
-                       pk[4 * c + 2], pk[4 * c + 3]);
-        fence_async_shared();
+        // P (bf16 pairs) back over the first 16 columns of this warp's S slice:
+        // the P V MMA's A operand, read from TMEM
+        tmem_st16u(lane_base + sb * KB + 32 * w, pk);
+        tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pfull[sb * NSL + w]);
@@ -731,7 +728,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                   smem_desc_sw128(k + kK2 + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
       umma_commit(&sfull[sb]);
     };
-    auto issue_acc = [&](int s, bool first) {
+    auto issue_acc = [&](int s, int sb, bool first) {
       if (KV) {
         const uint32_t pd = smem_u32(sPD), ds = smem_u32(sDS);
         const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kStrTile);
@@ -754,6 +751,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                     smem_desc_sw128(k + kk * 2048, 8192, 1024), idesc_acc,
                     (first && kk == 0) ? 0u : 1u);
       }
+      (void)sb;
       umma_commit(pdone);
       umma_commit(&empty[s]);
     };
@@ -787,7 +785,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         if (j > lo) {
           mbar_wait(pfull, (blkc - 1) & 1);
           tc_fence_after();
-          if (lane == 0) issue_acc(prev_s, j - 1 == lo);
+          if (lane == 0) issue_acc(prev_s, (blkc - 1) & 1, j - 1 == lo);
           __syncwarp();
         }
         prev_s = s;
@@ -800,7 +798,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       mbar_wait(pfull, (blkc - 1) & 1);
       tc_fence_after();
       if (lane == 0) {
-        issue_acc(prev_s, hi - 1 == lo);
+        issue_acc(prev_s, (blkc - 1) & 1, hi - 1 == lo);
         umma_commit(accfull);
         if (!KV) umma_commit(fixempty);
       }
