@@ -480,19 +480,23 @@ def run_gpu_arm(args, rank, world, local):
         W + K timed steps; returns (trainer, value, ms, launches, summary, clk)."""
         tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner=args.planner),
                      run_budget - nccl_bytes, local)
-        if dp is not None:
-            tr.attach_dp(dp, bucket_mb)
-        t_cal0 = time.perf_counter()
-        for b in batches(seqs[:calib], args.seed + 7 * rank + 1):
-            tr.step(*b, stream=stream)
-        calib_s = time.perf_counter() - t_cal0
-        torch.cuda.synchronize()
-        clk = None
-        if clocks:
-            with ClockSampler(local) as clk:
+        try:
+            if dp is not None:
+                tr.attach_dp(dp, bucket_mb)
+            t_cal0 = time.perf_counter()
+            for b in batches(seqs[:calib], args.seed + 7 * rank + 1):
+                tr.step(*b, stream=stream)
+            calib_s = time.perf_counter() - t_cal0
+            torch.cuda.synchronize()
+            clk = None
+            if clocks:
+                with ClockSampler(local) as clk:
+                    ms, launches = timed_run(tr, db)
+            else:
                 ms, launches = timed_run(tr, db)
-        else:
-            ms, launches = timed_run(tr, db)
+        except Exception:
+            tr.close()
+            raise
         ms = allmax(ms, world)
         rows = tr.rows[-args.steps:]
         over = [r for r in rows if r["peak_reserved"] > r["budget"]]
@@ -609,9 +613,17 @@ def run_gpu_arm(args, rank, world, local):
     other = {}
     if not args.profile_only:
         ob = "self" if args.budget_basis == "materialised" else "materialised"
-        t2, v2, _, _, s2, _ = mimose_run(int(args.budget_frac * bases[ob]))
-        t2.close()
-        other = {"basis": ob, "value": v2, "no_ckpt_peak_bytes": bases[ob], **s2}
+        ob_budget = int(args.budget_frac * bases[ob])
+        try:
+            t2, v2, _, _, s2, _ = mimose_run(ob_budget)
+            t2.close()
+            other = {"basis": ob, "value": v2, "no_ckpt_peak_bytes": bases[ob], **s2}
+        except _lib.MimoseError as e:
+            # e.g. QA / LM presets: the constant footprint (weights, grads, AdamW
+            # state) alone is >= the fraction of the smaller (flash) peak
+            torch.cuda.synchronize()
+            other = {"basis": ob, "value": None, "no_ckpt_peak_bytes": bases[ob],
+                     "budget_bytes": ob_budget, "infeasible": str(e)[:200]}
 
     # 6. no-checkpoint, unlimited-memory throughput on the same size stream
     nock = None

@@ -197,8 +197,12 @@ class Trainer:
         self.ctx = Context(budget_bytes, device)
         self.lib = self.ctx.lib
         h = C.c_void_p()
-        check(self.lib.mimose_trainer_create(self.ctx.handle, C.byref(model.to_c()),
-                                             C.byref(train.to_c()), C.byref(h)))
+        try:
+            check(self.lib.mimose_trainer_create(self.ctx.handle, C.byref(model.to_c()),
+                                                 C.byref(train.to_c()), C.byref(h)))
+        except Exception:
+            self.ctx.close()  # the arena goes back now, not at garbage collection
+            raise
         self.handle = h
         self._hook = None
         self.rows = []
