@@ -636,7 +636,7 @@ def run_gpu_arm(args, rank, world, local):
         ms_none = allmax(ms_none, world)
         nock = samples / (ms_none / 1000.0)
         base.close()
-    if other and nock:
+    if other and nock and other.get("value"):
         other["frac_of_no_ckpt"] = other["value"] / nock
 
     # 7. CPU baseline (rank 0, N=1 only): bounded sample of the same workload
