@@ -522,8 +522,10 @@ def run_gpu_arm(args, rank, world, local):
     # 2. Mimose under the headline budget
     tr, value, ms_max, launches, summ, clk = mimose_run(budget, clocks=True)
 
-    # 3. roofline: every instrumented launch timed by CUDA events on 2 extra steps
-    extra = batches(seqs[calib + n_total:calib + n_total + 2], args.seed + 99)
+    # 3. roofline: every instrumented launch timed by CUDA events on 4 extra steps
+    #    (their S drawn from the same stream; fewer steps make the family's
+    #    efficiency depend on which lengths happened to be drawn)
+    extra = batches(seqs[calib + n_total:calib + n_total + 4], args.seed + 99)
     extra_db = [DeviceBatch.from_host(t, ty, lb, model_cfg.vocab) for (t, ty, lb) in extra]
     import ctypes as C
     lib.mimose_profile_enable(1)
@@ -692,7 +694,7 @@ def run_gpu_arm(args, rank, world, local):
                          "ms_share_of_step": dms / step_ms_prof if step_ms_prof else None,
                          "launches": dn, "peak_kind": pk_kind + " sustained",
                          "stages": stages, "hbm_peak_gbs": peak_bw,
-                         "profiled": "2 extra planned steps, every launch bracketed by CUDA "
+                         "profiled": "4 extra planned steps, every launch bracketed by CUDA "
                                      "events on its stream; algorithmic flops / bytes per "
                                      "launch (DESIGN.md §2)"},
             "cpu_baseline": cpu,

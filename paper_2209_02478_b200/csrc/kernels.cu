@@ -396,48 +396,57 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
 // column sums of a bf16 matrix [rows][N] (ld) with optional 2-way grouping
 // partial[blockIdx.y][G][N]
 // =====================================================================
+// G = 1: plain column sums (bias gradients); G = 2: split by a per-row group
+// id (token-type gradients). Eight rows of 16-byte loads in flight per
+// thread (issued before any is consumed); fixed summation order.
+template <int G>
 __global__ void __launch_bounds__(256) colsum_partial_kernel(const bf16* __restrict__ x, int rows,
                                                              int N, int64_t ld,
                                                              const int32_t* __restrict__ grp,
-                                                             int G, float* __restrict__ partial) {
-  __shared__ float red[8][2][256];
+                                                             float* __restrict__ partial) {
+  __shared__ float red[8][G][256];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int col = (blockIdx.x * 32 + tx) * 8;
-  float acc[2][8] = {};
+  float acc[G][8] = {};
   if (col < N) {
-    // four rows per iteration, loads issued first (fixed summation order)
     const int step = gridDim.y * 8;
     int r = blockIdx.y * 8 + ty;
-    for (; r + 3 * step < rows; r += 4 * step) {
-      uint4 raw[4];
+    constexpr int kU = 8;
+    for (; r + (kU - 1) * step < rows; r += kU * step) {
+      uint4 raw[kU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < kU; ++u)
         raw[u] = __ldcs(reinterpret_cast<const uint4*>(x + (int64_t)(r + u * step) * ld + col));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < kU; ++u) {
         float v[8];
         unpack8(raw[u], v);
-        const int g = grp != nullptr ? grp[r + u * step] : 0;
+        if constexpr (G == 1) {
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          acc[0][e] += g == 0 ? v[e] : 0.f;
-          acc[1][e] += g == 1 ? v[e] : 0.f;
+          for (int e = 0; e < 8; ++e) acc[0][e] += v[e];
+        } else {
+          const int g = grp[r + u * step];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            acc[0][e] += g == 0 ? v[e] : 0.f;
+            acc[1][e] += g == 1 ? v[e] : 0.f;
+          }
         }
       }
     }
     for (; r < rows; r += step) {
       float v[8];
       load8(x + (int64_t)r * ld + col, v);
-      const int g = grp != nullptr ? grp[r] : 0;
+      const int g = G == 2 ? grp[r] : 0;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        acc[0][e] += g == 0 ? v[e] : 0.f;
-        acc[1][e] += g == 1 ? v[e] : 0.f;
+        acc[0][e] += (G == 1 || g == 0) ? v[e] : 0.f;
+        if constexpr (G == 2) acc[G - 1][e] += g == 1 ? v[e] : 0.f;
       }
     }
   }
 #pragma unroll
-  for (int g = 0; g < 2; ++g)
+  for (int g = 0; g < G; ++g)
 #pragma unroll
     for (int e = 0; e < 8; ++e) red[ty][g][tx * 8 + e] = acc[g][e];
   __syncthreads();
@@ -1200,12 +1209,17 @@ int colsum_row_blocks(int rows) {
 
 cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,
                    float* partial, float* out, cudaStream_t s) {
-  if (N % 8 || ld % 8 || G < 1 || G > 2) return cudaErrorInvalidValue;
+  if (N % 8 || ld % 8 || G < 1 || G > 2 || (G == 2 && groups == nullptr))
+    return cudaErrorInvalidValue;
   const int rb = colsum_row_blocks(rows);
   ProfScope prof("mem_colsum", 0, 2.0 * rows * N, s);
   dim3 grid((N + 255) / 256, rb);
-  mimose_dev::colsum_partial_kernel<<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N, ld,
-                                                         groups, G, partial);
+  if (G == 2 && groups != nullptr)
+    mimose_dev::colsum_partial_kernel<2><<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N,
+                                                              ld, groups, partial);
+  else
+    mimose_dev::colsum_partial_kernel<1><<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N,
+                                                              ld, nullptr, partial);
   count_launch();
   mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, 32), 256, 0, s>>>(
       partial, rb, G * N, G * N, out, nullptr, nullptr);

@@ -22,5 +22,6 @@ run() {  # kernel-regex skip count
   rm -f $OUT/fl_${TAG}_$K.ncu-rep
 }
 run flash_fwd_kernel 1 1
-run flash_bwd_kernel 2 2
+run flash_bwd_kernel 1 1
+run flash_bwd_kvt_kernel 1 1
 run flash_keep_mask_kernel 1 1
