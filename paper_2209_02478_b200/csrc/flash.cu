@@ -202,11 +202,12 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   dov.bs2 = (int64_t)S * ctx_ld;
   MatView cv = dov;
   cv.ptr = ctx;
-  CUtensorMap tq, tk, tv, to, tc, tk64, tv64;
+  CUtensorMap tq, tk, tv, to, tc, tk64, tv64, tq64, to64;
   if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
       !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128) ||
       !make_operand_map(&tc, cv, nh, B, 128) || !make_operand_map(&tk64, k, nh, B, 64) ||
-      !make_operand_map(&tv64, v, nh, B, 64))
+      !make_operand_map(&tv64, v, nh, B, 64) || !make_operand_map(&tq64, q, nh, B, 64) ||
+      !make_operand_map(&to64, dov, nh, B, 64))
     return cudaErrorInvalidValue;
   mimose_dev::FlashParams p{};
   p.S = S; p.nh = nh; p.B = B; p.ld = ld;
@@ -241,13 +242,13 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
     ProfScope prof("attn_flash_bwd_kv", 8.0 * 64 * pairs * nz,
                    nz * (8.0 * S * 64 + 8.0 * S + mbytes + 4.0 * S * 64), s);
     if (bwd_kv_transposed()) {
-      using Cfg = mimose_dev::FlashBwdKvCfg;
+      using Cfg = mimose_dev::FlashBwdKv2Cfg;
       static bool configured[2] = {false, false};
       const bool d = drop.threshold != 0;
       return launch_flash4(d ? mimose_dev::flash_bwd_kvt_kernel<true>
                              : mimose_dev::flash_bwd_kvt_kernel<false>,
-                           Cfg::kSmemBytes, Cfg::kThreads, std::min(items, flash_sm_count()), tq,
-                           tk, tv, to, p, s, configured[d]);
+                           Cfg::kSmemBytes, Cfg::kThreads, std::min(items, flash_sm_count()), tq64,
+                           tk, tv, to64, p, s, configured[d]);
     }
     static bool configured = false;
     return launch_flash5(mimose_dev::flash_bwd_kernel<0, 128>, CfgKV::kSmemBytes,
