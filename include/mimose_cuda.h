@@ -194,9 +194,8 @@ typedef struct {
   int estimator_order;         /* harness.hpp:53 */
   float lr, beta1, beta2, adam_eps, weight_decay, max_grad_norm;
   int attn_fused;              /* 3: flash attention (default; no S x S tensor); 2: fused
-                                  score + softmax kernels, whole key row in TMEM (S <= 512);
-                                  1: block-looped fused score kernels (S <= 2048); 0: QK^T GEMM
-                                  + softmax kernels */
+                                  score + softmax kernels, whole key row in TMEM (S <= 512, else
+                                  as 0); 0: QK^T GEMM + softmax kernels (materialised P / Pd) */
   int reserve_per_size;        /* automatic reserve: 1 = sized for this step's S and verified
                                   against the plan's own replay (simulate_iteration) - short
                                   inputs keep more units; 0 = worst case at seq_max */

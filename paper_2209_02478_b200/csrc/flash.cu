@@ -2,7 +2,6 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include "flash_bwd_kv_sm100.cuh"
 #include "flash_sm100.cuh"
 #include "ops.hpp"
 #include "ops_attn.hpp"
@@ -24,42 +23,6 @@ int flash_sm_count() {
     return v;
   }();
   return n;
-}
-
-// dK / dV kernel: the transposed-score kernel with A operands in TMEM
-// (flash_bwd_kv_sm100.cuh, default) or the staged-tile kernel<0>
-// (MIMOSE_FLASH_BWD_KV=staged)
-bool bwd_kv_transposed() {
-  static const bool v = [] {
-    const char* e = std::getenv("MIMOSE_FLASH_BWD_KV");
-    return e == nullptr || std::string(e) != "staged";
-  }();
-  return v;
-}
-
-template <typename Kern>
-cudaError_t launch_flash4(Kern kern, int smem, int threads, int grid, const CUtensorMap& a,
-                          const CUtensorMap& b, const CUtensorMap& c, const CUtensorMap& d,
-                          const mimose_dev::FlashParams& p, cudaStream_t s, bool& configured) {
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, d, p);
-  if (e != cudaSuccess) return e;
-  count_launch();
-  return cudaGetLastError();
 }
 
 template <typename Kern>
@@ -202,12 +165,11 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
   dov.bs2 = (int64_t)S * ctx_ld;
   MatView cv = dov;
   cv.ptr = ctx;
-  CUtensorMap tq, tk, tv, to, tc, tk64, tv64, tq64, to64;
+  CUtensorMap tq, tk, tv, to, tc, tk64, tv64;
   if (!make_operand_map(&tq, q, nh, B, 128) || !make_operand_map(&tk, k, nh, B, 128) ||
       !make_operand_map(&tv, v, nh, B, 128) || !make_operand_map(&to, dov, nh, B, 128) ||
       !make_operand_map(&tc, cv, nh, B, 128) || !make_operand_map(&tk64, k, nh, B, 64) ||
-      !make_operand_map(&tv64, v, nh, B, 64) || !make_operand_map(&tq64, q, nh, B, 64) ||
-      !make_operand_map(&to64, dov, nh, B, 64))
+      !make_operand_map(&tv64, v, nh, B, 64))
     return cudaErrorInvalidValue;
   mimose_dev::FlashParams p{};
   p.S = S; p.nh = nh; p.B = B; p.ld = ld;
@@ -241,15 +203,6 @@ cudaError_t flash_bwd(const MatView& q, const MatView& k, const MatView& v, cons
     // S, dPd recomputed; dV, dK accumulated: 4 MMAs per (query, key) block pair
     ProfScope prof("attn_flash_bwd_kv", 8.0 * 64 * pairs * nz,
                    nz * (8.0 * S * 64 + 8.0 * S + mbytes + 4.0 * S * 64), s);
-    if (bwd_kv_transposed()) {
-      using Cfg = mimose_dev::FlashBwdKv2Cfg;
-      static bool configured[2] = {false, false};
-      const bool d = drop.threshold != 0;
-      return launch_flash4(d ? mimose_dev::flash_bwd_kvt_kernel<true>
-                             : mimose_dev::flash_bwd_kvt_kernel<false>,
-                           Cfg::kSmemBytes, Cfg::kThreads, std::min(items, flash_sm_count()), tq64,
-                           tk, tv, to64, p, s, configured[d]);
-    }
     static bool configured = false;
     return launch_flash5(mimose_dev::flash_bwd_kernel<0, 128>, CfgKV::kSmemBytes,
                          CfgKV::kThreads, std::min(items, flash_sm_count()), tq, tk, tv, to, to,

@@ -31,18 +31,6 @@ cudaError_t attn_scores_bwd(const MatView& dout, const MatView& v, const void* P
                             int ld, int nh, int B, float ds_scale,
                             const mimose_dev::DropoutCfg& drop, cudaStream_t s);
 
-// Block-looped variants (attn2_sm100.cuh): any S <= 2048, optional causal
-// mask, two 256-column TMEM accumulators double-buffered across key blocks.
-bool attn2_supported(int S);
-cudaError_t attn2_scores_fwd(const MatView& q, const MatView& k, void* P, void* Pd, int S, int ld,
-                             int nh, int B, float alpha, const mimose_dev::DropoutCfg& drop,
-                             bool causal, cudaStream_t s);
-// dS from dO V^T and the saved P; rowsum(dP o P) from dO . ctx, ctx = the
-// forward attention output [B*S][H] (same layout and pitch as dout)
-cudaError_t attn2_scores_bwd(const MatView& dout, const MatView& v, const void* ctx, const void* P,
-                             void* dS, int S, int ld, int nh, int B, float ds_scale,
-                             const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s);
-
 // Flash attention (flash_sm100.cuh, head dim 64): no S x S tensor in HBM.
 // q / k / v: 4-D head views ([B][nh][S][64] over the packed qkv rows);
 // ctx: [B*S][ctx_ld] (head h at columns 64h); lse: [B*nh][S] log2-sum-exp of

@@ -181,6 +181,8 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   F_ = m.ffn;
   L_ = m.layers;
   if (t.ckpt_unit != 0 && t.ckpt_unit != 1) throw std::runtime_error("ckpt_unit must be 0 (block) or 1 (half)");
+  if (t.attn_fused != 0 && t.attn_fused != 2 && t.attn_fused != 3)
+    throw std::runtime_error("attn_fused must be 0 (GEMM + softmax), 2 (fused scores) or 3 (flash)");
   half_ = t.ckpt_unit == 1;
   if (units() > 64) throw std::runtime_error("at most 64 checkpoint units (layers <= 32 with half units)");
   if (H_ % 256 || H_ > 1024 || H_ / nh_ != 64 || F_ % 64 || L_ < 1 || L_ > 64)
@@ -429,9 +431,9 @@ void Trainer::build_params() {
   ck(cudaMemcpy(decay_chunk_, chunk.data(), chunk.size(), cudaMemcpyHostToDevice), "memcpy");
 }
 
-// attn_fused: 0 = QK^T GEMM + softmax kernels; 1 = block-looped fused score
-// kernels (attn2_sm100.cuh: any S <= 2048, causal too); 2 = single-row fused
-// kernels (attn_sm100.cuh: S <= 512, causal too); 3 = flash attention
+// attn_fused: 0 = QK^T GEMM + softmax kernels; 2 = single-row fused kernels
+// (attn_sm100.cuh: S <= 512, causal too; longer rows: the GEMM + softmax
+// pair); 3 = flash attention
 // (flash_sm100.cuh: no S x S tensor at all -- the block saves one fp32
 // log-sum-exp per row and, with dropout, one keep bit per score)
 // Dropped-out attention probabilities Pd are saved by default. With
@@ -452,7 +454,6 @@ bool Trainer::save_pd() const {
 // The forward, the backward and the byte model (block_work_bytes) all ask
 // this one function, so they always agree on the path for a given S.
 int Trainer::fused_attn(int S) const {
-  if (t_.attn_fused == 1 && mimose_ops::attn2_supported(S)) return 1;
   if (t_.attn_fused == 2 && mimose_ops::attn_fused_supported(S)) return 2;
   if (t_.attn_fused == 3 && mimose_ops::flash_supported(S)) return 3;
   return 0;
@@ -567,7 +568,7 @@ int64_t Trainer::block_work_bytes(int S) const {
       take_b(act); if (hid) take_b(act);        // dz1, da
       drop_b(act); drop_b(act); drop_b(st);     // dh1, z1, st1
     }
-    if (fused != 1 && !flash) drop_b(act);      // ctx
+    if (!flash) drop_b(act);                    // ctx
     take_b(act);                                // dctx
     if (hid) drop_b(act);                       // da
     if (flash) {
@@ -581,7 +582,6 @@ int64_t Trainer::block_work_bytes(int S) const {
       take_b(quad);                             // dP
       drop_b(act); drop_b(quad);                // dctx, P
       drop_b(quad); drop_b(qkv3);               // dP, qkv
-      if (fused == 1) drop_b(act);              // ctx
     }
     take_b(act);                                // dx
     if (pre) {
@@ -758,12 +758,7 @@ void* Trainer::attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, 
   void* Pd = m_.attn_dropout > 0.f ? take(quad, save_pd() ? act_tag : kTagTransient) : nullptr;
   const auto pdrop = mimose_ops::make_dropout(m_.attn_dropout, m_.seed, stream_id(g.step, l, kSiteAttnProbs));
   const int fused = fused_attn(S);
-  if (fused == 1) {
-    // fused, block-looped: scores stay in TMEM, softmax + dropout in the epilogue
-    ck(mimose_ops::attn2_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
-                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, m_.causal != 0, s),
-       "attn2_scores_fwd");
-  } else if (fused == 2) {
+  if (fused == 2) {
     // fused, whole key row in TMEM
     ck(mimose_ops::attn_scores_fwd(head_view(qkv, 0, S, 3 * H), head_view(qkv, H, S, 3 * H), Pm,
                                    Pd, S, ld, nh, g.B, 0.125f, pdrop, s, m_.causal != 0),
@@ -859,12 +854,7 @@ void* Trainer::attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaS
   drop(sv.Pd);
   sv.Pd = nullptr;
   void* dP = take(quad, kTagTransient);
-  if (fused == 1) {
-    ck(mimose_ops::attn2_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
-                                    sv.ctx, sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop,
-                                    m_.causal != 0, s),
-       "attn2_scores_bwd");
-  } else if (fused == 2) {
+  if (fused == 2) {
     // fused: dPd stays in TMEM; softmax backward in the epilogue writes dS
     ck(mimose_ops::attn_scores_bwd(head_view(dctx, 0, S, H), head_view(sv.qkv, 2 * H, S, 3 * H),
                                    sv.P, dP, S, ld, nh, g.B, 0.125f, pdrop, s),
@@ -1164,14 +1154,14 @@ void* Trainer::attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void
   void* dap = da ? da : (pre ? dh1 : dz1);
   // output projection: dWo = da^T ctx ; dctx = da Wo
   run_gemm(wgrad_call(dap, sv.ctx, T, (int)H, (int)H, G + P.wo.off), s);
-  // attn_fused 1 / 3 read ctx in attn_bwd (rowsum(dP o P) = dO . ctx)
+  // flash attention reads ctx in attn_bwd (rowsum(dP o P) = dO . ctx)
   const int fused = fused_attn(g.S);
-  if (fused != 1 && fused != 3) drop(sv.ctx);
+  if (fused != 3) drop(sv.ctx);
   void* dctx = take(T * H * 2, kTagTransient);
   run_gemm(dgrad_call(dap, W + P.wo.off, T, (int)H, (int)H, dctx, mimose_ops::kEpiBf16, nullptr), s);
   drop(da);
   void* dqkv = attn_bwd(l, sv, dctx, g, s);
-  if (fused == 1 || fused == 3) drop(sv.ctx);
+  if (fused == 3) drop(sv.ctx);
   // QKV projection: dbqkv, dWqkv = dqkv^T xin
   ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
      "colsum");

@@ -73,13 +73,13 @@ class TrainConfig:
     adam_eps: float = 1e-8
     weight_decay: float = 0.01
     max_grad_norm: float = 1.0
-    # attention: 3 (default) = flash attention, see below; 2 = single-row fused kernels (attn_sm100.cuh: the key
-    # row of a 128-query tile in TMEM, softmax / dropout / softmax-backward in
-    # the epilogue; S <= 512, causal too, else the pair below); 1 =
-    # block-looped fused kernels (attn2_sm100.cuh: any S <= 2048, causal too;
-    # correct but slower than both others today - profiles/README.md);
-    # 0 = QK^T GEMM + softmax kernels; 3 = flash attention (flash_sm100.cuh:
-    # no S x S tensor saved or written -- lse per row + keep bits; any S)
+    # attention kernels: 3 (default) = flash attention (flash_sm100.cuh: no
+    # S x S tensor saved or written -- lse per row + keep bits; any S);
+    # 2 = single-row fused score kernels (attn_sm100.cuh: the key row of a
+    # 128-query tile in TMEM, softmax / dropout / softmax-backward in the
+    # epilogue; S <= 512, causal too, longer rows as 0); 0 = QK^T GEMM +
+    # softmax kernels. 2 and 0 materialise P and dropout(P) like the
+    # reference model (HF BERT / GPT-2, bert12.model).
     attn_fused: int = 3
     # automatic reserve sized for each step's S (extras_bytes(S) + 2 %) instead
     # of seq_max: short inputs then keep more blocks (fewer recomputes)

@@ -53,7 +53,7 @@ def _grads_by_name(tr):
     return {name: g[off:off + n].copy() for name, (off, n) in tr.param_table().items()}
 
 
-@pytest.mark.parametrize("fused", [0, 1, 2, 3])
+@pytest.mark.parametrize("fused", [0, 2, 3])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [16, 45, 96])
 def test_step_parity_vs_cpu_oracle(cuda_device, dropout, S, fused):
@@ -178,7 +178,7 @@ def test_variant_device_inputs_match_host(cuda_device, variant):
     assert torch.equal(out[0][1], out[1][1])
 
 
-@pytest.mark.parametrize("fused", [0, 1, 2, 3])
+@pytest.mark.parametrize("fused", [0, 2, 3])
 def test_checkpointed_grads_bitwise_equal_plain(cuda_device, fused):
     """Recompute is deterministic: dropping any subset of blocks gives the
     exact same gradients (dropout on, so Philox regeneration is exercised)."""
@@ -348,13 +348,13 @@ def test_native_dp_world1_bucketed_allreduce_is_identity(cuda_device):
     assert torch.equal(runs[0][1], runs[1][1])
 
 
-# Block-looped fused attention (attn2_sm100.cuh) walks keys in 256-column
-# blocks: S > 256 exercises the online max / sum across blocks, S > 512 the
-# sequences the single-row kernel cannot hold, causal the masked blocks.
+# Long rows: S > 256 exercises flash attention's online max / sum across key
+# blocks, S > 512 the rows the single-row fused kernel cannot hold (mode 2
+# falls back to the GEMM + softmax pair there), causal the masked blocks.
 LONG = dict(TINY, layers=1, max_pos=640)
 
 
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 2, 3])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("dropout", [0.0, 0.1])
 @pytest.mark.parametrize("S", [300, 520])
@@ -376,7 +376,7 @@ def test_long_sequence_attention_vs_cpu_oracle(cuda_device, S, dropout, causal, 
 
 
 @pytest.mark.parametrize("S", [300, 600])
-@pytest.mark.parametrize("mode", [1, 2, 3])
+@pytest.mark.parametrize("mode", [0, 2, 3])
 @pytest.mark.parametrize("causal", [False, True])
 def test_long_sequence_checkpoint_bitwise(cuda_device, causal, mode, S):
     """Recompute through the block-looped kernels is bit-exact at S > 512."""

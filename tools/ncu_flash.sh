@@ -23,5 +23,4 @@ run() {  # kernel-regex skip count
 }
 run flash_fwd_kernel 1 1
 run flash_bwd_kernel 1 1
-run flash_bwd_kvt_kernel 1 1
 run flash_keep_mask_kernel 1 1

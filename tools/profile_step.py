@@ -51,7 +51,7 @@ def main():
     ap.add_argument("--attn-fused", action="store_true", help="(default) fused score kernels")
     ap.add_argument("--attn-unfused", action="store_true", help="GEMM + softmax kernel pair")
     ap.add_argument("--attn-mode", type=int, default=3,
-                    help="TrainConfig.attn_fused when fused: 3 flash, 2 single-row, 1 block-looped")
+                    help="TrainConfig.attn_fused when fused: 3 flash, 2 single-row fused scores")
     ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
     args = ap.parse_args()
     import numpy as np
