@@ -93,6 +93,9 @@ def parse():
                          "dtr (reactive eviction on the real arena, baselines.hpp:62-159)")
     ap.add_argument("--cache-tol", type=float, default=0.0,
                     help="plan-cache tolerance (reference scheduler.hpp:27, 204-221)")
+    ap.add_argument("--ffn-regen-g", type=int, default=0, choices=[0, 1],
+                    help="Mimose runs: kept FFN halves save u only and regenerate GELU(u) in the "
+                         "backward (the no-checkpoint baseline always saves both)")
     ap.add_argument("--ckpt-unit", type=int, default=1, choices=[0, 1],
                     help="checkpoint unit: 1 = block half (attention / FFN, default), 0 = block")
     ap.add_argument("--profile-only", action="store_true",
@@ -478,7 +481,8 @@ def run_gpu_arm(args, rank, world, local):
     def mimose_run(run_budget, clocks=False):
         """Mimose trainer under run_budget: sheltered calibration window, then
         W + K timed steps; returns (trainer, value, ms, launches, summary, clk)."""
-        tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner=args.planner),
+        tr = Trainer(model_cfg, dataclasses.replace(train_cfg, planner=args.planner,
+                                                    ffn_regen_g=args.ffn_regen_g),
                      run_budget - nccl_bytes, local)
         try:
             if dp is not None:
@@ -712,6 +716,7 @@ def run_gpu_arm(args, rank, world, local):
             "gpu_launches": int(launches),
             "clocks": clk.summary() if clk else None,
             "mimose": {"planner": args.planner, "cache_tolerance": args.cache_tol,
+                       "ffn_regen_g": args.ffn_regen_g,
                        "no_ckpt_samples_per_s": nock,
                        "frac_of_no_ckpt": (value / nock) if nock else None,
                        "basis": args.budget_basis, **summ},

@@ -202,6 +202,10 @@ typedef struct {
   int ckpt_unit;               /* checkpoint unit the planner schedules: 0 = transformer block
                                   (the reference's layer granularity), 1 = block half (attention
                                   half, FFN half: 2 x layers units, finer-grained drops) */
+  int ffn_regen_g;             /* 1: a kept FFN half saves the pre-activation u only and its
+                                  backward regenerates g = GELU(u) (bit-identical) for the W2
+                                  gradient: 8 H fewer bytes per token per kept block for one
+                                  elementwise pass; 0: u and g both saved */
 } mimose_train_cfg;
 
 enum {

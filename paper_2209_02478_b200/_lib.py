@@ -91,6 +91,7 @@ class TrainCfg(C.Structure):
         ("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("adam_eps", C.c_float),
         ("weight_decay", C.c_float), ("max_grad_norm", C.c_float),
         ("attn_fused", C.c_int), ("reserve_per_size", C.c_int), ("ckpt_unit", C.c_int),
+        ("ffn_regen_g", C.c_int),
     ]
 
 

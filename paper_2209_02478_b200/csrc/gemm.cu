@@ -404,6 +404,41 @@ int64_t splitk_workspace_bytes(int M, int N, int K) {
   return s > 1 ? (int64_t)s * M * N * 4 : 0;
 }
 
+// g = GELU(u) over bf16 elements, with the GEMM epilogue's own device
+// functions (gemm_sm100.cuh gelu_fast / gelu_tanh_f on the bf16 value): the
+// regenerated g is bit-identical to the one the bias+GELU epilogue produced.
+__global__ void gelu_regen_kernel(const __nv_bfloat16* __restrict__ u, __nv_bfloat16* __restrict__ g,
+                                  int64_t n8, int tanh_form) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(u) + i);
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw);
+    uint4 out;
+    uint32_t* o = reinterpret_cast<uint32_t*>(&out);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float a = __uint_as_float(w[q] << 16), b = __uint_as_float(w[q] & 0xFFFF0000u);
+      o[q] = tanh_form ? mimose_dev::pack_bf16x2(mimose_dev::gelu_tanh_f(a), mimose_dev::gelu_tanh_f(b))
+                       : mimose_dev::pack_bf16x2(mimose_dev::gelu_fast(a), mimose_dev::gelu_fast(b));
+    }
+    reinterpret_cast<uint4*>(g)[i] = out;
+  }
+}
+
+cudaError_t gelu_regen(const void* u, void* g, int64_t n, bool tanh_form, cudaStream_t s) {
+  if (n % 8) return cudaErrorInvalidValue;
+  ProfScope prof("mem_gelu_regen", 0, 4.0 * n, s);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t n8 = n / 8;
+  const int blocks = (int)std::min<int64_t>((n8 + 255) / 256, 8LL * sms);
+  gelu_regen_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(u),
+                                           static_cast<__nv_bfloat16*>(g), n8, tanh_form ? 1 : 0);
+  count_launch();
+  return cudaGetLastError();
+}
+
 uint64_t launch_count() { return g_launches.load(); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 

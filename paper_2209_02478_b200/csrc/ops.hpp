@@ -65,6 +65,10 @@ std::string gemm_profile_csv();
 
 // Number of kernels launched by this module since process start (telemetry
 // for the bench's gpu_launches count).
+// g = GELU(u) elementwise, bit-identical to the bias+GELU epilogue's g
+// (trainer: FFN halves that save u only regenerate g for the dW2 GEMM)
+cudaError_t gelu_regen(const void* u, void* g, int64_t n, bool tanh_form, cudaStream_t s);
+
 uint64_t launch_count();
 void count_launch();
 

@@ -542,10 +542,15 @@ int64_t Trainer::block_work_bytes(int S) const {
   int64_t live = 0, peak = 0;
   auto take_b = [&](int64_t n) { live += n; peak = std::max(peak, live); };
   auto drop_b = [&](int64_t n) { live -= n; };
+  const bool regen = t_.ffn_regen_g != 0;
+  auto g_use = [&] {  // the W2 gradient's g: saved, or regenerated then freed
+    if (regen) take_b(fact);
+    drop_b(fact);
+  };
   auto ffn = [&] {  // ffn_half_bwd: dy live -> dh1 (+ da) live
     if (pre) {
       if (hid) take_b(act);                     // df
-      drop_b(fact); take_b(fact);               // g -> du
+      g_use(); take_b(fact);                    // g -> du
       if (hid) drop_b(act);                     // df
       drop_b(fact);                             // u
       take_b(act); drop_b(act);                 // dh1, x2
@@ -556,7 +561,7 @@ int64_t Trainer::block_work_bytes(int S) const {
     } else {
       take_b(act); if (hid) take_b(act);        // dres (dz2), df
       drop_b(act); drop_b(act); drop_b(st);     // dy, z2, st2
-      drop_b(fact); take_b(fact);               // g -> du
+      g_use(); take_b(fact);                    // g -> du
       if (hid) drop_b(act);                     // df
       drop_b(fact);                             // u
       take_b(act);                              // dh1
@@ -655,7 +660,7 @@ void Trainer::build_spec() {
   // prior a(x) per token: attention half qkv + ctx + z1 + st1 + output h1;
   // FFN half u + g + z2 + st2 + output y
   const double attn_lin = static_cast<double>(12 * H + 8) + lin_extra;
-  const double ffn_lin = static_cast<double>(4 * F + 4 * H + 8);
+  const double ffn_lin = static_cast<double>((t_.ffn_regen_g ? 2 : 4) * F + 4 * H + 8);
   for (int u = 0; u < units(); ++u) {
     const bool attn_part = !half_ || u % 2 == 0;
     const bool ffn_part = !half_ || u % 2 == 1;
@@ -981,8 +986,9 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
     fin = x2;
   }
+  const bool regen = t_.ffn_regen_g != 0;
   void* u = take(T * F * 2, act_tag);
-  void* gg = take(T * F * 2, act_tag);
+  void* gg = take(T * F * 2, regen ? kTagTransient : act_tag);
   {
     GemmCall c = linear_call(fin, W + P.w1.off, T, (int)F, (int)H, u, mimose_ops::kEpiBiasGelu,
                              p32_ + P.b1.off);
@@ -1002,7 +1008,7 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
     c.drop = ffn_out_drop;
     run_gemm(c, s);
   }
-  if (!keep) drop(gg);
+  if (!keep || regen) drop(gg);
   if (!pre) {
     st2 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
@@ -1086,6 +1092,10 @@ void* Trainer::ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void**
   }
   void* dfp = df ? df : (pre ? dy : dres);
   // FFN2: dW2 = df^T g ; du = (df W2) * gelu'(u)
+  if (sv.g == nullptr) {  // u-only save: regenerate g (bit-identical to the forward's)
+    sv.g = take(T * F * 2, kTagTransient);
+    ck(mimose_ops::gelu_regen(sv.u, sv.g, T * F, m_.gelu_tanh != 0, s), "gelu_regen");
+  }
   run_gemm(wgrad_call(dfp, sv.g, T, (int)H, (int)F, G + P.w2.off), s);
   drop(sv.g);
   void* du = take(T * F * 2, kTagTransient);

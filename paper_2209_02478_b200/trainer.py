@@ -89,6 +89,10 @@ class TrainConfig:
     # half, 2 x layers units): an FFN half frees ~60 % of a block's bytes for
     # ~45 % of its forward time, so tight budgets recompute less
     ckpt_unit: int = 1
+    # kept FFN halves save u only; the backward regenerates g = GELU(u)
+    # (bit-identical) for the W2 gradient: 8 H fewer saved bytes per token and
+    # block for one elementwise pass
+    ffn_regen_g: int = 0
 
     def to_c(self):
         c = _lib.TrainCfg()

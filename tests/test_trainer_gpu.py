@@ -198,6 +198,27 @@ def test_checkpointed_grads_bitwise_equal_plain(cuda_device, fused):
         assert torch.equal(g, grads[0][1])
 
 
+@pytest.mark.parametrize("variant", ["bert-qa", "gpt2-lm"])
+def test_ffn_regen_g_bitwise_equal_saved_g(cuda_device, variant):
+    """u-only FFN saves (g regenerated for the W2 gradient) give the saved-g
+    run's loss and gradients bit for bit, with and without dropped units."""
+    shape = VARIANTS[variant]
+    out = []
+    for regen, forced in ((0, []), (1, []), (1, [1, 2]), (1, [0, 1, 2, 3])):
+        m = ModelConfig(hidden_dropout=0.1, attn_dropout=0.1, seed=77, **shape)
+        t = TrainConfig(planner="none", batch=8, seq_min=16, seq_max=96, ffn_regen_g=regen)
+        tr = Trainer(m, t, 4 * GiB)
+        tr.force_plan(forced)
+        rep = tr.step(*synthetic_task_batch(np.random.default_rng(41), tr.model, 8, 48),
+                      optimizer=False)
+        torch.cuda.synchronize()
+        out.append((rep["loss"], tr.grads().clone()))
+        tr.close()
+    for loss, g in out[1:]:
+        assert loss == out[0][0]
+        assert torch.equal(g, out[0][1])
+
+
 def test_repeated_steps_train_and_are_deterministic(cuda_device):
     rng = np.random.default_rng(3)
     batches = [synthetic_batch(rng, 8, s, TINY["vocab"], 4) for s in (32, 24, 32, 40)]
