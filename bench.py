@@ -615,9 +615,12 @@ def run_gpu_arm(args, rank, world, local):
     host_ms = [r["host_ms"] for r in tr.rows[-args.steps:]]
     tr.close()
 
-    # 5. the other budget basis, same size stream (the claim on both bases)
+    # 5. the other budget basis, same size stream (the claim on both bases).
+    #    N = 1 only: an infeasible budget fails on each rank at a step that
+    #    depends on its own lengths, and a rank leaving the collectives early
+    #    would hang the others.
     other = {}
-    if not args.profile_only:
+    if not args.profile_only and world == 1:
         ob = "self" if args.budget_basis == "materialised" else "materialised"
         ob_budget = int(args.budget_frac * bases[ob])
         try:

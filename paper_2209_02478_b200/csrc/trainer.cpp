@@ -904,12 +904,13 @@ void* Trainer::attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaS
 }
 
 // ------------------------------------------------------------ block halves
-// Each transformer block is two halves; the residual add (with its branch
-// dropout) is the epilogue of the projection GEMM that ends each half.
+// Each transformer block is two halves.
 //   BERT (post-LN)   attention  z1 = h + drop(attn(h) Wo + bo), h1 = LN1(z1)
 //                    FFN        z2 = h1 + drop(gelu(h1 W1 + b1) W2 + b2), y = LN2(z2)
+//                    (residual + dropout + LN in one row pass after each GEMM)
 //   GPT-2 (pre-LN)   attention  x1 = LN1(h), h1 = h + drop(attn(x1) Wo + bo)
 //                    FFN        x2 = LN2(h1), y = h1 + drop(gelu(x2 W1 + b1) W2 + b2)
+//                    (residual + dropout in the epilogue of the GEMM ending each half)
 // Saved sets: attention {qkv, lse (+ keep bits) | P (+ Pd), ctx, z1|x1, st1},
 // FFN {z2|x2, st2, u, g}.
 void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, const StepGeo& g,
@@ -937,24 +938,32 @@ void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, cons
   }
   void* ctx = attn_fwd(l, ain, save, g, s);
   if (pre && !keep) drop(x1);
-  // output projection; residual + branch dropout in the epilogue
-  void* z1 = pre ? h1 : take(T * H * 2, act_tag);
-  {
-    GemmCall c = linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, z1, mimose_ops::kEpiBf16,
+  void* z1 = nullptr;
+  if (pre) {
+    // output projection with the residual + branch dropout in the epilogue
+    GemmCall c = linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, h1, mimose_ops::kEpiBf16,
                              p32_ + P.bo.off);
     c.aux = h;
     c.drop = attn_out_drop;
     run_gemm(c, s);
-  }
-  if (!keep) drop(ctx);
-  if (!pre) {
+    if (!keep) drop(ctx);
+  } else {
+    // post-LN: the projection stays a light-epilogue GEMM; residual, branch
+    // dropout and LN1 in one row pass (Philox in the GEMM epilogue measured
+    // slower: the K = H projection is epilogue-bound, 29 -> 43 us at S = 288)
+    void* a = take(T * H * 2, kTagTransient);
+    run_gemm(linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, a, mimose_ops::kEpiBf16,
+                         p32_ + P.bo.off),
+             s);
+    if (!keep) drop(ctx);
+    z1 = keep ? take(T * H * 2, act_tag) : nullptr;
     st1 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.br = z1;
+    la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
     la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
-    la.stats = st1; la.y = h1;
+    la.z = z1; la.stats = st1; la.y = h1;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    if (!keep) drop(z1);
+    drop(a);
   }
   if (keep) {
     save->ctx = ctx;
@@ -1000,23 +1009,29 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
     drop(u);
     if (pre) drop(x2);
   }
-  void* z2 = pre ? y : take(T * H * 2, act_tag);
-  {
-    GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, z2, mimose_ops::kEpiBf16,
+  void* z2 = nullptr;
+  if (pre) {
+    // y = h1 + dropout(g W2^T + b2): residual + dropout in the GEMM epilogue
+    GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, y, mimose_ops::kEpiBf16,
                              p32_ + P.b2.off);
     c.aux = h1;
     c.drop = ffn_out_drop;
     run_gemm(c, s);
-  }
-  if (!keep || regen) drop(gg);
-  if (!pre) {
+    if (!keep || regen) drop(gg);
+  } else {
+    void* f = take(T * H * 2, kTagTransient);
+    run_gemm(linear_call(gg, W + P.w2.off, T, (int)H, (int)F, f, mimose_ops::kEpiBf16,
+                         p32_ + P.b2.off),
+             s);
+    if (!keep || regen) drop(gg);
+    z2 = keep ? take(T * H * 2, act_tag) : nullptr;
     st2 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
-    la.rows = (int)T; la.br = z2;
+    la.rows = (int)T; la.res = h1; la.br = f; la.br_drop = ffn_out_drop;
     la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
-    la.stats = st2; la.y = y;
+    la.z = z2; la.stats = st2; la.y = y;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
-    if (!keep) drop(z2);
+    drop(f);
   }
   if (keep) {
     save->z2 = pre ? x2 : z2;
