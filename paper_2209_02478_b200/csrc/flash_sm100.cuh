@@ -6,9 +6,11 @@
 //
 // Forward, one CTA per 128-query tile (persistent):
 //   warp 0   TMA producer: Q tile once, then K_j / V_j (128 keys) per block
-//   warp 1   MMA issuer:   S_j = Q K_j^T into one of two 128-column TMEM
-//            buffers; O_w += P_j[:, slice w] V_j[slice w] for the four 32-key
-//            slices, each into its own 64-column TMEM accumulator
+//   warp 1   MMA issuer:   S_j = Q K_j^T into the TMEM S buffer, issued as
+//            soon as the softmax warps have loaded S_{j-1} into registers;
+//            O_w += P_j[:, slice w] V_j[slice w] for the 32-key slices, each
+//            into its own 64-column TMEM accumulator, P_j read from one of two
+//            TMEM P buffers (so the next S never waits for a P V to finish)
 //   warps 2+ 16 softmax warps: warp (lane quarter q, key slice w) owns rows
 //            32q..32q+31 x keys 32w..32w+31 of every block and keeps its own
 //            running max / sum for them -- no cross-warp exchange per block.
@@ -67,7 +69,7 @@ struct FlashFwdCfg {
   static constexpr int kKVBytes = 2 * kKBytes;     // K block + V block
   static constexpr int kStages = 3;
   static constexpr int kXchBytes = 2 * 2 * kNSL * 128 * 4;  // [tile parity][m|l][slice][row]
-  static constexpr int kTmemCols = 4 * KB;         // 2 S buffers (KB) + kNSL O slices (64)
+  static constexpr int kTmemCols = 4 * KB;         // S (KB) + 2 P buffers (KB / 2) + kNSL O slices (64)
   static constexpr int kOCols = 64 / kNSL;         // output columns per warp in the combine
   static constexpr int kSmemBytes =
       kQBytes + kStages * kKVBytes + kXchBytes + 1024 + 512;
@@ -149,11 +151,15 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
   uint64_t* empty = full + NS;
   uint64_t* qfull = empty + NS;
   uint64_t* qempty = qfull + 1;
-  uint64_t* sfull = qempty + 1;   // [2] S buffers
-  uint64_t* sempty = sfull + 2;   // [2]
-  uint64_t* pfull = sempty + 2;         // [2 P buffers][NSL slices]
-  uint64_t* pvdone = pfull + 2 * NSL;   // [2][NSL]
-  uint64_t* ofull = pvdone + 2 * NSL;
+  // TMEM: one S buffer [0, KB) released as soon as the softmax warps have
+  // loaded it (so S_{j+1} runs while they compute block j), two P buffers
+  // [KB, 2 KB) (bf16 pairs, KB / 2 columns each) released by the P V commit,
+  // the NSL per-slice O accumulators [2 KB, 2 KB + 64 NSL)
+  uint64_t* sfull = qempty + 1;   // S landed
+  uint64_t* sfree = sfull + 1;    // S loaded by every softmax warp
+  uint64_t* pfull = sfree + 1;    // [2 P buffers][NSL slices]
+  uint64_t* pempty = pfull + 2 * NSL;  // [2] P buffer read by its P V MMAs
+  uint64_t* ofull = pempty + 2;
   uint64_t* oempty = ofull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(oempty + 1);
 
@@ -191,16 +197,10 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     }
     mbar_init(qfull, 1);
     mbar_init(qempty, 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&sfull[b], 1);
-      // S buffer b also carries P (bf16, written back over S) until its P V
-      // MMAs have read it: released by their commit
-      mbar_init(&sempty[b], 1);
-    }
-    for (int i = 0; i < 2 * NSL; ++i) {
-      mbar_init(&pfull[i], 4);  // the four lane-quarter warps of a slice
-      mbar_init(&pvdone[i], 1);
-    }
+    mbar_init(sfull, 1);
+    mbar_init(sfree, Cfg::kEW);
+    for (int i = 0; i < 2 * NSL; ++i) mbar_init(&pfull[i], 4);  // the slice's four lane-quarter warps
+    for (int b = 0; b < 2; ++b) mbar_init(&pempty[b], 1);
     mbar_init(ofull, 1);
     mbar_init(oempty, Cfg::kEW);
     fence_barrier_init();
@@ -253,9 +253,9 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         mbar_wait(&pfull[(b & 1) * NSL + w], (b >> 1) & 1);
         tc_fence_after();
         if (lane == 0) {
-          // A = P_b[:, slice w] from TMEM (bf16 pairs over the slice's first
-          // 16 columns of S buffer b), B = V rows of the slice (MN-major)
-          const uint32_t pa = tmem_base + (b & 1) * KB + 32 * w;
+          // A = P_b[:, slice w] from TMEM (bf16 pairs, 16 columns of P
+          // buffer b & 1), B = V rows of the slice (MN-major)
+          const uint32_t pa = tmem_base + KB + (b & 1) * (KB / 2) + 16 * w;
           const uint32_t va = smem_u32(sKV + stage * Cfg::kKVBytes + Cfg::kKBytes +
                                        (w >> 1) * 8192) + (w & 1) * 4096;
 #pragma unroll
@@ -263,12 +263,11 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
             umma_bf16_ts(tmem_base + 2 * KB + 64 * w, pa + 8 * kk,
                          smem_desc_sw128(va + kk * 2048, 8192, 1024), idesc_pv,
                          (j > 0 || kk > 0) ? 1u : 0u);
-          umma_commit(&pvdone[(b & 1) * NSL + w]);
         }
         __syncwarp();
       }
       if (lane == 0) {
-        umma_commit(&sempty[b & 1]);
+        umma_commit(&pempty[b & 1]);
         umma_commit(&empty[stage]);
       }
       if (lane == 0 && b < 256) FT(b * 4 + 2, FT_CLK());
@@ -284,16 +283,16 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
       for (int j = 0; j < nkb; ++j, ++kv, ++jb) {
         const int s = kv % NS;
         mbar_wait(&full[s], (kv / NS) & 1);
-        mbar_wait(&sempty[jb & 1], ((jb >> 1) & 1) ^ 1);
+        mbar_wait(sfree, (jb & 1) ^ 1);  // S_{jb-1} loaded by the softmax warps
         tc_fence_after();
         if (lane == 0 && jb < 256) FT(jb * 4 + 0, FT_CLK());
         if (lane == 0) {
           const uint32_t qa = smem_u32(sQ), ka = smem_u32(sKV + s * Cfg::kKVBytes);
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tmem_base + (jb & 1) * KB, smem_desc_sw128(qa + kk * 32, 16, 1024),
+            umma_bf16(tmem_base, smem_desc_sw128(qa + kk * 32, 16, 1024),
                       smem_desc_sw128(ka + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
-          umma_commit(&sfull[jb & 1]);
+          umma_commit(sfull);
           if (j == nkb - 1) umma_commit(qempty);
         }
         __syncwarp();
@@ -388,11 +387,15 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         if (warp_dead) lim = 0;
         const uint32_t kw = (DROP && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
         if (trw) FT(tro + 0, FT_CLK());
-        mbar_wait(&sfull[sb], (jb >> 1) & 1);
+        mbar_wait(sfull, jb & 1);
         tc_fence_after();
         uint32_t raw[32];
-        tmem_ld32_nowait(lane_base + sb * KB + 32 * w, raw);
+        tmem_ld32_nowait(lane_base + 32 * w, raw);
         tmem_wait_ld();
+        // S is in registers: the buffer is free for the next block's Q K^T
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(sfree);
         if (trw) FT(tro + 1, FT_CLK());
         // warp-uniform paths: every key valid (no per-score test) / none valid
         // (past the sequence end or above the diagonal: P = 0, no Philox)
@@ -426,7 +429,7 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
             const float alpha = mn == kNegInf ? 1.f : fl_ex2(m_used - mn);
             // O_w holds P V of the blocks so far: wait for the last one to land
             const int pb = jb - 1;
-            mbar_wait(&pvdone[(pb & 1) * NSL + w], (pb >> 1) & 1);
+            mbar_wait(&pempty[pb & 1], (pb >> 1) & 1);
             tc_fence_after();
 #pragma unroll 1
             for (int part = 0; part < 4; ++part) {
@@ -466,9 +469,12 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         }
         l += (ps2[0].x + ps2[0].y) + (ps2[1].x + ps2[1].y);
         if (trw) FT(tro + 2, FT_CLK());
-        // P (bf16 pairs) back over the first 16 columns of this warp's S slice:
-        // the P V MMA's A operand, read from TMEM
-        tmem_st16u(lane_base + sb * KB + 32 * w, pk);
+        // P (bf16 pairs) into P buffer sb, this warp's 16 columns: the P V
+        // MMA's A operand, read from TMEM. The buffer's previous block (jb - 2)
+        // must have been read by its P V MMAs.
+        mbar_wait(&pempty[sb], ((jb >> 1) & 1) ^ 1);
+        tc_fence_after();
+        tmem_st16u(lane_base + KB + sb * (KB / 2) + 16 * w, pk);
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();

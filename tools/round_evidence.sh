@@ -5,7 +5,7 @@ set -u
 TAG=${1:-r2}
 O=gpurun_out/ev_$TAG
 mkdir -p $O
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" > $O/status.txt
+if [ "${SKIP_PYTEST:-0}" != 1 ]; then timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" > $O/status.txt; fi
 timeout 900 python bench.py --steps 20 --warmup 5 > $O/bench_n1.json 2> $O/bench_n1.err; echo "bench rc=$?" >> $O/status.txt
 timeout 900 python bench.py --steps 100 --warmup 5 --no-cpu > $O/bench_n1_100steps.json 2>> $O/bench_n1.err; echo "bench100 rc=$?" >> $O/status.txt
 timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_reference_arm.json 2>> $O/bench_n1.err; echo "ref rc=$?" >> $O/status.txt
