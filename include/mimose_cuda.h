@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 5
+#define MIMOSE_ABI_VERSION 6
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
@@ -333,10 +333,28 @@ int mimose_embed_fwd(mimose_trainer* tr, const mimose_layer_io* io, void** h0,
                      mimose_saved** saved, void* stream);
 /* Unit forward x_in -> x_out ([batch*seq][hidden] bf16, caller's arena block).
  * saved == NULL: no-save forward (the unit is dropped: only x_out stays);
- * else *saved receives the unit's saved set. Recompute = the same call with
- * saved != NULL (same kernels, same Philox streams: bit-identical). */
+ * else *saved receives the unit's saved set. Either way the unit's checkpoint
+ * boundary is x_out plus (post-LN models) the output LayerNorm's statistics,
+ * 8 B per token, which the trainer holds until the unit's backward (its LN
+ * backward reads x-hat from the output). x_out must stay allocated until
+ * mimose_layer_bwd of the unit. */
 int mimose_layer_fwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,
                      void* x_out, mimose_saved** saved, void* stream);
+/* Recompute of a dropped unit before its backward (reference: the
+ * checkpointed layer's second forward, simulator.hpp:142-155): x_out is the
+ * output this step's mimose_layer_fwd wrote (still held); only what the
+ * backward reads is regenerated - same kernels and Philox streams, so the
+ * saved set is bit-identical to a saving forward's - and the output
+ * projection + LayerNorm that produced x_out are not rerun. *saved receives
+ * the saved set. Fails when the unit's boundary is not held (e.g. a
+ * both-halves-dropped block's attention half whose output was released: run
+ * mimose_layer_fwd with saved != NULL for it instead). */
+int mimose_layer_recompute(mimose_trainer* tr, int unit, const mimose_layer_io* io,
+                           const void* x_in, void* x_out, mimose_saved** saved, void* stream);
+/* Gives up a unit's boundary before its backward (the caller is about to free
+ * x_out, e.g. the attention half of a block whose two halves are dropped):
+ * releases the output statistics the trainer holds for it. */
+int mimose_layer_release(mimose_trainer* tr, int unit);
 /* Unit backward: consumes dy (arena block, grad of x_out) and saved; *dx =
  * grad of x_in (arena block). Units are differentiated last to first. */
 int mimose_layer_bwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,

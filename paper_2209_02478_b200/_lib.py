@@ -201,6 +201,9 @@ CUDA_SYMBOLS = [
     ("mimose_trainer_units", C.c_int, [_P, C.POINTER(C.c_int)]),
     ("mimose_embed_fwd", C.c_int, [_P, C.POINTER(LayerIO), C.POINTER(_P), C.POINTER(_P), _P]),
     ("mimose_layer_fwd", C.c_int, [_P, C.c_int, C.POINTER(LayerIO), _P, _P, C.POINTER(_P), _P]),
+    ("mimose_layer_recompute", C.c_int,
+     [_P, C.c_int, C.POINTER(LayerIO), _P, _P, C.POINTER(_P), _P]),
+    ("mimose_layer_release", C.c_int, [_P, C.c_int]),
     ("mimose_layer_bwd", C.c_int,
      [_P, C.c_int, C.POINTER(LayerIO), _P, _P, _P, C.POINTER(_P), _P]),
     ("mimose_head_fwd_bwd", C.c_int, [_P, C.POINTER(LayerIO), _P, C.POINTER(_P), _P]),
@@ -226,7 +229,7 @@ CUDA_SYMBOLS = [
       C.POINTER(C.c_int)]),
 ]
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 
 def _bind(lib, symbols):

@@ -235,6 +235,22 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     *reinterpret_cast<float4*>(gam) = g4[0];
     *reinterpret_cast<float4*>(gam + 4) = g4[1];
   }
+  // output-based x-hat (a.beta set: the row holds y = x-hat * gamma + beta):
+  // x-hat = y * (1 / gamma) - beta / gamma; a zero gamma column has no x-hat
+  // (its gradient terms vanish with gamma; its gamma gradient reads 0)
+  const bool from_y = a.beta != nullptr;
+  float xa[8], xb[8];
+  if (from_y) {
+    float bet[8];
+    const float4* b4 = reinterpret_cast<const float4*>(a.beta + col);
+    *reinterpret_cast<float4*>(bet) = b4[0];
+    *reinterpret_cast<float4*>(bet + 4) = b4[1];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      xa[e] = gam[e] != 0.f ? 1.f / gam[e] : 0.f;
+      xb[e] = -bet[e] * xa[e];
+    }
+  }
   float acc_g[8], acc_b[8], acc_d[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc_g[e] = acc_b[e] = acc_d[e] = 0.f;
@@ -271,9 +287,16 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     }
     float s1 = 0.f, s2 = 0.f;
     float xh[8];  // x-hat, reused below
+    if (!from_y) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        xa[e] = st_cur.y;
+        xb[e] = -st_cur.x * st_cur.y;
+      }
+    }
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      xh[e] = (zz[e] - st_cur.x) * st_cur.y;
+      xh[e] = fmaf(zz[e], xa[e], xb[e]);
       const float gg = dy[e] * gam[e];
       s1 += gg;
       s2 += gg * xh[e];

@@ -32,9 +32,13 @@ struct LnBwdArgs {
   const void* dy = nullptr;    // bf16
   const void* dy2 = nullptr;   // bf16, added to dy (nullable)
   DropoutCfg in_drop;          // dropout that followed the LN (embedding)
-  const void* z = nullptr;
+  const void* z = nullptr;     // LN input z, or (beta != nullptr) the LN output y
   const void* stats = nullptr;
   const float* gamma = nullptr;
+  // output-based x-hat: with beta set, `z` holds y = x-hat * gamma + beta (the
+  // saved / retained LN output) and x-hat = (y - beta) / gamma; only rstd of
+  // `stats` is read. Post-LN halves keep no LN input (lean saves).
+  const float* beta = nullptr;
   void* dz = nullptr;          // bf16 grad of z (residual path)
   void* dbr = nullptr;         // bf16 grad of the dropped-out branch (nullable)
   DropoutCfg br_drop;

@@ -237,6 +237,8 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
     ck(cudaEventCreateWithFlags(&stage_ev_[k], cudaEventDisableTiming), "event");
   }
   ev_.resize(2 * static_cast<size_t>(units()));
+  bnd_out_.assign(static_cast<size_t>(units()), nullptr);
+  bnd_st_.assign(static_cast<size_t>(units()), nullptr);
   for (auto& e : ev_) ck(cudaEventCreate(&e), "cudaEventCreate");
   for (int k = 0; k < kEvRing; ++k) {
     ck(cudaEventCreate(&step_ev_[k][0]), "cudaEventCreate");
@@ -560,7 +562,7 @@ int64_t Trainer::block_work_bytes(int S) const {
       drop_b(st);                               // st2
     } else {
       take_b(act); if (hid) take_b(act);        // dres (dz2), df
-      drop_b(act); drop_b(act); drop_b(st);     // dy, z2, st2
+      drop_b(act);                              // dy (LN2 backward reads y, st: boundary)
       g_use(); take_b(fact);                    // g -> du
       if (hid) drop_b(act);                     // df
       drop_b(fact);                             // u
@@ -571,7 +573,8 @@ int64_t Trainer::block_work_bytes(int S) const {
   auto attn = [&] {  // attn_half_bwd: dh1 (+ da) live -> dx live
     if (!pre) {
       take_b(act); if (hid) take_b(act);        // dz1, da
-      drop_b(act); drop_b(act); drop_b(st);     // dh1, z1, st1
+      drop_b(act);                              // dh1 (LN1 backward reads h1, st)
+      if (!half_) { drop_b(act); drop_b(st); }  // block-internal h1, st1
     }
     if (!flash) drop_b(act);                    // ctx
     take_b(act);                                // dctx
@@ -608,7 +611,7 @@ int64_t Trainer::block_work_bytes(int S) const {
   } else {
     live = peak = act;                          // dy
     ffn();
-    drop_b(act);                                // h1 (block-internal, saved)
+    if (pre) drop_b(act);                       // h1 (block-internal, saved; post-LN: after LN1')
     attn();
     work = peak;
   }
@@ -657,10 +660,13 @@ void Trainer::build_spec() {
   const double p_quad = flash ? (m_.attn_dropout > 0.f ? nh_ / (8.0 * B) : 0.0)
                               : (save_pd() ? 2.0 : 1.0) * nh_ * 2.0 / B;
   const double lin_extra = flash ? 4.0 * nh_ : 0.0;
-  // prior a(x) per token: attention half qkv + ctx + z1 + st1 + output h1;
-  // FFN half u + g + z2 + st2 + output y
-  const double attn_lin = static_cast<double>(12 * H + 8) + lin_extra;
-  const double ffn_lin = static_cast<double>((t_.ffn_regen_g ? 2 : 4) * F + 4 * H + 8);
+  // prior a(x) per token: attention half qkv + ctx (+ x1 + st1 pre-LN) + output
+  // h1 (+ its LN statistics post-LN); FFN half u + g (+ x2 + st2 pre-LN) +
+  // output y (+ statistics post-LN)
+  const bool pre = m_.arch == MIMOSE_ARCH_GPT2;
+  const double attn_lin = static_cast<double>(pre ? 12 * H + 8 : 10 * H + 8) + lin_extra;
+  const double ffn_lin =
+      static_cast<double>((t_.ffn_regen_g ? 2 : 4) * F + (pre ? 4 * H + 8 : 2 * H + 8));
   for (int u = 0; u < units(); ++u) {
     const bool attn_part = !half_ || u % 2 == 0;
     const bool ffn_part = !half_ || u % 2 == 1;
@@ -673,7 +679,7 @@ void Trainer::build_spec() {
     ls.category = quad > 0.0 ? mimose::LayerCategory::QuadraticStructure
                              : mimose::LayerCategory::ImplicitReduction;
     ls.activation_coeffs = {0.0, (attn_part ? attn_lin : 0.0) + (ffn_part ? ffn_lin : 0.0), quad};
-    ls.boundary_coeffs = {0.0, static_cast<double>(2 * H)};
+    ls.boundary_coeffs = {0.0, static_cast<double>(2 * H + (pre ? 0 : 8))};
     ls.forward_time_coeffs = {0.01, 1e-6};
     spec_.layers.push_back(ls);
   }
@@ -911,10 +917,16 @@ void* Trainer::attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaS
 //   GPT-2 (pre-LN)   attention  x1 = LN1(h), h1 = h + drop(attn(x1) Wo + bo)
 //                    FFN        x2 = LN2(h1), y = h1 + drop(gelu(x2 W1 + b1) W2 + b2)
 //                    (residual + dropout in the epilogue of the GEMM ending each half)
-// Saved sets: attention {qkv, lse (+ keep bits) | P (+ Pd), ctx, z1|x1, st1},
-// FFN {z2|x2, st2, u, g}.
-void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, const StepGeo& g,
-                            cudaStream_t s) {
+// Saved sets: attention {qkv, lse (+ keep bits) | P (+ Pd), ctx (, x1, st1
+// pre-LN)}, FFN {u, g (, x2, st2 pre-LN)}. Post-LN halves keep no LN input:
+// the LN backward takes x-hat from the LN OUTPUT (the unit's output, kept as
+// its boundary anyway) and rstd from the output statistics st_out, which the
+// boundary keeps too (8 B per token). So a dropped unit's recompute (lean)
+// stops before the output projection: attention = QKV GEMM + flash, FFN =
+// the FFN1 GEMM - the projection GEMM and LN that made the retained output
+// are not rerun (pre-LN likewise: the residual epilogue GEMM is skipped).
+void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, void* st_out,
+                            bool lean, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_;
   auto* W = static_cast<bf16raw*>(p16_);
@@ -938,7 +950,12 @@ void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, cons
   }
   void* ctx = attn_fwd(l, ain, save, g, s);
   if (pre && !keep) drop(x1);
-  void* z1 = nullptr;
+  if (lean) {  // recompute: h1 (and its statistics) are retained
+    save->ctx = ctx;
+    save->z1 = x1;
+    save->st1 = st1;
+    return;
+  }
   if (pre) {
     // output projection with the residual + branch dropout in the epilogue
     GemmCall c = linear_call(ctx, W + P.wo.off, T, (int)H, (int)H, h1, mimose_ops::kEpiBf16,
@@ -956,24 +973,23 @@ void Trainer::attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, cons
                          p32_ + P.bo.off),
              s);
     if (!keep) drop(ctx);
-    z1 = keep ? take(T * H * 2, act_tag) : nullptr;
-    st1 = keep ? take(T * 8, act_tag) : nullptr;
+    st1 = st_out;
     mimose_ops::LnFwdArgs la;
     la.rows = (int)T; la.res = h; la.br = a; la.br_drop = attn_out_drop;
     la.gamma = p32_ + P.ln1_g.off; la.beta = p32_ + P.ln1_b.off; la.eps = m_.ln_eps;
-    la.z = z1; la.stats = st1; la.y = h1;
+    la.stats = st1; la.y = h1;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
     drop(a);
   }
   if (keep) {
     save->ctx = ctx;
-    save->z1 = pre ? x1 : z1;
-    save->st1 = st1;
+    save->z1 = x1;
+    if (pre) save->st1 = st1;
   }
 }
 
-void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const StepGeo& g,
-                           cudaStream_t s) {
+void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, void* st_out,
+                           bool lean, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_, F = F_;
   auto* W = static_cast<bf16raw*>(p16_);
@@ -1009,7 +1025,14 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
     drop(u);
     if (pre) drop(x2);
   }
-  void* z2 = nullptr;
+  if (lean) {  // recompute: y (and its statistics) are retained
+    if (regen) drop(gg);
+    save->z2 = x2;
+    save->st2 = st2;
+    save->u = u;
+    save->g = gg;
+    return;
+  }
   if (pre) {
     // y = h1 + dropout(g W2^T + b2): residual + dropout in the GEMM epilogue
     GemmCall c = linear_call(gg, W + P.w2.off, T, (int)H, (int)F, y, mimose_ops::kEpiBf16,
@@ -1024,17 +1047,15 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
                          p32_ + P.b2.off),
              s);
     if (!keep || regen) drop(gg);
-    z2 = keep ? take(T * H * 2, act_tag) : nullptr;
-    st2 = keep ? take(T * 8, act_tag) : nullptr;
     mimose_ops::LnFwdArgs la;
     la.rows = (int)T; la.res = h1; la.br = f; la.br_drop = ffn_out_drop;
     la.gamma = p32_ + P.ln2_g.off; la.beta = p32_ + P.ln2_b.off; la.eps = m_.ln_eps;
-    la.z = z2; la.stats = st2; la.y = y;
+    la.stats = st_out; la.y = y;
     ck(mimose_ops::add_ln_fwd(la, (int)H, s), "add_ln_fwd");
     drop(f);
   }
   if (keep) {
-    save->z2 = pre ? x2 : z2;
+    save->z2 = x2;
     save->st2 = st2;
     save->u = u;
     save->g = gg;
@@ -1042,19 +1063,46 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const 
 }
 
 void Trainer::unit_fwd(int u, const void* in, void* out, UnitSave* save, const StepGeo& g,
-                       cudaStream_t s) {
+                       cudaStream_t s, bool lean) {
   if (u < 0 || u >= units()) throw std::runtime_error("unit index out of range");
+  if (lean && (save == nullptr || !has_boundary(u, out)))
+    throw std::runtime_error("unit_fwd: lean recompute needs the unit's boundary of this step");
   if (save != nullptr) save->live = true;
+  // a full forward (re)writes the unit's boundary: output + output LN statistics
+  void* st = nullptr;
+  if (!lean) {
+    drop_boundary(u);
+    if (post_ln()) st = take(g.T * 8, kTagBoundary);
+    bnd_out_[static_cast<size_t>(u)] = out;
+    bnd_st_[static_cast<size_t>(u)] = st;
+  }
   if (half_) {
-    if (u % 2 == 0) attn_half_fwd(u / 2, in, out, save ? &save->a : nullptr, g, s);
-    else ffn_half_fwd(u / 2, in, out, save ? &save->f : nullptr, g, s);
+    if (u % 2 == 0) attn_half_fwd(u / 2, in, out, save ? &save->a : nullptr, st, lean, g, s);
+    else ffn_half_fwd(u / 2, in, out, save ? &save->f : nullptr, st, lean, g, s);
     return;
   }
+  // whole block: h1 is block-internal, so even a lean recompute runs the
+  // attention half in full (h1 + its statistics into the saved set); only the
+  // FFN half stops before its output projection
   void* h1 = take(g.T * H_ * 2, save ? kTagAct : kTagTransient);
-  attn_half_fwd(u, in, h1, save ? &save->a : nullptr, g, s);
-  ffn_half_fwd(u, h1, out, save ? &save->f : nullptr, g, s);
+  void* st1 = save && post_ln() ? take(g.T * 8, kTagAct) : nullptr;
+  attn_half_fwd(u, in, h1, save ? &save->a : nullptr, st1, false, g, s);
+  if (save != nullptr && post_ln()) save->a.st1 = st1;
+  ffn_half_fwd(u, h1, out, save ? &save->f : nullptr, st, lean, g, s);
   if (save != nullptr) save->h1 = h1;
   else drop(h1);
+}
+
+void Trainer::drop_boundary(int u) {
+  const auto k = static_cast<size_t>(u);
+  drop(bnd_st_[k]);
+  bnd_out_[k] = nullptr;
+}
+
+// (step failure: the step scope already returned the blocks to the arena)
+void Trainer::clear_boundaries() {
+  std::fill(bnd_out_.begin(), bnd_out_.end(), nullptr);
+  std::fill(bnd_st_.begin(), bnd_st_.end(), nullptr);
 }
 
 void Trainer::free_save(UnitSave& sv) {
@@ -1071,8 +1119,8 @@ void Trainer::free_save(UnitSave& sv) {
 // FFN half: consumes dy (grad of y) and the saved set, returns d h1. Pre-LN
 // blocks also return (*da) the attention branch's dropped-out gradient and
 // accumulate dbo: both come out of LN2's backward, which already reads d h1.
-void* Trainer::ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void** da_out,
-                            const StepGeo& g, cudaStream_t s) {
+void* Trainer::ffn_half_bwd(int l, const void* h1, const void* y, const void* y_st, FfnSave& sv,
+                            void* dy, void** da_out, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_, F = F_;
   auto* W = static_cast<bf16raw*>(p16_);
@@ -1097,13 +1145,14 @@ void* Trainer::ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void**
   } else {
     dres = take(T * H * 2, kTagTransient);  // dz2
     df = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+    // x-hat from the LN output y (the unit's boundary) and its rstd
     mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dy; a.z = sv.z2; a.stats = sv.st2; a.gamma = p32_ + P.ln2_g.off;
+    a.rows = (int)T; a.dy = dy; a.z = y; a.stats = y_st; a.gamma = p32_ + P.ln2_g.off;
+    a.beta = p32_ + P.ln2_b.off;
     a.dz = dres; a.dbr = df; a.br_drop = ffn_out_drop;
     a.partial = ln_partial_;
     ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln2_g.off, G + P.ln2_b.off, G + P.b2.off, s), "ln_bwd");
     drop(dy);
-    drop(sv.z2); drop(sv.st2);
   }
   void* dfp = df ? df : (pre ? dy : dres);
   // FFN2: dW2 = df^T g ; du = (df W2) * gelu'(u)
@@ -1153,8 +1202,8 @@ void* Trainer::ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void**
 
 // Attention half: consumes d h1 (and, pre-LN, the FFN half's da), returns
 // d h (grad of the block input).
-void* Trainer::attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void* da,
-                             const StepGeo& g, cudaStream_t s) {
+void* Trainer::attn_half_bwd(int l, const void* h, void* h1, void* h1_st, bool own_h1,
+                             AttnSave& sv, void* dh1, void* da, const StepGeo& g, cudaStream_t s) {
   const LayerParams& P = lp_[l];
   const int64_t T = g.T, H = H_;
   auto* W = static_cast<bf16raw*>(p16_);
@@ -1168,13 +1217,19 @@ void* Trainer::attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void
     // LN1 backward (+ attention-output dropout, dbo)
     dz1 = take(T * H * 2, kTagTransient);
     da = hid_drop ? take(T * H * 2, kTagTransient) : nullptr;
+    // x-hat from the LN output h1 and its rstd (whole-block units own the
+    // block-internal h1 and its statistics: released right here)
     mimose_ops::LnBwdArgs a;
-    a.rows = (int)T; a.dy = dh1; a.z = sv.z1; a.stats = sv.st1; a.gamma = p32_ + P.ln1_g.off;
+    a.rows = (int)T; a.dy = dh1; a.z = h1; a.stats = h1_st; a.gamma = p32_ + P.ln1_g.off;
+    a.beta = p32_ + P.ln1_b.off;
     a.dz = dz1; a.dbr = da; a.br_drop = attn_out_drop;
     a.partial = ln_partial_;
     ck(mimose_ops::ln_bwd(a, (int)H, G + P.ln1_g.off, G + P.ln1_b.off, G + P.bo.off, s), "ln_bwd");
     drop(dh1);
-    drop(sv.z1); drop(sv.st1);
+    if (own_h1) {
+      drop(h1);
+      drop(h1_st);
+    }
   }
   void* dap = da ? da : (pre ? dh1 : dz1);
   // output projection: dWo = da^T ctx ; dctx = da Wo
@@ -1216,20 +1271,42 @@ void* Trainer::attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void
   return dx;
 }
 
+// The unit's boundary (output + post-LN statistics, bnd_out_ / bnd_st_) must
+// still be held: its LN backward reads them; the statistics are released
+// here, the output by the caller.
 void* Trainer::unit_bwd(int u, const void* in, UnitSave& sv, void* dy, void** aux,
                         const StepGeo& g, cudaStream_t s) {
   if (u < 0 || u >= units()) throw std::runtime_error("unit index out of range");
+  const auto k = static_cast<size_t>(u);
+  if (post_ln() && bnd_out_[k] == nullptr)
+    throw std::runtime_error("unit_bwd: the unit's output (boundary) is not held");
+  void* out = bnd_out_[k];
+  void* ost = bnd_st_[k];
   sv.live = false;
+  void* dx = nullptr;
   if (half_) {
-    if (u % 2 == 1) return ffn_half_bwd(u / 2, in, sv.f, dy, aux, g, s);
-    void* da = *aux;
-    *aux = nullptr;
-    return attn_half_bwd(u / 2, in, sv.a, dy, da, g, s);
+    if (u % 2 == 1) {
+      dx = ffn_half_bwd(u / 2, in, out, ost, sv.f, dy, aux, g, s);
+    } else {
+      void* da = *aux;
+      *aux = nullptr;
+      dx = attn_half_bwd(u / 2, in, out, ost, false, sv.a, dy, da, g, s);
+    }
+  } else {
+    void* da = nullptr;
+    void* dh1 = ffn_half_bwd(u, sv.h1, out, ost, sv.f, dy, &da, g, s);
+    if (post_ln()) {
+      // the attention half's LN backward reads h1: it releases h1 / st1
+      dx = attn_half_bwd(u, in, sv.h1, sv.a.st1, true, sv.a, dh1, da, g, s);
+      sv.h1 = nullptr;
+      sv.a.st1 = nullptr;
+    } else {
+      drop(sv.h1);
+      dx = attn_half_bwd(u, in, nullptr, nullptr, false, sv.a, dh1, da, g, s);
+    }
   }
-  void* da = nullptr;
-  void* dh1 = ffn_half_bwd(u, sv.h1, sv.f, dy, &da, g, s);
-  drop(sv.h1);
-  return attn_half_bwd(u, in, sv.a, dh1, da, g, s);
+  drop_boundary(u);
+  return dx;
 }
 // ------------------------------------------------------------ replay
 // Peak residency of one iteration under `plan` as THIS executor runs it:
@@ -1732,6 +1809,7 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
   resolve_step_ms(slot);
   ck(cudaEventRecord(step_ev_[slot][0], s), "event");
 
+  for (int u = 0; u < U; ++u) drop_boundary(u);  // (none left by a finished step)
   EmbedSave es;
   void* h0 = embed_fwd(in, g, es, s);
 
@@ -1803,7 +1881,10 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
     // both halves of a block dropped: its FFN half's output is the only
     // boundary kept; h1 is regenerated with the attention half's recompute
     // right before the FFN half's (see the backward loop and replay_peak)
-    if (pair_dropped(u, dropped) && !dtr) drop(out[u - 1]);
+    if (pair_dropped(u, dropped) && !dtr) {
+      drop_boundary(u - 1);
+      drop(out[u - 1]);
+    }
   }
   // memory-prediction error on the kept units (allocator-measured a_u(x))
   if (trained_) {
@@ -1841,8 +1922,9 @@ void Trainer::forward_backward(const StepInputs& in, int B, int S, cudaStream_t 
         out[u - 1] = take(T * H * 2, kTagBoundary);
         unit_fwd(u - 1, ha, out[u - 1], &saves[u - 1], g, s);
       }
-      // recompute, same kernels and Philox streams as the forward
-      unit_fwd(u, u == 0 ? h0 : out[u - 1], out[u], &saves[u], g, s);
+      // recompute, same kernels and Philox streams as the forward, of what
+      // the backward reads (the retained output is not regenerated)
+      unit_fwd(u, u == 0 ? h0 : out[u - 1], out[u], &saves[u], g, s, /*lean=*/true);
     }
     void* dx = unit_bwd(u, u == 0 ? h0 : out[u - 1], saves[u], dy, &aux, g, s);
     // a block's parameters are final once its attention half is done
@@ -1923,6 +2005,7 @@ void Trainer::end_step(bool ok) {
   in_step_ = false;
   if (!ok) {
     for (void* p : step_live_) ctx_->arena.free(p);
+    clear_boundaries();
     // the event slot of the failed step is recorded-but-unfinished at most
     for (int k = 0; k < kEvRing; ++k)
       if (step_ev_iter_[k] == iter_) step_ev_iter_[k] = -1;
@@ -2404,6 +2487,29 @@ int mimose_layer_fwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, co
     }
     *saved = sv;
   });
+}
+
+int mimose_layer_recompute(mimose_trainer* tr, int unit, const mimose_layer_io* io,
+                           const void* x_in, void* x_out, mimose_saved** saved, void* stream) {
+  if (!tr || !io || !x_in || !x_out || !saved) return fail("mimose_layer_recompute: null argument");
+  return guarded("mimose_layer_recompute", [&] {
+    Trainer* t = tr->impl;
+    const auto g = t->geometry(io->batch, io->seq, io->step);
+    auto* sv = new mimose_saved();
+    try {
+      t->unit_fwd(unit, x_in, x_out, &sv->unit, g, static_cast<cudaStream_t>(stream), true);
+    } catch (...) {
+      t->free_save(sv->unit);
+      delete sv;
+      throw;
+    }
+    *saved = sv;
+  });
+}
+
+int mimose_layer_release(mimose_trainer* tr, int unit) {
+  if (!tr || unit < 0 || unit >= tr->impl->units()) return fail("mimose_layer_release: bad argument");
+  return guarded("mimose_layer_release", [&] { tr->impl->drop_boundary(unit); });
 }
 
 int mimose_layer_bwd(mimose_trainer* tr, int unit, const mimose_layer_io* io, const void* x_in,

@@ -37,15 +37,17 @@ struct LayerParams {
   ParamRef wqkv, bqkv, wo, bo, ln1_g, ln1_b, w1, b1, w2, b2, ln2_g, ln2_b;
 };
 
-// Saved tensors of the attention half of a block. z1: post-LN = LN1 input
-// (h + dropout(attn)), pre-LN = LN1 output x1; st1 = LN1 {mean, rstd}.
+// Saved tensors of the attention half of a block. z1: pre-LN = LN1 output x1
+// (post-LN halves keep no LN input: their LN backward reads the LN output,
+// see Trainer::bnd_st_); st1 = LN1 {mean, rstd} (pre-LN; post-LN whole-block
+// units: the block-internal h1's).
 struct AttnSave {
   void *qkv = nullptr, *P = nullptr, *Pd = nullptr, *ctx = nullptr, *z1 = nullptr,
        *st1 = nullptr;
   void *lse = nullptr, *mask = nullptr;  // flash attention (attn_fused = 3) instead of P / Pd
 };
-// Saved tensors of the FFN half. z2: post-LN = LN2 input, pre-LN = LN2
-// output x2 (the FFN input); u = FFN1 pre-activation, g = GELU(u).
+// Saved tensors of the FFN half. z2: pre-LN = LN2 output x2 (the FFN input);
+// u = FFN1 pre-activation, g = GELU(u).
 struct FfnSave {
   void *z2 = nullptr, *st2 = nullptr, *u = nullptr, *g = nullptr;
 };
@@ -132,7 +134,12 @@ class Trainer {
   // n_dropped >= 0 the retained outputs of exactly that many dropped units,
   // else of every unit
   int64_t extras_bytes(int S, int n_dropped = -1) const;
-  int64_t unit_out_bytes(int S) const { return 2LL * t_.batch * S * H_; }
+  // a unit's checkpoint boundary: its output (+ post-LN: the output
+  // LayerNorm's {mean, rstd}, which its LN backward reads with the output)
+  int64_t unit_out_bytes(int S) const {
+    return (2LL * H_ + (post_ln() ? 8 : 0)) * t_.batch * S;
+  }
+  bool post_ln() const { return m_.arch != MIMOSE_ARCH_GPT2; }
   int64_t head_bytes(int S) const;
   int64_t block_work_bytes(int S) const;
   int64_t nonunit_bytes(int S) const;
@@ -163,23 +170,37 @@ class Trainer {
  public:
   int units() const { return half_ ? 2 * L_ : L_; }
   int unit_block(int u) const { return half_ ? u / 2 : u; }
+  // lean == true: recompute of a dropped unit whose boundary (output + its
+  // statistics, unit_out_bytes) this step still holds: only the tensors its
+  // backward reads are regenerated - the final projection GEMM and LayerNorm
+  // that produced the (retained) output are skipped
   void unit_fwd(int u, const void* in, void* out, UnitSave* save, const StepGeo& g,
-                cudaStream_t s);
+                cudaStream_t s, bool lean = false);
   void* unit_bwd(int u, const void* in, UnitSave& sv, void* dy, void** aux, const StepGeo& g,
                  cudaStream_t s);
+  // boundary records of the current step: unit output and (post-LN) its
+  // LayerNorm statistics, from the unit's forward until its backward
+  bool has_boundary(int u, const void* out) const {
+    return u >= 0 && u < units() && bnd_out_[static_cast<size_t>(u)] == out && out != nullptr;
+  }
+  void drop_boundary(int u);
+  void clear_boundaries();
   void free_save(UnitSave& sv);
   void* take(int64_t bytes, int tag);
   void drop(void*& p);
 
  private:
-  void attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, const StepGeo& g,
-                     cudaStream_t s);
-  void ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, const StepGeo& g,
-                    cudaStream_t s);
-  void* ffn_half_bwd(int l, const void* h1, FfnSave& sv, void* dy, void** da, const StepGeo& g,
-                     cudaStream_t s);
-  void* attn_half_bwd(int l, const void* h, AttnSave& sv, void* dh1, void* da, const StepGeo& g,
-                      cudaStream_t s);
+  // st_out: post-LN output LayerNorm statistics buffer (or null); lean: skip
+  // the output projection (+ LN) - the output already exists
+  void attn_half_fwd(int l, const void* h, void* h1, AttnSave* save, void* st_out, bool lean,
+                     const StepGeo& g, cudaStream_t s);
+  void ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, void* st_out, bool lean,
+                    const StepGeo& g, cudaStream_t s);
+  // y / y_st (h1 / h1_st): the half's output and its LN statistics (post-LN)
+  void* ffn_half_bwd(int l, const void* h1, const void* y, const void* y_st, FfnSave& sv,
+                     void* dy, void** da, const StepGeo& g, cudaStream_t s);
+  void* attn_half_bwd(int l, const void* h, void* h1, void* h1_st, bool own_h1, AttnSave& sv,
+                      void* dh1, void* da, const StepGeo& g, cudaStream_t s);
   void* attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, cudaStream_t s);
   void* attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
   int fused_attn(int S) const;
@@ -291,6 +312,7 @@ class Trainer {
   // does not shrink the arena for the next one
   bool in_step_ = false;
   std::unordered_set<void*> step_live_;
+  std::vector<void*> bnd_out_, bnd_st_;  // per unit: retained output / its LN statistics
   friend struct StepScope;
  public:
   void begin_step();

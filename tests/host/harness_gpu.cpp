@@ -280,6 +280,7 @@ int main(int argc, char** argv) {
       // keeps only the FFN half's output (the executor's rule, see
       // Trainer::replay_peak); h1 is regenerated before the FFN half's recompute
       if (half && u % 2 == 1 && (collect || (dropped[u] && dropped[u - 1]))) {
+        ck(mimose_layer_release(tr, u - 1), "release h1");
         ck(mimose_free(ctx, out[u - 1]), "free h1");
         out[u - 1] = nullptr;
       }
@@ -294,7 +295,7 @@ int main(int argc, char** argv) {
            "recompute attention half");
       }
       const void* in = u == 0 ? h0 : out[u - 1];
-      if (sv[u] == nullptr) ck(mimose_layer_fwd(tr, u, &io, in, out[u], &sv[u], s), "recompute");
+      if (sv[u] == nullptr) ck(mimose_layer_recompute(tr, u, &io, in, out[u], &sv[u], s), "recompute");
       void* dx = nullptr;
       ck(mimose_layer_bwd(tr, u, &io, in, sv[u], dy, &dx, s), "layer bwd");
       ck(mimose_free(ctx, out[u]), "free out");
