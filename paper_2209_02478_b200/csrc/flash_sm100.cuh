@@ -89,6 +89,53 @@ __device__ __forceinline__ uint32_t fl_pack(float a, float b) {
 template <int N>
 __device__ __forceinline__ void fl_epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
+// Store one 64-byte segment per lane (lane = a row; c = its four 16-byte
+// chunks, dst = the row's segment, ok = the row exists) with coalesced warp
+// stores: a 4x4 chunk transpose inside each group of four lanes (two
+// shfl_xor rounds), after which store k has lane 4g + i write chunk i of row
+// 4g + k - 8 whole 64-B segments per instruction instead of 32 scattered
+// 16-B pieces (the row-per-lane form costs one L2 request per lane and
+// stalled the attention epilogues for thousands of cycles).
+__device__ __forceinline__ void fl_store_rows64(uint4 (&c)[4], void* dst, bool ok) {
+  const uint32_t lane = threadIdx.x & 31;
+  uint32_t m[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    m[j][0] = c[j].x; m[j][1] = c[j].y; m[j][2] = c[j].z; m[j][3] = c[j].w;
+  }
+  // round 1 (lanes i, i ^ 2): swap the off-diagonal 2x2 blocks
+  const bool a = (lane >> 1) & 1;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t send = a ? m[k][w] : m[2 + k][w];
+      const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 2);
+      if (a) m[k][w] = got;
+      else m[2 + k][w] = got;
+    }
+  // round 2 (lanes i, i ^ 1): swap inside the 2x2 blocks
+  const bool b = lane & 1;
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t send = b ? m[2 * k][w] : m[2 * k + 1][w];
+      const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 1);
+      if (b) m[2 * k][w] = got;
+      else m[2 * k + 1][w] = got;
+    }
+  const uint64_t mine = reinterpret_cast<uint64_t>(dst);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int src = static_cast<int>(lane & ~3u) + k;
+    const uint64_t row = __shfl_sync(0xffffffffu, mine, src);
+    const bool rok = __shfl_sync(0xffffffffu, ok, src);
+    if (rok)
+      *reinterpret_cast<uint4*>(row + 16 * (lane & 3)) = make_uint4(m[k][0], m[k][1], m[k][2], m[k][3]);
+  }
+}
+
 // Pipeline trace (build with -DMIMOSE_FLASH_TRACE): CTA 0 stamps SM clocks.
 #ifdef MIMOSE_FLASH_TRACE
 __device__ unsigned long long g_flash_trace[4096];
@@ -241,6 +288,12 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     const uint32_t idesc_s = idesc_bf16_f32(128, KB, false, false);
     const uint32_t idesc_pv = idesc_bf16_f32(128, 64, false, true);
     int kv = 0, jb = 0, tc = 0;
+    // Warp-collective issue (umma_*_w: one lane elected inside the asm) with
+    // descriptors as base + offset: the SWIZZLE_128B descriptor's start field
+    // is addr >> 4, so a tile offset is added to it directly.
+    const uint64_t qdesc = smem_desc_sw128(smem_u32(sQ), 16, 1024);
+    const uint64_t kdesc = smem_desc_sw128(smem_u32(sKV), 16, 1024);                // K, stage 0
+    const uint64_t vdesc = smem_desc_sw128(smem_u32(sKV + Cfg::kKBytes), 8192, 1024);  // V, stage 0
     // O_w += P_b[:, 32w..32w+31] V[32w..32w+31, :] for block b (j-th of its tile)
     auto issue_pv = [&](int b, int j, int stage) {
       if (lane == 0 && b < 256) FT(b * 4 + 1, FT_CLK());
@@ -248,30 +301,23 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         mbar_wait(oempty, (tc & 1) ^ 1);  // the previous tile's O has been read
         tc_fence_after();
       }
-#pragma unroll 1
+#pragma unroll
       for (int w = 0; w < NSL; ++w) {
         mbar_wait(&pfull[(b & 1) * NSL + w], (b >> 1) & 1);
         tc_fence_after();
-        if (lane == 0) {
-          // A = P_b[:, slice w] from TMEM (bf16 pairs, 16 columns of P
-          // buffer b & 1), B = V rows of the slice (MN-major)
-          const uint32_t pa = tmem_base + KB + (b & 1) * (KB / 2) + 16 * w;
-          const uint32_t va = smem_u32(sKV + stage * Cfg::kKVBytes + Cfg::kKBytes +
-                                       (w >> 1) * 8192) + (w & 1) * 4096;
+        // A = P_b[:, slice w] from TMEM (bf16 pairs, 16 columns of P buffer
+        // b & 1), B = V rows of the slice (MN-major)
+        const uint32_t pa = tmem_base + KB + (b & 1) * (KB / 2) + 16 * w;
+        const uint64_t vd =
+            vdesc + (uint64_t)((stage * Cfg::kKVBytes + (w >> 1) * 8192 + (w & 1) * 4096) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < 2; ++kk)
-            umma_bf16_ts(tmem_base + 2 * KB + 64 * w, pa + 8 * kk,
-                         smem_desc_sw128(va + kk * 2048, 8192, 1024), idesc_pv,
-                         (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < 2; ++kk)
+          umma_bf16_ts_w(tmem_base + 2 * KB + 64 * w, pa + 8 * kk, vd + (uint64_t)(kk * 2048 >> 4),
+                         idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
       }
-      if (lane == 0) {
-        umma_commit(&pempty[b & 1]);
-        umma_commit(&empty[stage]);
-      }
+      umma_commit_w(&pempty[b & 1]);
+      umma_commit_w(&empty[stage]);
       if (lane == 0 && b < 256) FT(b * 4 + 2, FT_CLK());
-      __syncwarp();
     };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       int z_, qt_;
@@ -286,24 +332,20 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         mbar_wait(sfree, (jb & 1) ^ 1);  // S_{jb-1} loaded by the softmax warps
         tc_fence_after();
         if (lane == 0 && jb < 256) FT(jb * 4 + 0, FT_CLK());
-        if (lane == 0) {
-          const uint32_t qa = smem_u32(sQ), ka = smem_u32(sKV + s * Cfg::kKVBytes);
+        const uint64_t kd = kdesc + (uint64_t)((s * Cfg::kKVBytes) >> 4);
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16(tmem_base, smem_desc_sw128(qa + kk * 32, 16, 1024),
-                      smem_desc_sw128(ka + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
-          umma_commit(sfull);
-          if (j == nkb - 1) umma_commit(qempty);
-        }
-        __syncwarp();
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_w(tmem_base, qdesc + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s,
+                      kk != 0 ? 1u : 0u);
+        umma_commit_w(sfull);
+        if (j == nkb - 1) umma_commit_w(qempty);
         // the previous block's P V goes after this block's S, so the softmax
         // warps have S_j in hand while P_{j-1} V_{j-1} runs
         if (j > 0) issue_pv(jb - 1, j - 1, prev_stage);
         prev_stage = s;
       }
       issue_pv(jb - 1, nkb - 1, prev_stage);
-      if (lane == 0) umma_commit(ofull);
-      __syncwarp();
+      umma_commit_w(ofull);
     }
   } else {
     // ------------------------------------------------------------ softmax warps
@@ -354,7 +396,16 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(oempty);
-      if (pend_ok) {
+      if constexpr (OC == 32) {
+        uint4 ch[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          ch[q] = make_uint4(fl_pack(acc[8 * q] * inv, acc[8 * q + 1] * inv),
+                             fl_pack(acc[8 * q + 2] * inv, acc[8 * q + 3] * inv),
+                             fl_pack(acc[8 * q + 4] * inv, acc[8 * q + 5] * inv),
+                             fl_pack(acc[8 * q + 6] * inv, acc[8 * q + 7] * inv));
+        fl_store_rows64(ch, p.ctx + pend_ctx, pend_ok);
+      } else if (pend_ok) {
         uint4* dst = reinterpret_cast<uint4*>(p.ctx + pend_ctx);
 #pragma unroll
         for (int q = 0; q < OC / 8; ++q)
@@ -362,8 +413,8 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
                               fl_pack(acc[8 * q + 2] * inv, acc[8 * q + 3] * inv),
                               fl_pack(acc[8 * q + 4] * inv, acc[8 * q + 5] * inv),
                               fl_pack(acc[8 * q + 6] * inv, acc[8 * q + 7] * inv));
-        if (w == 0) p.lse[pend_grow] = M + __log2f(L);
       }
+      if (pend_ok && w == 0) p.lse[pend_grow] = M + __log2f(L);
       pend = false;
     };
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
@@ -530,13 +581,22 @@ struct FlashBwdCfg {
   static constexpr int kMinBlocks = (MODE == 1 && KB == 64) ? 2 : 1;
   static constexpr int kTile = 128 * 64 * 2;       // one 128-row x 64-dim bf16 tile
   static constexpr int kStrTile = (MODE == 0 ? 128 : KB) * 64 * 2;  // streamed tile
-  static constexpr int kStages = 2;
+  // streamed (Q, dO) | (K, V) ring: a stage is released only when its block's
+  // accumulation MMAs finish, so with two stages block j + 2's S / dPd MMAs
+  // waited for block j's accumulation plus a TMA round trip (the measured
+  // serialisation of the dK / dV kernel); 4 stages take the smem a second
+  // staging buffer would (measured no gain). The two-CTA dQ kernel has no
+  // room for a third stage (116.2 KB > 115.7 KB per CTA).
+  static constexpr int kStages = MODE == 0 ? 4 : 2;
   static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
+  // staged score tiles per block (dK / dV: Pd and dS; dQ: dS)
+  static constexpr int kSqPer = MODE == 0 ? 2 : 1;
+  static constexpr int kSqBufs = 1;
   static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
   // S double buffer (2 kKB) + dPd (kKB) + accumulators (128 for dK / dV, 64 for dQ)
   static constexpr int kTmemCols = MODE == 0 ? 512 : (KB == 64 ? 256 : 512);
   static constexpr int kSmemBytes = kFix * kTile + kStages * 2 * kStrTile +
-                                    (MODE == 0 ? 2 : 1) * kSqBytes + 1024 + 512;
+                                    kSqBufs * kSqPer * kSqBytes + 1024 + 512;
 };
 
 // per-score backward algebra for 16 keys (columns e0..e0+15 of the thread's
@@ -609,9 +669,11 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
   constexpr int kFix = Cfg::kFix;
   uint8_t* sFix = smem;
   uint8_t* sStr = smem + kFix * Cfg::kTile;
-  uint8_t* sDS = sStr + NS * 2 * Cfg::kStrTile;
-  uint8_t* sPD = sDS + Cfg::kSqBytes;  // KV only
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sDS + (KV ? 2 : 1) * Cfg::kSqBytes);
+  // staging buffer b: dS at sSq + b * kSqPer * kSqBytes, Pd (KV) right after
+  uint8_t* sSq = sStr + NS * 2 * Cfg::kStrTile;
+  constexpr int kSqBuf = Cfg::kSqPer * Cfg::kSqBytes;
+  constexpr int NQ = Cfg::kSqBufs;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sSq + NQ * kSqBuf);
   uint64_t* full = bars;             // [NS]
   uint64_t* empty = full + NS;       // [NS]
   uint64_t* fixfull = empty + NS;
@@ -621,9 +683,9 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
   uint64_t* sfull = fixempty + 1;  // [2] S[b] and dPd of a block landed
   uint64_t* sempty = sfull + 2;    // [2] S buffer b read
   uint64_t* dpempty = sempty + 2;  // dPd read
-  uint64_t* pfull = dpempty + 1;
-  uint64_t* pdone = pfull + 1;
-  uint64_t* accfull = pdone + 1;
+  uint64_t* pfull = dpempty + 1;   // [NQ] staging buffer written by the score warps
+  uint64_t* pdone = pfull + NQ;    // [NQ] staging buffer read by the accumulation MMAs
+  uint64_t* accfull = pdone + NQ;
   uint64_t* accempty = accfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
 
@@ -673,8 +735,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       mbar_init(&sempty[b2], Cfg::kEW);
     }
     mbar_init(dpempty, Cfg::kEW);
-    mbar_init(pfull, Cfg::kEW);
-    mbar_init(pdone, 1);
+    for (int q = 0; q < NQ; ++q) {
+      mbar_init(&pfull[q], Cfg::kEW);
+      mbar_init(&pdone[q], 1);
+    }
     mbar_init(accfull, 1);
     mbar_init(accempty, Cfg::kEW);
     fence_barrier_init();
@@ -719,47 +783,49 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     // Q : dQ += dS K (A K-major [query][key] tile, B = K MN-major)
     const uint32_t idesc_acc = idesc_bf16_f32(128, 64, KV, true);
     int st = 0, ic = 0, blkc = 0;  // blkc: inner blocks processed (barrier phases)
+    // warp-collective issue (umma_*_w), descriptors as base + (offset >> 4)
+    const uint64_t d_str16 = smem_desc_sw128(smem_u32(sStr), 16, 1024);    // streamed, K-major
+    const uint64_t d_fix16 = smem_desc_sw128(smem_u32(sFix), 16, 1024);    // fixed, K-major
+    const uint64_t d_str8k = smem_desc_sw128(smem_u32(sStr), 8192, 1024);  // streamed, MN-major
+    const uint64_t d_sq16k = smem_desc_sw128(smem_u32(sSq), 16384, 1024);  // staged, MN-major
+    const uint64_t d_sq16 = smem_desc_sw128(smem_u32(sSq), 16, 1024);      // staged, K-major
+    auto off = [](int bytes) { return (uint64_t)(bytes >> 4); };
     auto issue_sdp = [&](int s, int sb) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
-      const uint32_t q = smem_u32(KV ? sStr + s * 2 * Cfg::kStrTile : sFix);
-      const uint32_t k = smem_u32(KV ? sFix : sStr + s * 2 * Cfg::kStrTile);
+      const uint64_t q = KV ? d_str16 + off(s * 2 * Cfg::kStrTile) : d_fix16;
+      const uint64_t k = KV ? d_fix16 : d_str16 + off(s * 2 * Cfg::kStrTile);
       constexpr int kQ2 = KV ? Cfg::kStrTile : Cfg::kTile;   // dO follows Q
       constexpr int kK2 = KV ? Cfg::kTile : Cfg::kStrTile;   // V follows K
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem_base + sb * KBL, smem_desc_sw128(q + kk * 32, 16, 1024),
-                  smem_desc_sw128(k + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
+        umma_bf16_w(tmem_base + sb * KBL, q + off(kk * 32), k + off(kk * 32), idesc_s,
+                    kk != 0 ? 1u : 0u);
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
-        umma_bf16(tmem_base + 2 * KBL, smem_desc_sw128(q + kQ2 + kk * 32, 16, 1024),
-                  smem_desc_sw128(k + kK2 + kk * 32, 16, 1024), idesc_s, kk != 0 ? 1u : 0u);
-      umma_commit(&sfull[sb]);
+        umma_bf16_w(tmem_base + 2 * KBL, q + off(kQ2 + kk * 32), k + off(kK2 + kk * 32), idesc_s,
+                    kk != 0 ? 1u : 0u);
+      umma_commit_w(&sfull[sb]);
     };
-    auto issue_acc = [&](int s, int sb, bool first) {
+    auto issue_acc = [&](int s, int qb, bool first) {  // qb: staging buffer
       if (KV) {
-        const uint32_t pd = smem_u32(sPD), ds = smem_u32(sDS);
-        const uint32_t q = smem_u32(sStr + s * 2 * Cfg::kStrTile);
+        const uint64_t ds = d_sq16k + off(qb * kSqBuf), pd = ds + off(Cfg::kSqBytes);
+        const uint64_t q = d_str8k + off(s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // K = 128 queries, 16 per MMA
-          umma_bf16(tmem_base + 3 * KBL, smem_desc_sw128(pd + kk * 2048, 16384, 1024),
-                    smem_desc_sw128(q + Cfg::kStrTile + kk * 2048, 8192, 1024), idesc_acc,
-                    (first && kk == 0) ? 0u : 1u);
-          umma_bf16(tmem_base + 3 * KBL + 64, smem_desc_sw128(ds + kk * 2048, 16384, 1024),
-                    smem_desc_sw128(q + kk * 2048, 8192, 1024), idesc_acc,
-                    (first && kk == 0) ? 0u : 1u);
+          umma_bf16_w(tmem_base + 3 * KBL, pd + off(kk * 2048), q + off(Cfg::kStrTile + kk * 2048),
+                      idesc_acc, (first && kk == 0) ? 0u : 1u);
+          umma_bf16_w(tmem_base + 3 * KBL + 64, ds + off(kk * 2048), q + off(kk * 2048), idesc_acc,
+                      (first && kk == 0) ? 0u : 1u);
         }
       } else {
-        const uint32_t ds = smem_u32(sDS);
-        const uint32_t k = smem_u32(sStr + s * 2 * Cfg::kStrTile);
+        const uint64_t ds = d_sq16 + off(qb * kSqBuf);
+        const uint64_t k = d_str8k + off(s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < KBL / 16; ++kk)  // K = the block's keys
-          umma_bf16(tmem_base + 3 * KBL,
-                    smem_desc_sw128(ds + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024),
-                    smem_desc_sw128(k + kk * 2048, 8192, 1024), idesc_acc,
-                    (first && kk == 0) ? 0u : 1u);
+          umma_bf16_w(tmem_base + 3 * KBL, ds + off((kk >> 2) * 16384 + (kk & 3) * 32),
+                      k + off(kk * 2048), idesc_acc, (first && kk == 0) ? 0u : 1u);
       }
-      (void)sb;
-      umma_commit(pdone);
-      umma_commit(&empty[s]);
+      umma_commit_w(&pdone[qb]);
+      umma_commit_w(&empty[s]);
     };
     for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
       int lo, hi;
@@ -776,39 +842,38 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         mbar_wait(&sempty[blkc & 1], ((blkc >> 1) & 1) ^ 1);
         mbar_wait(dpempty, (blkc & 1) ^ 1);
         tc_fence_after();
-        if (lane == 0) {
-          issue_sdp(s, blkc & 1);
-          // dK / dV: the fixed K, V tiles feed only the S / dPd MMAs (the
-          // accumulation reads the staged tiles and the streamed pair), so they
-          // are released after the item's last S / dPd and the next item's
-          // loads overlap this one's tail. (dQ: the score warps read the fixed
-          // dO / O tiles and wait on fixfull, so those are released only after
-          // the item's last accumulation -- an earlier release would let the
-          // producer overwrite them, and lap fixfull, before the warps read.)
-          if (KV && j == hi - 1) umma_commit(fixempty);
-        }
-        __syncwarp();
+        if (KV && lane == 0 && blkc < 256) FT(blkc * 4 + 0, FT_CLK());
+        issue_sdp(s, blkc & 1);
+        // dK / dV: the fixed K, V tiles feed only the S / dPd MMAs (the
+        // accumulation reads the staged tiles and the streamed pair), so they
+        // are released after the item's last S / dPd and the next item's
+        // loads overlap this one's tail. (dQ: the score warps read the fixed
+        // dO / O tiles and wait on fixfull, so those are released only after
+        // the item's last accumulation -- an earlier release would let the
+        // producer overwrite them, and lap fixfull, before the warps read.)
+        if (KV && j == hi - 1) umma_commit_w(fixempty);
         if (j > lo) {
-          mbar_wait(pfull, (blkc - 1) & 1);
+          const int pb = blkc - 1;
+          if (j - 1 == lo) {
+            // the accumulators are free once the previous item's were read
+            // (the score warps drain them after this item's first block)
+            mbar_wait(accempty, (ic & 1) ^ 1);
+          }
+          mbar_wait(&pfull[pb % NQ], (pb / NQ) & 1);
           tc_fence_after();
-          if (lane == 0) issue_acc(prev_s, (blkc - 1) & 1, j - 1 == lo);
-          __syncwarp();
+          if (KV && lane == 0 && pb < 256) FT(pb * 4 + 1, FT_CLK());
+          issue_acc(prev_s, pb % NQ, j - 1 == lo);
+          if (KV && lane == 0 && pb < 256) FT(pb * 4 + 2, FT_CLK());
         }
         prev_s = s;
-        if (j == lo) {
-          // the accumulators are free once the previous item's were read
-          mbar_wait(accempty, (ic & 1) ^ 1);
-          tc_fence_after();
-        }
       }
-      mbar_wait(pfull, (blkc - 1) & 1);
+      const int pb = blkc - 1;
+      if (hi - 1 == lo) mbar_wait(accempty, (ic & 1) ^ 1);
+      mbar_wait(&pfull[pb % NQ], (pb / NQ) & 1);
       tc_fence_after();
-      if (lane == 0) {
-        issue_acc(prev_s, (blkc - 1) & 1, hi - 1 == lo);
-        umma_commit(accfull);
-        if (!KV) umma_commit(fixempty);
-      }
-      __syncwarp();
+      issue_acc(prev_s, pb % NQ, hi - 1 == lo);
+      umma_commit_w(accfull);
+      if (!KV) umma_commit_w(fixempty);
     }
   } else {
     // ------------------------------------------------------------ score warps
@@ -819,6 +884,72 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     const uint32_t lane_base = tmem_base + ((uint32_t)(quarter * 32) << 16);
     const bool dropout = p.drop.threshold != 0;
     int ic = 0, blkc = 0;
+    // accumulators of item `dic` (TMEM lanes = its 128 key / query rows) -> dqkv
+    auto drain = [&](int dic, int dblk, int dh, int db) {
+        if (KV && ew == 0 && lane == 0 && dic < 256) FT(2048 + dic * 4 + 0, FT_CLK());
+        mbar_wait(accfull, dic & 1);
+        if (KV && ew == 0 && lane == 0 && dic < 256) FT(2048 + dic * 4 + 1, FT_CLK());
+        tc_fence_after();
+        const int row = dblk * 128 + r;  // key (KV) or query (Q) row of this lane
+        if (KV) {
+          uint32_t o[32];
+          tmem_ld32_nowait(lane_base + 3 * KBL + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
+          tmem_wait_ld();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(accempty);
+          {
+            const long long H = p.ctx_ld;
+            const int rr = row < p.S ? row : 0;
+            __nv_bfloat16* dst = p.dqkv + ((long long)db * p.S + rr) * 3 * H + (w < 2 ? 2 * H : H) +
+                                 dh * 64 + 32 * (w & 1);
+            uint4 ch[4];
+  #pragma unroll
+            for (int q = 0; q < 4; ++q)
+              ch[q] = make_uint4(fl_pack(__uint_as_float(o[8 * q]), __uint_as_float(o[8 * q + 1])),
+                                 fl_pack(__uint_as_float(o[8 * q + 2]), __uint_as_float(o[8 * q + 3])),
+                                 fl_pack(__uint_as_float(o[8 * q + 4]), __uint_as_float(o[8 * q + 5])),
+                                 fl_pack(__uint_as_float(o[8 * q + 6]), __uint_as_float(o[8 * q + 7])));
+            fl_store_rows64(ch, dst, row < p.S);
+          }
+          if (ew == 0 && lane == 0 && dic < 256) FT(2048 + dic * 4 + 2, FT_CLK());
+        } else {
+          constexpr int OC = 64 / Cfg::kNSL;  // dQ columns of this warp
+          float o[OC];
+  #pragma unroll
+          for (int q = 0; q < OC / 16; ++q) {
+            uint32_t u[16];
+            tmem_ld16u_nowait(lane_base + 3 * KBL + OC * w + 16 * q, u);
+            tmem_wait_ld();
+  #pragma unroll
+            for (int e = 0; e < 16; ++e) o[16 * q + e] = __uint_as_float(u[e]);
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(accempty);
+          const long long H = p.ctx_ld;
+          const int rr = row < p.S ? row : 0;
+          __nv_bfloat16* dst = p.dqkv + ((long long)db * p.S + rr) * 3 * H + dh * 64 + OC * w;
+          if constexpr (OC == 32) {
+            uint4 ch[4];
+  #pragma unroll
+            for (int q = 0; q < 4; ++q)
+              ch[q] = make_uint4(fl_pack(o[8 * q], o[8 * q + 1]), fl_pack(o[8 * q + 2], o[8 * q + 3]),
+                                 fl_pack(o[8 * q + 4], o[8 * q + 5]),
+                                 fl_pack(o[8 * q + 6], o[8 * q + 7]));
+            fl_store_rows64(ch, dst, row < p.S);
+          } else if (row < p.S) {
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+  #pragma unroll
+            for (int q = 0; q < OC / 8; ++q)
+              d4[q] = make_uint4(fl_pack(o[8 * q], o[8 * q + 1]), fl_pack(o[8 * q + 2], o[8 * q + 3]),
+                                 fl_pack(o[8 * q + 4], o[8 * q + 5]),
+                                 fl_pack(o[8 * q + 6], o[8 * q + 7]));
+          }
+        }
+    };
+    bool pend = false;
+    int pend_ic = 0, pend_blk = 0, pend_h = 0, pend_b = 0;
     for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
       int z, blk;
       decode(item, z, blk);
@@ -848,6 +979,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         const int i = blk * 128 + r;
         if (w == 0 && i < p.S) p.dvec[(int64_t)z * p.S + i] = d_row;
       }
+      if (KV && ew == 0 && lane == 0 && ic < 256) FT(2048 + ic * 4 + 3, FT_CLK());
       for (int j = lo; j < hi; ++j, ++blkc) {
         const int qb = KV ? j : blk, kb = KV ? blk : j;  // query / key block
         const int i = qb * 128 + r;
@@ -861,7 +993,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         if (!row_ok) lim = 0;
         const uint32_t kw = (dropout && lim > 0) ? p.mask[grow * p.mw + (c0 >> 5)] : 0u;
         const int sbuf = blkc & 1;
+        const bool trw = KV && ew == 0 && lane == 0 && blkc < 256;
+        if (trw) FT(1024 + blkc * 4 + 0, FT_CLK());
         mbar_wait(&sfull[sbuf], (blkc >> 1) & 1);
+        if (trw) FT(1024 + blkc * 4 + 1, FT_CLK());
         tc_fence_after();
         const bool all_full = __all_sync(0xffffffffu, lim >= 32);
         const bool all_dead = __all_sync(0xffffffffu, lim <= 0);
@@ -907,64 +1042,31 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                                                p.sc, pk_pd, pk_ds);
           }
         }
-        // the previous block's accumulation MMAs have read the staged tiles
-        mbar_wait(pdone, (blkc & 1) ^ 1);
-        if (KV) flash_st_slice(sPD, r, w, pk_pd);
+        // the accumulation MMAs of this staging buffer's previous block
+        // (blkc - NQ) have read it
+        if (trw) FT(1024 + blkc * 4 + 2, FT_CLK());
+        const int sq = blkc % NQ;
+        mbar_wait(&pdone[sq], ((blkc / NQ) & 1) ^ 1);
+        uint8_t* sDS = sSq + sq * kSqBuf;
+        if (KV) flash_st_slice(sDS + Cfg::kSqBytes, r, w, pk_pd);
         flash_st_slice(sDS, r, w, pk_ds);
         fence_async_shared();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(pfull);
-      }
-      // ---- item end: accumulators out (TMEM lanes = the item's 128 rows)
-      mbar_wait(accfull, ic & 1);
-      tc_fence_after();
-      const int row = blk * 128 + r;  // key (KV) or query (Q) row of this lane
-      if (KV) {
-        uint32_t o[32];
-        tmem_ld32_nowait(lane_base + 3 * KBL + 32 * w, o);  // w 0,1: dV halves; 2,3: dK halves
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(accempty);
-        if (row < p.S) {
-          const long long H = p.ctx_ld;
-          __nv_bfloat16* dst = p.dqkv + ((long long)b * p.S + row) * 3 * H + (w < 2 ? 2 * H : H) +
-                               h * 64 + 32 * (w & 1);
-          uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            d4[q] = make_uint4(fl_pack(__uint_as_float(o[8 * q]), __uint_as_float(o[8 * q + 1])),
-                               fl_pack(__uint_as_float(o[8 * q + 2]), __uint_as_float(o[8 * q + 3])),
-                               fl_pack(__uint_as_float(o[8 * q + 4]), __uint_as_float(o[8 * q + 5])),
-                               fl_pack(__uint_as_float(o[8 * q + 6]), __uint_as_float(o[8 * q + 7])));
-        }
-      } else {
-        constexpr int OC = 64 / Cfg::kNSL;  // dQ columns of this warp
-        float o[OC];
-#pragma unroll
-        for (int q = 0; q < OC / 16; ++q) {
-          uint32_t u[16];
-          tmem_ld16u_nowait(lane_base + 3 * KBL + OC * w + 16 * q, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int e = 0; e < 16; ++e) o[16 * q + e] = __uint_as_float(u[e]);
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(accempty);
-        if (row < p.S) {
-          const long long H = p.ctx_ld;
-          uint4* d4 = reinterpret_cast<uint4*>(p.dqkv + ((long long)b * p.S + row) * 3 * H +
-                                               h * 64 + OC * w);
-#pragma unroll
-          for (int q = 0; q < OC / 8; ++q)
-            d4[q] = make_uint4(fl_pack(o[8 * q], o[8 * q + 1]), fl_pack(o[8 * q + 2], o[8 * q + 3]),
-                               fl_pack(o[8 * q + 4], o[8 * q + 5]),
-                               fl_pack(o[8 * q + 6], o[8 * q + 7]));
+        if (lane == 0) mbar_arrive(&pfull[sq]);
+        if (trw) FT(1024 + blkc * 4 + 3, FT_CLK());
+        if (j == lo && pend) {  // the previous item's accumulators
+          drain(pend_ic, pend_blk, pend_h, pend_b);
+          pend = false;
         }
       }
+      // item end: the accumulators are drained after the NEXT item's first
+      // block (drain()), so the wait for this item's last accumulation and
+      // the stores overlap that block's MMAs
+      pend = true;
+      pend_ic = ic; pend_blk = blk; pend_h = h; pend_b = b;
     }
+    if (pend) drain(pend_ic, pend_blk, pend_h, pend_b);
   }
   __syncthreads();
   if (warp == 1) {

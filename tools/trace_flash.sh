@@ -12,3 +12,4 @@ rm -f $T/paper_2209_02478_b200/*.so
    paper_2209_02478_b200/libmimose_cuda.so > build.log 2>&1) || { tail -20 $T/build.log; exit 1; }
 mkdir -p $ROOT/gpurun_out
 (cd $T && python tools/flash_trace.py "$@") > $ROOT/gpurun_out/flash_trace.txt 2>&1
+(cd $T && python tools/flash_trace_bwd.py "$@") > $ROOT/gpurun_out/flash_trace_bwd.txt 2>&1
