@@ -135,13 +135,14 @@ cudaError_t flash_fwd(const MatView& q, const MatView& k, const MatView& v, void
 cudaError_t flash_keep_mask(uint32_t* mask, int S, int ld, int nh, int B,
                             const mimose_dev::DropoutCfg& drop, bool causal, cudaStream_t s) {
   if (drop.threshold == 0) return cudaSuccess;
-  if (mask == nullptr || !flash_supported(S)) return cudaErrorInvalidValue;
+  if (mask == nullptr || !flash_supported(S) || ld % 8 != 0) return cudaErrorInvalidValue;
   const int mw = (S + 31) / 32;
+  if ((int64_t)B * nh * S * mw >= (int64_t(1) << 32)) return cudaErrorInvalidValue;
   ProfScope prof("attn_flash_mask", 0.0, (double)nh * B * 4.0 * S * mw, s);
   const int64_t n = (int64_t)B * nh * S * mw;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 16 * flash_sm_count());
   mimose_dev::flash_keep_mask_kernel<<<blocks, 256, 0, s>>>(
-      drop.seed, drop.stream, drop.threshold, (long long)B * nh * S, S, ld, mw, causal ? 1 : 0,
+      drop.seed, drop.stream, drop.threshold, (uint32_t)((int64_t)B * nh * S), S, ld, mw, causal ? 1 : 0,
       mask);
   count_launch();
   return cudaGetLastError();

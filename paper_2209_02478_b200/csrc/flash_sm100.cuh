@@ -71,8 +71,10 @@ struct FlashFwdCfg {
   static constexpr int kXchBytes = 2 * 2 * kNSL * 128 * 4;  // [tile parity][m|l][slice][row]
   static constexpr int kTmemCols = 4 * KB;         // S (KB) + 2 P buffers (KB / 2) + kNSL O slices (64)
   static constexpr int kOCols = 64 / kNSL;         // output columns per warp in the combine
+  // two Q buffers: the next tile's Q lands while this tile runs, so its first
+  // Q K^T is issued before this tile's last P V (no tile-boundary bubble)
   static constexpr int kSmemBytes =
-      kQBytes + kStages * kKVBytes + kXchBytes + 1024 + 512;
+      2 * kQBytes + kStages * kKVBytes + kXchBytes + 1024 + 512;
 };
 
 __device__ __forceinline__ float fl_ex2(float x) {
@@ -158,18 +160,22 @@ __device__ __forceinline__ unsigned long long fl_clk() {
 // The bits depend only on (seed, stream, shape), so this runs at full
 // occupancy ahead of the forward, which then tests one bit per score.
 __global__ void flash_keep_mask_kernel(uint64_t seed, uint64_t stream, uint32_t threshold,
-                                       long long rows, int S, int ld, int mw, int causal,
+                                       uint32_t rows, int S, int ld, int mw, int causal,
                                        uint32_t* __restrict__ mask) {
-  const long long n = rows * mw;
+  // 32-bit index math (the host guarantees rows * mw < 2^32): a 64-bit
+  // division per word cost as many instructions as one of its Philox calls
+  const uint32_t n = rows * (uint32_t)mw;
   const uint32_t thr_hi = threshold << 16;
-  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
-       t += (long long)gridDim.x * blockDim.x) {
-    const long long row = t / mw;
-    const int k = (int)(t % mw);
-    if (causal && 32 * k > (int)(row % S)) continue;  // all keys above the diagonal: never read
+  const uint32_t umw = (uint32_t)mw, uS = (uint32_t)S;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+    const uint32_t row = t / umw;
+    const uint32_t k = t - row * umw;
+    if (causal && 32 * k > row % uS) continue;  // all keys above the diagonal: never read
+    // ld % 8 == 0: the word's four Philox groups are consecutive
+    const uint64_t g0 = ((uint64_t)row * (uint32_t)ld + 32 * k) >> 3;
     uint64_t grp[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) grp[q] = ((uint64_t)row * ld + 32 * k + 8 * q) >> 3;
+    for (int q = 0; q < 4; ++q) grp[q] = g0 + q;
     uint32_t rnd[4][4];
     philox_n<4>(seed, stream, grp, rnd);
     uint32_t kw = 0;
@@ -191,18 +197,18 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + Cfg::kQBytes;
+  uint8_t* sQ = smem;  // [2] Q buffers (tile parity)
+  uint8_t* sKV = smem + 2 * Cfg::kQBytes;
   float* xch = reinterpret_cast<float*>(sKV + NS * Cfg::kKVBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xch) + Cfg::kXchBytes);
   uint64_t* empty = full + NS;
-  uint64_t* qfull = empty + NS;
-  uint64_t* qempty = qfull + 1;
+  uint64_t* qfull = empty + NS;   // [2]
+  uint64_t* qempty = qfull + 2;   // [2]
   // TMEM: one S buffer [0, KB) released as soon as the softmax warps have
   // loaded it (so S_{j+1} runs while they compute block j), two P buffers
   // [KB, 2 KB) (bf16 pairs, KB / 2 columns each) released by the P V commit,
   // the NSL per-slice O accumulators [2 KB, 2 KB + 64 NSL)
-  uint64_t* sfull = qempty + 1;   // S landed
+  uint64_t* sfull = qempty + 2;   // S landed
   uint64_t* sfree = sfull + 1;    // S loaded by every softmax warp
   uint64_t* pfull = sfree + 1;    // [2 P buffers][NSL slices]
   uint64_t* pempty = pfull + 2 * NSL;  // [2] P buffer read by its P V MMAs
@@ -242,8 +248,10 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(qfull, 1);
-    mbar_init(qempty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&qfull[b], 1);
+      mbar_init(&qempty[b], 1);
+    }
     mbar_init(sfull, 1);
     mbar_init(sfree, Cfg::kEW);
     for (int i = 0; i < 2 * NSL; ++i) mbar_init(&pfull[i], 4);  // the slice's four lane-quarter warps
@@ -267,9 +275,10 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         int z, qt;
         decode(tile, z, qt);
         const int h = z % p.nh, b = z / p.nh;
-        mbar_wait(qempty, (tc & 1) ^ 1);
-        mbar_arrive_expect_tx(qfull, Cfg::kQBytes);
-        tma_load_4d(&tmQ, qfull, sQ, 0, qt * 128, h, b);
+        const int qb = tc & 1;
+        mbar_wait(&qempty[qb], ((tc >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&qfull[qb], Cfg::kQBytes);
+        tma_load_4d(&tmQ, &qfull[qb], sQ + qb * Cfg::kQBytes, 0, qt * 128, h, b);
         const int nkb = nkb_of(qt);
         for (int j = 0; j < nkb; ++j, ++kv) {
           const int s = kv % NS;
@@ -294,11 +303,12 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     const uint64_t qdesc = smem_desc_sw128(smem_u32(sQ), 16, 1024);
     const uint64_t kdesc = smem_desc_sw128(smem_u32(sKV), 16, 1024);                // K, stage 0
     const uint64_t vdesc = smem_desc_sw128(smem_u32(sKV + Cfg::kKBytes), 8192, 1024);  // V, stage 0
-    // O_w += P_b[:, 32w..32w+31] V[32w..32w+31, :] for block b (j-th of its tile)
-    auto issue_pv = [&](int b, int j, int stage) {
+    // O_w += P_b[:, 32w..32w+31] V[32w..32w+31, :] for block b (j-th of tile
+    // number btc)
+    auto issue_pv = [&](int b, int j, int stage, int btc) {
       if (lane == 0 && b < 256) FT(b * 4 + 1, FT_CLK());
       if (j == 0) {
-        mbar_wait(oempty, (tc & 1) ^ 1);  // the previous tile's O has been read
+        mbar_wait(oempty, (btc & 1) ^ 1);  // the previous tile's O has been read
         tc_fence_after();
       }
 #pragma unroll
@@ -319,13 +329,19 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
       umma_commit_w(&empty[stage]);
       if (lane == 0 && b < 256) FT(b * 4 + 2, FT_CLK());
     };
+    // One flat block sequence across tiles: block g's Q K^T goes in before
+    // block g - 1's P V, also when g opens a new tile (its Q is already in the
+    // other buffer), so the softmax warps find S ready at every tile boundary.
+    bool have_prev = false, prev_last = false;
+    int prev_b = 0, prev_j = 0, prev_stage = 0, prev_tc = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tc) {
       int z_, qt_;
       decode(tile, z_, qt_);
       const int nkb = nkb_of(qt_);
-      mbar_wait(qfull, tc & 1);
+      const int qb = tc & 1;
+      mbar_wait(&qfull[qb], (tc >> 1) & 1);
       tc_fence_after();
-      int prev_stage = 0;
+      const uint64_t qd = qdesc + (uint64_t)((qb * Cfg::kQBytes) >> 4);
       for (int j = 0; j < nkb; ++j, ++kv, ++jb) {
         const int s = kv % NS;
         mbar_wait(&full[s], (kv / NS) & 1);
@@ -335,16 +351,22 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
         const uint64_t kd = kdesc + (uint64_t)((s * Cfg::kKVBytes) >> 4);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          umma_bf16_w(tmem_base, qdesc + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s,
+          umma_bf16_w(tmem_base, qd + (uint64_t)(kk * 2), kd + (uint64_t)(kk * 2), idesc_s,
                       kk != 0 ? 1u : 0u);
         umma_commit_w(sfull);
-        if (j == nkb - 1) umma_commit_w(qempty);
+        if (j == nkb - 1) umma_commit_w(&qempty[qb]);
         // the previous block's P V goes after this block's S, so the softmax
         // warps have S_j in hand while P_{j-1} V_{j-1} runs
-        if (j > 0) issue_pv(jb - 1, j - 1, prev_stage);
-        prev_stage = s;
+        if (have_prev) {
+          issue_pv(prev_b, prev_j, prev_stage, prev_tc);
+          if (prev_last) umma_commit_w(ofull);
+        }
+        have_prev = true;
+        prev_b = jb; prev_j = j; prev_stage = s; prev_tc = tc; prev_last = j == nkb - 1;
       }
-      issue_pv(jb - 1, nkb - 1, prev_stage);
+    }
+    if (have_prev) {
+      issue_pv(prev_b, prev_j, prev_stage, prev_tc);
       umma_commit_w(ofull);
     }
   } else {
@@ -587,15 +609,20 @@ struct FlashBwdCfg {
   // serialisation of the dK / dV kernel); 4 stages take the smem a second
   // staging buffer would (measured no gain). The two-CTA dQ kernel has no
   // room for a third stage (116.2 KB > 115.7 KB per CTA).
-  static constexpr int kStages = MODE == 0 ? 4 : 2;
+  static constexpr int kStages = MODE == 0 ? 3 : 2;
   static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
   // staged score tiles per block (dK / dV: Pd and dS; dQ: dS)
   static constexpr int kSqPer = MODE == 0 ? 2 : 1;
   static constexpr int kSqBufs = 1;
   static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
+  // dK / dV: the fixed K, V tiles are double-buffered, so the next item's
+  // land while this one runs and its first S / dPd MMAs go in before this
+  // item's last accumulation (no item-boundary bubble); the two-CTA dQ
+  // kernel has no room for a second set
+  static constexpr int kFixBufs = MODE == 0 ? 2 : 1;
   // S double buffer (2 kKB) + dPd (kKB) + accumulators (128 for dK / dV, 64 for dQ)
   static constexpr int kTmemCols = MODE == 0 ? 512 : (KB == 64 ? 256 : 512);
-  static constexpr int kSmemBytes = kFix * kTile + kStages * 2 * kStrTile +
+  static constexpr int kSmemBytes = kFixBufs * kFix * kTile + kStages * 2 * kStrTile +
                                     kSqBufs * kSqPer * kSqBytes + 1024 + 512;
 };
 
@@ -667,8 +694,9 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
   // fixed tiles: KV ? (K, V) : (Q, dO, O); streamed pairs: KV ? (Q, dO) : (K, V)
   constexpr int kFix = Cfg::kFix;
-  uint8_t* sFix = smem;
-  uint8_t* sStr = smem + kFix * Cfg::kTile;
+  constexpr int NF = Cfg::kFixBufs;
+  uint8_t* sFix = smem;  // [NF] fixed sets (item parity when NF = 2)
+  uint8_t* sStr = smem + NF * kFix * Cfg::kTile;
   // staging buffer b: dS at sSq + b * kSqPer * kSqBytes, Pd (KV) right after
   uint8_t* sSq = sStr + NS * 2 * Cfg::kStrTile;
   constexpr int kSqBuf = Cfg::kSqPer * Cfg::kSqBytes;
@@ -676,11 +704,11 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
   uint64_t* bars = reinterpret_cast<uint64_t*>(sSq + NQ * kSqBuf);
   uint64_t* full = bars;             // [NS]
   uint64_t* empty = full + NS;       // [NS]
-  uint64_t* fixfull = empty + NS;
-  uint64_t* fixempty = fixfull + 1;
+  uint64_t* fixfull = empty + NS;     // [NF]
+  uint64_t* fixempty = fixfull + NF;  // [NF]
   // S double-buffered in TMEM, dPd single: the score warps read dPd first and
   // release it, so the next block's S and dPd MMAs run while they compute
-  uint64_t* sfull = fixempty + 1;  // [2] S[b] and dPd of a block landed
+  uint64_t* sfull = fixempty + NF;  // [2] S[b] and dPd of a block landed
   uint64_t* sempty = sfull + 2;    // [2] S buffer b read
   uint64_t* dpempty = sempty + 2;  // dPd read
   uint64_t* pfull = dpempty + 1;   // [NQ] staging buffer written by the score warps
@@ -728,8 +756,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(fixfull, 1);
-    mbar_init(fixempty, 1);
+    for (int f = 0; f < NF; ++f) {
+      mbar_init(&fixfull[f], 1);
+      mbar_init(&fixempty[f], 1);
+    }
     for (int b2 = 0; b2 < 2; ++b2) {
       mbar_init(&sfull[b2], 1);
       mbar_init(&sempty[b2], Cfg::kEW);
@@ -758,11 +788,14 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         int z, blk;
         decode(item, z, blk);
         const int h = z % p.nh, b = z / p.nh;
-        mbar_wait(fixempty, (ic & 1) ^ 1);
-        mbar_arrive_expect_tx(fixfull, kFix * Cfg::kTile);
-        tma_load_4d(KV ? &tmK : &tmQ, fixfull, sFix, 0, blk * 128, h, b);
-        tma_load_4d(KV ? &tmV : &tmO, fixfull, sFix + Cfg::kTile, 0, blk * 128, h, b);
-        if (!KV) tma_load_4d(&tmC, fixfull, sFix + 2 * Cfg::kTile, 0, blk * 128, h, b);
+        const int fb = ic % NF;
+        const int fu = ic / NF;  // use count of set fb
+        uint8_t* fx = sFix + fb * kFix * Cfg::kTile;
+        mbar_wait(&fixempty[fb], (fu & 1) ^ 1);
+        mbar_arrive_expect_tx(&fixfull[fb], kFix * Cfg::kTile);
+        tma_load_4d(KV ? &tmK : &tmQ, &fixfull[fb], fx, 0, blk * 128, h, b);
+        tma_load_4d(KV ? &tmV : &tmO, &fixfull[fb], fx + Cfg::kTile, 0, blk * 128, h, b);
+        if (!KV) tma_load_4d(&tmC, &fixfull[fb], fx + 2 * Cfg::kTile, 0, blk * 128, h, b);
         int lo, hi;
         inner_range(blk, lo, hi);
         for (int j = lo; j < hi; ++j, ++st) {
@@ -790,9 +823,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     const uint64_t d_sq16k = smem_desc_sw128(smem_u32(sSq), 16384, 1024);  // staged, MN-major
     const uint64_t d_sq16 = smem_desc_sw128(smem_u32(sSq), 16, 1024);      // staged, K-major
     auto off = [](int bytes) { return (uint64_t)(bytes >> 4); };
-    auto issue_sdp = [&](int s, int sb) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
-      const uint64_t q = KV ? d_str16 + off(s * 2 * Cfg::kStrTile) : d_fix16;
-      const uint64_t k = KV ? d_fix16 : d_str16 + off(s * 2 * Cfg::kStrTile);
+    auto issue_sdp = [&](int s, int sb, int fb) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
+      const uint64_t fx = d_fix16 + off(fb * kFix * Cfg::kTile);
+      const uint64_t q = KV ? d_str16 + off(s * 2 * Cfg::kStrTile) : fx;
+      const uint64_t k = KV ? fx : d_str16 + off(s * 2 * Cfg::kStrTile);
       constexpr int kQ2 = KV ? Cfg::kStrTile : Cfg::kTile;   // dO follows Q
       constexpr int kK2 = KV ? Cfg::kTile : Cfg::kStrTile;   // V follows K
 #pragma unroll
@@ -827,15 +861,38 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       umma_commit_w(&pdone[qb]);
       umma_commit_w(&empty[s]);
     };
+    // One flat block sequence across items: block g's S / dPd MMAs go in
+    // before block g - 1's accumulation, also across an item boundary when the
+    // next item's fixed tiles are in the other set (NF = 2).
+    bool have_prev = false, prev_first = false, prev_last = false;
+    int prev_s = 0, prev_pb = 0, prev_ic = 0;
+    auto flush_prev = [&]() {
+      if (prev_first) mbar_wait(accempty, (prev_ic & 1) ^ 1);  // previous item's drained
+      mbar_wait(&pfull[prev_pb % NQ], (prev_pb / NQ) & 1);
+      tc_fence_after();
+      if (KV && lane == 0 && prev_pb < 256) FT(prev_pb * 4 + 1, FT_CLK());
+      issue_acc(prev_s, prev_pb % NQ, prev_first);
+      if (KV && lane == 0 && prev_pb < 256) FT(prev_pb * 4 + 2, FT_CLK());
+      if (prev_last) {
+        umma_commit_w(accfull);
+        // dQ: the score warps read the fixed dO / O tiles (D) and wait on
+        // fixfull, so the set is released only after the item's last
+        // accumulation -- an earlier release would let the producer
+        // overwrite them, and lap fixfull, before the warps read
+        if (!KV) umma_commit_w(&fixempty[prev_ic % NF]);
+      }
+      have_prev = false;
+    };
     for (int item = blockIdx.x; item < num_items; item += gridDim.x, ++ic) {
       int lo, hi;
       int z_, blk_;
       decode(item, z_, blk_);
       inner_range(blk_, lo, hi);
-      mbar_wait(fixfull, ic & 1);
+      const int fb = ic % NF;
+      // one fixed set: the previous item's last accumulation releases it
+      if (NF == 1 && have_prev) flush_prev();
+      mbar_wait(&fixfull[fb], (ic / NF) & 1);
       tc_fence_after();
-      // S / dPd of block j + 1 go in before the accumulation of block j
-      int prev_s = 0;
       for (int j = lo; j < hi; ++j, ++st, ++blkc) {
         const int s = st % NS;
         mbar_wait(&full[s], (st / NS) & 1);
@@ -843,38 +900,18 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
         mbar_wait(dpempty, (blkc & 1) ^ 1);
         tc_fence_after();
         if (KV && lane == 0 && blkc < 256) FT(blkc * 4 + 0, FT_CLK());
-        issue_sdp(s, blkc & 1);
+        issue_sdp(s, blkc & 1, fb);
         // dK / dV: the fixed K, V tiles feed only the S / dPd MMAs (the
-        // accumulation reads the staged tiles and the streamed pair), so they
-        // are released after the item's last S / dPd and the next item's
-        // loads overlap this one's tail. (dQ: the score warps read the fixed
-        // dO / O tiles and wait on fixfull, so those are released only after
-        // the item's last accumulation -- an earlier release would let the
-        // producer overwrite them, and lap fixfull, before the warps read.)
-        if (KV && j == hi - 1) umma_commit_w(fixempty);
-        if (j > lo) {
-          const int pb = blkc - 1;
-          if (j - 1 == lo) {
-            // the accumulators are free once the previous item's were read
-            // (the score warps drain them after this item's first block)
-            mbar_wait(accempty, (ic & 1) ^ 1);
-          }
-          mbar_wait(&pfull[pb % NQ], (pb / NQ) & 1);
-          tc_fence_after();
-          if (KV && lane == 0 && pb < 256) FT(pb * 4 + 1, FT_CLK());
-          issue_acc(prev_s, pb % NQ, j - 1 == lo);
-          if (KV && lane == 0 && pb < 256) FT(pb * 4 + 2, FT_CLK());
-        }
-        prev_s = s;
+        // accumulation reads the staged tiles and the streamed pair), so the
+        // set is released after the item's last S / dPd
+        if (KV && j == hi - 1) umma_commit_w(&fixempty[fb]);
+        if (have_prev) flush_prev();
+        have_prev = true;
+        prev_s = s; prev_pb = blkc; prev_ic = ic;
+        prev_first = j == lo; prev_last = j == hi - 1;
       }
-      const int pb = blkc - 1;
-      if (hi - 1 == lo) mbar_wait(accempty, (ic & 1) ^ 1);
-      mbar_wait(&pfull[pb % NQ], (pb / NQ) & 1);
-      tc_fence_after();
-      issue_acc(prev_s, pb % NQ, hi - 1 == lo);
-      umma_commit_w(accfull);
-      if (!KV) umma_commit_w(fixempty);
     }
+    if (have_prev) flush_prev();
   } else {
     // ------------------------------------------------------------ score warps
     const int ew = warp - 2;
@@ -960,9 +997,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
       // dO / O tiles (this kernel runs first and stores D for the dK / dV one)
       float d_row = 0.f;
       if (!KV) {
-        mbar_wait(fixfull, ic & 1);
-        const uint32_t ra = smem_u32(sFix + Cfg::kTile) + r * 128;
-        const uint32_t rc = smem_u32(sFix + 2 * Cfg::kTile) + r * 128;
+        const uint8_t* fx = sFix + (ic % NF) * kFix * Cfg::kTile;
+        mbar_wait(&fixfull[ic % NF], (ic / NF) & 1);
+        const uint32_t ra = smem_u32(fx + Cfg::kTile) + r * 128;
+        const uint32_t rc = smem_u32(fx + 2 * Cfg::kTile) + r * 128;
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
           const uint32_t off = (uint32_t)((c ^ (r & 7)) << 4);
