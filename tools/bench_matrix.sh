@@ -25,7 +25,7 @@ run roberta_base_tol0 --preset roberta-base-qa
 run roberta_base_tol002 --preset roberta-base-qa --cache-tol 0.02
 run roberta_large --preset roberta-large-qa
 run gpt2 --preset gpt2-medium-lm
-run gpt2_self --preset gpt2-medium-lm --budget-basis self --budget-frac 0.6
+run gpt2_self60 --preset gpt2-medium-lm --budget-basis self --budget-frac 0.6
 run bertlarge --preset bert-large-mlm
-run bertlarge_self --preset bert-large-mlm --budget-basis self --budget-frac 0.4
+run bertlarge_self50 --preset bert-large-mlm --budget-basis self --budget-frac 0.5
 run small4 --preset small4-h256
