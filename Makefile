@@ -29,7 +29,15 @@ CUDA_INC := $(dir $(shell which $(NVCC)))../include
 HDRS    := $(wildcard $(CSRC)/*.cuh) $(wildcard $(CSRC)/*.hpp) $(wildcard include/*.h) \
            $(wildcard include/mimose/*.hpp)
 
-all: $(PKG)/libmimose_cuda.so $(PKG)/libmimose_host.so $(BUILD)/harness_gpu
+all: $(PKG)/libmimose_cuda.so $(PKG)/libmimose_host.so $(BUILD)/harness_gpu $(BUILD)/mimose_gpu
+
+# the reference CLI's subcommands / flags / exit codes driving GPU runs
+$(BUILD)/mimose_gpu: $(PKG)/cli/mimose_gpu.cpp include/mimose_cuda.h include/mimose_planner.h \
+                     | $(PKG)/libmimose_cuda.so $(PKG)/libmimose_host.so
+	@mkdir -p $(BUILD)
+	$(CXX) -O2 -std=c++17 -Wall -Wextra -Iinclude -I$(CUDA_INC) $< -o $@ \
+	  -L$(PKG) -lmimose_cuda -lmimose_host -L$(dir $(shell which $(NVCC)))../lib64 -lcudart \
+	  -Wl,-rpath,'$$ORIGIN/../$(PKG)' -Wl,-rpath,$(dir $(shell which $(NVCC)))../lib64
 
 # compiled C++ host of the reference training loop over the two C ABIs (GPU test)
 $(BUILD)/harness_gpu: tests/host/harness_gpu.cpp include/mimose_cuda.h include/mimose_planner.h \
