@@ -606,13 +606,15 @@ struct FlashBwdCfg {
   // streamed (Q, dO) | (K, V) ring: a stage is released only when its block's
   // accumulation MMAs finish, so with two stages block j + 2's S / dPd MMAs
   // waited for block j's accumulation plus a TMA round trip (the measured
-  // serialisation of the dK / dV kernel); 4 stages take the smem a second
-  // staging buffer would (measured no gain). The two-CTA dQ kernel has no
-  // room for a third stage (116.2 KB > 115.7 KB per CTA).
-  static constexpr int kStages = MODE == 0 ? 3 : 2;
+  // serialisation of the dK / dV kernel). The dQ kernel keeps dS in TMEM
+  // (no staging tile), which leaves room for three stages in its two CTAs.
+  static constexpr int kStages = 3;
   static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
-  // staged score tiles per block (dK / dV: Pd and dS; dQ: dS)
-  static constexpr int kSqPer = MODE == 0 ? 2 : 1;
+  // staged score tiles per block: dK / dV stage Pd and dS in shared memory
+  // ([query][key], read by the MMA as MN-major A operands); the dQ kernel
+  // writes dS (bf16) into TMEM over the S slice it came from and the dQ MMA
+  // reads its A operand from TMEM (no st.shared / proxy fence)
+  static constexpr int kSqPer = MODE == 0 ? 2 : 0;
   static constexpr int kSqBufs = 1;
   static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
   // dK / dV: the fixed K, V tiles are double-buffered, so the next item's
@@ -709,10 +711,17 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
   // S double-buffered in TMEM, dPd single: the score warps read dPd first and
   // release it, so the next block's S and dPd MMAs run while they compute
   uint64_t* sfull = fixempty + NF;  // [2] S[b] and dPd of a block landed
-  uint64_t* sempty = sfull + 2;    // [2] S buffer b read
+  uint64_t* sempty = sfull + 2;    // [2] S buffer b free (dK / dV: read; dQ: its dS consumed)
   uint64_t* dpempty = sempty + 2;  // dPd read
-  uint64_t* pfull = dpempty + 1;   // [NQ] staging buffer written by the score warps
-  uint64_t* pdone = pfull + NQ;    // [NQ] staging buffer read by the accumulation MMAs
+  // dK / dV: [NQ] staging buffer written by the score warps (the pdone wait
+  // before each store keeps a fast warp from arriving for the next block
+  // early); dQ: [2] by block parity -- with no staging wait a warp with dead
+  // rows can run one block ahead, and one barrier would then complete a phase
+  // on mixed arrivals (it cannot run two ahead: block j + 2's S needs block
+  // j's accumulation, which needs pfull of block j)
+  constexpr int NPF = KV ? NQ : 2;
+  uint64_t* pfull = dpempty + 1;   // [NPF]
+  uint64_t* pdone = pfull + NPF;   // [NQ] staging buffer read by the accumulation MMAs
   uint64_t* accfull = pdone + NQ;
   uint64_t* accempty = accfull + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
@@ -762,13 +771,11 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     }
     for (int b2 = 0; b2 < 2; ++b2) {
       mbar_init(&sfull[b2], 1);
-      mbar_init(&sempty[b2], Cfg::kEW);
+      mbar_init(&sempty[b2], KV ? Cfg::kEW : 1);
     }
     mbar_init(dpempty, Cfg::kEW);
-    for (int q = 0; q < NQ; ++q) {
-      mbar_init(&pfull[q], Cfg::kEW);
-      mbar_init(&pdone[q], 1);
-    }
+    for (int q = 0; q < NPF; ++q) mbar_init(&pfull[q], Cfg::kEW);
+    for (int q = 0; q < NQ; ++q) mbar_init(&pdone[q], 1);
     mbar_init(accfull, 1);
     mbar_init(accempty, Cfg::kEW);
     fence_barrier_init();
@@ -821,7 +828,6 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     const uint64_t d_fix16 = smem_desc_sw128(smem_u32(sFix), 16, 1024);    // fixed, K-major
     const uint64_t d_str8k = smem_desc_sw128(smem_u32(sStr), 8192, 1024);  // streamed, MN-major
     const uint64_t d_sq16k = smem_desc_sw128(smem_u32(sSq), 16384, 1024);  // staged, MN-major
-    const uint64_t d_sq16 = smem_desc_sw128(smem_u32(sSq), 16, 1024);      // staged, K-major
     auto off = [](int bytes) { return (uint64_t)(bytes >> 4); };
     auto issue_sdp = [&](int s, int sb, int fb) {  // S = A0 B0^T, dPd = A1 B1^T (query rows)
       const uint64_t fx = d_fix16 + off(fb * kFix * Cfg::kTile);
@@ -839,7 +845,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                     kk != 0 ? 1u : 0u);
       umma_commit_w(&sfull[sb]);
     };
-    auto issue_acc = [&](int s, int qb, bool first) {  // qb: staging buffer
+    auto issue_acc = [&](int s, int qb, int sb, bool first) {  // qb: staging buffer, sb: S buffer
       if (KV) {
         const uint64_t ds = d_sq16k + off(qb * kSqBuf), pd = ds + off(Cfg::kSqBytes);
         const uint64_t q = d_str8k + off(s * 2 * Cfg::kStrTile);
@@ -850,15 +856,18 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
           umma_bf16_w(tmem_base + 3 * KBL + 64, ds + off(kk * 2048), q + off(kk * 2048), idesc_acc,
                       (first && kk == 0) ? 0u : 1u);
         }
+        umma_commit_w(&pdone[qb]);
       } else {
-        const uint64_t ds = d_sq16 + off(qb * kSqBuf);
+        // A = dS from TMEM: keys 32w..32w+31 of S buffer sb as bf16 pairs in
+        // columns [32w, 32w + 16) of the buffer; 16 keys (8 columns) per MMA
+        const uint32_t a0 = tmem_base + sb * KBL;
         const uint64_t k = d_str8k + off(s * 2 * Cfg::kStrTile);
 #pragma unroll
         for (int kk = 0; kk < KBL / 16; ++kk)  // K = the block's keys
-          umma_bf16_w(tmem_base + 3 * KBL, ds + off((kk >> 2) * 16384 + (kk & 3) * 32),
-                      k + off(kk * 2048), idesc_acc, (first && kk == 0) ? 0u : 1u);
+          umma_bf16_ts_w(tmem_base + 3 * KBL, a0 + (kk >> 1) * 32 + (kk & 1) * 8,
+                         k + off(kk * 2048), idesc_acc, (first && kk == 0) ? 0u : 1u);
+        umma_commit_w(&sempty[sb]);  // S buffer (and its dS) free for block + 2
       }
-      umma_commit_w(&pdone[qb]);
       umma_commit_w(&empty[s]);
     };
     // One flat block sequence across items: block g's S / dPd MMAs go in
@@ -868,10 +877,10 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
     int prev_s = 0, prev_pb = 0, prev_ic = 0;
     auto flush_prev = [&]() {
       if (prev_first) mbar_wait(accempty, (prev_ic & 1) ^ 1);  // previous item's drained
-      mbar_wait(&pfull[prev_pb % NQ], (prev_pb / NQ) & 1);
+      mbar_wait(&pfull[prev_pb % NPF], (prev_pb / NPF) & 1);
       tc_fence_after();
       if (KV && lane == 0 && prev_pb < 256) FT(prev_pb * 4 + 1, FT_CLK());
-      issue_acc(prev_s, prev_pb % NQ, prev_first);
+      issue_acc(prev_s, prev_pb % NQ, prev_pb & 1, prev_first);
       if (KV && lane == 0 && prev_pb < 256) FT(prev_pb * 4 + 2, FT_CLK());
       if (prev_last) {
         umma_commit_w(accfull);
@@ -1056,7 +1065,7 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
           const uint32_t (&dr)[16] = dpr[half];
           tmem_ld16u_nowait(lane_base + sbuf * KBL + 32 * w + 16 * half, sr);
           tmem_wait_ld();
-          if (half == 1) {
+          if (KV && half == 1) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&sempty[sbuf]);
@@ -1080,18 +1089,25 @@ __global__ void __launch_bounds__(FlashBwdCfg<MODE, KB>::kThreads,
                                                p.sc, pk_pd, pk_ds);
           }
         }
-        // the accumulation MMAs of this staging buffer's previous block
-        // (blkc - NQ) have read it
         if (trw) FT(1024 + blkc * 4 + 2, FT_CLK());
         const int sq = blkc % NQ;
-        mbar_wait(&pdone[sq], ((blkc / NQ) & 1) ^ 1);
-        uint8_t* sDS = sSq + sq * kSqBuf;
-        if (KV) flash_st_slice(sDS + Cfg::kSqBytes, r, w, pk_pd);
-        flash_st_slice(sDS, r, w, pk_ds);
-        fence_async_shared();
+        if (KV) {
+          // the accumulation MMAs of this staging buffer's previous block
+          // (blkc - NQ) have read it
+          mbar_wait(&pdone[sq], ((blkc / NQ) & 1) ^ 1);
+          uint8_t* sDS = sSq + sq * kSqBuf;
+          flash_st_slice(sDS + Cfg::kSqBytes, r, w, pk_pd);
+          flash_st_slice(sDS, r, w, pk_ds);
+          fence_async_shared();
+        } else {
+          // dS over the first half of this warp's own S slice (its S values
+          // are already in registers; no other warp reads these columns)
+          tmem_st16u(lane_base + sbuf * KBL + 32 * w, pk_ds);
+          tmem_wait_st();
+        }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&pfull[sq]);
+        if (lane == 0) mbar_arrive(&pfull[blkc % NPF]);
         if (trw) FT(1024 + blkc * 4 + 3, FT_CLK());
         if (j == lo && pend) {  // the previous item's accumulators
           drain(pend_ic, pend_blk, pend_h, pend_b);
