@@ -53,12 +53,19 @@ def main():
     ap.add_argument("--attn-mode", type=int, default=3,
                     help="TrainConfig.attn_fused when fused: 3 flash, 2 single-row fused scores")
     ap.add_argument("--time-steps", type=int, default=0, help="also time N steps at --seq")
+    ap.add_argument("--hidden-dropout", type=float, default=None,
+                    help="override the preset's hidden dropout (A/B of the Philox stages)")
+    ap.add_argument("--attn-dropout", type=float, default=None)
     args = ap.parse_args()
     import numpy as np
     import torch
     from paper_2209_02478_b200 import _lib
     from paper_2209_02478_b200.trainer import PRESETS, DeviceBatch, Trainer, synthetic_task_batch
     m, t = PRESETS[args.preset]
+    if args.hidden_dropout is not None:
+        m = dataclasses.replace(m, hidden_dropout=args.hidden_dropout)
+    if args.attn_dropout is not None:
+        m = dataclasses.replace(m, attn_dropout=args.attn_dropout)
     GiB = 1 << 30
     rng = np.random.default_rng(0)
     # budget basis: the materialised-attention model's no-ckpt peak (as bench.py)
