@@ -15,4 +15,12 @@ for P in 0 0.1; do timeout 600 python tools/bench_flash.py --p $P --classes --js
 timeout 1800 bash tools/sanitize.sh > $O/sanitize.log 2>&1; mv gpurun_out/san_* $O/ 2>/dev/null
 STEPS=30 timeout 2400 bash tools/bench_matrix.sh $TAG > $O/matrix_status.txt 2>&1; mv gpurun_out/bm_${TAG}_* $O/ 2>/dev/null
 for U in 1 0; do timeout 600 python tools/budget_sweep.py --unit $U --out $O/budget_sweep_u$U.json > /dev/null 2>&1; done
+# the reference CLI's grid (mimose_main.cpp cmd_compare) over real B200 runs:
+# BERT-base MC, S ~ U(64, 512), 4 planners x 3 budgets, 80 iterations each
+make -s build/mimose_gpu > /dev/null 2>&1 || g++ -O2 -std=c++17 -Iinclude -I/usr/local/cuda/include \
+  paper_2209_02478_b200/cli/mimose_gpu.cpp -o build/mimose_gpu -Lpaper_2209_02478_b200 -lmimose_cuda \
+  -lmimose_host -L/usr/local/cuda/lib64 -lcudart -Wl,-rpath,$PWD/paper_2209_02478_b200
+timeout 1800 build/mimose_gpu compare --model bert-base-mc --dist uniform:64:512 --batch-multiplier 64 \
+  --iters 80 --seed 2024 --budgets 6g,8g,12g --planners mimose,static-max,dtr,none \
+  --out $O/cli_compare_bert.csv > $O/cli_compare.log 2>&1; echo "cli compare rc=$?" >> $O/status.txt
 echo done >> $O/status.txt
