@@ -608,20 +608,28 @@ struct FlashBwdCfg {
   // waited for block j's accumulation plus a TMA round trip (the measured
   // serialisation of the dK / dV kernel). The dQ kernel keeps dS in TMEM
   // (no staging tile), which leaves room for three stages in its two CTAs.
-  static constexpr int kStages = 3;
+  // dK / dV smem split (A/B knob MIMOSE_FLASH_KV_CFG): 0 = two fixed K,V sets,
+  // three ring stages, one staging buffer (default); 1 = one fixed set, two
+  // stages, two staging buffers (no wait for the previous block's
+  // accumulation before the Pd / dS stores); 2 = one fixed set, four stages
+#ifndef MIMOSE_FLASH_KV_CFG
+#define MIMOSE_FLASH_KV_CFG 0
+#endif
+  static constexpr int kKvCfg = MODE == 0 ? MIMOSE_FLASH_KV_CFG : 0;
+  static constexpr int kStages = kKvCfg == 1 ? 2 : (kKvCfg == 2 ? 4 : 3);
   static constexpr int kSqBytes = 128 * kKB * 2;   // one [query][key] bf16 tile
   // staged score tiles per block: dK / dV stage Pd and dS in shared memory
   // ([query][key], read by the MMA as MN-major A operands); the dQ kernel
   // writes dS (bf16) into TMEM over the S slice it came from and the dQ MMA
   // reads its A operand from TMEM (no st.shared / proxy fence)
   static constexpr int kSqPer = MODE == 0 ? 2 : 0;
-  static constexpr int kSqBufs = 1;
+  static constexpr int kSqBufs = kKvCfg == 1 ? 2 : 1;
   static constexpr int kFix = MODE == 0 ? 2 : 3;   // K, V | Q, dO, O
   // dK / dV: the fixed K, V tiles are double-buffered, so the next item's
   // land while this one runs and its first S / dPd MMAs go in before this
   // item's last accumulation (no item-boundary bubble); the two-CTA dQ
   // kernel has no room for a second set
-  static constexpr int kFixBufs = MODE == 0 ? 2 : 1;
+  static constexpr int kFixBufs = (MODE == 0 && kKvCfg == 0) ? 2 : 1;
   // S double buffer (2 kKB) + dPd (kKB) + accumulators (128 for dK / dV, 64 for dQ)
   static constexpr int kTmemCols = MODE == 0 ? 512 : (KB == 64 ? 256 : 512);
   static constexpr int kSmemBytes = kFixBufs * kFix * kTile + kStages * 2 * kStrTile +

@@ -313,10 +313,21 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     const long long n4 = total / 4;
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
          i += (long long)gridDim.x * blockDim.x) {
-      float4 acc = reinterpret_cast<const float4*>(ws)[i];
-      for (int s = 1; s < splits; ++s) {
-        const float4 t = reinterpret_cast<const float4*>(ws + (long long)s * total)[i];
-        acc.x += t.x; acc.y += t.y; acc.z += t.z; acc.w += t.w;
+      // every split's partial (<= 8) loaded before the in-order sum: the
+      // loads overlap instead of one dependent round trip per split
+      float4 t[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)
+        if (s < splits) t[s] = __ldcs(reinterpret_cast<const float4*>(ws + (long long)s * total) + i);
+      float4 acc = t[0];
+#pragma unroll
+      for (int s = 1; s < 8; ++s)
+        if (s < splits) {
+          acc.x += t[s].x; acc.y += t[s].y; acc.z += t[s].z; acc.w += t[s].w;
+        }
+      for (int s = 8; s < splits; ++s) {  // forced split counts above 8
+        const float4 u = reinterpret_cast<const float4*>(ws + (long long)s * total)[i];
+        acc.x += u.x; acc.y += u.y; acc.z += u.z; acc.w += u.w;
       }
       float4* o = reinterpret_cast<float4*>(out) + i;
       if (beta != 0.f) {
@@ -569,7 +580,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
       break;
   }
   if (err == cudaSuccess && splits > 1) {
-    splitk_reduce_kernel<<<2 * sm_count(), 256, 0, stream>>>(
+    splitk_reduce_kernel<<<4 * sm_count(), 256, 0, stream>>>(
         static_cast<const float*>(c.workspace), splits, c.M, c.N, static_cast<float*>(c.out),
         c.ldo, c.beta);
     g_launches.fetch_add(1, std::memory_order_relaxed);

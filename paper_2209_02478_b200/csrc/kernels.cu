@@ -383,7 +383,11 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
 }
 
 // sum over blocks of partial[nblk][W] -> out segments. 8 row-phases per
-// column, each summed in order, then combined in a fixed order: deterministic.
+// column; each thread sums its rows (b = y, y + 8, ...) strictly in order,
+// with up to 16 of those loads issued before any is added (the partials are
+// L2-resident: the kernel is load-latency-bound, and 72 blocks with four
+// loads in flight took ~6 us per launch); the 8 phases are then combined in a
+// fixed order: deterministic.
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial,
                                                               int nblk, int W, int seg, float* o0,
                                                               float* o1, float* o2) {
@@ -392,16 +396,16 @@ __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __res
   const int i = blockIdx.x * 32 + x;
   float s = 0.f;
   if (i < W) {
-    // four independent chains (four loads in flight per thread), combined in
-    // a fixed order: deterministic
-    float s4[4] = {0.f, 0.f, 0.f, 0.f};
+    constexpr int kU = 16;
     int b = y;
-    for (; b + 24 < nblk; b += 32) {
+    for (; b + 8 * (kU - 1) < nblk; b += 8 * kU) {
+      float v[kU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) s4[u] += partial[(size_t)(b + 8 * u) * W + i];
+      for (int u = 0; u < kU; ++u) v[u] = partial[(size_t)(b + 8 * u) * W + i];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) s += v[u];
     }
-    for (int u = 0; b < nblk; b += 8, ++u) s4[u & 3] += partial[(size_t)b * W + i];
-    s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    for (; b < nblk; b += 8) s += partial[(size_t)b * W + i];
   }
   red[y][x] = s;
   __syncthreads();
@@ -1225,16 +1229,29 @@ cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float
   return cudaGetLastError();
 }
 
-int colsum_row_blocks(int rows) {
+// 256-thread colsum_partial blocks resident per SM (36-40 registers, 8-16 KB smem)
+constexpr int kColsumBlocksPerSm = 6;
+
+int colsum_row_blocks(int rows, int N) {
+  // one wave: a fixed 128 row blocks gave 1.1-1.5 waves at N = 2304 / 3072
+  // (the second, partial wave ran on a fraction of the SMs) and under-filled
+  // the machine at N = 768
   const int want = (rows + 31) / 32;
-  return want < 128 ? (want < 1 ? 1 : want) : 128;
+  const int ncol = (N + 255) / 256;
+  const int fill = std::max(1, kColsumBlocksPerSm * persistent_blocks() / ncol);
+  return std::max(1, std::min(want, fill));
+}
+
+int64_t colsum_scratch_bytes() {
+  // rb * G * N <= kColsumBlocksPerSm * SMs * 256 * G for every N, G <= 2
+  return (int64_t)kColsumBlocksPerSm * persistent_blocks() * 256 * 2 * 4 + 1024;
 }
 
 cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,
                    float* partial, float* out, cudaStream_t s) {
   if (N % 8 || ld % 8 || G < 1 || G > 2 || (G == 2 && groups == nullptr))
     return cudaErrorInvalidValue;
-  const int rb = colsum_row_blocks(rows);
+  const int rb = colsum_row_blocks(rows, N);
   ProfScope prof("mem_colsum", 0, 2.0 * rows * N, s);
   dim3 grid((N + 255) / 256, rb);
   if (G == 2 && groups != nullptr)

@@ -55,7 +55,12 @@ struct AdamWArgs {
 };
 
 int ln_bwd_blocks(int rows);
-int colsum_row_blocks(int rows);
+// row blocks of colsum over [rows][N]: one wave of the 256-thread partial
+// kernel (ceil(N / 256) column groups x row blocks ~ the resident blocks);
+// a function of (rows, N, SM count) only (deterministic partial layout)
+int colsum_row_blocks(int rows, int N);
+// scratch colsum needs for any (rows, N) and G <= 2
+int64_t colsum_scratch_bytes();
 int sumsq_blocks();
 
 cudaError_t add_ln_fwd(const LnFwdArgs& a, int H, cudaStream_t s);
@@ -65,7 +70,7 @@ cudaError_t embed_ln_fwd(const LnFwdArgs& a, int H, const int32_t* tok, const in
 cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float* dbias,
                    cudaStream_t s);
 // out[g][N] = sum over rows (with groups[r] == g) of x[r][:]; partial is
-// [colsum_row_blocks(rows)][G][N] scratch
+// [colsum_row_blocks(rows, N)][G][N] scratch (<= colsum_scratch_bytes())
 cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* groups, int G,
                    float* partial, float* out, cudaStream_t s);
 cudaError_t softmax_fwd(const void* scores, void* P, void* Pd, int64_t rows, int S, int ld,

@@ -205,10 +205,7 @@ Trainer::Trainer(mimose_ctx* ctx, const mimose_model_cfg& m, const mimose_train_
   const int64_t Tmax = (int64_t)t.batch * t.seq_max;
   const int lnb = mimose_ops::ln_bwd_blocks((int)Tmax);
   ln_partial_ = static_cast<float*>(take((int64_t)lnb * 3 * H_ * 4, kTagOther));
-  int64_t widest = std::max<int64_t>(std::max<int64_t>(3 * H_, F_), 2 * H_);
-  if (m.head == MIMOSE_HEAD_MLM) widest = std::max<int64_t>(widest, (m.vocab + 63) / 64 * 64);
-  col_partial_ =
-      static_cast<float*>(take((int64_t)mimose_ops::colsum_row_blocks((int)Tmax) * widest * 4 + 1024, kTagOther));
+  col_partial_ = static_cast<float*>(take(mimose_ops::colsum_scratch_bytes(), kTagOther));
   norm_partial_ = static_cast<float*>(take((int64_t)mimose_ops::sumsq_blocks() * 4, kTagOther));
   {
     // split-K workspace for the weight-gradient GEMMs (largest need over the shapes)
@@ -737,16 +734,23 @@ void* Trainer::attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, 
     ck(cudaEventRecord(side_ev_[0], s), "cudaEventRecord");
     ck(cudaStreamWaitEvent(side_, side_ev_[0], 0), "cudaStreamWaitEvent");
   }
-  if (kmask != nullptr) {
+  auto keep_bits = [&](cudaStream_t st) {
     ck(mimose_ops::flash_keep_mask(static_cast<uint32_t*>(kmask), S, ld, nh, g.B, fdrop,
-                                   m_.causal != 0, overlap ? side_ : s),
+                                   m_.causal != 0, st),
        "flash_keep_mask");
-    if (overlap) ck(cudaEventRecord(side_ev_[1], side_), "cudaEventRecord");
-  }
+  };
+  if (kmask != nullptr && !overlap) keep_bits(s);
   void* qkv = take(T * 3 * H * 2, act_tag);
   run_gemm(linear_call(x, W + P.wqkv.off, T, 3 * (int)H, (int)H, qkv, mimose_ops::kEpiBf16,
                        p32_ + P.bqkv.off),
            s);
+  if (overlap) {
+    // enqueued after the GEMM: its persistent CTAs take the SMs first and the
+    // ALU-bound keep-bit blocks fill the thread slots they leave (launched
+    // first, the keep-bit grid held every slot and the GEMM waited for it)
+    keep_bits(side_);
+    ck(cudaEventRecord(side_ev_[1], side_), "cudaEventRecord");
+  }
   if (flash) {
     // flash: ctx plus one fp32 log-sum-exp per row (and keep bits) instead of P / Pd
     if (overlap) ck(cudaStreamWaitEvent(s, side_ev_[1], 0), "cudaStreamWaitEvent");
