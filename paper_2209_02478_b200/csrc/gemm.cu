@@ -430,7 +430,10 @@ __global__ void gelu_regen_kernel(const __nv_bfloat16* __restrict__ u, __nv_bflo
     for (int q = 0; q < 4; ++q) {
       const float a = __uint_as_float(w[q] << 16), b = __uint_as_float(w[q] & 0xFFFF0000u);
       o[q] = tanh_form ? mimose_dev::pack_bf16x2(mimose_dev::gelu_tanh_f(a), mimose_dev::gelu_tanh_f(b))
-                       : mimose_dev::pack_bf16x2(mimose_dev::gelu_fast(a), mimose_dev::gelu_fast(b));
+                       : [&] {
+                           const float2 g = mimose_dev::gelu_fast2(make_float2(a, b));
+                           return mimose_dev::pack_bf16x2(g.x, g.y);
+                         }();
     }
     reinterpret_cast<uint4*>(g)[i] = out;
   }

@@ -158,29 +158,40 @@ __device__ __forceinline__ float erf_as(float z, float& ez2) {
 // and h = 0.5 * t * poly(t) * e = 0.5 * erfc(a):
 //   Phi(x) = x >= 0 ? 1 - h : h,   GELU(x) = x Phi(x),
 //   GELU'(x) = Phi(x) + x e / sqrt(2 pi).
-// 11-13 ALU ops + 2 MUFU per element (vs ~17 + 2 for the textbook form).
-__device__ __forceinline__ float gelu_half_erfc(float x, float& e) {
-  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.0f));
-  e = ex2_approx((-0.72134752044448170f * x) * x);  // -log2(e) / 2
+// Evaluated on PAIRS with the paired f32x2 instructions (FFMA2 / FMUL2: the
+// GELU / dGELU GEMM epilogues are issue-bound), 2 MUFU per element. Every
+// caller (GEMM epilogues, the u-only regeneration kernel) uses these pair
+// forms, so a regenerated g is bit-identical to the epilogue's.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 gelu_half_erfc2(float2 x, float2& e) {
+  const float2 ta = __ffma2_rn(f2(0.3275911f * 0.70710678118654752f),
+                               make_float2(fabsf(x.x), fabsf(x.y)), f2(1.0f));
+  const float2 t = make_float2(rcp_approx(ta.x), rcp_approx(ta.y));
+  const float2 ea = __fmul2_rn(__fmul2_rn(f2(-0.72134752044448170f), x), x);  // -log2(e) / 2
+  e = make_float2(ex2_approx(ea.x), ex2_approx(ea.y));
   // 0.5 * (A&S coefficients)
-  float poly = fmaf(0.5307027145f, t, -0.7265760135f);
-  poly = fmaf(poly, t, 0.7107068705f);
-  poly = fmaf(poly, t, -0.142248368f);
-  poly = fmaf(poly, t, 0.127414796f);
-  return (poly * t) * e;
+  float2 poly = __ffma2_rn(f2(0.5307027145f), t, f2(-0.7265760135f));
+  poly = __ffma2_rn(poly, t, f2(0.7107068705f));
+  poly = __ffma2_rn(poly, t, f2(-0.142248368f));
+  poly = __ffma2_rn(poly, t, f2(0.127414796f));
+  return __fmul2_rn(__fmul2_rn(poly, t), e);
 }
-__device__ __forceinline__ float gelu_fast(float x) {
-  float e;
-  const float h = gelu_half_erfc(x, e);
-  const float xh = x * h;
-  return x >= 0.f ? x - xh : xh;
+__device__ __forceinline__ float2 gelu_fast2(float2 x) {
+  float2 e;
+  const float2 h = gelu_half_erfc2(x, e);
+  const float2 xh = __fmul2_rn(x, h);
+  const float2 d = __ffma2_rn(xh, f2(-1.0f), x);  // x - xh (the product by -1 is exact)
+  return make_float2(x.x >= 0.f ? d.x : xh.x, x.y >= 0.f ? d.y : xh.y);
 }
-__device__ __forceinline__ float dgelu_fast(float x) {
-  float e;
-  const float h = gelu_half_erfc(x, e);
-  const float cdf = x >= 0.f ? 1.0f - h : h;
-  return fmaf(x * 0.39894228040143268f, e, cdf);
+__device__ __forceinline__ float2 dgelu_fast2(float2 x) {
+  float2 e;
+  const float2 h = gelu_half_erfc2(x, e);
+  const float2 omh = __ffma2_rn(h, f2(-1.0f), f2(1.0f));  // 1 - h
+  const float2 cdf = make_float2(x.x >= 0.f ? omh.x : h.x, x.y >= 0.f ? omh.y : h.y);
+  return __ffma2_rn(__fmul2_rn(x, f2(0.39894228040143268f)), e, cdf);
 }
+__device__ __forceinline__ float gelu_fast(float x) { return gelu_fast2(make_float2(x, x)).x; }
+__device__ __forceinline__ float dgelu_fast(float x) { return dgelu_fast2(make_float2(x, x)).x; }
 
 #ifdef MIMOSE_GELU_ERFF  // libm erff variant (A/B timing only)
 __device__ __forceinline__ float gelu_f(float x) {
@@ -248,10 +259,12 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
 #pragma unroll
         for (int q = 0; q < NV / 4; ++q) {
           const float4 b = __ldg(reinterpret_cast<const float4*>(bias_t) + q);  // warp-uniform
-          v[4 * q] += b.x;
-          v[4 * q + 1] += b.y;
-          v[4 * q + 2] += b.z;
-          v[4 * q + 3] += b.w;
+          const float2 lo = __fadd2_rn(make_float2(v[4 * q], v[4 * q + 1]), make_float2(b.x, b.y));
+          const float2 hi = __fadd2_rn(make_float2(v[4 * q + 2], v[4 * q + 3]), make_float2(b.z, b.w));
+          v[4 * q] = lo.x;
+          v[4 * q + 1] = lo.y;
+          v[4 * q + 2] = hi.x;
+          v[4 * q + 3] = hi.y;
         }
       } else {
 #pragma unroll
@@ -291,11 +304,20 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
           const uint4 raw = aux_pre != nullptr ? aux_pre[q]
                                                : *reinterpret_cast<const uint4*>(ax + 8 * q);
           const __nv_bfloat16* av = reinterpret_cast<const __nv_bfloat16*>(&raw);
+          if constexpr (EPI == kEpiBf16) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const float a = __bfloat162float(av[i]);
-            if constexpr (EPI == kEpiBf16) v[8 * q + i] += a;
-            else v[8 * q + i] *= p.gelu_tanh ? dgelu_tanh_f(a) : dgelu_fast(a);
+            for (int i = 0; i < 8; ++i) v[8 * q + i] += __bfloat162float(av[i]);
+          } else if (p.gelu_tanh) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * q + i] *= dgelu_tanh_f(__bfloat162float(av[i]));
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 d = dgelu_fast2(make_float2(__bfloat162float(av[i]), __bfloat162float(av[i + 1])));
+              const float2 r = __fmul2_rn(make_float2(v[8 * q + i], v[8 * q + i + 1]), d);
+              v[8 * q + i] = r.x;
+              v[8 * q + i + 1] = r.y;
+            }
           }
         }
       } else {
@@ -325,7 +347,11 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
       for (int i = 0; i < NV; ++i) g[i] = gelu_tanh_f(v[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < NV; ++i) g[i] = gelu_fast(v[i]);
+      for (int i = 0; i < NV; i += 2) {
+        const float2 r = gelu_fast2(make_float2(v[i], v[i + 1]));
+        g[i] = r.x;
+        g[i + 1] = r.y;
+      }
     }
   }
 }
