@@ -263,11 +263,14 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     ln_bwd_load<DY2, DRES>(a, row * H + col, cur);
     st_cur = reinterpret_cast<const float2*>(a.stats)[row];
   }
-  for (int it = 0; row < a.rows; row += step, ++it) {
-    const int64_t idx = row * H + col;
+  // element index of this thread's chunk, advanced by a constant per row
+  // (no 64-bit row * H products in the loop)
+  int64_t idx = row * H + col;
+  const int64_t didx = step * H;
+  for (int it = 0; row < a.rows; row += step, ++it, idx += didx) {
     const int64_t nrow = row + step;
     if (nrow < a.rows) {  // prefetch the next row of this group
-      ln_bwd_load<DY2, DRES>(a, nrow * H + col, nxt);
+      ln_bwd_load<DY2, DRES>(a, idx + didx, nxt);
       st_nxt = reinterpret_cast<const float2*>(a.stats)[nrow];
     }
     float zz[8], dy[8];
@@ -285,8 +288,6 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
 #pragma unroll
       for (int e = 0; e < 8; ++e) dy[e] = philox_keep(ph, e, thr_hi) ? dy[e] * a.in_drop.scale : 0.f;
     }
-    float s1 = 0.f, s2 = 0.f;
-    float xh[8];  // x-hat, reused below
     if (!from_y) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
@@ -294,13 +295,21 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
         xb[e] = -st_cur.x * st_cur.y;
       }
     }
+    // paired f32x2 math (FFMA2 / FMUL2 / FADD2) over the 8 columns:
+    // x-hat, g = dy * gamma and the two row sums (two paired chains each)
+    float xh[8], gg[8];
+    float2 s1p = make_float2(0.f, 0.f), s2p = s1p;
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      xh[e] = fmaf(zz[e], xa[e], xb[e]);
-      const float gg = dy[e] * gam[e];
-      s1 += gg;
-      s2 += gg * xh[e];
+    for (int e = 0; e < 8; e += 2) {
+      const float2 x2 = __ffma2_rn(make_float2(zz[e], zz[e + 1]), make_float2(xa[e], xa[e + 1]),
+                                   make_float2(xb[e], xb[e + 1]));
+      const float2 g2 = __fmul2_rn(make_float2(dy[e], dy[e + 1]), make_float2(gam[e], gam[e + 1]));
+      s1p = __fadd2_rn(s1p, g2);
+      s2p = __ffma2_rn(g2, x2, s2p);
+      xh[e] = x2.x; xh[e + 1] = x2.y;
+      gg[e] = g2.x; gg[e + 1] = g2.y;
     }
+    float s1 = s1p.x + s1p.y, s2 = s2p.x + s2p.y;
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     if constexpr (WPR > 1) {
@@ -317,12 +326,20 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
     }
     const float mg = s1 * (1.f / H);
     const float mgx = s2 * (1.f / H);
+    // dz = rstd * (g - mean(g) - x-hat * mean(g x-hat)); gamma / beta partials
     float dz[8];
+    const float2 rs2 = make_float2(st_cur.y, st_cur.y), nmg2 = make_float2(-mg, -mg);
+    const float2 nmgx2 = make_float2(-mgx, -mgx);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      dz[e] = st_cur.y * (dy[e] * gam[e] - mg - xh[e] * mgx);
-      acc_g[e] += dy[e] * xh[e];
-      acc_b[e] += dy[e];
+    for (int e = 0; e < 8; e += 2) {
+      const float2 x2 = make_float2(xh[e], xh[e + 1]), d2 = make_float2(dy[e], dy[e + 1]);
+      const float2 t2 = __ffma2_rn(x2, nmgx2, __fadd2_rn(make_float2(gg[e], gg[e + 1]), nmg2));
+      const float2 z2 = __fmul2_rn(rs2, t2);
+      dz[e] = z2.x; dz[e + 1] = z2.y;
+      const float2 ag = __ffma2_rn(d2, x2, make_float2(acc_g[e], acc_g[e + 1]));
+      const float2 ab = __fadd2_rn(make_float2(acc_b[e], acc_b[e + 1]), d2);
+      acc_g[e] = ag.x; acc_g[e + 1] = ag.y;
+      acc_b[e] = ab.x; acc_b[e + 1] = ab.y;
     }
     if constexpr (DRES) {
       float rr[8];
@@ -354,14 +371,27 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
       const uint32_t thr_hi = a.br_drop.threshold << 16;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        db[e] = bf16r(philox_keep(ph, e, thr_hi) ? dzr[e] * a.br_drop.scale : 0.f);
+        db[e] = philox_keep(ph, e, thr_hi) ? dzr[e] * a.br_drop.scale : 0.f;
     } else {
 #pragma unroll
-      for (int e = 0; e < 8; ++e) db[e] = bf16r(dzr[e] * a.br_drop.scale);
+      for (int e = 0; e < 8; ++e) db[e] = dzr[e] * a.br_drop.scale;
     }
+    // the branch gradient rounded to bf16 once: the stored words, widened
+    // back, are also what the bias gradient sums (= bf16r(db) before)
+    uint4 dbp;
+    {
+      uint32_t* hw = reinterpret_cast<uint32_t*>(&dbp);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) acc_d[e] += db[e];
-    if (a.dbr != nullptr) store8(static_cast<bf16*>(a.dbr) + idx, db);
+      for (int q = 0; q < 4; ++q) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(db[2 * q], db[2 * q + 1]);
+        hw[q] = *reinterpret_cast<uint32_t*>(&h);
+        const float2 r2 = make_float2(__uint_as_float(hw[q] << 16), __uint_as_float(hw[q] & 0xFFFF0000u));
+        const float2 ad = __fadd2_rn(make_float2(acc_d[2 * q], acc_d[2 * q + 1]), r2);
+        acc_d[2 * q] = ad.x;
+        acc_d[2 * q + 1] = ad.y;
+      }
+    }
+    if (a.dbr != nullptr) *reinterpret_cast<uint4*>(static_cast<bf16*>(a.dbr) + idx) = dbp;
     cur = nxt;
     st_cur = st_nxt;
   }

@@ -51,6 +51,19 @@ def main():
                                         workspace=ws, split_k=sk))
                 line.append(f"s{sk}:{ms*1e3:6.1f}")
             print(f"wgrad {m}x{n}x{T}: " + "  ".join(line) + "  (us; s0 = cost model)")
+    if "--direct" in sys.argv:
+        # epilogue output path: smem staging + TMA store (default) vs per-thread
+        # global stores (no staging traffic in shared memory)
+        for name, mk in (
+                ("ffn1 gelu", lambda d: ops.gemm(X, W1, out_f, epi=ops.EPI_BIAS_GELU, out2=out2,
+                                                 bias=b1, direct_store=d)),
+                ("ffn1 plain", lambda d: ops.gemm(X, W1, out_f, direct_store=d)),
+                ("dgelu", lambda d: ops.gemm(dY, W2, out_f, b_mn=True, epi=ops.EPI_DGELU, aux=U,
+                                             direct_store=d))):
+            for d in (False, True):
+                ms = t(lambda: mk(d))
+                print(f"{name:10s} direct={int(d)}: {ms*1e3:8.1f} us  "
+                      f"{2 * T * F * H / ms / 1e9:8.1f} TFLOP/s")
     if "--variants" in sys.argv:
         # epilogue-warp count x CTA pairing for the epilogue-heavy shapes
         for cg in (1, 2):
