@@ -429,9 +429,13 @@ RunOut run_gpu(const Opts& o, const std::string& planner, const std::string& bud
       mimose_step_report rep{};
       if (mimose_trainer_step(tr, b.tok.data(), b.typ.data(), b.lab.data(), B,
                               static_cast<int>(s), stream, &rep) != 0) {
-        // a step the arena could not hold: nothing recorded, counted here
+        const std::string e = mimose_last_error();
+        // a step the arena could not hold: nothing recorded (the trainer
+        // released its blocks), counted here; any other failure is an error
+        if (e.find("budget exceeded") == std::string::npos)
+          throw Fail("mimose_trainer_step (S=" + std::to_string(s) + "): " + e);
         ++out.failed;
-        std::cerr << "step failed (S=" << s << "): " << mimose_last_error() << "\n";
+        std::cerr << "step failed (S=" << s << "): " << e << "\n";
       }
     }
     char *sum = nullptr, *csv = nullptr, *txt = nullptr;
@@ -496,7 +500,16 @@ int cmd_compare(const Opts& o) {
   if (budgets.empty()) throw Fail("--budgets is required");
   for (const auto& b : budgets)
     for (const auto& p : split(o.planners)) {
-      const RunOut r = run_gpu(o, p, b);
+      RunOut r;
+      try {
+        r = run_gpu(o, p, b);
+      } catch (const Infeasible& e) {
+        // this cell's budget cannot hold the model: an empty row, exit 2
+        std::cerr << "infeasible (" << p << ", " << b << "): " << e.what() << "\n";
+        out << p << ',' << parse_bytes(b) << ",,,,,,,,,\n";
+        code = kInfeasible;
+        continue;
+      }
       const auto f = [&](const char* k) { return summary_field(r.summary, k); };
       out << p << ',' << f("budget_bytes") << ',' << f("total_time_ms") << ','
           << f("mean_peak_bytes") << ',' << f("recompute_total_ms") << ','

@@ -162,3 +162,10 @@ def test_compare_fit_and_infeasible_exit(cli, cuda_device, tmp_path):
     code, out, err = run(cli, "run", *COMMON, "--planner", "mimose", "--budget", "64m",
                          "--iters", 14, "--seed", 13, "--format", "summary")
     assert code == 2, (code, out, err)
+    # in a grid the infeasible cell is an empty row, the others still run
+    code, out, err = run(cli, "compare", *COMMON, "--budgets", "64m,2g", "--planners", "mimose",
+                         "--iters", 12, "--seed", 5)
+    assert code == 2, (code, out, err)
+    rows = [ln.split(",") for ln in out.strip().splitlines()[1:]]
+    assert [r[1] for r in rows] == [str(64 << 20), str(2 << 30)]
+    assert rows[0][2] == "" and rows[1][2] != ""
