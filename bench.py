@@ -73,11 +73,17 @@ def parse():
     ap.add_argument("--seed", type=int, default=2024)
     ap.add_argument("--no-baseline", action="store_true", help="skip no-ckpt throughput arm")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
-    ap.add_argument("--size-stream", default="per-rank", choices=["shared", "per-rank"],
-                    help="DP length policy: 'shared' = every rank draws S from the same seeded "
-                         "stream (length-synchronised sampling, no stragglers; data differs per "
-                         "rank); 'per-rank' = seed base+rank (independent lengths, max-over-"
-                         "ranks straggler cost)")
+    ap.add_argument("--size-stream", default="grouped", choices=["shared", "per-rank", "grouped"],
+                    help="DP length policy: 'grouped' (default) = length-grouped per-rank "
+                         "sampling: every step's length group comes from the seeded reference "
+                         "stream and each rank draws its own S within +-GROUP_JITTER of it from "
+                         "its own RNG (seed base+rank), so ranks train different lengths under "
+                         "their own plans without waiting for the longest of N independent "
+                         "draws (HF group_by_length practice); 'per-rank' = independent "
+                         "streams seed base+rank (max-over-ranks straggler cost); 'shared' = "
+                         "every rank the same S")
+    ap.add_argument("--group-jitter", type=float, default=0.05,
+                    help="relative per-rank spread of S inside a length group ('grouped')")
     ap.add_argument("--attn", default="flash", choices=["flash", "materialised"],
                     help="attention kernels of the measured runs: flash (attn_fused 3, no S x S "
                          "tensor) or materialised (attn_fused 2, P / Pd saved like the reference "
@@ -167,6 +173,17 @@ def sizes_for(dist, batch, iters, seed):
     from paper_2209_02478_b200 import planner
     xs = planner.host_lib().workload(dist, 1, iters, seed)
     return [int(x) for x in xs]
+
+
+def group_jitter(seqs, dist, jitter, seed):
+    """Length-grouped per-rank sizes: S_r = round(S * (1 + u)), u ~ U(-jitter,
+    jitter) from the rank's own RNG, clamped to the distribution's [LO, HI]
+    (the last two fields of uniform:LO:HI | normal:MU:SIGMA:LO:HI | ...)."""
+    f = dist.split(":")
+    lo, hi = int(f[-2]), int(f[-1])
+    g = np.random.default_rng(seed)
+    u = g.uniform(-jitter, jitter, size=len(seqs))
+    return [int(min(hi, max(lo, round(s * (1.0 + d))))) for s, d in zip(seqs, u)]
 
 
 def peaks():
@@ -425,9 +442,12 @@ def run_gpu_arm(args, rank, world, local):
     budget = int(args.budget_frac * peak_none)
 
     n_total = args.warmup + args.steps
-    # sizes: reference sampler; 'per-rank' seeds base + rank, 'shared' seeds base
+    # sizes: reference sampler; 'per-rank' seeds base + rank, 'shared' /
+    # 'grouped' seed base ('grouped' then jitters each step's S per rank)
     seqs = sizes_for(args.dist, B, 10_000,
                      args.seed + (rank if args.size_stream == "per-rank" else 0))
+    if args.size_stream == "grouped":
+        seqs = group_jitter(seqs, args.dist, args.group_jitter, args.seed + 7919 * (rank + 1))
 
     def batches(seq_list, seed):
         g = np.random.default_rng(seed)
@@ -693,6 +713,7 @@ def run_gpu_arm(args, rank, world, local):
                 "workload": PRESET_INFO[args.preset][0],
                 "global_batch": B * world, "seq_len": args.dist, "parallelism": f"dp{world}",
                 "dp_size_stream": args.size_stream,
+                **({"dp_group_jitter": args.group_jitter} if args.size_stream == "grouped" else {}),
                 "budget_frac_of_no_ckpt_peak": args.budget_frac, "budget_bytes": budget,
                 "no_ckpt_peak_bytes": peak_none, "seed": args.seed,
                 "attention": args.attn,
