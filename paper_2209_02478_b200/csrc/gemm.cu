@@ -379,14 +379,17 @@ bool make_output_map(CUtensorMap* map, void* ptr, int64_t rows, int64_t cols, in
 }
 
 // split-K count by a small cost model: mainloop time ~ waves * k-blocks per
-// split (one k-block of a 128x256 tile or a 256x256 pair tile ~ 512 tensor
-// cycles ~ 0.27 us), plus writing and re-reading the fp32 partials at HBM
-// speed. Keeps >= 8 k-blocks per split.
+// split (one k-block of a 128x256 tile per SM or a 256x256 pair tile per pair:
+// ~0.45 us measured at the sustained clocks, tools/bench_gemm.py --splitk;
+// the nominal 0.27 us made the model under-weight an extra wave and pick 2
+// splits for the 2304 x 768 QKV weight gradient, 66 us, where 5 run 62),
+// plus writing and re-reading the fp32 partials at HBM speed. Keeps >= 8
+// k-blocks per split.
 int pick_split_k(int M, int N, int K, int bn, int cg) {
   const int64_t tiles = (int64_t)((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
   const int64_t slots = sm_count() / cg;
   const int kb = (K + 63) / 64;
-  const double t_kb = 0.27e-6 * bn / 256.0, hbm = 6.0e12;
+  const double t_kb = 0.45e-6 * bn / 256.0, hbm = 6.0e12;
   auto cost = [&](int s) {
     const int64_t waves = (tiles * s + slots - 1) / slots;
     const double main = (double)waves * ((kb + s - 1) / s) * t_kb;
