@@ -12,6 +12,13 @@ timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > $O/bench_ref
 timeout 1200 bash tools/gpu_profile.sh $TAG bert-base-mc 288 40 > $O/gpu_profile.log 2>&1; echo "profile rc=$?" >> $O/status.txt
 mv gpurun_out/prof_${TAG}_* $O/ 2>/dev/null
 for P in 0 0.1; do timeout 600 python tools/bench_flash.py --p $P --classes --json $O/flash_p$P.json > /dev/null 2>&1; done
+# ncu of the flash kernels at the BERT-base and the long-sequence shape
+for SH in 64x12x288 8x16x1024; do
+  timeout 900 bash tools/ncu_flash.sh ${TAG}_$SH $SH 0.1 > /dev/null 2>&1
+  timeout 900 bash tools/ncu_flash_bwd.sh ${TAG}_$SH $SH 0.1 > /dev/null 2>&1
+done
+mv gpurun_out/fl_${TAG}_* gpurun_out/flb_${TAG}_* $O/ 2>/dev/null
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/status.txt
 timeout 1800 bash tools/sanitize.sh > $O/sanitize.log 2>&1; mv gpurun_out/san_* $O/ 2>/dev/null
 STEPS=30 timeout 2400 bash tools/bench_matrix.sh $TAG > $O/matrix_status.txt 2>&1; mv gpurun_out/bm_${TAG}_* $O/ 2>/dev/null
 for U in 1 0; do timeout 600 python tools/budget_sweep.py --unit $U --out $O/budget_sweep_u$U.json > /dev/null 2>&1; done
