@@ -53,22 +53,24 @@ __device__ __forceinline__ void ln_row_finish(float (&z)[VPL][8], int row, int l
     }
     return;
   }
-  // z arrives already rounded to bf16 (what is saved is what is normalised)
-  float s = 0.f;
+  // z arrives already rounded to bf16 (what is saved is what is normalised);
+  // row sums on paired f32x2 instructions (two independent chains each)
+  float2 s2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int c = 0; c < VPL; ++c)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) s += z[c][e];
-  const float mean = warp_sum(s) * (1.f / H);
-  float q = 0.f;
+    for (int e = 0; e < 8; e += 2) s2 = __fadd2_rn(s2, make_float2(z[c][e], z[c][e + 1]));
+  const float mean = warp_sum(s2.x + s2.y) * (1.f / H);
+  float2 q2 = make_float2(0.f, 0.f);
+  const float2 nm2 = make_float2(-mean, -mean);
 #pragma unroll
   for (int c = 0; c < VPL; ++c)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float d = z[c][e] - mean;
-      q += d * d;
+    for (int e = 0; e < 8; e += 2) {
+      const float2 d = __fadd2_rn(make_float2(z[c][e], z[c][e + 1]), nm2);
+      q2 = __ffma2_rn(d, d, q2);
     }
-  const float var = warp_sum(q) * (1.f / H);
+  const float var = warp_sum(q2.x + q2.y) * (1.f / H);
   const float rstd = rsqrtf(var + a.eps);
   if (a.stats != nullptr && lane == 0)
     reinterpret_cast<float2*>(a.stats)[row] = make_float2(mean, rstd);
@@ -84,10 +86,14 @@ __device__ __forceinline__ void ln_row_finish(float (&z)[VPL][8], int row, int l
     *reinterpret_cast<float4*>(b) = b4[0];
     *reinterpret_cast<float4*>(b + 4) = b4[1];
     const uint32_t m = dropout_mask8(a.out_drop, idx);
+    const float2 rs2 = make_float2(rstd, rstd);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float v = (z[c][e] - mean) * rstd * g[e] + b[e];
-      y[e] = ((m >> e) & 1u) ? v * a.out_drop.scale : 0.f;
+    for (int e = 0; e < 8; e += 2) {
+      // (z - mean) * rstd * gamma + beta, paired
+      const float2 xh = __fmul2_rn(__fadd2_rn(make_float2(z[c][e], z[c][e + 1]), nm2), rs2);
+      const float2 v = __ffma2_rn(xh, make_float2(g[e], g[e + 1]), make_float2(b[e], b[e + 1]));
+      y[e] = ((m >> e) & 1u) ? v.x * a.out_drop.scale : 0.f;
+      y[e + 1] = ((m >> (e + 1)) & 1u) ? v.y * a.out_drop.scale : 0.f;
     }
     store8(static_cast<bf16*>(a.y) + idx, y);
   }
