@@ -175,17 +175,6 @@ def sizes_for(dist, batch, iters, seed):
     return [int(x) for x in xs]
 
 
-def group_jitter(seqs, dist, jitter, seed):
-    """Length-grouped per-rank sizes: S_r = round(S * (1 + u)), u ~ U(-jitter,
-    jitter) from the rank's own RNG, clamped to the distribution's [LO, HI]
-    (the last two fields of uniform:LO:HI | normal:MU:SIGMA:LO:HI | ...)."""
-    f = dist.split(":")
-    lo, hi = int(f[-2]), int(f[-1])
-    g = np.random.default_rng(seed)
-    u = g.uniform(-jitter, jitter, size=len(seqs))
-    return [int(min(hi, max(lo, round(s * (1.0 + d))))) for s, d in zip(seqs, u)]
-
-
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -444,10 +433,12 @@ def run_gpu_arm(args, rank, world, local):
     n_total = args.warmup + args.steps
     # sizes: reference sampler; 'per-rank' seeds base + rank, 'shared' /
     # 'grouped' seed base ('grouped' then jitters each step's S per rank)
-    seqs = sizes_for(args.dist, B, 10_000,
-                     args.seed + (rank if args.size_stream == "per-rank" else 0))
     if args.size_stream == "grouped":
-        seqs = group_jitter(seqs, args.dist, args.group_jitter, args.seed + 7919 * (rank + 1))
+        from paper_2209_02478_b200.dp import rank_sizes_grouped
+        seqs = rank_sizes_grouped(args.dist, 10_000, args.seed, rank, args.group_jitter)
+    else:
+        seqs = sizes_for(args.dist, B, 10_000,
+                         args.seed + (rank if args.size_stream == "per-rank" else 0))
 
     def batches(seq_list, seed):
         g = np.random.default_rng(seed)

@@ -27,6 +27,23 @@ def rank_sizes(dist: str, iterations: int, base_seed: int, rank: int) -> List[in
     return [int(s) for s in host_lib().workload(dist, 1, iterations, base_seed + rank)]
 
 
+def rank_sizes_grouped(dist: str, iterations: int, base_seed: int, rank: int,
+                       jitter: float = 0.05) -> List[int]:
+    """Length-grouped per-rank sequence lengths: every step's length group is
+    the reference sampler's size (seed base, shared by all ranks); each rank
+    draws its own S within +-jitter of it from its own RNG and clamps to the
+    distribution's [LO, HI] (the last two fields of the spec). Ranks train
+    different lengths under their own plans without every step waiting for
+    the longest of N independent draws (HF Trainer group_by_length)."""
+    from .planner import host_lib
+    shared = [int(s) for s in host_lib().workload(dist, 1, iterations, base_seed)]
+    f = dist.split(":")
+    lo, hi = int(f[-2]), int(f[-1])
+    g = np.random.default_rng(base_seed + 7919 * (rank + 1))
+    u = g.uniform(-jitter, jitter, size=len(shared))
+    return [int(min(hi, max(lo, round(s * (1.0 + d))))) for s, d in zip(shared, u)]
+
+
 def allreduce_sum_(tensor, group=None):
     """In-place sum across ranks (NCCL for CUDA tensors, gloo for CPU)."""
     import torch.distributed as dist

@@ -67,3 +67,20 @@ def test_data_parallel_host_logic_world2():
     assert m0 != m1                      # ... and therefore plan differently
     assert g0 == g1 == [1.5, 1.5, 1.5]   # (1 + 2) / 2 on both ranks
     assert mx0 == mx1 == 20.0            # step time = slowest rank
+
+
+def test_length_grouped_rank_sizes():
+    """bench.py's default DP length policy: each rank its own S inside the
+    step's length group (the shared reference stream), +-jitter, clamped."""
+    from paper_2209_02478_b200 import dp, planner
+    shared = planner.host_lib().workload("uniform:64:512", 1, 200, 2024)
+    ranks = [dp.rank_sizes_grouped("uniform:64:512", 200, 2024, r, 0.05) for r in range(8)]
+    assert ranks[3] == dp.rank_sizes_grouped("uniform:64:512", 200, 2024, 3, 0.05)  # deterministic
+    for r in ranks:
+        assert all(64 <= s <= 512 for s in r)
+        assert all(abs(s - g) <= 0.05 * g + 1 for s, g in zip(r, shared))
+    # ranks differ (own mini-batch lengths) but stay grouped: the step's
+    # longest rank is within ~5 % of its mean (independent streams: ~1.6x)
+    assert any(ranks[0][i] != ranks[1][i] for i in range(200))
+    spread = [max(r[i] for r in ranks) / (sum(r[i] for r in ranks) / 8) for i in range(200)]
+    assert max(spread) < 1.06
