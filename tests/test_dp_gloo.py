@@ -80,7 +80,7 @@ def test_length_grouped_rank_sizes():
         assert all(64 <= s <= 512 for s in r)
         assert all(abs(s - g) <= 0.05 * g + 1 for s, g in zip(r, shared))
     # ranks differ (own mini-batch lengths) but stay grouped: the step's
-    # longest rank is within ~5 % of its mean (independent streams: ~1.6x)
+    # longest rank is within ~5-8 % of its mean (independent streams: ~1.6x)
     assert any(ranks[0][i] != ranks[1][i] for i in range(200))
     spread = [max(r[i] for r in ranks) / (sum(r[i] for r in ranks) / 8) for i in range(200)]
-    assert max(spread) < 1.06
+    assert max(spread) < 1.08
