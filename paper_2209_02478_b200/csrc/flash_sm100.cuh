@@ -88,8 +88,11 @@ __device__ __forceinline__ uint32_t fl_pack(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// named barrier `id` (1..15) over N threads
 template <int N>
-__device__ __forceinline__ void fl_epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void fl_bar(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(N) : "memory");
+}
 
 // Store one 64-byte segment per lane (lane = a row; c = its four 16-byte
 // chunks, dst = the row's segment, ok = the row exists) with coalesced warp
@@ -386,7 +389,9 @@ __global__ void __launch_bounds__(FlashFwdCfg<KB>::kThreads, FlashFwdCfg<KB>::kM
     auto finish = [&]() {
       mbar_wait(ofull, pend_tc & 1);
       tc_fence_after();
-      fl_epi_bar<32 * Cfg::kEW>();  // every warp has stored its slice statistics
+      // the quarter's NSL warps (the only writers of these rows' slice
+      // statistics) have stored them: one named barrier per lane quarter
+      fl_bar<32 * NSL>(1 + quarter);
       const float* xm = xch + (pend_tc & 1) * (2 * NSL * 128);
       const float* xl = xm + NSL * 128;
       float M = kNegInf;
