@@ -143,12 +143,14 @@ def test_run_matches_reference_replay_of_measured_profile(cli, cuda_device, tmp_
 def test_compare_fit_and_infeasible_exit(cli, cuda_device, tmp_path):
     # compare: the reference's grid CSV over planners x budgets
     code, out, err = run(cli, "compare", *COMMON, "--budgets", "2g,3g", "--planners",
-                         "mimose,none", "--iters", 12, "--seed", 5)
+                         "mimose,static-max,dtr,none", "--iters", 12, "--seed", 5)
     assert code == 0, err
     lines = out.strip().splitlines()
     assert lines[0].startswith("planner,budget_bytes,total_time_ms,mean_peak_bytes")
-    assert [ln.split(",")[0] for ln in lines[1:]] == ["mimose", "none", "mimose", "none"]
-    assert [int(ln.split(",")[1]) for ln in lines[1:]] == [2 << 30, 2 << 30, 3 << 30, 3 << 30]
+    assert [ln.split(",")[0] for ln in lines[1:]] == ["mimose", "static-max", "dtr", "none"] * 2
+    assert [int(ln.split(",")[1]) for ln in lines[1:]] == [2 << 30] * 4 + [3 << 30] * 4
+    # every cell ran all 12 iterations inside its budget (oom_risk column 0)
+    assert all(ln.split(",")[8] == "0" for ln in lines[1:])
     # fit: GPU-measured samples in the reference CSV format + an estimator dump
     code, _, err = run(cli, "fit", *COMMON, "--seed", 3, "--iters", 12, "--budget", "2g",
                        "--dump-estimator", "est.txt", "--dump-samples", "samples.csv",
