@@ -77,9 +77,32 @@ __device__ __forceinline__ bool mbar_try_wait_sleep(uint32_t addr, uint32_t pari
 // never completes (a pipeline bug) traps after ~2^36 cycles (~35 s) instead
 // of hanging; release builds wait (a preempted or time-sliced context must
 // not be killed by a clock-based trap).
+// MIMOSE_MBAR_WAIT_MODE: 1 (default) = plain try_wait retries (each try
+// blocks for the hardware's own time limit), the watchdog clock read once
+// per 1024 retries; 0 = retries with a suspend-time hint (NANOSLEEP.SYNCS,
+// woken by every barrier event of the SM: in the dK/dV kernel the waiting
+// warps' retry loops were 23 % of the executed instructions). Same-box A/B:
+// flash dQ -2 %, dK/dV / forward / GEMMs equal or slightly faster.
+#ifndef MIMOSE_MBAR_WAIT_MODE
+#define MIMOSE_MBAR_WAIT_MODE 1
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   if (mbar_try_wait(addr, parity)) return;
+#if MIMOSE_MBAR_WAIT_MODE == 1
+#ifdef MIMOSE_MBAR_WATCHDOG
+  const long long t0 = clock64();
+  for (;;) {
+#pragma unroll 1
+    for (int k = 0; k < 1024; ++k)
+      if (mbar_try_wait(addr, parity)) return;
+    if (clock64() - t0 > (1LL << 36)) __trap();
+  }
+#else
+  while (!mbar_try_wait(addr, parity)) {
+  }
+#endif
+#else
 #ifdef MIMOSE_MBAR_WATCHDOG
   const long long t0 = clock64();
   while (!mbar_try_wait_sleep(addr, parity)) {
@@ -88,6 +111,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #else
   while (!mbar_try_wait_sleep(addr, parity)) {
   }
+#endif
 #endif
 }
 
