@@ -418,37 +418,53 @@ __global__ void __launch_bounds__(LnBwdGeo<WPR>::THREADS, LnBwdGeo<WPR>::MINB)
   }
 }
 
-// sum over blocks of partial[nblk][W] -> out segments. 8 row-phases per
-// column; each thread sums its rows (b = y, y + 8, ...) strictly in order,
-// with up to 16 of those loads issued before any is added (the partials are
-// L2-resident: the kernel is load-latency-bound, and 72 blocks with four
-// loads in flight took ~6 us per launch); the 8 phases are then combined in a
-// fixed order: deterministic.
+// sum over blocks of partial[nblk][W] -> out segments. A block owns
+// kRedCols columns with 256 / kRedCols row phases each; each thread sums its
+// rows (b = y, y + P, ...) strictly in order, with up to 16 of those loads
+// issued before any is added (the partials are L2-resident: the kernel is
+// load-latency-bound -- 32 columns x 8 phases gave 72 blocks for W = 2304,
+// half the SMs, ~5.7 us per launch); the phases are then combined in a fixed
+// order (eight runs of P / 8, then the eight run sums): deterministic.
+constexpr int kRedCols = 8;
 __global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ partial,
                                                               int nblk, int W, int seg, float* o0,
                                                               float* o1, float* o2) {
-  __shared__ float red[8][33];
-  const int x = threadIdx.x & 31, y = threadIdx.x >> 5;
-  const int i = blockIdx.x * 32 + x;
+  constexpr int CW = kRedCols, P = 256 / CW;
+  __shared__ float red[P][CW + 1];
+  const int x = threadIdx.x % CW, y = threadIdx.x / CW;
+  const int i = blockIdx.x * CW + x;
   float s = 0.f;
   if (i < W) {
     constexpr int kU = 16;
     int b = y;
-    for (; b + 8 * (kU - 1) < nblk; b += 8 * kU) {
+    for (; b + P * (kU - 1) < nblk; b += P * kU) {
       float v[kU];
 #pragma unroll
-      for (int u = 0; u < kU; ++u) v[u] = partial[(size_t)(b + 8 * u) * W + i];
+      for (int u = 0; u < kU; ++u) v[u] = partial[(size_t)(b + P * u) * W + i];
 #pragma unroll
       for (int u = 0; u < kU; ++u) s += v[u];
     }
-    for (; b < nblk; b += 8) s += partial[(size_t)b * W + i];
+    float v[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) v[u] = b + P * u < nblk ? partial[(size_t)(b + P * u) * W + i] : 0.f;
+#pragma unroll
+    for (int u = 0; u < kU; ++u)
+      if (b + P * u < nblk) s += v[u];
   }
   red[y][x] = s;
+  __syncthreads();
+  constexpr int R = P / 8;
+  if (y < 8) {
+    float t = red[y * R][x];
+#pragma unroll
+    for (int k = 1; k < R; ++k) t += red[y * R + k][x];
+    red[y * R][x] = t;  // only this thread reads / writes rows y R .. y R + R - 1 of column x
+  }
   __syncthreads();
   if (y == 0 && i < W) {
     float t = red[0][x];
 #pragma unroll
-    for (int k = 1; k < 8; ++k) t += red[k][x];
+    for (int k = 1; k < 8; ++k) t += red[k * R][x];
     const int k = i / seg, j = i % seg;
     float* o = k == 0 ? o0 : (k == 1 ? o1 : o2);
     if (o != nullptr) o[j] = t;
@@ -1259,8 +1275,9 @@ cudaError_t ln_bwd(const LnBwdArgs& a, int H, float* dgamma, float* dbeta, float
   }
   count_launch();
   if (e != cudaSuccess) return e;
-  mimose_dev::reduce_partials_kernel<<<grid_for(3 * H, 32), 256, 0, s>>>(a.partial, nblk, 3 * H,
-                                                                        H, dgamma, dbeta, dbias);
+  using mimose_dev::kRedCols;
+  mimose_dev::reduce_partials_kernel<<<grid_for(3 * H, kRedCols), 256, 0, s>>>(
+      a.partial, nblk, 3 * H, H, dgamma, dbeta, dbias);
   count_launch();
   return cudaGetLastError();
 }
@@ -1297,7 +1314,8 @@ cudaError_t colsum(const void* x, int rows, int N, int64_t ld, const int32_t* gr
     mimose_dev::colsum_partial_kernel<1><<<grid, 256, 0, s>>>(static_cast<const bf16*>(x), rows, N,
                                                               ld, nullptr, partial);
   count_launch();
-  mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, 32), 256, 0, s>>>(
+  using mimose_dev::kRedCols;
+  mimose_dev::reduce_partials_kernel<<<grid_for((int64_t)G * N, kRedCols), 256, 0, s>>>(
       partial, rb, G * N, G * N, out, nullptr, nullptr);
   count_launch();
   return cudaGetLastError();
@@ -1521,8 +1539,9 @@ cudaError_t qa_head_bwd(const void* x, const float* dlogits, int T, int H, const
                                                       w, static_cast<bf16*>(dx), partial);
   count_launch();
   const int W = 2 * H + 2;
-  mimose_dev::reduce_partials_kernel<<<grid_for(W, 32), 256, 0, s>>>(partial, rb, W, 2 * H, dW,
-                                                                    db, nullptr);
+  using mimose_dev::kRedCols;
+  mimose_dev::reduce_partials_kernel<<<grid_for(W, kRedCols), 256, 0, s>>>(partial, rb, W, 2 * H,
+                                                                         dW, db, nullptr);
   count_launch();
   return cudaGetLastError();
 }
