@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define MIMOSE_ABI_VERSION 6
+#define MIMOSE_ABI_VERSION 7
 
 typedef struct mimose_ctx mimose_ctx;
 typedef struct mimose_trainer mimose_trainer;
@@ -97,6 +97,9 @@ typedef struct {
   int64_t workspace_bytes;
   int force_ew;      /* 0 = heuristic epilogue warps; 8 / 16 forces it */
   int force_cg;      /* 0 = heuristic; 1 = one SM per tile, 2 = CTA pair (cta_group::2) */
+  float* rowsum;     /* epi 3 with a_mn = 1, unbatched: also rowsum[m] = sum_k A[m][k]
+                        (fp32, overwritten: the bias gradient of a weight gradient);
+                        split-K then needs split_k * M * (N + 1) * 4 workspace bytes */
 } mimose_gemm_args;
 
 int mimose_gemm(const mimose_gemm_args* args, void* stream);

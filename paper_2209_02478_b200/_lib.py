@@ -65,6 +65,7 @@ class GemmArgs(C.Structure):
         ("force_bn", C.c_int), ("direct_store", C.c_int),
         ("split_k", C.c_int), ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64),
         ("force_ew", C.c_int), ("force_cg", C.c_int),
+        ("rowsum", C.c_void_p),
     ]
 
 
@@ -229,7 +230,7 @@ CUDA_SYMBOLS = [
       C.POINTER(C.c_int)]),
 ]
 
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 
 def _bind(lib, symbols):

@@ -151,6 +151,7 @@ int mimose_gemm(const mimose_gemm_args* a, void* stream) {
   c.split_k = a->split_k;
   c.workspace = a->workspace;
   c.workspace_bytes = a->workspace_bytes;
+  c.rowsum = a->rowsum;
   cudaError_t e = mimose_ops::gemm(c, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "mimose_gemm");
   return 0;

@@ -303,10 +303,21 @@ int pick_bn(const GemmCall& c) {
   return 128;
 }
 
-// out[m][n] (ld) = sum_s ws[s][m][n] (+ beta * out), fixed summation order
+// out[m][n] (ld) = sum_s ws[s][m][n] (+ beta * out), fixed summation order;
+// with rs_out: rs_out[m] = sum_s ws[splits * M * N + s * M + m] (row sums of A)
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
-                                     float* __restrict__ out, long long ldo, float beta) {
+                                     float* __restrict__ out, long long ldo, float beta,
+                                     float* __restrict__ rs_out) {
   const long long total = (long long)M * N;
+  if (rs_out != nullptr) {
+    const float* rs = ws + (long long)splits * total;
+    for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M;
+         m += (long long)gridDim.x * blockDim.x) {
+      float acc = rs[m];
+      for (int s = 1; s < splits; ++s) acc += rs[(long long)s * M + m];
+      rs_out[m] = acc;
+    }
+  }
   const bool v4 = (N % 4 == 0) && (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (v4 && ldo == N) {
     // dense output: linear index, no row / column division
@@ -415,7 +426,7 @@ int64_t splitk_workspace_bytes(int M, int N, int K) {
   c.workspace = &dummy;  // "a workspace will be provided"
   const int bn = pick_bn(c);
   int s = pick_split_k(M, N, K, bn, pick_cg(c, bn));
-  return s > 1 ? (int64_t)s * M * N * 4 : 0;
+  return s > 1 ? (int64_t)s * M * (N + 1) * 4 : 0;  // + [splits][M] row-sum partials
 }
 
 // g = GELU(u) over bf16 elements, with the GEMM epilogue's own device
@@ -468,13 +479,17 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   int ew = pick_ew(c, bn);
   const int cg = pick_cg(c, bn);
   if (cg == 2) ew = (c.epi == kEpiBiasGelu || c.epi == kEpiDGelu) ? 16 : 8;  // launch_pair
+  if (c.rowsum != nullptr &&
+      (c.epi != kEpiF32 || !c.a_mn || c.nb1 != 1 || c.nb2 != 1 || c.causal_k != 0 || c.causal_tiles))
+    return cudaErrorInvalidValue;
   int splits = 1;
   if (c.epi == kEpiF32 && c.nb1 == 1 && c.nb2 == 1 && c.workspace != nullptr && c.split_k != 1 &&
       c.N % 4 == 0 && (reinterpret_cast<uintptr_t>(c.workspace) & 15) == 0) {
     splits = c.split_k > 1 ? c.split_k : pick_split_k(c.M, c.N, c.K, bn, cg);
     const int kb = (c.K + 63) / 64;
     if (splits > kb) splits = kb;
-    while (splits > 1 && (int64_t)splits * c.M * c.N * 4 > c.workspace_bytes) --splits;
+    const int64_t per_split = (int64_t)c.M * (c.N + (c.rowsum != nullptr ? 1 : 0)) * 4;
+    while (splits > 1 && splits * per_split > c.workspace_bytes) --splits;
   }
   CUtensorMap ta, tb;
   if (!make_map(&ta, c.A, c.nb1, c.nb2, c.a_mn ? 64u : 128u)) return cudaErrorInvalidValue;
@@ -494,6 +509,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   p.causal_tiles = c.causal_tiles ? 1 : 0;
   p.causal_k = c.causal_k;
   if (c.causal_k != 0 && splits > 1) return cudaErrorInvalidValue;
+  p.rowsum = c.rowsum;
   if (c.drop.threshold != 0 && (c.epi != kEpiBf16 || c.nb1 != 1 || c.nb2 != 1 || c.N % 8 != 0))
     return cudaErrorInvalidValue;  // dropout index = row * ldo + col, 8-column groups
   {
@@ -511,6 +527,8 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     p.kb_per_split = kbps;
   }
   p.splits = splits;
+  if (c.rowsum != nullptr && splits > 1)  // per-split partials, summed by the reduce below
+    p.rowsum = static_cast<float*>(c.workspace) + (int64_t)splits * c.M * c.N;
   // output through TMA when the view is addressable (16 B pitch / batch strides)
   CUtensorMap td{}, td2{};
   if (splits > 1) {
@@ -588,7 +606,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   if (err == cudaSuccess && splits > 1) {
     splitk_reduce_kernel<<<4 * sm_count(), 256, 0, stream>>>(
         static_cast<const float*>(c.workspace), splits, c.M, c.N, static_cast<float*>(c.out),
-        c.ldo, c.beta);
+        c.ldo, c.beta, c.rowsum);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     err = cudaGetLastError();
   }

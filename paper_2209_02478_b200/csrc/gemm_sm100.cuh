@@ -59,6 +59,9 @@ struct GemmParams {
   int causal_k;             // causal contractions over S: 1 = only k <= row contributes
                             // (P V, dS K), 2 = only k >= row (P^T dO, dS^T Q); the
                             // k-blocks outside are exact zeros and are skipped
+  float* rowsum;            // kEpiF32, MN-major A: sums of A's rows over this split's K
+                            // range -> rowsum[split * M + m] (the bias gradient of a
+                            // weight-gradient GEMM, dY^T 1, read from the staged dY tiles)
 };
 
 constexpr int kBM = 128;
@@ -69,7 +72,12 @@ constexpr int kSmemBudget = 227 * 1024;
 // accumulator columns. 8 (column halves) by default; 16 (column quarters)
 // for the math-heavy GELU / dGELU epilogues and the write-bound attention
 // contractions, which would otherwise leave the tensor pipe idle.
-constexpr int gemm_threads(int EW) { return 64 + 32 * EW; }  // warp0 TMA, warp1 MMA, rest epilogue
+// warp 0 TMA, warp 1 MMA, EW epilogue warps; fp32 (weight-gradient) kernels
+// add kRsWarps A-row-sum warps after the epilogue warps
+constexpr int kRsWarps = 4;
+constexpr int gemm_threads(int EW, int EPI = -1) {
+  return 64 + 32 * EW + (EPI == kEpiF32 ? 32 * kRsWarps : 0);
+}
 
 // staged row chunk of one epilogue warp: 128 B (SWIZZLE_128B) or 64 B
 // (SWIZZLE_64B) when the warp's column span is narrower than 128 B or when
@@ -94,7 +102,7 @@ struct GemmCfg {
   static constexpr int kEsz = EPI == kEpiF32 ? 4 : 2;
   static constexpr int kEpiWarps = EW;
   static constexpr int kColParts = EW / 4;
-  static constexpr int kThreads = gemm_threads(EW);
+  static constexpr int kThreads = gemm_threads(EW, EPI);
   static constexpr int kChunkBytes = gemm_chunk_bytes(BN, EPI, EW);
   static constexpr int kChunkCols = kChunkBytes / kEsz;
   static constexpr int kBufBytes = 32 * kChunkBytes;  // 32 rows x one chunk
@@ -110,19 +118,21 @@ struct GemmCfg {
   // bias is read straight from global memory (uniform across the warp: one
   // L1 broadcast per float4) rather than staged per tile in shared memory
   static constexpr int kBiasBytes = 0;
+  // row-sum warps' per-tile combine: [kRsWarps][128] floats after the barriers
+  static constexpr int kRsBytes = EPI == kEpiF32 ? kRsWarps * 128 * 4 : 0;
   // 64-wide tiles (the streaming attention contractions, K = S) run two CTAs
   // per SM: two independent load / MMA / epilogue pipelines, each with half
   // the shared memory and TMEM
   static constexpr int kMinBlocks = (BN == 64 && EW == 8 && EPI == kEpiBf16 && CG == 1) ? 2 : 1;
   static constexpr int kStagesRaw =
-      (kSmemBudget / kMinBlocks - 1024 - 512 - kStagingBytes - kBiasBytes) / kStageBytes;
+      (kSmemBudget / kMinBlocks - 1024 - 512 - kStagingBytes - kBiasBytes - kRsBytes) / kStageBytes;
   // two-CTA-per-SM contractions measured fastest with 3 stages (S = 288
   // step, P.V / dV / dK / dQ: 2 stages 2.40 ms, 3 stages 2.12, 4 stages 2.69)
   static constexpr int kMaxStages = kMinBlocks == 2 ? 3 : 8;
   static constexpr int kStages = kStagesRaw > kMaxStages ? kMaxStages : kStagesRaw;
   static constexpr int kTmemCols = kAcc * BN;
   static constexpr int kSmemBytes =
-      kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 512;
+      kStages * kStageBytes + kStagingBytes + kBiasBytes + 1024 + 512 + kRsBytes;
   static_assert(kStages >= 2, "not enough shared memory for a pipeline");
 };
 
@@ -375,7 +385,7 @@ __device__ __forceinline__ unsigned long long clk64() {
 #endif
 
 template <int BN, int EPI, int EW, int CG>
-__global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::kMinBlocks))
+__global__ void __launch_bounds__(gemm_threads(EW, EPI), (GemmCfg<BN, EPI, EW, CG>::kMinBlocks))
     gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap tmA,
                         const __grid_constant__ CUtensorMap tmB,
                         const __grid_constant__ CUtensorMap tmD,
@@ -398,6 +408,11 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
   uint64_t* tempty = tfull + Cfg::kAcc;    // [kAcc]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + Cfg::kAcc);
   uint64_t* abar = tempty + Cfg::kAcc + 1;  // [EW][kBufs] aux-tile arrivals
+  uint64_t* rs_done = abar + kEpiWarps * Cfg::kBufs;  // [S] row-sum warps done with a stage
+  float* rs_red = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512);  // [4][128]
+  static_assert((2 * S + 2 * Cfg::kAcc + 1 + EW * Cfg::kBufs + S) * 8 <= 512,
+                "barrier block overflows its 512 B");
+  const bool rowsum = EPI == kEpiF32 && p.rowsum != nullptr;
 
   const int warp = threadIdx.x >> 5;
   const uint32_t lane = threadIdx.x & 31;
@@ -424,6 +439,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       mbar_init(&tempty[a], kEpiWarps * CG);  // one arrive per epilogue warp (of both CTAs)
     }
     for (int i = 0; i < kEpiWarps * Cfg::kBufs; ++i) mbar_init(&abar[i], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&rs_done[s], kRsWarps);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -463,6 +479,7 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph ^ 1);
+          if (rowsum) mbar_wait(&rs_done[s], ph ^ 1);  // the row-sum warp has read it too
           uint8_t* a_dst = sA + s * Cfg::kABytes;
           uint8_t* b_dst = sB + s * Cfg::kBBytes;
           const int k0 = kb * kBK;
@@ -571,6 +588,86 @@ __global__ void __launch_bounds__(gemm_threads(EW), (GemmCfg<BN, EPI, EW, CG>::k
       if (lane == 0 && local < 64) { GT(local * 8 + 1, GT_CLK()); GT(local * 8 + 2, fw); }
       ++local;
     }
+    }
+  } else if (EPI == kEpiF32 && warp >= 2 + EW) {
+    // ------------------------------------------------------------ A row sums
+    // (MN-major A = dY of a weight gradient: its rows' sums over K are the
+    // bias gradient). The kRsWarps warps follow the producer's stage
+    // sequence: a stage is read after the MMAs that consumed it completed
+    // (empty[s]: the commit reaches both CTAs of a pair) and handed back to
+    // the producer by rs_done[s]. Only the first column tile of each row
+    // block sums. Warp rw takes K rows [16 rw, 16 rw + 16) of the stage;
+    // lane l reads 16-byte chunk (l & 7) of 64-row block ((l >> 3) & 1) in
+    // rows of parity (l >> 4): 2 rows x 128 values per load, conflict free.
+    // Per tile: lanes l, l ^ 16 combine by shuffle, the warps through smem
+    // in a fixed order (deterministic).
+    if (rowsum) {
+      const int rw = warp - 2 - EW;
+      int it = 0;
+      const int j = (lane >> 3) & 1, c = lane & 7, r0 = lane >> 4;
+      for (int tile = blockIdx.x / CG; tile < num_tiles; tile += gridDim.x / CG) {
+        const int zz = tile / tiles_per_batch;
+        const int t_in = tile % tiles_per_batch;
+        const int split = zz % p.splits;
+        const int kb0 = split * p.kb_per_split;
+        const int kb1 = min(num_kb, kb0 + p.kb_per_split);
+        const bool active = t_in % tiles_n == 0;
+        float2 acc[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = make_float2(0.f, 0.f);
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
+          const int s = it % S;
+          const uint32_t ph = (it / S) & 1;
+          mbar_wait(&empty[s], ph);
+          if (active) {
+            const uint32_t base = smem_u32(sA + s * Cfg::kABytes) + j * 8192;
+            uint4 q[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int k = 16 * rw + 2 * i + r0;
+              q[i] = ld_shared_v4(base + k * 128 + ((c ^ (k & 7)) << 4));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const uint32_t w[4] = {q[i].x, q[i].y, q[i].z, q[i].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                acc[e] = __fadd2_rn(acc[e], make_float2(__uint_as_float(w[e] << 16),
+                                                        __uint_as_float(w[e] & 0xFFFF0000u)));
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&rs_done[s]);
+        }
+        if (active) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            acc[e].x += __shfl_xor_sync(0xffffffffu, acc[e].x, 16);
+            acc[e].y += __shfl_xor_sync(0xffffffffu, acc[e].y, 16);
+          }
+          const int col = j * 64 + c * 8;  // this lane's 8 row-sum slots
+          if (lane < 16) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              rs_red[rw * 128 + col + 2 * e] = acc[e].x;
+              rs_red[rw * 128 + col + 2 * e + 1] = acc[e].y;
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kRsWarps) : "memory");
+          if (rw == 0 && lane < 16) {
+            const int m = (t_in / tiles_n) * kTileM + (int)rank * kBM + col;
+            float* dst = p.rowsum + (size_t)split * p.M + m;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              float v = rs_red[col + e];
+#pragma unroll
+              for (int w2 = 1; w2 < kRsWarps; ++w2) v += rs_red[w2 * 128 + col + e];
+              if (m + e < p.M) dst[e] = v;
+            }
+          }
+          asm volatile("bar.sync 1, %0;" ::"n"(32 * kRsWarps) : "memory");  // rs_red reusable
+        }
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue

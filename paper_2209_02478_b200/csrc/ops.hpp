@@ -51,6 +51,12 @@ struct GemmCall {
   mimose_dev::DropoutCfg drop;    // kEpiBf16: dropout on the product before adding aux
   bool causal_tiles = false;      // skip tiles above the diagonal (causal S x S scores)
   int causal_k = 0;               // 1: only k <= row contributes, 2: only k >= row (causal)
+  // kEpiF32 with MN-major A, unbatched, not causal: also write the sums of
+  // A's rows over K to rowsum[M] (fp32, overwritten) -- the bias gradient
+  // of a weight-gradient GEMM (A = dY), summed from the staged operand
+  // tiles instead of a second pass over dY. Split-K partials take
+  // splits * M floats of `workspace` after the [splits][M][N] block.
+  float* rowsum = nullptr;
 };
 
 cudaError_t gemm(const GemmCall& c, cudaStream_t stream);

@@ -1174,9 +1174,13 @@ void* Trainer::ffn_half_bwd(int l, const void* h1, const void* y, const void* y_
   }
   drop(df);
   drop(sv.u);
-  ck(mimose_ops::colsum(du, (int)T, (int)F, F, nullptr, 1, col_partial_, G + P.b1.off, s), "colsum");
-  // FFN1: dW1 = du^T (FFN input)
-  run_gemm(wgrad_call(du, pre ? sv.z2 : h1, T, (int)F, (int)H, G + P.w1.off), s);
+  // FFN1: dW1 = du^T (FFN input); db1 = du^T 1 summed by the same GEMM from
+  // its staged du tiles (no second pass over du)
+  {
+    GemmCall c = wgrad_call(du, pre ? sv.z2 : h1, T, (int)F, (int)H, G + P.w1.off);
+    c.rowsum = G + P.b1.off;
+    run_gemm(c, s);
+  }
   void* dh1 = take(T * H * 2, kTagTransient);
   if (pre) {
     drop(sv.z2);
@@ -1246,10 +1250,13 @@ void* Trainer::attn_half_bwd(int l, const void* h, void* h1, void* h1_st, bool o
   drop(da);
   void* dqkv = attn_bwd(l, sv, dctx, g, s);
   if (fused == 3) drop(sv.ctx);
-  // QKV projection: dbqkv, dWqkv = dqkv^T xin
-  ck(mimose_ops::colsum(dqkv, (int)T, 3 * (int)H, 3 * H, nullptr, 1, col_partial_, G + P.bqkv.off, s),
-     "colsum");
-  run_gemm(wgrad_call(dqkv, pre ? sv.z1 : h, T, 3 * (int)H, (int)H, G + P.wqkv.off), s);
+  // QKV projection: dWqkv = dqkv^T xin, dbqkv = dqkv^T 1 (row sums of the
+  // GEMM's staged dqkv tiles)
+  {
+    GemmCall c = wgrad_call(dqkv, pre ? sv.z1 : h, T, 3 * (int)H, (int)H, G + P.wqkv.off);
+    c.rowsum = G + P.bqkv.off;
+    run_gemm(c, s);
+  }
   void* dx = take(T * H * 2, kTagTransient);
   if (pre) {
     // dx1 = dqkv Wqkv ; dx = LN1'(dx1) + d h1

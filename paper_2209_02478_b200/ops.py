@@ -37,11 +37,13 @@ def _view(t: torch.Tensor, nb1: int, nb2: int):
 
 def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None, bias=None,
          alpha=1.0, beta=0.0, force_bn=0, force_ew=0, force_cg=0, direct_store=False, split_k=1,
-         workspace=None, stream=None):
+         workspace=None, rowsum=None, stream=None):
     """out[z] = alpha * op(a)[z] @ op(b)[z]^T with the kernel's epilogue.
 
     a: [.., M, K] (a_mn False) or [.., K, M] (a_mn True); b: [.., N, K] or [.., K, N].
     out: [.., M, N] (bf16, or fp32 for EPI_F32).
+    rowsum: fp32 [M] (EPI_F32, a_mn, unbatched): also the sums of op(a)'s rows
+    over K (the bias gradient of a weight gradient).
     """
     nb2 = out.shape[0] if out.dim() == 4 else 1
     nb1 = out.shape[-3] if out.dim() >= 3 else 1
@@ -73,6 +75,9 @@ def gemm(a, b, out, *, a_mn=False, b_mn=False, epi=EPI_BF16, out2=None, aux=None
     if workspace is not None:
         args.workspace = workspace.data_ptr()
         args.workspace_bytes = workspace.numel() * workspace.element_size()
+    if rowsum is not None:
+        assert rowsum.dtype == torch.float32 and rowsum.numel() == M
+        args.rowsum = rowsum.data_ptr()
     lib = cuda_lib()
     check(lib.mimose_gemm(C.byref(args), _stream(stream)))
     return out

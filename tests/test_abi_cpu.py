@@ -41,7 +41,7 @@ def test_cuda_lib_exports_exactly_the_header():
     assert all(s.startswith("mimose_") for s in exp), [s for s in exp if not s.startswith("mimose_")]
     bound = {name for name, _, _ in _lib.CUDA_SYMBOLS}
     assert set(decl) == bound, set(decl) ^ bound
-    assert lib.mimose_abi_version() == _lib.ABI_VERSION == 6
+    assert lib.mimose_abi_version() == _lib.ABI_VERSION == 7
 
 
 def test_host_lib_exports_exactly_the_header():

@@ -181,3 +181,50 @@ def test_gemm_wgrad_split_k(cuda_device, split, shape):
     torch.cuda.synchronize()
     _check_f32(out, dY.float().t() @ X.float(), K)
     assert torch.equal(out, out2)  # run-to-run bitwise
+
+
+@pytest.mark.parametrize("cg", [0, 1, 2])
+@pytest.mark.parametrize("split", [0, 1, 2, 5])
+@pytest.mark.parametrize("shape", [(3072, 768, 18432), (2304, 768, 4096), (104, 200, 1000),
+                                   (768, 3072, 2560)])
+def test_gemm_wgrad_rowsum(cuda_device, cg, split, shape):
+    """Weight gradient + bias gradient in one GEMM: the extra warp's sums of the
+    staged dY tiles equal dY's column sums (fp32 over the same bf16 values),
+    dW is bitwise the GEMM without them, and both are run-to-run bitwise."""
+    ops = _ops()
+    torch.manual_seed(11)
+    M, N, K = shape
+    if cg == 2 and M <= 128:
+        pytest.skip("CTA pairs need M > 128")
+    dY = _rand(K, M)
+    X = _rand(K, N)
+    ws = torch.empty(8 * M * (N + 1), device="cuda")
+    kw = dict(a_mn=True, b_mn=True, epi=ops.EPI_F32, split_k=split, workspace=ws, force_cg=cg,
+              force_bn=256 if cg == 2 else 0)
+    ref_w = torch.empty(M, N, device="cuda")
+    ops.gemm(dY, X, ref_w, **kw)
+    outs = []
+    for _ in range(2):
+        w = torch.empty(M, N, device="cuda")
+        db = torch.full((M,), float("nan"), device="cuda")
+        ops.gemm(dY, X, w, rowsum=db, **kw)
+        outs.append((w, db))
+    torch.cuda.synchronize()
+    ref_b = dY.double().sum(0)
+    for w, db in outs:
+        assert torch.equal(w, ref_w)
+        err = (db.double() - ref_b).abs()
+        bound = 2e-6 * dY.double().abs().sum(0) + 1e-6
+        assert torch.all(err <= bound), f"max err {err.max().item()}"
+    assert torch.equal(outs[0][1], outs[1][1])
+
+
+def test_gemm_rowsum_rejects_unsupported(cuda_device):
+    ops = _ops()
+    A, B = _rand(256, 128), _rand(192, 128)
+    db = torch.empty(256, device="cuda")
+    with pytest.raises(Exception):  # K-major A has no row-sum path
+        ops.gemm(A, B, torch.empty(256, 192, device="cuda"), epi=ops.EPI_F32, rowsum=db)
+    with pytest.raises(Exception):  # bf16 epilogues neither
+        ops.gemm(A.t().contiguous(), B, torch.empty(256, 192, device="cuda", dtype=torch.bfloat16),
+                 a_mn=True, rowsum=db)

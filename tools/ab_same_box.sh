@@ -34,6 +34,10 @@ import csv, sys, collections, json
 agg = collections.Counter()
 for r in csv.DictReader(open(sys.argv[1])):
     agg[r["class"]] += float(r["ms"])
+    agg["total"] += float(r["ms"])
+    if r["class"] == "gemm_dense":  # per shape: M N K ... epi
+        d = r["desc"].split()
+        agg["  gemm " + " ".join(d[:3] + d[7:8])] += float(r["ms"])
 print(json.dumps(agg))
 PY
     done
