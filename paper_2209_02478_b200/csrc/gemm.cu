@@ -303,21 +303,29 @@ int pick_bn(const GemmCall& c) {
   return 128;
 }
 
+// rs_out[m] = sum_p rs[p * M + m], p = 0 .. nparts - 1 in order (row-sum partials)
+__device__ __forceinline__ void rowsum_parts(const float* __restrict__ rs, int nparts, int M,
+                                             float* __restrict__ rs_out) {
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M;
+       m += (long long)gridDim.x * blockDim.x) {
+    float acc = rs[m];
+    for (int q = 1; q < nparts; ++q) acc += rs[(long long)q * M + m];
+    rs_out[m] = acc;
+  }
+}
+__global__ void rowsum_reduce_kernel(const float* __restrict__ rs, int nparts, int M,
+                                     float* __restrict__ rs_out) {
+  rowsum_parts(rs, nparts, M, rs_out);
+}
+
 // out[m][n] (ld) = sum_s ws[s][m][n] (+ beta * out), fixed summation order;
-// with rs_out: rs_out[m] = sum_s ws[splits * M * N + s * M + m] (row sums of A)
+// with rs_out: rs_out[m] = sum of the rs_parts row-sum partials after the
+// [splits][M][N] block
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
                                      float* __restrict__ out, long long ldo, float beta,
-                                     float* __restrict__ rs_out) {
+                                     float* __restrict__ rs_out, int rs_parts) {
   const long long total = (long long)M * N;
-  if (rs_out != nullptr) {
-    const float* rs = ws + (long long)splits * total;
-    for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M;
-         m += (long long)gridDim.x * blockDim.x) {
-      float acc = rs[m];
-      for (int s = 1; s < splits; ++s) acc += rs[(long long)s * M + m];
-      rs_out[m] = acc;
-    }
-  }
+  if (rs_out != nullptr) rowsum_parts(ws + (long long)splits * total, rs_parts, M, rs_out);
   const bool v4 = (N % 4 == 0) && (ldo % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   if (v4 && ldo == N) {
     // dense output: linear index, no row / column division
@@ -426,7 +434,9 @@ int64_t splitk_workspace_bytes(int M, int N, int K) {
   c.workspace = &dummy;  // "a workspace will be provided"
   const int bn = pick_bn(c);
   int s = pick_split_k(M, N, K, bn, pick_cg(c, bn));
-  return s > 1 ? (int64_t)s * M * (N + 1) * 4 : 0;  // + [splits][M] row-sum partials
+  // split-K partials + [splits][tiles_n <= N / 64][M] row-sum partials (one
+  // per column tile)
+  return (int64_t)s * M * ((s > 1 ? N : 0) + (N + 63) / 64) * 4;
 }
 
 // g = GELU(u) over bf16 elements, with the GEMM epilogue's own device
@@ -488,7 +498,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     splits = c.split_k > 1 ? c.split_k : pick_split_k(c.M, c.N, c.K, bn, cg);
     const int kb = (c.K + 63) / 64;
     if (splits > kb) splits = kb;
-    const int64_t per_split = (int64_t)c.M * (c.N + (c.rowsum != nullptr ? 1 : 0)) * 4;
+    const int64_t per_split = (int64_t)c.M * c.N * 4;
     while (splits > 1 && splits * per_split > c.workspace_bytes) --splits;
   }
   CUtensorMap ta, tb;
@@ -527,8 +537,27 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
     p.kb_per_split = kbps;
   }
   p.splits = splits;
-  if (c.rowsum != nullptr && splits > 1)  // per-split partials, summed by the reduce below
-    p.rowsum = static_cast<float*>(c.workspace) + (int64_t)splits * c.M * c.N;
+  // row sums: every column tile of a row block sums 1 / tiles_n of the
+  // k-blocks into its own partial (balanced: with one tile per CTA the first
+  // column tiles alone would set the kernel time) when the workspace holds
+  // [splits][tiles_n][M] partials after the split-K block; else the first
+  // column tile sums all, per split
+  int rs_parts = 1;
+  float* rs_ws = nullptr;
+  if (c.rowsum != nullptr) {
+    const int tiles_n = (c.N + bn - 1) / bn;
+    const int64_t base = splits > 1 ? (int64_t)splits * c.M * c.N : 0;
+    if (tiles_n > 1 && c.workspace != nullptr &&
+        (base + (int64_t)splits * tiles_n * c.M) * 4 <= c.workspace_bytes)
+      rs_parts = tiles_n;
+    if (splits > 1 || rs_parts > 1) {
+      if ((base + (int64_t)splits * rs_parts * c.M) * 4 > c.workspace_bytes)
+        return cudaErrorInvalidValue;
+      rs_ws = static_cast<float*>(c.workspace) + base;
+      p.rowsum = rs_ws;
+    }
+  }
+  p.rs_parts = rs_parts;
   // output through TMA when the view is addressable (16 B pitch / batch strides)
   CUtensorMap td{}, td2{};
   if (splits > 1) {
@@ -606,7 +635,11 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   if (err == cudaSuccess && splits > 1) {
     splitk_reduce_kernel<<<4 * sm_count(), 256, 0, stream>>>(
         static_cast<const float*>(c.workspace), splits, c.M, c.N, static_cast<float*>(c.out),
-        c.ldo, c.beta, c.rowsum);
+        c.ldo, c.beta, c.rowsum, splits * rs_parts);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    err = cudaGetLastError();
+  } else if (err == cudaSuccess && rs_ws != nullptr) {
+    rowsum_reduce_kernel<<<(c.M + 255) / 256, 256, 0, stream>>>(rs_ws, rs_parts, c.M, c.rowsum);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     err = cudaGetLastError();
   }

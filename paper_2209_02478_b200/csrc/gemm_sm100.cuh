@@ -60,8 +60,11 @@ struct GemmParams {
                             // (P V, dS K), 2 = only k >= row (P^T dO, dS^T Q); the
                             // k-blocks outside are exact zeros and are skipped
   float* rowsum;            // kEpiF32, MN-major A: sums of A's rows over this split's K
-                            // range -> rowsum[split * M + m] (the bias gradient of a
-                            // weight-gradient GEMM, dY^T 1, read from the staged dY tiles)
+                            // range (the bias gradient of a weight-gradient GEMM, dY^T 1,
+                            // read from the staged dY tiles) -> rowsum[part * M + m]
+  int rs_parts;             // 1: the first column tile of a row block sums every k-block
+                            // (part = split); tiles_n: column tile tn sums the k-blocks
+                            // kb0 + tn, + tiles_n, ... (part = split * tiles_n + tn)
 };
 
 constexpr int kBM = 128;
@@ -611,7 +614,8 @@ __global__ void __launch_bounds__(gemm_threads(EW, EPI), (GemmCfg<BN, EPI, EW, C
         const int split = zz % p.splits;
         const int kb0 = split * p.kb_per_split;
         const int kb1 = min(num_kb, kb0 + p.kb_per_split);
-        const bool active = t_in % tiles_n == 0;
+        const int tn = t_in % tiles_n;
+        const bool active = p.rs_parts > 1 || tn == 0;
         float2 acc[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[e] = make_float2(0.f, 0.f);
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(gemm_threads(EW, EPI), (GemmCfg<BN, EPI, EW, C
           const int s = it % S;
           const uint32_t ph = (it / S) & 1;
           mbar_wait(&empty[s], ph);
-          if (active) {
+          if (active && (p.rs_parts == 1 || (kb - kb0) % p.rs_parts == tn)) {
             const uint32_t base = smem_u32(sA + s * Cfg::kABytes) + j * 8192;
             uint4 q[8];
 #pragma unroll
@@ -656,7 +660,8 @@ __global__ void __launch_bounds__(gemm_threads(EW, EPI), (GemmCfg<BN, EPI, EW, C
           asm volatile("bar.sync 1, %0;" ::"n"(32 * kRsWarps) : "memory");
           if (rw == 0 && lane < 16) {
             const int m = (t_in / tiles_n) * kTileM + (int)rank * kBM + col;
-            float* dst = p.rowsum + (size_t)split * p.M + m;
+            const int part = p.rs_parts > 1 ? split * p.rs_parts + tn : split;
+            float* dst = p.rowsum + (size_t)part * p.M + m;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               float v = rs_red[col + e];

@@ -183,14 +183,18 @@ def test_gemm_wgrad_split_k(cuda_device, split, shape):
     assert torch.equal(out, out2)  # run-to-run bitwise
 
 
+@pytest.mark.parametrize("roomy", [True, False])
 @pytest.mark.parametrize("cg", [0, 1, 2])
 @pytest.mark.parametrize("split", [0, 1, 2, 5])
 @pytest.mark.parametrize("shape", [(3072, 768, 18432), (2304, 768, 4096), (104, 200, 1000),
                                    (768, 3072, 2560)])
-def test_gemm_wgrad_rowsum(cuda_device, cg, split, shape):
-    """Weight gradient + bias gradient in one GEMM: the extra warp's sums of the
-    staged dY tiles equal dY's column sums (fp32 over the same bf16 values),
-    dW is bitwise the GEMM without them, and both are run-to-run bitwise."""
+def test_gemm_wgrad_rowsum(cuda_device, cg, split, shape, roomy):
+    """Weight gradient + bias gradient in one GEMM: the row-sum warps' sums of
+    the staged dY tiles equal dY's column sums (fp32 over the same bf16
+    values), dW is bitwise the GEMM without them, and both are run-to-run
+    bitwise. roomy: the workspace holds a row-sum partial per column tile
+    (every tile sums a share of the k-blocks); tight: only per split (the
+    first column tile sums them all)."""
     ops = _ops()
     torch.manual_seed(11)
     M, N, K = shape
@@ -198,7 +202,7 @@ def test_gemm_wgrad_rowsum(cuda_device, cg, split, shape):
         pytest.skip("CTA pairs need M > 128")
     dY = _rand(K, M)
     X = _rand(K, N)
-    ws = torch.empty(8 * M * (N + 1), device="cuda")
+    ws = torch.empty(8 * M * (N + (N + 63) // 64) if roomy else 8 * M * N + 8 * M, device="cuda")
     kw = dict(a_mn=True, b_mn=True, epi=ops.EPI_F32, split_k=split, workspace=ws, force_cg=cg,
               force_bn=256 if cg == 2 else 0)
     ref_w = torch.empty(M, N, device="cuda")
