@@ -16,9 +16,15 @@
 //
 // The book-keeping core (ArenaBook) is plain host C++ so it is unit-testable
 // without a GPU; DeviceArena binds it to one cudaMalloc'd region. Frees are
-// stream-ordered by construction: the executor issues every kernel on one
-// compute stream, so a block freed after its last use may be handed out
-// again immediately.
+// ordered on the step's compute stream: a block freed after its last use there
+// may be handed out again immediately. The arena does not track streams, so
+// the two other streams follow one rule each (trainer.cpp):
+//   - keep-bit side stream: its block is taken on the host before the side
+//     stream waits on an event recorded on the compute stream (every earlier
+//     use of those bytes has finished), and the compute stream waits on the
+//     side stream's completion event before the block is read or dropped;
+//   - NCCL comm stream (dp.cpp): it only touches the gradient buffers, which
+//     live for the whole run, and is joined before the optimizer and hooks.
 #pragma once
 
 #include <cstddef>
