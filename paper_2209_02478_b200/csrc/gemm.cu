@@ -252,7 +252,8 @@ int pick_cg(const GemmCall& c, int bn) {
   // pipeline, and the pair's joint accumulator release costs it (852 -> 794
   // TFLOP/s); the GELU GEMM's mainloop is the slower side and the pair's
   // halved B traffic helps it (887 -> 909)
-  if (c.epi == kEpiDGelu) return 1;
+  // (with the derivative saved by the forward, dGELU is a plain product: light)
+  if (c.epi == kEpiDGelu && !c.gelu_deriv) return 1;
   return 2;
 }
 
@@ -289,7 +290,7 @@ int pick_bn(const GemmCall& c) {
   // light-epilogue unbatched GEMMs run 256-wide tiles on CTA pairs (see
   // pick_cg): take them whenever the pair grid is not clearly worse-filled
   // than the 128-wide single-SM grid (pair tiles are ~1.3x faster per flop)
-  if (c.N > 128 && batches == 1 && c.M > 128 && c.epi != kEpiDGelu &&
+  if (c.N > 128 && batches == 1 && c.M > 128 && (c.epi != kEpiDGelu || c.gelu_deriv) &&
       c.force_cg != 1) {
     const int64_t pairs = sm_count() / 2;
     const int64_t tp = ((c.M + 255) / 256) * ((c.N + 255) / 256);
@@ -515,6 +516,7 @@ cudaError_t gemm(const GemmCall& c, cudaStream_t stream) {
   p.ldo = c.ldo; p.obs1 = c.obs1; p.obs2 = c.obs2;
   p.alpha = c.alpha; p.beta = c.beta;
   p.gelu_tanh = c.gelu_tanh;
+  p.gelu_deriv = c.gelu_deriv;
   p.drop = c.drop;
   p.causal_tiles = c.causal_tiles ? 1 : 0;
   p.causal_k = c.causal_k;

@@ -51,6 +51,9 @@ struct GemmParams {
   int splits;               // split-K factor (>1: fp32 partials, batch must be 1)
   int kb_per_split;         // k-blocks per split
   int gelu_tanh;            // GELU flavour of kEpiBiasGelu / kEpiDGelu: 0 erf, 1 tanh
+  int gelu_deriv;           // kEpiBiasGelu: out = GELU'(u) instead of u (the backward's
+                            // only use of u); kEpiDGelu: aux already holds GELU'(u), so
+                            // the epilogue is a plain product
   DropoutCfg drop;          // kEpiBf16: dropout on (alpha*acc + bias) before adding aux
   int causal_tiles;         // batched S x S score GEMMs of a causal model: skip tiles
                             // whose columns (keys) all exceed their rows (queries)
@@ -203,6 +206,18 @@ __device__ __forceinline__ float2 dgelu_fast2(float2 x) {
   const float2 cdf = make_float2(x.x >= 0.f ? omh.x : h.x, x.y >= 0.f ? omh.y : h.y);
   return __ffma2_rn(__fmul2_rn(x, f2(0.39894228040143268f)), e, cdf);
 }
+// GELU and GELU' of the same pair from one h / e evaluation (bit-identical to
+// gelu_fast2 / dgelu_fast2: same operations on the same values)
+__device__ __forceinline__ float2 gelu_both2(float2 x, float2& dg) {
+  float2 e;
+  const float2 h = gelu_half_erfc2(x, e);
+  const float2 xh = __fmul2_rn(x, h);
+  const float2 d = __ffma2_rn(xh, f2(-1.0f), x);
+  const float2 omh = __ffma2_rn(h, f2(-1.0f), f2(1.0f));
+  const float2 cdf = make_float2(x.x >= 0.f ? omh.x : h.x, x.y >= 0.f ? omh.y : h.y);
+  dg = __ffma2_rn(__fmul2_rn(x, f2(0.39894228040143268f)), e, cdf);
+  return make_float2(x.x >= 0.f ? d.x : xh.x, x.y >= 0.f ? d.y : xh.y);
+}
 __device__ __forceinline__ float gelu_fast(float x) { return gelu_fast2(make_float2(x, x)).x; }
 __device__ __forceinline__ float dgelu_fast(float x) { return dgelu_fast2(make_float2(x, x)).x; }
 
@@ -250,6 +265,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// GELU' rounded to bf16 before the dGELU product: the value the forward
+// saves in gelu_deriv mode, so both modes give bit-identical gradients
+__device__ __forceinline__ float2 bf16_round2(float2 x) {
+  const uint32_t h = pack_bf16x2(x.x, x.y);
+  return make_float2(__uint_as_float(h << 16), __uint_as_float(h & 0xFFFF0000u));
+}
+__device__ __forceinline__ float bf16_round(float x) { return bf16_round2(make_float2(x, x)).x; }
 
 // Epilogue math on NV consecutive accumulator columns of one row (values in
 // v, first column col0). `bias_t` points at this chunk's slice of the bias
@@ -320,13 +342,22 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
           if constexpr (EPI == kEpiBf16) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[8 * q + i] += __bfloat162float(av[i]);
+          } else if (p.gelu_deriv) {
+#pragma unroll
+            for (int i = 0; i < 8; i += 2) {
+              const float2 r = __fmul2_rn(make_float2(v[8 * q + i], v[8 * q + i + 1]),
+                                          make_float2(__bfloat162float(av[i]), __bfloat162float(av[i + 1])));
+              v[8 * q + i] = r.x;
+              v[8 * q + i + 1] = r.y;
+            }
           } else if (p.gelu_tanh) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) v[8 * q + i] *= dgelu_tanh_f(__bfloat162float(av[i]));
+            for (int i = 0; i < 8; ++i) v[8 * q + i] *= bf16_round(dgelu_tanh_f(__bfloat162float(av[i])));
           } else {
 #pragma unroll
             for (int i = 0; i < 8; i += 2) {
-              const float2 d = dgelu_fast2(make_float2(__bfloat162float(av[i]), __bfloat162float(av[i + 1])));
+              const float2 d = bf16_round2(
+                  dgelu_fast2(make_float2(__bfloat162float(av[i]), __bfloat162float(av[i + 1]))));
               const float2 r = __fmul2_rn(make_float2(v[8 * q + i], v[8 * q + i + 1]), d);
               v[8 * q + i] = r.x;
               v[8 * q + i + 1] = r.y;
@@ -339,7 +370,7 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
           if (col0 + i < p.N) {
             const float a = __bfloat162float(ax[i]);
             if constexpr (EPI == kEpiBf16) v[i] += a;
-            else v[i] *= p.gelu_tanh ? dgelu_tanh_f(a) : dgelu_fast(a);
+            else v[i] *= p.gelu_deriv ? a : bf16_round(p.gelu_tanh ? dgelu_tanh_f(a) : dgelu_fast(a));
           }
         }
       }
@@ -355,7 +386,25 @@ __device__ __forceinline__ void epilogue_math(float (&v)[NV], float (&g)[NV], co
       v[i] = __uint_as_float(h << 16);
       v[i + 1] = __uint_as_float(h & 0xFFFF0000u);
     }
-    if (p.gelu_tanh) {
+    if (p.gelu_deriv) {  // g = GELU(u), v = GELU'(u) from one erfc / exponential
+      if (p.gelu_tanh) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          g[i] = gelu_tanh_f(v[i]);
+          v[i] = dgelu_tanh_f(v[i]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < NV; i += 2) {
+          float2 d;
+          const float2 r = gelu_both2(make_float2(v[i], v[i + 1]), d);
+          g[i] = r.x;
+          g[i + 1] = r.y;
+          v[i] = d.x;
+          v[i + 1] = d.y;
+        }
+      }
+    } else if (p.gelu_tanh) {
 #pragma unroll
       for (int i = 0; i < NV; ++i) g[i] = gelu_tanh_f(v[i]);
     } else {

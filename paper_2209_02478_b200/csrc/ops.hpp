@@ -48,6 +48,7 @@ struct GemmCall {
   void* workspace = nullptr;
   int64_t workspace_bytes = 0;
   int gelu_tanh = 0;              // GELU flavour for kEpiBiasGelu / kEpiDGelu
+  int gelu_deriv = 0;             // kEpiBiasGelu: out = GELU'(u); kEpiDGelu: aux is GELU'(u)
   mimose_dev::DropoutCfg drop;    // kEpiBf16: dropout on the product before adding aux
   bool causal_tiles = false;      // skip tiles above the diagonal (causal S x S scores)
   int causal_k = 0;               // 1: only k <= row contributes, 2: only k >= row (causal)

@@ -450,6 +450,19 @@ bool Trainer::save_pd() const {
   return keep && m_.attn_dropout > 0.f;
 }
 
+// FFN1's GEMM saves GELU'(u) instead of the pre-activation u when the kept
+// FFN half also keeps g = GELU(u) (u's only other reader is the u-only
+// regeneration of g): the forward epilogue derives GELU' from the same erfc /
+// exponential as GELU, and the backward's dGELU GEMM becomes a plain product
+// (light epilogue, CTA pair). Same bytes saved. MIMOSE_FFN_DERIV=0: save u.
+bool Trainer::ffn_deriv() const {
+  static const bool on = [] {
+    const char* e = std::getenv("MIMOSE_FFN_DERIV");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on && t_.ffn_regen_g == 0;
+}
+
 // The forward, the backward and the byte model (block_work_bytes) all ask
 // this one function, so they always agree on the path for a given S.
 int Trainer::fused_attn(int S) const {
@@ -1023,6 +1036,7 @@ void Trainer::ffn_half_fwd(int l, const void* h1, void* y, FfnSave* save, void* 
                              p32_ + P.b1.off);
     c.out2 = gg;
     c.gelu_tanh = m_.gelu_tanh;
+    c.gelu_deriv = ffn_deriv();
     run_gemm(c, s);
   }
   if (!keep) {
@@ -1170,6 +1184,7 @@ void* Trainer::ffn_half_bwd(int l, const void* h1, const void* y, const void* y_
   {
     GemmCall c = dgrad_call(dfp, W + P.w2.off, T, (int)H, (int)F, du, mimose_ops::kEpiDGelu, sv.u);
     c.gelu_tanh = m_.gelu_tanh;
+    c.gelu_deriv = ffn_deriv();  // sv.u holds GELU'(u)
     run_gemm(c, s);
   }
   drop(df);

@@ -203,6 +203,7 @@ class Trainer {
                       void* dh1, void* da, const StepGeo& g, cudaStream_t s);
   void* attn_fwd(int l, const void* x, AttnSave* save, const StepGeo& g, cudaStream_t s);
   void* attn_bwd(int l, AttnSave& sv, void* dctx, const StepGeo& g, cudaStream_t s);
+  bool ffn_deriv() const;
   int fused_attn(int S) const;
   bool save_pd() const;
   void* head_fwd_bwd(const StepInputs& in, const void* hidden, const StepGeo& g, cudaStream_t s);
